@@ -1,0 +1,229 @@
+/*
+ * mdnn.h — C ABI of the B200-native MoDL / VarNet hot path.
+ *
+ * This is the drop-in boundary for the reference's nlop operator API
+ * (/root/reference/proj/include/mdnn/nlop.hpp:18-83 NlopNode, :89-437 Nlop,
+ * nn.hpp:68-222 Model algebra, recon.hpp:82-904 SENSE/CG/MoDL/VarNet
+ * constructors, optim.hpp:81-108,314-399 Adam + run_step).  The same header is
+ * implemented twice:
+ *
+ *   libmdnn_b200.so   — the product: C++ host graph over device arrays and
+ *                       hand-written sm_100a kernels (paper_2202_14005_b200/csrc)
+ *   libmdnn_ref.so    — test oracle only: a thin shim over the unmodified
+ *                       reference headers (oracle/ref_shim.cpp, built into
+ *                       oracle/_ref/), used by tests/ and bench.py --impl reference.
+ *
+ * Conventions (reference: common.hpp:58-68, mdarray.hpp:23-200):
+ *   - every array is complex64 interleaved (re, im), column-major, rank 1..16,
+ *     strides counted in complex elements;
+ *   - `device` = -1 for host memory, >= 0 for a CUDA device pointer (GPU build);
+ *   - all calls are synchronous with respect to host buffers; device buffers
+ *     are ordered on the library's stream for that device.
+ *
+ * Errors: every int-returning call returns 0 on success or one of MDNN_ERR_*
+ * (the reference's exception taxonomy, common.hpp:15-26, with the CLI's exit
+ * codes, cli.hpp:357-371); the message is in mdnn_last_error() (thread-local).
+ * Handle-returning calls return NULL on error.
+ */
+#ifndef MDNN_H
+#define MDNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDNN_MAX_RANK 16
+
+enum mdnn_status {
+    MDNN_OK = 0,
+    MDNN_ERR_OTHER = 1,
+    MDNN_ERR_SHAPE = 2,  /* ShapeError */
+    MDNN_ERR_IO = 3,     /* IoError */
+    MDNN_ERR_CONFIG = 4, /* ConfigError */
+    MDNN_ERR_SOLVER = 5, /* SolverError */
+    MDNN_ERR_BOUNDS = 6, /* BoundsError */
+    MDNN_ERR_ALIAS = 7,  /* AliasError */
+    MDNN_ERR_STALE = 8,  /* StaleDerivativeError */
+    MDNN_ERR_CUDA = 9    /* device failure (GPU build only) */
+};
+
+typedef struct mdnn_array {
+    float* data;                   /* interleaved complex64 */
+    int rank;                      /* 1..16 */
+    int device;                    /* -1 host, >=0 CUDA ordinal */
+    long dims[MDNN_MAX_RANK];
+    long strides[MDNN_MAX_RANK];   /* complex elements; ignored if has_strides == 0 */
+    int has_strides;               /* 0: default column-major strides */
+} mdnn_array;
+
+typedef struct mdnn_nlop mdnn_nlop;   /* refcounted graph handle (shares nodes) */
+typedef struct mdnn_model mdnn_model; /* Model<R>: nlop + named args + outputs */
+typedef struct mdnn_trainer mdnn_trainer;
+
+/* ---- library ------------------------------------------------------------ */
+const char* mdnn_last_error(void);
+const char* mdnn_backend(void);            /* "b200-sm100a" or "reference-cpu" */
+int mdnn_set_device(int device);           /* GPU build: selects device + stream */
+int mdnn_synchronize(void);
+int mdnn_set_option(const char* key, long value); /* e.g. "conv_tf32", "fused_sense" */
+
+/* ---- Nlop (nlop.hpp:89-437) --------------------------------------------- */
+void mdnn_nlop_free(mdnn_nlop* h);
+mdnn_nlop* mdnn_nlop_ref(mdnn_nlop* h);    /* new handle sharing the same graph */
+int mdnn_nlop_n_in(const mdnn_nlop* h);
+int mdnn_nlop_n_out(const mdnn_nlop* h);
+int mdnn_nlop_in_dims(const mdnn_nlop* h, int i, int* rank, long* dims);
+int mdnn_nlop_out_dims(const mdnn_nlop* h, int o, int* rank, long* dims);
+
+/* apply (nlop.hpp:125): outputs are written into caller buffers */
+int mdnn_nlop_apply(mdnn_nlop* h, int n_in, const mdnn_array* in, int n_out, mdnn_array* out);
+/* dy = D_i F_o dx at the last forward (nlop.hpp:158) */
+int mdnn_nlop_derivative(mdnn_nlop* h, int o, int i, const mdnn_array* dx, mdnn_array* dy);
+/* dx = (D_i F_o)^H dy (nlop.hpp:247) */
+int mdnn_nlop_adjoint(mdnn_nlop* h, int o, int i, const mdnn_array* dy, mdnn_array* dx);
+/* one reverse sweep (nlop.hpp:206); wanted[i]==0 skips input i (its dx is
+   left untouched); wanted == NULL means all inputs */
+int mdnn_nlop_adjoint_all(mdnn_nlop* h, int o, const mdnn_array* dy, int n_in, mdnn_array* dx,
+                          const uint8_t* wanted);
+
+/* composition algebra (nlop.hpp:265-350) — new handles, inputs unchanged */
+mdnn_nlop* mdnn_nlop_combine(const mdnn_nlop* f, const mdnn_nlop* g);
+mdnn_nlop* mdnn_nlop_link(const mdnn_nlop* h, int o, int i);
+mdnn_nlop* mdnn_nlop_duplicate(const mdnn_nlop* h, int i, int j);
+mdnn_nlop* mdnn_nlop_chain(const mdnn_nlop* f, const mdnn_nlop* g);
+
+/* ---- atoms on the hot path (ops.hpp:1433-1485 factories + nodes) -------- */
+mdnn_nlop* mdnn_nlop_dft(int rank, const long* dims, unsigned long flags, int inverse); /* linop_dft, linop.hpp:132 */
+mdnn_nlop* mdnn_nlop_tenmul(int rank, const long* iter, const long* out_dims, const long* so,
+                            const long* in1_dims, const long* s1, const long* in2_dims, const long* s2); /* ops.hpp:69 */
+mdnn_nlop* mdnn_nlop_add(int rank, const long* dims, int subtract);            /* ops.hpp:122 */
+mdnn_nlop* mdnn_nlop_bcast_add(int rank, const long* x_dims, const long* b_dims); /* ops.hpp:153 */
+mdnn_nlop* mdnn_nlop_fork(int rank, const long* dims, int n);                  /* ops.hpp:214 */
+mdnn_nlop* mdnn_nlop_zconj(int rank, const long* dims);                        /* ops.hpp:246 */
+mdnn_nlop* mdnn_nlop_zreal(int rank, const long* dims);                        /* ops.hpp:266 */
+mdnn_nlop* mdnn_nlop_real_chan(int rank, const long* dims, int chan_dim);      /* ops.hpp:318 */
+mdnn_nlop* mdnn_nlop_chan_cplx(int rank, const long* dims, int chan_dim);      /* ops.hpp:376 */
+mdnn_nlop* mdnn_nlop_crelu(int rank, const long* dims);                        /* ops.hpp:451 */
+mdnn_nlop* mdnn_nlop_exp_real(int rank, const long* dims);                     /* ops.hpp:672 */
+mdnn_nlop* mdnn_nlop_mse(int rank, const long* dims);                          /* ops.hpp:874 */
+mdnn_nlop* mdnn_nlop_batchnorm(int rank, const long* dims, unsigned long flags, int train,
+                               double eps, double momentum);                   /* ops.hpp:1070 */
+mdnn_nlop* mdnn_nlop_rbf(int rank, const long* z_dims, int filter_dim, int n_centers,
+                         const float* centers, float sigma);                   /* ops.hpp:1308 */
+mdnn_nlop* mdnn_nlop_pad(int rank, const long* in_dims, const long* out_dims, const long* corner); /* linop.hpp:142 */
+
+/* SENSE (recon.hpp:18-42 SenseDims) */
+typedef struct mdnn_sense_dims {
+    long x, y, coils, maps, batch;
+} mdnn_sense_dims;
+/* inverse of S with x = input 0 (recon.hpp:211-329, make_inverse_nlop :326) */
+mdnn_nlop* mdnn_nlop_inverse(const mdnn_nlop* s, long max_iter, double tol);
+/* last CG status of an inverse node graph (recon.hpp:136-140): first InverseNode found */
+int mdnn_nlop_cg_status(const mdnn_nlop* h, long* iterations, double* rel_residual, int* converged);
+
+/* plain CG-SENSE linop applications on one array set (recon.hpp:82-195) */
+int mdnn_sense_forward(const mdnn_array* coils, const mdnn_array* pattern, const mdnn_array* x, mdnn_array* y);
+int mdnn_sense_adjoint(const mdnn_array* coils, const mdnn_array* pattern, const mdnn_array* y, mdnn_array* x);
+int mdnn_sense_normal(const mdnn_array* coils, const mdnn_array* pattern, float lambda, const mdnn_array* x, mdnn_array* y);
+int mdnn_cg_normal_solve(const mdnn_array* coils, const mdnn_array* pattern, float lambda, const mdnn_array* b,
+                         long max_iter, double tol, mdnn_array* x, long* iterations, double* rel_residual);
+/* dft on one array (fft.hpp:180) */
+int mdnn_dft(const mdnn_array* in, unsigned long flags, int inverse, mdnn_array* out);
+
+/* ---- Model (nn.hpp:68-222) ------------------------------------------------ */
+enum mdnn_arg_kind { MDNN_ARG_DATA = 0, MDNN_ARG_WEIGHTS = 1, MDNN_ARG_MOVING_STATS = 2 };
+
+void mdnn_model_free(mdnn_model* m);
+mdnn_nlop* mdnn_model_nlop(const mdnn_model* m); /* new handle; caller frees */
+int mdnn_model_n_args(const mdnn_model* m);
+const char* mdnn_model_arg_name(const mdnn_model* m, int i);
+int mdnn_model_arg_kind(const mdnn_model* m, int i);
+int mdnn_model_arg_real(const mdnn_model* m, int i);
+int mdnn_model_n_outs(const mdnn_model* m);
+const char* mdnn_model_out_name(const mdnn_model* m, int o);
+int mdnn_model_arg_index(const mdnn_model* m, const char* name);
+int mdnn_model_output_index(const mdnn_model* m, const char* name);
+long mdnn_model_num_real_params(const mdnn_model* m);
+/* seeded init of one weights/moving-stats argument (nn.hpp:117-145), host or device out */
+int mdnn_model_init_weight(const mdnn_model* m, uint64_t seed, const char* name, mdnn_array* out);
+
+/* model algebra */
+mdnn_model* mdnn_model_chain(const mdnn_model* a, const mdnn_model* b, const char* b_in, int a_out);
+mdnn_model* mdnn_model_link(const mdnn_model* m, int out_idx, const char* arg);
+mdnn_model* mdnn_model_combine(const mdnn_model* a, const mdnn_model* b);
+mdnn_model* mdnn_model_dedupe(const mdnn_model* m);
+
+/* layers (nn.hpp:344-453) */
+typedef struct mdnn_conv_spec {
+    int rank;
+    long in_dims[MDNN_MAX_RANK];
+    int n_axes;
+    int axes[4];
+    long kernel[4];
+    int chan_dim;
+    long out_channels;
+    int pad_same;
+    int transposed;
+} mdnn_conv_spec;
+mdnn_model* mdnn_conv_layer(const char* name, const mdnn_conv_spec* spec, int bias);
+mdnn_model* mdnn_batchnorm_layer(const char* name, int rank, const long* dims, unsigned long flags,
+                                 int train, double eps, double momentum);
+
+/* networks (recon.hpp:499-904).  The constructors build the reference's
+   graphs with the two wiring fixes documented in DESIGN.md §Oracle. */
+typedef struct mdnn_modl_cfg {
+    long iterations, layers, filters, kernel, cg_iter;
+    double cg_tol, lambda_init;
+    long im_x, im_y, coils, maps, batch;
+    int train_mode;
+} mdnn_modl_cfg;
+typedef struct mdnn_varnet_cfg {
+    long iterations, filters, kernel, rbf;
+    long im_x, im_y, coils, maps, batch;
+} mdnn_varnet_cfg;
+void mdnn_modl_cfg_default(mdnn_modl_cfg* c);
+void mdnn_varnet_cfg_default(mdnn_varnet_cfg* c);
+mdnn_model* mdnn_build_modl(const mdnn_modl_cfg* cfg);
+mdnn_model* mdnn_build_varnet(const mdnn_varnet_cfg* cfg);
+/* SENSE fragments as models (recon.hpp:394-418, :807-820) */
+mdnn_model* mdnn_sense_normal_fragment(const mdnn_sense_dims* sd);
+mdnn_model* mdnn_sense_adjoint_fragment(const mdnn_sense_dims* sd);
+mdnn_model* mdnn_modl_normal_plus_lambda(const mdnn_sense_dims* sd);
+mdnn_model* mdnn_loss_model_mse(int rank, const long* dims);
+
+/* ---- simulation fixtures (simulate.hpp:40-133) --------------------------- */
+/* draw_phantom/draw_coils for item s with seed (hash_rand(seed,2s) / 2s+1) into
+   host arrays of dims [X,Y,1,1,...] and [X,Y,1,C,...] */
+int mdnn_sim_item(uint64_t seed, long item, long x, long y, long coils, float* phantom, float* coil_maps);
+int mdnn_sim_pattern(long y, long accel, long acl, float* pattern);
+
+/* ---- training (optim.hpp:20-108, :218-415) ------------------------------- */
+typedef struct mdnn_train_cfg {
+    double lr, beta1, beta2, eps, clip;
+} mdnn_train_cfg;
+void mdnn_train_cfg_default(mdnn_train_cfg* c);
+/* joins model output "out" with an MSE loss against data arg "reference" */
+mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg* cfg, uint64_t seed);
+void mdnn_trainer_free(mdnn_trainer* t);
+int mdnn_trainer_set_data(mdnn_trainer* t, const char* name, const mdnn_array* a);
+int mdnn_trainer_set_weight(mdnn_trainer* t, const char* name, const mdnn_array* a);
+int mdnn_trainer_get_weight(mdnn_trainer* t, const char* name, mdnn_array* out);
+int mdnn_trainer_get_grad(mdnn_trainer* t, const char* name, mdnn_array* out);
+/* forward + backward: loss (host double, synchronising) and gradients into the
+   flat gradient buffer; no weight update */
+int mdnn_trainer_forward_backward(mdnn_trainer* t, double* loss);
+/* flat fp32 gradient buffer (device pointer in the GPU build) for all-reduce */
+int mdnn_trainer_grad_buffer(mdnn_trainer* t, float** ptr, long* n_floats);
+/* scale gradients (e.g. 1/world), realify/clip, Adam, prox, moving stats */
+int mdnn_trainer_update(mdnn_trainer* t, float grad_scale);
+/* run_step = forward_backward + update(1) */
+int mdnn_trainer_step(mdnn_trainer* t, double* loss);
+int mdnn_trainer_n_weights(const mdnn_trainer* t);
+const char* mdnn_trainer_weight_name(const mdnn_trainer* t, int k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDNN_H */

@@ -1,0 +1,915 @@
+// TEST ORACLE — not product code.
+//
+// C-ABI shim (include/mdnn.h) over the UNMODIFIED reference library
+// (/root/reference/proj/include/mdnn/*.hpp, header-only C++20, compiled in
+// place by oracle/Makefile into oracle/_ref/).  Only tests/, smoke() and
+// bench.py's cpu_baseline / --impl reference legs may load it.
+//
+// The reference's network constructors throw as shipped:
+//   * modl_denoiser_fragment hard-codes output index 1 for the CNN output
+//     (recon.hpp:799-801), which is a batch-norm statistic in train mode;
+//   * varnet_step_model links by the FIRST arg named "b" (recon.hpp:636,
+//     nn.hpp:86-92), which is the DC block's x0, creating a cycle.
+// fixed_modl_denoiser / fixed_varnet_step below re-assemble the same graphs
+// with the reference's own public API, resolving the CNN output by name and
+// linking into the add's own "b" (the last argument).  Everything else
+// (build_modl / build_varnet loops, modl_step_model, fragments, nodes, CG,
+// InverseNode, Adam, run_step) is the reference code itself.
+//
+// REF_REAL selects float (the fp32 baseline to match) or double (truth).
+
+#include <mdnn/simulate.hpp>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../include/mdnn.h"
+
+#ifndef REF_REAL
+#define REF_REAL float
+#endif
+
+using namespace mdnn;
+using R = REF_REAL;
+using A = MdArray<R>;
+
+struct mdnn_nlop {
+    Nlop<R> op;
+};
+struct mdnn_model {
+    Model<R> m;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg)
+{
+    g_err = msg;
+    return code;
+}
+
+template<class F>
+int guard(F&& f)
+{
+    try {
+        f();
+        return MDNN_OK;
+    } catch (const ShapeError& e) {
+        return set_err(MDNN_ERR_SHAPE, e.what());
+    } catch (const BoundsError& e) {
+        return set_err(MDNN_ERR_BOUNDS, e.what());
+    } catch (const AliasError& e) {
+        return set_err(MDNN_ERR_ALIAS, e.what());
+    } catch (const StaleDerivativeError& e) {
+        return set_err(MDNN_ERR_STALE, e.what());
+    } catch (const SolverError& e) {
+        return set_err(MDNN_ERR_SOLVER, e.what());
+    } catch (const IoError& e) {
+        return set_err(MDNN_ERR_IO, e.what());
+    } catch (const ConfigError& e) {
+        return set_err(MDNN_ERR_CONFIG, e.what());
+    } catch (const std::exception& e) {
+        return set_err(MDNN_ERR_OTHER, e.what());
+    }
+}
+
+template<class T, class F>
+T* guard_ptr(F&& f)
+{
+    T* out = nullptr;
+    if (guard([&] { out = f(); }) != MDNN_OK)
+        return nullptr;
+    return out;
+}
+
+Dims mkdims(int rank, const long* d) { return Dims(d, d + rank); }
+
+A from_c(const mdnn_array& a)
+{
+    if (a.device >= 0)
+        throw ConfigError("reference shim: device arrays are not supported");
+    Dims d(a.dims, a.dims + a.rank);
+    A out(d);
+    Dims s = a.has_strides ? Dims(a.strides, a.strides + a.rank) : default_strides(d);
+    Dims idx(d.size(), 0);
+    auto* o = out.data();
+    long n = out.size();
+    for (long k = 0; k < n; k++) {
+        long off = 0;
+        for (size_t i = 0; i < d.size(); i++)
+            off += idx[i] * s[i];
+        o[k] = std::complex<R>(R(a.data[2 * off]), R(a.data[2 * off + 1]));
+        for (size_t i = 0; i < d.size(); i++) {
+            if (++idx[i] < d[i])
+                break;
+            idx[i] = 0;
+        }
+    }
+    return out;
+}
+
+void to_c(const A& src, mdnn_array& a)
+{
+    if (a.device >= 0)
+        throw ConfigError("reference shim: device arrays are not supported");
+    Dims d(a.dims, a.dims + a.rank);
+    if (d != src.dims())
+        throw ShapeError("output buffer dims " + dims_to_string(d) + " != " + dims_to_string(src.dims()));
+    A c = src.has_default_strides() ? src : src.clone();
+    Dims s = a.has_strides ? Dims(a.strides, a.strides + a.rank) : default_strides(d);
+    Dims idx(d.size(), 0);
+    const auto* v = c.data();
+    long n = c.size();
+    for (long k = 0; k < n; k++) {
+        long off = 0;
+        for (size_t i = 0; i < d.size(); i++)
+            off += idx[i] * s[i];
+        a.data[2 * off] = float(v[k].real());
+        a.data[2 * off + 1] = float(v[k].imag());
+        for (size_t i = 0; i < d.size(); i++) {
+            if (++idx[i] < d[i])
+                break;
+            idx[i] = 0;
+        }
+    }
+}
+
+mdnn_nlop* wrap(Nlop<R> op) { return new mdnn_nlop{std::move(op)}; }
+mdnn_model* wrapm(Model<R> m) { return new mdnn_model{std::move(m)}; }
+
+SenseDims to_sd(const mdnn_sense_dims* s) { return SenseDims{s->x, s->y, s->coils, s->maps, s->batch}; }
+
+ModlConfig to_modl(const mdnn_modl_cfg* c)
+{
+    ModlConfig m;
+    m.iterations = c->iterations;
+    m.layers = c->layers;
+    m.filters = c->filters;
+    m.kernel = c->kernel;
+    m.cg_iter = c->cg_iter;
+    m.cg_tol = c->cg_tol;
+    m.lambda_init = c->lambda_init;
+    m.im_x = c->im_x;
+    m.im_y = c->im_y;
+    m.coils = c->coils;
+    m.maps = c->maps;
+    m.batch = c->batch;
+    m.train_mode = c->train_mode != 0;
+    return m;
+}
+
+VarNetConfig to_varnet(const mdnn_varnet_cfg* c)
+{
+    VarNetConfig v;
+    v.iterations = c->iterations;
+    v.filters = c->filters;
+    v.kernel = c->kernel;
+    v.rbf = c->rbf;
+    v.im_x = c->im_x;
+    v.im_y = c->im_y;
+    v.coils = c->coils;
+    v.maps = c->maps;
+    v.batch = c->batch;
+    return v;
+}
+
+// -- fixed re-assembly of the two broken builders (see header comment) ------
+
+Model<R> plain_model(Nlop<R> op, std::vector<typename Model<R>::Arg> args, std::vector<std::string> outs)
+{
+    Model<R> m;
+    m.op = std::move(op);
+    m.args = std::move(args);
+    m.out_names = std::move(outs);
+    return m;
+}
+
+Model<R> first_map_slice(const SenseDims& sd)
+{
+    return plain_model(nlop_from_linop(linop_slice<R>(sd.image(), dim_maps, 0, 1), "first_map"),
+                       {{"x", ArgKind::Data, {}, nullptr, false}}, {"out"});
+}
+
+Model<R> embed_first_map(const SenseDims& sd, const Dims& img1)
+{
+    auto s = linop_slice<R>(sd.image(), dim_maps, 0, 1);
+    Linop<R> em(img1, sd.image(), [s](const A& v) { return s.adjoint(v); },
+                [s](const A& v) { return s.forward(v); });
+    return plain_model(nlop_from_linop(em, "embed_map"), {{"x", ArgKind::Data, {}, nullptr, false}}, {"out"});
+}
+
+// recon.hpp:714-803 with the CNN output resolved by name (fix for :799-801)
+Model<R> fixed_modl_denoiser(const ModlConfig& cfg, const std::string& stat_suffix)
+{
+    SenseDims sd = cfg.sense();
+    SenseDims sd1 = sd;
+    sd1.maps = 1;
+    Model<R> cnn;
+    if (sd.maps > 1)
+        cnn = first_map_slice(sd);
+    Dims cur = sd1.image();
+    const unsigned long bn_flags = (1UL << dim_x) | (1UL << dim_y) | (1UL << dim_batch);
+    for (long l = 0; l < cfg.layers; l++) {
+        const bool last = l + 1 == cfg.layers;
+        const std::string ln = "dw" + std::to_string(l);
+        ConvSpec spec;
+        spec.in_dims = cur;
+        spec.axes = {dim_x, dim_y};
+        spec.kernel = {cfg.kernel, cfg.kernel};
+        spec.chan_dim = dim_chan;
+        spec.out_channels = last ? 1 : cfg.filters;
+        spec.pad_same = true;
+        auto conv = conv_layer<R>(ln, spec, last);
+        cnn = cnn.valid() ? model_chain(cnn, conv, "x") : conv;
+        cur = spec.out_dims();
+        if (last)
+            break;
+        auto bn = batchnorm_layer<R>(ln + "_bn", cur, bn_flags, cfg.train_mode);
+        if (!stat_suffix.empty() && cfg.train_mode)
+            for (auto& n : bn.out_names)
+                if (n != "out")
+                    n += stat_suffix;
+        cnn = model_chain(cnn, bn, "x");
+        Dims gdims(max_rank, 1);
+        gdims[dim_chan] = cur[dim_chan];
+        auto gamma = plain_model(
+            Nlop<R>(detail::tenmul<R>("bn_scale" + std::to_string(l), cur, cur, cur, gdims)),
+            {{"x", ArgKind::Data, {}, nullptr, false},
+             {ln + "_g", ArgKind::Weights, Initializer::constant(1), nullptr, false}},
+            {"out"});
+        cnn = model_chain(cnn, gamma, "x");
+        auto beta = plain_model(Nlop<R>(std::make_shared<BroadcastAddNode<R>>(cur, gdims)),
+                                {{"x", ArgKind::Data, {}, nullptr, false},
+                                 {ln + "_beta", ArgKind::Weights, Initializer::constant(0), nullptr, false}},
+                                {"out"});
+        cnn = model_chain(cnn, beta, "x");
+        auto act = plain_model(Nlop<R>(std::make_shared<CReluNode<R>>(cur)),
+                               {{"x", ArgKind::Data, {}, nullptr, false}}, {"out"});
+        cnn = model_chain(cnn, act, "x");
+    }
+    if (sd.maps > 1)
+        cnn = model_chain(cnn, embed_first_map(sd, sd1.image()), "x");
+
+    auto fork = plain_model(Nlop<R>(std::make_shared<ForkNode<R>>(sd.image(), 2)),
+                            {{"x", ArgKind::Data, {}, nullptr, false}}, {"cnn_in", "skip"});
+    Model<R> f = model_chain(fork, cnn, "x", 0);
+    f = model_chain(f, detail::add_fragment<R>(sd.image()), "a", f.output_index("out"));
+    return model_link(f, f.output_index("skip"), "b");
+}
+
+// recon.hpp:826-869 (unchanged logic, calling the fixed denoiser)
+Model<R> fixed_modl_step(const ModlConfig& cfg, const std::string& stat_suffix)
+{
+    SenseDims sd = cfg.sense();
+    Dims img = sd.image();
+    Dims sdims(max_rank, 1);
+    Model<R> dw = fixed_modl_denoiser(cfg, stat_suffix);
+    auto lam = plain_model(Nlop<R>(std::make_shared<ExpRealNode<R>>(sdims)),
+                           {{"lam_log", ArgKind::Weights, Initializer::constant(std::log(cfg.lambda_init)), nullptr, true}},
+                           {"out"});
+    auto lam_fork = plain_model(Nlop<R>(std::make_shared<ForkNode<R>>(sdims, 2)),
+                                {{"x", ArgKind::Data, {}, nullptr, false}}, {"lam_rhs", "lam_inv"});
+    lam = model_chain(lam, lam_fork, "x");
+    Model<R> rhs = model_chain(dw, detail::scalar_mul_fragment<R>(sd, "lam_mul", ArgKind::Data), "x");
+    rhs = model_chain(rhs, detail::add_fragment<R>(img), "a");
+    rhs.out_names[rhs.output_index("out")] = "rhs";
+    auto s_model = detail::modl_normal_plus_lambda<R>(sd);
+    Model<R> inv;
+    inv.op = make_inverse_nlop<R>(s_model.op, cfg.cg_iter, cfg.cg_tol);
+    inv.args = s_model.args;
+    inv.args[0] = {"y", ArgKind::Data, {}, nullptr, false};
+    inv.out_names = {"out"};
+    Model<R> m = model_combine(lam, model_combine(rhs, inv));
+    m = model_link(m, m.output_index("lam_rhs"), "lam_mul");
+    m = model_link(m, m.output_index("lam_inv"), "lambda");
+    m = model_link(m, m.output_index("rhs"), "y");
+    for (auto& a : m.args)
+        if (a.name == "b")
+            a.name = "x0";
+    return model_dedupe(std::move(m));
+}
+
+Model<R> fixed_build_modl(const ModlConfig& cfg)
+{
+    cfg.validate();
+    SenseDims sd = cfg.sense();
+    Model<R> adj = detail::sense_adjoint_fragment<R>(sd);
+    adj.args[adj.arg_index("x")].name = "kspace";
+    auto fork = plain_model(Nlop<R>(std::make_shared<ForkNode<R>>(sd.image(), 2)),
+                            {{"x", ArgKind::Data, {}, nullptr, false}}, {"out", "x0src"});
+    Model<R> net = model_chain(adj, fork, "x");
+    for (long t = 0; t < cfg.iterations; t++) {
+        const bool last = t + 1 == cfg.iterations;
+        auto step = fixed_modl_step(cfg, last ? "" : "@" + std::to_string(t));
+        net = model_chain(net, step, "x", net.output_index("out"));
+        net = model_dedupe(std::move(net));
+    }
+    net = model_link(net, net.output_index("x0src"), "x0");
+    net.rebatch = [cfg](long b) {
+        ModlConfig c = cfg;
+        c.batch = b;
+        return fixed_build_modl(c);
+    };
+    return net;
+}
+
+// recon.hpp:618-645 with the link into the add's own "b" (fix for :636)
+Model<R> fixed_varnet_step(const VarNetConfig& cfg, const std::string& prefix)
+{
+    SenseDims sd = cfg.sense();
+    Dims img = sd.image();
+    Model<R> reg = detail::varnet_reg_fragment<R>(cfg, prefix);
+    Model<R> dc = detail::sense_normal_fragment<R>(sd);
+    dc = model_chain(dc, detail::sub_fragment<R>(img), "a");
+    dc = model_chain(dc, detail::scalar_mul_fragment<R>(sd, prefix + "_lam", ArgKind::Weights), "x");
+    auto& lam = dc.args[dc.arg_index(prefix + "_lam")];
+    lam.init = Initializer::constant(1.0);
+    lam.real_weights = true;
+    lam.prox = std::make_shared<NonNegProx<R>>();
+
+    Model<R> m = model_combine(reg, dc);                      // outputs [reg, dc]
+    m = model_chain(m, detail::add_fragment<R>(img), "a", 0); // outputs [dc, reg + b]
+    {
+        const int last = int(m.args.size()) - 1;             // the add's own "b"
+        m.op = link(m.op, 0, last);
+        m.args.erase(m.args.begin() + last);
+        m.out_names.erase(m.out_names.begin());
+    }
+    m = model_chain(m, detail::sub_fragment<R>(img), "b", 0); // a - (reg + dc)
+    for (auto& a : m.args) {
+        if (a.name == "a")
+            a.name = "x";
+        else if (a.name == "b")
+            a.name = "x0";
+    }
+    return model_dedupe(std::move(m));
+}
+
+Model<R> fixed_build_varnet(const VarNetConfig& cfg)
+{
+    cfg.validate();
+    SenseDims sd = cfg.sense();
+    Model<R> adj = detail::sense_adjoint_fragment<R>(sd);
+    adj.args[adj.arg_index("x")].name = "kspace";
+    auto fork = plain_model(Nlop<R>(std::make_shared<ForkNode<R>>(sd.image(), 2)),
+                            {{"x", ArgKind::Data, {}, nullptr, false}}, {"out", "x0src"});
+    Model<R> net = model_chain(adj, fork, "x");
+    for (long t = 0; t < cfg.iterations; t++) {
+        auto step = fixed_varnet_step(cfg, "it" + std::to_string(t));
+        net = model_chain(net, step, "x", net.output_index("out"));
+        net = model_dedupe(std::move(net));
+    }
+    net = model_link(net, net.output_index("x0src"), "x0");
+    net.rebatch = [cfg](long b) {
+        VarNetConfig c = cfg;
+        c.batch = b;
+        return fixed_build_varnet(c);
+    };
+    return net;
+}
+
+InverseNode<R>* find_inverse(const Nlop<R>& op)
+{
+    for (auto& n : op.nodes())
+        if (auto* p = dynamic_cast<InverseNode<R>*>(n.get()))
+            return p;
+    return nullptr;
+}
+
+} // namespace
+
+struct mdnn_trainer {
+    Model<R> joint;
+    TrainConfig cfg;
+    std::map<std::string, A> weights;
+    std::map<std::string, A> batch;
+    std::map<std::string, A> grads;
+    std::vector<AdamState<R>> adam;
+    std::vector<IpalmState<R>> ipalm;
+    std::vector<int> weight_args;
+    std::vector<std::string> weight_names;
+    std::vector<A> last_outs;
+    std::vector<float> flat;
+};
+
+extern "C" {
+
+const char* mdnn_last_error(void) { return g_err.c_str(); }
+const char* mdnn_backend(void) { return sizeof(R) == 8 ? "reference-cpu-f64" : "reference-cpu-f32"; }
+int mdnn_set_device(int) { return MDNN_OK; }
+int mdnn_synchronize(void) { return MDNN_OK; }
+int mdnn_set_option(const char*, long) { return MDNN_OK; }
+
+void mdnn_nlop_free(mdnn_nlop* h) { delete h; }
+mdnn_nlop* mdnn_nlop_ref(mdnn_nlop* h) { return new mdnn_nlop{h->op}; }
+int mdnn_nlop_n_in(const mdnn_nlop* h) { return h->op.n_in(); }
+int mdnn_nlop_n_out(const mdnn_nlop* h) { return h->op.n_out(); }
+
+int mdnn_nlop_in_dims(const mdnn_nlop* h, int i, int* rank, long* dims)
+{
+    return guard([&] {
+        const auto& d = h->op.in_dims(i);
+        *rank = int(d.size());
+        std::copy(d.begin(), d.end(), dims);
+    });
+}
+
+int mdnn_nlop_out_dims(const mdnn_nlop* h, int o, int* rank, long* dims)
+{
+    return guard([&] {
+        const auto& d = h->op.out_dims(o);
+        *rank = int(d.size());
+        std::copy(d.begin(), d.end(), dims);
+    });
+}
+
+int mdnn_nlop_apply(mdnn_nlop* h, int n_in, const mdnn_array* in, int n_out, mdnn_array* out)
+{
+    return guard([&] {
+        std::vector<A> args;
+        for (int i = 0; i < n_in; i++)
+            args.push_back(from_c(in[i]));
+        auto res = h->op.apply(args);
+        if (n_out != int(res.size()))
+            throw ShapeError("apply: expected " + std::to_string(res.size()) + " outputs");
+        for (int o = 0; o < n_out; o++)
+            if (out[o].data)
+                to_c(res[o], out[o]);
+    });
+}
+
+int mdnn_nlop_derivative(mdnn_nlop* h, int o, int i, const mdnn_array* dx, mdnn_array* dy)
+{
+    return guard([&] { to_c(h->op.derivative(o, i, from_c(*dx)), *dy); });
+}
+
+int mdnn_nlop_adjoint(mdnn_nlop* h, int o, int i, const mdnn_array* dy, mdnn_array* dx)
+{
+    return guard([&] { to_c(h->op.adjoint_derivative(o, i, from_c(*dy)), *dx); });
+}
+
+int mdnn_nlop_adjoint_all(mdnn_nlop* h, int o, const mdnn_array* dy, int n_in, mdnn_array* dx, const uint8_t* wanted)
+{
+    return guard([&] {
+        auto res = h->op.adjoint_all(o, from_c(*dy));
+        for (int i = 0; i < n_in && i < int(res.size()); i++)
+            if ((!wanted || wanted[i]) && dx[i].data)
+                to_c(res[i], dx[i]);
+    });
+}
+
+mdnn_nlop* mdnn_nlop_combine(const mdnn_nlop* f, const mdnn_nlop* g)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(combine(f->op, g->op)); });
+}
+mdnn_nlop* mdnn_nlop_link(const mdnn_nlop* h, int o, int i)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(link(h->op, o, i)); });
+}
+mdnn_nlop* mdnn_nlop_duplicate(const mdnn_nlop* h, int i, int j)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(duplicate(h->op, i, j)); });
+}
+mdnn_nlop* mdnn_nlop_chain(const mdnn_nlop* f, const mdnn_nlop* g)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(chain(f->op, g->op)); });
+}
+
+mdnn_nlop* mdnn_nlop_dft(int rank, const long* dims, unsigned long flags, int inverse)
+{
+    return guard_ptr<mdnn_nlop>([&] {
+        auto d = mkdims(rank, dims);
+        Linop<R> l(d, d, [flags, inverse](const A& x) { return dft(x, flags, inverse != 0); },
+                   [flags, inverse](const A& y) { return dft(y, flags, inverse == 0); });
+        return wrap(nlop_from_linop(l, inverse ? "ifft" : "fft"));
+    });
+}
+
+mdnn_nlop* mdnn_nlop_tenmul(int rank, const long* iter, const long* od, const long* so, const long* i1,
+                            const long* s1, const long* i2, const long* s2)
+{
+    return guard_ptr<mdnn_nlop>([&] {
+        return wrap(Nlop<R>(std::make_shared<TenMulNode<R>>("tenmul", mkdims(rank, iter), mkdims(rank, od),
+                                                            mkdims(rank, so), mkdims(rank, i1), mkdims(rank, s1),
+                                                            mkdims(rank, i2), mkdims(rank, s2))));
+    });
+}
+
+mdnn_nlop* mdnn_nlop_add(int rank, const long* dims, int subtract)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(nlop_add<R>(mkdims(rank, dims), subtract != 0)); });
+}
+mdnn_nlop* mdnn_nlop_bcast_add(int rank, const long* x, const long* b)
+{
+    return guard_ptr<mdnn_nlop>(
+        [&] { return wrap(Nlop<R>(std::make_shared<BroadcastAddNode<R>>(mkdims(rank, x), mkdims(rank, b)))); });
+}
+mdnn_nlop* mdnn_nlop_fork(int rank, const long* dims, int n)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(Nlop<R>(std::make_shared<ForkNode<R>>(mkdims(rank, dims), n))); });
+}
+mdnn_nlop* mdnn_nlop_zconj(int rank, const long* dims)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(nlop_zconj<R>(mkdims(rank, dims))); });
+}
+mdnn_nlop* mdnn_nlop_zreal(int rank, const long* dims)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(nlop_zreal<R>(mkdims(rank, dims))); });
+}
+mdnn_nlop* mdnn_nlop_real_chan(int rank, const long* dims, int cd)
+{
+    return guard_ptr<mdnn_nlop>(
+        [&] { return wrap(Nlop<R>(std::make_shared<RealChanNode<R>>(mkdims(rank, dims), cd))); });
+}
+mdnn_nlop* mdnn_nlop_chan_cplx(int rank, const long* dims, int cd)
+{
+    return guard_ptr<mdnn_nlop>(
+        [&] { return wrap(Nlop<R>(std::make_shared<ChanCplxNode<R>>(mkdims(rank, dims), cd))); });
+}
+mdnn_nlop* mdnn_nlop_crelu(int rank, const long* dims)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(Nlop<R>(std::make_shared<CReluNode<R>>(mkdims(rank, dims)))); });
+}
+mdnn_nlop* mdnn_nlop_exp_real(int rank, const long* dims)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(Nlop<R>(std::make_shared<ExpRealNode<R>>(mkdims(rank, dims)))); });
+}
+mdnn_nlop* mdnn_nlop_mse(int rank, const long* dims)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(nlop_loss<R>(LossKind::Mse, mkdims(rank, dims))); });
+}
+mdnn_nlop* mdnn_nlop_batchnorm(int rank, const long* dims, unsigned long flags, int train, double eps, double mom)
+{
+    return guard_ptr<mdnn_nlop>([&] {
+        return wrap(Nlop<R>(std::make_shared<BatchNormNode<R>>(mkdims(rank, dims), flags, train != 0, eps, mom)));
+    });
+}
+mdnn_nlop* mdnn_nlop_rbf(int rank, const long* z, int fd, int n, const float* centers, float sigma)
+{
+    return guard_ptr<mdnn_nlop>([&] {
+        std::vector<R> c(centers, centers + n);
+        return wrap(Nlop<R>(std::make_shared<RbfNode<R>>(mkdims(rank, z), fd, c, R(sigma))));
+    });
+}
+mdnn_nlop* mdnn_nlop_pad(int rank, const long* in, const long* out, const long* corner)
+{
+    return guard_ptr<mdnn_nlop>([&] {
+        return wrap(nlop_from_linop(linop_pad<R>(mkdims(rank, in), mkdims(rank, out), mkdims(rank, corner)), "pad"));
+    });
+}
+
+mdnn_nlop* mdnn_nlop_inverse(const mdnn_nlop* s, long max_iter, double tol)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(make_inverse_nlop<R>(s->op, max_iter, tol)); });
+}
+
+int mdnn_nlop_cg_status(const mdnn_nlop* h, long* iterations, double* rel_residual, int* converged)
+{
+    return guard([&] {
+        auto* inv = find_inverse(h->op);
+        if (!inv)
+            throw ConfigError("cg_status: no inverse node in graph");
+        const auto& st = inv->last_status();
+        *iterations = st.iterations;
+        *rel_residual = st.rel_residual;
+        *converged = st.converged ? 1 : 0;
+    });
+}
+
+int mdnn_sense_forward(const mdnn_array* coils, const mdnn_array* pattern, const mdnn_array* x, mdnn_array* y)
+{
+    return guard([&] { to_c(build_sense<R>(from_c(*coils), from_c(*pattern)).forward(from_c(*x)), *y); });
+}
+int mdnn_sense_adjoint(const mdnn_array* coils, const mdnn_array* pattern, const mdnn_array* y, mdnn_array* x)
+{
+    return guard([&] { to_c(build_sense<R>(from_c(*coils), from_c(*pattern)).adjoint(from_c(*y)), *x); });
+}
+int mdnn_sense_normal(const mdnn_array* coils, const mdnn_array* pattern, float lambda, const mdnn_array* x,
+                      mdnn_array* y)
+{
+    return guard([&] {
+        auto a = build_sense<R>(from_c(*coils), from_c(*pattern));
+        auto xv = from_c(*x);
+        auto w = a.normal(xv);
+        md_axpy(w, std::complex<R>(R(lambda)), xv);
+        to_c(w, *y);
+    });
+}
+int mdnn_cg_normal_solve(const mdnn_array* coils, const mdnn_array* pattern, float lambda, const mdnn_array* b,
+                         long max_iter, double tol, mdnn_array* x, long* iterations, double* rel_residual)
+{
+    return guard([&] {
+        auto a = build_sense<R>(from_c(*coils), from_c(*pattern));
+        CgStatus st;
+        auto r = cg_normal_solve<R>(a, R(lambda), from_c(*b), max_iter, tol, &st);
+        to_c(r, *x);
+        if (iterations)
+            *iterations = st.iterations;
+        if (rel_residual)
+            *rel_residual = st.rel_residual;
+    });
+}
+int mdnn_dft(const mdnn_array* in, unsigned long flags, int inverse, mdnn_array* out)
+{
+    return guard([&] { to_c(dft(from_c(*in), flags, inverse != 0), *out); });
+}
+
+// ---- Model ------------------------------------------------------------------
+
+void mdnn_model_free(mdnn_model* m) { delete m; }
+mdnn_nlop* mdnn_model_nlop(const mdnn_model* m) { return new mdnn_nlop{m->m.op}; }
+int mdnn_model_n_args(const mdnn_model* m) { return int(m->m.args.size()); }
+const char* mdnn_model_arg_name(const mdnn_model* m, int i) { return m->m.args.at(i).name.c_str(); }
+int mdnn_model_arg_kind(const mdnn_model* m, int i) { return int(m->m.args.at(i).kind); }
+int mdnn_model_arg_real(const mdnn_model* m, int i) { return m->m.args.at(i).real_weights ? 1 : 0; }
+int mdnn_model_n_outs(const mdnn_model* m) { return int(m->m.out_names.size()); }
+const char* mdnn_model_out_name(const mdnn_model* m, int o) { return m->m.out_names.at(o).c_str(); }
+int mdnn_model_arg_index(const mdnn_model* m, const char* name)
+{
+    int r = -1;
+    if (guard([&] { r = m->m.arg_index(name); }) != MDNN_OK)
+        return -1;
+    return r;
+}
+int mdnn_model_output_index(const mdnn_model* m, const char* name)
+{
+    int r = -1;
+    if (guard([&] { r = m->m.output_index(name); }) != MDNN_OK)
+        return -1;
+    return r;
+}
+long mdnn_model_num_real_params(const mdnn_model* m) { return m->m.num_real_params(); }
+
+int mdnn_model_init_weight(const mdnn_model* m, uint64_t seed, const char* name, mdnn_array* out)
+{
+    return guard([&] {
+        auto w = m->m.init_weights(seed);
+        auto it = w.find(name);
+        if (it == w.end())
+            throw ConfigError(std::string("init_weight: no weights argument ") + name);
+        to_c(it->second, *out);
+    });
+}
+
+mdnn_model* mdnn_model_chain(const mdnn_model* a, const mdnn_model* b, const char* b_in, int a_out)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(model_chain(a->m, b->m, b_in, a_out)); });
+}
+mdnn_model* mdnn_model_link(const mdnn_model* m, int out_idx, const char* arg)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(model_link(m->m, out_idx, arg)); });
+}
+mdnn_model* mdnn_model_combine(const mdnn_model* a, const mdnn_model* b)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(model_combine(a->m, b->m)); });
+}
+mdnn_model* mdnn_model_dedupe(const mdnn_model* m)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(model_dedupe(m->m)); });
+}
+
+mdnn_model* mdnn_conv_layer(const char* name, const mdnn_conv_spec* s, int bias)
+{
+    return guard_ptr<mdnn_model>([&] {
+        ConvSpec spec;
+        spec.in_dims = mkdims(s->rank, s->in_dims);
+        spec.axes.assign(s->axes, s->axes + s->n_axes);
+        spec.kernel.assign(s->kernel, s->kernel + s->n_axes);
+        spec.chan_dim = s->chan_dim;
+        spec.out_channels = s->out_channels;
+        spec.pad_same = s->pad_same != 0;
+        spec.transposed = s->transposed != 0;
+        return wrapm(conv_layer<R>(name, spec, bias != 0));
+    });
+}
+mdnn_model* mdnn_batchnorm_layer(const char* name, int rank, const long* dims, unsigned long flags, int train,
+                                 double eps, double mom)
+{
+    return guard_ptr<mdnn_model>(
+        [&] { return wrapm(batchnorm_layer<R>(name, mkdims(rank, dims), flags, train != 0, eps, mom)); });
+}
+
+void mdnn_modl_cfg_default(mdnn_modl_cfg* c)
+{
+    ModlConfig d;
+    c->iterations = d.iterations;
+    c->layers = d.layers;
+    c->filters = d.filters;
+    c->kernel = d.kernel;
+    c->cg_iter = d.cg_iter;
+    c->cg_tol = d.cg_tol;
+    c->lambda_init = d.lambda_init;
+    c->im_x = d.im_x;
+    c->im_y = d.im_y;
+    c->coils = d.coils;
+    c->maps = d.maps;
+    c->batch = d.batch;
+    c->train_mode = d.train_mode ? 1 : 0;
+}
+void mdnn_varnet_cfg_default(mdnn_varnet_cfg* c)
+{
+    VarNetConfig d;
+    c->iterations = d.iterations;
+    c->filters = d.filters;
+    c->kernel = d.kernel;
+    c->rbf = d.rbf;
+    c->im_x = d.im_x;
+    c->im_y = d.im_y;
+    c->coils = d.coils;
+    c->maps = d.maps;
+    c->batch = d.batch;
+}
+mdnn_model* mdnn_build_modl(const mdnn_modl_cfg* cfg)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(fixed_build_modl(to_modl(cfg))); });
+}
+mdnn_model* mdnn_build_varnet(const mdnn_varnet_cfg* cfg)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(fixed_build_varnet(to_varnet(cfg))); });
+}
+mdnn_model* mdnn_sense_normal_fragment(const mdnn_sense_dims* sd)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(detail::sense_normal_fragment<R>(to_sd(sd))); });
+}
+mdnn_model* mdnn_sense_adjoint_fragment(const mdnn_sense_dims* sd)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(detail::sense_adjoint_fragment<R>(to_sd(sd))); });
+}
+mdnn_model* mdnn_modl_normal_plus_lambda(const mdnn_sense_dims* sd)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(detail::modl_normal_plus_lambda<R>(to_sd(sd))); });
+}
+mdnn_model* mdnn_loss_model_mse(int rank, const long* dims)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(loss_model<R>(LossKind::Mse, mkdims(rank, dims))); });
+}
+
+int mdnn_sim_item(uint64_t seed, long item, long x, long y, long coils, float* phantom, float* coil_maps)
+{
+    return guard([&] {
+        Dims img(max_rank, 1), cm(max_rank, 1);
+        img[0] = cm[0] = x;
+        img[1] = cm[1] = y;
+        cm[3] = coils;
+        A ph(img), cc(cm);
+        Rng prng(hash_rand(seed, 2 * uint64_t(item)));
+        Rng crng(hash_rand(seed, 2 * uint64_t(item) + 1));
+        detail::draw_phantom<R>(ph, prng);
+        detail::draw_coils<R>(cc, crng);
+        for (long k = 0; k < ph.size(); k++) {
+            phantom[2 * k] = float(ph.data()[k].real());
+            phantom[2 * k + 1] = float(ph.data()[k].imag());
+        }
+        for (long k = 0; k < cc.size(); k++) {
+            coil_maps[2 * k] = float(cc.data()[k].real());
+            coil_maps[2 * k + 1] = float(cc.data()[k].imag());
+        }
+    });
+}
+
+int mdnn_sim_pattern(long y, long accel, long acl, float* pattern)
+{
+    return guard([&] {
+        auto p = make_pattern<R>(y, accel, acl);
+        for (long k = 0; k < y; k++) {
+            pattern[2 * k] = float(p.data()[k].real());
+            pattern[2 * k + 1] = float(p.data()[k].imag());
+        }
+    });
+}
+
+// ---- training -----------------------------------------------------------------
+
+void mdnn_train_cfg_default(mdnn_train_cfg* c)
+{
+    TrainConfig d;
+    c->lr = d.lr;
+    c->beta1 = d.adam.beta1;
+    c->beta2 = d.adam.beta2;
+    c->eps = d.adam.eps;
+    c->clip = d.clip;
+}
+
+mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg* c, uint64_t seed)
+{
+    return guard_ptr<mdnn_trainer>([&] {
+        auto t = std::make_unique<mdnn_trainer>();
+        t->cfg.algo = OptAlgo::Adam;
+        t->cfg.lr = c->lr;
+        t->cfg.adam.beta1 = c->beta1;
+        t->cfg.adam.beta2 = c->beta2;
+        t->cfg.adam.eps = c->eps;
+        t->cfg.clip = c->clip;
+        t->cfg.seed = seed;
+        const auto& m = model->m;
+        auto loss = loss_model<R>(LossKind::Mse, m.op.out_dims(m.output_index("out")));
+        t->joint = model_chain(m, loss, "prediction", m.output_index("out"));
+        t->weights = t->joint.init_weights(seed);
+        t->adam.resize(t->joint.args.size());
+        t->ipalm.resize(t->joint.args.size());
+        for (size_t i = 0; i < t->joint.args.size(); i++)
+            if (t->joint.args[i].kind == ArgKind::Weights) {
+                t->weight_args.push_back(int(i));
+                t->weight_names.push_back(t->joint.args[i].name);
+            }
+        return t.release();
+    });
+}
+
+void mdnn_trainer_free(mdnn_trainer* t) { delete t; }
+
+int mdnn_trainer_set_data(mdnn_trainer* t, const char* name, const mdnn_array* a)
+{
+    return guard([&] { t->batch[name] = from_c(*a); });
+}
+int mdnn_trainer_set_weight(mdnn_trainer* t, const char* name, const mdnn_array* a)
+{
+    return guard([&] {
+        if (!t->weights.count(name))
+            throw ConfigError(std::string("no weight named ") + name);
+        t->weights[name] = from_c(*a);
+    });
+}
+int mdnn_trainer_get_weight(mdnn_trainer* t, const char* name, mdnn_array* out)
+{
+    return guard([&] { to_c(t->weights.at(name), *out); });
+}
+int mdnn_trainer_get_grad(mdnn_trainer* t, const char* name, mdnn_array* out)
+{
+    return guard([&] { to_c(t->grads.at(name), *out); });
+}
+
+int mdnn_trainer_forward_backward(mdnn_trainer* t, double* loss)
+{
+    // optim.hpp:341-381 (eval, loss check, adjoint_all) without the update
+    return guard([&] {
+        auto& J = t->joint;
+        const int loss_idx = J.output_index("loss");
+        t->last_outs = J.op.apply(J.gather_inputs(t->weights, t->batch));
+        double lv = t->last_outs[loss_idx].data()[0].real();
+        if (!std::isfinite(lv))
+            throw SolverError("training aborted: non-finite loss");
+        auto grads = J.op.adjoint_all(loss_idx, A::scalar(std::complex<R>(1)));
+        t->grads.clear();
+        t->flat.clear();
+        for (int i : t->weight_args) {
+            t->grads[J.args[i].name] = grads[i];
+            for (long k = 0; k < grads[i].size(); k++) {
+                t->flat.push_back(float(grads[i].data()[k].real()));
+                t->flat.push_back(float(grads[i].data()[k].imag()));
+            }
+        }
+        if (loss)
+            *loss = lv;
+    });
+}
+
+int mdnn_trainer_grad_buffer(mdnn_trainer* t, float** ptr, long* n)
+{
+    *ptr = t->flat.data();
+    *n = long(t->flat.size());
+    return MDNN_OK;
+}
+
+int mdnn_trainer_update(mdnn_trainer* t, float grad_scale)
+{
+    // optim.hpp:383-399 per-weight update, from the (possibly reduced) flat buffer
+    return guard([&] {
+        auto& J = t->joint;
+        long off = 0;
+        for (int i : t->weight_args) {
+            const auto& arg = J.args[i];
+            auto& w = t->weights.at(arg.name);
+            A g(w.dims());
+            for (long k = 0; k < g.size(); k++, off += 2)
+                g.data()[k] = std::complex<R>(R(t->flat[off] * grad_scale), R(t->flat[off + 1] * grad_scale));
+            detail::clip_gradient(g, t->cfg.clip);
+            if (arg.real_weights)
+                md_foreach(g, [](auto& v) { v = std::complex<R>(v.real(), 0); });
+            adam_step(w, g, t->adam[i], t->cfg.adam, R(t->cfg.lr));
+            if (arg.real_weights)
+                md_foreach(w, [](auto& v) { v = std::complex<R>(v.real(), 0); });
+            if (arg.prox)
+                arg.prox->apply(w, R(t->cfg.lr));
+        }
+        update_stats(J, t->last_outs, t->weights);
+    });
+}
+
+int mdnn_trainer_step(mdnn_trainer* t, double* loss)
+{
+    // the reference's own run_step (optim.hpp:314)
+    return guard([&] {
+        double lv = run_step(t->joint, t->weights, t->batch, t->cfg, t->adam, t->ipalm);
+        if (loss)
+            *loss = lv;
+    });
+}
+
+int mdnn_trainer_n_weights(const mdnn_trainer* t) { return int(t->weight_names.size()); }
+const char* mdnn_trainer_weight_name(const mdnn_trainer* t, int k) { return t->weight_names.at(k).c_str(); }
+
+} // extern "C"
