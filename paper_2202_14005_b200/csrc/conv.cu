@@ -1,0 +1,229 @@
+// Complex "same" cross-correlation layers (conv_layer, nn.hpp:344-426; the
+// TenMul wiring of conv_tenmul, nn.hpp:305-337) on CUDA cores.
+//
+//   fwd        y[p,f]  = sum_{t,c} x[p+t-c0, c] w[t,c,f]
+//   bwd-data   dx[q,c] = sum_{t,f} dy[q-t+c0, f] conj(w[t,c,f])
+//   bwd-weight dw[t,c,f] = sum_p dy[p,f] conj(x[p+t-c0, c])
+//
+// Canonical layout (x fastest, channel on dim 2, batch on dim 15).  These
+// kernels serve every channel count and kernel size; the 64->64 MoDL layers
+// are dispatched to the tcgen05 implicit-GEMM path in conv_tc.cu when it is
+// enabled.  Reductions are fixed-order (no atomics): bitwise run-to-run stable.
+#include "kernels.h"
+
+#include <algorithm>
+
+namespace mdnn {
+
+namespace {
+
+constexpr int TX = 32, TY = 8;   // output tile (pixels)
+constexpr int FG = 8;            // output channels per block
+constexpr int MAXK = 11;
+
+// mode 0: fwd (in = x, Cin in, weights w[t,c,f]); mode 1: bwd-data (in = dy,
+// channels Cout, weights conj(w[t,c,f]) flipped, output channel c)
+template<int MODE>
+__global__ void __launch_bounds__(TX* TY) k_conv_direct(cfloat* __restrict__ out, const cfloat* __restrict__ in,
+                                                       const cfloat* __restrict__ w, ConvGeom g)
+{
+    __shared__ float2 tile[TY + MAXK - 1][TX + MAXK - 1];
+    __shared__ float2 wsh[MAXK * MAXK][FG];
+    const long nin = MODE == 0 ? g.Cin : g.Cout;
+    const long nout = MODE == 0 ? g.Cout : g.Cin;
+    const long ngrp = (nout + FG - 1) / FG;
+    const long b = blockIdx.z / ngrp;
+    const long f0 = (blockIdx.z % ngrp) * FG;
+    const long x0 = long(blockIdx.x) * TX, y0 = long(blockIdx.y) * TY;
+    const int KX = int(g.KX), KY = int(g.KY);
+    // offset of the input window: fwd  in[p + t - c0]
+    //                             bwd  in[q - t + c0] = in[q + t' - (K-1-c0)], t' = K-1-t
+    const long ox = MODE == 0 ? g.px : (g.KX - 1 - g.px);
+    const long oy = MODE == 0 ? g.py : (g.KY - 1 - g.py);
+    const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+    float2 acc[FG];
+#pragma unroll
+    for (int f = 0; f < FG; f++)
+        acc[f] = float2{0.f, 0.f};
+    const int HX = TX + KX - 1, HY = TY + KY - 1;
+    for (long c = 0; c < nin; c++) {
+        const cfloat* src = in + g.X * g.Y * (c + nin * b);
+        for (int e = threadIdx.x; e < HX * HY; e += blockDim.x) {
+            int hx = e % HX, hy = e / HX;
+            long gx = x0 + hx - ox, gy = y0 + hy - oy;
+            tile[hy][hx] = (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? src[gx + g.X * gy] : float2{0.f, 0.f};
+        }
+        for (int e = threadIdx.x; e < KX * KY * FG; e += blockDim.x) {
+            int t = e % (KX * KY), f = e / (KX * KY);
+            long fo = f0 + f;
+            float2 v{0.f, 0.f};
+            if (fo < nout) {
+                if (MODE == 0) {
+                    v = w[t + g.KX * g.KY * (c + g.Cin * fo)];
+                } else {
+                    // tap t' of the flipped kernel = t = K-1-t' per axis; weight w[t, fo(=c_in), c(=f_out)]
+                    int tpx = t % KX, tpy = t / KX;
+                    long tt = (KX - 1 - tpx) + g.KX * (KY - 1 - tpy);
+                    float2 ww = w[tt + g.KX * g.KY * (fo + g.Cin * c)];
+                    v = float2{ww.x, -ww.y};
+                }
+            }
+            wsh[t][f] = v;
+        }
+        __syncthreads();
+        for (int ky = 0; ky < KY; ky++)
+            for (int kx = 0; kx < KX; kx++) {
+                float2 xv = tile[ty + ky][tx + kx];
+                const int t = kx + KX * ky;
+#pragma unroll
+                for (int f = 0; f < FG; f++) {
+                    float2 wv = wsh[t][f];
+                    acc[f].x = fmaf(xv.x, wv.x, fmaf(-xv.y, wv.y, acc[f].x));
+                    acc[f].y = fmaf(xv.x, wv.y, fmaf(xv.y, wv.x, acc[f].y));
+                }
+            }
+        __syncthreads();
+    }
+    const long px = x0 + tx, py = y0 + ty;
+    if (px < g.X && py < g.Y)
+#pragma unroll
+        for (int f = 0; f < FG; f++)
+            if (f0 + f < nout)
+                out[px + g.X * (py + g.Y * ((f0 + f) + nout * b))] = acc[f];
+}
+
+// bwd-weight: block = (c-group x f-group, split); loops over its share of
+// pixel tiles; thread owns combos (t, c, f) accumulated in registers.
+constexpr int WG_C = 4, WG_F = 8;         // channels per block
+constexpr int WTX = 32, WTY = 8;          // pixel tile
+constexpr int WMAXC = 4;                  // combos per thread
+
+__global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, const cfloat* __restrict__ x,
+                                                    const cfloat* __restrict__ dy, ConvGeom g, int nsplit)
+{
+    __shared__ float2 xt[WG_C][WTY + MAXK - 1][WTX + MAXK - 1];
+    __shared__ float2 dyt[WG_F][WTY][WTX];
+    const int KX = int(g.KX), KY = int(g.KY), KK = KX * KY;
+    const long ncg = (g.Cin + WG_C - 1) / WG_C;
+    const long c0 = (blockIdx.x % ncg) * WG_C;
+    const long f0 = (blockIdx.x / ncg) * WG_F;
+    const int split = blockIdx.y;
+    const long ntx = (g.X + WTX - 1) / WTX, nty = (g.Y + WTY - 1) / WTY;
+    const long ntiles = ntx * nty * g.B;
+    const int ncombo = KK * WG_C * WG_F;
+    const int HX = WTX + KX - 1, HY = WTY + KY - 1;
+    float2 acc[WMAXC];
+#pragma unroll
+    for (int i = 0; i < WMAXC; i++)
+        acc[i] = float2{0.f, 0.f};
+    for (long tile = split; tile < ntiles; tile += nsplit) {
+        const long b = tile / (ntx * nty);
+        const long tr = tile % (ntx * nty);
+        const long x0 = (tr % ntx) * WTX, y0 = (tr / ntx) * WTY;
+        for (int e = threadIdx.x; e < WG_C * HX * HY; e += blockDim.x) {
+            int hx = e % HX, hy = (e / HX) % HY, cc = e / (HX * HY);
+            long gx = x0 + hx - g.px, gy = y0 + hy - g.py, c = c0 + cc;
+            xt[cc][hy][hx] = (c < g.Cin && gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y)
+                                 ? x[gx + g.X * (gy + g.Y * (c + g.Cin * b))]
+                                 : float2{0.f, 0.f};
+        }
+        for (int e = threadIdx.x; e < WG_F * WTX * WTY; e += blockDim.x) {
+            int px = e % WTX, py = (e / WTX) % WTY, ff = e / (WTX * WTY);
+            long gx = x0 + px, gy = y0 + py, f = f0 + ff;
+            dyt[ff][py][px] = (f < g.Cout && gx < g.X && gy < g.Y) ? dy[gx + g.X * (gy + g.Y * (f + g.Cout * b))]
+                                                                   : float2{0.f, 0.f};
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < WMAXC; i++) {
+            int combo = threadIdx.x + i * blockDim.x;
+            if (combo >= ncombo)
+                break;
+            int t = combo % KK, cc = (combo / KK) % WG_C, ff = combo / (KK * WG_C);
+            int kx = t % KX, ky = t / KX;
+            float ar = acc[i].x, ai = acc[i].y;
+            for (int py = 0; py < WTY; py++)
+                for (int px = 0; px < WTX; px++) {
+                    float2 d = dyt[ff][py][px];
+                    float2 xv = xt[cc][py + ky][px + kx];
+                    // d * conj(xv)
+                    ar = fmaf(d.x, xv.x, fmaf(d.y, xv.y, ar));
+                    ai = fmaf(d.y, xv.x, fmaf(-d.x, xv.y, ai));
+                }
+            acc[i] = float2{ar, ai};
+        }
+        __syncthreads();
+    }
+    // partial layout [split][t + KK*(c + Cin*f)]
+    for (int i = 0; i < WMAXC; i++) {
+        int combo = threadIdx.x + i * blockDim.x;
+        if (combo >= ncombo)
+            break;
+        int t = combo % KK, cc = (combo / KK) % WG_C, ff = combo / (KK * WG_C);
+        long c = c0 + cc, f = f0 + ff;
+        if (c < g.Cin && f < g.Cout)
+            part[size_t(split) * KK * g.Cin * g.Cout + t + KK * (c + g.Cin * f)] = acc[i];
+    }
+}
+
+__global__ void k_sum_splits(cfloat* out, const float2* part, long n, int nsplit)
+{
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+        double ar = 0, ai = 0;
+        for (int s = 0; s < nsplit; s++) {
+            ar += part[size_t(s) * n + i].x;
+            ai += part[size_t(s) * n + i].y;
+        }
+        out[i] = float2{float(ar), float(ai)};
+    }
+}
+
+void check_geom(const ConvGeom& g)
+{
+    if (g.KX > MAXK || g.KY > MAXK)
+        throw ConfigError("conv: kernel extent > 11 not supported on device");
+}
+
+} // namespace
+
+void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
+{
+    check_geom(g);
+    dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
+              unsigned(g.B * ((g.Cout + FG - 1) / FG)));
+    k_conv_direct<0><<<grid, TX * TY, 0, ctx().stream>>>(y, x, w, g);
+    KERNEL_CHECK();
+}
+
+void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom& g)
+{
+    check_geom(g);
+    dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
+              unsigned(g.B * ((g.Cin + FG - 1) / FG)));
+    k_conv_direct<1><<<grid, TX * TY, 0, ctx().stream>>>(dx, dy, w, g);
+    KERNEL_CHECK();
+}
+
+void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g)
+{
+    check_geom(g);
+    const long KK = g.KX * g.KY;
+    if (KK * WG_C * WG_F > 256 * WMAXC)
+        throw ConfigError("conv: kernel too large for the weight-gradient kernel");
+    const long ngroups = ((g.Cin + WG_C - 1) / WG_C) * ((g.Cout + WG_F - 1) / WG_F);
+    const long ntiles = ((g.X + WTX - 1) / WTX) * ((g.Y + WTY - 1) / WTY) * g.B;
+    long target = long(ctx().sm_count) * 4;
+    int nsplit = int(std::max(1L, std::min(ntiles, (target + ngroups - 1) / ngroups)));
+    const long n = KK * g.Cin * g.Cout;
+    auto& c = ctx();
+    float2* part;
+    CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
+    dim3 grid{unsigned(ngroups), unsigned(nsplit)};
+    k_conv_wgrad<<<grid, 256, 0, c.stream>>>(part, x, dy, g, nsplit);
+    KERNEL_CHECK();
+    k_sum_splits<<<int(std::min(1024L, (n + 255) / 256)), 256, 0, c.stream>>>(dw, part, n, nsplit);
+    KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(part, c.stream));
+}
+
+} // namespace mdnn

@@ -1,0 +1,163 @@
+// Launchers for every device kernel of the hot path.  All launch on the
+// current device context's stream (core.h); none synchronises.
+#pragma once
+
+#include "core.h"
+
+#include <functional>
+
+namespace mdnn {
+
+// ---- generic md helpers (ew.cu) -------------------------------------------
+// dst[p.sd] = src[p.ss] over dims (strides in complex elements)
+void launch_strided_copy(const Dims& dims, cfloat* dst, const Dims& sd, const cfloat* src, const Dims& ss);
+void launch_layout_convert(const DArray& in, const DArray& out);
+
+// out = a + s * b (n complex); s real
+void launch_add(cfloat* out, const cfloat* a, const cfloat* b, float s, long n);
+// y += alpha * x
+void launch_axpy(cfloat* y, cfloat alpha, const cfloat* x, long n);
+// out = s * in (complex s)
+void launch_scale(cfloat* out, const cfloat* in, cfloat s, long n);
+// out = scalar[0] * in, scalar read on the device; conj_s conjugates it
+void launch_scale_dev(cfloat* out, const cfloat* in, const cfloat* scalar, bool conj_s, long n);
+void launch_conj(cfloat* out, const cfloat* in, long n);
+// out = (factor * Re(scalar[0])) * in
+void launch_scale_dev_real(cfloat* out, const cfloat* in, const cfloat* scalar, float factor, long n);
+// out[0] = (factor * Re(in[0]), 0)
+void launch_real_scalar(cfloat* out, const cfloat* in, float factor);
+void launch_real(cfloat* out, const cfloat* in, long n);
+void launch_crelu(cfloat* out, const cfloat* in, long n);
+void launch_crelu_mask(cfloat* out, const cfloat* d, const cfloat* x, long n);
+void launch_exp_real(cfloat* out, const cfloat* in, long n);
+void launch_mul_real_real(cfloat* out, const cfloat* y, const cfloat* d, long n); // out = (Re y * Re d, 0)
+void launch_neg(cfloat* out, const cfloat* in, long n);
+
+// complex split/join on a channel dim (RealChan / ChanCplx, ops.hpp:318-411):
+// in [.., 1(chan), ..] -> out [.., 2, ..]; inner = prod dims before chan, outer = after
+void launch_real_chan_split(cfloat* out, const cfloat* in, long inner, long outer);
+void launch_real_chan_join(cfloat* out, const cfloat* in, long inner, long outer);
+
+// Broadcast binary op over out dims with per-operand strides (0 = broadcast).
+// op: 0 = a + b, 1 = a * b, 2 = a * conj(b)
+void launch_bcast_binary(const Dims& dims, cfloat* out, const cfloat* a, const Dims& sa, const cfloat* b,
+                         const Dims& sb, int op);
+
+// "ISO" reductions: data viewed as [inner][stat][outer] (column-major, inner
+// fastest); out[stat] = sum over inner,outer of f(a, b) computed in double,
+// deterministic two-stage tree.  mode: 0 sum a; 1 sum a*conj(b); 2 sum |a|^2 (real)
+void launch_iso_reduce(cfloat* out, const cfloat* a, const cfloat* b, long inner, long nstat, long outer, int mode,
+                       float scale);
+
+// Batch-global complex dot <a,b> = sum a conj(b) accumulated in double
+// (mdarray.hpp:679-708) into a device double2 (no host sync).
+void launch_zdot(double* out2, const cfloat* a, const cfloat* b, long n);
+double host_znorm(const cfloat* a, long n);
+
+// generic TenMul contraction (md_fmac2 / md_zfmacc2, mdarray.hpp:485-523):
+// out[p.so] += in1[p.s1] * (conj?)in2[p.s2], out zeroed by the caller
+void launch_fmac_generic(const Dims& iter, cfloat* out, const Dims& so, const cfloat* in1, const Dims& s1,
+                         const cfloat* in2, const Dims& s2, bool conj2);
+
+// ---- FFT (fft.cu) -----------------------------------------------------------
+// unitary (1/sqrt n) uncentred DFT along one dim of a column-major array
+void launch_fft_dim(cfloat* out, const cfloat* in, const Dims& dims, int dim, bool inverse);
+// true if every prime factor of n has a device radix (<= 31) and n fits smem
+bool fft_supported(long n);
+// multi-dim dft (fft.hpp:180-226): out may equal in
+void fft_flags(cfloat* out, const cfloat* in, const Dims& dims, unsigned long flags, bool inverse);
+
+// ---- SENSE (sense.cu) ---------------------------------------------------------
+struct SenseGeom {
+    long X, Y, C, M, B;             // image x, y, coils, map sets, batch
+    long pat_x, pat_y, pat_c, pat_b; // pattern extents (each 1 = broadcast, or full)
+};
+// coil images u[x,y,c,b] = sum_m C[x,y,c,m,b] x[x,y,m,b]
+void launch_coil_mul(cfloat* u, const cfloat* x, const cfloat* coils, const SenseGeom& g);
+// x[x,y,m,b] = sum_c conj(C[x,y,c,m,b]) u[x,y,c,b]
+void launch_coil_adj(cfloat* x, const cfloat* u, const cfloat* coils, const SenseGeom& g);
+// u *= pattern (broadcast over x if pattern_xinv, over coils always)
+void launch_pattern_mul(cfloat* out, const cfloat* u, const cfloat* pattern, const SenseGeom& g);
+// A x  = P F C x       (recon.hpp:100-110): out [X,Y,1,C,1..,B]
+void sense_forward(cfloat* y, const cfloat* x, const cfloat* coils, const cfloat* pattern, const SenseGeom& g);
+// A^H y = C^H F^H P y  (recon.hpp:111-121)
+void sense_adjoint(cfloat* x, const cfloat* y, const cfloat* coils, const cfloat* pattern, const SenseGeom& g);
+// out = A^H A x + lam * x; lam is a device complex scalar (may be null = 0).
+// Uses the fused single-pass y-only kernel when the pattern is x-invariant.
+// coils2 (nullable) = the maps of the adjoint coil combine when they differ
+void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloat* pattern, const cfloat* lam,
+                  const SenseGeom& g, const cfloat* coils2 = nullptr);
+// CG on S = A^H A + lam (recon.hpp:143-181), device-resident state and scalars.
+struct CgResult {
+    long iterations;
+    double rel_residual;
+    bool converged;
+};
+// status_out (device, nullable): [iterations, rel_residual, converged] as doubles
+void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfloat* pattern, const cfloat* lam,
+                      const SenseGeom& g, long max_iter, double tol, double* status_out);
+CgResult read_cg_status(const double* status_dev);
+// CG for an arbitrary Hermitian positive-definite map given as a callback
+// (InverseNode over a user graph, recon.hpp:295-304); same device state machine.
+using CgApply = std::function<void(const cfloat* p, cfloat* ap)>;
+void cg_generic_device(cfloat* x, const cfloat* b, long n, const CgApply& apply, long max_iter, double tol,
+                       double* status_out);
+
+// ---- conv (conv.cu) -----------------------------------------------------------
+struct ConvGeom {
+    long X, Y, B;      // spatial extent (same padding) and batch
+    long Cin, Cout;    // complex channels
+    long KX, KY;       // kernel extents
+    long px, py;       // corner offsets ((k-1)/2)
+};
+// y[p,f] = sum_{t,c} x[p+t-c0, c] w[t,c,f]
+void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g);
+// dx[q,c] = sum_{t,f} dy[q-t+c0, f] conj(w[t,c,f])
+void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom& g);
+// dw[t,c,f] = sum_p dy[p,f] conj(x[p+t-c0, c])
+void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
+
+// ---- batch norm (bn.cu) ----------------------------------------------------------
+struct IsoGeom {
+    long inner, nstat, outer;
+};
+// train forward: mean, var (biased, E|x-mu|^2), u = x - mu, istd, y = u * istd,
+// moving stats out = (1-mom) in + mom batch  (ops.hpp:1104-1136)
+void bn_train_forward(cfloat* y, cfloat* u, cfloat* istd, cfloat* mean_out, cfloat* var_out, const cfloat* x,
+                      const cfloat* mean_in, const cfloat* var_in, const IsoGeom& g, float eps, float mom);
+void bn_infer_forward(cfloat* y, cfloat* u, cfloat* istd, const cfloat* x, const cfloat* mean_in,
+                      const cfloat* var_in, const IsoGeom& g, float eps);
+// train adjoint wrt x (ops.hpp:1245-1263)
+void bn_train_adjoint_x(cfloat* dx, const cfloat* g_in, const cfloat* u, const cfloat* istd, const IsoGeom& g);
+// train tangent wrt x (ops.hpp:1172-1190)
+void bn_train_deriv_x(cfloat* dy, const cfloat* dx, const cfloat* u, const cfloat* istd, const IsoGeom& g);
+// per-stat broadcast multiply out = in * s[stat] (conj optional)
+void launch_stat_mul(cfloat* out, const cfloat* in, const cfloat* s, const IsoGeom& g, bool conj_s);
+// out = in + b[stat]
+void launch_stat_add(cfloat* out, const cfloat* in, const cfloat* b, const IsoGeom& g);
+// out = s[stat]*c : out[i] = u[i] * f(stat) -- helper for BN adjoint wrt stats
+void launch_stat_mul_u_f(cfloat* out, const cfloat* u, const cfloat* f, const IsoGeom& g);
+
+// ---- RBF (rbf.cu, ops.hpp:1308-1427) -------------------------------------------------
+struct RbfGeom {
+    long inner, nf, outer; // z viewed [inner][filter][outer]
+    int nw;
+    float sigma;
+};
+void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
+void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
+void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
+void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g);
+void rbf_deriv_w(cfloat* dy, const cfloat* dw, const cfloat* z, const float* mu, const RbfGeom& g);
+
+// ---- loss / optimiser (train.cu) ------------------------------------------------------
+// mse: out scalar = (1/n) sum |p - r|^2 (double accumulate), diff = p - r
+void mse_forward(cfloat* loss, cfloat* diff, const cfloat* p, const cfloat* r, long n);
+// complex Adam (optim.hpp:81-108) on a flat complex range
+void adam_update(cfloat* theta, cfloat* m, float* v, const cfloat* g, long n, float lr, float b1, float b2,
+                 float eps, float c1, float c2, float gscale, bool real_weights, bool nonneg_prox);
+// flat gradient gather/scatter
+void launch_copy(cfloat* dst, const cfloat* src, long n);
+void launch_check_finite(const cfloat* a, long n); // sets ERRF_NONFINITE_GRAD
+
+} // namespace mdnn

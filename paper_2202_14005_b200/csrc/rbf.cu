@@ -1,0 +1,151 @@
+// Gaussian radial-basis activation of the Variational Network (RbfNode,
+// ops.hpp:1308-1427):  phi(z)_k = sum_j w[f,j] exp(-(z_k - mu_j)^2 / (2 sigma^2))
+// acting on Re z, with z viewed as [inner][filter][outer] and w as [nf, nw].
+// Weight gradients reduce per (filter, basis) with fixed-order partials.
+#include "kernels.h"
+
+#include <algorithm>
+
+namespace mdnn {
+
+namespace {
+
+constexpr int kT = 256;
+constexpr int kMaxW = 64;
+
+int grid_for(long n)
+{
+    long blocks = (n + kT - 1) / kT;
+    return int(std::max(1L, std::min(blocks, long(ctx().sm_count) * 8)));
+}
+
+__device__ __forceinline__ float gauss(float z, float mu, float sigma)
+{
+    float d = (z - mu) / sigma;
+    return expf(-d * d / 2.f);
+}
+
+// mode 0: y = phi(z); 1: dz = Re(g) * phi'(z) (adjoint, also tangent with g = dx);
+// 2: y = sum_j Re(dw) e_j (tangent wrt w)
+__global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z, const cfloat* __restrict__ w,
+                          const cfloat* __restrict__ gin, const float* __restrict__ mu, RbfGeom g, int mode)
+{
+    __shared__ float smu[kMaxW];
+    for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
+        smu[j] = mu[j];
+    __syncthreads();
+    const long n = g.inner * g.nf * g.outer;
+    const float s2 = g.sigma * g.sigma;
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+        const long f = (i / g.inner) % g.nf;
+        const float zk = z[i].x;
+        float acc = 0.f;
+        for (int j = 0; j < g.nw; j++) {
+            const float e = gauss(zk, smu[j], g.sigma);
+            const float wj = w[f + j * g.nf].x;
+            if (mode == 1)
+                acc += wj * e * (-(zk - smu[j]) / s2);
+            else
+                acc += wj * e;
+        }
+        if (mode == 1)
+            acc *= gin[i].x;
+        out[i] = float2{acc, 0.f};
+    }
+}
+
+// partial[(f * nw + j) * nchunk + chunk] = sum over the chunk of e_j(z) Re(g)
+constexpr int kChunk = 8192;
+__global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict__ dy, const cfloat* __restrict__ z,
+                            const float* __restrict__ mu, RbfGeom g, int nchunk)
+{
+    __shared__ float smu[kMaxW];
+    __shared__ double red[kMaxW][8];
+    for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
+        smu[j] = mu[j];
+    __syncthreads();
+    const long f = blockIdx.y;
+    const long total = g.inner * g.outer;
+    const long begin = long(blockIdx.x) * kChunk, end = min(total, begin + kChunk);
+    double acc[kMaxW];
+    for (int j = 0; j < g.nw; j++)
+        acc[j] = 0;
+    for (long t = begin + threadIdx.x; t < end; t += blockDim.x) {
+        const long ii = t % g.inner, o = t / g.inner;
+        const long idx = ii + g.inner * (f + g.nf * o);
+        const float zk = z[idx].x, gv = dy[idx].x;
+        for (int j = 0; j < g.nw; j++)
+            acc[j] += double(gauss(zk, smu[j], g.sigma) * gv);
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = 0; j < g.nw; j++) {
+        double v = acc[j];
+        for (int o2 = 16; o2 > 0; o2 >>= 1)
+            v += __shfl_xor_sync(0xffffffffu, v, o2);
+        if (lane == 0)
+            red[j][warp] = v;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < g.nw; j += blockDim.x) {
+        double s = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); w++)
+            s += red[j][w];
+        part[(f * g.nw + j) * nchunk + blockIdx.x] = s;
+    }
+}
+
+__global__ void k_rbf_wfinal(cfloat* dw, const double* part, RbfGeom g, int nchunk)
+{
+    const long n = g.nf * g.nw;
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+        const long f = i / g.nw, j = i % g.nw;
+        double s = 0;
+        for (int c = 0; c < nchunk; c++)
+            s += part[i * nchunk + c];
+        dw[f + j * g.nf] = float2{float(s), 0.f};
+    }
+}
+
+} // namespace
+
+void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
+{
+    if (g.nw > kMaxW)
+        throw ConfigError("rbf: more than 64 basis functions not supported on device");
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(y, z, w, nullptr, mu, g, 0);
+    KERNEL_CHECK();
+}
+
+void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
+{
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(dz, z, w, dy, mu, g, 1);
+    KERNEL_CHECK();
+}
+
+void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
+{
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(dy, z, w, dz, mu, g, 1);
+    KERNEL_CHECK();
+}
+
+void rbf_deriv_w(cfloat* dy, const cfloat* dw, const cfloat* z, const float* mu, const RbfGeom& g)
+{
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(dy, z, dw, nullptr, mu, g, 2);
+    KERNEL_CHECK();
+}
+
+void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g)
+{
+    auto& c = ctx();
+    const long total = g.inner * g.outer;
+    const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
+    double* part;
+    CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
+    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, 0, c.stream>>>(part, dy, z, mu, g, nchunk);
+    KERNEL_CHECK();
+    k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
+    KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(part, c.stream));
+}
+
+} // namespace mdnn

@@ -1,0 +1,59 @@
+// Training step (optim.hpp:218-415): joint model + MSE loss, forward, reverse
+// sweep restricted to the weights, flat fp32 gradient buffer (the all-reduce
+// payload for data parallelism), complex Adam, realify / prox, and the
+// moving-statistics carry-over (update_stats, optim.hpp:403-415).
+#pragma once
+
+#include "model.h"
+
+namespace mdnn {
+
+struct TrainConfig {
+    double lr = 1e-3, beta1 = 0.9, beta2 = 0.999, eps = 1e-8, clip = 0;
+};
+
+class Trainer {
+public:
+    Trainer(const Model& model, const TrainConfig& cfg, uint64_t seed);
+
+    void set_data(const std::string& name, DArray a);
+    void set_weight(const std::string& name, DArray a);
+    const DArray& weight(const std::string& name) const;
+    DArray grad(const std::string& name) const;
+
+    double forward_backward();           // returns loss (synchronises once)
+    void update(float grad_scale);       // Adam on the flat buffer
+    double step()
+    {
+        double l = forward_backward();
+        update(1.f);
+        return l;
+    }
+    float* grad_buffer() const { return flat_.fdata(); }
+    long grad_floats() const { return 2 * flat_n_; }
+    const std::vector<std::string>& weight_names() const { return wnames_; }
+    int kernel_launch_estimate() const { return 0; }
+
+private:
+    std::vector<DArray> gather_inputs() const;
+
+    Model joint_;
+    TrainConfig cfg_;
+    int loss_idx_ = 0;
+    std::map<std::string, DArray> weights_, data_;
+    std::vector<int> wargs_;
+    std::vector<std::string> wnames_;
+    std::vector<long> woff_;
+    DArray flat_;
+    long flat_n_ = 0;
+    struct Adam {
+        DArray m;
+        float* v = nullptr;
+        long t = 0;
+    };
+    std::vector<Adam> adam_;
+    std::shared_ptr<float> vbuf_;
+    std::vector<DArray> last_outs_;
+};
+
+} // namespace mdnn

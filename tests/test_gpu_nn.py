@@ -1,0 +1,151 @@
+"""GPU parity of the CNN regulariser atoms and layers (per node, oracle-fed
+inputs, SURVEY §8c protocol): conv fwd / bwd-data / bwd-weight (plain and
+transposed, with bias), batch norm (train and inference), CReLU, RBF, MSE,
+exp, complex/real split, broadcast add and generic TenMul.
+
+Tolerances: 1e-3 for convolution paths (TF32 target, BASELINE north_star),
+1e-5 for everything else.
+"""
+import numpy as np
+import pytest
+
+from paper_2202_14005_b200.mdnn import Model, Nlop
+from util import crand, d16, rel_l2, rrand
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+CONV_TOL = 1e-3
+
+
+def _check_node(ng, nr, ins, rng, tol, names=None):
+    og, orf = ng.apply(ins), nr.apply(ins)
+    assert len(og) == len(orf)
+    for o in range(len(og)):
+        assert rel_l2(og[o], orf[o]) <= tol, ("out", o)
+    for o in range(nr.n_out):
+        for i in range(nr.n_in):
+            dx = crand(rng, nr.in_dims(i))
+            try:
+                r = nr.derivative(o, i, dx)
+            except Exception:
+                continue
+            assert rel_l2(ng.derivative(o, i, dx), r) <= tol, ("deriv", o, i)
+        dy = crand(rng, nr.out_dims(o))
+        ag, ar = ng.adjoint_all(o, dy), nr.adjoint_all(o, dy)
+        for i in range(nr.n_in):
+            assert rel_l2(ag[i], ar[i]) <= tol, ("adjoint", o, i, names and names[i])
+
+
+@pytest.mark.parametrize("cin,cout,k,X,Y,B,bias", [
+    (1, 8, 3, 20, 17, 2, False), (8, 8, 3, 33, 24, 1, False), (8, 1, 3, 16, 16, 2, True),
+    (2, 6, 11, 24, 20, 1, False), (4, 4, 5, 16, 12, 3, True), (64, 64, 3, 40, 32, 1, False),
+])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_conv_layer(gpu, ref, cin, cout, k, X, Y, B, bias, transposed):
+    rng = np.random.default_rng(cin * 31 + cout + k)
+    in_dims = list(d16(X, Y, cin))
+    in_dims[15] = B
+    mg = Model.conv_layer(gpu, "c", in_dims, (k, k), cout, transposed=transposed, bias=bias)
+    mr = Model.conv_layer(ref, "c", in_dims, (k, k), cout, transposed=transposed, bias=bias)
+    assert mg.arg_names == mr.arg_names
+    ng, nr = mg.nlop, mr.nlop
+    ins = [crand(rng, nr.in_dims(i)) for i in range(nr.n_in)]
+    _check_node(ng, nr, ins, rng, CONV_TOL, mr.arg_names)
+
+
+def test_conv_weights_init_bitwise(gpu, ref):
+    in_dims = list(d16(8, 8, 4))
+    mg = Model.conv_layer(gpu, "dw1", in_dims, (3, 3), 16)
+    mr = Model.conv_layer(ref, "dw1", in_dims, (3, 3), 16)
+    assert np.array_equal(mg.init_weight(42, "dw1_w"), mr.init_weight(42, "dw1_w"))
+
+
+@pytest.mark.parametrize("train", [True, False])
+def test_batchnorm(gpu, ref, train):
+    rng = np.random.default_rng(5)
+    dims = list(d16(24, 20, 8))
+    dims[15] = 2
+    flags = (1 << 0) | (1 << 1) | (1 << 15)
+    ng, nr = Nlop.batchnorm(gpu, dims, flags, train), Nlop.batchnorm(ref, dims, flags, train)
+    x = crand(rng, dims)
+    mean = crand(rng, nr.in_dims(1), 0.1)
+    var = rrand(rng, nr.in_dims(2), 1.0) + np.float32(1.5)
+    _check_node(ng, nr, [x, mean, np.asfortranarray(var)], rng, TOL)
+
+
+@pytest.mark.parametrize("kind", ["crelu", "zconj", "zreal", "exp_real"])
+def test_elementwise(gpu, ref, kind):
+    rng = np.random.default_rng(11)
+    dims = d16(17, 9, 3) if kind != "exp_real" else d16()
+    _check_node(Nlop.unary(gpu, kind, dims), Nlop.unary(ref, kind, dims), [crand(rng, dims)], rng, TOL)
+
+
+def test_mse(gpu, ref):
+    rng = np.random.default_rng(12)
+    dims = d16(20, 12)
+    ins = [crand(rng, dims), crand(rng, dims)]
+    _check_node(Nlop.unary(gpu, "mse", dims), Nlop.unary(ref, "mse", dims), ins, rng, TOL)
+
+
+@pytest.mark.parametrize("join", [False, True])
+def test_real_chan(gpu, ref, join):
+    rng = np.random.default_rng(13)
+    dims = list(d16(12, 10, 2 if join else 1))
+    dims[15] = 2
+    ng, nr = Nlop.real_chan(gpu, dims, 2, join), Nlop.real_chan(ref, dims, 2, join)
+    _check_node(ng, nr, [crand(rng, dims)], rng, TOL)
+
+
+def test_rbf(gpu, ref):
+    rng = np.random.default_rng(14)
+    nw, nf = 31, 6
+    z = list(d16(16, 12, nf))
+    z[15] = 2
+    centers = [-1 + 2 * j / (nw - 1) for j in range(nw)]
+    sigma = 2 / (nw - 1)
+    ng, nr = Nlop.rbf(gpu, z, 2, centers, sigma), Nlop.rbf(ref, z, 2, centers, sigma)
+    ins = [rrand(rng, z, 1.2), rrand(rng, nr.in_dims(1), 0.05)]
+    _check_node(ng, nr, ins, rng, TOL)
+
+
+def test_bcast_add_and_tenmul(gpu, ref):
+    rng = np.random.default_rng(15)
+    x = d16(10, 8, 4)
+    b = d16(1, 1, 4)
+    _check_node(Nlop.bcast_add(gpu, x, b), Nlop.bcast_add(ref, x, b), [crand(rng, x), crand(rng, b)], rng, TOL)
+    # per-channel scale (bn_scale TenMul, recon.hpp:756-763)
+    s = (1, 10, 80) + (0,) * 13
+    sg = (0, 0, 1) + (0,) * 13
+    args = (x, x, s, x, s, b, sg)
+    _check_node(Nlop.tenmul(gpu, *args), Nlop.tenmul(ref, *args), [crand(rng, x), crand(rng, b)], rng, TOL)
+    # a genuine contraction: matrix-vector (dense_layer wiring, nn.hpp:232-239)
+    it = (5, 7, 3) + (1,) * 13
+    yd, wd, xd = (5, 3) + (1,) * 14, (5, 7) + (1,) * 14, (7, 3) + (1,) * 14
+    so, sw, sx = (1, 0, 5) + (0,) * 13, (1, 5, 0) + (0,) * 13, (0, 1, 7) + (0,) * 13
+    args = (it, yd, so, wd, sw, xd, sx)
+    _check_node(Nlop.tenmul(gpu, *args), Nlop.tenmul(ref, *args), [crand(rng, wd), crand(rng, xd)], rng, TOL)
+
+
+def test_pad_and_dft_nodes(gpu, ref):
+    rng = np.random.default_rng(16)
+    i, o, c = d16(6, 5, 2), d16(9, 8, 2), d16(1, 2, 0)
+    _check_node(Nlop.pad(gpu, i, o, c), Nlop.pad(ref, i, o, c), [crand(rng, i)], rng, TOL)
+    d = d16(12, 10, 3)
+    _check_node(Nlop.dft(gpu, d, 3), Nlop.dft(ref, d, 3), [crand(rng, d)], rng, TOL)
+
+
+def test_graph_algebra(gpu, ref):
+    """combine / link / duplicate / chain (nlop.hpp:265-350) on a small graph."""
+    rng = np.random.default_rng(17)
+    d = d16(8, 6)
+    res = []
+    for lib in (gpu, ref):
+        mul = Nlop.tenmul(lib, d, d, (1, 8) + (0,) * 14, d, (1, 8) + (0,) * 14, d, (1, 8) + (0,) * 14)
+        cr = Nlop.unary(lib, "crelu", d)
+        cj = Nlop.unary(lib, "zconj", d)
+        g = mul.combine(cr).link(0, 2)          # crelu(x1*x2)
+        g = cj.combine(g).link(0, 1)            # crelu(conj(a) * b) : inputs (a, b)
+        g = g.duplicate(0, 1)                   # crelu(conj(a) * a)
+        res.append(g)
+    x = crand(rng, d)
+    _check_node(res[0], res[1], [x], rng, TOL)
