@@ -68,6 +68,17 @@ const char* mdnn_backend(void);            /* "b200-sm100a" or "reference-cpu" *
 int mdnn_set_device(int device);           /* GPU build: selects device + stream */
 int mdnn_synchronize(void);
 int mdnn_set_option(const char* key, long value); /* e.g. "conv_tf32", "fused_sense" */
+/* the library's CUDA stream on the current device (cudaStream_t), so callers
+   can order collectives / events with its kernels; NULL in the CPU shim */
+void* mdnn_stream(void);
+/* live per-kernel timing (CUDA events on the library stream) for tagged
+   launch sites, e.g. "sense_normal_y", "conv_fwd"; used by bench.py */
+int mdnn_profile_enable(int on);
+/* total_work: summed algorithmic bytes (SENSE/CG tags) or flops (conv tags) */
+int mdnn_profile_read(const char* tag, long* launches, double* total_ms, double* total_work);
+int mdnn_profile_reset(void);
+/* number of device kernels this library has launched (all devices) */
+long mdnn_launch_count(void);
 
 /* ---- Nlop (nlop.hpp:89-437) --------------------------------------------- */
 void mdnn_nlop_free(mdnn_nlop* h);

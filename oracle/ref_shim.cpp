@@ -402,6 +402,18 @@ const char* mdnn_backend(void) { return sizeof(R) == 8 ? "reference-cpu-f64" : "
 int mdnn_set_device(int) { return MDNN_OK; }
 int mdnn_synchronize(void) { return MDNN_OK; }
 int mdnn_set_option(const char*, long) { return MDNN_OK; }
+void* mdnn_stream(void) { return nullptr; }
+int mdnn_profile_enable(int) { return MDNN_OK; }
+int mdnn_profile_read(const char*, long* n, double* ms, double* work)
+{
+    *n = 0;
+    *ms = 0;
+    if (work)
+        *work = 0;
+    return MDNN_OK;
+}
+long mdnn_launch_count(void) { return 0; }
+int mdnn_profile_reset(void) { return MDNN_OK; }
 
 void mdnn_nlop_free(mdnn_nlop* h) { delete h; }
 mdnn_nlop* mdnn_nlop_ref(mdnn_nlop* h) { return new mdnn_nlop{h->op}; }

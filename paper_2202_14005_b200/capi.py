@@ -72,6 +72,12 @@ _SIGS = {
     "mdnn_set_device": (C.c_int, [C.c_int]),
     "mdnn_synchronize": (C.c_int, []),
     "mdnn_set_option": (C.c_int, [C.c_char_p, C.c_long]),
+    "mdnn_stream": (C.c_void_p, []),
+    "mdnn_profile_enable": (C.c_int, [C.c_int]),
+    "mdnn_profile_read": (C.c_int, [C.c_char_p, C.POINTER(C.c_long), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]),
+    "mdnn_profile_reset": (C.c_int, []),
+    "mdnn_launch_count": (C.c_long, []),
     "mdnn_nlop_free": (None, [P]),
     "mdnn_nlop_ref": (P, [P]),
     "mdnn_nlop_n_in": (C.c_int, [P]),

@@ -4,6 +4,7 @@
 #include "../../include/mdnn.h"
 
 #include "kernels.h"
+#include "profile.h"
 #include "train.h"
 
 #include <cstring>
@@ -156,6 +157,30 @@ int mdnn_set_option(const char* key, long value)
         (void)key;
         (void)value;
     });
+}
+
+void* mdnn_stream(void)
+{
+    void* s = nullptr;
+    guard([&] { s = static_cast<void*>(ctx().stream); });
+    return s;
+}
+
+int mdnn_profile_enable(int on)
+{
+    return guard([&] { prof_enable(on != 0); });
+}
+
+int mdnn_profile_read(const char* tag, long* launches, double* total_ms, double* total_work)
+{
+    return guard([&] { prof_read(tag, launches, total_ms, total_work); });
+}
+
+long mdnn_launch_count(void) { return launch_count(); }
+
+int mdnn_profile_reset(void)
+{
+    return guard([] { prof_reset(); });
 }
 
 void mdnn_nlop_free(mdnn_nlop* h) { delete h; }
@@ -392,7 +417,7 @@ int mdnn_cg_normal_solve(const mdnn_array* coils, const mdnn_array* pattern, flo
             throw ShapeError("cg: rhs dims mismatch");
         DArray lam = DArray::scalar(lambda);
         DArray out(img_dims(g), false);
-        DArray st(Dims{2}, true);
+        DArray st(Dims{3}, true); // 3 doubles
         cg_normal_device(out.data(), B.data(), C.data(), P.data(), lam.data(), g, max_iter, tol,
                          reinterpret_cast<double*>(st.data()));
         auto res = read_cg_status(reinterpret_cast<double*>(st.data()));

@@ -10,6 +10,7 @@
 // are dispatched to the tcgen05 implicit-GEMM path in conv_tc.cu when it is
 // enabled.  Reductions are fixed-order (no atomics): bitwise run-to-run stable.
 #include "kernels.h"
+#include "profile.h"
 
 #include <algorithm>
 
@@ -94,10 +95,11 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(cfloat* __restrict__ out
 
 // bwd-weight: block = (c-group x f-group, split); loops over its share of
 // pixel tiles; thread owns combos (t, c, f) accumulated in registers.
-constexpr int WG_C = 4, WG_F = 8;         // channels per block
 constexpr int WTX = 32, WTY = 8;          // pixel tile
 constexpr int WMAXC = 4;                  // combos per thread
 
+// WG_C x WG_F channel pairs per block; (4, 8) for 3x3-5x5 kernels, (1, 8) up to 11x11
+template<int WG_C, int WG_F>
 __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, const cfloat* __restrict__ x,
                                                     const cfloat* __restrict__ dy, ConvGeom g, int nsplit)
 {
@@ -178,6 +180,12 @@ __global__ void k_sum_splits(cfloat* out, const float2* part, long n, int nsplit
     }
 }
 
+// algorithmic flops of one pass: 8 per complex MAC
+double conv_flops(const ConvGeom& g)
+{
+    return 8.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * g.KX * g.KY;
+}
+
 void check_geom(const ConvGeom& g)
 {
     if (g.KX > MAXK || g.KY > MAXK)
@@ -191,6 +199,7 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
     check_geom(g);
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cout + FG - 1) / FG)));
+    ProfScope prof("conv_fwd", conv_flops(g));
     k_conv_direct<0><<<grid, TX * TY, 0, ctx().stream>>>(y, x, w, g);
     KERNEL_CHECK();
 }
@@ -200,6 +209,7 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
     check_geom(g);
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cin + FG - 1) / FG)));
+    ProfScope prof("conv_bwd_data", conv_flops(g));
     k_conv_direct<1><<<grid, TX * TY, 0, ctx().stream>>>(dx, dy, w, g);
     KERNEL_CHECK();
 }
@@ -208,6 +218,8 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
 {
     check_geom(g);
     const long KK = g.KX * g.KY;
+    const bool small_k = KK * 4 * 8 <= 256 * WMAXC;
+    const int WG_C = small_k ? 4 : 1, WG_F = 8;
     if (KK * WG_C * WG_F > 256 * WMAXC)
         throw ConfigError("conv: kernel too large for the weight-gradient kernel");
     const long ngroups = ((g.Cin + WG_C - 1) / WG_C) * ((g.Cout + WG_F - 1) / WG_F);
@@ -219,7 +231,11 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     float2* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
     dim3 grid{unsigned(ngroups), unsigned(nsplit)};
-    k_conv_wgrad<<<grid, 256, 0, c.stream>>>(part, x, dy, g, nsplit);
+    ProfScope prof("conv_bwd_weight", conv_flops(g));
+    if (small_k)
+        k_conv_wgrad<4, 8><<<grid, 256, 0, c.stream>>>(part, x, dy, g, nsplit);
+    else
+        k_conv_wgrad<1, 8><<<grid, 256, 0, c.stream>>>(part, x, dy, g, nsplit);
     KERNEL_CHECK();
     k_sum_splits<<<int(std::min(1024L, (n + 255) / 256)), 256, 0, c.stream>>>(dw, part, n, nsplit);
     KERNEL_CHECK();

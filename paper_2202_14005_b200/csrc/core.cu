@@ -1,6 +1,7 @@
 #include "core.h"
 #include "kernels.h"
 
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -13,6 +14,10 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line)
         throw CudaError(std::string("CUDA error '") + cudaGetErrorString(e) + "' in " + what + " (" + file + ":"
                         + std::to_string(line) + ")");
 }
+
+static std::atomic<long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long launch_count() { return g_launches.load(); }
 
 long md_size(const Dims& d)
 {
@@ -101,6 +106,22 @@ Context& ctx()
     else
         cudaSetDevice(t_device);
     return *it->second;
+}
+
+void allow_max_dyn_smem(const void* func)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, bool> done;
+    auto& c = ctx();
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(c.device, func);
+    if (done.count(key))
+        return;
+    cudaFuncAttributes fa;
+    CUDA_CHECK(cudaFuncGetAttributes(&fa, func));
+    int dyn = int(c.smem_optin) - int(fa.sharedSizeBytes);
+    CUDA_CHECK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    done[key] = true;
 }
 
 void set_device(int dev)

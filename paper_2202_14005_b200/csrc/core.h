@@ -44,8 +44,14 @@ MDNN_ERR(CudaError, 9)
 #undef MDNN_ERR
 
 void cuda_check(cudaError_t e, const char* what, const char* file, int line);
+void count_launch(); // every kernel launch site reports here (bench gpu_launches)
+long launch_count();
 #define CUDA_CHECK(x) ::mdnn::cuda_check((x), #x, __FILE__, __LINE__)
-#define KERNEL_CHECK() ::mdnn::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+#define KERNEL_CHECK()                                                                \
+    do {                                                                              \
+        ::mdnn::count_launch();                                                       \
+        ::mdnn::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);  \
+    } while (0)
 
 using Dims = std::vector<long>;
 long md_size(const Dims& d);
@@ -72,6 +78,9 @@ struct Context {
     std::string err_detail;
 };
 Context& ctx();             // context of the current device (creates on first use)
+// opt a kernel into the largest dynamic shared memory the device allows
+// (opt-in limit minus the kernel's static shared memory); once per device
+void allow_max_dyn_smem(const void* func);
 void set_device(int dev);
 void sync_and_check();      // cudaStreamSynchronize + device error flags
 enum ErrFlag : unsigned { ERRF_CG_BREAKDOWN = 1u, ERRF_CG_NONFINITE = 2u, ERRF_NONFINITE_GRAD = 4u };

@@ -9,6 +9,7 @@
 // scaled by 1/sqrt(n) on the way out: one HBM read + one write per element.
 #include "fft.cuh"
 #include "kernels.h"
+#include "profile.h"
 
 #include <cmath>
 #include <map>
@@ -208,13 +209,10 @@ void launch_fft_dim(cfloat* out, const cfloat* in, const Dims& dims, int dim, bo
     auto& c = ctx();
     if (smem > c.smem_optin)
         throw ConfigError("dft: line length " + std::to_string(n) + " exceeds shared memory");
-    static bool attr_set[64] = {};
-    if (!attr_set[c.device]) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_fft_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c.smem_optin)));
-        attr_set[c.device] = true;
-    }
+    allow_max_dyn_smem(reinterpret_cast<const void*>(k_fft_lines));
     long blocks = mode == 0 ? ((sd + W - 1) / W) * outer : (outer + W - 1) / W;
     float scale = float(1.0 / std::sqrt(double(n)));
+    ProfScope prof("fft", 16.0 * double(n) * double(sd) * double(outer));
     k_fft_lines<<<unsigned(blocks), 256, smem, c.stream>>>(out, in, plan, sd, outer, W, LD, mode, inverse, scale);
     KERNEL_CHECK();
 }

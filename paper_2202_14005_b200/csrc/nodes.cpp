@@ -889,12 +889,16 @@ public:
             launch_scale_dev(o.data(), x.data(), dx.data(), false, o.size());
             return o;
         }
-        if (i == 1) // sum conj(C2) F^H P F (dC1 x)
-            return coil_ifft_adj(sd_, pat_mul(sd_, coil_fft(sd_, x, dx), P), C2);
         if (i == 2) // sum conj(C2) F^H (dP F(C1 x))
             return coil_ifft_adj(sd_, pat_mul(sd_, coil_fft(sd_, x, C1), dx), C2);
-        // i == 3, coil-combine maps: sum conj(dC2) F^H P F(C1 x)
-        return coil_ifft_adj(sd_, pat_mul(sd_, coil_fft(sd_, x, C1), P), dx);
+        // coil-multiply maps: sum conj(C2) F^H P F (dC1 x)
+        auto d1 = [&] { return coil_ifft_adj(sd_, pat_mul(sd_, coil_fft(sd_, x, dx), P), C2); };
+        // coil-combine maps: sum conj(dC2) F^H P F(C1 x)
+        auto d2 = [&] { return coil_ifft_adj(sd_, pat_mul(sd_, coil_fft(sd_, x, C1), P), dx); };
+        if (!lam_)
+            return i == 1 ? d1() : d2();
+        // lambda variant: the single (deduped) coils input feeds both
+        return accumulate(d1(), d2());
     }
     DArray adjoint(int, int i, const DArray& g) override
     {
@@ -919,21 +923,25 @@ public:
             launch_iso_reduce(o.data(), g.data(), x.data(), md_size(sd_.image()), 1, 1, 1, 1.f);
             return o;
         }
-        DArray Pc = conj_of(P);
-        if (i == 1) { // w conj(x), w = F^H conj(P) F (C2 g)
-            DArray w(sd_.coil_img(), false);
-            DArray k = pat_mul(sd_, coil_fft(sd_, g, C2), Pc);
-            fft_flags(w.data(), k.data(), k.dims, 3UL, true);
-            return coil_bcast(sd_, w, x, 2, false);
-        }
         if (i == 2) // sum F(C2 g) conj(F(C1 x))
             return pattern_reduce(sd_, coil_fft(sd_, g, C2), coil_fft(sd_, x, C1));
-        // i == 3: conj(g) v, v = F^H P F (C1 x)  ->  conj(v) * g, conjugated
-        DArray v(sd_.coil_img(), false);
-        DArray k = pat_mul(sd_, coil_fft(sd_, x, C1), P);
-        fft_flags(v.data(), k.data(), k.dims, 3UL, true);
-        DArray t = coil_bcast(sd_, v, g, 2, true); // conj(v) * conj(g)
-        return conj_of(t);
+        // coil-multiply maps: w conj(x), w = F^H conj(P) F (C2 g)
+        auto a1 = [&] {
+            DArray w(sd_.coil_img(), false);
+            DArray k = pat_mul(sd_, coil_fft(sd_, g, C2), conj_of(P));
+            fft_flags(w.data(), k.data(), k.dims, 3UL, true);
+            return coil_bcast(sd_, w, x, 2, false);
+        };
+        // coil-combine maps: conj(g) v, v = F^H P F (C1 x)  (= conj(conj(v) g))
+        auto a2 = [&] {
+            DArray v(sd_.coil_img(), false);
+            DArray k = pat_mul(sd_, coil_fft(sd_, x, C1), P);
+            fft_flags(v.data(), k.data(), k.dims, 3UL, true);
+            return conj_of(coil_bcast(sd_, v, g, 1, true));
+        };
+        if (!lam_)
+            return i == 1 ? a1() : a2();
+        return accumulate(a1(), a2());
     }
 
     DArray apply_S(const DArray& x, const DArray& C1, const DArray& P, const DArray& C2, const DArray& l) const
@@ -989,7 +997,7 @@ public:
         DArray v(sd_.coil_img(), false);
         DArray k = pat_mul(sd_, y, P);
         fft_flags(v.data(), k.data(), k.dims, 3UL, true);
-        return conj_of(coil_bcast(sd_, v, g, 2, true));
+        return conj_of(coil_bcast(sd_, v, g, 1, true)); // conj(conj(v) g) = conj(g) v
     }
 
 private:
@@ -1151,7 +1159,7 @@ private:
     DArray solve(const DArray& b, bool record)
     {
         if (!status_.valid())
-            status_ = DArray(Dims{2}, true); // 3 doubles fit in 2 complex floats
+            status_ = DArray(Dims{3}, true); // [iterations, rel_residual, converged] as doubles
         DArray x(b.dims, false);
         double* st = record ? reinterpret_cast<double*>(status_.data()) : nullptr;
         if (fused_) {

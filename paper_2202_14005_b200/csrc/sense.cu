@@ -16,6 +16,7 @@
 // p = r + beta p into the load and emits per-CTA partials of <p, Ap>.
 #include "fft.cuh"
 #include "kernels.h"
+#include "profile.h"
 
 #include <algorithm>
 #include <climits>
@@ -376,12 +377,13 @@ void launch_normal_y(NormalArgs a, const SenseGeom& g)
     a.W = pick_w(g.Y, int(g.M));
     size_t smem = size_t(2 * g.M + 2) * g.Y * a.W * sizeof(float2);
     auto& c = ctx();
-    static bool attr[64] = {};
-    if (!attr[c.device]) {
-        CUDA_CHECK(cudaFuncSetAttribute(k_normal_y, cudaFuncAttributeMaxDynamicSharedMemorySize, int(c.smem_optin)));
-        attr[c.device] = true;
-    }
+    allow_max_dyn_smem(reinterpret_cast<const void*>(k_normal_y));
     long nxb = (g.X + a.W - 1) / a.W;
+    // algorithmic bytes: A^H A + lam reads x + coils and writes the
+    // image; the CG launch also reads r and rewrites p (8 XYB (CM + 4M))
+    const double xyb = double(g.X) * g.Y * g.B;
+    const double work = 8.0 * xyb * (g.C * g.M + (a.mode == 1 ? 4 : 2) * g.M);
+    ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
     k_normal_y<<<unsigned(nxb * g.B), kT, smem, c.stream>>>(a, plan);
     KERNEL_CHECK();
 }

@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
 
 
 def _inputs(ref, model, X, Y, NC, B, seed=42, rbf_perturb=False):
-    ph, cm, pat = sim_data(ref, X, Y, NC, B)
+    # 3-fold regular + 2 ACL lines: genuinely undersampled at these toy sizes
+    ph, cm, pat = sim_data(ref, X, Y, NC, B, accel=3, acl=2)
     import ctypes as C
     ks = np.zeros(kspace_dims(X, Y, NC, B), dtype=np.complex64, order="F")
     ref.check(ref.so.mdnn_sense_forward(C.byref(ref.arr(cm)), C.byref(ref.arr(pat)), C.byref(ref.arr(ph)),

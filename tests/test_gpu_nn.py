@@ -128,7 +128,7 @@ def test_bcast_add_and_tenmul(gpu, ref):
 
 def test_pad_and_dft_nodes(gpu, ref):
     rng = np.random.default_rng(16)
-    i, o, c = d16(6, 5, 2), d16(9, 8, 2), d16(1, 2, 0)
+    i, o, c = d16(6, 5, 2), d16(9, 8, 2), (1, 2) + (0,) * 14
     _check_node(Nlop.pad(gpu, i, o, c), Nlop.pad(ref, i, o, c), [crand(rng, i)], rng, TOL)
     d = d16(12, 10, 3)
     _check_node(Nlop.dft(gpu, d, 3), Nlop.dft(ref, d, 3), [crand(rng, d)], rng, TOL)
