@@ -154,8 +154,11 @@ int mdnn_synchronize(void)
 int mdnn_set_option(const char* key, long value)
 {
     return guard([&] {
-        (void)key;
-        (void)value;
+        std::string k = key ? key : "";
+        if (k == "conv_tc")
+            conv_tc_enable(value != 0);
+        else
+            throw ConfigError("unknown option '" + k + "'");
     });
 }
 

@@ -197,6 +197,10 @@ void check_geom(const ConvGeom& g)
 void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
 {
     check_geom(g);
+    if (conv_tc_supported(g.Cin, g.Cout, g.KX, g.KY)) {
+        conv_tc_run(y, x, w, g, 0);
+        return;
+    }
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cout + FG - 1) / FG)));
     ProfScope prof("conv_fwd", conv_flops(g));
@@ -207,6 +211,10 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
 void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom& g)
 {
     check_geom(g);
+    if (conv_tc_supported(g.Cin, g.Cout, g.KX, g.KY)) {
+        conv_tc_run(dx, dy, w, g, 1);
+        return;
+    }
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cin + FG - 1) / FG)));
     ProfScope prof("conv_bwd_data", conv_flops(g));

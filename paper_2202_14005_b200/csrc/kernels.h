@@ -116,6 +116,10 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g);
 void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom& g);
 // dw[t,c,f] = sum_p dy[p,f] conj(x[p+t-c0, c])
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
+// tcgen05 TF32 implicit-GEMM path (conv_tc.cu) for 3x3 layers with 32/64 channels
+void conv_tc_enable(bool on);
+bool conv_tc_supported(long cin, long cout, long kx, long ky);
+void conv_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode);
 
 // ---- batch norm (bn.cu) ----------------------------------------------------------
 struct IsoGeom {

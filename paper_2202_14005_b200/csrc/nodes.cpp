@@ -173,8 +173,15 @@ public:
           s2_(std::move(s2))
     {
         const Dims& o = outs_[0];
-        if (iter_ == o && ins_[0] == o && so_ == default_strides(o) && s1_ == default_strides(o)
-            && s2_ == stride_for(ins_[1], iter_)) {
+        // strides on extent-1 iteration dims never move the pointer: ignore them
+        auto same = [&](const Dims& a, const Dims& b) {
+            for (size_t d = 0; d < iter_.size(); d++)
+                if (iter_[d] > 1 && a[d] != b[d])
+                    return false;
+            return true;
+        };
+        if (iter_ == o && ins_[0] == o && same(so_, default_strides(o)) && same(s1_, default_strides(o))
+            && same(s2_, stride_for(ins_[1], iter_))) {
             iso_ = iso_of(o, ins_[1]);
         }
     }

@@ -39,6 +39,9 @@ def _check_node(ng, nr, ins, rng, tol, names=None):
 @pytest.mark.parametrize("cin,cout,k,X,Y,B,bias", [
     (1, 8, 3, 20, 17, 2, False), (8, 8, 3, 33, 24, 1, False), (8, 1, 3, 16, 16, 2, True),
     (2, 6, 11, 24, 20, 1, False), (4, 4, 5, 16, 12, 3, True), (64, 64, 3, 40, 32, 1, False),
+    # tcgen05 TF32 path: full and partial 32x16 super-tiles, 32- and 64-channel variants
+    (64, 64, 3, 64, 48, 2, False), (32, 32, 3, 36, 20, 1, False), (32, 64, 3, 33, 17, 1, False),
+    (64, 32, 3, 32, 16, 2, True),
 ])
 @pytest.mark.parametrize("transposed", [False, True])
 def test_conv_layer(gpu, ref, cin, cout, k, X, Y, B, bias, transposed):
@@ -51,6 +54,28 @@ def test_conv_layer(gpu, ref, cin, cout, k, X, Y, B, bias, transposed):
     ng, nr = mg.nlop, mr.nlop
     ins = [crand(rng, nr.in_dims(i)) for i in range(nr.n_in)]
     _check_node(ng, nr, ins, rng, CONV_TOL, mr.arg_names)
+
+
+def test_conv_tensor_core_vs_cuda_core(gpu):
+    """The tcgen05 TF32 path agrees with the fp32 CUDA-core path within the
+    TF32 budget (per pass: RN operands ~3e-4)."""
+    import ctypes as C
+    rng = np.random.default_rng(21)
+    in_dims = list(d16(96, 64, 64))
+    in_dims[15] = 2
+    m = Model.conv_layer(gpu, "c", in_dims, (3, 3), 64)
+    n = m.nlop
+    x, w = crand(rng, n.in_dims(0)), crand(rng, n.in_dims(1), 0.05)
+    dy = crand(rng, n.out_dims(0))
+    res = []
+    for tc in (1, 0):
+        gpu.check(gpu.so.mdnn_set_option(b"conv_tc", tc))
+        y = n.apply([x, w])[0]
+        dx = n.adjoint_all(0, dy)
+        res.append((y, dx[0], dx[1]))
+    gpu.check(gpu.so.mdnn_set_option(b"conv_tc", 1))
+    for a, b in zip(res[0], res[1]):
+        assert rel_l2(a, b) <= 1e-3
 
 
 def test_conv_weights_init_bitwise(gpu, ref):
