@@ -225,6 +225,10 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g)
 {
     check_geom(g);
+    if (conv_tc_wgrad_supported(g.Cin, g.Cout, g.KX, g.KY)) {
+        conv_tc_wgrad(dw, x, dy, g);
+        return;
+    }
     const long KK = g.KX * g.KY;
     const bool small_k = KK * 4 * 8 <= 256 * WMAXC;
     const int WG_C = small_k ? 4 : 1, WG_F = 8;

@@ -200,6 +200,154 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Backward-weight: per tap t, D_t[m = x channel (re|im)][n = dy channel (re|im)]
+//   = sum_p x[p + t - c0][m] * dy[p][n]
+// as a K = pixels GEMM with both operands MN-major straight from CHLAST rows.
+// A CTA owns one kernel row ky (3 accumulators, kx = 0..2, 3 x N TMEM
+// columns) and a contiguous range of 64-pixel dy row segments; per segment
+// it TMA-loads the dy segment and the 66-pixel x halo row once and feeds the
+// 3 taps from row-shifted views.  Partials per CTA are reduced in a fixed
+// order (deterministic) and folded into complex dW:
+//   Re dW = D[cr][fr] + D[ci][fi],  Im dW = D[cr][fi] - D[ci][fr].
+constexpr int WG_SEG = 64;                    // dy pixels per segment (8 K-steps)
+constexpr int WG_XROWS = 72;                  // x halo rows per channel block (66 used, 1024-B aligned)
+constexpr int WG_XBLK = WG_XROWS * 128;       // 9216 B
+constexpr int WG_DBLK = WG_SEG * 128;         // 8192 B
+constexpr int WG_STAGES = 3;
+
+template<int N>
+struct WgSmem {
+    static constexpr int STAGE = 4 * WG_XBLK + (N / 32) * WG_DBLK;
+    static constexpr int BAR_OFF = WG_STAGES * STAGE;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template<int N>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_conv_tc_wgrad(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
+                    float* __restrict__ part, int X, int Y, int B, int nsplit)
+{
+    using S = WgSmem<N>;
+    constexpr int TMEM_COLS = 3 * N <= 128 ? 128 : (3 * N <= 256 ? 256 : 512);
+    constexpr int NDB = N / 32;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + WG_STAGES;
+    uint64_t* tmem_full = bars + 2 * WG_STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int ky = blockIdx.x % 3, split = blockIdx.x / 3;
+    const int segx = (X + WG_SEG - 1) / WG_SEG;
+    const long nseg = long(segx) * Y * B;
+    const long s_begin = nseg * split / nsplit, s_end = nseg * (split + 1) / nsplit;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_x);
+        prefetch_tmap(&tm_dy);
+        for (int i = 0; i < WG_STAGES; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tmem_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1)
+        tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (long s = s_begin; s < s_end; s++, it++) {
+                const int sx = int(s % segx), y = int((s / segx) % Y), b = int(s / (long(segx) * Y));
+                const int x0 = sx * WG_SEG;
+                const uint32_t st = it % WG_STAGES, ph = (it / WG_STAGES) & 1;
+                mbar_wait(&empty[st], ph ^ 1);
+                mbar_arrive_expect_tx(&full[st], 4 * (WG_SEG + 2) * 128 + NDB * WG_SEG * 128);
+                uint8_t* base = smem + st * S::STAGE;
+                for (int j = 0; j < 4; j++)
+                    tma_load_4d(base + j * WG_XBLK, &tm_x, &full[st], j * 32, x0 - 1, y + ky - 1, b);
+                for (int j = 0; j < NDB; j++)
+                    tma_load_4d(base + 4 * WG_XBLK + j * WG_DBLK, &tm_dy, &full[st], j * 32, x0, y, b);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // a_major = b_major = MN (bits 15, 16)
+            constexpr uint32_t idesc = idesc_tf32(128, N) | (1u << 15) | (1u << 16);
+            uint32_t it = 0;
+            const uint32_t sbase = smem_u32(smem);
+            for (long s = s_begin; s < s_end; s++, it++) {
+                const uint32_t st = it % WG_STAGES, ph = (it / WG_STAGES) & 1;
+                mbar_wait(&full[st], ph);
+                tc_fence_after();
+                const uint32_t xb = sbase + st * S::STAGE, db = xb + 4 * WG_XBLK;
+#pragma unroll
+                for (int ks = 0; ks < WG_SEG / 8; ks++) {
+                    const uint64_t bd = umma_desc_sw128(db + ks * 8 * 128, 1024, WG_DBLK);
+#pragma unroll
+                    for (int kx = 0; kx < 3; kx++) {
+                        const uint64_t ad = umma_desc_sw128(xb + (kx + ks * 8) * 128, 1024, WG_XBLK);
+                        mma_tf32(tmem_base + kx * N, ad, bd, idesc, (s != s_begin || ks != 0) ? 1u : 0u);
+                    }
+                }
+                mma_commit(&empty[st]);
+            }
+            mma_commit(tmem_full);
+        }
+    } else {
+        const int lg = warp & 3;
+        const int m = lg * 32 + lane; // x channel (re|im)
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const bool any = s_end > s_begin;
+        for (int kx = 0; kx < 3; kx++) {
+            float* dst = part + ((size_t(split) * 9 + ky * 3 + kx) * 128 + m) * N;
+#pragma unroll 1
+            for (int nc = 0; nc < N / 32; nc++) {
+                float v[32];
+                tmem_ld32(tmem_base + (uint32_t(lg * 32) << 16) + kx * N + nc * 32, v);
+                tmem_ld_wait();
+                float4* d4 = reinterpret_cast<float4*>(dst + nc * 32);
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    d4[q] = any ? make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3])
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+// dw[t, c, f] from the per-split real blocks (fixed split order, fp64 sums)
+__global__ void k_wgrad_fold(cfloat* __restrict__ dw, const float* __restrict__ part, int Cin, int Cout, int N,
+                             int nsplit)
+{
+    const int n_out = 9 * Cin * Cout;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_out; i += gridDim.x * blockDim.x) {
+        const int t = i % 9, c = (i / 9) % Cin, f = i / (9 * Cin);
+        double re = 0, im = 0;
+        for (int s = 0; s < nsplit; s++) {
+            const float* D = part + (size_t(s) * 9 + t) * 128 * N;
+            re += double(D[c * N + f]) + double(D[(Cin + c) * N + Cout + f]);
+            im += double(D[c * N + Cout + f]) - double(D[(Cin + c) * N + f]);
+        }
+        dw[t + 9 * (c + Cin * f)] = float2{float(re), float(im)};
+    }
+}
+
 // packed real-block weights Bt[n][k], k = t*CIN2 + (in re | in im), n = (out re | out im);
 // mode 0 (fwd): u = w[t, c=in, f=out]; mode 1 (bwd-data): u = conj(w[flip t, c=out, f=in])
 __global__ void k_pack_weights(float* __restrict__ bt, const cfloat* __restrict__ w, int KX, int KY, int Cin,
@@ -264,12 +412,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
     return fn;
 }
 
-CUtensorMap make_act_map(const float* base, int C2, int X, int Y, int B)
+CUtensorMap make_act_map(const float* base, int C2, int X, int Y, int B, int box_x = HALO_P, int box_y = HALO_L)
 {
     CUtensorMap m;
     cuuint64_t dims[4] = {cuuint64_t(C2), cuuint64_t(X), cuuint64_t(Y), cuuint64_t(B)};
     cuuint64_t strides[3] = {cuuint64_t(C2) * 4, cuuint64_t(C2) * 4 * X, cuuint64_t(C2) * 4 * X * Y};
-    cuuint32_t box[4] = {32, HALO_P, HALO_L, 1};
+    cuuint32_t box[4] = {32, cuuint32_t(box_x), cuuint32_t(box_y), 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -317,9 +465,70 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
     KERNEL_CHECK();
 }
 
+template<int N>
+void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, int B, int Cin, int Cout)
+{
+    auto& c = ctx();
+    CUtensorMap tx = make_act_map(x, 128, X, Y, B, WG_SEG + 2, 1);
+    CUtensorMap td = make_act_map(dy, N, X, Y, B, WG_SEG, 1);
+    auto kern = k_conv_tc_wgrad<N>;
+    const int smem = WgSmem<N>::TOTAL;
+    static std::mutex mu;
+    static std::map<int, bool> done;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done[c.device]) {
+            CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            done[c.device] = true;
+        }
+    }
+    const long nseg = long((X + WG_SEG - 1) / WG_SEG) * Y * B;
+    const int nsplit = int(std::max(1L, std::min<long>(c.sm_count / 3, nseg)));
+    float* part;
+    CUDA_CHECK(cudaMallocAsync(&part, sizeof(float) * size_t(nsplit) * 9 * 128 * N, c.stream));
+    kern<<<3 * nsplit, NTHREADS, smem, c.stream>>>(tx, td, part, X, Y, B, nsplit);
+    KERNEL_CHECK();
+    k_wgrad_fold<<<int(std::min(1024, (9 * Cin * Cout + 255) / 256)), 256, 0, c.stream>>>(dw, part, Cin, Cout, N,
+                                                                                         nsplit);
+    KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(part, c.stream));
+}
+
 bool g_tc_enabled = true;
 
 } // namespace
+
+bool conv_tc_wgrad_supported(long cin, long cout, long kx, long ky)
+{
+    return g_tc_enabled && kx == 3 && ky == 3 && cin == 64 && (cout == 32 || cout == 64);
+}
+
+// dw = conv_bwd_weight(x, dy) on the tensor cores (x: Cin channels, dy: Cout channels)
+void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g)
+{
+    auto& c = ctx();
+    const long inner = g.X * g.Y;
+    float *xs, *ds;
+    CUDA_CHECK(cudaMallocAsync(&xs, sizeof(float) * 2 * g.Cin * inner * g.B, c.stream));
+    CUDA_CHECK(cudaMallocAsync(&ds, sizeof(float) * 2 * g.Cout * inner * g.B, c.stream));
+    dim3 cb(32, 8);
+    k_to_chlast_tf32<<<dim3(unsigned((inner + 31) / 32), unsigned((g.Cin + 31) / 32), unsigned(g.B)), cb, 0,
+                       c.stream>>>(xs, x, inner, g.Cin, g.B);
+    KERNEL_CHECK();
+    k_to_chlast_tf32<<<dim3(unsigned((inner + 31) / 32), unsigned((g.Cout + 31) / 32), unsigned(g.B)), cb, 0,
+                       c.stream>>>(ds, dy, inner, g.Cout, g.B);
+    KERNEL_CHECK();
+    {
+        const double flops = 8.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * 9;
+        ProfScope prof("conv_tc_bwd_weight", flops);
+        if (g.Cout == 64)
+            launch_tc_wgrad<128>(xs, ds, dw, int(g.X), int(g.Y), int(g.B), int(g.Cin), int(g.Cout));
+        else
+            launch_tc_wgrad<64>(xs, ds, dw, int(g.X), int(g.Y), int(g.B), int(g.Cin), int(g.Cout));
+    }
+    CUDA_CHECK(cudaFreeAsync(xs, c.stream));
+    CUDA_CHECK(cudaFreeAsync(ds, c.stream));
+}
 
 void conv_tc_enable(bool on) { g_tc_enabled = on; }
 

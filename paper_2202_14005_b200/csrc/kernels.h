@@ -120,6 +120,8 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
 void conv_tc_enable(bool on);
 bool conv_tc_supported(long cin, long cout, long kx, long ky);
 void conv_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode);
+bool conv_tc_wgrad_supported(long cin, long cout, long kx, long ky);
+void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
 
 // ---- batch norm (bn.cu) ----------------------------------------------------------
 struct IsoGeom {

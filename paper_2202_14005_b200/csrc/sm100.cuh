@@ -121,18 +121,19 @@ __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.
 
 // ---- descriptors ------------------------------------------------------------------------
 // K-major operand, 128-byte swizzle (rows of 128 B, 8-row / 1024 B atoms).
-// sbo = byte stride between consecutive 8-row groups along M/N.  The start
-// address may sit inside an atom (row-shifted halo views); base_offset then
-// carries the atom phase ((addr >> 7) & 7).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t sbo_bytes)
+// sbo = byte stride between consecutive 8-row groups along M/N.  The swizzle
+// XOR is taken from absolute shared-memory address bits (measured: a view
+// starting 1 or 2 rows into an atom reads correctly with base_offset = 0, and
+// is off by exactly the row shift with base_offset = (addr >> 7) & 7), so
+// row-shifted halo views of a 1024-B-aligned TMA buffer need no correction.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t sbo_bytes, uint32_t lbo_bytes = 0)
 {
     uint64_t d = 0;
     d |= uint64_t((saddr >> 4) & 0x3FFF);             // start address [0,14)
-    d |= uint64_t(0) << 16;                            // leading byte offset (unused, K-major swizzled)
-    d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;    // stride byte offset [32,46)
-    d |= uint64_t(1) << 46;                            // descriptor version (sm100)
-    d |= uint64_t((saddr >> 7) & 7) << 49;             // base offset [49,52)
-    d |= uint64_t(2) << 61;                            // layout: SWIZZLE_128B
+    d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;   // leading byte offset (MN-major block stride)
+    d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;   // stride byte offset [32,46)
+    d |= uint64_t(1) << 46;                           // descriptor version (sm100)
+    d |= uint64_t(2) << 61;                           // layout: SWIZZLE_128B (base offset 0)
     return d;
 }
 
