@@ -194,14 +194,6 @@ def config_of(args, B, world):
             "global_batch": B * world, "parallelism": f"dp{world}", "l2": "inputs > L2 (no flush)"}
 
 
-class DevBuf:
-    """__cuda_array_interface__ view of the library's flat gradient buffer."""
-
-    def __init__(self, ptr, n, stream):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
-                                         "stream": stream or 1}
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -225,6 +217,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2202_14005_b200 import load_library
+    from paper_2202_14005_b200.dp import DataParallelTrainer
     from paper_2202_14005_b200.mdnn import Trainer
 
     torch.cuda.set_device(local)
@@ -238,8 +231,7 @@ def main():
     data = make_data(lib, X, Y, NC, B, first_item=rank * B)
     model = build_model(lib, args.workload, B)
     tr = Trainer(lib, model, seed=42)
-    gptr, gn = tr.grad_buffer()
-    grads = torch.as_tensor(DevBuf(gptr, gn, lib.so.mdnn_stream()), device=torch.device("cuda", local))
+    dpt = DataParallelTrainer(tr, world=world, device=torch.device("cuda", local))
     dev = {k: torch.from_numpy(np.ascontiguousarray(v.transpose())).to(f"cuda:{local}") for k, v in data.items()}
     for k, v in dev.items():
         tr.set_data(k, v)
@@ -248,11 +240,7 @@ def main():
     h2d = sum(int(v.numel()) * 8 for k, v in pinned.items())
 
     def step():
-        tr.forward_backward()
-        if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(grads)
-        tr.update(1.0 / world)
+        dpt.step()  # forward + backward, NCCL all-reduce on the library stream, Adam
 
     def barrier():
         if world > 1:

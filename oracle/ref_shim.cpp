@@ -822,11 +822,14 @@ mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg*
         t->weights = t->joint.init_weights(seed);
         t->adam.resize(t->joint.args.size());
         t->ipalm.resize(t->joint.args.size());
+        size_t nflat = 0;
         for (size_t i = 0; i < t->joint.args.size(); i++)
             if (t->joint.args[i].kind == ArgKind::Weights) {
                 t->weight_args.push_back(int(i));
                 t->weight_names.push_back(t->joint.args[i].name);
+                nflat += 2 * size_t(md_size(t->joint.op.in_dims(int(i))));
             }
+        t->flat.assign(nflat, 0.f); // fixed buffer: callers may hold its address
         return t.release();
     });
 }
@@ -866,12 +869,13 @@ int mdnn_trainer_forward_backward(mdnn_trainer* t, double* loss)
             throw SolverError("training aborted: non-finite loss");
         auto grads = J.op.adjoint_all(loss_idx, A::scalar(std::complex<R>(1)));
         t->grads.clear();
-        t->flat.clear();
+        size_t off = 0;
         for (int i : t->weight_args) {
             t->grads[J.args[i].name] = grads[i];
-            for (long k = 0; k < grads[i].size(); k++) {
-                t->flat.push_back(float(grads[i].data()[k].real()));
-                t->flat.push_back(float(grads[i].data()[k].imag()));
+            A g = grads[i].has_default_strides() ? grads[i] : grads[i].clone();
+            for (long k = 0; k < g.size(); k++) {
+                t->flat[off++] = float(g.data()[k].real());
+                t->flat[off++] = float(g.data()[k].imag());
             }
         }
         if (loss)

@@ -5,10 +5,11 @@
 //   bwd-data   dx[q,c] = sum_{t,f} dy[q-t+c0, f] conj(w[t,c,f])
 //   bwd-weight dw[t,c,f] = sum_p dy[p,f] conj(x[p+t-c0, c])
 //
-// Canonical layout (x fastest, channel on dim 2, batch on dim 15).  These
-// kernels serve every channel count and kernel size; the 64->64 MoDL layers
-// are dispatched to the tcgen05 implicit-GEMM path in conv_tc.cu when it is
-// enabled.  Reductions are fixed-order (no atomics): bitwise run-to-run stable.
+// Each activation operand may be stored CANON (reference layout) or CHLAST
+// (channels-last planar, core.h).  These kernels serve every channel count
+// and kernel size (MoDL 1->F / F->1, VarNet 2->24 / 24->2 at 11x11); 3x3
+// layers with 32/64 channels go to the tcgen05 path (conv_tc.cu).
+// Reductions are fixed-order (no atomics): bitwise run-to-run stable.
 #include "kernels.h"
 #include "profile.h"
 
@@ -22,11 +23,40 @@ constexpr int TX = 32, TY = 8;   // output tile (pixels)
 constexpr int FG = 8;            // output channels per block
 constexpr int MAXK = 11;
 
+// element (item b, pixel xy = x + X*y, channel c) of a C-channel tensor
+struct Acc {
+    const cfloat* p;
+    long C, XY;
+    bool chl;
+    __device__ __forceinline__ float2 ld(long b, long xy, long c) const
+    {
+        if (chl) {
+            const float* f = reinterpret_cast<const float*>(p) + (b * XY + xy) * 2 * C;
+            return float2{f[c], f[C + c]};
+        }
+        return p[xy + XY * (c + C * b)];
+    }
+};
+struct Out {
+    cfloat* p;
+    long C, XY;
+    bool chl;
+    __device__ __forceinline__ void st(long b, long xy, long c, float2 v) const
+    {
+        if (chl) {
+            float* f = reinterpret_cast<float*>(p) + (b * XY + xy) * 2 * C;
+            f[c] = v.x;
+            f[C + c] = v.y;
+        } else {
+            p[xy + XY * (c + C * b)] = v;
+        }
+    }
+};
+
 // mode 0: fwd (in = x, Cin in, weights w[t,c,f]); mode 1: bwd-data (in = dy,
 // channels Cout, weights conj(w[t,c,f]) flipped, output channel c)
 template<int MODE>
-__global__ void __launch_bounds__(TX* TY) k_conv_direct(cfloat* __restrict__ out, const cfloat* __restrict__ in,
-                                                       const cfloat* __restrict__ w, ConvGeom g)
+__global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const cfloat* __restrict__ w, ConvGeom g)
 {
     __shared__ float2 tile[TY + MAXK - 1][TX + MAXK - 1];
     __shared__ float2 wsh[MAXK * MAXK][FG];
@@ -37,8 +67,7 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(cfloat* __restrict__ out
     const long f0 = (blockIdx.z % ngrp) * FG;
     const long x0 = long(blockIdx.x) * TX, y0 = long(blockIdx.y) * TY;
     const int KX = int(g.KX), KY = int(g.KY);
-    // offset of the input window: fwd  in[p + t - c0]
-    //                             bwd  in[q - t + c0] = in[q + t' - (K-1-c0)], t' = K-1-t
+    // input window offset: fwd in[p + t - c0]; bwd in[q - t + c0] = in[q + t' - (K-1-c0)]
     const long ox = MODE == 0 ? g.px : (g.KX - 1 - g.px);
     const long oy = MODE == 0 ? g.py : (g.KY - 1 - g.py);
     const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
@@ -48,11 +77,11 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(cfloat* __restrict__ out
         acc[f] = float2{0.f, 0.f};
     const int HX = TX + KX - 1, HY = TY + KY - 1;
     for (long c = 0; c < nin; c++) {
-        const cfloat* src = in + g.X * g.Y * (c + nin * b);
         for (int e = threadIdx.x; e < HX * HY; e += blockDim.x) {
             int hx = e % HX, hy = e / HX;
             long gx = x0 + hx - ox, gy = y0 + hy - oy;
-            tile[hy][hx] = (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? src[gx + g.X * gy] : float2{0.f, 0.f};
+            tile[hy][hx] = (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? in.ld(b, gx + g.X * gy, c)
+                                                                       : float2{0.f, 0.f};
         }
         for (int e = threadIdx.x; e < KX * KY * FG; e += blockDim.x) {
             int t = e % (KX * KY), f = e / (KX * KY);
@@ -62,7 +91,6 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(cfloat* __restrict__ out
                 if (MODE == 0) {
                     v = w[t + g.KX * g.KY * (c + g.Cin * fo)];
                 } else {
-                    // tap t' of the flipped kernel = t = K-1-t' per axis; weight w[t, fo(=c_in), c(=f_out)]
                     int tpx = t % KX, tpy = t / KX;
                     long tt = (KX - 1 - tpx) + g.KX * (KY - 1 - tpy);
                     float2 ww = w[tt + g.KX * g.KY * (fo + g.Cin * c)];
@@ -90,7 +118,7 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(cfloat* __restrict__ out
 #pragma unroll
         for (int f = 0; f < FG; f++)
             if (f0 + f < nout)
-                out[px + g.X * (py + g.Y * ((f0 + f) + nout * b))] = acc[f];
+                out.st(b, px + g.X * py, f0 + f, acc[f]);
 }
 
 // bwd-weight: block = (c-group x f-group, split); loops over its share of
@@ -100,8 +128,7 @@ constexpr int WMAXC = 4;                  // combos per thread
 
 // WG_C x WG_F channel pairs per block; (4, 8) for 3x3-5x5 kernels, (1, 8) up to 11x11
 template<int WG_C, int WG_F>
-__global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, const cfloat* __restrict__ x,
-                                                    const cfloat* __restrict__ dy, ConvGeom g, int nsplit)
+__global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, Acc x, Acc dy, ConvGeom g, int nsplit)
 {
     __shared__ float2 xt[WG_C][WTY + MAXK - 1][WTX + MAXK - 1];
     __shared__ float2 dyt[WG_F][WTY][WTX];
@@ -125,15 +152,13 @@ __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, c
         for (int e = threadIdx.x; e < WG_C * HX * HY; e += blockDim.x) {
             int hx = e % HX, hy = (e / HX) % HY, cc = e / (HX * HY);
             long gx = x0 + hx - g.px, gy = y0 + hy - g.py, c = c0 + cc;
-            xt[cc][hy][hx] = (c < g.Cin && gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y)
-                                 ? x[gx + g.X * (gy + g.Y * (c + g.Cin * b))]
-                                 : float2{0.f, 0.f};
+            xt[cc][hy][hx] = (c < g.Cin && gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? x.ld(b, gx + g.X * gy, c)
+                                                                                        : float2{0.f, 0.f};
         }
         for (int e = threadIdx.x; e < WG_F * WTX * WTY; e += blockDim.x) {
             int px = e % WTX, py = (e / WTX) % WTY, ff = e / (WTX * WTY);
             long gx = x0 + px, gy = y0 + py, f = f0 + ff;
-            dyt[ff][py][px] = (f < g.Cout && gx < g.X && gy < g.Y) ? dy[gx + g.X * (gy + g.Y * (f + g.Cout * b))]
-                                                                   : float2{0.f, 0.f};
+            dyt[ff][py][px] = (f < g.Cout && gx < g.X && gy < g.Y) ? dy.ld(b, gx + g.X * gy, f) : float2{0.f, 0.f};
         }
         __syncthreads();
 #pragma unroll
@@ -156,7 +181,6 @@ __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, c
         }
         __syncthreads();
     }
-    // partial layout [split][t + KK*(c + Cin*f)]
     for (int i = 0; i < WMAXC; i++) {
         int combo = threadIdx.x + i * blockDim.x;
         if (combo >= ncombo)
@@ -203,8 +227,10 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
     }
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cout + FG - 1) / FG)));
+    const long XY = g.X * g.Y;
     ProfScope prof("conv_fwd", conv_flops(g));
-    k_conv_direct<0><<<grid, TX * TY, 0, ctx().stream>>>(y, x, w, g);
+    k_conv_direct<0><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+                                                         Acc{x, g.Cin, XY, g.in_chlast}, w, g);
     KERNEL_CHECK();
 }
 
@@ -217,8 +243,10 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
     }
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cin + FG - 1) / FG)));
+    const long XY = g.X * g.Y;
     ProfScope prof("conv_bwd_data", conv_flops(g));
-    k_conv_direct<1><<<grid, TX * TY, 0, ctx().stream>>>(dx, dy, w, g);
+    k_conv_direct<1><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+                                                         Acc{dy, g.Cout, XY, g.out_chlast}, w, g);
     KERNEL_CHECK();
 }
 
@@ -239,15 +267,17 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     long target = long(ctx().sm_count) * 4;
     int nsplit = int(std::max(1L, std::min(ntiles, (target + ngroups - 1) / ngroups)));
     const long n = KK * g.Cin * g.Cout;
+    const long XY = g.X * g.Y;
     auto& c = ctx();
     float2* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
     dim3 grid{unsigned(ngroups), unsigned(nsplit)};
     ProfScope prof("conv_bwd_weight", conv_flops(g));
+    Acc ax{x, g.Cin, XY, g.in_chlast}, ad{dy, g.Cout, XY, g.out_chlast};
     if (small_k)
-        k_conv_wgrad<4, 8><<<grid, 256, 0, c.stream>>>(part, x, dy, g, nsplit);
+        k_conv_wgrad<4, 8><<<grid, 256, 0, c.stream>>>(part, ax, ad, g, nsplit);
     else
-        k_conv_wgrad<1, 8><<<grid, 256, 0, c.stream>>>(part, x, dy, g, nsplit);
+        k_conv_wgrad<1, 8><<<grid, 256, 0, c.stream>>>(part, ax, ad, g, nsplit);
     KERNEL_CHECK();
     k_sum_splits<<<int(std::min(1024L, (n + 255) / 256)), 256, 0, c.stream>>>(dw, part, n, nsplit);
     KERNEL_CHECK();

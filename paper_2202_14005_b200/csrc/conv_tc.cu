@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             // a_major = b_major = MN (bits 15, 16)
+            // a_major = b_major = MN (bits 15, 16); operands SWIZZLE_128B_BASE32B
             constexpr uint32_t idesc = idesc_tf32(128, N) | (1u << 15) | (1u << 16);
             uint32_t it = 0;
             const uint32_t sbase = smem_u32(smem);
@@ -291,10 +292,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const uint32_t xb = sbase + st * S::STAGE, db = xb + 4 * WG_XBLK;
 #pragma unroll
                 for (int ks = 0; ks < WG_SEG / 8; ks++) {
-                    const uint64_t bd = umma_desc_sw128(db + ks * 8 * 128, 1024, WG_DBLK);
+                    const uint64_t bd = umma_desc_mn_sw128_32b(db + ks * 8 * 128, 512, WG_DBLK);
 #pragma unroll
                     for (int kx = 0; kx < 3; kx++) {
-                        const uint64_t ad = umma_desc_sw128(xb + (kx + ks * 8) * 128, 1024, WG_XBLK);
+                        const uint64_t ad = umma_desc_mn_sw128_32b(xb + (kx + ks * 8) * 128, 512, WG_XBLK);
                         mma_tf32(tmem_base + kx * N, ad, bd, idesc, (s != s_begin || ks != 0) ? 1u : 0u);
                     }
                 }
@@ -412,7 +413,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn()
     return fn;
 }
 
-CUtensorMap make_act_map(const float* base, int C2, int X, int Y, int B, int box_x = HALO_P, int box_y = HALO_L)
+CUtensorMap make_act_map(const float* base, int C2, int X, int Y, int B, int box_x = HALO_P, int box_y = HALO_L,
+                         CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B)
 {
     CUtensorMap m;
     cuuint64_t dims[4] = {cuuint64_t(C2), cuuint64_t(X), cuuint64_t(Y), cuuint64_t(B)};
@@ -420,8 +422,8 @@ CUtensorMap make_act_map(const float* base, int C2, int X, int Y, int B, int box
     cuuint32_t box[4] = {32, cuuint32_t(box_x), cuuint32_t(box_y), 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         throw CudaError("cuTensorMapEncodeTiled(activation) failed: " + std::to_string(int(r)));
     return m;
@@ -469,8 +471,8 @@ template<int N>
 void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, int B, int Cin, int Cout)
 {
     auto& c = ctx();
-    CUtensorMap tx = make_act_map(x, 128, X, Y, B, WG_SEG + 2, 1);
-    CUtensorMap td = make_act_map(dy, N, X, Y, B, WG_SEG, 1);
+    CUtensorMap tx = make_act_map(x, 128, X, Y, B, WG_SEG + 2, 1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    CUtensorMap td = make_act_map(dy, N, X, Y, B, WG_SEG, 1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     auto kern = k_conv_tc_wgrad<N>;
     const int smem = WgSmem<N>::TOTAL;
     static std::mutex mu;
@@ -504,20 +506,43 @@ bool conv_tc_wgrad_supported(long cin, long cout, long kx, long ky)
 }
 
 // dw = conv_bwd_weight(x, dy) on the tensor cores (x: Cin channels, dy: Cout channels)
+namespace {
+
+__global__ void k_round_tf32(float* __restrict__ out, const float* __restrict__ in, long n)
+{
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
+        out[i] = to_tf32(in[i]);
+}
+
+// TF32-rounded CHLAST view of a C-channel operand: the array itself when it
+// already is one, else a staged copy (*tmp, freed by the caller)
+const float* stage_operand(const cfloat* p, long C, const ConvGeom& g, bool chlast, bool tf32, float** tmp)
+{
+    *tmp = nullptr;
+    if (chlast && tf32)
+        return reinterpret_cast<const float*>(p);
+    auto& c = ctx();
+    const long inner = g.X * g.Y, n = 2 * C * inner * g.B;
+    CUDA_CHECK(cudaMallocAsync(tmp, sizeof(float) * n, c.stream));
+    if (chlast) {
+        k_round_tf32<<<int(std::min<long>(c.sm_count * 8, (n + 255) / 256)), 256, 0, c.stream>>>(
+            *tmp, reinterpret_cast<const float*>(p), n);
+    } else {
+        k_to_chlast_tf32<<<dim3(unsigned((inner + 31) / 32), unsigned((C + 31) / 32), unsigned(g.B)), dim3(32, 8), 0,
+                           c.stream>>>(*tmp, p, inner, C, g.B);
+    }
+    KERNEL_CHECK();
+    return *tmp;
+}
+
+} // namespace
+
 void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g)
 {
     auto& c = ctx();
-    const long inner = g.X * g.Y;
-    float *xs, *ds;
-    CUDA_CHECK(cudaMallocAsync(&xs, sizeof(float) * 2 * g.Cin * inner * g.B, c.stream));
-    CUDA_CHECK(cudaMallocAsync(&ds, sizeof(float) * 2 * g.Cout * inner * g.B, c.stream));
-    dim3 cb(32, 8);
-    k_to_chlast_tf32<<<dim3(unsigned((inner + 31) / 32), unsigned((g.Cin + 31) / 32), unsigned(g.B)), cb, 0,
-                       c.stream>>>(xs, x, inner, g.Cin, g.B);
-    KERNEL_CHECK();
-    k_to_chlast_tf32<<<dim3(unsigned((inner + 31) / 32), unsigned((g.Cout + 31) / 32), unsigned(g.B)), cb, 0,
-                       c.stream>>>(ds, dy, inner, g.Cout, g.B);
-    KERNEL_CHECK();
+    float *xt, *dt;
+    const float* xs = stage_operand(x, g.Cin, g, g.in_chlast, g.in_tf32, &xt);
+    const float* ds = stage_operand(dy, g.Cout, g, g.out_chlast, g.out_tf32, &dt);
     {
         const double flops = 8.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * 9;
         ProfScope prof("conv_tc_bwd_weight", flops);
@@ -526,8 +551,10 @@ void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom
         else
             launch_tc_wgrad<64>(xs, ds, dw, int(g.X), int(g.Y), int(g.B), int(g.Cin), int(g.Cout));
     }
-    CUDA_CHECK(cudaFreeAsync(xs, c.stream));
-    CUDA_CHECK(cudaFreeAsync(ds, c.stream));
+    if (xt)
+        CUDA_CHECK(cudaFreeAsync(xt, c.stream));
+    if (dt)
+        CUDA_CHECK(cudaFreeAsync(dt, c.stream));
 }
 
 void conv_tc_enable(bool on) { g_tc_enabled = on; }
@@ -545,19 +572,18 @@ void conv_tc_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvGeo
 {
     auto& c = ctx();
     const long nin = mode == 0 ? g.Cin : g.Cout, nout = mode == 0 ? g.Cout : g.Cin;
+    const bool in_chl = mode == 0 ? g.in_chlast : g.out_chlast, in_rnd = mode == 0 ? g.in_tf32 : g.out_tf32;
+    const bool out_chl = mode == 0 ? g.out_chlast : g.in_chlast;
     const long inner = g.X * g.Y;
-    // operand staging: CHLAST + RN tf32
-    float* act;
-    float* res;
+    // operand staging only when the producer did not already deliver CHLAST + RN tf32
+    float* act_tmp;
+    const float* act = stage_operand(inp, nin, g, in_chl, in_rnd, &act_tmp);
+    float* res = out_chl ? reinterpret_cast<float*>(outp) : nullptr;
     float* wpk;
     const long K = 9 * 2 * nin, N = 2 * nout;
-    CUDA_CHECK(cudaMallocAsync(&act, sizeof(float) * 2 * nin * inner * g.B, c.stream));
-    CUDA_CHECK(cudaMallocAsync(&res, sizeof(float) * 2 * nout * inner * g.B, c.stream));
+    if (!out_chl)
+        CUDA_CHECK(cudaMallocAsync(&res, sizeof(float) * 2 * nout * inner * g.B, c.stream));
     CUDA_CHECK(cudaMallocAsync(&wpk, sizeof(float) * K * N, c.stream));
-    dim3 cb(32, 8);
-    k_to_chlast_tf32<<<dim3(unsigned((inner + 31) / 32), unsigned((nin + 31) / 32), unsigned(g.B)), cb, 0,
-                       c.stream>>>(act, inp, inner, nin, g.B);
-    KERNEL_CHECK();
     k_pack_weights<<<int(std::min<long>(1024, (K * N + 255) / 256)), 256, 0, c.stream>>>(
         wpk, w, int(g.KX), int(g.KY), int(g.Cin), int(g.Cout), mode);
     KERNEL_CHECK();
@@ -574,19 +600,20 @@ void conv_tc_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvGeo
         else
             launch_tc<64, 64>(act, wpk, res, X, Y, B);
     }
-    // CHLAST -> CANON
-    DArray tmp_in, tmp_out;
-    Dims d(max_rank, 1);
-    d[0] = g.X;
-    d[1] = g.Y;
-    d[2] = nout;
-    d[15] = g.B;
-    DArray src = DArray::view(reinterpret_cast<cfloat*>(res), d);
-    src.layout = Layout::CHLAST;
-    DArray dst = DArray::view(outp, d);
-    launch_layout_convert(src, dst);
-    CUDA_CHECK(cudaFreeAsync(act, c.stream));
-    CUDA_CHECK(cudaFreeAsync(res, c.stream));
+    if (!out_chl) { // CHLAST -> CANON for a reference-layout consumer
+        Dims d(max_rank, 1);
+        d[0] = g.X;
+        d[1] = g.Y;
+        d[2] = nout;
+        d[15] = g.B;
+        DArray src = DArray::view(reinterpret_cast<cfloat*>(res), d);
+        src.layout = Layout::CHLAST;
+        DArray dst = DArray::view(outp, d);
+        launch_layout_convert(src, dst);
+        CUDA_CHECK(cudaFreeAsync(res, c.stream));
+    }
+    if (act_tmp)
+        CUDA_CHECK(cudaFreeAsync(act_tmp, c.stream));
     CUDA_CHECK(cudaFreeAsync(wpk, c.stream));
 }
 

@@ -206,12 +206,14 @@ DArray to_layout(const DArray& a, Layout l)
 {
     if (a.layout == l)
         return a;
-    DArray o(a.dims, false, l);
     if (a.dims.size() < 3 || a.dims[2] == 1) {
-        // one channel: CANON and CHLAST coincide byte for byte
-        CUDA_CHECK(cudaMemcpyAsync(o.buf->ptr, a.buf->ptr, a.buf->bytes, cudaMemcpyDeviceToDevice, ctx().stream));
+        // one channel: CANON and CHLAST coincide byte for byte -> relabel, no copy
+        DArray o = a;
+        o.layout = l;
         return o;
     }
+    DArray o(a.dims, false, l);
+    o.tf32 = a.tf32;
     launch_layout_convert(a, o);
     return o;
 }

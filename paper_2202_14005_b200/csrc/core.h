@@ -105,6 +105,9 @@ struct DArray {
     Dims dims;
     std::shared_ptr<Buffer> buf;
     Layout layout = Layout::CANON;
+    // values are already rounded RN to TF32 (set by producers that feed a
+    // tensor-core convolution; lets the consumer skip its operand conversion)
+    bool tf32 = false;
 
     DArray() = default;
     explicit DArray(Dims d, bool zero = true, Layout l = Layout::CANON);

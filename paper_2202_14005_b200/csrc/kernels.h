@@ -109,6 +109,10 @@ struct ConvGeom {
     long Cin, Cout;    // complex channels
     long KX, KY;       // kernel extents
     long px, py;       // corner offsets ((k-1)/2)
+    // storage of the Cin-channel tensor (x / dx) and the Cout-channel tensor
+    // (y / dy): false = CANON, true = CHLAST; *_tf32: operand already RN-rounded
+    bool in_chlast = false, out_chlast = false;
+    bool in_tf32 = false, out_tf32 = false;
 };
 // y[p,f] = sum_{t,c} x[p+t-c0, c] w[t,c,f]
 void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g);

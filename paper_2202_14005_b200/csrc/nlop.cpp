@@ -181,7 +181,7 @@ std::vector<DArray> Nlop::adjoint_all(int o, const DArray& dy, const std::vector
         for (int p = 0; p < node.n_out(); p++) {
             if (!cot[ni][p].valid())
                 continue;
-            DArray g = std::move(cot[ni][p]);
+            DArray g = as_layout(std::move(cot[ni][p]), node.out_layout(p));
             node.adjoint_all(p, g, contrib, wk);
             for (int k = 0; k < node.n_in(); k++) {
                 if (k >= int(contrib.size()) || !contrib[k].valid())

@@ -51,10 +51,16 @@ public:
     virtual bool holomorphic() const { return false; }
     // cotangent of output o to every wanted input (containers override)
     virtual void adjoint_all(int o, const DArray& dy, std::vector<DArray>& dx, const std::vector<char>& want);
-    // storage layout the node wants for input i / produces on output o
+    // storage layout the node wants for input i / produces on output o (the
+    // engine hands cotangents of output o to adjoint_all in out_layout(o))
     virtual Layout in_layout(int i) const
     {
         (void)i;
+        return Layout::CANON;
+    }
+    virtual Layout out_layout(int o) const
+    {
+        (void)o;
         return Layout::CANON;
     }
 

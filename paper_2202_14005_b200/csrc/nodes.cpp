@@ -1232,9 +1232,27 @@ public:
         g_.KY = s.kernel[1];
         g_.px = (g_.KX - 1) / 2;
         g_.py = (g_.KY - 1) / 2;
+        // channels-last storage for multi-channel activations: requested by the
+        // builder (MoDL denoiser chain) or implied by the tensor-core path
+        const bool tc = conv_tc_supported(g_.Cin, g_.Cout, g_.KX, g_.KY);
+        const bool chl = s.chlast_hint > 0 || (s.chlast_hint == 0 && tc);
+        g_.in_chlast = chl && g_.Cin > 1;
+        g_.out_chlast = chl && g_.Cout > 1;
     }
     bool holomorphic() const override { return !t_; }
-    // inputs: fwd (x, w); transposed (w, y)
+    Layout act_layout(bool in_side) const
+    {
+        return (in_side ? g_.in_chlast : g_.out_chlast) ? Layout::CHLAST : Layout::CANON;
+    }
+    // fwd inputs (x, w) -> y ; transposed inputs (w, y) -> x
+    Layout in_layout(int i) const override
+    {
+        if (!t_)
+            return i == 0 ? act_layout(true) : Layout::CANON;
+        return i == 1 ? act_layout(false) : Layout::CANON;
+    }
+    Layout out_layout(int) const override { return act_layout(t_); }
+
     void forward(const std::vector<DArray>& in, std::vector<DArray>& out, bool store) override
     {
         if (!t_)
@@ -1264,25 +1282,42 @@ public:
     }
 
 private:
-    DArray fwd(const DArray& x, const DArray& w) const
+    // the Cin-side tensor (x / dx) and the Cout-side tensor (y / dy) in the
+    // layouts this node stores them in
+    DArray as_in(const DArray& a) const { return a.layout == act_layout(true) ? a : to_layout(a, act_layout(true)); }
+    DArray as_out(const DArray& a) const
     {
+        return a.layout == act_layout(false) ? a : to_layout(a, act_layout(false));
+    }
+    DArray fwd(const DArray& x0, const DArray& w) const
+    {
+        DArray x = as_in(x0);
         Dims od = t_ ? ins_[1] : outs_[0];
-        DArray y(od, false);
-        conv_fwd(y.data(), x.data(), w.data(), g_);
+        DArray y(od, false, act_layout(false));
+        ConvGeom g = g_;
+        g.in_tf32 = x.tf32;
+        conv_fwd(y.data(), x.data(), w.data(), g);
         return y;
     }
-    DArray bwd_data(const DArray& dy, const DArray& w) const
+    DArray bwd_data(const DArray& dy0, const DArray& w) const
     {
+        DArray dy = as_out(dy0);
         Dims xd = t_ ? outs_[0] : ins_[0];
-        DArray dx(xd, false);
-        conv_bwd_data(dx.data(), dy.data(), w.data(), g_);
+        DArray dx(xd, false, act_layout(true));
+        ConvGeom g = g_;
+        g.out_tf32 = dy.tf32;
+        conv_bwd_data(dx.data(), dy.data(), w.data(), g);
         return dx;
     }
-    DArray bwd_weight(const DArray& x, const DArray& dy) const
+    DArray bwd_weight(const DArray& x0, const DArray& dy0) const
     {
+        DArray x = as_in(x0), dy = as_out(dy0);
         Dims wd = t_ ? ins_[0] : ins_[1];
         DArray dw(wd, false);
-        conv_bwd_weight(dw.data(), x.data(), dy.data(), g_);
+        ConvGeom g = g_;
+        g.in_tf32 = x.tf32;
+        g.out_tf32 = dy.tf32;
+        conv_bwd_weight(dw.data(), x.data(), dy.data(), g);
         return dw;
     }
     bool t_;

@@ -69,6 +69,10 @@ struct ConvSpec {
     long out_channels = 1;
     bool pad_same = false;
     bool transposed = false;
+    // storage hint for multi-channel activations (not part of the reference
+    // spec): 0 = auto (channels-last iff the tensor-core path applies),
+    // 1 = channels-last (MoDL denoiser chain), -1 = reference layout
+    int chlast_hint = 0;
     Dims weight_dims() const;
     Dims out_dims() const;
 };

@@ -33,17 +33,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Bounded wait: a pipeline that never completes (e.g. a TMA transaction-count
+// mismatch) traps after ~4 s instead of hanging the device.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase)
 {
-    asm volatile(
-        "{\n\t"
-        ".reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-        "@!P1 bra WAIT_%=;\n\t"
-        "}" ::"r"(smem_u32(bar)),
-        "r"(phase), "r"(0x989680)
-        : "memory");
+    const long long t0 = clock64();
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t"
+            ".reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t"
+            "}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase), "r"(1000000)
+            : "memory");
+        if (done)
+            return;
+        if (clock64() - t0 > 8000000000LL)
+            __trap();
+    }
 }
 
 // ---- TMA ---------------------------------------------------------------------------
@@ -134,6 +144,21 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t sbo
     d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;   // stride byte offset [32,46)
     d |= uint64_t(1) << 46;                           // descriptor version (sm100)
     d |= uint64_t(2) << 61;                           // layout: SWIZZLE_128B (base offset 0)
+    return d;
+}
+
+// MN-major TF32 operand: the only legal layout is SWIZZLE_128B_BASE32B
+// (layout type 1; TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B), 32 elements
+// (128 B) contiguous along M/N per row, K atoms of 4 rows.
+// lbo = byte stride between 32-element M/N blocks, sbo = between 4-row K groups.
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128_32b(uint32_t saddr, uint32_t sbo_bytes, uint32_t lbo_bytes)
+{
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(1) << 61; // SWIZZLE_128B_BASE32B
     return d;
 }
 
