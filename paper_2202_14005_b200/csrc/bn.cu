@@ -117,6 +117,20 @@ void launch_stat_mul_u_f(cfloat* out, const cfloat* u, const cfloat* f, const Is
     launch_stat_mul(out, u, f, g, false);
 }
 
+namespace {
+__global__ void k_real_to_complex(cfloat* out, const float* in, long n)
+{
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
+        out[i] = cfloat{in[i], 0.f};
+}
+} // namespace
+
+void launch_real_to_complex(cfloat* out, const float* in, long n)
+{
+    k_real_to_complex<<<grid_for(n), kT, 0, ctx().stream>>>(out, in, n);
+    KERNEL_CHECK();
+}
+
 void bn_train_forward(cfloat* y, cfloat* u, cfloat* istd, cfloat* mean_out, cfloat* var_out, const cfloat* x,
                       const cfloat* mean_in, const cfloat* var_in, const IsoGeom& g, float eps, float mom)
 {

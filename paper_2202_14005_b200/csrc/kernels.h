@@ -147,6 +147,17 @@ void launch_stat_mul(cfloat* out, const cfloat* in, const cfloat* s, const IsoGe
 void launch_stat_add(cfloat* out, const cfloat* in, const cfloat* b, const IsoGeom& g);
 // out = s[stat]*c : out[i] = u[i] * f(stat) -- helper for BN adjoint wrt stats
 void launch_stat_mul_u_f(cfloat* out, const cfloat* u, const cfloat* f, const IsoGeom& g);
+// out[i] = (in[i], 0)
+void launch_real_to_complex(cfloat* out, const float* in, long n);
+
+// ---- fused BN + gamma + beta + CReLU on CHLAST activations (bnblock.cu) --------------
+// x, out, dx, gout: CHLAST floats of npix pixels x C channels; mu/istd: per-channel
+// device scratch kept by the node for the backward pass
+void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, float2* var_out, const float* x,
+                     const float2* mean_in, const float2* var_in, const float2* gamma, const float2* beta, long npix,
+                     int C, float eps, float mom, bool round_tf32);
+void bnblock_backward(float* dx, float2* dgamma, float2* dbeta, const float* gout, const float* x, const float2* mu,
+                      const float* istd, const float2* gamma, const float2* beta, long npix, int C, bool round_tf32);
 
 // ---- RBF (rbf.cu, ops.hpp:1308-1427) -------------------------------------------------
 struct RbfGeom {

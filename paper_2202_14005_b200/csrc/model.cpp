@@ -1,5 +1,7 @@
 #include "model.h"
 
+#include "kernels.h"
+
 #include <algorithm>
 
 namespace mdnn {
@@ -231,6 +233,11 @@ Model modl_denoiser(const ModlConfig& cfg, const std::string& stat_suffix)
         cnn = first_map_slice(sd);
     Dims cur = sd1.image();
     const unsigned long bn_flags = (1UL << dim_x) | (1UL << dim_y) | (1UL << dim_batch);
+    // train mode with a supported width: the BN / gamma / beta / CReLU chain runs
+    // as one fused channels-last node, and every conv of the chain keeps its
+    // feature maps channels-last (no layout conversions inside the denoiser)
+    const bool fused = cfg.train_mode && bnblock_supported(cfg.filters) && cfg.layers >= 2;
+    auto is_tc = [&](long cin, long cout) { return conv_tc_supported(cin, cout, cfg.kernel, cfg.kernel); };
     for (long l = 0; l < cfg.layers; l++) {
         const bool last = l + 1 == cfg.layers;
         const std::string ln = "dw" + std::to_string(l);
@@ -241,11 +248,26 @@ Model modl_denoiser(const ModlConfig& cfg, const std::string& stat_suffix)
         spec.chan_dim = dim_chan;
         spec.out_channels = last ? 1 : cfg.filters;
         spec.pad_same = true;
+        spec.chlast_hint = fused ? 1 : 0;
         Model conv = conv_layer(ln, spec, last);
         cnn = cnn.valid() ? model_chain(cnn, conv, "x") : conv;
+        const long cin = cur[dim_chan];
         cur = spec.out_dims();
         if (last)
             break;
+        if (fused) {
+            const bool next_tc = is_tc(cfg.filters, l + 2 == cfg.layers ? 1 : cfg.filters);
+            const bool this_tc = is_tc(cin, cfg.filters);
+            Model blk = plain(Nlop(node_bnblock(cur, next_tc, this_tc)),
+                              {data_arg("x"),
+                               Arg{ln + "_bn_mean", ArgKind::MovingStats, Initializer::constant(0), ProxKind::None, false},
+                               Arg{ln + "_bn_var", ArgKind::MovingStats, Initializer::constant(1), ProxKind::None, false},
+                               Arg{ln + "_g", ArgKind::Weights, Initializer::constant(1), ProxKind::None, false},
+                               Arg{ln + "_beta", ArgKind::Weights, Initializer::constant(0), ProxKind::None, false}},
+                              {ln + "_bn_mean" + stat_suffix, ln + "_bn_var" + stat_suffix, "out"});
+            cnn = model_chain(cnn, blk, "x");
+            continue;
+        }
         Model bn = batchnorm_layer(ln + "_bn", cur, bn_flags, cfg.train_mode);
         if (!stat_suffix.empty() && cfg.train_mode)
             for (auto& n : bn.out_names)

@@ -1325,6 +1325,190 @@ private:
     std::vector<DArray> st_;
 };
 
+// ---------------------------------------------------------------------------
+// Fused BatchNorm -> bn_scale TenMul -> BroadcastAdd -> CReLU (train mode) on
+// channels-last activations.  Same values and derivatives as the reference
+// chain (ops.hpp:1070-1298, 69-118, 153-209, 451-475); 2 HBM passes forward,
+// 2 backward.  Rare paths (tangents, statistics-output cotangents) reuse the
+// reference-layout kernels.
+class BnBlockNode : public Atom {
+public:
+    BnBlockNode(const Dims& d, bool round_out, bool round_dx, double eps, double mom)
+        : Atom("bn_block", {d, sdims(d), sdims(d), sdims(d), sdims(d)}, {sdims(d), sdims(d), d}),
+          round_out_(round_out), round_dx_(round_dx), eps_(float(eps)), mom_(float(mom))
+    {
+        C_ = d[2];
+        npix_ = md_size(d) / C_;
+        geo_ = IsoGeom{d[0] * d[1], C_, npix_ / (d[0] * d[1])};
+        m_ = double(npix_);
+    }
+    static Dims sdims(Dims d)
+    {
+        for (size_t k = 0; k < d.size(); k++)
+            if (k != size_t(dim_chan))
+                d[k] = 1;
+        return d;
+    }
+    Layout in_layout(int i) const override { return i == 0 ? Layout::CHLAST : Layout::CANON; }
+    Layout out_layout(int o) const override { return o == 2 ? Layout::CHLAST : Layout::CANON; }
+    bool zero_deriv(int o, int i) const override
+    {
+        if (o == 2)
+            return !(i == 0 || i == 3 || i == 4);
+        if (o == 0)
+            return !(i == 0 || i == 1);
+        return !(i == 0 || i == 2);
+    }
+    void forward(const std::vector<DArray>& in, std::vector<DArray>& out, bool store) override
+    {
+        const Dims& sd = ins_[1];
+        DArray y(ins_[0], false, Layout::CHLAST), mo(sd, false), vo(sd, false);
+        DArray mu(sd, false), istd(Dims{C_}, false);
+        bnblock_forward(y.fdata(), mu.data(), istd.fdata(), mo.data(), vo.data(), in[0].fdata(), in[1].data(),
+                        in[2].data(), in[3].data(), in[4].data(), npix_, int(C_), eps_, mom_, round_out_);
+        y.tf32 = round_out_;
+        out[0] = mo;
+        out[1] = vo;
+        out[2] = y;
+        if (store) {
+            x_ = in[0];
+            g_ = in[3];
+            b_ = in[4];
+            mu_ = mu;
+            istd_ = istd;
+        }
+        bump_generation();
+    }
+    void adjoint_all(int o, const DArray& gin, std::vector<DArray>& dx, const std::vector<char>& want) override
+    {
+        require_forward();
+        dx.assign(n_in(), DArray{});
+        const Dims& sd = ins_[1];
+        if (o == 2) {
+            DArray dxx, dg, db;
+            if (want[0])
+                dxx = DArray(ins_[0], false, Layout::CHLAST);
+            if (want[3])
+                dg = DArray(sd, false);
+            if (want[4])
+                db = DArray(sd, false);
+            if (!want[0] && !want[3] && !want[4])
+                return;
+            // the reduction pass always produces both sums; route them to scratch when unwanted
+            DArray sg = want[3] ? dg : DArray(sd, false), sb = want[4] ? db : DArray(sd, false);
+            bnblock_backward(want[0] ? dxx.fdata() : nullptr, sg.data(), sb.data(), gin.fdata(), x_.fdata(),
+                             mu_.data(), istd_.fdata(), g_.data(), b_.data(), npix_, int(C_), round_dx_);
+            if (want[0]) {
+                dxx.tf32 = round_dx_;
+                dx[0] = dxx;
+            }
+            if (want[3])
+                dx[3] = dg;
+            if (want[4])
+                dx[4] = db;
+            return;
+        }
+        // moving-statistics outputs (ops.hpp:1265-1282)
+        const int own = o == 0 ? 1 : 2;
+        if (want[own]) {
+            DArray t(sd, false);
+            launch_scale(t.data(), gin.data(), cfloat{1.f - mom_, 0.f}, t.size());
+            dx[own] = t;
+        }
+        if (want[0]) {
+            DArray xc = to_layout(x_, Layout::CANON);
+            DArray r(ins_[0], false);
+            if (o == 0) { // (mom/m) broadcast(g)
+                DArray z(ins_[0], true), t(ins_[0], false);
+                launch_stat_add(t.data(), z.data(), gin.data(), geo_);
+                launch_scale(r.data(), t.data(), cfloat{float(mom_ / m_), 0.f}, r.size());
+            } else { // u * (mom 2 Re(g) / m)
+                DArray u = centred(xc), q(sd, false), f(sd, false);
+                launch_real(q.data(), gin.data(), q.size());
+                launch_scale(f.data(), q.data(), cfloat{float(mom_ * 2.0 / m_), 0.f}, f.size());
+                launch_stat_mul(r.data(), u.data(), f.data(), geo_, false);
+            }
+            dx[0] = to_layout(r, Layout::CHLAST);
+        }
+    }
+    DArray adjoint(int o, int i, const DArray& g) override
+    {
+        std::vector<char> want(n_in(), 0);
+        want[i] = 1;
+        std::vector<DArray> dx;
+        adjoint_all(o, as_out(o, g), dx, want);
+        return dx[i].valid() ? dx[i] : DArray(ins_[i]);
+    }
+    DArray deriv(int o, int i, const DArray& d0) override
+    {
+        require_forward();
+        const Dims& sd = ins_[1];
+        DArray xc = to_layout(x_, Layout::CANON);
+        DArray u = centred(xc);
+        if (o == 2) {
+            // z = g * yhat + beta, yhat = u * istd ; tangent masked by CReLU(z)
+            DArray yh(ins_[0], false), t1(ins_[0], false), z(ins_[0], false), dz(ins_[0], false);
+            DArray istd_c = istd_complex();
+            launch_stat_mul(yh.data(), u.data(), istd_c.data(), geo_, false);
+            launch_stat_mul(t1.data(), yh.data(), g_.data(), geo_, false);
+            launch_stat_add(z.data(), t1.data(), b_.data(), geo_);
+            if (i == 0) {
+                DArray dc = to_layout(d0, Layout::CANON), dyh(ins_[0], false);
+                bn_train_deriv_x(dyh.data(), dc.data(), u.data(), istd_c.data(), geo_);
+                launch_stat_mul(dz.data(), dyh.data(), g_.data(), geo_, false);
+            } else if (i == 3) {
+                launch_stat_mul(dz.data(), yh.data(), d0.data(), geo_, false);
+            } else {
+                DArray zero(ins_[0], true);
+                launch_stat_add(dz.data(), zero.data(), d0.data(), geo_);
+            }
+            DArray r(ins_[0], false);
+            launch_crelu_mask(r.data(), dz.data(), z.data(), r.size());
+            return to_layout(r, Layout::CHLAST);
+        }
+        DArray r(sd, false);
+        if (i != 0) {
+            launch_scale(r.data(), d0.data(), cfloat{1.f - mom_, 0.f}, r.size());
+            return r;
+        }
+        DArray dc = to_layout(d0, Layout::CANON);
+        if (o == 0) {
+            launch_iso_reduce(r.data(), dc.data(), nullptr, geo_.inner, geo_.nstat, geo_.outer, 0, float(mom_ / m_));
+        } else {
+            DArray p(sd, false), q(sd, false);
+            launch_iso_reduce(p.data(), dc.data(), u.data(), geo_.inner, geo_.nstat, geo_.outer, 1, 1.f);
+            launch_real(q.data(), p.data(), q.size());
+            launch_scale(r.data(), q.data(), cfloat{float(mom_ * 2.0 / m_), 0.f}, r.size());
+        }
+        return r;
+    }
+
+private:
+    DArray as_out(int o, const DArray& g) const { return to_layout(g, out_layout(o)); }
+    // u = x - mu (reference layout)
+    DArray centred(const DArray& xc) const
+    {
+        DArray nm(ins_[1], false), u(ins_[0], false);
+        launch_neg(nm.data(), mu_.data(), nm.size());
+        launch_stat_add(u.data(), xc.data(), nm.data(), geo_);
+        return u;
+    }
+    // istd as complex (istd, 0) per channel for the reference-layout kernels
+    DArray istd_complex() const
+    {
+        DArray r(ins_[1], false);
+        launch_real_to_complex(r.data(), istd_.fdata(), C_);
+        return r;
+    }
+
+    bool round_out_, round_dx_;
+    float eps_, mom_;
+    long C_ = 1, npix_ = 1;
+    double m_ = 1;
+    IsoGeom geo_{};
+    DArray x_, g_, b_, mu_, istd_;
+};
+
 } // namespace
 
 // ---------------------------------------------------------------------------
@@ -1359,6 +1543,13 @@ NodePtr node_batchnorm(const Dims& d, unsigned long flags, bool train, double ep
 NodePtr node_rbf(const Dims& z, int fd, const std::vector<float>& mu, float sigma)
 {
     return std::make_shared<RbfNode>(z, fd, mu, sigma);
+}
+bool bnblock_supported(long channels) { return channels >= 1 && channels <= 256 && 256 % channels == 0; }
+NodePtr node_bnblock(const Dims& dims, bool round_out, bool round_dx, double eps, double mom)
+{
+    if (!bnblock_supported(dims.at(dim_chan)))
+        throw ConfigError("bn_block: channel count must divide 256");
+    return std::make_shared<BnBlockNode>(dims, round_out, round_dx, eps, mom);
 }
 NodePtr node_sense_normal(const SenseDims& sd) { return std::make_shared<SenseNormalNode>(sd, false); }
 NodePtr node_sense_normal_lambda(const SenseDims& sd) { return std::make_shared<SenseNormalNode>(sd, true); }

@@ -23,6 +23,13 @@ NodePtr node_exp_real(const Dims& dims);
 NodePtr node_mse(const Dims& dims);
 NodePtr node_batchnorm(const Dims& dims, unsigned long flags, bool train, double eps, double mom);
 NodePtr node_rbf(const Dims& z, int filter_dim, const std::vector<float>& centers, float sigma);
+// fused train-mode BatchNorm(x, y, batch) -> gamma -> beta -> CReLU block of the
+// MoDL denoiser (recon.hpp:748-776): inputs (x, mean, var, g, beta),
+// outputs (mean', var', out) — the reference chain's argument / output order.
+// round_out / round_dx: RN-round the output / input cotangent to TF32 for a
+// tensor-core convolution consumer.
+NodePtr node_bnblock(const Dims& dims, bool round_out, bool round_dx, double eps = 1e-5, double mom = 0.1);
+bool bnblock_supported(long channels);
 
 // ---- fused SENSE nodes ----------------------------------------------------
 struct SenseDims {

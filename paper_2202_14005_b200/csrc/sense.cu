@@ -357,6 +357,19 @@ __global__ void __launch_bounds__(kT) k_normal_y(NormalArgs a, fftd::Plan plan)
     (void)XY;
 }
 
+} // namespace
+} // namespace mdnn
+#include <map>
+#include <mutex>
+namespace mdnn {
+namespace {
+#include "sense_fast.cuh"
+
+bool fast_ok(const SenseGeom& g, const cfloat* coils, const cfloat* coils2)
+{
+    return g.M == 1 && coils2 == coils && g.pat_x == 1 && g.pat_c == 1 && fast_n1(g.Y) != 0;
+}
+
 int pick_w(long Y, int M)
 {
     int W = 16;
@@ -542,6 +555,25 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
 {
     if (!coils2)
         coils2 = coils;
+    if (fast_ok(g, coils, coils2)) {
+        NormalArgs a{};
+        a.out = out;
+        a.x = x;
+        a.coils = coils;
+        a.coils2 = coils2;
+        a.pattern = pattern;
+        a.lam = lam;
+        a.X = g.X;
+        a.Y = g.Y;
+        a.C = g.C;
+        a.M = g.M;
+        a.B = g.B;
+        a.ps = pat_strides(g);
+        a.mode = 0;
+        a.errflags = ctx().d_errflags;
+        if (dispatch_fast<1>(a, nullptr, 0))
+            return;
+    }
     if (fused_ok(g)) {
         NormalArgs a{};
         a.out = out;
@@ -658,6 +690,43 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
     }
     auto& c = ctx();
     const int n_upd = grid_for(n);
+    if (fast_ok(g, coils, coils)) {
+        // register-resident kernel, coils split over 2 CTAs -> 2 Ap planes;
+        // p ping-pongs between two buffers (no CTA reads a p another rewrites)
+        constexpr int NS = 2;
+        CgMem m = cg_alloc(max_iter, tol, int(fast_ctas(g, NS)), n_upd);
+        DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{NS * n}, false);
+        cfloat* P[2] = {pb.data(), pb.data() + n};
+        cg_start(m, x, b, r.data(), P[1], n);
+        for (int it = 0; it < max_iter; it++) {
+            NormalArgs a{};
+            a.out = ap.data();
+            a.x = r.data();
+            a.p = P[it & 1];
+            a.coils = coils;
+            a.coils2 = coils;
+            a.pattern = pattern;
+            a.lam = lam;
+            a.X = g.X;
+            a.Y = g.Y;
+            a.C = g.C;
+            a.M = g.M;
+            a.B = g.B;
+            a.ps = pat_strides(g);
+            a.mode = 1;
+            a.it = it;
+            a.cg = m.st;
+            a.errflags = c.d_errflags;
+            dispatch_fast<NS>(a, P[(it + 1) & 1], n);
+            k_cg_update_planes<<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(), n,
+                                                          NS, n, c.d_errflags);
+            KERNEL_CHECK();
+        }
+        k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
+        KERNEL_CHECK();
+        CUDA_CHECK(cudaFreeAsync(m.mem, c.stream));
+        return;
+    }
     const int n_pap = int(normal_y_ctas(g));
     CgMem m = cg_alloc(max_iter, tol, n_pap, n_upd);
     DArray r(Dims{n}, false), p(Dims{n}, false), ap(Dims{n}, false);

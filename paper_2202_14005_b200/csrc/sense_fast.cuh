@@ -1,0 +1,262 @@
+// Register-resident fused A^H A (+ lambda) for Y = N1 * N2 (included by sense.cu).
+//
+// Per CTA: W image columns x all Y rows of one item, a contiguous range of
+// coils (coil-split across NSPLIT CTAs for load balance; the partial results
+// land in NSPLIT planes that the CG update sums, and <p, Ap> is linear in Ap
+// so its per-CTA partials stay exact).  Per coil, with y = j + N2*q:
+//   stage A  thread (w, j):   v[q] = C[y] x[y]  -> DFT_N1 over q -> twiddle
+//                              W_Y^{j k1} -> smem S[k1][j]
+//   stage B  thread (w, k1):  DFT_N2 over j -> spectrum X[k1 + N1 k2]
+//                              -> mask P/Y -> IDFT_N2 -> conj twiddle -> S
+//   stage C  thread (w, j):   IDFT_N1 over k1 -> acc[q] += conj(C[y]) v[q]
+// Stage A and C threads own the same y positions, so the coil values loaded
+// for stage A are reused for the combine and the accumulators never leave
+// registers.  S is double-buffered by coil parity: 2 barriers per coil.
+#pragma once
+
+template<int N1, int N2, int W, int NSPLIT>
+__global__ void __launch_bounds__(W* N2, 2)
+    k_normal_fast(NormalArgs a, const float2* __restrict__ tw, cfloat* __restrict__ p_out, long plane)
+{
+    using namespace fftd;
+    constexpr int Y = N1 * N2;
+    constexpr int NT = W * N2;
+    extern __shared__ float2 dsm[];
+    float2* S0 = dsm;                 // [2][N1 * N2 * W]
+    float2* stw = S0 + 2 * Y * W;     // [Y]
+    float2* spat = stw + Y;           // [Y]
+    float2* xs = spat + Y;            // [Y * W]
+    __shared__ float s_beta;
+    __shared__ float2 s_lam;
+
+    const int tid = threadIdx.x;
+    const int w = tid % W, j = tid / W;
+    const long nxb = (a.X + W - 1) / W;
+    long blk = blockIdx.x;
+    const int split = int(blk % NSPLIT);
+    blk /= NSPLIT;
+    const long x0 = (blk % nxb) * W, b = blk / nxb;
+    const long xx = x0 + w;
+    const bool colok = xx < a.X;
+    const long c_begin = a.C * split / NSPLIT, c_end = a.C * (split + 1) / NSPLIT;
+    const float invY = 1.f / float(Y);
+
+    for (int e = tid; e < Y; e += NT) {
+        stw[e] = tw[e];
+        float2 pv = a.pattern[e * a.ps.sy + b * a.ps.sb];
+        spat[e] = float2{pv.x * invY, pv.y * invY};
+    }
+    if (tid == 0) {
+        s_beta = a.mode == 1 ? cg_prologue(a.cg, a.it, a.errflags) : 0.f;
+        s_lam = a.lam ? a.lam[0] : float2{0.f, 0.f};
+    }
+    __syncthreads();
+    const float beta = s_beta;
+    if (a.mode == 1 && beta < 0.f)
+        return;
+
+    // image column strip (x, or p = r + beta p_prev) -> smem
+    const long img_base = xx + a.X * a.Y * b;
+#pragma unroll
+    for (int q = 0; q < N1; q++) {
+        const int y = j + N2 * q;
+        const long gi = img_base + a.X * y;
+        float2 v{0.f, 0.f};
+        if (colok) {
+            if (a.mode == 0) {
+                v = a.x[gi];
+            } else if (a.it == 0) {
+                v = p_out[gi];
+            } else {
+                const float2 r = a.x[gi], pp = a.p[gi];
+                v = float2{r.x + beta * pp.x, r.y + beta * pp.y};
+                if (split == 0)
+                    p_out[gi] = v;
+            }
+        }
+        xs[y * W + w] = v;
+    }
+    __syncthreads();
+
+    float2 acc[N1];
+#pragma unroll
+    for (int q = 0; q < N1; q++)
+        acc[q] = float2{0.f, 0.f};
+
+    for (long c = c_begin; c < c_end; c++) {
+        float2* Sb = S0 + (c & 1) * (Y * W);
+        const long coil_base = xx + a.X * a.Y * (c + a.C * b);
+        // ---- stage A: coil multiply, DFT over q, twiddle -> S
+        float2 cv[N1], v[N1];
+#pragma unroll
+        for (int q = 0; q < N1; q++)
+            cv[q] = colok ? a.coils[coil_base + a.X * (j + N2 * q)] : float2{0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < N1; q++)
+            v[q] = cmul(cv[q], xs[(j + N2 * q) * W + w]);
+        dft_reg<N1, -1>(v);
+#pragma unroll
+        for (int k1 = 0; k1 < N1; k1++)
+            Sb[(k1 * N2 + j) * W + w] = k1 == 0 ? v[0] : cmul(v[k1], stw[j * N1 + k1]);
+        __syncthreads();
+        // ---- stage B: DFT over j, mask, inverse DFT over k2, conj twiddle
+        if (tid < W * N1) {
+            const int wb = tid % W, k1 = tid / W;
+            float2 u[N2];
+#pragma unroll
+            for (int jj = 0; jj < N2; jj++)
+                u[jj] = Sb[(k1 * N2 + jj) * W + wb];
+            dft_reg<N2, -1>(u);
+#pragma unroll
+            for (int k2 = 0; k2 < N2; k2++)
+                u[k2] = cmul(u[k2], spat[k1 + N1 * k2]);
+            dft_reg<N2, +1>(u);
+#pragma unroll
+            for (int jj = 0; jj < N2; jj++)
+                Sb[(k1 * N2 + jj) * W + wb] = k1 == 0 ? u[jj] : cmulc(u[jj], stw[jj * N1 + k1]);
+        }
+        __syncthreads();
+        // ---- stage C: inverse DFT over k1, conj-coil accumulate
+#pragma unroll
+        for (int k1 = 0; k1 < N1; k1++)
+            v[k1] = Sb[(k1 * N2 + j) * W + w];
+        dft_reg<N1, +1>(v);
+#pragma unroll
+        for (int q = 0; q < N1; q++) {
+            const float2 t = cmulc(v[q], cv[q]);
+            acc[q].x += t.x;
+            acc[q].y += t.y;
+        }
+    }
+
+    // ---- epilogue: + lambda x (split 0), store plane, <p, Ap> partial
+    double2 part{0, 0};
+#pragma unroll
+    for (int q = 0; q < N1; q++) {
+        const int y = j + N2 * q;
+        const float2 xv = xs[y * W + w];
+        float2 o = acc[q];
+        if (split == 0) {
+            const float2 lx = cmul(xv, s_lam);
+            o.x += lx.x;
+            o.y += lx.y;
+        }
+        if (colok) {
+            a.out[plane * split + img_base + a.X * y] = o;
+            part.x += double(xv.x) * o.x + double(xv.y) * o.y;
+            part.y += double(xv.y) * o.x - double(xv.x) * o.y;
+        }
+    }
+    if (a.mode == 1) {
+        part = block_sum2(part);
+        if (tid == 0)
+            a.cg->part_pap[blockIdx.x] = part;
+    }
+}
+
+template<int N1, int N2, int W>
+constexpr size_t fast_smem_bytes()
+{
+    return sizeof(float2) * (2 * N1 * N2 * W + 2 * N1 * N2 + N1 * N2 * W);
+}
+
+// forward twiddles tw[j * N1 + k1] = exp(-2 pi i j k1 / Y), double-accurate, per (device, Y)
+const float2* fast_twiddles(int N1, int N2)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, float2*> cache;
+    auto& c = ctx();
+    const int Y = N1 * N2;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(c.device, Y * 1000 + N1);
+    auto it = cache.find(key);
+    if (it != cache.end())
+        return it->second;
+    std::vector<float2> h(Y);
+    for (int j = 0; j < N2; j++)
+        for (int k1 = 0; k1 < N1; k1++) {
+            const long m = (long(j) * k1) % Y;
+            const double ang = -2.0 * M_PI * double(m) / double(Y);
+            h[j * N1 + k1] = float2{float(std::cos(ang)), float(std::sin(ang))};
+        }
+    float2* d;
+    CUDA_CHECK(cudaMalloc(&d, sizeof(float2) * Y));
+    CUDA_CHECK(cudaMemcpy(d, h.data(), sizeof(float2) * Y, cudaMemcpyHostToDevice));
+    cache[key] = d;
+    return d;
+}
+
+template<int N1, int N2, int W, int NSPLIT>
+void launch_fast(NormalArgs a, cfloat* p_out, long plane)
+{
+    auto kern = k_normal_fast<N1, N2, W, NSPLIT>;
+    constexpr size_t smem = fast_smem_bytes<N1, N2, W>();
+    allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
+    const long nxb = (a.X + W - 1) / W;
+    const double xyb = double(a.X) * a.Y * a.B;
+    const double work = 8.0 * xyb * (a.C + (a.mode == 1 ? 4 : 2));
+    ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
+    kern<<<unsigned(nxb * a.B * NSPLIT), W * N2, smem, ctx().stream>>>(a, fast_twiddles(N1, N2), p_out, plane);
+    KERNEL_CHECK();
+}
+
+// (N1, N2) factorisation of Y handled by the register-resident kernel, or 0
+int fast_n1(long Y)
+{
+    switch (Y) {
+    case 128: case 256: case 320: case 368: case 512: case 640:
+        return Y == 128 ? 8 : 16;
+    default:
+        return 0;
+    }
+}
+
+template<int NSPLIT>
+bool dispatch_fast(NormalArgs a, cfloat* p_out, long plane)
+{
+    constexpr int W = 8;
+    switch (a.Y) {
+    case 128: launch_fast<8, 16, W, NSPLIT>(a, p_out, plane); return true;
+    case 256: launch_fast<16, 16, W, NSPLIT>(a, p_out, plane); return true;
+    case 320: launch_fast<16, 20, W, NSPLIT>(a, p_out, plane); return true;
+    case 368: launch_fast<16, 23, W, NSPLIT>(a, p_out, plane); return true;
+    case 512: launch_fast<16, 32, W, NSPLIT>(a, p_out, plane); return true;
+    case 640: launch_fast<16, 40, W, NSPLIT>(a, p_out, plane); return true;
+    default: return false;
+    }
+}
+
+long fast_ctas(const SenseGeom& g, int nsplit) { return ((g.X + 7) / 8) * g.B * nsplit; }
+
+// CG update with NSPLIT Ap planes: x += alpha p ; r -= alpha (sum of planes)
+__global__ void k_cg_update_planes(CgDev* st, int it, cfloat* x, cfloat* r, const cfloat* p, const cfloat* ap,
+                                   long n, int nplanes, long plane, unsigned* errflags)
+{
+    __shared__ float s_alpha;
+    if (threadIdx.x == 0)
+        s_alpha = cg_alpha(st, it, errflags);
+    __syncthreads();
+    const float al = s_alpha;
+    if (!(al > 0.f))
+        return;
+    double2 part{0, 0};
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+        float2 av = ap[i];
+        for (int s = 1; s < nplanes; s++) {
+            const float2 t = ap[i + s * plane];
+            av.x += t.x;
+            av.y += t.y;
+        }
+        float2 pv = p[i], xv = x[i], rv = r[i];
+        xv.x += al * pv.x;
+        xv.y += al * pv.y;
+        rv.x += -al * av.x;
+        rv.y += -al * av.y;
+        x[i] = xv;
+        r[i] = rv;
+        part.x += double(rv.x) * rv.x + double(rv.y) * rv.y;
+    }
+    part = block_sum2(part);
+    if (threadIdx.x == 0)
+        st->part_rr[blockIdx.x] = part;
+}

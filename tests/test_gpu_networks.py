@@ -43,6 +43,11 @@ def _run(lib, build, cfg, data, w):
     wanted = [k == ARG_WEIGHTS for _, k, _ in m.args]
     g = n.adjoint_all(oi, dy, wanted)
     grads = {a: g[i] for i, (a, k, _) in enumerate(m.args) if k == ARG_WEIGHTS}
+    # tangents (Nlop::derivative) along the first two weights' directions
+    for a, k, _ in [x for x in m.args if x[1] == ARG_WEIGHTS][:3]:
+        i = m.arg_index(a)
+        dx = crand(np.random.default_rng(7 + i), n.in_dims(i), 0.01)
+        grads["tangent:" + a] = n.derivative(oi, i, dx)
     return dict(zip(m.out_names, outs)), grads
 
 
