@@ -330,7 +330,8 @@ def roofline(lib, step_ms_total):
         pass
     tags = {"sense_normal_y_cg": "hbm", "sense_normal_y": "hbm", "fft": "hbm", "conv_fwd": "tensor",
             "conv_bwd_data": "tensor", "conv_bwd_weight": "tensor", "conv_tc_fwd": "tensor",
-            "conv_tc_bwd_data": "tensor", "conv_tc_bwd_weight": "tensor"}
+            "conv_tc_bwd_data": "tensor", "conv_tc_bwd_weight": "tensor", "conv_thin_fwd": "hbm",
+            "conv_thin_bwd_data": "hbm", "conv_thin_bwd_weight": "hbm", "bnblock_fwd": "hbm", "bnblock_bwd": "hbm"}
     rows = []
     for tag, bound in tags.items():
         n, ms, work = C.c_long(), C.c_double(), C.c_double()

@@ -67,7 +67,10 @@ const char* mdnn_last_error(void);
 const char* mdnn_backend(void);            /* "b200-sm100a" or "reference-cpu" */
 int mdnn_set_device(int device);           /* GPU build: selects device + stream */
 int mdnn_synchronize(void);
-int mdnn_set_option(const char* key, long value); /* e.g. "conv_tf32", "fused_sense" */
+/* "conv_tc" (1 = tcgen05 TF32 convolutions where supported, 0 = fp32 CUDA
+   cores), "conv_chlast" (1 = auto-layout convolutions keep multi-channel
+   activations channels-last; test hook for the thin-conv kernels) */
+int mdnn_set_option(const char* key, long value);
 /* the library's CUDA stream on the current device (cudaStream_t), so callers
    can order collectives / events with its kernels; NULL in the CPU shim */
 void* mdnn_stream(void);

@@ -157,6 +157,8 @@ int mdnn_set_option(const char* key, long value)
         std::string k = key ? key : "";
         if (k == "conv_tc")
             conv_tc_enable(value != 0);
+        else if (k == "conv_chlast")
+            conv_force_chlast(value != 0);
         else
             throw ConfigError("unknown option '" + k + "'");
     });

@@ -225,6 +225,10 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
         conv_tc_run(y, x, w, g, 0);
         return;
     }
+    if (conv_thin_supported(g)) {
+        conv_thin_run(y, x, w, g, 0);
+        return;
+    }
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cout + FG - 1) / FG)));
     const long XY = g.X * g.Y;
@@ -241,6 +245,10 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
         conv_tc_run(dx, dy, w, g, 1);
         return;
     }
+    if (conv_thin_supported(g)) {
+        conv_thin_run(dx, dy, w, g, 1);
+        return;
+    }
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cin + FG - 1) / FG)));
     const long XY = g.X * g.Y;
@@ -255,6 +263,10 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     check_geom(g);
     if (conv_tc_wgrad_supported(g.Cin, g.Cout, g.KX, g.KY)) {
         conv_tc_wgrad(dw, x, dy, g);
+        return;
+    }
+    if (conv_thin_supported(g)) {
+        conv_thin_wgrad(dw, x, dy, g);
         return;
     }
     const long KK = g.KX * g.KY;

@@ -559,6 +559,12 @@ void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom
 
 void conv_tc_enable(bool on) { g_tc_enabled = on; }
 
+namespace {
+bool g_force_chlast = false;
+}
+void conv_force_chlast(bool on) { g_force_chlast = on; }
+bool conv_chlast_forced() { return g_force_chlast; }
+
 // 3x3, 2*Cin in {64, 128} floats per pixel, 2*Cout in {64, 128}
 bool conv_tc_supported(long cin, long cout, long kx, long ky)
 {

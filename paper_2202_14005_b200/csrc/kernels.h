@@ -122,9 +122,16 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
 // tcgen05 TF32 implicit-GEMM path (conv_tc.cu) for 3x3 layers with 32/64 channels
 void conv_tc_enable(bool on);
+// test hook: auto-layout convs store multi-channel activations channels-last
+void conv_force_chlast(bool on);
+bool conv_chlast_forced();
 bool conv_tc_supported(long cin, long cout, long kx, long ky);
 void conv_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode);
 bool conv_tc_wgrad_supported(long cin, long cout, long kx, long ky);
+// thin layers (one side 1 channel, wide side CHLAST): conv_thin.cu
+bool conv_thin_supported(const ConvGeom& g);
+void conv_thin_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode);
+void conv_thin_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
 void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
 
 // ---- batch norm (bn.cu) ----------------------------------------------------------

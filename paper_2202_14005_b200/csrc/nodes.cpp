@@ -1235,7 +1235,7 @@ public:
         // channels-last storage for multi-channel activations: requested by the
         // builder (MoDL denoiser chain) or implied by the tensor-core path
         const bool tc = conv_tc_supported(g_.Cin, g_.Cout, g_.KX, g_.KY);
-        const bool chl = s.chlast_hint > 0 || (s.chlast_hint == 0 && tc);
+        const bool chl = s.chlast_hint > 0 || (s.chlast_hint == 0 && (tc || conv_chlast_forced()));
         g_.in_chlast = chl && g_.Cin > 1;
         g_.out_chlast = chl && g_.Cout > 1;
     }

@@ -14,13 +14,19 @@
 // registers.  S is double-buffered by coil parity: 2 barriers per coil.
 #pragma once
 
+template<int N1, int N2, int W>
+constexpr int fast_threads()
+{
+    return ((W * N2 + 31) / 32) * 32; // whole warps: block_sum2 needs full warps
+}
+
 template<int N1, int N2, int W, int NSPLIT>
-__global__ void __launch_bounds__(W* N2, 2)
+__global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
     k_normal_fast(NormalArgs a, const float2* __restrict__ tw, cfloat* __restrict__ p_out, long plane)
 {
     using namespace fftd;
     constexpr int Y = N1 * N2;
-    constexpr int NT = W * N2;
+    constexpr int NT = fast_threads<N1, N2, W>();
     extern __shared__ float2 dsm[];
     float2* S0 = dsm;                 // [2][N1 * N2 * W]
     float2* stw = S0 + 2 * Y * W;     // [Y]
@@ -30,14 +36,16 @@ __global__ void __launch_bounds__(W* N2, 2)
     __shared__ float2 s_lam;
 
     const int tid = threadIdx.x;
-    const int w = tid % W, j = tid / W;
+    const int w = tid % W, j0 = tid / W;
+    const bool active = j0 < N2;      // padding lanes only join barriers / reductions
+    const int j = active ? j0 : 0;
     const long nxb = (a.X + W - 1) / W;
     long blk = blockIdx.x;
     const int split = int(blk % NSPLIT);
     blk /= NSPLIT;
     const long x0 = (blk % nxb) * W, b = blk / nxb;
     const long xx = x0 + w;
-    const bool colok = xx < a.X;
+    const bool colok = active && xx < a.X;
     const long c_begin = a.C * split / NSPLIT, c_end = a.C * (split + 1) / NSPLIT;
     const float invY = 1.f / float(Y);
 
@@ -74,7 +82,8 @@ __global__ void __launch_bounds__(W* N2, 2)
                     p_out[gi] = v;
             }
         }
-        xs[y * W + w] = v;
+        if (active)
+            xs[y * W + w] = v;
     }
     __syncthreads();
 
@@ -95,9 +104,11 @@ __global__ void __launch_bounds__(W* N2, 2)
         for (int q = 0; q < N1; q++)
             v[q] = cmul(cv[q], xs[(j + N2 * q) * W + w]);
         dft_reg<N1, -1>(v);
+        if (active) {
 #pragma unroll
-        for (int k1 = 0; k1 < N1; k1++)
-            Sb[(k1 * N2 + j) * W + w] = k1 == 0 ? v[0] : cmul(v[k1], stw[j * N1 + k1]);
+            for (int k1 = 0; k1 < N1; k1++)
+                Sb[(k1 * N2 + j) * W + w] = k1 == 0 ? v[0] : cmul(v[k1], stw[j * N1 + k1]);
+        }
         __syncthreads();
         // ---- stage B: DFT over j, mask, inverse DFT over k2, conj twiddle
         if (tid < W * N1) {
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(W* N2, 2)
             o.x += lx.x;
             o.y += lx.y;
         }
-        if (colok) {
+        if (colok) { // padding lanes: colok false, part stays 0
             a.out[plane * split + img_base + a.X * y] = o;
             part.x += double(xv.x) * o.x + double(xv.y) * o.y;
             part.y += double(xv.y) * o.x - double(xv.x) * o.y;
@@ -196,7 +207,7 @@ void launch_fast(NormalArgs a, cfloat* p_out, long plane)
     const double xyb = double(a.X) * a.Y * a.B;
     const double work = 8.0 * xyb * (a.C + (a.mode == 1 ? 4 : 2));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    kern<<<unsigned(nxb * a.B * NSPLIT), W * N2, smem, ctx().stream>>>(a, fast_twiddles(N1, N2), p_out, plane);
+    kern<<<unsigned(nxb * a.B * NSPLIT), fast_threads<N1, N2, W>(), smem, ctx().stream>>>(a, fast_twiddles(N1, N2), p_out, plane);
     KERNEL_CHECK();
 }
 

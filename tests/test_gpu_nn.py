@@ -56,6 +56,29 @@ def test_conv_layer(gpu, ref, cin, cout, k, X, Y, B, bias, transposed):
     _check_node(ng, nr, ins, rng, CONV_TOL, mr.arg_names)
 
 
+@pytest.mark.parametrize("cin,cout,k,X,Y,B,bias", [
+    # one side single-channel, wide side channels-last: the thin-conv kernels
+    (1, 64, 3, 40, 36, 2, False), (64, 1, 3, 33, 20, 2, True), (1, 8, 5, 20, 17, 1, True),
+    (16, 1, 3, 17, 35, 3, False), (1, 32, 3, 64, 48, 1, False),
+    # multi-channel non-TC shape stored channels-last (CUDA-core CHLAST path)
+    (8, 8, 3, 20, 12, 2, False),
+])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_conv_layer_chlast(gpu, ref, cin, cout, k, X, Y, B, bias, transposed):
+    rng = np.random.default_rng(cin * 37 + cout + k)
+    in_dims = list(d16(X, Y, cin))
+    in_dims[15] = B
+    gpu.check(gpu.so.mdnn_set_option(b"conv_chlast", 1))
+    try:
+        mg = Model.conv_layer(gpu, "c", in_dims, (k, k), cout, transposed=transposed, bias=bias)
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"conv_chlast", 0))
+    mr = Model.conv_layer(ref, "c", in_dims, (k, k), cout, transposed=transposed, bias=bias)
+    ng, nr = mg.nlop, mr.nlop
+    ins = [crand(rng, nr.in_dims(i)) for i in range(nr.n_in)]
+    _check_node(ng, nr, ins, rng, CONV_TOL, mr.arg_names)
+
+
 def test_conv_tensor_core_vs_cuda_core(gpu):
     """The tcgen05 TF32 path agrees with the fp32 CUDA-core path within the
     TF32 budget (per pass: RN operands ~3e-4)."""
