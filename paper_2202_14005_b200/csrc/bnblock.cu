@@ -24,58 +24,124 @@ constexpr int kT = 256;
 
 __device__ __forceinline__ float maybe_round(float v, bool r) { return r ? sm100::to_tf32(v) : v; }
 
+// Thread mapping for all passes: a thread owns the channel pair (2l, 2l+1),
+// l = tid % (C/2), and reads / writes them as float2 from the Re and Im halves
+// of the pixel (warp-contiguous 8-byte accesses).  C/2 divides the block, so
+// the pair is fixed for a thread across its grid-stride pixel loop.
+struct Pair {
+    int tpp, l, pl, ppb; // threads per pixel, pair index, pixel lane, pixels per sweep
+    __device__ explicit Pair(int C)
+    {
+        tpp = C / 2;
+        l = threadIdx.x % tpp;
+        pl = threadIdx.x / tpp;
+        ppb = kT / tpp;
+    }
+};
+
+__device__ __forceinline__ float2 ld2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+__device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
+
+// fixed-order reduction of NV doubles per thread over the pixel lanes of each
+// pair; the pair's two channels land in part[(blk * C + c) * NV + j]
+template<int NV>
+__device__ void fold_lanes(double* __restrict__ part, double (&a)[2][NV], const Pair& q, int C)
+{
+    extern __shared__ double sh[];
+#pragma unroll
+    for (int k = 0; k < 2; k++)
+#pragma unroll
+        for (int j = 0; j < NV; j++)
+            sh[(threadIdx.x * 2 + k) * NV + j] = a[k][j];
+    __syncthreads();
+    if (threadIdx.x < C) {
+        const int c = threadIdx.x, l = c / 2, k = c % 2;
+        double r[NV];
+#pragma unroll
+        for (int j = 0; j < NV; j++)
+            r[j] = 0;
+        for (int lane = 0; lane < q.ppb; lane++)
+#pragma unroll
+            for (int j = 0; j < NV; j++)
+                r[j] += sh[((lane * q.tpp + l) * 2 + k) * NV + j];
+#pragma unroll
+        for (int j = 0; j < NV; j++)
+            part[(size_t(blockIdx.x) * C + c) * NV + j] = r[j];
+    }
+}
+
+// block-per-channel fixed-order tree over the per-block partials
+template<int NV>
+__device__ void sum_partials(double (&r)[NV], const double* __restrict__ part, int nblocks, int C, int c)
+{
+    __shared__ double s[NV][kT];
+    double a[NV];
+#pragma unroll
+    for (int j = 0; j < NV; j++)
+        a[j] = 0;
+    for (int k = threadIdx.x; k < nblocks; k += kT)
+#pragma unroll
+        for (int j = 0; j < NV; j++)
+            a[j] += part[(size_t(k) * C + c) * NV + j];
+#pragma unroll
+    for (int j = 0; j < NV; j++)
+        s[j][threadIdx.x] = a[j];
+    __syncthreads();
+    for (int h = kT / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h)
+#pragma unroll
+            for (int j = 0; j < NV; j++)
+                s[j][threadIdx.x] += s[j][threadIdx.x + h];
+        __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < NV; j++)
+        r[j] = s[j][0];
+}
+
 // pass 1 forward: per block partial [Sum Re, Sum Im, Sum |x|^2] per channel
 __global__ void __launch_bounds__(kT) k_stats(double* __restrict__ part, const float* __restrict__ x, long npix,
                                               int C, long pix_per_block)
 {
-    extern __shared__ double sh[];
-    const int ppb = kT / C; // pixels per sweep (C divides 256)
-    const int c = threadIdx.x % C, pl = threadIdx.x / C;
+    const Pair q(C);
     const long p0 = long(blockIdx.x) * pix_per_block, p1 = min(npix, p0 + pix_per_block);
-    double sr = 0, si = 0, sq = 0;
-    for (long p = p0 + pl; p < p1; p += ppb) {
-        const float re = x[p * 2 * C + c], im = x[p * 2 * C + C + c];
-        sr += re;
-        si += im;
-        sq += double(re) * re + double(im) * im;
-    }
-    // reduce over the ppb pixel lanes of each channel (fixed order)
-    double* s = sh;
-    s[threadIdx.x * 3 + 0] = sr;
-    s[threadIdx.x * 3 + 1] = si;
-    s[threadIdx.x * 3 + 2] = sq;
-    __syncthreads();
-    if (threadIdx.x < C) {
-        double a = 0, b = 0, q = 0;
-        for (int k = 0; k < ppb; k++) {
-            a += s[(k * C + c) * 3 + 0];
-            b += s[(k * C + c) * 3 + 1];
-            q += s[(k * C + c) * 3 + 2];
+    double a[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    constexpr int U = 4;
+    for (long p = p0 + q.pl; p < p1; p += U * q.ppb) {
+        float2 re[U], im[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const long pp = p + u * q.ppb;
+            re[u] = pp < p1 ? ld2(x + pp * 2 * C + 2 * q.l) : float2{0.f, 0.f};
+            im[u] = pp < p1 ? ld2(x + pp * 2 * C + C + 2 * q.l) : float2{0.f, 0.f};
         }
-        double* dst = part + (size_t(blockIdx.x) * C + c) * 3;
-        dst[0] = a;
-        dst[1] = b;
-        dst[2] = q;
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            a[0][0] += re[u].x;
+            a[0][1] += im[u].x;
+            a[0][2] += double(re[u].x) * re[u].x + double(im[u].x) * im[u].x;
+            a[1][0] += re[u].y;
+            a[1][1] += im[u].y;
+            a[1][2] += double(re[u].y) * re[u].y + double(im[u].y) * im[u].y;
+        }
     }
+    fold_lanes<3>(part, a, q, C);
 }
 
-// final: mean, var (biased), istd, moving statistics
-__global__ void k_stats_final(float2* __restrict__ mu, float* __restrict__ istd, float2* __restrict__ mean_out,
-                              float2* __restrict__ var_out, const double* __restrict__ part, int nblocks, int C,
-                              long m, const float2* __restrict__ mean_in, const float2* __restrict__ var_in,
-                              float eps, float mom)
+// final: mean, var (biased), istd, moving statistics; one block per channel
+__global__ void __launch_bounds__(kT) k_stats_final(float2* __restrict__ mu, float* __restrict__ istd,
+                                                    float2* __restrict__ mean_out, float2* __restrict__ var_out,
+                                                    const double* __restrict__ part, int nblocks, int C, long m,
+                                                    const float2* __restrict__ mean_in,
+                                                    const float2* __restrict__ var_in, float eps, float mom)
 {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C)
+    const int c = blockIdx.x;
+    double r[3];
+    sum_partials<3>(r, part, nblocks, C, c);
+    if (threadIdx.x != 0)
         return;
-    double a = 0, b = 0, q = 0;
-    for (int k = 0; k < nblocks; k++) {
-        a += part[(size_t(k) * C + c) * 3 + 0];
-        b += part[(size_t(k) * C + c) * 3 + 1];
-        q += part[(size_t(k) * C + c) * 3 + 2];
-    }
-    const double mr = a / double(m), mi = b / double(m);
-    const double var = q / double(m) - (mr * mr + mi * mi);
+    const double mr = r[0] / double(m), mi = r[1] / double(m);
+    const double var = r[2] / double(m) - (mr * mr + mi * mi);
     const float meanr = float(mr), meani = float(mi), v = float(var > 0 ? var : 0);
     mu[c] = float2{meanr, meani};
     istd[c] = 1.f / sqrtf(v + eps);
@@ -87,23 +153,60 @@ __global__ void k_stats_final(float2* __restrict__ mu, float* __restrict__ istd,
     }
 }
 
+struct ChanCoef {
+    float2 m, g, bb;
+    float s;
+};
+
+__device__ __forceinline__ ChanCoef coef(const float2* mu, const float* istd, const float2* gamma,
+                                         const float2* beta, int c)
+{
+    return ChanCoef{mu[c], gamma[c], beta[c], istd[c]};
+}
+
+// yhat = (x - mu) istd ; z = g yhat + beta
+__device__ __forceinline__ void bn_z(const ChanCoef& k, float xr, float xi, float& hr, float& hi, float& zr,
+                                     float& zi)
+{
+    hr = (xr - k.m.x) * k.s;
+    hi = (xi - k.m.y) * k.s;
+    zr = k.g.x * hr - k.g.y * hi + k.bb.x;
+    zi = k.g.x * hi + k.g.y * hr + k.bb.y;
+}
+
 // pass 2 forward: out = crelu(g * (x - mu) * istd + beta)
 __global__ void __launch_bounds__(kT) k_apply(float* __restrict__ out, const float* __restrict__ x,
                                               const float2* __restrict__ mu, const float* __restrict__ istd,
                                               const float2* __restrict__ gamma, const float2* __restrict__ beta,
                                               long npix, int C, bool rnd)
 {
-    const long n = npix * C;
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-        const int c = int(i % C);
-        const long p = i / C;
-        const float xr = x[p * 2 * C + c], xi = x[p * 2 * C + C + c];
-        const float2 m = mu[c], g = gamma[c], bb = beta[c];
-        const float s = istd[c];
-        const float hr = (xr - m.x) * s, hi = (xi - m.y) * s;
-        float zr = g.x * hr - g.y * hi + bb.x, zi = g.x * hi + g.y * hr + bb.y;
-        out[p * 2 * C + c] = maybe_round(zr > 0.f ? zr : 0.f, rnd);
-        out[p * 2 * C + C + c] = maybe_round(zi > 0.f ? zi : 0.f, rnd);
+    const int tpp = C / 2, l = threadIdx.x % tpp;
+    const ChanCoef k0 = coef(mu, istd, gamma, beta, 2 * l), k1 = coef(mu, istd, gamma, beta, 2 * l + 1);
+    const long pstride = long(gridDim.x) * kT / tpp;
+    constexpr int U = 2;
+    for (long p = (long(blockIdx.x) * kT + threadIdx.x) / tpp; p < npix; p += U * pstride) {
+        float2 re[U], im[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const long pp = p + u * pstride;
+            if (pp < npix) {
+                re[u] = ld2(x + pp * 2 * C + 2 * l);
+                im[u] = ld2(x + pp * 2 * C + C + 2 * l);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const long pp = p + u * pstride;
+            if (pp >= npix)
+                break;
+            float hr, hi, z0r, z0i, z1r, z1i;
+            bn_z(k0, re[u].x, im[u].x, hr, hi, z0r, z0i);
+            bn_z(k1, re[u].y, im[u].y, hr, hi, z1r, z1i);
+            st2(out + pp * 2 * C + 2 * l,
+                float2{maybe_round(fmaxf(z0r, 0.f), rnd), maybe_round(fmaxf(z1r, 0.f), rnd)});
+            st2(out + pp * 2 * C + C + 2 * l,
+                float2{maybe_round(fmaxf(z0i, 0.f), rnd), maybe_round(fmaxf(z1i, 0.f), rnd)});
+        }
     }
 }
 
@@ -114,55 +217,53 @@ __global__ void __launch_bounds__(kT) k_bwd_reduce(double* __restrict__ part, co
                                                    const float2* __restrict__ beta, long npix, int C,
                                                    long pix_per_block)
 {
-    extern __shared__ double sh[];
-    const int ppb = kT / C;
-    const int c = threadIdx.x % C, pl = threadIdx.x / C;
+    const Pair q(C);
+    const ChanCoef kc[2] = {coef(mu, istd, gamma, beta, 2 * q.l), coef(mu, istd, gamma, beta, 2 * q.l + 1)};
     const long p0 = long(blockIdx.x) * pix_per_block, p1 = min(npix, p0 + pix_per_block);
-    const float2 m = mu[c], g = gamma[c], bb = beta[c];
-    const float s = istd[c];
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-    for (long p = p0 + pl; p < p1; p += ppb) {
-        const float xr = x[p * 2 * C + c], xi = x[p * 2 * C + C + c];
-        const float hr = (xr - m.x) * s, hi = (xi - m.y) * s;
-        const float zr = g.x * hr - g.y * hi + bb.x, zi = g.x * hi + g.y * hr + bb.y;
-        const float gr = zr > 0.f ? gout[p * 2 * C + c] : 0.f;
-        const float gi = zi > 0.f ? gout[p * 2 * C + C + c] : 0.f;
-        a0 += gr;
-        a1 += gi;
-        // gz * conj(yhat)
-        a2 += double(gr) * hr + double(gi) * hi;
-        a3 += double(gi) * hr - double(gr) * hi;
+    double a[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    constexpr int U = 2;
+    for (long p = p0 + q.pl; p < p1; p += U * q.ppb) {
+        float2 xr[U], xi[U], gr[U], gi[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const long pp = p + u * q.ppb;
+            const bool ok = pp < p1;
+            xr[u] = ok ? ld2(x + pp * 2 * C + 2 * q.l) : float2{0.f, 0.f};
+            xi[u] = ok ? ld2(x + pp * 2 * C + C + 2 * q.l) : float2{0.f, 0.f};
+            gr[u] = ok ? ld2(gout + pp * 2 * C + 2 * q.l) : float2{0.f, 0.f};
+            gi[u] = ok ? ld2(gout + pp * 2 * C + C + 2 * q.l) : float2{0.f, 0.f};
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                float hr, hi, zr, zi;
+                bn_z(kc[k], k ? xr[u].y : xr[u].x, k ? xi[u].y : xi[u].x, hr, hi, zr, zi);
+                const float g_r = zr > 0.f ? (k ? gr[u].y : gr[u].x) : 0.f;
+                const float g_i = zi > 0.f ? (k ? gi[u].y : gi[u].x) : 0.f;
+                a[k][0] += g_r;
+                a[k][1] += g_i;
+                // gz * conj(yhat)
+                a[k][2] += double(g_r) * hr + double(g_i) * hi;
+                a[k][3] += double(g_i) * hr - double(g_r) * hi;
+            }
+        }
     }
-    double* s4 = sh;
-    s4[threadIdx.x * 4 + 0] = a0;
-    s4[threadIdx.x * 4 + 1] = a1;
-    s4[threadIdx.x * 4 + 2] = a2;
-    s4[threadIdx.x * 4 + 3] = a3;
-    __syncthreads();
-    if (threadIdx.x < C) {
-        double r[4] = {0, 0, 0, 0};
-        for (int k = 0; k < ppb; k++)
-            for (int j = 0; j < 4; j++)
-                r[j] += s4[(k * C + c) * 4 + j];
-        double* dst = part + (size_t(blockIdx.x) * C + c) * 4;
-        for (int j = 0; j < 4; j++)
-            dst[j] = r[j];
-    }
+    fold_lanes<4>(part, a, q, C);
 }
 
-// final backward: dbeta = S1, dgamma = S2, and the per-channel coefficients
+// final backward (block per channel): dbeta = S1, dgamma = S2, and the coefficients
 //   gm = conj(g) S1 / m ;  fh = -Re(conj(g) S2) * istd / m   (dx = (gyh - gm) istd + yhat * fh)
-__global__ void k_bwd_final(float2* __restrict__ dbeta, float2* __restrict__ dgamma, float2* __restrict__ gm,
-                            float* __restrict__ fh, const double* __restrict__ part, int nblocks, int C, long m,
-                            const float2* __restrict__ gamma, const float* __restrict__ istd)
+__global__ void __launch_bounds__(kT) k_bwd_final(float2* __restrict__ dbeta, float2* __restrict__ dgamma,
+                                                  float2* __restrict__ gm, float* __restrict__ fh,
+                                                  const double* __restrict__ part, int nblocks, int C, long m,
+                                                  const float2* __restrict__ gamma, const float* __restrict__ istd)
 {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= C)
+    const int c = blockIdx.x;
+    double r[4];
+    sum_partials<4>(r, part, nblocks, C, c);
+    if (threadIdx.x != 0)
         return;
-    double r[4] = {0, 0, 0, 0};
-    for (int k = 0; k < nblocks; k++)
-        for (int j = 0; j < 4; j++)
-            r[j] += part[(size_t(k) * C + c) * 4 + j];
     if (dbeta)
         dbeta[c] = float2{float(r[0]), float(r[1])};
     if (dgamma)
@@ -183,21 +284,29 @@ __global__ void __launch_bounds__(kT) k_bwd_apply(float* __restrict__ dx, const 
                                                   const float2* __restrict__ beta, const float2* __restrict__ gm,
                                                   const float* __restrict__ fh, long npix, int C, bool rnd)
 {
-    const long n = npix * C;
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-        const int c = int(i % C);
-        const long p = i / C;
-        const float xr = x[p * 2 * C + c], xi = x[p * 2 * C + C + c];
-        const float2 m = mu[c], g = gamma[c], bb = beta[c], gmc = gm[c];
-        const float s = istd[c], f = fh[c];
-        const float hr = (xr - m.x) * s, hi = (xi - m.y) * s;
-        const float zr = g.x * hr - g.y * hi + bb.x, zi = g.x * hi + g.y * hr + bb.y;
-        const float gr = zr > 0.f ? gout[p * 2 * C + c] : 0.f;
-        const float gi = zi > 0.f ? gout[p * 2 * C + C + c] : 0.f;
-        // gyh = gz * conj(g)
-        const float yr = gr * g.x + gi * g.y, yi = gi * g.x - gr * g.y;
-        dx[p * 2 * C + c] = maybe_round((yr - gmc.x) * s + hr * f, rnd);
-        dx[p * 2 * C + C + c] = maybe_round((yi - gmc.y) * s + hi * f, rnd);
+    const int tpp = C / 2, l = threadIdx.x % tpp;
+    const ChanCoef kc[2] = {coef(mu, istd, gamma, beta, 2 * l), coef(mu, istd, gamma, beta, 2 * l + 1)};
+    const float2 gmc[2] = {gm[2 * l], gm[2 * l + 1]};
+    const float fc[2] = {fh[2 * l], fh[2 * l + 1]};
+    const long pstride = long(gridDim.x) * kT / tpp;
+    for (long p = (long(blockIdx.x) * kT + threadIdx.x) / tpp; p < npix; p += pstride) {
+        const float2 xr = ld2(x + p * 2 * C + 2 * l), xi = ld2(x + p * 2 * C + C + 2 * l);
+        const float2 gr2 = ld2(gout + p * 2 * C + 2 * l), gi2 = ld2(gout + p * 2 * C + C + 2 * l);
+        float o_r[2], o_i[2];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            float hr, hi, zr, zi;
+            bn_z(kc[k], k ? xr.y : xr.x, k ? xi.y : xi.x, hr, hi, zr, zi);
+            const float g_r = zr > 0.f ? (k ? gr2.y : gr2.x) : 0.f;
+            const float g_i = zi > 0.f ? (k ? gi2.y : gi2.x) : 0.f;
+            const float2 g = kc[k].g;
+            // gyh = gz * conj(g)
+            const float yr = g_r * g.x + g_i * g.y, yi = g_i * g.x - g_r * g.y;
+            o_r[k] = maybe_round((yr - gmc[k].x) * kc[k].s + hr * fc[k], rnd);
+            o_i[k] = maybe_round((yi - gmc[k].y) * kc[k].s + hi * fc[k], rnd);
+        }
+        st2(dx + p * 2 * C + 2 * l, float2{o_r[0], o_r[1]});
+        st2(dx + p * 2 * C + C + 2 * l, float2{o_i[0], o_i[1]});
     }
 }
 
@@ -207,10 +316,10 @@ int reduce_blocks(long npix)
     return int(std::max(1L, std::min(b, (npix + 255) / 256)));
 }
 
-int grid_ew(long n)
+int grid_ew(long npix, int C)
 {
-    long b = (n + kT - 1) / kT;
-    return int(std::max(1L, std::min(b, long(ctx().sm_count) * 16)));
+    long b = (npix * (C / 2) + kT - 1) / kT;
+    return int(std::max(1L, std::min(b, long(ctx().sm_count) * 8)));
 }
 
 } // namespace
@@ -220,19 +329,19 @@ void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, floa
                      int C, float eps, float mom, bool round_tf32)
 {
     auto& c = ctx();
-    if (256 % C != 0)
-        throw ConfigError("bnblock: channel count must divide 256");
+    if (C < 2 || 256 % C != 0)
+        throw ConfigError("bnblock: channel count must be >= 2 and divide 256");
     const int nb = reduce_blocks(npix);
     const long ppb = (npix + nb - 1) / nb;
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * 3 * C * nb, c.stream));
     ProfScope prof("bnblock_fwd", 8.0 * 2 * npix * C + 8.0 * npix * C);
-    k_stats<<<nb, kT, sizeof(double) * 3 * kT, c.stream>>>(part, x, npix, C, ppb);
+    k_stats<<<nb, kT, sizeof(double) * 2 * 3 * kT, c.stream>>>(part, x, npix, C, ppb);
     KERNEL_CHECK();
-    k_stats_final<<<(C + 63) / 64, 64, 0, c.stream>>>(mu, istd, mean_out, var_out, part, nb, C, npix, mean_in,
+    k_stats_final<<<C, kT, 0, c.stream>>>(mu, istd, mean_out, var_out, part, nb, C, npix, mean_in,
                                                        var_in, eps, mom);
     KERNEL_CHECK();
-    k_apply<<<grid_ew(npix * C), kT, 0, c.stream>>>(out, x, mu, istd, gamma, beta, npix, C, round_tf32);
+    k_apply<<<grid_ew(npix, C), kT, 0, c.stream>>>(out, x, mu, istd, gamma, beta, npix, C, round_tf32);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
@@ -250,12 +359,12 @@ void bnblock_backward(float* dx, float2* dgamma, float2* dbeta, const float* gou
     CUDA_CHECK(cudaMallocAsync(&gm, sizeof(float2) * C, c.stream));
     CUDA_CHECK(cudaMallocAsync(&fh, sizeof(float) * C, c.stream));
     ProfScope prof("bnblock_bwd", 8.0 * 5 * npix * C);
-    k_bwd_reduce<<<nb, kT, sizeof(double) * 4 * kT, c.stream>>>(part, gout, x, mu, istd, gamma, beta, npix, C, ppb);
+    k_bwd_reduce<<<nb, kT, sizeof(double) * 2 * 4 * kT, c.stream>>>(part, gout, x, mu, istd, gamma, beta, npix, C, ppb);
     KERNEL_CHECK();
-    k_bwd_final<<<(C + 63) / 64, 64, 0, c.stream>>>(dbeta, dgamma, gm, fh, part, nb, C, npix, gamma, istd);
+    k_bwd_final<<<C, kT, 0, c.stream>>>(dbeta, dgamma, gm, fh, part, nb, C, npix, gamma, istd);
     KERNEL_CHECK();
     if (dx) {
-        k_bwd_apply<<<grid_ew(npix * C), kT, 0, c.stream>>>(dx, gout, x, mu, istd, gamma, beta, gm, fh, npix, C,
+        k_bwd_apply<<<grid_ew(npix, C), kT, 0, c.stream>>>(dx, gout, x, mu, istd, gamma, beta, gm, fh, npix, C,
                                                             round_tf32);
         KERNEL_CHECK();
     }

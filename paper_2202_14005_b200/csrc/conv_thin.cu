@@ -1,14 +1,22 @@
 // "Thin" complex convolutions: one side has a single channel (MoDL's first
 // layer 1 -> F and last layer F -> 1, conv_layer nn.hpp:344-426).  The wide
 // side is channels-last (CHLAST), the thin side is a plain image (for one
-// channel the two layouts coincide).  These passes are memory-bound (9 complex
-// MACs per wide element), so every kernel streams the wide tensor once with
-// warp-contiguous channel accesses and keeps the thin image tile in smem.
+// channel the two layouts coincide).  With 9 complex MACs per wide element
+// these passes sit between the HBM and the FP32 roofline, so every kernel
+// streams the wide tensor exactly once, coalesced, and keeps the thin image in
+// shared memory:
 //
-//   expand  out[p, f] = sum_t thin[p + dir (t - c0)] * U[t, f]
-//   reduce  out[q]    = sum_{t, c} wide[q + dir (t - c0), c] * U[t, c]
-//   wgrad   dw[t, f]  = sum_p g[p, f] * conj(h[p + t - c0])   (one of g/h wide)
-// with U a per-launch packing of w (or its flipped conjugate for adjoints).
+//   expand  out[p, f] = sum_t thin[p + t - o] * U[t, f]
+//           thread = (channel f, row segment); U[., f] in registers; a K x K
+//           register window slides along x (K smem loads per output pixel).
+//   reduce  out[q]    = sum_t z_t[q + t - o],  z_t[h] = sum_c wide[h, c] U[t, c]
+//           per halo pixel the K^2 tap projections over all channels (channel
+//           chunks staged through smem, U broadcast), then a K^2 gather.
+//   wgrad   dw[t, f]  = sum_p g[p, f] conj(h[p + t - c0])  (one of g / h wide)
+//           persistent CTAs, thread = (channel, row segment), K^2 register
+//           accumulators, the thin operand as a sliding register window; per-CTA
+//           partials folded in a fixed order (bitwise run-to-run stable).
+// U is a per-launch packing of w (or its flipped conjugate for the adjoints).
 #include "kernels.h"
 #include "profile.h"
 
@@ -18,13 +26,13 @@ namespace mdnn {
 
 namespace {
 
-constexpr int TX = 32, TY = 8, MAXK = 5, MAXF = 256;
+constexpr int TX = 32, NT = 256, MAXF = 256;
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
 
 // U[t][f] for the 4 uses; w has dims [KX, KY, Cin, Cout]
 //   mode 0: fwd 1 -> F           U[t][f] = w[t, 0, f]
-//   mode 1: bwd-data of F -> 1   U[t][c] = conj(w[flip t, c, 0])   (expand with dir +1 on flipped taps)
+//   mode 1: bwd-data of F -> 1   U[t][c] = conj(w[flip t, c, 0])   (expand on flipped taps)
 //   mode 2: fwd F -> 1           U[t][c] = w[t, c, 0]
 //   mode 3: bwd-data of 1 -> F   U[t][f] = conj(w[flip t, 0, f])
 __global__ void k_pack_thin(float2* U, const float2* w, int KX, int KY, int F, int mode)
@@ -45,203 +53,344 @@ __global__ void k_pack_thin(float2* U, const float2* w, int KX, int KY, int F, i
     }
 }
 
-// thin -> wide, block = TX x TY pixel tile of one item; thread (f, pixel lane)
-__global__ void __launch_bounds__(256) k_thin_expand(float* __restrict__ out, const float2* __restrict__ in,
-                                                     const float2* __restrict__ U, int X, int Y, int F, int KX, int KY,
-                                                     int ox, int oy)
+// zero-padded halo of a one-channel image: tile[hy][hx] = img[x0 + hx - ox, y0 + hy - oy]
+template<int HX, int HY>
+__device__ __forceinline__ void load_halo(float2* tile, const float2* __restrict__ img, int X, int Y, long b, int x0,
+                                          int y0, int ox, int oy)
 {
-    __shared__ float2 tile[(TY + MAXK - 1) * (TX + MAXK - 1)];
-    extern __shared__ float2 su[]; // [KK][F]
-    const int KK = KX * KY;
-    const int HX = TX + KX - 1, HY = TY + KY - 1;
-    const long b = blockIdx.z;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const long XY = long(X) * Y;
     for (int e = threadIdx.x; e < HX * HY; e += blockDim.x) {
         const int hx = e % HX, hy = e / HX;
         const int gx = x0 + hx - ox, gy = y0 + hy - oy;
-        tile[e] = (gx >= 0 && gx < X && gy >= 0 && gy < Y) ? in[gx + long(X) * gy + XY * b] : float2{0.f, 0.f};
-    }
-    for (int e = threadIdx.x; e < KK * F; e += blockDim.x)
-        su[e] = U[e];
-    __syncthreads();
-    const int lanes = blockDim.x / F; // pixels processed concurrently
-    const int f = threadIdx.x % F, pl = threadIdx.x / F;
-    if (pl >= lanes)
-        return;
-    for (int pix = pl; pix < TX * TY; pix += lanes) {
-        const int px = pix % TX, py = pix / TX;
-        const int gx = x0 + px, gy = y0 + py;
-        if (gx >= X || gy >= Y)
-            continue;
-        float2 acc{0.f, 0.f};
-        for (int ky = 0; ky < KY; ky++)
-            for (int kx = 0; kx < KX; kx++) {
-                const float2 t = cmul(tile[(py + ky) * HX + px + kx], su[(kx + KX * ky) * F + f]);
-                acc.x += t.x;
-                acc.y += t.y;
-            }
-        float* dst = out + ((b * XY) + gx + long(X) * gy) * 2 * F;
-        dst[f] = acc.x;
-        dst[F + f] = acc.y;
+        tile[e] = (gx >= 0 && gx < X && gy >= 0 && gy < Y) ? img[gx + long(X) * gy + XY * b] : float2{0.f, 0.f};
     }
 }
 
-// wide -> thin, one output pixel per thread; channels streamed in chunks of CC
-constexpr int CC = 8;
-__global__ void __launch_bounds__(TX* TY) k_thin_reduce(float2* __restrict__ out, const float* __restrict__ in,
-                                                        const float2* __restrict__ U, int X, int Y, int F, int KX,
-                                                        int KY, int ox, int oy)
+// thin -> wide.  Block = TX x TY pixel tile of one item.
+template<int K>
+__global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, const float2* __restrict__ in,
+                                                    const float2* __restrict__ U, int X, int Y, int F, int ox, int oy)
 {
-    __shared__ float2 tile[(TY + MAXK - 1) * (TX + MAXK - 1) * CC];
-    __shared__ float2 su[MAXK * MAXK * CC];
-    const int KK = KX * KY;
-    const int HX = TX + KX - 1, HY = TY + KY - 1;
+    constexpr int TY = 8, HX = TX + K - 1, HY = TY + K - 1;
+    __shared__ float2 tile[HX * HY];
     const long b = blockIdx.z;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const long XY = long(X) * Y;
-    const int px = threadIdx.x % TX, py = threadIdx.x / TX;
-    float2 acc{0.f, 0.f};
-    for (int c0 = 0; c0 < F; c0 += CC) {
-        const int nc = min(CC, F - c0);
-        __syncthreads();
-        for (int e = threadIdx.x; e < HX * HY * CC; e += blockDim.x) {
-            const int cc = e % CC, hp = e / CC;
-            const int hx = hp % HX, hy = hp / HX;
-            const int gx = x0 + hx - ox, gy = y0 + hy - oy;
-            float2 v{0.f, 0.f};
-            if (cc < nc && gx >= 0 && gx < X && gy >= 0 && gy < Y) {
-                const float* src = in + ((b * XY) + gx + long(X) * gy) * 2 * F;
-                v = float2{src[c0 + cc], src[F + c0 + cc]};
-            }
-            tile[hp * CC + cc] = v;
-        }
-        for (int e = threadIdx.x; e < KK * CC; e += blockDim.x) {
-            const int cc = e % CC, t = e / CC;
-            su[e] = cc < nc ? U[t * F + c0 + cc] : float2{0.f, 0.f};
-        }
-        __syncthreads();
-        for (int ky = 0; ky < KY; ky++)
-            for (int kx = 0; kx < KX; kx++) {
-                const float2* tp = tile + ((py + ky) * HX + px + kx) * CC;
-                const float2* up = su + (kx + KX * ky) * CC;
+    load_halo<HX, HY>(tile, in, X, Y, b, x0, y0, ox, oy);
+    const int f = threadIdx.x % F, lane = threadIdx.x / F, lanes = NT / F;
+    float2 u[K * K];
 #pragma unroll
-                for (int cc = 0; cc < CC; cc++) {
-                    const float2 t = cmul(tp[cc], up[cc]);
+    for (int t = 0; t < K * K; t++)
+        u[t] = U[t * F + f];
+    __syncthreads();
+    const int nseg = max(1, lanes / TY), seglen = TX / nseg;
+    for (int it = lane; it < TY * nseg; it += lanes) {
+        const int row = it / nseg, xs = (it % nseg) * seglen;
+        const int gy = y0 + row;
+        if (gy >= Y)
+            continue;
+        float2 win[K][K];
+#pragma unroll
+        for (int ky = 0; ky < K; ky++)
+#pragma unroll
+            for (int kx = 0; kx < K - 1; kx++)
+                win[ky][kx] = tile[(row + ky) * HX + xs + kx];
+        float* rowp = out + (b * XY + long(X) * gy) * 2 * F;
+        for (int i = 0; i < seglen; i++) {
+            const int px = xs + i;
+#pragma unroll
+            for (int ky = 0; ky < K; ky++)
+                win[ky][K - 1] = tile[(row + ky) * HX + px + K - 1];
+            float2 acc{0.f, 0.f};
+#pragma unroll
+            for (int ky = 0; ky < K; ky++)
+#pragma unroll
+                for (int kx = 0; kx < K; kx++) {
+                    const float2 t = cmul(win[ky][kx], u[kx + K * ky]);
                     acc.x += t.x;
                     acc.y += t.y;
                 }
+            const int gx = x0 + px;
+            if (gx < X) {
+                rowp[long(gx) * 2 * F + f] = acc.x;
+                rowp[long(gx) * 2 * F + F + f] = acc.y;
             }
+#pragma unroll
+            for (int ky = 0; ky < K; ky++)
+#pragma unroll
+                for (int kx = 0; kx < K - 1; kx++)
+                    win[ky][kx] = win[ky][kx + 1];
+        }
     }
-    const int gx = x0 + px, gy = y0 + py;
-    if (gx < X && gy < Y)
-        out[(b * XY) + gx + long(X) * gy] = acc;
 }
 
-// weight gradient with one thin operand.  g is the "dy" side, h the "x" side:
-//   dw[t, f] = sum_p g[p, f] conj(h[p + t - c0, f])   (the wide side carries f)
-// thin_is_h: h is the 1-channel image (1 -> F layer), else g is (F -> 1 layer).
-// Block = pixel tile; thread (f, lane); K^2 accumulators per thread; partials
-// per block [block][t][f] reduced in fixed order by k_thin_wsum.
-__global__ void __launch_bounds__(256) k_thin_wgrad(float2* __restrict__ part, const float2* __restrict__ g_thin,
-                                                    const float* __restrict__ g_wide, const float2* __restrict__ h_thin,
-                                                    const float* __restrict__ h_wide, int X, int Y, int F, int KX,
-                                                    int KY, int c0x, int c0y, bool thin_is_h)
+// wide -> thin.  Output tile TX x TY; halo pixels h own the K^2 tap projections.
+constexpr int RCC = 8; // channels per smem chunk
+template<int K>
+struct ReduceCfg {
+    static constexpr int TY = K == 3 ? 16 : 8;
+    static constexpr int HX = TX + K - 1, HY = TY + K - 1, NH = HX * HY, KK = K * K;
+    static constexpr int PP = (NH + NT - 1) / NT; // halo pixels per thread
+    static constexpr int PITCH = 2 * RCC + 1;     // conflict-free per-pixel rows
+    static constexpr int IN_FLOATS = ((NH * PITCH + 1) / 2) * 2;
+    static constexpr int Z_FLOATS = NH * KK * 2;
+    static constexpr size_t smem()
+    {
+        return sizeof(float) * (IN_FLOATS > Z_FLOATS ? IN_FLOATS : Z_FLOATS) + sizeof(float2) * KK * RCC;
+    }
+};
+
+template<int K>
+__global__ void __launch_bounds__(NT) k_thin_reduce(float2* __restrict__ out, const float* __restrict__ in,
+                                                    const float2* __restrict__ U, int X, int Y, int F, int ox, int oy)
 {
-    __shared__ float2 tile[(TY + MAXK - 1) * (TX + MAXK - 1)];
-    const int KK = KX * KY;
-    const int HX = TX + KX - 1, HY = TY + KY - 1;
+    using Cfg = ReduceCfg<K>;
+    constexpr int HX = Cfg::HX, NH = Cfg::NH, KK = Cfg::KK, PP = Cfg::PP, PITCH = Cfg::PITCH, TY = Cfg::TY;
+    extern __shared__ float smr[];
+    float* sin = smr;                                     // [NH][PITCH]   (phase 1)
+    float2* z = reinterpret_cast<float2*>(smr);           // [NH][KK]      (phase 2, aliases sin)
+    constexpr int ZOFF = Cfg::IN_FLOATS > Cfg::Z_FLOATS ? Cfg::IN_FLOATS : Cfg::Z_FLOATS;
+    float2* su = reinterpret_cast<float2*>(smr + ZOFF);   // [KK][RCC]
     const long b = blockIdx.z;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const long XY = long(X) * Y;
-    // thin operand tile: for thin h, the halo of h; for thin g, just the tile (no halo)
-    if (thin_is_h) {
-        for (int e = threadIdx.x; e < HX * HY; e += blockDim.x) {
-            const int hx = e % HX, hy = e / HX;
-            const int gx = x0 + hx - c0x, gy = y0 + hy - c0y;
-            tile[e] = (gx >= 0 && gx < X && gy >= 0 && gy < Y) ? h_thin[gx + long(X) * gy + XY * b] : float2{0.f, 0.f};
+    float2 acc[PP][KK];
+#pragma unroll
+    for (int k = 0; k < PP; k++)
+#pragma unroll
+        for (int t = 0; t < KK; t++)
+            acc[k][t] = float2{0.f, 0.f};
+    for (int c0 = 0; c0 < F; c0 += RCC) {
+        const int nc = min(RCC, F - c0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < NH * 2 * RCC; e += NT) {
+            const int cc = e % RCC, part = (e / RCC) & 1, h = e / (2 * RCC);
+            const int hx = h % HX, hy = h / HX;
+            const int gx = x0 + hx - ox, gy = y0 + hy - oy;
+            float v = 0.f;
+            if (cc < nc && gx >= 0 && gx < X && gy >= 0 && gy < Y)
+                v = in[(b * XY + gx + long(X) * gy) * 2 * F + part * F + c0 + cc];
+            sin[h * PITCH + part * RCC + cc] = v;
         }
-    } else {
-        for (int e = threadIdx.x; e < TX * TY; e += blockDim.x) {
-            const int gx = x0 + e % TX, gy = y0 + e / TX;
-            tile[e] = (gx < X && gy < Y) ? g_thin[gx + long(X) * gy + XY * b] : float2{0.f, 0.f};
+        for (int e = threadIdx.x; e < KK * RCC; e += NT) {
+            const int t = e / RCC, cc = e % RCC;
+            su[e] = cc < nc ? U[t * F + c0 + cc] : float2{0.f, 0.f};
         }
-    }
-    __syncthreads();
-    const int lanes = blockDim.x / F;
-    const int f = threadIdx.x % F, pl = threadIdx.x / F;
-    constexpr int NA = MAXK * MAXK;
-    float2 acc[NA];
+        __syncthreads();
+#pragma unroll 2
+        for (int cc = 0; cc < RCC; cc++) {
+            float2 v[PP];
 #pragma unroll
-    for (int t = 0; t < NA; t++)
-        acc[t] = float2{0.f, 0.f};
-    if (pl < lanes) {
-        for (int pix = pl; pix < TX * TY; pix += lanes) {
-            const int px = pix % TX, py = pix / TX;
-            const int gx = x0 + px, gy = y0 + py;
-            if (gx >= X || gy >= Y)
-                continue;
-            if (thin_is_h) {
-                const float* gw = g_wide + ((b * XY) + gx + long(X) * gy) * 2 * F;
-                const float2 gv{gw[f], gw[F + f]};
+            for (int k = 0; k < PP; k++) {
+                const int h = threadIdx.x + k * NT;
+                v[k] = h < NH ? float2{sin[h * PITCH + cc], sin[h * PITCH + RCC + cc]} : float2{0.f, 0.f};
+            }
 #pragma unroll
-                for (int t = 0; t < NA; t++) {
-                    if (t >= KK)
-                        break;
-                    const int kx = t % KX, ky = t / KX;
-                    const float2 hv = tile[(py + ky) * HX + px + kx];
-                    acc[t].x += gv.x * hv.x + gv.y * hv.y;
-                    acc[t].y += gv.y * hv.x - gv.x * hv.y;
-                }
-            } else {
-                const float2 gv = tile[py * TX + px];
+            for (int t = 0; t < KK; t++) {
+                const float2 uu = su[t * RCC + cc];
 #pragma unroll
-                for (int t = 0; t < NA; t++) {
-                    if (t >= KK)
-                        break;
-                    const int kx = t % KX, ky = t / KX;
-                    const int hx = gx + kx - c0x, hy = gy + ky - c0y;
-                    if (hx < 0 || hx >= X || hy < 0 || hy >= Y)
-                        continue;
-                    const float* hw = h_wide + ((b * XY) + hx + long(X) * hy) * 2 * F;
-                    const float2 hv{hw[f], hw[F + f]};
-                    acc[t].x += gv.x * hv.x + gv.y * hv.y;
-                    acc[t].y += gv.y * hv.x - gv.x * hv.y;
+                for (int k = 0; k < PP; k++) {
+                    acc[k][t].x += v[k].x * uu.x - v[k].y * uu.y;
+                    acc[k][t].y += v[k].x * uu.y + v[k].y * uu.x;
                 }
             }
         }
     }
-    // reduce the pixel lanes of each f in fixed order through smem
-    extern __shared__ float2 sred[]; // [lanes][KK][F]
-    if (pl < lanes)
-        for (int t = 0; t < KK && t < NA; t++)
-            sred[(pl * KK + t) * F + f] = acc[t];
     __syncthreads();
-    const long blk = (long(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    for (int e = threadIdx.x; e < KK * F; e += blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < PP; k++) {
+        const int h = threadIdx.x + k * NT;
+        if (h < NH)
+#pragma unroll
+            for (int t = 0; t < KK; t++)
+                z[h * KK + t] = acc[k][t];
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < TX * TY; q += NT) {
+        const int px = q % TX, py = q / TX;
+        const int gx = x0 + px, gy = y0 + py;
+        float2 s{0.f, 0.f};
+#pragma unroll
+        for (int ky = 0; ky < K; ky++)
+#pragma unroll
+            for (int kx = 0; kx < K; kx++) {
+                const float2 v = z[((py + ky) * HX + px + kx) * KK + kx + K * ky];
+                s.x += v.x;
+                s.y += v.y;
+            }
+        if (gx < X && gy < Y)
+            out[b * XY + gx + long(X) * gy] = s;
+    }
+}
+
+// Weight gradient with one thin operand; persistent CTAs over TX x 8 tiles.
+//   WIDE_IS_G (1 -> F layer, g = dy wide, h = x thin):
+//       acc[t] += g[p, f] conj(h[p + t - c0]),  window over h with offset c0
+//   else (F -> 1 layer, g = dy thin, h = x wide), substituting p' = p + t - c0:
+//       acc[t] += g[p' - t + c0] conj(h[p', c]), window over g with offset K-1-c0
+//       and flipped tap index.
+template<int K, bool WIDE_IS_G>
+__global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, const float* __restrict__ wide,
+                                                   const float2* __restrict__ thin, int X, int Y, int B, int F,
+                                                   int ox, int oy)
+{
+    constexpr int TY = 8, HX = TX + K - 1, HY = TY + K - 1, KK = K * K;
+    __shared__ float2 tile[HX * HY];
+    extern __shared__ float2 sred[]; // [lanes][KK][F] = NT * KK float2
+    const long XY = long(X) * Y;
+    const int ntx = (X + TX - 1) / TX, nty = (Y + TY - 1) / TY;
+    const long ntiles = long(ntx) * nty * B;
+    const int f = threadIdx.x % F, lane = threadIdx.x / F, lanes = NT / F;
+    const int nseg = max(1, lanes / TY), seglen = TX / nseg;
+    float2 acc[KK];
+#pragma unroll
+    for (int t = 0; t < KK; t++)
+        acc[t] = float2{0.f, 0.f};
+    for (long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        const int x0 = int(tl % ntx) * TX, y0 = int((tl / ntx) % nty) * TY;
+        const long b = tl / (long(ntx) * nty);
+        __syncthreads();
+        load_halo<HX, HY>(tile, thin, X, Y, b, x0, y0, ox, oy);
+        __syncthreads();
+        for (int it = lane; it < TY * nseg; it += lanes) {
+            const int row = it / nseg, xs = (it % nseg) * seglen;
+            const int gy = y0 + row;
+            if (gy >= Y)
+                continue;
+            float2 win[K][K];
+#pragma unroll
+            for (int ky = 0; ky < K; ky++)
+#pragma unroll
+                for (int kx = 0; kx < K - 1; kx++)
+                    win[ky][kx] = tile[(row + ky) * HX + xs + kx];
+            const float* rowp = wide + (b * XY + long(X) * gy) * 2 * F;
+            const int xend = min(seglen, X - x0 - xs);
+            float2 vn{0.f, 0.f};
+            if (xend > 0)
+                vn = float2{rowp[long(x0 + xs) * 2 * F + f], rowp[long(x0 + xs) * 2 * F + F + f]};
+            for (int i = 0; i < xend; i++) {
+                const int px = xs + i;
+                const float2 v = vn;
+                if (i + 1 < xend) // software prefetch of the next wide element
+                    vn = float2{rowp[long(x0 + px + 1) * 2 * F + f], rowp[long(x0 + px + 1) * 2 * F + F + f]};
+#pragma unroll
+                for (int ky = 0; ky < K; ky++)
+                    win[ky][K - 1] = tile[(row + ky) * HX + px + K - 1];
+#pragma unroll
+                for (int ky = 0; ky < K; ky++)
+#pragma unroll
+                    for (int kx = 0; kx < K; kx++) {
+                        const float2 s = win[ky][kx];
+                        if (WIDE_IS_G) {
+                            // v * conj(s)
+                            acc[kx + K * ky].x += v.x * s.x + v.y * s.y;
+                            acc[kx + K * ky].y += v.y * s.x - v.x * s.y;
+                        } else {
+                            // s * conj(v)
+                            const int t = (K - 1 - kx) + K * (K - 1 - ky);
+                            acc[t].x += s.x * v.x + s.y * v.y;
+                            acc[t].y += s.y * v.x - s.x * v.y;
+                        }
+                    }
+#pragma unroll
+                for (int ky = 0; ky < K; ky++)
+#pragma unroll
+                    for (int kx = 0; kx < K - 1; kx++)
+                        win[ky][kx] = win[ky][kx + 1];
+            }
+        }
+    }
+    // fold the lanes of each channel in a fixed order
+#pragma unroll
+    for (int t = 0; t < KK; t++)
+        sred[(lane * KK + t) * F + f] = acc[t];
+    __syncthreads();
+    for (int e = threadIdx.x; e < KK * F; e += NT) {
         float2 s{0.f, 0.f};
         for (int l = 0; l < lanes; l++) {
             s.x += sred[l * KK * F + e].x;
             s.y += sred[l * KK * F + e].y;
         }
-        part[blk * KK * F + e] = s;
+        part[long(blockIdx.x) * KK * F + e] = s;
     }
 }
 
-__global__ void k_thin_wsum(float2* __restrict__ dw, const float2* __restrict__ part, long nblk, int KK, int F,
-                            bool f_is_cout)
+// dw[t + KK f] = sum over CTAs of part[blk][t * F + f]; one block per output,
+// fixed-order tree in double
+__global__ void __launch_bounds__(NT) k_thin_wsum(float2* __restrict__ dw, const float2* __restrict__ part, int nblk,
+                                                  int KK, int F)
 {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < KK * F; e += gridDim.x * blockDim.x) {
-        double sr = 0, si = 0;
-        for (long k = 0; k < nblk; k++) {
-            sr += part[k * KK * F + e].x;
-            si += part[k * KK * F + e].y;
-        }
-        const int t = e / F, f = e % F;
-        // w dims [KX, KY, Cin, Cout]: 1 -> F: index t + KK * f; F -> 1: t + KK * c
-        (void)f_is_cout;
-        dw[t + long(KK) * f] = float2{float(sr), float(si)};
+    __shared__ double sr[NT], si[NT];
+    const int e = blockIdx.x;
+    double a = 0, c = 0;
+    for (int k = threadIdx.x; k < nblk; k += NT) {
+        const float2 v = part[long(k) * KK * F + e];
+        a += v.x;
+        c += v.y;
     }
+    sr[threadIdx.x] = a;
+    si[threadIdx.x] = c;
+    __syncthreads();
+    for (int s = NT / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            sr[threadIdx.x] += sr[threadIdx.x + s];
+            si[threadIdx.x] += si[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int t = e / F, f = e % F;
+        dw[t + long(KK) * f] = float2{float(sr[0]), float(si[0])};
+    }
+}
+
+float2* pack_u(const cfloat* w, const ConvGeom& g, int F, int pmode)
+{
+    auto& c = ctx();
+    const int KK = int(g.KX * g.KY);
+    float2* U;
+    CUDA_CHECK(cudaMallocAsync(&U, sizeof(float2) * KK * F, c.stream));
+    k_pack_thin<<<std::max(1, (KK * F + 255) / 256), 256, 0, c.stream>>>(U, w, int(g.KX), int(g.KY), F, pmode);
+    KERNEL_CHECK();
+    return U;
+}
+
+template<int K>
+void run_thin(cfloat* outp, const cfloat* inp, const float2* U, const ConvGeom& g, int F, bool expand, int ox, int oy)
+{
+    auto& c = ctx();
+    if (expand) {
+        dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + 7) / 8), unsigned(g.B));
+        k_thin_expand<K><<<grid, NT, 0, c.stream>>>(reinterpret_cast<float*>(outp), inp, U, int(g.X), int(g.Y), F,
+                                                    ox, oy);
+    } else {
+        using Cfg = ReduceCfg<K>;
+        auto kern = k_thin_reduce<K>;
+        allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
+        dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + Cfg::TY - 1) / Cfg::TY), unsigned(g.B));
+        kern<<<grid, NT, Cfg::smem(), c.stream>>>(outp, reinterpret_cast<const float*>(inp), U, int(g.X), int(g.Y),
+                                                  F, ox, oy);
+    }
+    KERNEL_CHECK();
+}
+
+template<int K>
+void run_thin_wgrad(float2* part, int nblk, const cfloat* x, const cfloat* dy, const ConvGeom& g, int F, bool one_in)
+{
+    auto& c = ctx();
+    const size_t smem = sizeof(float2) * NT * K * K;
+    if (one_in) { // g = dy wide, h = x thin, window offset c0
+        auto kern = k_thin_wgrad<K, true>;
+        allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
+        kern<<<nblk, NT, smem, c.stream>>>(part, reinterpret_cast<const float*>(dy), x, int(g.X), int(g.Y), int(g.B),
+                                           F, int(g.px), int(g.py));
+    } else { // g = dy thin, h = x wide, window offset K-1-c0
+        auto kern = k_thin_wgrad<K, false>;
+        allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
+        kern<<<nblk, NT, smem, c.stream>>>(part, reinterpret_cast<const float*>(x), dy, int(g.X), int(g.Y), int(g.B),
+                                           F, int(K - 1 - g.px), int(K - 1 - g.py));
+    }
+    KERNEL_CHECK();
 }
 
 } // namespace
@@ -250,7 +399,7 @@ bool conv_thin_supported(const ConvGeom& g)
 {
     const bool one_in = g.Cin == 1, one_out = g.Cout == 1;
     const long F = one_in ? g.Cout : g.Cin;
-    if (one_in == one_out || F > MAXF || 256 % F != 0 || g.KX > MAXK || g.KY > MAXK || g.KX * g.KY > 25)
+    if (one_in == one_out || F > MAXF || 256 % F != 0 || g.KX != g.KY || (g.KX != 3 && g.KX != 5))
         return false;
     // the wide side must be channels-last (the thin side is layout-free)
     return one_in ? g.out_chlast : g.in_chlast;
@@ -262,28 +411,21 @@ void conv_thin_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvG
     auto& c = ctx();
     const bool one_in = g.Cin == 1;
     const int F = int(one_in ? g.Cout : g.Cin);
-    const int KK = int(g.KX * g.KY);
     // expand (thin -> wide): fwd of 1->F, bwd-data of F->1; reduce otherwise
     const bool expand = (mode == 0) == one_in;
     const int pmode = mode == 0 ? (one_in ? 0 : 2) : (one_in ? 3 : 1);
-    float2* U;
-    CUDA_CHECK(cudaMallocAsync(&U, sizeof(float2) * KK * F, c.stream));
-    k_pack_thin<<<std::max(1, (KK * F + 255) / 256), 256, 0, c.stream>>>(U, w, int(g.KX), int(g.KY), F, pmode);
-    KERNEL_CHECK();
+    float2* U = pack_u(w, g, F, pmode);
     // window offset: forward reads p + t - c0; adjoints use flipped taps with offset K-1-c0
     const int ox = mode == 0 ? int(g.px) : int(g.KX - 1 - g.px);
     const int oy = mode == 0 ? int(g.py) : int(g.KY - 1 - g.py);
-    dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY), unsigned(g.B));
-    // HBM-bound: algorithmic bytes = wide side once + thin side once
-    ProfScope prof(mode == 0 ? "conv_thin_fwd" : "conv_thin_bwd_data", 8.0 * double(g.X) * g.Y * g.B * (F + 1));
-    if (expand)
-        k_thin_expand<<<grid, 256, sizeof(float2) * KK * F, c.stream>>>(reinterpret_cast<float*>(outp), inp, U,
-                                                                       int(g.X), int(g.Y), F, int(g.KX), int(g.KY), ox,
-                                                                       oy);
-    else
-        k_thin_reduce<<<grid, TX * TY, 0, c.stream>>>(outp, reinterpret_cast<const float*>(inp), U, int(g.X),
-                                                      int(g.Y), F, int(g.KX), int(g.KY), ox, oy);
-    KERNEL_CHECK();
+    {
+        // HBM-bound: algorithmic bytes = wide side once + thin side once
+        ProfScope prof(mode == 0 ? "conv_thin_fwd" : "conv_thin_bwd_data", 8.0 * double(g.X) * g.Y * g.B * (F + 1));
+        if (g.KX == 3)
+            run_thin<3>(outp, inp, U, g, F, expand, ox, oy);
+        else
+            run_thin<5>(outp, inp, U, g, F, expand, ox, oy);
+    }
     CUDA_CHECK(cudaFreeAsync(U, c.stream));
 }
 
@@ -294,24 +436,19 @@ void conv_thin_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     const bool one_in = g.Cin == 1;
     const int F = int(one_in ? g.Cout : g.Cin);
     const int KK = int(g.KX * g.KY);
-    dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY), unsigned(g.B));
-    const long nblk = long(grid.x) * grid.y * grid.z;
-    const int lanes = 256 / F;
+    const long ntiles = ((g.X + TX - 1) / TX) * ((g.Y + 7) / 8) * g.B;
+    const int nblk = int(std::min<long>(ntiles, 2L * c.sm_count));
     float2* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * nblk * KK * F, c.stream));
-    ProfScope prof("conv_thin_bwd_weight", 8.0 * double(g.X) * g.Y * g.B * (F + 1));
-    const size_t smem = sizeof(float2) * size_t(lanes) * KK * F;
-    if (one_in) // h = x thin, g = dy wide
-        k_thin_wgrad<<<grid, 256, smem, c.stream>>>(part, nullptr, reinterpret_cast<const float*>(dy), x, nullptr,
-                                                     int(g.X), int(g.Y), F, int(g.KX), int(g.KY), int(g.px),
-                                                     int(g.py), true);
-    else // g = dy thin, h = x wide
-        k_thin_wgrad<<<grid, 256, smem, c.stream>>>(part, dy, nullptr, nullptr, reinterpret_cast<const float*>(x),
-                                                     int(g.X), int(g.Y), F, int(g.KX), int(g.KY), int(g.px),
-                                                     int(g.py), false);
-    KERNEL_CHECK();
-    k_thin_wsum<<<std::max(1, (KK * F + 255) / 256), 256, 0, c.stream>>>(dw, part, nblk, KK, F, one_in);
-    KERNEL_CHECK();
+    {
+        ProfScope prof("conv_thin_bwd_weight", 8.0 * double(g.X) * g.Y * g.B * (F + 1));
+        if (g.KX == 3)
+            run_thin_wgrad<3>(part, nblk, x, dy, g, F, one_in);
+        else
+            run_thin_wgrad<5>(part, nblk, x, dy, g, F, one_in);
+        k_thin_wsum<<<KK * F, NT, 0, c.stream>>>(dw, part, nblk, KK, F);
+        KERNEL_CHECK();
+    }
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
 

@@ -1544,11 +1544,11 @@ NodePtr node_rbf(const Dims& z, int fd, const std::vector<float>& mu, float sigm
 {
     return std::make_shared<RbfNode>(z, fd, mu, sigma);
 }
-bool bnblock_supported(long channels) { return channels >= 1 && channels <= 256 && 256 % channels == 0; }
+bool bnblock_supported(long channels) { return channels >= 2 && channels <= 256 && 256 % channels == 0; }
 NodePtr node_bnblock(const Dims& dims, bool round_out, bool round_dx, double eps, double mom)
 {
     if (!bnblock_supported(dims.at(dim_chan)))
-        throw ConfigError("bn_block: channel count must divide 256");
+        throw ConfigError("bn_block: channel count must be >= 2 and divide 256");
     return std::make_shared<BnBlockNode>(dims, round_out, round_dx, eps, mom);
 }
 NodePtr node_sense_normal(const SenseDims& sd) { return std::make_shared<SenseNormalNode>(sd, false); }

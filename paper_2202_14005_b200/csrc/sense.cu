@@ -113,18 +113,15 @@ struct CgDev {
     int n_rr;         // partial count written by the update kernel
     double2* part_pap;
     double2* part_rr;
+    double pap_sum;   // <p, Ap> of the current iteration, folded by the producer's last CTA
+    double rr_sum;    // <r, r> after the latest update
+    unsigned cnt_pap; // CTA arrival counters (reset by the folding CTA)
+    unsigned cnt_rr;
     float* rs;        // [max_iter + 1]
     float* alpha;     // [max_iter]
     float* beta;      // [max_iter]
 };
 
-__device__ double sum_partials_re(const double2* p, int n)
-{
-    double s = 0;
-    for (int i = 0; i < n; i++)
-        s += p[i].x;
-    return s;
-}
 
 // Prologue of iteration `it` of the S kernel, run by thread 0 of every CTA
 // (all CTAs compute bit-identical values).  Returns beta (or -1 to skip).
@@ -137,7 +134,7 @@ __device__ float cg_prologue(CgDev* st, int it, unsigned* errflags)
     if (it == 0) {
         rs_it = st->rs[0];
     } else {
-        double sum = sum_partials_re(st->part_rr, st->n_rr);
+        double sum = st->rr_sum;
         rs_it = float(sum);
         if (!isfinite(rs_it)) {
             if (blockIdx.x == 0) {
@@ -164,7 +161,7 @@ __device__ float cg_alpha(CgDev* st, int it, unsigned* errflags)
 {
     if (st->done_at <= it)
         return 0.f;
-    double s = sum_partials_re(st->part_pap, st->n_pap);
+    double s = st->pap_sum;
     float pap = float(s);
     if (!isfinite(pap) || pap <= 0.f) {
         if (blockIdx.x == 0) {
@@ -202,6 +199,32 @@ __device__ double2 block_sum2(double2 v)
     }
     __syncthreads();
     return v;
+}
+
+// Every CTA of a partial-producing kernel calls this with its block sum (valid
+// on thread 0).  The last CTA to arrive folds all partials in a fixed order
+// (thread-strided, then the block tree) and publishes the real part, so the
+// consumers read one scalar instead of re-summing gridDim partials per CTA.
+__device__ void publish_partial(double2* parts, double* result, unsigned* counter, double2 part)
+{
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+        parts[blockIdx.x] = part;
+        __threadfence();
+        s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last)
+        return;
+    __threadfence();
+    double2 v{0, 0};
+    for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x)
+        v.x += __ldcg(&parts[k].x);
+    v = block_sum2(v);
+    if (threadIdx.x == 0) {
+        *result = v.x;
+        *counter = 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -351,8 +374,7 @@ __global__ void __launch_bounds__(kT) k_normal_y(NormalArgs a, fftd::Plan plan)
         }
     if (a.mode == 1) {
         part = block_sum2(part);
-        if (threadIdx.x == 0)
-            a.cg->part_pap[blockIdx.x] = part;
+        publish_partial(a.cg->part_pap, &a.cg->pap_sum, &a.cg->cnt_pap, part);
     }
     (void)XY;
 }
@@ -445,8 +467,7 @@ __global__ void k_cg_pap(CgDev* st, int it, const cfloat* p, const cfloat* ap, l
         part.y += double(a.y) * b.x - double(a.x) * b.y;
     }
     part = block_sum2(part);
-    if (threadIdx.x == 0)
-        st->part_pap[blockIdx.x] = part;
+    publish_partial(st->part_pap, &st->pap_sum, &st->cnt_pap, part);
 }
 
 __global__ void k_cg_update(CgDev* st, int it, cfloat* x, cfloat* r, const cfloat* p, const cfloat* ap, long n,
@@ -472,8 +493,7 @@ __global__ void k_cg_update(CgDev* st, int it, cfloat* x, cfloat* r, const cfloa
         part.x += double(rv.x) * rv.x + double(rv.y) * rv.y;
     }
     part = block_sum2(part);
-    if (threadIdx.x == 0)
-        st->part_rr[blockIdx.x] = part;
+    publish_partial(st->part_rr, &st->rr_sum, &st->cnt_rr, part);
 }
 
 __global__ void k_cg_final(CgDev* st, double* status_out, unsigned* errflags)
@@ -484,7 +504,7 @@ __global__ void k_cg_final(CgDev* st, double* status_out, unsigned* errflags)
     float rs_last;
     if (it == INT_MAX) {
         it = st->max_iter;
-        rs_last = float(sum_partials_re(st->part_rr, st->n_rr));
+        rs_last = float(st->rr_sum);
         if (!isfinite(rs_last))
             atomicOr(errflags, unsigned(ERRF_CG_NONFINITE));
     } else {

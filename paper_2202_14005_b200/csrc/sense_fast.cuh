@@ -160,8 +160,7 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
     }
     if (a.mode == 1) {
         part = block_sum2(part);
-        if (tid == 0)
-            a.cg->part_pap[blockIdx.x] = part;
+        publish_partial(a.cg->part_pap, &a.cg->pap_sum, &a.cg->cnt_pap, part);
     }
 }
 
@@ -268,6 +267,5 @@ __global__ void k_cg_update_planes(CgDev* st, int it, cfloat* x, cfloat* r, cons
         part.x += double(rv.x) * rv.x + double(rv.y) * rv.y;
     }
     part = block_sum2(part);
-    if (threadIdx.x == 0)
-        st->part_rr[blockIdx.x] = part;
+    publish_partial(st->part_rr, &st->rr_sum, &st->cnt_rr, part);
 }
