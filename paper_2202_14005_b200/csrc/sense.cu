@@ -244,6 +244,7 @@ struct NormalArgs {
     long X, Y, C, M, B;
     PatStr ps;
     int W;
+    int nsplit;          // fast kernel: coil ranges per column strip (Ap planes)
     int mode;
     int it;
     CgDev* cg;
@@ -591,7 +592,8 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
         a.ps = pat_strides(g);
         a.mode = 0;
         a.errflags = ctx().d_errflags;
-        if (dispatch_fast<1>(a, nullptr, 0))
+        a.nsplit = 1;
+        if (dispatch_fast(a, nullptr, 0))
             return;
     }
     if (fused_ok(g)) {
@@ -711,9 +713,10 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
     auto& c = ctx();
     const int n_upd = grid_for(n);
     if (fast_ok(g, coils, coils)) {
-        // register-resident kernel, coils split over 2 CTAs -> 2 Ap planes;
-        // p ping-pongs between two buffers (no CTA reads a p another rewrites)
-        constexpr int NS = 2;
+        // register-resident kernel, coils split over NS CTAs -> NS Ap planes
+        // (NS picked against the wave tail); p ping-pongs between two buffers
+        // (no CTA reads a p another rewrites)
+        const int NS = fast_nsplit(g);
         CgMem m = cg_alloc(max_iter, tol, int(fast_ctas(g, NS)), n_upd);
         DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{NS * n}, false);
         cfloat* P[2] = {pb.data(), pb.data() + n};
@@ -737,7 +740,8 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             a.it = it;
             a.cg = m.st;
             a.errflags = c.d_errflags;
-            dispatch_fast<NS>(a, P[(it + 1) & 1], n);
+            a.nsplit = NS;
+            dispatch_fast(a, P[(it + 1) & 1], n);
             k_cg_update_planes<<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(), n,
                                                           NS, n, c.d_errflags);
             KERNEL_CHECK();

@@ -1,17 +1,20 @@
 // Register-resident fused A^H A (+ lambda) for Y = N1 * N2 (included by sense.cu).
 //
 // Per CTA: W image columns x all Y rows of one item, a contiguous range of
-// coils (coil-split across NSPLIT CTAs for load balance; the partial results
-// land in NSPLIT planes that the CG update sums, and <p, Ap> is linear in Ap
-// so its per-CTA partials stay exact).  Per coil, with y = j + N2*q:
+// coils (coil-split across nsplit CTAs against the wave tail; the partial
+// results land in nsplit planes that the CG update sums, and <p, Ap> is linear
+// in Ap so its per-CTA partials stay exact).  Per coil, with y = j + N2*q:
 //   stage A  thread (w, j):   v[q] = C[y] x[y]  -> DFT_N1 over q -> twiddle
 //                              W_Y^{j k1} -> smem S[k1][j]
 //   stage B  thread (w, k1):  DFT_N2 over j -> spectrum X[k1 + N1 k2]
 //                              -> mask P/Y -> IDFT_N2 -> conj twiddle -> S
 //   stage C  thread (w, j):   IDFT_N1 over k1 -> acc[q] += conj(C[y]) v[q]
-// Stage A and C threads own the same y positions, so the coil values loaded
-// for stage A are reused for the combine and the accumulators never leave
-// registers.  S is double-buffered by coil parity: 2 barriers per coil.
+// Stage A and C threads own the same y positions, so the coil values read for
+// stage A are reused for the combine and the accumulators never leave
+// registers.  The next coil's W x Y slice is prefetched into shared memory
+// with cp.async (zero-filled past the image edge) while stages B and C of the
+// current coil run, so no warp waits on HBM inside the coil loop.  S is
+// double-buffered by coil parity: 2 barriers per coil.
 #pragma once
 
 template<int N1, int N2, int W>
@@ -20,7 +23,16 @@ constexpr int fast_threads()
     return ((W * N2 + 31) / 32) * 32; // whole warps: block_sum2 needs full warps
 }
 
-template<int N1, int N2, int W, int NSPLIT>
+__device__ __forceinline__ void cp_async8(float2* dst, const float2* src, bool valid)
+{
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 8 : 0; // src-size 0: zero fill
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template<int N1, int N2, int W>
 __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
     k_normal_fast(NormalArgs a, const float2* __restrict__ tw, cfloat* __restrict__ p_out, long plane)
 {
@@ -32,6 +44,7 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
     float2* stw = S0 + 2 * Y * W;     // [Y]
     float2* spat = stw + Y;           // [Y]
     float2* xs = spat + Y;            // [Y * W]
+    float2* scoil = xs + Y * W;       // [Y * W] next coil slice
     __shared__ float s_beta;
     __shared__ float2 s_lam;
 
@@ -41,13 +54,26 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
     const int j = active ? j0 : 0;
     const long nxb = (a.X + W - 1) / W;
     long blk = blockIdx.x;
-    const int split = int(blk % NSPLIT);
-    blk /= NSPLIT;
+    const int split = int(blk % a.nsplit);
+    blk /= a.nsplit;
     const long x0 = (blk % nxb) * W, b = blk / nxb;
     const long xx = x0 + w;
     const bool colok = active && xx < a.X;
-    const long c_begin = a.C * split / NSPLIT, c_end = a.C * (split + 1) / NSPLIT;
+    const long c_begin = a.C * split / a.nsplit, c_end = a.C * (split + 1) / a.nsplit;
     const float invY = 1.f / float(Y);
+
+    // prefetch the first coil slice (thread (w, j) copies the rows it will read)
+    auto prefetch = [&](long c) {
+        if (!active)
+            return;
+        const float2* src = a.coils + (colok ? xx : 0) + a.X * a.Y * (c + a.C * b);
+#pragma unroll
+        for (int q = 0; q < N1; q++)
+            cp_async8(scoil + (j + N2 * q) * W + w, src + a.X * (j + N2 * q), colok);
+    };
+    if (c_begin < c_end)
+        prefetch(c_begin);
+    cp_async_commit();
 
     for (int e = tid; e < Y; e += NT) {
         stw[e] = tw[e];
@@ -60,8 +86,10 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
     }
     __syncthreads();
     const float beta = s_beta;
-    if (a.mode == 1 && beta < 0.f)
+    if (a.mode == 1 && beta < 0.f) {
+        cp_async_wait_all();
         return;
+    }
 
     // image column strip (x, or p = r + beta p_prev) -> smem
     const long img_base = xx + a.X * a.Y * b;
@@ -85,6 +113,7 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
         if (active)
             xs[y * W + w] = v;
     }
+    cp_async_wait_all();
     __syncthreads();
 
     float2 acc[N1];
@@ -94,12 +123,11 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
 
     for (long c = c_begin; c < c_end; c++) {
         float2* Sb = S0 + (c & 1) * (Y * W);
-        const long coil_base = xx + a.X * a.Y * (c + a.C * b);
         // ---- stage A: coil multiply, DFT over q, twiddle -> S
         float2 cv[N1], v[N1];
 #pragma unroll
         for (int q = 0; q < N1; q++)
-            cv[q] = colok ? a.coils[coil_base + a.X * (j + N2 * q)] : float2{0.f, 0.f};
+            cv[q] = scoil[(j + N2 * q) * W + w];
 #pragma unroll
         for (int q = 0; q < N1; q++)
             v[q] = cmul(cv[q], xs[(j + N2 * q) * W + w]);
@@ -110,6 +138,10 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
                 Sb[(k1 * N2 + j) * W + w] = k1 == 0 ? v[0] : cmul(v[k1], stw[j * N1 + k1]);
         }
         __syncthreads();
+        // scoil is free: fetch the next coil while stages B and C run
+        if (c + 1 < c_end)
+            prefetch(c + 1);
+        cp_async_commit();
         // ---- stage B: DFT over j, mask, inverse DFT over k2, conj twiddle
         if (tid < W * N1) {
             const int wb = tid % W, k1 = tid / W;
@@ -126,6 +158,7 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
             for (int jj = 0; jj < N2; jj++)
                 Sb[(k1 * N2 + jj) * W + wb] = k1 == 0 ? u[jj] : cmulc(u[jj], stw[jj * N1 + k1]);
         }
+        cp_async_wait_all();
         __syncthreads();
         // ---- stage C: inverse DFT over k1, conj-coil accumulate
 #pragma unroll
@@ -167,7 +200,7 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
 template<int N1, int N2, int W>
 constexpr size_t fast_smem_bytes()
 {
-    return sizeof(float2) * (2 * N1 * N2 * W + 2 * N1 * N2 + N1 * N2 * W);
+    return sizeof(float2) * (2 * N1 * N2 * W + 2 * N1 * N2 + 2 * N1 * N2 * W);
 }
 
 // forward twiddles tw[j * N1 + k1] = exp(-2 pi i j k1 / Y), double-accurate, per (device, Y)
@@ -196,17 +229,17 @@ const float2* fast_twiddles(int N1, int N2)
     return d;
 }
 
-template<int N1, int N2, int W, int NSPLIT>
+template<int N1, int N2, int W>
 void launch_fast(NormalArgs a, cfloat* p_out, long plane)
 {
-    auto kern = k_normal_fast<N1, N2, W, NSPLIT>;
+    auto kern = k_normal_fast<N1, N2, W>;
     constexpr size_t smem = fast_smem_bytes<N1, N2, W>();
     allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
     const long nxb = (a.X + W - 1) / W;
     const double xyb = double(a.X) * a.Y * a.B;
     const double work = 8.0 * xyb * (a.C + (a.mode == 1 ? 4 : 2));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    kern<<<unsigned(nxb * a.B * NSPLIT), fast_threads<N1, N2, W>(), smem, ctx().stream>>>(a, fast_twiddles(N1, N2), p_out, plane);
+    kern<<<unsigned(nxb * a.B * a.nsplit), fast_threads<N1, N2, W>(), smem, ctx().stream>>>(a, fast_twiddles(N1, N2), p_out, plane);
     KERNEL_CHECK();
 }
 
@@ -221,22 +254,39 @@ int fast_n1(long Y)
     }
 }
 
-template<int NSPLIT>
 bool dispatch_fast(NormalArgs a, cfloat* p_out, long plane)
 {
     constexpr int W = 8;
     switch (a.Y) {
-    case 128: launch_fast<8, 16, W, NSPLIT>(a, p_out, plane); return true;
-    case 256: launch_fast<16, 16, W, NSPLIT>(a, p_out, plane); return true;
-    case 320: launch_fast<16, 20, W, NSPLIT>(a, p_out, plane); return true;
-    case 368: launch_fast<16, 23, W, NSPLIT>(a, p_out, plane); return true;
-    case 512: launch_fast<16, 32, W, NSPLIT>(a, p_out, plane); return true;
-    case 640: launch_fast<16, 40, W, NSPLIT>(a, p_out, plane); return true;
+    case 128: launch_fast<8, 16, W>(a, p_out, plane); return true;
+    case 256: launch_fast<16, 16, W>(a, p_out, plane); return true;
+    case 320: launch_fast<16, 20, W>(a, p_out, plane); return true;
+    case 368: launch_fast<16, 23, W>(a, p_out, plane); return true;
+    case 512: launch_fast<16, 32, W>(a, p_out, plane); return true;
+    case 640: launch_fast<16, 40, W>(a, p_out, plane); return true;
     default: return false;
     }
 }
 
 long fast_ctas(const SenseGeom& g, int nsplit) { return ((g.X + 7) / 8) * g.B * nsplit; }
+
+// coil split minimising (waves) x (coils per CTA + ~1 coil of per-CTA overhead)
+// at 2 resident CTAs per SM
+int fast_nsplit(const SenseGeom& g)
+{
+    const long strips = (g.X + 7) / 8 * g.B, slots = 2L * ctx().sm_count;
+    int best = 1;
+    double best_t = 1e300;
+    for (int ns = 1; ns <= std::min<long>(g.C, 8); ns++) {
+        const double waves = double((strips * ns + slots - 1) / slots);
+        const double t = waves * (double((g.C + ns - 1) / ns) + 1.0);
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best = ns;
+        }
+    }
+    return best;
+}
 
 // CG update with NSPLIT Ap planes: x += alpha p ; r -= alpha (sum of planes)
 __global__ void k_cg_update_planes(CgDev* st, int it, cfloat* x, cfloat* r, const cfloat* p, const cfloat* ap,
