@@ -124,89 +124,134 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
     }
 }
 
-// wide -> thin.  Output tile TX x TY; halo pixels h own the K^2 tap projections.
-constexpr int RCC = 8; // channels per smem chunk
+// wide -> thin.  Output tile TX x TY; halo pixel h is owned by thread h % NT,
+// which streams its own channel rows (8 channels = 2 x 16 B of Re and of Im
+// per chunk) into private shared-memory slots with cp.async, double-buffered,
+// so the channel loop needs no block barrier; U[t][c] is staged once and read
+// as broadcasts.  The K^2 tap projections z_t[h] then meet in shared memory
+// for the final K^2 gather.
+constexpr int RCC = 8; // channels per chunk
 template<int K>
 struct ReduceCfg {
     static constexpr int TY = K == 3 ? 16 : 8;
     static constexpr int HX = TX + K - 1, HY = TY + K - 1, NH = HX * HY, KK = K * K;
     static constexpr int PP = (NH + NT - 1) / NT; // halo pixels per thread
-    static constexpr int PITCH = 2 * RCC + 1;     // conflict-free per-pixel rows
-    static constexpr int IN_FLOATS = ((NH * PITCH + 1) / 2) * 2;
-    static constexpr int Z_FLOATS = NH * KK * 2;
-    static constexpr size_t smem()
+    // staging: [buf][PP][quad 0..3][NT] float4   (quad: Re lo, Re hi, Im lo, Im hi)
+    static constexpr int STAGE_F4 = 2 * PP * 4 * NT;
+    static constexpr int Z_F2 = NH * KK;
+    static constexpr size_t stage_bytes() { return sizeof(float4) * STAGE_F4; }
+    static constexpr size_t z_bytes() { return sizeof(float2) * Z_F2; }
+    static constexpr size_t smem(int F)
     {
-        return sizeof(float) * (IN_FLOATS > Z_FLOATS ? IN_FLOATS : Z_FLOATS) + sizeof(float2) * KK * RCC;
+        return (stage_bytes() > z_bytes() ? stage_bytes() : z_bytes()) + sizeof(float2) * KK * F;
     }
 };
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid)
+{
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int sz = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template<int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 template<int K>
-__global__ void __launch_bounds__(NT) k_thin_reduce(float2* __restrict__ out, const float* __restrict__ in,
-                                                    const float2* __restrict__ U, int X, int Y, int F, int ox, int oy)
+__global__ void __launch_bounds__(NT, K == 3 ? 2 : 1) k_thin_reduce(float2* __restrict__ out, const float* __restrict__ in,
+                                                       const float2* __restrict__ U, int X, int Y, int F, int ox,
+                                                       int oy)
 {
     using Cfg = ReduceCfg<K>;
-    constexpr int HX = Cfg::HX, NH = Cfg::NH, KK = Cfg::KK, PP = Cfg::PP, PITCH = Cfg::PITCH, TY = Cfg::TY;
-    extern __shared__ float smr[];
-    float* sin = smr;                                     // [NH][PITCH]   (phase 1)
-    float2* z = reinterpret_cast<float2*>(smr);           // [NH][KK]      (phase 2, aliases sin)
-    constexpr int ZOFF = Cfg::IN_FLOATS > Cfg::Z_FLOATS ? Cfg::IN_FLOATS : Cfg::Z_FLOATS;
-    float2* su = reinterpret_cast<float2*>(smr + ZOFF);   // [KK][RCC]
+    constexpr int HX = Cfg::HX, NH = Cfg::NH, KK = Cfg::KK, PP = Cfg::PP, TY = Cfg::TY;
+    extern __shared__ float4 smr4[];
+    float4* stage = smr4;                                  // [2][PP][4][NT]
+    float2* z = reinterpret_cast<float2*>(smr4);           // [NH][KK] after the channel loop
+    constexpr size_t ZOFF = (Cfg::stage_bytes() > Cfg::z_bytes() ? Cfg::stage_bytes() : Cfg::z_bytes());
+    float2* su = reinterpret_cast<float2*>(reinterpret_cast<char*>(smr4) + ZOFF); // [KK][F]
+    const int tid = threadIdx.x;
     const long b = blockIdx.z;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const long XY = long(X) * Y;
+    for (int e = tid; e < KK * F; e += NT)
+        su[e] = U[e];
+
+    // per owned halo pixel: source row (or null when outside the image)
+    const float* src[PP];
+#pragma unroll
+    for (int k = 0; k < PP; k++) {
+        const int h = tid + k * NT;
+        const int hx = h % HX, hy = h / HX;
+        const int gx = x0 + hx - ox, gy = y0 + hy - oy;
+        src[k] = (h < NH && gx >= 0 && gx < X && gy >= 0 && gy < Y) ? in + (b * XY + gx + long(X) * gy) * 2 * F
+                                                                     : nullptr;
+    }
+    auto issue = [&](int chunk, int buf) {
+        const int c0 = chunk * RCC;
+#pragma unroll
+        for (int k = 0; k < PP; k++)
+#pragma unroll
+            for (int qd = 0; qd < 4; qd++) {
+                const bool ok = src[k] != nullptr;
+                const float* g = ok ? src[k] + (qd >> 1) * F + c0 + (qd & 1) * 4 : in;
+                cp_async16(&stage[((buf * PP + k) * 4 + qd) * NT + tid], g, ok);
+            }
+        cp_commit();
+    };
+    const int nchunk = F / RCC;
+    issue(0, 0);
+    __syncthreads(); // su visible
+
     float2 acc[PP][KK];
 #pragma unroll
     for (int k = 0; k < PP; k++)
 #pragma unroll
         for (int t = 0; t < KK; t++)
             acc[k][t] = float2{0.f, 0.f};
-    for (int c0 = 0; c0 < F; c0 += RCC) {
-        const int nc = min(RCC, F - c0);
-        __syncthreads();
-        for (int e = threadIdx.x; e < NH * 2 * RCC; e += NT) {
-            const int cc = e % RCC, part = (e / RCC) & 1, h = e / (2 * RCC);
-            const int hx = h % HX, hy = h / HX;
-            const int gx = x0 + hx - ox, gy = y0 + hy - oy;
-            float v = 0.f;
-            if (cc < nc && gx >= 0 && gx < X && gy >= 0 && gy < Y)
-                v = in[(b * XY + gx + long(X) * gy) * 2 * F + part * F + c0 + cc];
-            sin[h * PITCH + part * RCC + cc] = v;
+    for (int ch = 0; ch < nchunk; ch++) {
+        const int buf = ch & 1;
+        if (ch + 1 < nchunk) {
+            issue(ch + 1, buf ^ 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
         }
-        for (int e = threadIdx.x; e < KK * RCC; e += NT) {
-            const int t = e / RCC, cc = e % RCC;
-            su[e] = cc < nc ? U[t * F + c0 + cc] : float2{0.f, 0.f};
-        }
-        __syncthreads();
-#pragma unroll 2
-        for (int cc = 0; cc < RCC; cc++) {
-            float2 v[PP];
+        float re[PP][RCC], im[PP][RCC];
 #pragma unroll
-            for (int k = 0; k < PP; k++) {
-                const int h = threadIdx.x + k * NT;
-                v[k] = h < NH ? float2{sin[h * PITCH + cc], sin[h * PITCH + RCC + cc]} : float2{0.f, 0.f};
-            }
+        for (int k = 0; k < PP; k++) {
+            const float4 a0 = stage[((buf * PP + k) * 4 + 0) * NT + tid];
+            const float4 a1 = stage[((buf * PP + k) * 4 + 1) * NT + tid];
+            const float4 b0 = stage[((buf * PP + k) * 4 + 2) * NT + tid];
+            const float4 b1 = stage[((buf * PP + k) * 4 + 3) * NT + tid];
+            re[k][0] = a0.x, re[k][1] = a0.y, re[k][2] = a0.z, re[k][3] = a0.w;
+            re[k][4] = a1.x, re[k][5] = a1.y, re[k][6] = a1.z, re[k][7] = a1.w;
+            im[k][0] = b0.x, im[k][1] = b0.y, im[k][2] = b0.z, im[k][3] = b0.w;
+            im[k][4] = b1.x, im[k][5] = b1.y, im[k][6] = b1.z, im[k][7] = b1.w;
+        }
+        const float2* uc = su + ch * RCC;
+#pragma unroll
+        for (int cc = 0; cc < RCC; cc++)
 #pragma unroll
             for (int t = 0; t < KK; t++) {
-                const float2 uu = su[t * RCC + cc];
+                const float2 uu = uc[t * F + cc];
 #pragma unroll
                 for (int k = 0; k < PP; k++) {
-                    acc[k][t].x += v[k].x * uu.x - v[k].y * uu.y;
-                    acc[k][t].y += v[k].x * uu.y + v[k].y * uu.x;
+                    acc[k][t].x += re[k][cc] * uu.x - im[k][cc] * uu.y;
+                    acc[k][t].y += re[k][cc] * uu.y + im[k][cc] * uu.x;
                 }
             }
-        }
     }
-    __syncthreads();
+    __syncthreads(); // all staging reads done before z overwrites it
 #pragma unroll
     for (int k = 0; k < PP; k++) {
-        const int h = threadIdx.x + k * NT;
+        const int h = tid + k * NT;
         if (h < NH)
 #pragma unroll
             for (int t = 0; t < KK; t++)
                 z[h * KK + t] = acc[k][t];
     }
     __syncthreads();
-    for (int q = threadIdx.x; q < TX * TY; q += NT) {
+    for (int q = tid; q < TX * TY; q += NT) {
         const int px = q % TX, py = q / TX;
         const int gx = x0 + px, gy = y0 + py;
         float2 s{0.f, 0.f};
@@ -368,7 +413,7 @@ void run_thin(cfloat* outp, const cfloat* inp, const float2* U, const ConvGeom& 
         auto kern = k_thin_reduce<K>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
         dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + Cfg::TY - 1) / Cfg::TY), unsigned(g.B));
-        kern<<<grid, NT, Cfg::smem(), c.stream>>>(outp, reinterpret_cast<const float*>(inp), U, int(g.X), int(g.Y),
+        kern<<<grid, NT, Cfg::smem(F), c.stream>>>(outp, reinterpret_cast<const float*>(inp), U, int(g.X), int(g.Y),
                                                   F, ox, oy);
     }
     KERNEL_CHECK();
@@ -399,7 +444,7 @@ bool conv_thin_supported(const ConvGeom& g)
 {
     const bool one_in = g.Cin == 1, one_out = g.Cout == 1;
     const long F = one_in ? g.Cout : g.Cin;
-    if (one_in == one_out || F > MAXF || 256 % F != 0 || g.KX != g.KY || (g.KX != 3 && g.KX != 5))
+    if (one_in == one_out || F > MAXF || 256 % F != 0 || F % RCC != 0 || g.KX != g.KY || (g.KX != 3 && g.KX != 5))
         return false;
     // the wide side must be channels-last (the thin side is layout-free)
     return one_in ? g.out_chlast : g.in_chlast;

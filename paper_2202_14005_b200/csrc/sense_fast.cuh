@@ -92,26 +92,30 @@ __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), 2)
     }
 
     // image column strip (x, or p = r + beta p_prev) -> smem
+    // all loads first (p_out may alias nothing we read, but the compiler
+    // cannot know: interleaving the stores would serialise the loads)
     const long img_base = xx + a.X * a.Y * b;
+    {
+        float2 v[N1], pv[N1];
+        const float2* src = a.mode == 0 ? a.x : (a.it == 0 ? p_out : a.x);
+        const bool upd = a.mode == 1 && a.it > 0;
 #pragma unroll
-    for (int q = 0; q < N1; q++) {
-        const int y = j + N2 * q;
-        const long gi = img_base + a.X * y;
-        float2 v{0.f, 0.f};
-        if (colok) {
-            if (a.mode == 0) {
-                v = a.x[gi];
-            } else if (a.it == 0) {
-                v = p_out[gi];
-            } else {
-                const float2 r = a.x[gi], pp = a.p[gi];
-                v = float2{r.x + beta * pp.x, r.y + beta * pp.y};
-                if (split == 0)
-                    p_out[gi] = v;
-            }
+        for (int q = 0; q < N1; q++) {
+            const long gi = img_base + a.X * (j + N2 * q);
+            v[q] = colok ? src[gi] : float2{0.f, 0.f};
+            pv[q] = (colok && upd) ? a.p[gi] : float2{0.f, 0.f};
         }
-        if (active)
-            xs[y * W + w] = v;
+#pragma unroll
+        for (int q = 0; q < N1; q++) {
+            const int y = j + N2 * q;
+            if (upd) {
+                v[q] = float2{v[q].x + beta * pv[q].x, v[q].y + beta * pv[q].y};
+                if (split == 0 && colok)
+                    p_out[img_base + a.X * y] = v[q];
+            }
+            if (active)
+                xs[y * W + w] = v[q];
+        }
     }
     cp_async_wait_all();
     __syncthreads();

@@ -55,12 +55,27 @@ def main(workload="modl_c2"):
         t["update"] = time.perf_counter() - a
         t["total"] = time.perf_counter() - t0
         print({k: round(v * 1e3, 2) for k, v in t.items()}, "ms", flush=True)
-    # host launch overhead: time to enqueue (no sync) vs device time
-    lib.check(lib.so.mdnn_profile_enable(0))
-    a = time.perf_counter()
-    tr.forward_backward()
-    b = time.perf_counter()
-    print("forward_backward wall incl. final sync", round((b - a) * 1e3, 2), "ms")
+    # spike hunt: per-step wall time and per-tag device time
+    import ctypes as C
+    tags = ["sense_normal_y_cg", "sense_normal_y", "fft", "conv_tc_fwd", "conv_tc_bwd_data", "conv_tc_bwd_weight",
+            "conv_thin_fwd", "conv_thin_bwd_data", "conv_thin_bwd_weight", "bnblock_fwd", "bnblock_bwd",
+            "conv_fwd", "conv_bwd_data", "conv_bwd_weight"]
+    for rep in range(10):
+        lib.check(lib.so.mdnn_profile_reset())
+        lib.check(lib.so.mdnn_profile_enable(1))
+        a = time.perf_counter()
+        tr.forward_backward()
+        tr.update(1.0)
+        sync()
+        wall = time.perf_counter() - a
+        lib.check(lib.so.mdnn_profile_enable(0))
+        dev = {}
+        for tg in tags:
+            n, ms, work = C.c_long(), C.c_double(), C.c_double()
+            lib.check(lib.so.mdnn_profile_read(tg.encode(), C.byref(n), C.byref(ms), C.byref(work)))
+            if n.value:
+                dev[tg] = round(ms.value, 1)
+        print(f"rep {rep}: wall {wall * 1e3:.1f} ms, tagged device {sum(dev.values()):.1f} ms", dev, flush=True)
 
 
 if __name__ == "__main__":
