@@ -157,6 +157,10 @@ int mdnn_set_option(const char* key, long value)
         std::string k = key ? key : "";
         if (k == "conv_tc")
             conv_tc_enable(value != 0);
+        else if (k == "sense_rank")
+            sense_rank_enable(value != 0);
+        else if (k == "sense_rank_ctas")
+            sense_rank_ctas(value);
         else if (k == "conv_chlast")
             conv_force_chlast(value != 0);
         else

@@ -122,6 +122,10 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
 // tcgen05 TF32 implicit-GEMM path (conv_tc.cu) for 3x3 layers with 32/64 channels
 void conv_tc_enable(bool on);
+// persistent mask-pruned A^H A kernel (sense_rank.cuh); off = sense_fast.cuh path
+void sense_rank_enable(bool on);
+void sense_rank_ctas(long g);
+bool rank_enabled();
 // test hook: auto-layout convs store multi-channel activations channels-last
 void conv_force_chlast(bool on);
 bool conv_chlast_forced();

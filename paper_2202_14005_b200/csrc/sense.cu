@@ -17,6 +17,9 @@
 #include "fft.cuh"
 #include "kernels.h"
 #include "profile.h"
+#include "sm100.cuh"
+
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <climits>
@@ -387,6 +390,7 @@ __global__ void __launch_bounds__(kT) k_normal_y(NormalArgs a, fftd::Plan plan)
 namespace mdnn {
 namespace {
 #include "sense_fast.cuh"
+#include "sense_rank.cuh"
 
 bool fast_ok(const SenseGeom& g, const cfloat* coils, const cfloat* coils2)
 {
@@ -576,6 +580,31 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
 {
     if (!coils2)
         coils2 = coils;
+    if (coils2 == coils && rank_enabled()) {
+        const RankPlan rp = rank_plan(g, coils);
+        if (rp.ok) {
+            DArray plane1(Dims{g.X * g.Y * g.B}, false);
+            RankArgs a{};
+            a.out = out;
+            a.out1 = plane1.data();
+            a.x = x;
+            a.pattern = pattern;
+            a.lam = lam;
+            a.ps = pat_strides(g);
+            a.mode = 0;
+            a.errflags = ctx().d_errflags;
+            launch_rank(rp, a, coils, g);
+            const long n = g.X * g.Y * g.B;
+            if (rp.W == 8)
+                k_rank_merge<8><<<grid_for(n), kT, 0, ctx().stream>>>(out, plane1.data(), g.X, g.Y, g.B, rp.nxb, g.C,
+                                                                      rp.units, rp.G);
+            else
+                k_rank_merge<4><<<grid_for(n), kT, 0, ctx().stream>>>(out, plane1.data(), g.X, g.Y, g.B, rp.nxb, g.C,
+                                                                      rp.units, rp.G);
+            KERNEL_CHECK();
+            return;
+        }
+    }
     if (fast_ok(g, coils, coils2)) {
         NormalArgs a{};
         a.out = out;
@@ -712,6 +741,44 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
     }
     auto& c = ctx();
     const int n_upd = grid_for(n);
+    const RankPlan rp = rank_enabled() ? rank_plan(g, coils) : RankPlan{};
+    if (rp.ok) {
+        // persistent rank kernel: Ap in plane 0 (+ plane 1 for split strips);
+        // p ping-pongs between two buffers (no CTA reads a p another rewrites)
+        CgMem m = cg_alloc(max_iter, tol, rp.G, n_upd);
+        DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{2 * n}, false);
+        cfloat* P[2] = {pb.data(), pb.data() + n};
+        cg_start(m, x, b, r.data(), P[1], n);
+        for (int it = 0; it < max_iter; it++) {
+            RankArgs a{};
+            a.out = ap.data();
+            a.out1 = ap.data() + n;
+            a.x = r.data();
+            a.p = P[it & 1];
+            a.p_out = P[(it + 1) & 1];
+            a.pattern = pattern;
+            a.lam = lam;
+            a.ps = pat_strides(g);
+            a.mode = 1;
+            a.it = it;
+            a.cg = m.st;
+            a.errflags = c.d_errflags;
+            launch_rank(rp, a, coils, g);
+            if (rp.W == 8)
+                k_cg_update_rank<8><<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
+                                                                ap.data() + n, g.X, g.Y, g.B, rp.nxb, g.C, rp.units,
+                                                                rp.G, c.d_errflags);
+            else
+                k_cg_update_rank<4><<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
+                                                                ap.data() + n, g.X, g.Y, g.B, rp.nxb, g.C, rp.units,
+                                                                rp.G, c.d_errflags);
+            KERNEL_CHECK();
+        }
+        k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
+        KERNEL_CHECK();
+        CUDA_CHECK(cudaFreeAsync(m.mem, c.stream));
+        return;
+    }
     if (fast_ok(g, coils, coils)) {
         // register-resident kernel, coils split over NS CTAs -> NS Ap planes
         // (NS picked against the wave tail); p ping-pongs between two buffers
@@ -782,6 +849,14 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(m.mem, c.stream));
 }
+
+namespace {
+bool g_rank_enabled = true;
+}
+// rank-kernel CTA count override lives in sense_rank.cuh (g_rank_ctas)
+void sense_rank_enable(bool on) { g_rank_enabled = on; }
+void sense_rank_ctas(long g) { g_rank_ctas = g; }
+bool rank_enabled() { return g_rank_enabled; }
 
 CgResult read_cg_status(const double* status_dev)
 {
