@@ -584,6 +584,7 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
         const RankPlan rp = rank_plan(g, coils);
         if (rp.ok) {
             DArray plane1(Dims{g.X * g.Y * g.B}, false);
+            DArray plans(Dims{long((rank_plan_bytes(g) + 7) / 8)}, false);
             RankArgs a{};
             a.out = out;
             a.out1 = plane1.data();
@@ -593,7 +594,9 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
             a.ps = pat_strides(g);
             a.mode = 0;
             a.errflags = ctx().d_errflags;
-            launch_rank(rp, a, coils, g);
+            unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
+            launch_rank_plan(rp, a, g, pl);
+            launch_rank(rp, a, coils, g, pl);
             const long n = g.X * g.Y * g.B;
             if (rp.W == 8)
                 k_rank_merge<8><<<grid_for(n), kT, 0, ctx().stream>>>(out, plane1.data(), g.X, g.Y, g.B, rp.nxb, g.C,
@@ -747,8 +750,16 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
         // p ping-pongs between two buffers (no CTA reads a p another rewrites)
         CgMem m = cg_alloc(max_iter, tol, rp.G, n_upd);
         DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{2 * n}, false);
+        DArray plans(Dims{long((rank_plan_bytes(g) + 7) / 8)}, false);
+        unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
         cfloat* P[2] = {pb.data(), pb.data() + n};
         cg_start(m, x, b, r.data(), P[1], n);
+        {
+            RankArgs a{};
+            a.pattern = pattern;
+            a.ps = pat_strides(g);
+            launch_rank_plan(rp, a, g, pl);
+        }
         for (int it = 0; it < max_iter; it++) {
             RankArgs a{};
             a.out = ap.data();
@@ -763,7 +774,7 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             a.it = it;
             a.cg = m.st;
             a.errflags = c.d_errflags;
-            launch_rank(rp, a, coils, g);
+            launch_rank(rp, a, coils, g, pl);
             if (rp.W == 8)
                 k_cg_update_rank<8><<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
                                                                 ap.data() + n, g.X, g.Y, g.B, rp.nxb, g.C, rp.units,

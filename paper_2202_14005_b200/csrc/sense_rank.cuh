@@ -39,15 +39,13 @@ struct RankCfg {
     static constexpr int Y = N1 * N2;
     static constexpr int W = N2 <= 24 ? 8 : 4;             // columns per strip
     static constexpr int NT = ((W * N2 + 31) / 32) * 32;   // threads (w, j)
-    static constexpr int JP = (N2 + 1) / 2;                // shuffle-paired j slots
-    static constexpr int KMAX = (N2 % 2 == 1) ? 5 : 2;      // terms per row before a full DFT pays
+    static constexpr int JH = (N2 + 1) / 2;                // j per half-row (stage-B thread pairs)
     static constexpr int TMAX = 32;                        // terms per CTA
     static constexpr int NBOX = rank_nbox(Y);              // TMA boxes per coil slice (rows <= 256)
     static constexpr int BOXR = Y / NBOX;
-    static constexpr int UNION = Y * W;                    // float2: term pairs + full rows (>= all-full)
-    static constexpr size_t SLOT = size_t(Y) * W;          // float2 per ring slot
-    // dynamic smem (float2): ring[2][Y*W] | xs[Y*W] | un[UNION] | D[TMAX*W] | ttw[TMAX*N2] | stw[Y] | spat[Y]
-    static constexpr size_t SMEM = sizeof(float2) * (2 * SLOT + SLOT + UNION + TMAX * W + TMAX * N2 + 2 * Y) + 128;
+    static constexpr size_t SLOT = size_t(Y) * W;          // float2 per ring slot / S / xs
+    // dynamic smem (float2): ring[2][SLOT] | S[SLOT] | xs[SLOT] | ttw[TMAX*N2] | stw[Y]
+    static constexpr size_t SMEM = sizeof(float2) * (4 * SLOT + TMAX * N2 + Y) + 128;
     static constexpr int MINB = 2 * (SMEM + 4096) <= 228 * 1024 ? 2 : 1;
     static_assert(Y % NBOX == 0, "TMA box rows must tile Y");
 };
@@ -78,43 +76,133 @@ __host__ __device__ __forceinline__ bool rank_split(long s, long C, long U, long
     return rank_owner(s * C, U, G) != rank_owner(s * C + C - 1, U, G);
 }
 
+// Per-CTA row plan (shared memory), rebuilt when the item's pattern changes.
+// Every non-identity row is a term row (min(#{p != 0}, #{p != 1}) <= N2 / 2
+// terms); the first TMAX terms have precomputed twiddle rows (ttw), later
+// ones index the Y-point table on the fly.
+template<int N1, int N2>
+struct RankPlanSm {
+    static constexpr int TTOT = N1 * (N2 / 2);
+    int nwork, T;
+    int work_k1[N1];   // non-identity rows, fewest terms first
+    int mode[N1];      // 0 identity, 1 identity + terms, 2 terms only
+    int nt[N1], off[N1], key[N1];
+    int tk[TTOT];
+    float2 coef[TTOT];
+};
+
+// all threads; ends with a barrier
+template<int N1, int N2>
+__device__ void rank_build_plan(RankPlanSm<N1, N2>& pl, const RankArgs& a, int b, float2* ttw, const float2* stw)
+{
+    using Cfg = RankCfg<N1, N2>;
+    constexpr int Y = Cfg::Y, NT = Cfg::NT, TMAX = Cfg::TMAX;
+    constexpr float invN2 = 1.f / float(N2);
+    const int tid = threadIdx.x;
+    const long pb = long(b) * a.ps.sb;
+    if (tid < N1) {
+        int nz = 0, n1 = 0;
+        for (int k2 = 0; k2 < N2; k2++) {
+            const float2 pv = a.pattern[(tid + N1 * k2) * a.ps.sy + pb];
+            nz += (pv.x != 0.f || pv.y != 0.f);
+            n1 += (pv.x != 1.f || pv.y != 0.f);
+        }
+        const int n = min(nz, n1);
+        pl.nt[tid] = n;
+        pl.mode[tid] = n == 0 ? (n1 == 0 ? 0 : 2) : (nz <= n1 ? 2 : 1);
+        pl.key[tid] = n1 == 0 ? -1 : n; // identity rows sort first and are skipped
+    }
+    __syncthreads();
+    if (tid < N1) {
+        int off = 0, rank = 0, nid = 0, T = 0;
+        const int k = pl.key[tid];
+        for (int r = 0; r < N1; r++) {
+            off += r < tid ? pl.nt[r] : 0;
+            T += pl.nt[r];
+            const int kr = pl.key[r];
+            rank += (kr < k) || (kr == k && r < tid);
+            nid += kr < 0;
+        }
+        pl.off[tid] = off;
+        if (k >= 0)
+            pl.work_k1[rank - nid] = tid;
+        if (tid == 0) {
+            pl.nwork = N1 - nid;
+            pl.T = T;
+        }
+        const int md = pl.mode[tid];
+        if (md != 0) {
+            const float bb = md == 1 ? 1.f : 0.f;
+            int t = off;
+            for (int k2 = 0; k2 < N2; k2++) {
+                const float2 pv = a.pattern[(tid + N1 * k2) * a.ps.sy + pb];
+                if (pv.x != bb || pv.y != 0.f) {
+                    pl.tk[t] = tid + N1 * k2;
+                    pl.coef[t] = float2{(pv.x - bb) * invN2, pv.y * invN2};
+                    t++;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < min(pl.T, TMAX) * N2; e += NT) {
+        const int t = e / N2, jj = e % N2;
+        ttw[e] = stw[(jj * pl.tk[t]) % Y];
+    }
+    __syncthreads();
+}
+
+// Global plan record per pattern item: [RankPlanSm | ttw[TMAX * N2]], 16-B multiple.
+template<int N1, int N2>
+struct RankPlanRec {
+    static constexpr size_t PL = (sizeof(RankPlanSm<N1, N2>) + 15) & ~size_t(15);
+    static constexpr size_t BYTES = PL + sizeof(float2) * RankCfg<N1, N2>::TMAX * N2;
+};
+
+// one CTA per pattern item (grid = 1 for a broadcast pattern)
+template<int N1, int N2>
+__global__ void __launch_bounds__(RankCfg<N1, N2>::NT) k_rank_plan(RankArgs a, unsigned char* plans)
+{
+    unsigned char* rec = plans + RankPlanRec<N1, N2>::BYTES * blockIdx.x;
+    rank_build_plan<N1, N2>(*reinterpret_cast<RankPlanSm<N1, N2>*>(rec), a, int(blockIdx.x),
+                            reinterpret_cast<float2*>(rec + RankPlanRec<N1, N2>::PL), a.tw);
+}
+
 template<int N1, int N2>
 __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
-    k_normal_rank(RankArgs a, const __grid_constant__ CUtensorMap tmap)
+    k_normal_rank(RankArgs a, const __grid_constant__ CUtensorMap tmap, const unsigned char* __restrict__ plans)
 {
     using namespace fftd;
     using Cfg = RankCfg<N1, N2>;
-    constexpr int Y = Cfg::Y, W = Cfg::W, NT = Cfg::NT, JP = Cfg::JP, KMAX = Cfg::KMAX, TMAX = Cfg::TMAX;
-    extern __shared__ __align__(128) unsigned char rank_smem[];
-    float2* ring = reinterpret_cast<float2*>((reinterpret_cast<uintptr_t>(rank_smem) + 127) & ~uintptr_t(127));
-    float2* xs = ring + 2 * Cfg::SLOT;
-    float2* un = xs + Cfg::SLOT;
-    float2* Ds = un + Cfg::UNION;
-    float2* ttw = Ds + TMAX * W;
+    constexpr int Y = Cfg::Y, W = Cfg::W, NT = Cfg::NT, JH = Cfg::JH, TMAX = Cfg::TMAX;
+    extern __shared__ __align__(128) float2 rank_smem[];
+    float2* ring = rank_smem;
+    float2* S = ring + 2 * Cfg::SLOT;
+    float2* xs = S + Cfg::SLOT;
+    float2* ttw = xs + Cfg::SLOT;
     float2* stw = ttw + TMAX * N2;
-    float2* spat = stw + Y;
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ float s_beta;
     __shared__ float2 s_lam;
-    __shared__ int s_cnt[N1], s_bb[N1], s_mode[N1], s_off[N1], s_nt[N1];
-    __shared__ int s_fullk1[N1], s_tk[TMAX], s_T, s_nfull;
-    __shared__ float2 s_coef[TMAX];
+    __shared__ __align__(16) RankPlanSm<N1, N2> pl;
 
     const int tid = threadIdx.x;
     const int w = tid % W, j0 = tid / W;
     const bool active = j0 < N2;
     const int j = active ? j0 : N2 - 1;
-    const long U = a.units, C = a.C;
-    const long u_begin = U * blockIdx.x / a.G, u_end = U * (blockIdx.x + 1) / a.G;
+    const int C = int(a.C), nxb = int(a.nxb);
+    const int U = int(a.units);
+    const int u_begin = int(long(U) * blockIdx.x / a.G), u_end = int(long(U) * (blockIdx.x + 1) / a.G);
+    const int n = u_end - u_begin;
 
-    auto issue = [&](long u, int slot) { // TMA of unit u's coil slice into ring slot
-        const long s = u / C, c = u % C;
-        const long b = s / a.nxb, xblk = s % a.nxb;
-        const int row0 = int(Y * (c + C * b));
+    auto issue = [&](int u, int slot) { // TMA of unit u's coil slice into ring slot
+        const int s = u / C, c = u - s * C;
+        const int b = s / nxb, xblk = s - b * nxb;
+        const int row0 = Y * (c + C * b);
         sm100::mbar_arrive_expect_tx(&s_bar[slot], uint32_t(Cfg::SLOT * sizeof(float2)));
 #pragma unroll
         for (int k = 0; k < Cfg::NBOX; k++)
-            sm100::tma_load_2d(ring + slot * Cfg::SLOT + k * Cfg::BOXR * W, &tmap, &s_bar[slot], int(2 * W * xblk),
+            sm100::tma_load_2d(ring + slot * Cfg::SLOT + k * Cfg::BOXR * W, &tmap, &s_bar[slot], 2 * W * xblk,
                                row0 + k * Cfg::BOXR);
     };
     if (tid == 0) {
@@ -122,8 +210,8 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
         sm100::mbar_init(&s_bar[0], 1);
         sm100::mbar_init(&s_bar[1], 1);
         sm100::fence_barrier_init();
-        for (long u = u_begin; u < u_end && u < u_begin + 2; u++)
-            issue(u, int(u - u_begin));
+        for (int i = 0; i < n && i < 2; i++)
+            issue(u_begin + i, i);
         s_beta = a.mode == 1 ? cg_prologue(a.cg, a.it, a.errflags) : 0.f;
         s_lam = a.lam ? a.lam[0] : float2{0.f, 0.f};
     }
@@ -133,273 +221,254 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
     const float beta = s_beta;
     if (a.mode == 1 && beta < 0.f) {
         // CG already stopped: drain the TMA ring before exiting
-        for (long u = u_begin; u < u_end && u < u_begin + 2; u++)
-            sm100::mbar_wait(&s_bar[u - u_begin], 0);
+        for (int i = 0; i < n && i < 2; i++)
+            sm100::mbar_wait(&s_bar[i], 0);
         return;
     }
     const bool upd = a.mode == 1 && a.it > 0;
     const float2 lam = s_lam;
-    constexpr float invN1 = 1.f / float(N1), invN2 = 1.f / float(N2);
+    constexpr float invN1 = 1.f / float(N1);
 
+    int plan_b = -1;
+    int n_items = 0, my_h = 0, my_k1 = 0, my_ww = 0, my_md = 0, my_nt = 0, my_off = 0;
+    bool my_item = false;
     double2 part{0, 0};
-    long plan_b = -1;
-    long u = u_begin;
-    while (u < u_end) {
-        const long s = u / C;
-        const long b = s / a.nxb, xblk = s % a.nxb;
-        const long c0 = u % C;
-        const long seg_end = min(u_end, (s + 1) * C);
-        const bool first = c0 == 0;
-        const long xx = xblk * W + w;
-        const bool colok = active && xx < a.X;
+    float2 acc[N1], cv[N1];
+    int seg_s = u_begin / C;           // strip of the open segment
+    int c_cur = u_begin - seg_s * C;   // coil of unit i
+    bool seg_first = c_cur == 0;
 
-        // ---- row plan for item b (pattern may differ per item) --------------
-        if (b != plan_b && (plan_b < 0 || a.ps.sb != 0)) {
-            __syncthreads(); // previous plan no longer read
-            for (int e = tid; e < Y; e += NT)
-                spat[e] = a.pattern[e * a.ps.sy + b * a.ps.sb];
-            __syncthreads();
-            if (tid < N1) {
-                const int k1 = tid;
-                int nz = 0, n1 = 0;
-                for (int k2 = 0; k2 < N2; k2++) {
-                    const float2 pv = spat[k1 + N1 * k2];
-                    nz += (pv.x != 0.f || pv.y != 0.f);
-                    n1 += (pv.x != 1.f || pv.y != 0.f);
-                }
-                s_bb[k1] = nz <= n1 ? 0 : 1;
-                s_cnt[k1] = min(nz, n1);
-            }
-            __syncthreads();
-            if (tid == 0) {
-                // term rows while the union buffer and TMAX allow (cheapest
-                // rows first), the rest full; modes: 0 identity, 1 add terms,
-                // 2 replace by terms, 3 full DFT
-                int order[N1];
-                for (int k = 0; k < N1; k++)
-                    order[k] = k;
-                for (int i = 1; i < N1; i++) {
-                    const int r = order[i];
-                    int k = i - 1;
-                    while (k >= 0 && s_cnt[order[k]] > s_cnt[r]) {
-                        order[k + 1] = order[k];
-                        k--;
-                    }
-                    order[k + 1] = r;
-                }
-                int T = 0, nfull = 0, used = 0;
-                const int row_full = N2 * W, term_sz = JP * W;
-                for (int i = 0; i < N1; i++) {
-                    const int k1 = order[i], n = s_cnt[k1];
-                    const int remaining = N1 - i - 1; // rows still to place may all go full
-                    const bool fit = n <= KMAX && T + n <= TMAX
-                                     && used + n * term_sz + remaining * row_full <= Cfg::UNION;
-                    if (n == 0) {
-                        s_mode[k1] = s_bb[k1] ? 0 : 2;
-                        s_nt[k1] = 0;
-                        s_off[k1] = 0;
-                    } else if (fit) {
-                        s_mode[k1] = s_bb[k1] ? 1 : 2;
-                        s_nt[k1] = n;
-                        s_off[k1] = T;
-                        T += n;
-                        used += n * term_sz;
-                    } else {
-                        s_mode[k1] = 3;
-                        s_nt[k1] = 0;
-                        s_off[k1] = nfull;
-                        s_fullk1[nfull++] = k1;
-                        used += row_full;
-                    }
-                }
-                s_T = T;
-                s_nfull = nfull;
-            }
-            __syncthreads();
-            if (tid < N1) {
-                const int k1 = tid, bb = s_bb[k1];
-                if (s_mode[k1] == 1 || s_mode[k1] == 2) {
-                    int t = s_off[k1];
-                    for (int k2 = 0; k2 < N2; k2++) {
-                        const float2 pv = spat[k1 + N1 * k2];
-                        if (pv.x != float(bb) || pv.y != 0.f) {
-                            s_tk[t] = k1 + N1 * k2;
-                            s_coef[t] = float2{(pv.x - float(bb)) * invN2, pv.y * invN2};
-                            t++;
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-            for (int e = tid; e < s_T * N2; e += NT) {
-                const int t = e / N2, jj = e % N2;
-                ttw[e] = stw[(jj * s_tk[t]) % Y];
-            }
-            __syncthreads();
-            plan_b = b;
-        }
-        const int T = s_T, nfull = s_nfull;
-        float2* Pbuf = un;                       // [T][JP][W]
-        float2* Rbuf = un + T * JP * W;          // [nfull][N2][W]
-
-        // ---- x (or p = r + beta p_prev) column strip -> xs ----------------------
-        {
-            const long img_base = xx + a.X * Y * b;
-            float2 v[N1], pv[N1];
-            const float2* src = a.mode == 0 ? a.x : (a.it == 0 ? a.p_out : a.x);
-#pragma unroll
-            for (int q = 0; q < N1; q++) {
-                const long gi = img_base + a.X * (j + N2 * q);
-                v[q] = colok ? src[gi] : float2{0.f, 0.f};
-                pv[q] = (colok && upd) ? a.p[gi] : float2{0.f, 0.f};
-            }
-#pragma unroll
-            for (int q = 0; q < N1; q++) {
-                const int y = j + N2 * q;
-                if (upd) {
-                    v[q] = float2{v[q].x + beta * pv[q].x, v[q].y + beta * pv[q].y};
-                    if (first && colok)
-                        a.p_out[img_base + a.X * y] = v[q];
-                }
-                if (active)
-                    xs[y * W + w] = v[q];
-            }
-        }
-
-        float2 acc[N1];
-#pragma unroll
-        for (int q = 0; q < N1; q++)
-            acc[q] = float2{0.f, 0.f};
-
-        for (; u < seg_end; u++) {
-            const long i = u - u_begin;
-            const int slot = int(i & 1);
-            const float2* cs = ring + slot * Cfg::SLOT;
-            sm100::mbar_wait(&s_bar[slot], uint32_t((i >> 1) & 1));
-            // ---- phase 1: coil multiply, DFT over q, term products / full rows
+    // iteration i: [C(unit i-1) (+ epilogue) ; A(unit i)] | barrier | B(unit i) | barrier
+    for (int i = 0; i <= n; i++) {
+        const bool opens = i < n && (i == 0 || c_cur == 0);
+        if (i >= 1) {
+            // ---- C(i-1): inverse DFT over k1, conj-coil accumulate
             float2 v[N1];
-            {
-                float2 cv[N1];
 #pragma unroll
-                for (int q = 0; q < N1; q++)
-                    cv[q] = cs[(j + N2 * q) * W + w];
-#pragma unroll
-                for (int q = 0; q < N1; q++)
-                    v[q] = active ? cmul(cv[q], xs[(j + N2 * q) * W + w]) : float2{0.f, 0.f};
-            }
-            dft_reg<N1, -1>(v);
-#pragma unroll
-            for (int k1 = 0; k1 < N1; k1++) {
-                const int mode = s_mode[k1];
-                if (mode == 3) {
-                    if (active)
-                        Rbuf[(s_off[k1] * N2 + j) * W + w] = v[k1];
-                } else if (mode != 0 || s_nt[k1] > 0) {
-                    const int off = s_off[k1], nt = s_nt[k1];
-                    for (int t = off; t < off + nt; t++) {
-                        float2 pr = cmul(v[k1], ttw[t * N2 + j]);
-                        pr.x += __shfl_xor_sync(0xffffffffu, pr.x, W);
-                        pr.y += __shfl_xor_sync(0xffffffffu, pr.y, W);
-                        if (!(j0 & 1) && j0 < N2)
-                            Pbuf[(t * JP + (j0 >> 1)) * W + w] = pr;
-                    }
-                }
-            }
-            __syncthreads();
-            // both readers of this slot are done after the barrier of the next
-            // unit's phase 1; refill the other slot now (its unit finished)
-            if (tid == 0 && i >= 1 && u + 1 < u_end)
-                issue(u + 1, slot ^ 1);
-            // ---- phase 2: term sums (t, w) and full rows (r, w) -----------------
-            for (int it2 = tid; it2 < (T + nfull) * W; it2 += NT) {
-                const int ww = it2 % W, t = it2 / W;
-                if (t < T) {
-                    float2 d{0.f, 0.f};
-#pragma unroll
-                    for (int jp = 0; jp < JP; jp++) {
-                        const float2 pv = Pbuf[(t * JP + jp) * W + ww];
-                        d.x += pv.x;
-                        d.y += pv.y;
-                    }
-                    Ds[t * W + ww] = cmul(d, s_coef[t]);
-                } else {
-                    const int r = t - T, k1 = s_fullk1[r];
-                    float2* row = Rbuf + r * N2 * W + ww;
-                    float2 uu[N2];
-#pragma unroll
-                    for (int jj = 0; jj < N2; jj++)
-                        uu[jj] = row[jj * W];
-#pragma unroll
-                    for (int jj = 1; jj < N2; jj++)
-                        uu[jj] = cmul(uu[jj], stw[jj * k1]);
-                    dft_reg<N2, -1>(uu);
-#pragma unroll
-                    for (int k2 = 0; k2 < N2; k2++) {
-                        const float2 pv = spat[k1 + N1 * k2];
-                        uu[k2] = cmul(uu[k2], float2{pv.x * invN2, pv.y * invN2});
-                    }
-                    dft_reg<N2, +1>(uu);
-#pragma unroll
-                    for (int jj = 1; jj < N2; jj++)
-                        uu[jj] = cmulc(uu[jj], stw[jj * k1]);
-#pragma unroll
-                    for (int jj = 0; jj < N2; jj++)
-                        row[jj * W] = uu[jj];
-                }
-            }
-            __syncthreads();
-            // ---- phase 3: rows back into registers, inverse DFT, conj-coil accumulate
-#pragma unroll
-            for (int k1 = 0; k1 < N1; k1++) {
-                const int mode = s_mode[k1];
-                if (mode == 3) {
-                    v[k1] = Rbuf[(s_off[k1] * N2 + j) * W + w];
-                } else if (mode != 0) {
-                    if (mode == 2)
-                        v[k1] = float2{0.f, 0.f};
-                    const int off = s_off[k1], nt = s_nt[k1];
-                    for (int t = off; t < off + nt; t++) {
-                        const float2 dt = Ds[t * W + w], tv = ttw[t * N2 + j]; // v += d conj(tv)
-                        v[k1].x = fmaf(dt.x, tv.x, v[k1].x);
-                        v[k1].y = fmaf(dt.y, tv.x, v[k1].y);
-                        v[k1].x = fmaf(dt.y, tv.y, v[k1].x);
-                        v[k1].y = fmaf(-dt.x, tv.y, v[k1].y);
-                    }
-                }
-            }
+            for (int k1 = 0; k1 < N1; k1++)
+                v[k1] = S[(k1 * N2 + j) * W + w];
             dft_reg<N1, +1>(v);
 #pragma unroll
             for (int q = 0; q < N1; q++) {
-                const float2 cv = cs[(j + N2 * q) * W + w];
-                const float2 t = cmulc(v[q], cv);
+                const float2 t = cmulc(v[q], cv[q]);
                 acc[q].x += t.x;
                 acc[q].y += t.y;
             }
-            (void)KMAX;
-        }
-
-        // ---- segment epilogue: 1/N1, + lambda x (plane 0), store, <p, Ap> -----
-        {
-            const long img_base = xx + a.X * Y * b;
-            cfloat* dst = first ? a.out : a.out1;
+            if (i == n || c_cur == 0) {
+                // ---- segment epilogue: 1/N1, + lambda x (plane 0), store, <p, Ap>
+                const int b = seg_s / nxb, xx = (seg_s - b * nxb) * W + w;
+                const long img_base = xx + a.X * Y * long(b);
+                cfloat* dst = seg_first ? a.out : a.out1;
 #pragma unroll
-            for (int q = 0; q < N1; q++) {
-                const int y = j + N2 * q;
-                const float2 xv = xs[y * W + w];
-                float2 o{acc[q].x * invN1, acc[q].y * invN1};
-                if (first) {
-                    const float2 lx = cmul(xv, lam);
-                    o.x += lx.x;
-                    o.y += lx.y;
-                }
-                if (colok) {
-                    dst[img_base + a.X * y] = o;
-                    part.x += double(xv.x) * o.x + double(xv.y) * o.y;
-                    part.y += double(xv.y) * o.x - double(xv.x) * o.y;
+                for (int q = 0; q < N1; q++) {
+                    const int y = j + N2 * q;
+                    const float2 xv = xs[y * W + w];
+                    float2 o{acc[q].x * invN1, acc[q].y * invN1};
+                    if (seg_first) {
+                        const float2 lx = cmul(xv, lam);
+                        o.x += lx.x;
+                        o.y += lx.y;
+                    }
+                    if (active && xx < a.X) {
+                        dst[img_base + a.X * y] = o;
+                        part.x += double(xv.x) * o.x + double(xv.y) * o.y;
+                        part.y += double(xv.y) * o.x - double(xv.x) * o.y;
+                    }
                 }
             }
         }
-        __syncthreads(); // xs / plan reuse by the next segment
+        if (i < n) {
+            if (opens) {
+                if (i > 0)
+                    seg_s++;
+                seg_first = c_cur == 0;
+                const int b = seg_s / nxb;
+                if (b != plan_b && (plan_b < 0 || a.ps.sb != 0)) {
+                    // B(i-1) is done (barrier); C does not read the plan
+                    using Rec = RankPlanRec<N1, N2>;
+                    const int4* src = reinterpret_cast<const int4*>(plans + Rec::BYTES * (a.ps.sb != 0 ? b : 0));
+                    int4* dpl = reinterpret_cast<int4*>(&pl);
+                    for (int e = tid; e < int(Rec::PL / 16); e += NT)
+                        dpl[e] = src[e];
+                    const int4* src2 = reinterpret_cast<const int4*>(reinterpret_cast<const unsigned char*>(src) + Rec::PL);
+                    int4* dtw = reinterpret_cast<int4*>(ttw);
+                    for (int e = tid; e < int(TMAX * N2 * sizeof(float2) / 16); e += NT)
+                        dtw[e] = src2[e];
+                    __syncthreads();
+                    plan_b = b;
+                    // this thread's first stage-B item (the loop handles any others)
+                    const int it0 = tid, nitems = pl.nwork * W * 2;
+                    my_item = it0 < nitems;
+                    my_h = it0 & 1;
+                    my_k1 = my_item ? pl.work_k1[(it0 >> 1) / W] : 0;
+                    my_ww = (it0 >> 1) % W;
+                    my_md = pl.mode[my_k1];
+                    my_nt = pl.nt[my_k1];
+                    my_off = pl.off[my_k1];
+                    n_items = nitems;
+                }
+                // ---- open a segment: x (or p = r + beta p_prev) strip -> xs
+                const int xx = (seg_s - b * nxb) * W + w;
+                const bool colok = active && xx < a.X;
+                const long img_base = xx + a.X * Y * long(b);
+                float2 v[N1], pv[N1];
+                const float2* src = a.mode == 0 ? a.x : (a.it == 0 ? a.p_out : a.x);
+#pragma unroll
+                for (int q = 0; q < N1; q++) {
+                    const long gi = img_base + a.X * (j + N2 * q);
+                    v[q] = colok ? src[gi] : float2{0.f, 0.f};
+                    pv[q] = (colok && upd) ? a.p[gi] : float2{0.f, 0.f};
+                }
+#pragma unroll
+                for (int q = 0; q < N1; q++) {
+                    const int y = j + N2 * q;
+                    if (upd) {
+                        v[q] = float2{v[q].x + beta * pv[q].x, v[q].y + beta * pv[q].y};
+                        if (seg_first && colok)
+                            a.p_out[img_base + a.X * y] = v[q];
+                    }
+                    if (active)
+                        xs[y * W + w] = v[q];
+                    acc[q] = float2{0.f, 0.f};
+                }
+            }
+            // ---- A(i): coil multiply, DFT over q -> S (untwiddled)
+            const int slot = i & 1;
+            const float2* cs = ring + slot * Cfg::SLOT;
+            sm100::mbar_wait(&s_bar[slot], uint32_t((i >> 1) & 1));
+            float2 v[N1];
+            // padding threads (j clamped) compute on valid rows; their results are never stored
+            const float2* csp = cs + j * W + w;
+            const float2* xsp = xs + j * W + w;
+#pragma unroll
+            for (int q = 0; q < N1; q++)
+                cv[q] = csp[N2 * W * q];
+#pragma unroll
+            for (int q = 0; q < N1; q++)
+                v[q] = cmul(cv[q], xsp[N2 * W * q]);
+            dft_reg<N1, -1>(v);
+            if (active) {
+#pragma unroll
+                for (int k1 = 0; k1 < N1; k1++)
+                    S[(k1 * N2 + j) * W + w] = v[k1];
+            }
+        }
+        __syncthreads();
+        if (i >= n)
+            break;
+        c_cur = c_cur + 1 == C ? 0 : c_cur + 1;
+        // slot i & 1 is consumed (coils now live in registers): refill it
+        if (tid == 0 && i + 2 < n)
+            issue(u_begin + i + 2, i & 1);
+        // ---- B(i): per non-identity row, a thread pair (h = j half) per column:
+        //   r = b A + sum_t coef_t (sum_j A_j w_t[j]) conj(w_t[j])
+        for (int item = tid; item < n_items; item += NT) {
+            int h = my_h, ww = my_ww, k1 = my_k1, md = my_md, nt = my_nt, off = my_off;
+            if (item != tid) {
+                h = item & 1;
+                ww = (item >> 1) % W;
+                k1 = pl.work_k1[(item >> 1) / W];
+                md = pl.mode[k1];
+                nt = pl.nt[k1];
+                off = pl.off[k1];
+            }
+            float2* row = S + k1 * N2 * W + ww;
+            const unsigned pmask = 3u << ((tid & 31) & ~1);
+            const int jb = h * JH;
+            float2 uu[JH];
+#pragma unroll
+            for (int jj = 0; jj < JH; jj++)
+                uu[jj] = (jb + jj < N2) ? row[(jb + jj) * W] : float2{0.f, 0.f};
+            if (nt <= 2 && off + nt <= TMAX) {
+                // common case (<= 2 terms, precomputed twiddle rows): both dot
+                // products in one pass (4 independent chains), then in place
+                const bool two = nt == 2;
+                const float2* t0 = ttw + off * N2 + jb;
+                const float2* t1 = ttw + (two ? off + 1 : off) * N2 + jb;
+                float2 a0{0.f, 0.f}, a1{0.f, 0.f};
+#pragma unroll
+                for (int jj = 0; jj < JH; jj++) {
+                    if (jb + jj < N2) {
+                        const float2 p0 = t0[jj], p1 = t1[jj];
+                        a0.x = fmaf(uu[jj].x, p0.x, a0.x);
+                        a0.y = fmaf(uu[jj].x, p0.y, a0.y);
+                        a1.x = fmaf(uu[jj].x, p1.x, a1.x);
+                        a1.y = fmaf(uu[jj].x, p1.y, a1.y);
+                        a0.x = fmaf(-uu[jj].y, p0.y, a0.x);
+                        a0.y = fmaf(uu[jj].y, p0.x, a0.y);
+                        a1.x = fmaf(-uu[jj].y, p1.y, a1.x);
+                        a1.y = fmaf(uu[jj].y, p1.x, a1.y);
+                    }
+                }
+                a0.x += __shfl_xor_sync(pmask, a0.x, 1);
+                a0.y += __shfl_xor_sync(pmask, a0.y, 1);
+                a1.x += __shfl_xor_sync(pmask, a1.x, 1);
+                a1.y += __shfl_xor_sync(pmask, a1.y, 1);
+                a0 = nt > 0 ? cmul(a0, pl.coef[off]) : float2{0.f, 0.f};
+                a1 = two ? cmul(a1, pl.coef[off + 1]) : float2{0.f, 0.f};
+#pragma unroll
+                for (int jj = 0; jj < JH; jj++) {
+                    if (jb + jj < N2) {
+                        const float2 p0 = t0[jj], p1 = t1[jj]; // u = b u + d conj(tw)
+                        float2 r = md == 1 ? uu[jj] : float2{0.f, 0.f};
+                        r.x = fmaf(a0.x, p0.x, r.x);
+                        r.y = fmaf(a0.y, p0.x, r.y);
+                        r.x = fmaf(a0.y, p0.y, r.x);
+                        r.y = fmaf(-a0.x, p0.y, r.y);
+                        r.x = fmaf(a1.x, p1.x, r.x);
+                        r.y = fmaf(a1.y, p1.x, r.y);
+                        r.x = fmaf(a1.y, p1.y, r.x);
+                        r.y = fmaf(-a1.x, p1.y, r.y);
+                        row[(jb + jj) * W] = r;
+                    }
+                }
+            } else {
+                // general rows: any number of terms, twiddles indexed on the fly
+                float2 rr[JH];
+#pragma unroll
+                for (int jj = 0; jj < JH; jj++)
+                    rr[jj] = md == 1 ? uu[jj] : float2{0.f, 0.f};
+                for (int t = off; t < off + nt; t++) {
+                    const int k = pl.tk[t];
+                    const int m00 = (jb * k) % Y;
+                    int m0 = m00;
+                    float2 e0{0.f, 0.f};
+#pragma unroll
+                    for (int jj = 0; jj < JH; jj++) {
+                        if (jb + jj < N2) {
+                            const float2 tv = stw[m0];
+                            e0.x = fmaf(uu[jj].x, tv.x, e0.x);
+                            e0.y = fmaf(uu[jj].x, tv.y, e0.y);
+                            e0.x = fmaf(-uu[jj].y, tv.y, e0.x);
+                            e0.y = fmaf(uu[jj].y, tv.x, e0.y);
+                        }
+                        m0 += k;
+                        m0 -= m0 >= Y ? Y : 0;
+                    }
+                    e0.x += __shfl_xor_sync(pmask, e0.x, 1);
+                    e0.y += __shfl_xor_sync(pmask, e0.y, 1);
+                    e0 = cmul(e0, pl.coef[t]);
+                    m0 = m00;
+#pragma unroll
+                    for (int jj = 0; jj < JH; jj++) {
+                        if (jb + jj < N2) {
+                            const float2 tv = stw[m0];
+                            rr[jj].x = fmaf(e0.x, tv.x, rr[jj].x);
+                            rr[jj].y = fmaf(e0.y, tv.x, rr[jj].y);
+                            rr[jj].x = fmaf(e0.y, tv.y, rr[jj].x);
+                            rr[jj].y = fmaf(-e0.x, tv.y, rr[jj].y);
+                        }
+                        m0 += k;
+                        m0 -= m0 >= Y ? Y : 0;
+                    }
+                }
+#pragma unroll
+                for (int jj = 0; jj < JH; jj++)
+                    if (jb + jj < N2)
+                        row[(jb + jj) * W] = rr[jj];
+            }
+        }
+        __syncthreads();
     }
     if (a.mode == 1) {
         part = block_sum2(part);
@@ -504,12 +573,12 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
     r.strips = r.nxb * g.B;
     r.units = r.strips * g.C;
     r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : 2L * ctx().sm_count, r.strips));
-    r.ok = g.Y * g.C * g.B < (1L << 31);
+    r.ok = r.units < (1L << 30) && g.Y * g.C * g.B < (1L << 30) && g.X * g.Y < (1L << 30);
     return r;
 }
 
 template<int N1, int N2>
-void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g)
+void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const unsigned char* plans)
 {
     using Cfg = RankCfg<N1, N2>;
     CUtensorMap m;
@@ -532,11 +601,31 @@ void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g)
     const double xyb = double(g.X) * g.Y * g.B;
     const double work = 8.0 * xyb * (g.C + (a.mode == 1 ? 4 : 2));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    kern<<<a.G, Cfg::NT, Cfg::SMEM, ctx().stream>>>(a, m);
+    kern<<<a.G, Cfg::NT, Cfg::SMEM, ctx().stream>>>(a, m, plans);
     KERNEL_CHECK();
 }
 
-void launch_rank(const RankPlan& rp, RankArgs a, const cfloat* coils, const SenseGeom& g)
+// per-item row plans of the pattern (once per pattern, before the launches that use it)
+template<int N1, int N2>
+void launch_rank_plan_t(const RankArgs& a, unsigned char* plans, int nitems)
+{
+    k_rank_plan<N1, N2><<<nitems, RankCfg<N1, N2>::NT, 0, ctx().stream>>>(a, plans);
+    KERNEL_CHECK();
+}
+
+#define RANK_SHAPES(X_) X_(128, 8, 16) X_(256, 16, 16) X_(320, 16, 20) X_(368, 16, 23) X_(512, 16, 32) X_(640, 16, 40)
+
+// device memory for the per-item plans of a pattern
+size_t rank_plan_bytes(const SenseGeom& g)
+{
+    const long items = g.pat_b > 1 ? g.pat_b : 1;
+#define X_(YY, A1, A2) \
+    case YY: return RankPlanRec<A1, A2>::BYTES * items;
+    switch (g.Y) { RANK_SHAPES(X_) default: return 0; }
+#undef X_
+}
+
+void fill_rank_args(const RankPlan& rp, RankArgs& a, const SenseGeom& g)
 {
     a.tw = fast_twiddles(rp.N1, rp.N2);
     a.X = g.X;
@@ -545,13 +634,24 @@ void launch_rank(const RankPlan& rp, RankArgs a, const cfloat* coils, const Sens
     a.nxb = rp.nxb;
     a.units = rp.units;
     a.G = rp.G;
-    switch (g.Y) {
-    case 128: launch_rank_t<8, 16>(a, coils, g); break;
-    case 256: launch_rank_t<16, 16>(a, coils, g); break;
-    case 320: launch_rank_t<16, 20>(a, coils, g); break;
-    case 368: launch_rank_t<16, 23>(a, coils, g); break;
-    case 512: launch_rank_t<16, 32>(a, coils, g); break;
-    case 640: launch_rank_t<16, 40>(a, coils, g); break;
-    default: throw Error("rank A^H A: unsupported Y");
-    }
+}
+
+void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsigned char* plans)
+{
+    fill_rank_args(rp, a, g);
+    const int items = int(g.pat_b > 1 ? g.pat_b : 1);
+#define X_(YY, A1, A2) \
+    case YY: launch_rank_plan_t<A1, A2>(a, plans, items); return;
+    switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }
+#undef X_
+}
+
+void launch_rank(const RankPlan& rp, RankArgs a, const cfloat* coils, const SenseGeom& g,
+                 const unsigned char* plans)
+{
+    fill_rank_args(rp, a, g);
+#define X_(YY, A1, A2) \
+    case YY: launch_rank_t<A1, A2>(a, coils, g, plans); return;
+    switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }
+#undef X_
 }

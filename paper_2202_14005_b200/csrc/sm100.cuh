@@ -35,8 +35,24 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
 }
 // Bounded wait: a pipeline that never completes (e.g. a TMA transaction-count
 // mismatch) traps after ~4 s instead of hanging the device.
+__device__ __forceinline__ uint32_t mbar_try(uint64_t* bar, uint32_t phase)
+{
+    uint32_t done;
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t"
+        "}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return done;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase)
 {
+    if (mbar_try(bar, phase))
+        return;
     const long long t0 = clock64();
     uint32_t done = 0;
     while (true) {

@@ -136,4 +136,4 @@ def test_rank_deterministic(gpu, ref, rank_opts):
     gpu.check(gpu.so.mdnn_set_option(b"sense_rank_ctas", 7))
     a = _normal(gpu, cm, pat, ph)
     b = _normal(gpu, cm, pat, ph)
-    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.array_equal(np.ascontiguousarray(a).view(np.uint32), np.ascontiguousarray(b).view(np.uint32))

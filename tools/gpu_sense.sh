@@ -1,7 +1,7 @@
 #!/bin/bash
 # SENSE-only GPU pass: sense parity tests + micro-bench (+ optional ncu of k_normal)
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_sense_rank.py tests/test_gpu_sense.py tests/test_gpu_golden.py -x -q > gpurun_out/pytest_sense.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_sense.log
+timeout 600 python -m pytest --timeout 120 tests/test_gpu_sense_rank.py tests/test_gpu_sense.py tests/test_gpu_golden.py -x -q > gpurun_out/pytest_sense.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_sense.log
 timeout 300 python tools/sense_bench.py 320 368 15 8 640 368 15 4 256 256 8 16 512 512 32 4 > gpurun_out/sense_bench.log 2>&1
 if [ -n "$NCU" ]; then
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_normal -s 6 -c 2 \
