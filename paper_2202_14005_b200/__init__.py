@@ -13,7 +13,7 @@ from .capi import Lib, MdnnError  # noqa: F401
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libmdnn_b200.so")
+LIB_PATH = os.environ.get("MDNN_B200_LIB") or os.path.join(PKG_DIR, "libmdnn_b200.so")  # env: A/B builds
 
 _lib = None
 

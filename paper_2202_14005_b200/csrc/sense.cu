@@ -584,7 +584,7 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
         const RankPlan rp = rank_plan(g, coils);
         if (rp.ok) {
             DArray plane1(Dims{g.X * g.Y * g.B}, false);
-            DArray plans(Dims{long((rank_plan_bytes(g) + 7) / 8)}, false);
+            DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
             RankArgs a{};
             a.out = out;
             a.out1 = plane1.data();
@@ -598,12 +598,9 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
             launch_rank_plan(rp, a, g, pl);
             launch_rank(rp, a, coils, g, pl);
             const long n = g.X * g.Y * g.B;
-            if (rp.W == 8)
-                k_rank_merge<8><<<grid_for(n), kT, 0, ctx().stream>>>(out, plane1.data(), g.X, g.Y, g.B, rp.nxb, g.C,
-                                                                      rp.units, rp.G);
-            else
-                k_rank_merge<4><<<grid_for(n), kT, 0, ctx().stream>>>(out, plane1.data(), g.X, g.Y, g.B, rp.nxb, g.C,
-                                                                      rp.units, rp.G);
+            k_rank_merge<<<grid_for(n), 256, 0, ctx().stream>>>(out, plane1.data(), rank_split_flags(g, pl),
+                                                                int(g.X), int(g.Y * g.B), int(g.Y), int(rp.nxb),
+                                                                rp.W == 8 ? 3 : 2);
             KERNEL_CHECK();
             return;
         }
@@ -748,9 +745,11 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
     if (rp.ok) {
         // persistent rank kernel: Ap in plane 0 (+ plane 1 for split strips);
         // p ping-pongs between two buffers (no CTA reads a p another rewrites)
-        CgMem m = cg_alloc(max_iter, tol, rp.G, n_upd);
+        // few update CTAs: one contended counter atomic per CTA in publish_partial
+        const int n_updr = int(std::min<long>(2L * c.sm_count, g.Y * g.B));
+        CgMem m = cg_alloc(max_iter, tol, rp.G, n_updr);
         DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{2 * n}, false);
-        DArray plans(Dims{long((rank_plan_bytes(g) + 7) / 8)}, false);
+        DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
         unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
         cfloat* P[2] = {pb.data(), pb.data() + n};
         cg_start(m, x, b, r.data(), P[1], n);
@@ -775,14 +774,11 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             a.cg = m.st;
             a.errflags = c.d_errflags;
             launch_rank(rp, a, coils, g, pl);
-            if (rp.W == 8)
-                k_cg_update_rank<8><<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
-                                                                ap.data() + n, g.X, g.Y, g.B, rp.nxb, g.C, rp.units,
-                                                                rp.G, c.d_errflags);
-            else
-                k_cg_update_rank<4><<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
-                                                                ap.data() + n, g.X, g.Y, g.B, rp.nxb, g.C, rp.units,
-                                                                rp.G, c.d_errflags);
+            ProfScope prof("cg_update_rank", 8.0 * n * 7);
+            k_cg_update_rank<<<n_updr, 512, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
+                                                          ap.data() + n, rank_split_flags(g, pl), int(g.X),
+                                                          int(g.Y * g.B), int(g.Y), int(rp.nxb),
+                                                          rp.W == 8 ? 3 : 2, c.d_errflags);
             KERNEL_CHECK();
         }
         k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);

@@ -24,6 +24,8 @@
 //    coil and all threads busy in both long phases.
 #pragma once
 
+#include <type_traits>
+
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
 
 constexpr int rank_nbox(int Y)
@@ -37,17 +39,24 @@ constexpr int rank_nbox(int Y)
 template<int N1, int N2>
 struct RankCfg {
     static constexpr int Y = N1 * N2;
-    static constexpr int W = N2 <= 24 ? 8 : 4;             // columns per strip
+#ifndef RANK_W
+#define RANK_W 8
+#endif
+    static constexpr int W = N2 <= 24 ? RANK_W : 4;        // columns per strip
     static constexpr int NT = ((W * N2 + 31) / 32) * 32;   // threads (w, j)
-    static constexpr int JH = (N2 + 1) / 2;                // j per half-row (stage-B thread pairs)
-    static constexpr int TMAX = 32;                        // terms per CTA
+    static constexpr int N2P = N2 + (N2 & 1);              // S / twiddle row pitch (even: unguarded halves)
+    static constexpr int JH = N2P / 2;                     // j per half-row (stage-B thread pairs)
+    static constexpr int TMAX = W == 8 ? 32 : 24;          // terms with precomputed twiddle rows
     static constexpr int NBOX = rank_nbox(Y);              // TMA boxes per coil slice (rows <= 256)
     static constexpr int BOXR = Y / NBOX;
     static constexpr size_t SLOT = size_t(Y) * W;          // float2 per ring slot / S / xs
-    // dynamic smem (float2): ring[2][SLOT] | S[SLOT] | xs[SLOT] | ttw[TMAX*N2] | stw[Y]
-    static constexpr size_t SMEM = sizeof(float2) * (4 * SLOT + TMAX * N2 + Y) + 128;
-    static constexpr int MINB = 2 * (SMEM + 4096) <= 228 * 1024 ? 2 : 1;
+    static constexpr size_t SSLOT = size_t(N1) * N2P * W;  // S (row pitch N2P)
+    // dynamic smem (float2): ring[2][SLOT] | S[SSLOT] | xs[SLOT] | ttw[TMAX*N2P]
+    static constexpr size_t SMEM = sizeof(float2) * (3 * SLOT + SSLOT + TMAX * N2P);
+    static constexpr int MINB = 4 * (SMEM + 4096) <= 228 * 1024 ? 4 : 3 * (SMEM + 4096) <= 228 * 1024 ? 3
+                              : 2 * (SMEM + 4096) <= 228 * 1024 ? 2 : 1;
     static_assert(Y % NBOX == 0, "TMA box rows must tile Y");
+    static_assert(JH % 2 == 0, "stage-B half rows are read as float4 pairs");
 };
 
 struct RankArgs {
@@ -145,9 +154,10 @@ __device__ void rank_build_plan(RankPlanSm<N1, N2>& pl, const RankArgs& a, int b
         }
     }
     __syncthreads();
-    for (int e = tid; e < min(pl.T, TMAX) * N2; e += NT) {
-        const int t = e / N2, jj = e % N2;
-        ttw[e] = stw[(jj * pl.tk[t]) % Y];
+    constexpr int N2P = Cfg::N2P;
+    for (int e = tid; e < min(pl.T, TMAX) * N2P; e += NT) {
+        const int t = e / N2P, jj = e % N2P;
+        ttw[e] = jj < N2 ? stw[(jj * pl.tk[t]) % Y] : float2{0.f, 0.f}; // zero pad: no contribution
     }
     __syncthreads();
 }
@@ -156,7 +166,7 @@ __device__ void rank_build_plan(RankPlanSm<N1, N2>& pl, const RankArgs& a, int b
 template<int N1, int N2>
 struct RankPlanRec {
     static constexpr size_t PL = (sizeof(RankPlanSm<N1, N2>) + 15) & ~size_t(15);
-    static constexpr size_t BYTES = PL + sizeof(float2) * RankCfg<N1, N2>::TMAX * N2;
+    static constexpr size_t BYTES = PL + sizeof(float2) * RankCfg<N1, N2>::TMAX * RankCfg<N1, N2>::N2P;
 };
 
 // one CTA per pattern item (grid = 1 for a broadcast pattern)
@@ -174,13 +184,12 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
 {
     using namespace fftd;
     using Cfg = RankCfg<N1, N2>;
-    constexpr int Y = Cfg::Y, W = Cfg::W, NT = Cfg::NT, JH = Cfg::JH, TMAX = Cfg::TMAX;
+    constexpr int Y = Cfg::Y, W = Cfg::W, NT = Cfg::NT, JH = Cfg::JH, TMAX = Cfg::TMAX, N2P = Cfg::N2P;
     extern __shared__ __align__(128) float2 rank_smem[];
     float2* ring = rank_smem;
     float2* S = ring + 2 * Cfg::SLOT;
-    float2* xs = S + Cfg::SLOT;
+    float2* xs = S + Cfg::SSLOT;
     float2* ttw = xs + Cfg::SLOT;
-    float2* stw = ttw + TMAX * N2;
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ float s_beta;
     __shared__ float2 s_lam;
@@ -215,8 +224,10 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
         s_beta = a.mode == 1 ? cg_prologue(a.cg, a.it, a.errflags) : 0.f;
         s_lam = a.lam ? a.lam[0] : float2{0.f, 0.f};
     }
-    for (int e = tid; e < Y; e += NT)
-        stw[e] = a.tw[e];
+    if constexpr (N2P != N2) { // pad column of S stays zero (read by stage B, never by A/C)
+        for (int e = tid; e < N1 * W; e += NT)
+            S[((e / W) * N2P + N2) * W + e % W] = float2{0.f, 0.f};
+    }
     __syncthreads();
     const float beta = s_beta;
     if (a.mode == 1 && beta < 0.f) {
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
             float2 v[N1];
 #pragma unroll
             for (int k1 = 0; k1 < N1; k1++)
-                v[k1] = S[(k1 * N2 + j) * W + w];
+                v[k1] = S[(k1 * N2P + j) * W + w];
             dft_reg<N1, +1>(v);
 #pragma unroll
             for (int q = 0; q < N1; q++) {
@@ -292,7 +303,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
                         dpl[e] = src[e];
                     const int4* src2 = reinterpret_cast<const int4*>(reinterpret_cast<const unsigned char*>(src) + Rec::PL);
                     int4* dtw = reinterpret_cast<int4*>(ttw);
-                    for (int e = tid; e < int(TMAX * N2 * sizeof(float2) / 16); e += NT)
+                    for (int e = tid; e < int(TMAX * N2P * sizeof(float2) / 16); e += NT)
                         dtw[e] = src2[e];
                     __syncthreads();
                     plan_b = b;
@@ -350,7 +361,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
             if (active) {
 #pragma unroll
                 for (int k1 = 0; k1 < N1; k1++)
-                    S[(k1 * N2 + j) * W + w] = v[k1];
+                    S[(k1 * N2P + j) * W + w] = v[k1];
             }
         }
         __syncthreads();
@@ -372,24 +383,28 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
                 nt = pl.nt[k1];
                 off = pl.off[k1];
             }
-            float2* row = S + k1 * N2 * W + ww;
+            float2* row = S + k1 * N2P * W + ww;
             const unsigned pmask = 3u << ((tid & 31) & ~1);
             const int jb = h * JH;
             float2 uu[JH];
 #pragma unroll
             for (int jj = 0; jj < JH; jj++)
-                uu[jj] = (jb + jj < N2) ? row[(jb + jj) * W] : float2{0.f, 0.f};
+                uu[jj] = row[(jb + jj) * W]; // pad column: finite junk times a zero twiddle
             if (nt <= 2 && off + nt <= TMAX) {
                 // common case (<= 2 terms, precomputed twiddle rows): both dot
                 // products in one pass (4 independent chains), then in place
                 const bool two = nt == 2;
-                const float2* t0 = ttw + off * N2 + jb;
-                const float2* t1 = ttw + (two ? off + 1 : off) * N2 + jb;
+                const float2* t0 = ttw + off * N2P + jb;
+                const float2* t1 = ttw + (two ? off + 1 : off) * N2P + jb;
                 float2 a0{0.f, 0.f}, a1{0.f, 0.f};
+                const float4* t0v = reinterpret_cast<const float4*>(t0); // 16-B aligned: N2P, jb even
+                const float4* t1v = reinterpret_cast<const float4*>(t1);
 #pragma unroll
                 for (int jj = 0; jj < JH; jj++) {
-                    if (jb + jj < N2) {
-                        const float2 p0 = t0[jj], p1 = t1[jj];
+                    {
+                        const float4 q0 = t0v[jj >> 1], q1 = t1v[jj >> 1];
+                        const float2 p0 = (jj & 1) ? float2{q0.z, q0.w} : float2{q0.x, q0.y};
+                        const float2 p1 = (jj & 1) ? float2{q1.z, q1.w} : float2{q1.x, q1.y};
                         a0.x = fmaf(uu[jj].x, p0.x, a0.x);
                         a0.y = fmaf(uu[jj].x, p0.y, a0.y);
                         a1.x = fmaf(uu[jj].x, p1.x, a1.x);
@@ -406,13 +421,20 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
                 a1.y += __shfl_xor_sync(pmask, a1.y, 1);
                 a0 = nt > 0 ? cmul(a0, pl.coef[off]) : float2{0.f, 0.f};
                 a1 = two ? cmul(a1, pl.coef[off + 1]) : float2{0.f, 0.f};
+                auto scatter = [&](auto keep) { // u = b u + d conj(tw), b as a compile-time flag
 #pragma unroll
-                for (int jj = 0; jj < JH; jj++) {
-                    if (jb + jj < N2) {
-                        const float2 p0 = t0[jj], p1 = t1[jj]; // u = b u + d conj(tw)
-                        float2 r = md == 1 ? uu[jj] : float2{0.f, 0.f};
-                        r.x = fmaf(a0.x, p0.x, r.x);
-                        r.y = fmaf(a0.y, p0.x, r.y);
+                    for (int jj = 0; jj < JH; jj++) {
+                        const float4 q0 = t0v[jj >> 1], q1 = t1v[jj >> 1];
+                        const float2 p0 = (jj & 1) ? float2{q0.z, q0.w} : float2{q0.x, q0.y};
+                        const float2 p1 = (jj & 1) ? float2{q1.z, q1.w} : float2{q1.x, q1.y};
+                        float2 r;
+                        if constexpr (decltype(keep)::value) {
+                            r.x = fmaf(a0.x, p0.x, uu[jj].x);
+                            r.y = fmaf(a0.y, p0.x, uu[jj].y);
+                        } else {
+                            r.x = a0.x * p0.x;
+                            r.y = a0.y * p0.x;
+                        }
                         r.x = fmaf(a0.y, p0.y, r.x);
                         r.y = fmaf(-a0.x, p0.y, r.y);
                         r.x = fmaf(a1.x, p1.x, r.x);
@@ -421,7 +443,11 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
                         r.y = fmaf(-a1.x, p1.y, r.y);
                         row[(jb + jj) * W] = r;
                     }
-                }
+                };
+                if (md == 1)
+                    scatter(std::true_type{});
+                else
+                    scatter(std::false_type{});
             } else {
                 // general rows: any number of terms, twiddles indexed on the fly
                 float2 rr[JH];
@@ -436,7 +462,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
 #pragma unroll
                     for (int jj = 0; jj < JH; jj++) {
                         if (jb + jj < N2) {
-                            const float2 tv = stw[m0];
+                            const float2 tv = __ldg(&a.tw[m0]);
                             e0.x = fmaf(uu[jj].x, tv.x, e0.x);
                             e0.y = fmaf(uu[jj].x, tv.y, e0.y);
                             e0.x = fmaf(-uu[jj].y, tv.y, e0.x);
@@ -452,7 +478,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
 #pragma unroll
                     for (int jj = 0; jj < JH; jj++) {
                         if (jb + jj < N2) {
-                            const float2 tv = stw[m0];
+                            const float2 tv = __ldg(&a.tw[m0]);
                             rr[jj].x = fmaf(e0.x, tv.x, rr[jj].x);
                             rr[jj].y = fmaf(e0.y, tv.x, rr[jj].y);
                             rr[jj].x = fmaf(e0.y, tv.y, rr[jj].x);
@@ -477,56 +503,116 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
 }
 
 // out (+)= plane 1 for pixels of split strips (mode 0 result assembly)
-template<int W>
-__global__ void k_rank_merge(cfloat* out, const cfloat* plane1, long X, long Y, long B, long nxb, long C, long U,
-                             long G)
+__global__ void __launch_bounds__(256) k_rank_merge(cfloat* out, const cfloat* plane1,
+                                                    const unsigned char* __restrict__ split, int X, int rows, int Y,
+                                                    int nxb, int wshift)
 {
-    const long n = X * Y * B;
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-        const long x = i % X, b = i / (X * Y);
-        const long s = b * nxb + x / W;
-        if (rank_split(s, C, U, G)) {
-            float2 o = out[i];
-            const float2 t = plane1[i];
-            out[i] = float2{o.x + t.x, o.y + t.y};
+    const int X2 = X >> 1;
+    for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int sb = (row / Y) * nxb;
+        const long base = long(row) * X2;
+        for (int xp = threadIdx.x; xp < X2; xp += blockDim.x) {
+            if (!split[sb + ((2 * xp) >> wshift)])
+                continue;
+            const long i = base + xp;
+            float4 o = reinterpret_cast<float4*>(out)[i];
+            const float4 t = reinterpret_cast<const float4*>(plane1)[i];
+            o.x += t.x;
+            o.y += t.y;
+            o.z += t.z;
+            o.w += t.w;
+            reinterpret_cast<float4*>(out)[i] = o;
         }
     }
 }
 
-// CG update with the two-plane Ap: x += alpha p ; r -= alpha Ap ; <r, r> partial
-template<int W>
-__global__ void k_cg_update_rank(CgDev* st, int it, cfloat* x, cfloat* r, const cfloat* p, const cfloat* ap,
-                                 const cfloat* ap1, long X, long Y, long B, long nxb, long C, long U, long G,
-                                 unsigned* errflags)
+// CG update with the two-plane Ap: x += alpha p ; r -= alpha Ap ; <r, r> partial.
+// Blocks walk whole image rows (no per-element division), two complex per
+// thread (float4); split[s] flags strips whose Ap has a plane-1 part.
+__global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloat* __restrict__ x,
+                                                        cfloat* __restrict__ r, const cfloat* __restrict__ p,
+                                                        const cfloat* __restrict__ ap,
+                                                        const cfloat* __restrict__ ap1,
+                                                        const unsigned char* __restrict__ split, int X, int rows,
+                                                        int Y, int nxb, int wshift, unsigned* errflags)
 {
     __shared__ float s_alpha;
     if (threadIdx.x == 0)
         s_alpha = cg_alpha(st, it, errflags);
+    const int X2 = X >> 1;
+    const int npair = rows * X2;
+    const int stride = gridDim.x * blockDim.x;
+    const float4* ap4 = reinterpret_cast<const float4*>(ap);
+    const float4* ap14 = reinterpret_cast<const float4*>(ap1);
+    const float4* p4 = reinterpret_cast<const float4*>(p);
+    float4* x4 = reinterpret_cast<float4*>(x);
+    float4* r4 = reinterpret_cast<float4*>(r);
+    constexpr int U = 2; // element pairs in flight per thread
+    float4 av[U], t1[U], pv[U], xv[U], rv[U];
+    bool sp[U], ok[U];
+    int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    auto load = [&](int base) {
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            const int i = base + k * stride;
+            ok[k] = i < npair;
+            const int ii = ok[k] ? i : 0;
+            av[k] = ap4[ii];
+            t1[k] = ap14[ii]; // junk outside split strips: not used there
+            pv[k] = p4[ii];
+            xv[k] = x4[ii];
+            rv[k] = r4[ii];
+            const int row = ii / X2, xp = ii - row * X2;
+            sp[k] = split[(row / Y) * nxb + ((2 * xp) >> wshift)];
+        }
+    };
+    load(i0);
     __syncthreads();
     const float al = s_alpha;
     if (!(al > 0.f))
         return;
-    const long n = X * Y * B;
     double2 part{0, 0};
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-        const long xq = i % X, b = i / (X * Y);
-        float2 av = ap[i];
-        if (rank_split(b * nxb + xq / W, C, U, G)) {
-            const float2 t = ap1[i];
-            av.x += t.x;
-            av.y += t.y;
+    while (true) {
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            if (!ok[k])
+                continue;
+            float4 a = av[k];
+            if (sp[k]) {
+                a.x += t1[k].x;
+                a.y += t1[k].y;
+                a.z += t1[k].z;
+                a.w += t1[k].w;
+            }
+            float4 xx = xv[k], rr = rv[k];
+            xx.x += al * pv[k].x;
+            xx.y += al * pv[k].y;
+            xx.z += al * pv[k].z;
+            xx.w += al * pv[k].w;
+            rr.x += -al * a.x;
+            rr.y += -al * a.y;
+            rr.z += -al * a.z;
+            rr.w += -al * a.w;
+            const int i = i0 + k * stride;
+            x4[i] = xx;
+            r4[i] = rr;
+            part.x += double(rr.x) * rr.x + double(rr.y) * rr.y;
+            part.x += double(rr.z) * rr.z + double(rr.w) * rr.w;
         }
-        float2 pv = p[i], xv = x[i], rv = r[i];
-        xv.x += al * pv.x;
-        xv.y += al * pv.y;
-        rv.x += -al * av.x;
-        rv.y += -al * av.y;
-        x[i] = xv;
-        r[i] = rv;
-        part.x += double(rv.x) * rv.x + double(rv.y) * rv.y;
+        i0 += U * stride;
+        if (i0 >= npair)
+            break;
+        load(i0);
     }
     part = block_sum2(part);
     publish_partial(st->part_rr, &st->rr_sum, &st->cnt_rr, part);
+}
+
+// split flags of every strip (written once per plan buffer)
+__global__ void k_rank_split_flags(unsigned char* flags, long strips, long C, long U, long G)
+{
+    for (long s = blockIdx.x * long(blockDim.x) + threadIdx.x; s < strips; s += long(gridDim.x) * blockDim.x)
+        flags[s] = rank_split(s, C, U, G) ? 1 : 0;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 rank_encode_fn()
@@ -568,11 +654,20 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
         return r;
     r.N1 = n1;
     r.N2 = n2;
-    r.W = n2 <= 24 ? 8 : 4;
+    r.W = n2 <= 24 ? RANK_W : 4;
     r.nxb = (g.X + r.W - 1) / r.W;
     r.strips = r.nxb * g.B;
     r.units = r.strips * g.C;
-    r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : 2L * ctx().sm_count, r.strips));
+    int minb = 1;
+    switch (g.Y) {
+    case 128: minb = RankCfg<8, 16>::MINB; break;
+    case 256: minb = RankCfg<16, 16>::MINB; break;
+    case 320: minb = RankCfg<16, 20>::MINB; break;
+    case 368: minb = RankCfg<16, 23>::MINB; break;
+    case 512: minb = RankCfg<16, 32>::MINB; break;
+    case 640: minb = RankCfg<16, 40>::MINB; break;
+    }
+    r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : long(minb) * ctx().sm_count, r.strips));
     r.ok = r.units < (1L << 30) && g.Y * g.C * g.B < (1L << 30) && g.X * g.Y < (1L << 30);
     return r;
 }
@@ -616,13 +711,19 @@ void launch_rank_plan_t(const RankArgs& a, unsigned char* plans, int nitems)
 #define RANK_SHAPES(X_) X_(128, 8, 16) X_(256, 16, 16) X_(320, 16, 20) X_(368, 16, 23) X_(512, 16, 32) X_(640, 16, 40)
 
 // device memory for the per-item plans of a pattern
-size_t rank_plan_bytes(const SenseGeom& g)
+size_t rank_plan_record_bytes(const SenseGeom& g)
 {
     const long items = g.pat_b > 1 ? g.pat_b : 1;
 #define X_(YY, A1, A2) \
     case YY: return RankPlanRec<A1, A2>::BYTES * items;
     switch (g.Y) { RANK_SHAPES(X_) default: return 0; }
 #undef X_
+}
+// [per-item plan records | split flag per strip]
+size_t rank_plan_bytes(const SenseGeom& g, const RankPlan& rp) { return rank_plan_record_bytes(g) + size_t(rp.strips); }
+const unsigned char* rank_split_flags(const SenseGeom& g, const unsigned char* plans)
+{
+    return plans + rank_plan_record_bytes(g);
 }
 
 void fill_rank_args(const RankPlan& rp, RankArgs& a, const SenseGeom& g)
@@ -640,6 +741,9 @@ void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsign
 {
     fill_rank_args(rp, a, g);
     const int items = int(g.pat_b > 1 ? g.pat_b : 1);
+    k_rank_split_flags<<<int(std::min<long>((rp.strips + 255) / 256, 64)), 256, 0, ctx().stream>>>(
+        plans + rank_plan_record_bytes(g), rp.strips, g.C, rp.units, rp.G);
+    KERNEL_CHECK();
 #define X_(YY, A1, A2) \
     case YY: launch_rank_plan_t<A1, A2>(a, plans, items); return;
     switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }

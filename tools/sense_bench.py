@@ -64,27 +64,32 @@ def main():
             gb = 8.0 * B * X * Y * (NC + 2) / 1e9
             res.update(apply_us=1e3 * ms, apply_gbs=gb / (ms / 1e3), apply_frac=gb / (ms / 1e3) / peak)
         if args.cg:
-            lib.check(lib.so.mdnn_profile_reset())
-            lib.check(lib.so.mdnn_profile_enable(1))
             it = C.c_long()
             st = (C.c_double * 3)()
-            for _ in range(2):
+
+            def solve():
                 lib.check(lib.so.mdnn_cg_normal_solve(C.byref(A[0]), C.byref(A[1]), C.c_float(0.05), C.byref(A[2]),
                                                       10, C.c_double(0.0), C.byref(A[3]), C.byref(it), st))
+            for _ in range(2):
+                solve()
             lib.check(lib.so.mdnn_synchronize())
-            lib.check(lib.so.mdnn_profile_reset())
             n = max(1, args.iters // 4)
             e0.record(stream)
             for _ in range(n):
-                lib.check(lib.so.mdnn_cg_normal_solve(C.byref(A[0]), C.byref(A[1]), C.c_float(0.05), C.byref(A[2]),
-                                                      10, C.c_double(0.0), C.byref(A[3]), C.byref(it), st))
+                solve()
             e1.record(stream)
             lib.check(lib.so.mdnn_synchronize())
             ms = e0.elapsed_time(e1) / n
             gb = 10 * 8.0 * B * X * Y * (NC + 10) / 1e9
             res.update(cg10_ms=ms, cg10_gbs=gb / (ms / 1e3), cg10_frac=gb / (ms / 1e3) / peak, cg_iters=it.value)
+            # per-kernel device times from a separate profiled pass (events cost launch gaps)
+            lib.check(lib.so.mdnn_profile_reset())
+            lib.check(lib.so.mdnn_profile_enable(1))
+            for _ in range(n):
+                solve()
+            lib.check(lib.so.mdnn_synchronize())
             cnt, tms, work = C.c_long(), C.c_double(), C.c_double()
-            for tag in ("sense_normal_y_cg", "cg_update"):
+            for tag in ("sense_normal_y_cg", "cg_update_rank"):
                 lib.check(lib.so.mdnn_profile_read(tag.encode(), C.byref(cnt), C.byref(tms), C.byref(work)))
                 if cnt.value:
                     res[tag + "_us"] = 1e3 * tms.value / cnt.value
