@@ -12,4 +12,4 @@ if [ -n "$NCU_LIST" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_list.log 2>&1
 fi
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/bench.log gpurun_out/smoke.log
+for f in gpurun_out/pytest_gpu.log gpurun_out/bench.log gpurun_out/smoke.log; do tail -n 3 $f; done
