@@ -28,8 +28,6 @@ namespace {
 
 constexpr int TX = 32, NT = 256, MAXF = 256;
 
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
-
 // U[t][f] for the 4 uses; w has dims [KX, KY, Cin, Cout]
 //   mode 0: fwd 1 -> F           U[t][f] = w[t, 0, f]
 //   mode 1: bwd-data of F -> 1   U[t][c] = conj(w[flip t, c, 0])   (expand on flipped taps)
@@ -95,25 +93,30 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
 #pragma unroll
             for (int kx = 0; kx < K - 1; kx++)
                 win[ky][kx] = tile[(row + ky) * HX + xs + kx];
-        float* rowp = out + (b * XY + long(X) * gy) * 2 * F;
-        for (int i = 0; i < seglen; i++) {
+        float* op = out + (b * XY + long(X) * gy + x0 + xs) * 2 * F + f;
+        for (int i = 0; i < seglen; i++, op += 2 * F) {
             const int px = xs + i;
 #pragma unroll
             for (int ky = 0; ky < K; ky++)
                 win[ky][K - 1] = tile[(row + ky) * HX + px + K - 1];
-            float2 acc{0.f, 0.f};
+            // two accumulator pairs (even / odd taps): 4 FFMA per complex MAC, short chains
+            float2 acc{0.f, 0.f}, acc2{0.f, 0.f};
 #pragma unroll
             for (int ky = 0; ky < K; ky++)
 #pragma unroll
                 for (int kx = 0; kx < K; kx++) {
-                    const float2 t = cmul(win[ky][kx], u[kx + K * ky]);
-                    acc.x += t.x;
-                    acc.y += t.y;
+                    const float2 w_ = win[ky][kx], uu = u[kx + K * ky];
+                    float2& a_ = ((kx + K * ky) & 1) ? acc2 : acc;
+                    a_.x = fmaf(w_.x, uu.x, a_.x);
+                    a_.y = fmaf(w_.x, uu.y, a_.y);
+                    a_.x = fmaf(-w_.y, uu.y, a_.x);
+                    a_.y = fmaf(w_.y, uu.x, a_.y);
                 }
-            const int gx = x0 + px;
-            if (gx < X) {
-                rowp[long(gx) * 2 * F + f] = acc.x;
-                rowp[long(gx) * 2 * F + F + f] = acc.y;
+            acc.x += acc2.x;
+            acc.y += acc2.y;
+            if (x0 + px < X) {
+                op[0] = acc.x;
+                op[F] = acc.y;
             }
 #pragma unroll
             for (int ky = 0; ky < K; ky++)
@@ -236,8 +239,10 @@ __global__ void __launch_bounds__(NT, K == 3 ? 2 : 1) k_thin_reduce(float2* __re
                 const float2 uu = uc[t * F + cc];
 #pragma unroll
                 for (int k = 0; k < PP; k++) {
-                    acc[k][t].x += re[k][cc] * uu.x - im[k][cc] * uu.y;
-                    acc[k][t].y += re[k][cc] * uu.y + im[k][cc] * uu.x;
+                    acc[k][t].x = fmaf(re[k][cc], uu.x, acc[k][t].x);
+                    acc[k][t].y = fmaf(re[k][cc], uu.y, acc[k][t].y);
+                    acc[k][t].x = fmaf(-im[k][cc], uu.y, acc[k][t].x);
+                    acc[k][t].y = fmaf(im[k][cc], uu.x, acc[k][t].y);
                 }
             }
     }
@@ -308,16 +313,24 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
 #pragma unroll
                 for (int kx = 0; kx < K - 1; kx++)
                     win[ky][kx] = tile[(row + ky) * HX + xs + kx];
-            const float* rowp = wide + (b * XY + long(X) * gy) * 2 * F;
             const int xend = min(seglen, X - x0 - xs);
-            float2 vn{0.f, 0.f};
-            if (xend > 0)
-                vn = float2{rowp[long(x0 + xs) * 2 * F + f], rowp[long(x0 + xs) * 2 * F + F + f]};
+            // wide operand walked with a pointer (2F floats per pixel), PD pixels
+            // of loads in flight ahead of the taps
+            constexpr int PD = 4;
+            const float* wp = wide + (b * XY + long(X) * gy + x0 + xs) * 2 * F + f;
+            float2 pre[PD];
+#pragma unroll
+            for (int d = 0; d < PD; d++)
+                pre[d] = d < xend ? float2{__ldg(wp + d * 2 * F), __ldg(wp + d * 2 * F + F)} : float2{0.f, 0.f};
+            wp += PD * 2 * F;
             for (int i = 0; i < xend; i++) {
                 const int px = xs + i;
-                const float2 v = vn;
-                if (i + 1 < xend) // software prefetch of the next wide element
-                    vn = float2{rowp[long(x0 + px + 1) * 2 * F + f], rowp[long(x0 + px + 1) * 2 * F + F + f]};
+                const float2 v = pre[0];
+#pragma unroll
+                for (int d = 0; d < PD - 1; d++)
+                    pre[d] = pre[d + 1];
+                pre[PD - 1] = i + PD < xend ? float2{__ldg(wp), __ldg(wp + F)} : float2{0.f, 0.f};
+                wp += 2 * F;
 #pragma unroll
                 for (int ky = 0; ky < K; ky++)
                     win[ky][K - 1] = tile[(row + ky) * HX + px + K - 1];
@@ -328,13 +341,18 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
                         const float2 s = win[ky][kx];
                         if (WIDE_IS_G) {
                             // v * conj(s)
-                            acc[kx + K * ky].x += v.x * s.x + v.y * s.y;
-                            acc[kx + K * ky].y += v.y * s.x - v.x * s.y;
+                            float2& a_ = acc[kx + K * ky];
+                            a_.x = fmaf(v.x, s.x, a_.x);
+                            a_.y = fmaf(v.y, s.x, a_.y);
+                            a_.x = fmaf(v.y, s.y, a_.x);
+                            a_.y = fmaf(-v.x, s.y, a_.y);
                         } else {
                             // s * conj(v)
-                            const int t = (K - 1 - kx) + K * (K - 1 - ky);
-                            acc[t].x += s.x * v.x + s.y * v.y;
-                            acc[t].y += s.y * v.x - s.x * v.y;
+                            float2& a_ = acc[(K - 1 - kx) + K * (K - 1 - ky)];
+                            a_.x = fmaf(s.x, v.x, a_.x);
+                            a_.y = fmaf(s.y, v.x, a_.y);
+                            a_.x = fmaf(s.y, v.y, a_.x);
+                            a_.y = fmaf(-s.x, v.y, a_.y);
                         }
                     }
 #pragma unroll
@@ -482,7 +500,7 @@ void conv_thin_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     const int F = int(one_in ? g.Cout : g.Cin);
     const int KK = int(g.KX * g.KY);
     const long ntiles = ((g.X + TX - 1) / TX) * ((g.Y + 7) / 8) * g.B;
-    const int nblk = int(std::min<long>(ntiles, 2L * c.sm_count));
+    const int nblk = int(std::min<long>(ntiles, 3L * c.sm_count));
     float2* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * nblk * KK * F, c.stream));
     {
