@@ -237,6 +237,21 @@ int mdnn_trainer_step(mdnn_trainer* t, double* loss);
 int mdnn_trainer_n_weights(const mdnn_trainer* t);
 const char* mdnn_trainer_weight_name(const mdnn_trainer* t, int k);
 
+/* ---- cfl files and weight bundles (cfl.hpp:15-142) -----------------------
+ * Byte-compatible with the reference: <base>.hdr ("# Dimensions" + 16 dims)
+ * and <base>.cfl (interleaved complex64, column-major).  Bundles: a directory
+ * of cfl pairs + manifest.txt ("format 1", sorted meta, "array <name>"). */
+int mdnn_cfl_dims(const char* base, long* dims16);                     /* cfl_read header, cfl.hpp:53-73 */
+int mdnn_cfl_read(const char* base, mdnn_array* out);                  /* cfl_read, cfl.hpp:53-88 */
+int mdnn_cfl_write(const char* base, const mdnn_array* a);             /* cfl_write, cfl.hpp:19-51 */
+/* WeightsBundle::save of every trainer weight plus n_meta key/value pairs (cfl.hpp:97-111) */
+int mdnn_weights_save(mdnn_trainer* t, const char* dir, int n_meta, const char* const* keys,
+                      const char* const* vals);
+/* WeightsBundle::load (cfl.hpp:113-135) into the trainer's weights by name */
+int mdnn_weights_load(mdnn_trainer* t, const char* dir);
+/* WeightsBundle::meta_or: copies the value (or fallback) into buf, NUL-terminated (cfl.hpp:137-141) */
+int mdnn_weights_meta(const char* dir, const char* key, const char* fallback, char* buf, long buflen);
+
 #ifdef __cplusplus
 }
 #endif

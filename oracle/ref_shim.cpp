@@ -19,6 +19,7 @@
 // REF_REAL selects float (the fp32 baseline to match) or double (truth).
 
 #include <mdnn/simulate.hpp>
+#include <mdnn/cfl.hpp>
 
 #include <cstring>
 #include <memory>
@@ -927,5 +928,106 @@ int mdnn_trainer_step(mdnn_trainer* t, double* loss)
 
 int mdnn_trainer_n_weights(const mdnn_trainer* t) { return int(t->weight_names.size()); }
 const char* mdnn_trainer_weight_name(const mdnn_trainer* t, int k) { return t->weight_names.at(k).c_str(); }
+
+} // extern "C"
+
+// ---- cfl files and weight bundles: the reference's own cfl.hpp -----------------
+namespace {
+// precision casts for the cfl legs (cfl files are complex64 by definition)
+MdArray<float> to_f32(const A& a0)
+{
+    A a = a0.has_default_strides() ? a0 : a0.clone();
+    MdArray<float> o(a.dims());
+    for (long k = 0; k < a.size(); k++)
+        o.data()[k] = std::complex<float>(float(a.data()[k].real()), float(a.data()[k].imag()));
+    return o;
+}
+A from_f32(const MdArray<float>& a)
+{
+    A o(a.dims());
+    for (long k = 0; k < a.size(); k++)
+        o.data()[k] = std::complex<R>(R(a.data()[k].real()), R(a.data()[k].imag()));
+    return o;
+}
+}
+extern "C" {
+
+int mdnn_cfl_dims(const char* base, long* dims16)
+{
+    return guard([&] {
+        // the reference reads header and payload together (cfl.hpp:53-88)
+        auto a = cfl_read(base);
+        for (int k = 0; k < max_rank; k++)
+            dims16[k] = k < a.rank() ? a.dims()[k] : 1;
+    });
+}
+
+int mdnn_cfl_read(const char* base, mdnn_array* out)
+{
+    return guard([&] {
+        auto a = cfl_read(base);
+        Dims vd(out->dims, out->dims + out->rank);
+        vd.resize(max_rank, 1);
+        Dims ad(a.dims().begin(), a.dims().end());
+        ad.resize(max_rank, 1);
+        if (vd != ad)
+            throw ShapeError(std::string("cfl_read: dims mismatch for ") + base);
+        A v = from_f32(a);
+        A r(Dims(out->dims, out->dims + out->rank));
+        std::memcpy(static_cast<void*>(r.data()), v.data(), sizeof(std::complex<R>) * size_t(v.size()));
+        to_c(r, *out);
+    });
+}
+
+int mdnn_cfl_write(const char* base, const mdnn_array* a)
+{
+    return guard([&] { cfl_write(base, to_f32(from_c(*a))); });
+}
+
+int mdnn_weights_save(mdnn_trainer* t, const char* dir, int n_meta, const char* const* keys,
+                      const char* const* vals)
+{
+    return guard([&] {
+        WeightsBundle b;
+        for (int i = 0; i < n_meta; i++)
+            b.meta[keys[i]] = vals[i];
+        for (const auto& [name, arr] : t->weights)
+            b.arrays.emplace(name, to_f32(arr));
+        b.save(dir);
+    });
+}
+
+int mdnn_weights_load(mdnn_trainer* t, const char* dir)
+{
+    return guard([&] {
+        auto b = WeightsBundle::load(dir);
+        for (const auto& [name, arr] : b.arrays) {
+            if (!t->weights.count(name))
+                throw ConfigError("no weight named " + name);
+            // cfl arrays come back with 16 dims: keep the argument's own rank
+            A w = from_f32(arr);
+            const Dims& want = t->weights[name].dims();
+            Dims wp = want, ap(arr.dims().begin(), arr.dims().end());
+            wp.resize(max_rank, 1);
+            ap.resize(max_rank, 1);
+            if (wp != ap)
+                throw ShapeError("weights bundle: array " + name + " has the wrong shape");
+            A r(want);
+            std::memcpy(static_cast<void*>(r.data()), w.data(), sizeof(std::complex<R>) * size_t(w.size()));
+            t->weights[name] = r;
+        }
+    });
+}
+
+int mdnn_weights_meta(const char* dir, const char* key, const char* fallback, char* buf, long buflen)
+{
+    return guard([&] {
+        auto b = WeightsBundle::load(dir);
+        std::string v = b.meta_or(key, fallback ? fallback : "");
+        if (long(v.size()) + 1 > buflen)
+            throw BoundsError("mdnn_weights_meta: buffer too small");
+        std::memcpy(buf, v.c_str(), v.size() + 1);
+    });
+}
 
 } // extern "C"

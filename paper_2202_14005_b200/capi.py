@@ -159,6 +159,12 @@ _SIGS = {
     "mdnn_trainer_step": (C.c_int, [P, C.POINTER(C.c_double)]),
     "mdnn_trainer_n_weights": (C.c_int, [P]),
     "mdnn_trainer_weight_name": (C.c_char_p, [P, C.c_int]),
+    "mdnn_cfl_dims": (C.c_int, [C.c_char_p, L]),
+    "mdnn_cfl_read": (C.c_int, [C.c_char_p, C.POINTER(mdnn_array)]),
+    "mdnn_cfl_write": (C.c_int, [C.c_char_p, C.POINTER(mdnn_array)]),
+    "mdnn_weights_save": (C.c_int, [P, C.c_char_p, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]),
+    "mdnn_weights_load": (C.c_int, [P, C.c_char_p]),
+    "mdnn_weights_meta": (C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_long]),
 }
 EXPORTED_SYMBOLS = tuple(_SIGS)
 

@@ -3,11 +3,13 @@
 // cli.hpp:357-371) and keeps the message in a thread-local string.
 #include "../../include/mdnn.h"
 
+#include "cfl.h"
 #include "kernels.h"
 #include "profile.h"
 #include "train.h"
 
 #include <cstring>
+#include <fstream>
 
 using namespace mdnn;
 
@@ -700,5 +702,99 @@ int mdnn_trainer_step(mdnn_trainer* t, double* loss)
 }
 int mdnn_trainer_n_weights(const mdnn_trainer* t) { return int(t->t->weight_names().size()); }
 const char* mdnn_trainer_weight_name(const mdnn_trainer* t, int k) { return t->t->weight_names().at(k).c_str(); }
+
+} // extern "C"
+
+// ---- cfl files and weight bundles -------------------------------------------
+extern "C" {
+
+int mdnn_cfl_dims(const char* base, long* dims16)
+{
+    return guard([&] {
+        const Dims d = cfl_read_dims(base);
+        for (int k = 0; k < max_rank; k++)
+            dims16[k] = d[k];
+    });
+}
+
+int mdnn_cfl_read(const char* base, mdnn_array* out)
+{
+    return guard([&] {
+        DArray a = cfl_read(base);
+        HostView v = hv(*out);
+        Dims vd = v.dims;
+        vd.resize(max_rank, 1);
+        if (vd != a.dims)
+            throw ShapeError(std::string("cfl_read: ") + base + " has dims " + dims_to_string(a.dims)
+                             + ", output buffer " + dims_to_string(vd));
+        DArray r = a; // same buffer, the caller's (possibly shorter) rank
+        r.dims = v.dims;
+        out_arr(r, *out);
+        sync_and_check();
+    });
+}
+
+int mdnn_cfl_write(const char* base, const mdnn_array* a)
+{
+    return guard([&] {
+        cfl_write(base, in_arr(*a));
+        sync_and_check();
+    });
+}
+
+int mdnn_weights_save(mdnn_trainer* t, const char* dir, int n_meta, const char* const* keys,
+                      const char* const* vals)
+{
+    return guard([&] {
+        WeightsBundle b;
+        for (int i = 0; i < n_meta; i++)
+            b.meta[keys[i]] = vals[i];
+        for (const auto& [name, arr] : t->t->all_weights()) // weights + moving statistics (cli.hpp:219-224)
+            b.arrays.emplace(name, arr);
+        b.save(dir);
+        sync_and_check();
+    });
+}
+
+int mdnn_weights_load(mdnn_trainer* t, const char* dir)
+{
+    return guard([&] {
+        WeightsBundle b = WeightsBundle::load(dir);
+        for (auto& [name, arr] : b.arrays) {
+            // cfl arrays come back with 16 dims: keep the argument's own rank
+            const auto& all = t->t->all_weights();
+            auto it = all.find(name);
+            if (it == all.end())
+                throw ConfigError("trainer: no weight named '" + name + "'");
+            Dims want = it->second.dims, wp = want;
+            wp.resize(max_rank, 1);
+            if (wp != arr.dims)
+                throw ShapeError("weights bundle: array '" + name + "' has the wrong shape");
+            DArray r = arr;
+            r.dims = want;
+            t->t->set_weight(name, r);
+        }
+        sync_and_check();
+    });
+}
+
+int mdnn_weights_meta(const char* dir, const char* key, const char* fallback, char* buf, long buflen)
+{
+    return guard([&] {
+        // manifest only (arrays are not read)
+        std::ifstream mf(std::string(dir) + "/manifest.txt");
+        if (!mf)
+            throw IoError(std::string("missing weights manifest in ") + dir);
+        std::string line, val = fallback ? fallback : "";
+        while (std::getline(mf, line)) {
+            const auto sp = line.find(' ');
+            if (line.substr(0, sp) == key && std::string(key) != "array")
+                val = sp == std::string::npos ? "" : line.substr(sp + 1);
+        }
+        if (long(val.size()) + 1 > buflen)
+            throw BoundsError("mdnn_weights_meta: buffer too small");
+        std::memcpy(buf, val.c_str(), val.size() + 1);
+    });
+}
 
 } // extern "C"

@@ -32,6 +32,8 @@ public:
     float* grad_buffer() const { return flat_.fdata(); }
     long grad_floats() const { return 2 * flat_n_; }
     const std::vector<std::string>& weight_names() const { return wnames_; }
+    // every non-data argument (trainable weights and moving statistics), by name
+    const std::map<std::string, DArray>& all_weights() const { return weights_; }
     int kernel_launch_estimate() const { return 0; }
 
 private:

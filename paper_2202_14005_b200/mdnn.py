@@ -312,6 +312,17 @@ class Trainer:
         a = np.asfortranarray(np.asarray(a, dtype=np.complex64))
         self.lib.check(self.lib.so.mdnn_trainer_set_weight(self.h, name.encode(), C.byref(self.lib.arr(a))))
 
+    def save_weights(self, directory, meta=None):
+        """WeightsBundle::save of every weight (cfl.hpp:97-111)."""
+        meta = dict(meta or {})
+        keys = (C.c_char_p * max(1, len(meta)))(*[k.encode() for k in meta])
+        vals = (C.c_char_p * max(1, len(meta)))(*[str(v).encode() for v in meta.values()])
+        self.lib.check(self.lib.so.mdnn_weights_save(self.h, str(directory).encode(), len(meta), keys, vals))
+
+    def load_weights(self, directory):
+        """WeightsBundle::load into the weights by name (cfl.hpp:113-135)."""
+        self.lib.check(self.lib.so.mdnn_weights_load(self.h, str(directory).encode()))
+
     def weight_names(self):
         so = self.lib.so
         return [so.mdnn_trainer_weight_name(self.h, k).decode() for k in range(so.mdnn_trainer_n_weights(self.h))]
@@ -346,3 +357,30 @@ class Trainer:
         loss = C.c_double()
         self.lib.check(self.lib.so.mdnn_trainer_step(self.h, C.byref(loss)))
         return loss.value
+
+
+# ---- cfl files (cfl.hpp:19-88) ----------------------------------------------
+def cfl_dims(lib: Lib, base):
+    d = (C.c_long * 16)()
+    lib.check(lib.so.mdnn_cfl_dims(str(base).encode(), d))
+    return tuple(d[k] for k in range(16))
+
+
+def cfl_read(lib: Lib, base, out=None):
+    """Read <base>.cfl into `out` (host numpy F-order or device torch array) or a new host array."""
+    if out is None:
+        out = cfl_zeros(cfl_dims(lib, base))
+    lib.check(lib.so.mdnn_cfl_read(str(base).encode(), C.byref(lib.arr(out))))
+    return out
+
+
+def cfl_write(lib: Lib, base, a):
+    if isinstance(a, np.ndarray):
+        a = np.asfortranarray(a.astype(np.complex64))
+    lib.check(lib.so.mdnn_cfl_write(str(base).encode(), C.byref(lib.arr(a))))
+
+
+def weights_meta(lib: Lib, directory, key, fallback=""):
+    buf = C.create_string_buffer(4096)
+    lib.check(lib.so.mdnn_weights_meta(str(directory).encode(), key.encode(), fallback.encode(), buf, 4096))
+    return buf.value.decode()
