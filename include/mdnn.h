@@ -134,6 +134,10 @@ typedef struct mdnn_sense_dims {
 } mdnn_sense_dims;
 /* inverse of S with x = input 0 (recon.hpp:211-329, make_inverse_nlop :326) */
 mdnn_nlop* mdnn_nlop_inverse(const mdnn_nlop* s, long max_iter, double tol);
+/* checkpoint(f) (nlop.hpp:439-522): forward keeps only the inputs, every
+ * derivative batch re-runs the inner forward; reexecutions() of its node */
+mdnn_nlop* mdnn_nlop_checkpoint(const mdnn_nlop* f);
+long mdnn_nlop_checkpoint_reexecutions(const mdnn_nlop* h); /* -1: no checkpoint node */
 /* last CG status of an inverse node graph (recon.hpp:136-140): first InverseNode found */
 int mdnn_nlop_cg_status(const mdnn_nlop* h, long* iterations, double* rel_residual, int* converged);
 

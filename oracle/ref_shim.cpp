@@ -579,6 +579,19 @@ mdnn_nlop* mdnn_nlop_inverse(const mdnn_nlop* s, long max_iter, double tol)
     return guard_ptr<mdnn_nlop>([&] { return wrap(make_inverse_nlop<R>(s->op, max_iter, tol)); });
 }
 
+mdnn_nlop* mdnn_nlop_checkpoint(const mdnn_nlop* f)
+{
+    return guard_ptr<mdnn_nlop>([&] { return new mdnn_nlop{checkpoint(f->op)}; });
+}
+
+long mdnn_nlop_checkpoint_reexecutions(const mdnn_nlop* h)
+{
+    for (auto& n : h->op.nodes())
+        if (auto* p = dynamic_cast<CheckpointNode<R>*>(n.get()))
+            return p->reexecutions();
+    return -1;
+}
+
 int mdnn_nlop_cg_status(const mdnn_nlop* h, long* iterations, double* rel_residual, int* converged)
 {
     return guard([&] {

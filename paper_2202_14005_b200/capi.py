@@ -109,6 +109,8 @@ _SIGS = {
     "mdnn_nlop_rbf": (P, [C.c_int, L, C.c_int, C.c_int, C.POINTER(C.c_float), C.c_float]),
     "mdnn_nlop_pad": (P, [C.c_int, L, L, L]),
     "mdnn_nlop_inverse": (P, [P, C.c_long, C.c_double]),
+    "mdnn_nlop_checkpoint": (P, [P]),
+    "mdnn_nlop_checkpoint_reexecutions": (C.c_long, [P]),
     "mdnn_nlop_cg_status": (C.c_int, [P, L, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     "mdnn_sense_forward": (C.c_int, [C.POINTER(mdnn_array)] * 4),
     "mdnn_sense_adjoint": (C.c_int, [C.POINTER(mdnn_array)] * 4),

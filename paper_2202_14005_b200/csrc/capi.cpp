@@ -358,6 +358,18 @@ mdnn_nlop* mdnn_nlop_inverse(const mdnn_nlop* s, long max_iter, double tol)
     return guard_ptr<mdnn_nlop>([&] { return wrap(Nlop(node_inverse(s->op, max_iter, tol))); });
 }
 
+mdnn_nlop* mdnn_nlop_checkpoint(const mdnn_nlop* f)
+{
+    return guard_ptr<mdnn_nlop>([&] { return wrap(Nlop(node_checkpoint(f->op))); });
+}
+
+long mdnn_nlop_checkpoint_reexecutions(const mdnn_nlop* h)
+{
+    long r = -1;
+    guard([&] { r = checkpoint_reexecutions(h->op); });
+    return r;
+}
+
 int mdnn_nlop_cg_status(const mdnn_nlop* h, long* iterations, double* rel_residual, int* converged)
 {
     return guard([&] {

@@ -70,6 +70,16 @@ std::vector<DArray> Nlop::apply(const std::vector<DArray>& in)
             throw ShapeError("nlop apply: input " + std::to_string(i) + " expected " + dims_to_string(in_dims_[i])
                              + ", got " + dims_to_string(in[i].dims));
     }
+    auto out = run_forward(in, true);
+    last_gens_.resize(nodes_.size());
+    for (size_t n = 0; n < nodes_.size(); n++)
+        last_gens_[n] = nodes_[n]->generation();
+    has_forward_ = true;
+    return out;
+}
+
+std::vector<DArray> Nlop::run_forward(const std::vector<DArray>& in, bool store)
+{
     std::vector<std::vector<DArray>> vals(nodes_.size());
     std::vector<DArray> args;
     for (int ni : topo_) {
@@ -81,17 +91,13 @@ std::vector<DArray> Nlop::apply(const std::vector<DArray>& in)
             args.push_back(as_layout(v, node.in_layout(k)));
         }
         std::vector<DArray> outs(node.n_out());
-        node.forward(args, outs, true);
+        node.forward(args, outs, store);
         vals[ni] = std::move(outs);
         // release values no longer needed by later consumers is left to refcounts
     }
-    last_gens_.resize(nodes_.size());
-    for (size_t n = 0; n < nodes_.size(); n++)
-        last_gens_[n] = nodes_[n]->generation();
-    has_forward_ = true;
     std::vector<DArray> out;
     for (auto s : outputs_)
-        out.push_back(vals[s.node][s.port]);
+        out.push_back(as_layout(vals[s.node][s.port], Layout::CANON));
     return out;
 }
 

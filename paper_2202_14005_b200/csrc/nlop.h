@@ -97,6 +97,9 @@ public:
     const Dims& out_dims(int o) const;
 
     std::vector<DArray> apply(const std::vector<DArray>& in);
+    // forward sweep without the derivative bookkeeping (containers: store =
+    // false evaluates without retaining state, nlop.hpp:363-386)
+    std::vector<DArray> run_forward(const std::vector<DArray>& in, bool store);
     DArray derivative(int o, int i, const DArray& dx);
     std::vector<DArray> adjoint_all(int o, const DArray& dy, const std::vector<char>& want = {});
     DArray adjoint_derivative(int o, int i, const DArray& dy);

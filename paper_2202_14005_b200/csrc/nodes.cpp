@@ -1560,6 +1560,76 @@ NodePtr node_inverse(const Nlop& s, long max_iter, double tol)
     return std::make_shared<InverseNode>(s, max_iter, tol);
 }
 
+// ---------------------------------------------------------------------------
+// CheckpointNode (nlop.hpp:439-513).  Recompute-for-memory: the
+// inner nodes run with store = false, so only the container's inputs stay
+// alive between forward and backward.  The hot path has no stochastic nodes,
+// so there are no RNG counters to rewind.
+class CheckpointNode : public Node {
+public:
+    explicit CheckpointNode(Nlop inner) : Node("checkpoint", dims_in(inner), dims_out(inner)), inner_(std::move(inner))
+    {
+    }
+    void forward(const std::vector<DArray>& in, std::vector<DArray>& out, bool) override
+    {
+        saved_in_ = in;
+        out = inner_.run_forward(in, false);
+        bump_generation();
+    }
+    DArray deriv(int o, int i, const DArray& dx) override
+    {
+        reexecute();
+        return inner_.derivative(o, i, dx);
+    }
+    DArray adjoint(int o, int i, const DArray& dy) override
+    {
+        reexecute();
+        return inner_.adjoint_derivative(o, i, dy);
+    }
+    void adjoint_all(int o, const DArray& dy, std::vector<DArray>& dx, const std::vector<char>& want) override
+    {
+        reexecute();
+        dx = inner_.adjoint_all(o, dy, want);
+    }
+    long reexecutions() const { return reexec_; }
+
+private:
+    static std::vector<Dims> dims_in(const Nlop& f)
+    {
+        std::vector<Dims> d;
+        for (int i = 0; i < f.n_in(); i++)
+            d.push_back(f.in_dims(i));
+        return d;
+    }
+    static std::vector<Dims> dims_out(const Nlop& f)
+    {
+        std::vector<Dims> d;
+        for (int o = 0; o < f.n_out(); o++)
+            d.push_back(f.out_dims(o));
+        return d;
+    }
+    void reexecute()
+    {
+        require_forward();
+        inner_.apply(saved_in_);
+        reexec_++;
+    }
+
+    Nlop inner_;
+    std::vector<DArray> saved_in_;
+    long reexec_ = 0;
+};
+
+NodePtr node_checkpoint(const Nlop& inner) { return std::make_shared<CheckpointNode>(inner); }
+
+long checkpoint_reexecutions(const Nlop& h)
+{
+    for (auto& n : h.nodes())
+        if (auto* p = dynamic_cast<CheckpointNode*>(n.get()))
+            return p->reexecutions();
+    return -1;
+}
+
 bool inverse_status(const Nlop& h, long* iterations, double* rel, int* conv)
 {
     for (auto& n : h.nodes())

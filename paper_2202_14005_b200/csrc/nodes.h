@@ -63,6 +63,13 @@ NodePtr node_sense_adjoint(const SenseDims& sd);
 // A x as sense_forward_fragment (recon.hpp:394-400): (x, coils, pattern)
 NodePtr node_sense_forward(const SenseDims& sd);
 
+// CheckpointNode (nlop.hpp:439-513): forward keeps only the inputs (shared
+// immutable device arrays, no clones) and evaluates the inner graph without
+// derivative state; every derivative batch re-runs the inner forward first.
+NodePtr node_checkpoint(const Nlop& inner);
+// re-executions of the first checkpoint node in h (-1: none)
+long checkpoint_reexecutions(const Nlop& h);
+
 // InverseNode (recon.hpp:211-329)
 NodePtr node_inverse(const Nlop& s, long max_iter, double tol);
 bool inverse_status(const Nlop& h, long* iterations, double* rel_residual, int* converged);

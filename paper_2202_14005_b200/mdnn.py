@@ -164,6 +164,13 @@ class Nlop:
     def inverse(self, max_iter=10, tol=1e-6):
         return Nlop(self.lib, self.lib.so.mdnn_nlop_inverse(self.h, max_iter, tol))
 
+    def checkpoint(self):
+        """checkpoint(f) (nlop.hpp:516-522): recompute-for-memory container."""
+        return Nlop(self.lib, self.lib.checkp(self.lib.so.mdnn_nlop_checkpoint(self.h)))
+
+    def reexecutions(self):
+        return self.lib.so.mdnn_nlop_checkpoint_reexecutions(self.h)
+
 
 def sense_dims(x, y, coils=1, maps=1, batch=1):
     return mdnn_sense_dims(x, y, coils, maps, batch)
