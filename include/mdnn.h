@@ -220,6 +220,8 @@ int mdnn_sim_pattern(long y, long accel, long acl, float* pattern);
 /* ---- training (optim.hpp:20-108, :218-415) ------------------------------- */
 typedef struct mdnn_train_cfg {
     double lr, beta1, beta2, eps, clip;
+    int algo;                        /* OptAlgo (optim.hpp:10): 0 sgd, 1 adam (default), 2 ipalm */
+    double ipalm_alpha, ipalm_beta;  /* IpalmParams (optim.hpp:26-29) */
 } mdnn_train_cfg;
 void mdnn_train_cfg_default(mdnn_train_cfg* c);
 /* joins model output "out" with an MSE loss against data arg "reference" */

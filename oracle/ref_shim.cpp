@@ -817,13 +817,20 @@ void mdnn_train_cfg_default(mdnn_train_cfg* c)
     c->beta2 = d.adam.beta2;
     c->eps = d.adam.eps;
     c->clip = d.clip;
+    c->algo = int(d.algo);
+    c->ipalm_alpha = d.ipalm.alpha;
+    c->ipalm_beta = d.ipalm.beta;
 }
 
 mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg* c, uint64_t seed)
 {
     return guard_ptr<mdnn_trainer>([&] {
         auto t = std::make_unique<mdnn_trainer>();
-        t->cfg.algo = OptAlgo::Adam;
+        if (c->algo < 0 || c->algo > 2)
+            throw ConfigError("unknown optimizer id " + std::to_string(c->algo));
+        t->cfg.algo = OptAlgo(c->algo);
+        t->cfg.ipalm.alpha = c->ipalm_alpha;
+        t->cfg.ipalm.beta = c->ipalm_beta;
         t->cfg.lr = c->lr;
         t->cfg.adam.beta1 = c->beta1;
         t->cfg.adam.beta2 = c->beta2;
@@ -919,7 +926,12 @@ int mdnn_trainer_update(mdnn_trainer* t, float grad_scale)
             detail::clip_gradient(g, t->cfg.clip);
             if (arg.real_weights)
                 md_foreach(g, [](auto& v) { v = std::complex<R>(v.real(), 0); });
-            adam_step(w, g, t->adam[i], t->cfg.adam, R(t->cfg.lr));
+            if (t->cfg.algo == OptAlgo::Ipalm)
+                throw ConfigError("ipalm updates per block inside run_step; use mdnn_trainer_step");
+            if (t->cfg.algo == OptAlgo::Sgd)
+                sgd_step(w, g, R(t->cfg.lr));
+            else
+                adam_step(w, g, t->adam[i], t->cfg.adam, R(t->cfg.lr));
             if (arg.real_weights)
                 md_foreach(w, [](auto& v) { v = std::complex<R>(v.real(), 0); });
             if (arg.prox)

@@ -61,7 +61,10 @@ class mdnn_varnet_cfg(C.Structure):
 
 class mdnn_train_cfg(C.Structure):
     _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
-                ("clip", C.c_double)]
+                ("clip", C.c_double), ("algo", C.c_int), ("ipalm_alpha", C.c_double), ("ipalm_beta", C.c_double)]
+
+
+ALGO_SGD, ALGO_ADAM, ALGO_IPALM = 0, 1, 2
 
 
 P = C.c_void_p

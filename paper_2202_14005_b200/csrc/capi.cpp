@@ -646,6 +646,9 @@ void mdnn_train_cfg_default(mdnn_train_cfg* c)
     c->beta2 = d.beta2;
     c->eps = d.eps;
     c->clip = d.clip;
+    c->algo = int(d.algo);
+    c->ipalm_alpha = d.ipalm_alpha;
+    c->ipalm_beta = d.ipalm_beta;
 }
 
 mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg* c, uint64_t seed)
@@ -657,6 +660,11 @@ mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg*
         cfg.beta2 = c->beta2;
         cfg.eps = c->eps;
         cfg.clip = c->clip;
+        if (c->algo < 0 || c->algo > 2)
+            throw ConfigError("unknown optimizer id " + std::to_string(c->algo));
+        cfg.algo = OptAlgo(c->algo);
+        cfg.ipalm_alpha = c->ipalm_alpha;
+        cfg.ipalm_beta = c->ipalm_beta;
         auto t = new mdnn_trainer{std::make_unique<Trainer>(model->m, cfg, seed)};
         sync_and_check();
         return t;

@@ -191,5 +191,9 @@ void adam_update(cfloat* theta, cfloat* m, float* v, const cfloat* g, long n, fl
 // flat gradient gather/scatter
 void launch_copy(cfloat* dst, const cfloat* src, long n);
 void launch_check_finite(const cfloat* a, long n); // sets ERRF_NONFINITE_GRAD
+// sgd_step with the clip scale, realify and NonNegProx folded in
+void sgd_update(cfloat* theta, const cfloat* g, long n, float lr, float gscale, bool real_weights, bool nonneg_prox);
+// NonNegProx (nn.hpp:57-64): v = (max(Re v, 0), 0)
+void launch_prox_nonneg(cfloat* w, long n);
 
 } // namespace mdnn

@@ -116,7 +116,9 @@ double Trainer::forward_backward()
 
 void Trainer::update(float grad_scale)
 {
-    // optim.hpp:383-399 per weight: clip, realify, Adam, realify, prox
+    if (cfg_.algo == OptAlgo::Ipalm)
+        throw ConfigError("trainer: ipalm updates per block inside step(); use mdnn_trainer_step");
+    // optim.hpp:383-399 per weight: clip, realify, Adam / SGD, realify, prox
     for (size_t k = 0; k < wargs_.size(); k++) {
         const Arg& a = joint_.args[wargs_[k]];
         DArray& w = weights_[a.name];
@@ -129,6 +131,12 @@ void Trainer::update(float grad_scale)
             if (nrm > cfg_.clip)
                 scale *= float(cfg_.clip / nrm);
         }
+        if (cfg_.algo == OptAlgo::Sgd) {
+            // sgd_step (optim.hpp:66-71) on the clipped, realified gradient, then realify / prox
+            sgd_update(nw.data(), g, w.size(), float(cfg_.lr), scale, a.real_weights, a.prox == ProxKind::NonNeg);
+            w = nw;
+            continue;
+        }
         auto& st = adam_[k];
         st.t++;
         const float c1 = 1.f / float(1.0 - std::pow(cfg_.beta1, double(st.t)));
@@ -137,16 +145,84 @@ void Trainer::update(float grad_scale)
                     float(cfg_.beta2), float(cfg_.eps), c1, c2, scale, a.real_weights, a.prox == ProxKind::NonNeg);
         w = nw;
     }
-    // update_stats: moving-statistics outputs feed their same-named inputs
+    update_stats(last_outs_);
+}
+
+// update_stats: moving-statistics outputs feed their same-named inputs (optim.hpp:403-415)
+void Trainer::update_stats(const std::vector<DArray>& outs)
+{
     for (const auto& a : joint_.args) {
         if (a.kind != ArgKind::MovingStats)
             continue;
         for (size_t o = 0; o < joint_.out_names.size(); o++)
             if (joint_.out_names[o] == a.name) {
-                weights_[a.name] = last_outs_[o];
+                weights_[a.name] = outs[o];
                 break;
             }
     }
+}
+
+// clip_gradient (optim.hpp:201-208) and realify, in place
+void Trainer::finish_grad(DArray& g, const Arg& a, float grad_scale) const
+{
+    if (cfg_.clip > 0) {
+        const double nrm = host_znorm(g.data(), g.size());
+        if (nrm > cfg_.clip)
+            launch_scale(g.data(), g.data(), cfloat{float(cfg_.clip / nrm), 0.f}, g.size());
+    }
+    if (grad_scale != 1.f)
+        launch_scale(g.data(), g.data(), cfloat{grad_scale, 0.f}, g.size());
+    if (a.real_weights)
+        launch_real(g.data(), g.data(), g.size());
+}
+
+double Trainer::ipalm_step()
+{
+    const int nb = int(wargs_.size());
+    if (ipalm_prev_.size() != size_t(nb))
+        ipalm_prev_.resize(nb);
+    const float lr = float(cfg_.lr), al = float(cfg_.ipalm_alpha), be = float(cfg_.ipalm_beta);
+    // cur: the iterate the gradient oracle sees (blocks < j updated, j at z, > j old)
+    std::vector<DArray> in = gather_inputs();
+    double loss = 0;
+    for (int j = 0; j < nb; j++) {
+        const Arg& a = joint_.args[wargs_[j]];
+        DArray& theta = weights_[a.name];
+        if (!ipalm_prev_[j].valid())
+            ipalm_prev_[j] = theta.clone();
+        const long n = theta.size();
+        DArray d(theta.dims, false), y(theta.dims, false), z(theta.dims, false);
+        launch_add(d.data(), theta.data(), ipalm_prev_[j].data(), -1.f, n); // theta - prev
+        launch_add(y.data(), theta.data(), d.data(), al, n);                // prox extrapolation
+        launch_add(z.data(), theta.data(), d.data(), be, n);                // gradient extrapolation
+        in[wargs_[j]] = z;
+        auto outs = joint_.op.apply(in);
+        cfloat lv;
+        CUDA_CHECK(cudaMemcpyAsync(&lv, outs[loss_idx_].data(), sizeof(cfloat), cudaMemcpyDeviceToHost,
+                                   ctx().stream));
+        sync_and_check();
+        loss = double(lv.x);
+        if (!std::isfinite(loss))
+            throw SolverError("training aborted: non-finite loss");
+        DArray g = joint_.op.adjoint_derivative(loss_idx_, wargs_[j], DArray::scalar(1.f)).clone();
+        launch_check_finite(g.data(), n); // check_gradient_finite (optim.hpp:143)
+        finish_grad(g, a, 1.f);
+        launch_add(y.data(), y.data(), g.data(), -lr, n);
+        if (a.prox == ProxKind::NonNeg)
+            launch_prox_nonneg(y.data(), n);
+        ipalm_prev_[j] = theta;
+        theta = y;
+        in[wargs_[j]] = y;
+        // the flat buffer mirrors the last block gradients (inspection / tests)
+        launch_copy(flat_.data() + woff_[j], g.data(), n);
+    }
+    bool has_stats = false;
+    for (const auto& a : joint_.args)
+        has_stats |= a.kind == ArgKind::MovingStats;
+    if (has_stats)
+        update_stats(joint_.op.apply(gather_inputs()));
+    sync_and_check();
+    return loss;
 }
 
 } // namespace mdnn

@@ -8,8 +8,12 @@
 
 namespace mdnn {
 
+// OptAlgo (optim.hpp:10) and the TrainConfig fields the step uses (optim.hpp:20-56)
+enum class OptAlgo { Sgd = 0, Adam = 1, Ipalm = 2 };
 struct TrainConfig {
     double lr = 1e-3, beta1 = 0.9, beta2 = 0.999, eps = 1e-8, clip = 0;
+    OptAlgo algo = OptAlgo::Adam;
+    double ipalm_alpha = 0.5, ipalm_beta = 0.5;
 };
 
 class Trainer {
@@ -25,10 +29,15 @@ public:
     void update(float grad_scale);       // Adam on the flat buffer
     double step()
     {
+        if (cfg_.algo == OptAlgo::Ipalm)
+            return ipalm_step();
         double l = forward_backward();
         update(1.f);
         return l;
     }
+    // one iPALM sweep over the weight blocks in Gauss-Seidel order
+    // (ipalm_step + run_step's iPALM branch, optim.hpp:118-153, 331-370)
+    double ipalm_step();
     float* grad_buffer() const { return flat_.fdata(); }
     long grad_floats() const { return 2 * flat_n_; }
     const std::vector<std::string>& weight_names() const { return wnames_; }
@@ -54,6 +63,9 @@ private:
         long t = 0;
     };
     std::vector<Adam> adam_;
+    std::vector<DArray> ipalm_prev_; // IpalmState::prev per weight block
+    void update_stats(const std::vector<DArray>& outs);
+    void finish_grad(DArray& g, const Arg& a, float grad_scale) const; // clip + realify
     std::shared_ptr<float> vbuf_;
     std::vector<DArray> last_outs_;
 };

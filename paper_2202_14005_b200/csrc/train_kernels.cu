@@ -50,7 +50,46 @@ __global__ void k_adam(cfloat* __restrict__ th, cfloat* __restrict__ m, float* _
     }
 }
 
+// sgd_step (optim.hpp:66-71) with run_step's clip scale, realify and prox (optim.hpp:383-396)
+__global__ void k_sgd(float2* __restrict__ th, const float2* __restrict__ g, long n, float lr, float gscale,
+                      bool real_w, bool nonneg)
+{
+    for (long k = blockIdx.x * long(blockDim.x) + threadIdx.x; k < n; k += long(gridDim.x) * blockDim.x) {
+        float2 gv = g[k];
+        gv.x *= gscale;
+        gv.y = real_w ? 0.f : gv.y * gscale;
+        float2 t = th[k];
+        t.x -= lr * gv.x;
+        t.y -= lr * gv.y;
+        if (real_w)
+            t.y = 0.f;
+        if (nonneg)
+            t = float2{t.x > 0.f ? t.x : 0.f, 0.f};
+        th[k] = t;
+    }
+}
+
+__global__ void k_prox_nonneg(float2* w, long n)
+{
+    for (long k = blockIdx.x * long(blockDim.x) + threadIdx.x; k < n; k += long(gridDim.x) * blockDim.x) {
+        const float2 t = w[k];
+        w[k] = float2{t.x > 0.f ? t.x : 0.f, 0.f};
+    }
+}
+
 } // namespace
+
+void sgd_update(cfloat* theta, const cfloat* g, long n, float lr, float gscale, bool real_weights, bool nonneg_prox)
+{
+    k_sgd<<<grid_for(n), kT, 0, ctx().stream>>>(theta, g, n, lr, gscale, real_weights, nonneg_prox);
+    KERNEL_CHECK();
+}
+
+void launch_prox_nonneg(cfloat* w, long n)
+{
+    k_prox_nonneg<<<grid_for(n), kT, 0, ctx().stream>>>(w, n);
+    KERNEL_CHECK();
+}
 
 void mse_forward(cfloat* loss, cfloat* diff, const cfloat* p, const cfloat* r, long n)
 {

@@ -119,3 +119,32 @@ def test_training_steps_match_reference(gpu, ref, net):
     for name in trainers[1].weight_names():
         wg, wr = trainers[0].get_weight(name), trainers[1].get_weight(name)
         assert rel_l2(wg, wr) <= 1e-3, name
+
+
+@pytest.mark.parametrize("net,algo", [("varnet", "ipalm"), ("modl", "ipalm"), ("modl", "sgd"), ("varnet", "sgd")])
+def test_optimizer_trajectories_match_reference(gpu, ref, net, algo):
+    """SGD and iPALM (optim.hpp:66-71, 110-153; run_step's iPALM branch
+    :331-370, Gauss-Seidel block order, VarNet's CLI default cli.hpp:194)
+    against the reference's own run_step."""
+    from paper_2202_14005_b200.capi import ALGO_IPALM, ALGO_SGD
+    X, Y, NC, B = 16, 12, 3, 2
+    if net == "modl":
+        cfg = dict(iterations=2, layers=3, filters=4, cg_iter=5, im_x=X, im_y=Y, coils=NC, batch=B)
+        build = Model.modl
+    else:
+        cfg = dict(iterations=2, filters=3, kernel=5, rbf=7, im_x=X, im_y=Y, coils=NC, batch=B)
+        build = Model.varnet
+    mref = build(ref, **cfg)
+    data, _ = _inputs(ref, mref, X, Y, NC, B)
+    code = {"sgd": ALGO_SGD, "ipalm": ALGO_IPALM}[algo]
+    losses, trainers = [], []
+    for lib in (gpu, ref):
+        t = Trainer(lib, build(lib, **cfg), seed=42, lr=1e-3, algo=code, ipalm_alpha=0.5, ipalm_beta=0.5)
+        for k, v in data.items():
+            t.set_data(k, v)
+        losses.append([t.step() for _ in range(3)])
+        trainers.append(t)
+    np.testing.assert_allclose(losses[0], losses[1], rtol=1e-4)
+    for name in trainers[1].weight_names():
+        wg, wr = trainers[0].get_weight(name), trainers[1].get_weight(name)
+        assert rel_l2(wg, wr) <= 1e-3, name
