@@ -41,12 +41,17 @@ constexpr int HALO_BYTES = HALO_L * HALO_P * 128;
 constexpr int NBSTAGE = 2;
 constexpr int NTHREADS = 192;
 
+// epilogue staging per warp: 32 pixels x 16 accumulator columns, pitch 20 floats
+constexpr int EPI_PITCH = 20;
+constexpr int EPI_WARP_BYTES = 32 * EPI_PITCH * 4;
+
 template<int N>
 struct TcSmem {
     static constexpr int B_BYTES = N * 128;
     static constexpr int HALO_OFF = 0;
     static constexpr int B_OFF = 2 * HALO_BYTES;
-    static constexpr int BAR_OFF = B_OFF + NBSTAGE * B_BYTES;
+    static constexpr int EPI_OFF = B_OFF + NBSTAGE * B_BYTES;
+    static constexpr int BAR_OFF = EPI_OFF + 4 * EPI_WARP_BYTES;
     static constexpr int TOTAL = BAR_OFF + 256 + 1024; // + barriers + alignment slack
 };
 
@@ -161,31 +166,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
         // ---------------- epilogue: TMEM -> registers -> global ----------------
         const int lg = warp & 3; // TMEM lane group this warp may access
-        const int r = lg * 32 + lane;
-        const int gy = r / 8, gx = r % 8;
+        float* estage = reinterpret_cast<float*>(smem + S::EPI_OFF + lg * EPI_WARP_BYTES);
         uint32_t ti = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
             const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
             const int x0 = tx * TILE_X, y0 = ty * TILE_Y;
             mbar_wait(tmem_full, ti & 1);
             tc_fence_after();
-            const int py = y0 + gy;
+                // Staged through shared memory so that each store instruction
+            // writes 8 pixels x 64 contiguous bytes (lanes 4 per pixel)
+            // instead of 32 scattered 16-byte pieces (LSU-throttled).
+            // Warp lg owns pixel rows gy = 4 lg .. 4 lg + 3 of each M-tile.
+            const int qd = lane & 3, pl = lane >> 2;
 #pragma unroll 1
             for (int xt = 0; xt < 4; xt++) {
-                const int px = x0 + xt * 8 + gx;
-                const bool ok = px < X && py < Y;
-                float* dst = out + ((long(b) * Y + py) * X + px) * N;
 #pragma unroll 1
-                for (int nc = 0; nc < N / 32; nc++) {
-                    float v[32];
-                    tmem_ld32(tmem_base + (uint32_t(lg * 32) << 16) + xt * N + nc * 32, v);
+                for (int nc = 0; nc < N / 16; nc++) {
+                    float v[16];
+                    tmem_ld16(tmem_base + (uint32_t(lg * 32) << 16) + xt * N + nc * 16, v);
                     tmem_ld_wait();
-                    if (ok) {
-                        float4* d4 = reinterpret_cast<float4*>(dst + nc * 32);
+                    float4* st4 = reinterpret_cast<float4*>(estage + lane * EPI_PITCH);
 #pragma unroll
-                        for (int q = 0; q < 8; q++)
-                            d4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    for (int q = 0; q < 4; q++)
+                        st4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int it = 0; it < 4; it++) {
+                        const int rr = it * 8 + pl; // staged pixel: row 4 lg + it, x offset pl
+                        const int px = x0 + xt * 8 + pl, py = y0 + lg * 4 + it;
+                        const float4 val = reinterpret_cast<const float4*>(estage + rr * EPI_PITCH)[qd];
+                        if (px < X && py < Y)
+                            reinterpret_cast<float4*>(out + ((long(b) * Y + py) * X + px) * N + nc * 16)[qd] = val;
                     }
+                    __syncwarp();
                 }
             }
             tc_fence_before();

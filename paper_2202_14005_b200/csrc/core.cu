@@ -1,4 +1,6 @@
 #include "core.h"
+
+#include <cstdlib>
 #include "kernels.h"
 
 #include <atomic>
@@ -85,6 +87,18 @@ Context* make_ctx(int dev)
     CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thresh = UINT64_MAX;
     CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thresh));
+    // optional up-front reservation (MDNN_POOL_RESERVE_GB): the pool maps its
+    // physical memory once instead of growing while steps are in flight
+    if (const char* r = std::getenv("MDNN_POOL_RESERVE_GB")) {
+        const size_t bytes = size_t(std::atof(r) * 1e9);
+        if (bytes) {
+            void* p = nullptr;
+            CUDA_CHECK(cudaMallocAsync(&p, bytes, c->stream));
+            CUDA_CHECK(cudaFreeAsync(p, c->stream));
+            CUDA_CHECK(cudaStreamSynchronize(c->stream));
+            c->pool_reserved = bytes;
+        }
+    }
     CUDA_CHECK(cudaMalloc(&c->d_errflags, 64));
     CUDA_CHECK(cudaMemset(c->d_errflags, 0, 64));
     return c.release();
@@ -181,13 +195,29 @@ DArray DArray::clone() const
     return o;
 }
 
+namespace {
+__global__ void k_set_scalar(float2* p, float re, float im) { *p = float2{re, im}; }
+} // namespace
+
 DArray DArray::scalar(float re, float im)
 {
+    // value travels as a kernel argument: no host staging, no stream synchronisation
     DArray a(Dims{1}, false);
-    cfloat v{re, im};
-    CUDA_CHECK(cudaMemcpyAsync(a.buf->ptr, &v, sizeof(v), cudaMemcpyHostToDevice, ctx().stream));
-    CUDA_CHECK(cudaStreamSynchronize(ctx().stream)); // host value is on the stack
+    k_set_scalar<<<1, 1, 0, ctx().stream>>>(a.data(), re, im);
+    KERNEL_CHECK();
     return a;
+}
+
+void reserve_pool(size_t bytes)
+{
+    auto& c = ctx();
+    if (c.pool_reserved >= bytes)
+        return;
+    void* p = nullptr;
+    CUDA_CHECK(cudaMallocAsync(&p, bytes, c.stream));
+    CUDA_CHECK(cudaFreeAsync(p, c.stream));
+    CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    c.pool_reserved = bytes;
 }
 
 DArray DArray::view(cfloat* p, Dims d)

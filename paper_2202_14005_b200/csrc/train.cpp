@@ -2,12 +2,23 @@
 
 #include "kernels.h"
 
+#include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 
 namespace mdnn {
 
 Trainer::Trainer(const Model& model, const TrainConfig& cfg, uint64_t seed) : cfg_(cfg)
 {
+    // pre-map the allocator pool (MDNN_POOL_RESERVE_GB overrides; default half
+    // of the free device memory, at most 96 GB)
+    if (!std::getenv("MDNN_POOL_RESERVE_GB")) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+            reserve_pool(std::min<size_t>(free_b / 2, size_t(96) << 30));
+    }
     const int oi = model.output_index("out");
     joint_ = model_chain(model, loss_model_mse(model.op.out_dims(oi)), "prediction", oi);
     loss_idx_ = joint_.output_index("loss");
@@ -94,6 +105,8 @@ std::vector<DArray> Trainer::gather_inputs() const
 
 double Trainer::forward_backward()
 {
+    static const bool trace = std::getenv("MDNN_TRACE_HOST") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     last_outs_ = joint_.op.apply(gather_inputs());
     std::vector<char> want(joint_.args.size(), 0);
     for (int i : wargs_)
@@ -108,7 +121,21 @@ double Trainer::forward_backward()
     cfloat lv;
     CUDA_CHECK(cudaMemcpyAsync(&lv, last_outs_[loss_idx_].data(), sizeof(cfloat), cudaMemcpyDeviceToHost,
                                ctx().stream));
+    const auto t1 = std::chrono::steady_clock::now();
     sync_and_check();
+    if (trace) {
+        const auto t2 = std::chrono::steady_clock::now();
+        cudaMemPool_t pool;
+        uint64_t res = 0, used = 0, hi = 0;
+        cudaDeviceGetDefaultMemPool(&pool, ctx().device);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &hi);
+        std::fprintf(stderr, "[mdnn] forward_backward host enqueue %.2f ms, wait %.2f ms; pool reserved %.2f GB "
+                     "(high %.2f) used %.2f GB\n",
+                     std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                     std::chrono::duration<double, std::milli>(t2 - t1).count(), res / 1e9, hi / 1e9, used / 1e9);
+    }
     if (!std::isfinite(lv.x))
         throw SolverError("training aborted: non-finite loss");
     return double(lv.x);
