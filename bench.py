@@ -105,19 +105,36 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
 
-    def stop(self):
+    def wait_first(self, timeout=5.0):
+        t0 = time.monotonic()
+        while self.proc and not self.lines and time.monotonic() - t0 < timeout:
+            time.sleep(0.05)
+
+    def mark(self):
+        return time.monotonic()
+
+    def stop(self, t_begin=None, t_end=None):
+        """Samples inside [t_begin, t_end] (plus the nearest one on each side,
+        so a short timed region still has its bracketing samples)."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        time.sleep(0.25)  # one more sample after the region
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        lines = self.lines
+        if t_begin is not None and lines:
+            inside = [k for k, (t, _) in enumerate(lines) if t_begin <= t <= t_end]
+            before = [k for k, (t, _) in enumerate(lines) if t < t_begin][-1:]
+            after = [k for k, (t, _) in enumerate(lines) if t > t_end][:1]
+            lines = [lines[k] for k in before + inside + after]
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -197,8 +214,8 @@ def config_of(args, B, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="modl_c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -251,13 +268,15 @@ def main():
         torch.cuda.synchronize()
         lib.check(lib.so.mdnn_synchronize())
 
+    clk = ClockSampler(local)
+    clk.start()
     for _ in range(args.warmup):
         step()
     barrier()
+    clk.wait_first()
 
     # ---- device-timed region (inputs resident in HBM) --------------------
-    clk = ClockSampler(local)
-    clk.start()
+    t_begin = clk.mark()
     l0 = lib.so.mdnn_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -267,7 +286,7 @@ def main():
     e1.record(stream)
     barrier()
     launches = lib.so.mdnn_launch_count() - l0
-    clocks = clk.stop()
+    clocks = clk.stop(t_begin, clk.mark())
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{local}")

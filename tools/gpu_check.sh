@@ -11,5 +11,7 @@ timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.log 2>&1; echo "ben
 if [ -n "$NCU_LIST" ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_list.log 2>&1
+timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
+   --log-file gpurun_out/traffic.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_traffic.log 2>&1
 fi
 for f in gpurun_out/pytest_gpu.log gpurun_out/bench.log gpurun_out/smoke.log; do tail -n 3 $f; done
