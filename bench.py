@@ -354,7 +354,14 @@ def roofline(lib, step_ms_total):
     `ahha` is the fused A^H A kernel the metric names."""
     p, src = peaks()
     hbm = p["hbm_gbs"]
-    tf32 = p["bf16_tflops"] / 2.0
+    # dense TF32 tensor peak: measured on this pool's B200 with cuBLAS
+    # (tools/tf32_peak.py -> profiles/tf32_peak.json, burst); else bf16 / 2
+    tf32, tf32_src = p["bf16_tflops"] / 2.0, "bf16_tflops/2 (TF32)"
+    try:
+        with open(os.path.join(REPO, "profiles", "tf32_peak.json")) as f:
+            tf32, tf32_src = float(json.load(f)["tf32_tflops"]), "tf32_tflops (profiles/tf32_peak.json, cuBLAS burst)"
+    except Exception:
+        pass
     traffic = {}
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
@@ -380,7 +387,7 @@ def roofline(lib, step_ms_total):
         rows.append({"kernel": tag, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                      "frac": ach / peak, "launches": n.value, "ms_total": ms.value,
                      "share_of_step_time": ms.value / step_ms_total,
-                     "traffic": traffic.get(tag), "peak_source": f"{src} ({'hbm_gbs' if bound == 'hbm' else 'bf16_tflops/2 (TF32)'})"})
+                     "traffic": traffic.get(tag), "peak_source": f"measured hbm_gbs ({src})" if bound == "hbm" else f"measured {tf32_src}"})
     rows.sort(key=lambda r: -r["ms_total"])
     dom = rows[0] if rows else None
     ahha = next((r for r in rows if r["kernel"].startswith("sense_normal_y")), None)

@@ -20,8 +20,9 @@ namespace mdnn {
 namespace {
 
 constexpr int TX = 32, TY = 8;   // output tile (pixels)
-constexpr int FG = 8;            // output channels per block
 constexpr int MAXK = 11;
+// output channels per block: 8, or exactly 2 for the VarNet 24 -> 2 adjoint
+inline int fg_for(long nout) { return nout <= 2 ? 2 : 8; }
 
 // element (item b, pixel xy = x + X*y, channel c) of a C-channel tensor
 struct Acc {
@@ -55,7 +56,7 @@ struct Out {
 
 // mode 0: fwd (in = x, Cin in, weights w[t,c,f]); mode 1: bwd-data (in = dy,
 // channels Cout, weights conj(w[t,c,f]) flipped, output channel c)
-template<int MODE>
+template<int MODE, int FG>
 __global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const cfloat* __restrict__ w, ConvGeom g)
 {
     __shared__ float2 tile[TY + MAXK - 1][TX + MAXK - 1];
@@ -192,6 +193,80 @@ __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, A
     }
 }
 
+// bwd-weight, register-blocked along kx: thread (ky, c, f) keeps the K
+// accumulators of one kernel row and slides a K-wide window of x along each
+// pixel row (1 dy + 1 x smem load per K complex MACs).  Block = all
+// (ky, c, f) combos (K * Cin * Cout <= 576 threads: the VarNet 2 <-> 24
+// 11x11 layers); grid = pixel-tile splits, partials folded by k_sum_splits.
+template<int K>
+__global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part, Acc x, Acc dy, ConvGeom g,
+                                                        int nsplit)
+{
+    constexpr int HX = WTX + K - 1, HY = WTY + K - 1;
+    extern __shared__ float2 wsm[];
+    const int Cin = int(g.Cin), Cout = int(g.Cout);
+    float2* xt = wsm;                          // [Cin][HY][HX]
+    float2* dyt = wsm + Cin * HY * HX;         // [Cout][WTY][WTX]
+    const int nthr = K * Cin * Cout;
+    const int tid = threadIdx.x;
+    const int ky = tid % K, c = (tid / K) % Cin, f = tid / (K * Cin);
+    const bool act = tid < nthr;
+    const long ntx = (g.X + WTX - 1) / WTX, nty = (g.Y + WTY - 1) / WTY;
+    const long ntiles = ntx * nty * g.B;
+    float2 acc[K];
+#pragma unroll
+    for (int k = 0; k < K; k++)
+        acc[k] = float2{0.f, 0.f};
+    for (long tile = blockIdx.x; tile < ntiles; tile += nsplit) {
+        const long b = tile / (ntx * nty);
+        const long tr = tile % (ntx * nty);
+        const long x0 = (tr % ntx) * WTX, y0 = (tr / ntx) * WTY;
+        __syncthreads();
+        for (int e = tid; e < Cin * HX * HY; e += blockDim.x) {
+            const int hx = e % HX, hy = (e / HX) % HY, cc = e / (HX * HY);
+            const long gx = x0 + hx - g.px, gy = y0 + hy - g.py;
+            xt[e] = (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? x.ld(b, gx + g.X * gy, cc) : float2{0.f, 0.f};
+        }
+        for (int e = tid; e < Cout * WTX * WTY; e += blockDim.x) {
+            const int px = e % WTX, py = (e / WTX) % WTY, ff = e / (WTX * WTY);
+            const long gx = x0 + px, gy = y0 + py;
+            dyt[e] = (gx < g.X && gy < g.Y) ? dy.ld(b, gx + g.X * gy, ff) : float2{0.f, 0.f};
+        }
+        __syncthreads();
+        if (!act)
+            continue;
+        for (int py = 0; py < WTY; py++) {
+            const float2* xr = xt + (c * HY + py + ky) * HX;
+            const float2* dr = dyt + (f * WTY + py) * WTX;
+            float2 win[K];
+#pragma unroll
+            for (int k = 0; k < K - 1; k++)
+                win[k] = xr[k];
+#pragma unroll 4
+            for (int px = 0; px < WTX; px++) {
+                win[K - 1] = xr[px + K - 1];
+                const float2 d = dr[px];
+#pragma unroll
+                for (int kx = 0; kx < K; kx++) { // acc[kx] += d * conj(x[px + kx])
+                    acc[kx].x = fmaf(d.x, win[kx].x, acc[kx].x);
+                    acc[kx].y = fmaf(d.y, win[kx].x, acc[kx].y);
+                    acc[kx].x = fmaf(d.y, win[kx].y, acc[kx].x);
+                    acc[kx].y = fmaf(-d.x, win[kx].y, acc[kx].y);
+                }
+#pragma unroll
+                for (int k = 0; k < K - 1; k++)
+                    win[k] = win[k + 1];
+            }
+        }
+    }
+    if (act) {
+        const long KK = long(K) * K;
+#pragma unroll
+        for (int kx = 0; kx < K; kx++)
+            part[size_t(blockIdx.x) * KK * Cin * Cout + (kx + K * ky) + KK * (c + long(Cin) * f)] = acc[kx];
+    }
+}
+
 __global__ void k_sum_splits(cfloat* out, const float2* part, long n, int nsplit)
 {
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
@@ -229,12 +304,17 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
         conv_thin_run(y, x, w, g, 0);
         return;
     }
+    const int FGv = fg_for(g.Cout);
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
-              unsigned(g.B * ((g.Cout + FG - 1) / FG)));
+              unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
     ProfScope prof("conv_fwd", conv_flops(g));
-    k_conv_direct<0><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
-                                                         Acc{x, g.Cin, XY, g.in_chlast}, w, g);
+    if (FGv == 2)
+        k_conv_direct<0, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g);
+    else
+        k_conv_direct<0, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g);
     KERNEL_CHECK();
 }
 
@@ -249,12 +329,17 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
         conv_thin_run(dx, dy, w, g, 1);
         return;
     }
+    const int FGv = fg_for(g.Cin);
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
-              unsigned(g.B * ((g.Cin + FG - 1) / FG)));
+              unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
     ProfScope prof("conv_bwd_data", conv_flops(g));
-    k_conv_direct<1><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
-                                                         Acc{dy, g.Cout, XY, g.out_chlast}, w, g);
+    if (FGv == 2)
+        k_conv_direct<1, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g);
+    else
+        k_conv_direct<1, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g);
     KERNEL_CHECK();
 }
 
@@ -270,6 +355,28 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
         return;
     }
     const long KK = g.KX * g.KY;
+    if (g.KX == 11 && g.KY == 11 && 11 * g.Cin * g.Cout <= 576) {
+        // register-blocked kernel (VarNet K = 11 layers)
+        auto& c = ctx();
+        const long ntiles = ((g.X + WTX - 1) / WTX) * ((g.Y + WTY - 1) / WTY) * g.B;
+        const int nsplit = int(std::min<long>(ntiles, 2L * c.sm_count));
+        const long n = KK * g.Cin * g.Cout;
+        const long XY = g.X * g.Y;
+        const size_t smem = sizeof(float2) * (g.Cin * (WTY + 10) * (WTX + 10) + g.Cout * WTX * WTY);
+        float2* part;
+        CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
+        ProfScope prof("conv_bwd_weight", conv_flops(g));
+        auto kern = k_conv_wgrad_rb<11>;
+        allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
+        const int nthr = int(((11 * g.Cin * g.Cout + 31) / 32) * 32);
+        kern<<<nsplit, nthr, smem, c.stream>>>(part, Acc{x, g.Cin, XY, g.in_chlast}, Acc{dy, g.Cout, XY, g.out_chlast},
+                                              g, nsplit);
+        KERNEL_CHECK();
+        k_sum_splits<<<int(std::min(1024L, (n + 255) / 256)), 256, 0, c.stream>>>(dw, part, n, nsplit);
+        KERNEL_CHECK();
+        CUDA_CHECK(cudaFreeAsync(part, c.stream));
+        return;
+    }
     const bool small_k = KK * 4 * 8 <= 256 * WMAXC;
     const int WG_C = small_k ? 4 : 1, WG_F = 8;
     if (KK * WG_C * WG_F > 256 * WMAXC)

@@ -38,7 +38,7 @@ def _check_node(ng, nr, ins, rng, tol, names=None):
 
 @pytest.mark.parametrize("cin,cout,k,X,Y,B,bias", [
     (1, 8, 3, 20, 17, 2, False), (8, 8, 3, 33, 24, 1, False), (8, 1, 3, 16, 16, 2, True),
-    (2, 6, 11, 24, 20, 1, False), (4, 4, 5, 16, 12, 3, True), (64, 64, 3, 40, 32, 1, False),
+    (2, 6, 11, 24, 20, 1, False), (2, 24, 11, 40, 24, 2, False), (4, 4, 5, 16, 12, 3, True), (64, 64, 3, 40, 32, 1, False),
     # tcgen05 TF32 path: full and partial 32x16 super-tiles, 32- and 64-channel variants
     (64, 64, 3, 64, 48, 2, False), (32, 32, 3, 36, 20, 1, False), (32, 64, 3, 33, 17, 1, False),
     (64, 32, 3, 32, 16, 2, True),
