@@ -258,6 +258,31 @@ int mdnn_weights_load(mdnn_trainer* t, const char* dir);
 /* WeightsBundle::meta_or: copies the value (or fallback) into buf, NUL-terminated (cfl.hpp:137-141) */
 int mdnn_weights_meta(const char* dir, const char* key, const char* fallback, char* buf, long buflen);
 
+/* ---- reconet driver (cli.hpp:52-265) ------------------------------------
+ * The train / apply command either side of the training step, on cfl files.
+ * Fields mirror ReconetOptions (cli.hpp:52-65); -1 / NULL mean "default" or
+ * "take it from the weights bundle".  Strings are not copied past the call. */
+typedef struct mdnn_reconet_opts {
+    const char* network;       /* "varnet" | "modl" */
+    int do_train, do_apply;    /* exactly one */
+    int normalize;             /* per-item 1 / max |A^H y| (recon.hpp:464-493) */
+    const char* pattern_file;  /* NULL / "": estimate_pattern from k-space (cli.hpp:28-50) */
+    const char* init_weights;  /* warm-start bundle for --train */
+    long iterations, filters, kernel, rbf, layers, cg_iter;
+    long epochs, batch_size;
+    double lr;                 /* <= 0: 1e-2 varnet, 1e-3 modl */
+    const char* optimizer;     /* NULL / "": ipalm for varnet, adam for modl */
+    uint64_t seed;
+    int verbose;               /* print "epoch k loss v" per epoch */
+    const char* kspace_file;
+    const char* coils_file;
+    const char* weights_dir;   /* bundle written by --train, read by --apply */
+    const char* target_file;   /* --train: reference images; --apply: output */
+} mdnn_reconet_opts;
+void mdnn_reconet_opts_default(mdnn_reconet_opts* o);
+int mdnn_reconet(const mdnn_reconet_opts* o);                                    /* cmd_reconet, cli.hpp:94-265 */
+int mdnn_estimate_pattern(const mdnn_array* kspace, mdnn_array* pattern);       /* cli.hpp:28-50 */
+
 #ifdef __cplusplus
 }
 #endif

@@ -1056,3 +1056,272 @@ int mdnn_weights_meta(const char* dir, const char* key, const char* fallback, ch
 }
 
 } // extern "C"
+
+// ---- reconet driver: cmd_reconet (cli.hpp:94-265) restated over the reference's
+// own cfl / normalize / train / builders (cli.hpp itself needs CLI11, absent) ----
+namespace {
+
+MdArray<float> ref_estimate_pattern(const MdArray<float>& kspace) // cli.hpp:28-50
+{
+    Dims pd(max_rank, 1);
+    pd[dim_y] = kspace.dims()[dim_y];
+    MdArray<float> p(pd);
+    auto kc = kspace.clone();
+    const auto* kv = kc.data();
+    Dims str = default_strides(kspace.dims());
+    const long ny = kspace.dims()[dim_y];
+    const long line = str[dim_y];
+    const long total = kspace.size();
+    for (long y = 0; y < ny; y++) {
+        bool any = false;
+        for (long off = y * line; off < total && !any; off += ny * line)
+            for (long k = 0; k < line; k++)
+                if (kv[off + k] != std::complex<float>(0)) {
+                    any = true;
+                    break;
+                }
+        p.data()[y] = any ? 1.f : 0.f;
+    }
+    return p;
+}
+
+void ref_check_dim_match(const std::string& fa, const MdArray<float>& a, const std::string& fb,
+                         const MdArray<float>& b, int dim)
+{
+    if (a.dims()[dim] != b.dims()[dim])
+        throw ShapeError("file '" + fa + "' dimension " + std::to_string(dim) + " (=" + std::to_string(a.dims()[dim])
+                         + ") does not match file '" + fb + "' dimension " + std::to_string(dim) + " (="
+                         + std::to_string(b.dims()[dim]) + ")");
+}
+
+long ref_meta_long(const WeightsBundle& b, const std::string& key, long fallback)
+{
+    auto it = b.meta.find(key);
+    return it == b.meta.end() ? fallback : std::stol(it->second);
+}
+
+std::string cs(const char* p) { return p ? p : ""; }
+
+// Reference bug (third wiring fix): cfl_read pads every array to
+// rank 16, so bundle weights fed back through gather_inputs trip Nlop::apply's
+// exact dims check (nlop.hpp:131-134) for any weight of rank < 16 — the CLI's
+// apply and --init paths (cli.hpp:212-216, 228-231) throw ShapeError.  Reshape
+// each bundle array to its argument's own dims when the padded shapes agree.
+void fit_bundle_ranks(const Model<R>& m, std::map<std::string, MdArray<R>>& w)
+{
+    for (size_t i = 0; i < m.args.size(); i++) {
+        auto it = w.find(m.args[i].name);
+        if (it == w.end())
+            continue;
+        const Dims& want = m.op.in_dims(int(i));
+        if (it->second.dims() == want)
+            continue;
+        Dims p = want, q(it->second.dims().begin(), it->second.dims().end());
+        p.resize(max_rank, 1);
+        q.resize(max_rank, 1);
+        if (p != q)
+            throw ShapeError("weights bundle: array '" + it->first + "' has the wrong shape");
+        MdArray<R> r(want);
+        std::memcpy(static_cast<void*>(r.data()), it->second.data(), sizeof(std::complex<R>) * size_t(r.size()));
+        it->second = r;
+    }
+}
+
+int ref_reconet(const mdnn_reconet_opts* c)
+{
+    std::string network = cs(c->network);
+    bool do_train = c->do_train != 0, do_apply = c->do_apply != 0, normalize_on = c->normalize != 0;
+    if (do_train == do_apply)
+        throw ConfigError("reconet: exactly one of --train / --apply is required");
+    if (network != "varnet" && network != "modl")
+        throw ConfigError("reconet: --network must be varnet or modl");
+    auto kspace = cfl_read(cs(c->kspace_file));
+    auto coils = cfl_read(cs(c->coils_file));
+    for (int d : {dim_x, dim_y, dim_coil, dim_batch})
+        ref_check_dim_match(cs(c->coils_file), coils, cs(c->kspace_file), kspace, d);
+    const std::string pfile = cs(c->pattern_file);
+    MdArray<float> pattern = pfile.empty() ? ref_estimate_pattern(kspace) : cfl_read(pfile);
+    ref_check_dim_match(pfile.empty() ? "<estimated pattern>" : pfile, pattern, cs(c->kspace_file), kspace, dim_y);
+    check_pattern_binary(pattern);
+
+    const long n = kspace.dims()[dim_batch];
+    const long maps = coils.dims()[dim_maps];
+    VarNetConfig vn;
+    ModlConfig md;
+    vn.im_x = md.im_x = kspace.dims()[dim_x];
+    vn.im_y = md.im_y = kspace.dims()[dim_y];
+    vn.coils = md.coils = kspace.dims()[dim_coil];
+    vn.maps = md.maps = maps;
+
+    WeightsBundle bundle;
+    if (do_apply || !cs(c->init_weights).empty()) {
+        bundle = WeightsBundle::load(do_apply ? cs(c->weights_dir) : cs(c->init_weights));
+        if (bundle.meta_or("network", network) != network)
+            throw ConfigError("weights bundle was trained for network '" + bundle.meta_or("network", "?") + "', not '"
+                              + network + "'");
+        auto take = [&](const std::string& key, long& dst) { dst = ref_meta_long(bundle, key, dst); };
+        if (network == "varnet") {
+            take("iterations", vn.iterations);
+            take("filters", vn.filters);
+            take("kernel", vn.kernel);
+            take("rbf", vn.rbf);
+        } else {
+            take("iterations", md.iterations);
+            take("layers", md.layers);
+            take("filters", md.filters);
+            take("kernel", md.kernel);
+            take("cg_iter", md.cg_iter);
+        }
+        if (do_apply)
+            normalize_on = bundle.meta_or("normalize", "0") == "1";
+    }
+    auto override_long = [](long flag, long& dst, const char* what, bool frozen) {
+        if (flag < 0)
+            return;
+        if (frozen && flag != dst)
+            throw ConfigError(std::string("flag --") + what + " conflicts with the weights bundle");
+        dst = flag;
+    };
+    if (network == "varnet") {
+        override_long(c->iterations, vn.iterations, "iterations", do_apply);
+        override_long(c->filters, vn.filters, "filters", do_apply);
+        override_long(c->kernel, vn.kernel, "kernel", do_apply);
+        override_long(c->rbf, vn.rbf, "rbf", do_apply);
+    } else {
+        override_long(c->iterations, md.iterations, "iterations", do_apply);
+        override_long(c->layers, md.layers, "layers", do_apply);
+        override_long(c->filters, md.filters, "filters", do_apply);
+        override_long(c->cg_iter, md.cg_iter, "cg-iter", do_apply);
+    }
+
+    MdArray<float> scale;
+    if (normalize_on) {
+        auto sense = build_sense<float>(coils, pattern);
+        auto x0 = sense.adjoint(kspace);
+        auto nr = normalize(x0, kspace);
+        scale = nr.scale;
+        kspace = nr.scaled;
+    }
+
+    if (do_train) {
+        auto reference = cfl_read(cs(c->target_file));
+        for (int d : {dim_x, dim_y, dim_batch})
+            ref_check_dim_match(cs(c->target_file), reference, cs(c->kspace_file), kspace, d);
+        if (normalize_on)
+            reference = apply_scale(reference, scale, false);
+        TrainConfig tc;
+        tc.epochs = c->epochs;
+        tc.batch_size = c->batch_size;
+        tc.seed = c->seed;
+        tc.deterministic = true;
+        tc.drop_last = true;
+        tc.verbose = c->verbose != 0;
+        const std::string opt = cs(c->optimizer);
+        tc.algo = !opt.empty() ? opt_algo_from_string(opt) : (network == "varnet" ? OptAlgo::Ipalm : OptAlgo::Adam);
+        tc.lr = c->lr > 0 ? c->lr : (network == "varnet" ? 1e-2 : 1e-3);
+        Model<R> net;
+        if (network == "varnet") {
+            vn.batch = tc.batch_size;
+            net = fixed_build_varnet(vn);
+        } else {
+            md.batch = tc.batch_size;
+            md.train_mode = true;
+            net = fixed_build_modl(md);
+        }
+        Dataset<R> data;
+        data.add("kspace", from_f32(kspace));
+        data.add("coils", from_f32(coils));
+        data.add("reference", from_f32(reference));
+        data.arrays.emplace("pattern", from_f32(pattern));
+        std::map<std::string, MdArray<R>> weights;
+        for (const auto& [name, arr] : bundle.arrays)
+            weights.emplace(name, from_f32(arr));
+        fit_bundle_ranks(net, weights);
+        train(net, LossKind::Mse, data, tc, weights);
+        WeightsBundle out;
+        out.meta["network"] = network;
+        out.meta["normalize"] = normalize_on ? "1" : "0";
+        out.meta["seed"] = std::to_string(c->seed);
+        if (network == "varnet") {
+            out.meta["iterations"] = std::to_string(vn.iterations);
+            out.meta["filters"] = std::to_string(vn.filters);
+            out.meta["kernel"] = std::to_string(vn.kernel);
+            out.meta["rbf"] = std::to_string(vn.rbf);
+        } else {
+            out.meta["iterations"] = std::to_string(md.iterations);
+            out.meta["layers"] = std::to_string(md.layers);
+            out.meta["filters"] = std::to_string(md.filters);
+            out.meta["kernel"] = std::to_string(md.kernel);
+            out.meta["cg_iter"] = std::to_string(md.cg_iter);
+        }
+        out.meta["epochs"] = std::to_string(c->epochs);
+        for (const auto& [name, arr] : weights)
+            out.arrays.emplace(name, to_f32(arr));
+        out.save(cs(c->weights_dir));
+        return 0;
+    }
+
+    std::map<std::string, MdArray<R>> weights;
+    for (const auto& [name, arr] : bundle.arrays)
+        weights.emplace(name, from_f32(arr));
+    SenseDims sdn{kspace.dims()[dim_x], kspace.dims()[dim_y], kspace.dims()[dim_coil], maps, n};
+    MdArray<float> output(sdn.image());
+    const long chunk = std::min(n, c->batch_size);
+    Model<R> net;
+    long built = -1;
+    for (long pos = 0; pos < n; pos += chunk) {
+        long cnt = std::min(chunk, n - pos);
+        if (built != cnt) {
+            if (network == "varnet") {
+                vn.batch = cnt;
+                net = fixed_build_varnet(vn);
+            } else {
+                md.batch = cnt;
+                md.train_mode = false;
+                net = fixed_build_modl(md);
+            }
+            built = cnt;
+        }
+        fit_bundle_ranks(net, weights);
+        std::map<std::string, MdArray<R>> dmap;
+        dmap["kspace"] = from_f32(kspace.slice(dim_batch, pos, cnt).clone());
+        dmap["coils"] = from_f32(coils.slice(dim_batch, pos, cnt).clone());
+        dmap["pattern"] = from_f32(pattern);
+        auto outs = net.op.apply(net.gather_inputs(weights, dmap));
+        auto res = to_f32(outs[net.output_index("out")]);
+        auto dst = output.slice(dim_batch, pos, cnt);
+        md_copy2(dst.dims(), dst, dst.strides(), res, res.strides());
+    }
+    if (normalize_on)
+        output = apply_scale(output, scale, true);
+    cfl_write(cs(c->target_file), output);
+    return 0;
+}
+
+} // namespace
+
+extern "C" {
+
+void mdnn_reconet_opts_default(mdnn_reconet_opts* o)
+{
+    std::memset(o, 0, sizeof(*o));
+    o->network = "varnet";
+    o->iterations = o->filters = o->kernel = o->rbf = o->layers = o->cg_iter = -1;
+    o->epochs = 10;
+    o->batch_size = 10;
+    o->lr = -1;
+    o->seed = 42;
+    o->verbose = 1;
+}
+
+int mdnn_reconet(const mdnn_reconet_opts* o)
+{
+    return guard([&] { ref_reconet(o); });
+}
+
+int mdnn_estimate_pattern(const mdnn_array* kspace, mdnn_array* pattern)
+{
+    return guard([&] { to_c(from_f32(ref_estimate_pattern(to_f32(from_c(*kspace)))), *pattern); });
+}
+
+} // extern "C"

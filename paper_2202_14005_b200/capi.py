@@ -67,6 +67,16 @@ class mdnn_train_cfg(C.Structure):
 ALGO_SGD, ALGO_ADAM, ALGO_IPALM = 0, 1, 2
 
 
+class mdnn_reconet_opts(C.Structure):
+    _fields_ = [("network", C.c_char_p), ("do_train", C.c_int), ("do_apply", C.c_int), ("normalize", C.c_int),
+                ("pattern_file", C.c_char_p), ("init_weights", C.c_char_p),
+                ("iterations", C.c_long), ("filters", C.c_long), ("kernel", C.c_long), ("rbf", C.c_long),
+                ("layers", C.c_long), ("cg_iter", C.c_long), ("epochs", C.c_long), ("batch_size", C.c_long),
+                ("lr", C.c_double), ("optimizer", C.c_char_p), ("seed", C.c_uint64), ("verbose", C.c_int),
+                ("kspace_file", C.c_char_p), ("coils_file", C.c_char_p), ("weights_dir", C.c_char_p),
+                ("target_file", C.c_char_p)]
+
+
 P = C.c_void_p
 L = C.POINTER(C.c_long)
 _SIGS = {
@@ -164,6 +174,9 @@ _SIGS = {
     "mdnn_trainer_step": (C.c_int, [P, C.POINTER(C.c_double)]),
     "mdnn_trainer_n_weights": (C.c_int, [P]),
     "mdnn_trainer_weight_name": (C.c_char_p, [P, C.c_int]),
+    "mdnn_reconet_opts_default": (None, [C.POINTER(mdnn_reconet_opts)]),
+    "mdnn_reconet": (C.c_int, [C.POINTER(mdnn_reconet_opts)]),
+    "mdnn_estimate_pattern": (C.c_int, [C.POINTER(mdnn_array), C.POINTER(mdnn_array)]),
     "mdnn_cfl_dims": (C.c_int, [C.c_char_p, L]),
     "mdnn_cfl_read": (C.c_int, [C.c_char_p, C.POINTER(mdnn_array)]),
     "mdnn_cfl_write": (C.c_int, [C.c_char_p, C.POINTER(mdnn_array)]),

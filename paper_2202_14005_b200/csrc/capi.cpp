@@ -4,6 +4,7 @@
 #include "../../include/mdnn.h"
 
 #include "cfl.h"
+#include "reconet.h"
 #include "kernels.h"
 #include "profile.h"
 #include "train.h"
@@ -814,6 +815,62 @@ int mdnn_weights_meta(const char* dir, const char* key, const char* fallback, ch
         if (long(val.size()) + 1 > buflen)
             throw BoundsError("mdnn_weights_meta: buffer too small");
         std::memcpy(buf, val.c_str(), val.size() + 1);
+    });
+}
+
+} // extern "C"
+
+// ---- reconet driver -----------------------------------------------------------
+extern "C" {
+
+void mdnn_reconet_opts_default(mdnn_reconet_opts* o)
+{
+    std::memset(o, 0, sizeof(*o));
+    o->network = "varnet";
+    o->iterations = o->filters = o->kernel = o->rbf = o->layers = o->cg_iter = -1;
+    o->epochs = 10;
+    o->batch_size = 10;
+    o->lr = -1;
+    o->seed = 42;
+    o->verbose = 1;
+}
+
+int mdnn_reconet(const mdnn_reconet_opts* c)
+{
+    return guard([&] {
+        auto str = [](const char* p) { return std::string(p ? p : ""); };
+        ReconetOptions o;
+        o.network = str(c->network);
+        o.do_train = c->do_train != 0;
+        o.do_apply = c->do_apply != 0;
+        o.normalize = c->normalize != 0;
+        o.pattern_file = str(c->pattern_file);
+        o.init_weights = str(c->init_weights);
+        o.iterations = c->iterations;
+        o.filters = c->filters;
+        o.kernel = c->kernel;
+        o.rbf = c->rbf;
+        o.layers = c->layers;
+        o.cg_iter = c->cg_iter;
+        o.epochs = c->epochs;
+        o.batch_size = c->batch_size;
+        o.lr = c->lr;
+        o.optimizer = str(c->optimizer);
+        o.seed = c->seed;
+        o.verbose = c->verbose != 0;
+        o.kspace_file = str(c->kspace_file);
+        o.coils_file = str(c->coils_file);
+        o.weights_dir = str(c->weights_dir);
+        o.target_file = str(c->target_file);
+        run_reconet(o);
+    });
+}
+
+int mdnn_estimate_pattern(const mdnn_array* kspace, mdnn_array* pattern)
+{
+    return guard([&] {
+        out_arr(estimate_pattern(in_arr(*kspace)), *pattern);
+        sync_and_check();
     });
 }
 
