@@ -54,11 +54,31 @@ struct Out {
     }
 };
 
+// Real-operand fast path.  VarNet's convolutions see real data throughout
+// (RealChan output, RBF output, real-valued weights by the real_weights flag):
+// a complex MAC with Im = 0 on both sides reduces to one real FMA whose
+// result is bitwise the real part the complex formula produces (the extra
+// products are exact zeros), and the imaginary part is zero.  A tiny kernel
+// raises a device flag if any operand element has a nonzero imaginary part;
+// the conv kernels read it (block-uniform) and pick the complex or the real
+// inner loop — no host synchronisation, any complex input takes the full path.
+__global__ void k_imag_any(const float2* __restrict__ a, long n, unsigned* flag)
+{
+    int any = 0;
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
+        any |= a[i].y != 0.f;
+    any = __syncthreads_or(any);
+    if (any && threadIdx.x == 0)
+        atomicOr(flag, 1u);
+}
+
 // mode 0: fwd (in = x, Cin in, weights w[t,c,f]); mode 1: bwd-data (in = dy,
 // channels Cout, weights conj(w[t,c,f]) flipped, output channel c)
 template<int MODE, int FG>
-__global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const cfloat* __restrict__ w, ConvGeom g)
+__global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const cfloat* __restrict__ w, ConvGeom g,
+                                                        const unsigned* __restrict__ imag_flag)
 {
+    const bool real = imag_flag && *imag_flag == 0;
     __shared__ float2 tile[TY + MAXK - 1][TX + MAXK - 1];
     __shared__ float2 wsh[MAXK * MAXK][FG];
     const long nin = MODE == 0 ? g.Cin : g.Cout;
@@ -101,17 +121,28 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const c
             wsh[t][f] = v;
         }
         __syncthreads();
-        for (int ky = 0; ky < KY; ky++)
-            for (int kx = 0; kx < KX; kx++) {
-                float2 xv = tile[ty + ky][tx + kx];
-                const int t = kx + KX * ky;
+        if (real) {
+            for (int ky = 0; ky < KY; ky++)
+                for (int kx = 0; kx < KX; kx++) {
+                    const float xr = tile[ty + ky][tx + kx].x;
+                    const int t = kx + KX * ky;
 #pragma unroll
-                for (int f = 0; f < FG; f++) {
-                    float2 wv = wsh[t][f];
-                    acc[f].x = fmaf(xv.x, wv.x, fmaf(-xv.y, wv.y, acc[f].x));
-                    acc[f].y = fmaf(xv.x, wv.y, fmaf(xv.y, wv.x, acc[f].y));
+                    for (int f = 0; f < FG; f++)
+                        acc[f].x = fmaf(xr, wsh[t][f].x, acc[f].x);
                 }
-            }
+        } else {
+            for (int ky = 0; ky < KY; ky++)
+                for (int kx = 0; kx < KX; kx++) {
+                    float2 xv = tile[ty + ky][tx + kx];
+                    const int t = kx + KX * ky;
+#pragma unroll
+                    for (int f = 0; f < FG; f++) {
+                        float2 wv = wsh[t][f];
+                        acc[f].x = fmaf(xv.x, wv.x, fmaf(-xv.y, wv.y, acc[f].x));
+                        acc[f].y = fmaf(xv.x, wv.y, fmaf(xv.y, wv.x, acc[f].y));
+                    }
+                }
+        }
         __syncthreads();
     }
     const long px = x0 + tx, py = y0 + ty;
@@ -200,8 +231,9 @@ __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, A
 // 11x11 layers); grid = pixel-tile splits, partials folded by k_sum_splits.
 template<int K>
 __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part, Acc x, Acc dy, ConvGeom g,
-                                                        int nsplit)
+                                                        int nsplit, const unsigned* __restrict__ imag_flag)
 {
+    const bool real = imag_flag && *imag_flag == 0;
     constexpr int HX = WTX + K - 1, HY = WTY + K - 1;
     extern __shared__ float2 wsm[];
     const int Cin = int(g.Cin), Cout = int(g.Cout);
@@ -242,20 +274,34 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
 #pragma unroll
             for (int k = 0; k < K - 1; k++)
                 win[k] = xr[k];
+            if (real) {
 #pragma unroll 4
-            for (int px = 0; px < WTX; px++) {
-                win[K - 1] = xr[px + K - 1];
-                const float2 d = dr[px];
+                for (int px = 0; px < WTX; px++) {
+                    win[K - 1] = xr[px + K - 1];
+                    const float d = dr[px].x;
 #pragma unroll
-                for (int kx = 0; kx < K; kx++) { // acc[kx] += d * conj(x[px + kx])
-                    acc[kx].x = fmaf(d.x, win[kx].x, acc[kx].x);
-                    acc[kx].y = fmaf(d.y, win[kx].x, acc[kx].y);
-                    acc[kx].x = fmaf(d.y, win[kx].y, acc[kx].x);
-                    acc[kx].y = fmaf(-d.x, win[kx].y, acc[kx].y);
+                    for (int kx = 0; kx < K; kx++)
+                        acc[kx].x = fmaf(d, win[kx].x, acc[kx].x);
+#pragma unroll
+                    for (int k = 0; k < K - 1; k++)
+                        win[k] = win[k + 1];
                 }
+            } else {
+#pragma unroll 4
+                for (int px = 0; px < WTX; px++) {
+                    win[K - 1] = xr[px + K - 1];
+                    const float2 d = dr[px];
 #pragma unroll
-                for (int k = 0; k < K - 1; k++)
-                    win[k] = win[k + 1];
+                    for (int kx = 0; kx < K; kx++) { // acc[kx] += d * conj(x[px + kx])
+                        acc[kx].x = fmaf(d.x, win[kx].x, acc[kx].x);
+                        acc[kx].y = fmaf(d.y, win[kx].x, acc[kx].y);
+                        acc[kx].x = fmaf(d.y, win[kx].y, acc[kx].x);
+                        acc[kx].y = fmaf(-d.x, win[kx].y, acc[kx].y);
+                    }
+#pragma unroll
+                    for (int k = 0; k < K - 1; k++)
+                        win[k] = win[k + 1];
+                }
             }
         }
     }
@@ -291,6 +337,20 @@ void check_geom(const ConvGeom& g)
         throw ConfigError("conv: kernel extent > 11 not supported on device");
 }
 
+// device flag: 1 if any of the operands has a nonzero imaginary part
+unsigned* imag_flag(std::initializer_list<std::pair<const cfloat*, long>> ops)
+{
+    auto& c = ctx();
+    unsigned* f;
+    CUDA_CHECK(cudaMallocAsync(&f, sizeof(unsigned), c.stream));
+    CUDA_CHECK(cudaMemsetAsync(f, 0, sizeof(unsigned), c.stream));
+    for (auto [p, n] : ops) {
+        k_imag_any<<<int(std::min<long>((n + 255) / 256, 2L * c.sm_count)), 256, 0, c.stream>>>(p, n, f);
+        KERNEL_CHECK();
+    }
+    return f;
+}
+
 } // namespace
 
 void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
@@ -309,13 +369,15 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
               unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
     ProfScope prof("conv_fwd", conv_flops(g));
+    unsigned* fl = imag_flag({{x, XY * g.Cin * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
     if (FGv == 2)
         k_conv_direct<0, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
-                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g);
+                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
     else
         k_conv_direct<0, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
-                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g);
+                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
     KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
 }
 
 void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom& g)
@@ -334,13 +396,15 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
               unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
     ProfScope prof("conv_bwd_data", conv_flops(g));
+    unsigned* fl = imag_flag({{dy, XY * g.Cout * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
     if (FGv == 2)
         k_conv_direct<1, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
-                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g);
+                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
     else
         k_conv_direct<1, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
-                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g);
+                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
     KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
 }
 
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g)
@@ -369,9 +433,11 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
         auto kern = k_conv_wgrad_rb<11>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
         const int nthr = int(((11 * g.Cin * g.Cout + 31) / 32) * 32);
+        unsigned* fl = imag_flag({{x, XY * g.Cin * g.B}, {dy, XY * g.Cout * g.B}});
         kern<<<nsplit, nthr, smem, c.stream>>>(part, Acc{x, g.Cin, XY, g.in_chlast}, Acc{dy, g.Cout, XY, g.out_chlast},
-                                              g, nsplit);
+                                              g, nsplit, fl);
         KERNEL_CHECK();
+        CUDA_CHECK(cudaFreeAsync(fl, c.stream));
         k_sum_splits<<<int(std::min(1024L, (n + 255) / 256)), 256, 0, c.stream>>>(dw, part, n, nsplit);
         KERNEL_CHECK();
         CUDA_CHECK(cudaFreeAsync(part, c.stream));

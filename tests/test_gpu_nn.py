@@ -197,3 +197,31 @@ def test_graph_algebra(gpu, ref):
         res.append(g)
     x = crand(rng, d)
     _check_node(res[0], res[1], [x], rng, TOL)
+
+
+@pytest.mark.parametrize("cin,cout,k", [(2, 24, 11), (2, 6, 11), (3, 5, 5)])
+@pytest.mark.parametrize("transposed", [False, True])
+def test_conv_layer_real_operands(gpu, ref, cin, cout, k, transposed):
+    """VarNet-style real-valued activations, weights and cotangents take the
+    real-operand fast path of the CUDA-core convolutions (conv.cu); values,
+    tangents and adjoints still match the reference's complex arithmetic, and
+    the imaginary parts stay exactly zero."""
+    rng = np.random.default_rng(cin * 7 + cout + k)
+    X, Y, B = 36, 20, 2
+    in_dims = list(d16(X, Y, cin))
+    in_dims[15] = B
+    mg = Model.conv_layer(gpu, "c", in_dims, (k, k), cout, transposed=transposed, bias=False)
+    mr = Model.conv_layer(ref, "c", in_dims, (k, k), cout, transposed=transposed, bias=False)
+    ng, nr = mg.nlop, mr.nlop
+    ins = [rrand(rng, nr.in_dims(i)) for i in range(nr.n_in)]
+    og, orf = ng.apply(ins)[0], nr.apply(ins)[0]
+    assert rel_l2(og, orf) <= 1e-5 and not np.any(og.imag)
+    dy = rrand(rng, nr.out_dims(0))
+    ag, ar = ng.adjoint_all(0, dy), nr.adjoint_all(0, dy)
+    for i in range(nr.n_in):
+        assert rel_l2(ag[i], ar[i]) <= 1e-5, i
+        assert not np.any(ag[i].imag), i
+    # a complex cotangent switches back to the complex path
+    dyc = crand(rng, nr.out_dims(0))
+    for u, v in zip(ng.adjoint_all(0, dyc), nr.adjoint_all(0, dyc)):
+        assert rel_l2(u, v) <= 1e-5
