@@ -105,7 +105,10 @@ __global__ void __launch_bounds__(kT) k_stats(double* __restrict__ part, const f
 {
     const Pair q(C);
     const long p0 = long(blockIdx.x) * pix_per_block, p1 = min(npix, p0 + pix_per_block);
-    double a[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    // fp32 running sums per thread (a few hundred terms each, fixed order),
+    // folded across threads and blocks in double: the stream is HBM-bound,
+    // a double accumulate per element was not (FP64 + conversions)
+    float f[2][3] = {{0, 0, 0}, {0, 0, 0}};
     constexpr int U = 4;
     for (long p = p0 + q.pl; p < p1; p += U * q.ppb) {
         float2 re[U], im[U];
@@ -117,14 +120,20 @@ __global__ void __launch_bounds__(kT) k_stats(double* __restrict__ part, const f
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            a[0][0] += re[u].x;
-            a[0][1] += im[u].x;
-            a[0][2] += double(re[u].x) * re[u].x + double(im[u].x) * im[u].x;
-            a[1][0] += re[u].y;
-            a[1][1] += im[u].y;
-            a[1][2] += double(re[u].y) * re[u].y + double(im[u].y) * im[u].y;
+            f[0][0] += re[u].x;
+            f[0][1] += im[u].x;
+            f[0][2] = fmaf(re[u].x, re[u].x, fmaf(im[u].x, im[u].x, f[0][2]));
+            f[1][0] += re[u].y;
+            f[1][1] += im[u].y;
+            f[1][2] = fmaf(re[u].y, re[u].y, fmaf(im[u].y, im[u].y, f[1][2]));
         }
     }
+    double a[2][3];
+#pragma unroll
+    for (int k = 0; k < 2; k++)
+#pragma unroll
+        for (int j = 0; j < 3; j++)
+            a[k][j] = f[k][j];
     fold_lanes<3>(part, a, q, C);
 }
 
@@ -220,7 +229,7 @@ __global__ void __launch_bounds__(kT) k_bwd_reduce(double* __restrict__ part, co
     const Pair q(C);
     const ChanCoef kc[2] = {coef(mu, istd, gamma, beta, 2 * q.l), coef(mu, istd, gamma, beta, 2 * q.l + 1)};
     const long p0 = long(blockIdx.x) * pix_per_block, p1 = min(npix, p0 + pix_per_block);
-    double a[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+    float f[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}; // fp32 per thread, double across threads (see k_stats)
     constexpr int U = 2;
     for (long p = p0 + q.pl; p < p1; p += U * q.ppb) {
         float2 xr[U], xi[U], gr[U], gi[U];
@@ -241,14 +250,20 @@ __global__ void __launch_bounds__(kT) k_bwd_reduce(double* __restrict__ part, co
                 bn_z(kc[k], k ? xr[u].y : xr[u].x, k ? xi[u].y : xi[u].x, hr, hi, zr, zi);
                 const float g_r = zr > 0.f ? (k ? gr[u].y : gr[u].x) : 0.f;
                 const float g_i = zi > 0.f ? (k ? gi[u].y : gi[u].x) : 0.f;
-                a[k][0] += g_r;
-                a[k][1] += g_i;
+                f[k][0] += g_r;
+                f[k][1] += g_i;
                 // gz * conj(yhat)
-                a[k][2] += double(g_r) * hr + double(g_i) * hi;
-                a[k][3] += double(g_i) * hr - double(g_r) * hi;
+                f[k][2] = fmaf(g_r, hr, fmaf(g_i, hi, f[k][2]));
+                f[k][3] = fmaf(g_i, hr, fmaf(-g_r, hi, f[k][3]));
             }
         }
     }
+    double a[2][4];
+#pragma unroll
+    for (int k = 0; k < 2; k++)
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            a[k][j] = f[k][j];
     fold_lanes<4>(part, a, q, C);
 }
 
