@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kT) k_stats(double* __restrict__ part, const f
     // folded across threads and blocks in double: the stream is HBM-bound,
     // a double accumulate per element was not (FP64 + conversions)
     float f[2][3] = {{0, 0, 0}, {0, 0, 0}};
-    constexpr int U = 4;
+    constexpr int U = 8; // 128 B of loads in flight per thread (latency-bound otherwise)
     for (long p = p0 + q.pl; p < p1; p += U * q.ppb) {
         float2 re[U], im[U];
 #pragma unroll
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kT) k_bwd_apply(float* __restrict__ dx, const 
 
 int reduce_blocks(long npix)
 {
-    long b = long(ctx().sm_count) * 4;
+    long b = long(ctx().sm_count) * 8;
     return int(std::max(1L, std::min(b, (npix + 255) / 256)));
 }
 
