@@ -94,6 +94,8 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
             for (int kx = 0; kx < K - 1; kx++)
                 win[ky][kx] = tile[(row + ky) * HX + xs + kx];
         float* op = out + (b * XY + long(X) * gy + x0 + xs) * 2 * F + f;
+        // unrolled: the window shifts become register renames
+#pragma unroll 8
         for (int i = 0; i < seglen; i++, op += 2 * F) {
             const int px = xs + i;
 #pragma unroll
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
             for (int d = 0; d < PD; d++)
                 pre[d] = d < xend ? float2{__ldg(wp + d * 2 * F), __ldg(wp + d * 2 * F + F)} : float2{0.f, 0.f};
             wp += PD * 2 * F;
+#pragma unroll 8
             for (int i = 0; i < xend; i++) {
                 const int px = xs + i;
                 const float2 v = pre[0];
