@@ -164,6 +164,8 @@ int mdnn_set_option(const char* key, long value)
             sense_rank_enable(value != 0);
         else if (k == "sense_rank_ctas")
             sense_rank_ctas(value);
+        else if (k == "sense_rank_tm")
+            sense_rank_tm_enable(value != 0);
         else if (k == "conv_chlast")
             conv_force_chlast(value != 0);
         else

@@ -125,6 +125,7 @@ void conv_tc_enable(bool on);
 // persistent mask-pruned A^H A kernel (sense_rank.cuh); off = sense_fast.cuh path
 void sense_rank_enable(bool on);
 void sense_rank_ctas(long g);
+void sense_rank_tm_enable(bool on);
 bool rank_enabled();
 // test hook: auto-layout convs store multi-channel activations channels-last
 void conv_force_chlast(bool on);

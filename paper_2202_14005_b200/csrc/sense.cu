@@ -583,11 +583,13 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
     if (coils2 == coils && rank_enabled()) {
         const RankPlan rp = rank_plan(g, coils);
         if (rp.ok) {
-            DArray plane1(Dims{g.X * g.Y * g.B}, false);
+            const long n = g.X * g.Y * g.B;
+            DArray plane1(Dims{n * std::max(1, rp.planes - 1)}, false);
             DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
             RankArgs a{};
             a.out = out;
             a.out1 = plane1.data();
+            a.pstride = n;
             a.x = x;
             a.pattern = pattern;
             a.lam = lam;
@@ -597,10 +599,9 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
             unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
             launch_rank_plan(rp, a, g, pl);
             launch_rank(rp, a, coils, g, pl);
-            const long n = g.X * g.Y * g.B;
             k_rank_merge<<<grid_for(n), 256, 0, ctx().stream>>>(out, plane1.data(), rank_split_flags(g, pl),
                                                                 int(g.X), int(g.Y * g.B), int(g.Y), int(rp.nxb),
-                                                                rp.W == 8 ? 3 : 2);
+                                                                rp.W == 8 ? 3 : 2, n);
             KERNEL_CHECK();
             return;
         }
@@ -748,7 +749,7 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
         // few update CTAs: one contended counter atomic per CTA in publish_partial
         const int n_updr = int(std::min<long>(2L * c.sm_count, g.Y * g.B));
         CgMem m = cg_alloc(max_iter, tol, rp.G, n_updr);
-        DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{2 * n}, false);
+        DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{n * std::max(2, rp.planes)}, false);
         DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
         unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
         cfloat* P[2] = {pb.data(), pb.data() + n};
@@ -763,6 +764,7 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             RankArgs a{};
             a.out = ap.data();
             a.out1 = ap.data() + n;
+            a.pstride = n;
             a.x = r.data();
             a.p = P[it & 1];
             a.p_out = P[(it + 1) & 1];
@@ -778,7 +780,7 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             k_cg_update_rank<<<n_updr, 512, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
                                                           ap.data() + n, rank_split_flags(g, pl), int(g.X),
                                                           int(g.Y * g.B), int(g.Y), int(rp.nxb),
-                                                          rp.W == 8 ? 3 : 2, c.d_errflags);
+                                                          rp.W == 8 ? 3 : 2, n, c.d_errflags);
             KERNEL_CHECK();
         }
         k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
@@ -863,6 +865,7 @@ bool g_rank_enabled = true;
 // rank-kernel CTA count override lives in sense_rank.cuh (g_rank_ctas)
 void sense_rank_enable(bool on) { g_rank_enabled = on; }
 void sense_rank_ctas(long g) { g_rank_ctas = g; }
+void sense_rank_tm_enable(bool on) { g_rank_tm = on; }
 bool rank_enabled() { return g_rank_enabled; }
 
 CgResult read_cg_status(const double* status_dev)

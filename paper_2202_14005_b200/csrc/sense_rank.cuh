@@ -27,6 +27,7 @@
 #include <type_traits>
 
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
+bool g_rank_tm = false; // TMEM-resident variant (sense_rank_tm.cuh) for N1 = 16
 
 constexpr int rank_nbox(int Y)
 {
@@ -61,7 +62,8 @@ struct RankCfg {
 
 struct RankArgs {
     cfloat* out;          // plane 0 (mode 0: the result; mode 1: Ap)
-    cfloat* out1;         // plane 1 (split strips)
+    cfloat* out1;         // planes 1.. (strips shared by several CTAs), plane stride pstride
+    long pstride;
     const cfloat* x;      // mode 0: input image; mode 1: r
     cfloat* p;            // mode 1: previous search direction
     cfloat* p_out;        // mode 1: new search direction (== x source at it 0)
@@ -83,6 +85,17 @@ __host__ __device__ __forceinline__ long rank_owner(long u, long U, long G) { re
 __host__ __device__ __forceinline__ bool rank_split(long s, long C, long U, long G)
 {
     return rank_owner(s * C, U, G) != rank_owner(s * C + C - 1, U, G);
+}
+// number of CTAs (= Ap planes) sharing strip s
+__host__ __device__ __forceinline__ int rank_planes(long s, long C, long U, long G)
+{
+    return int(rank_owner(s * C + C - 1, U, G) - rank_owner(s * C, U, G) + 1);
+}
+// destination of a segment's partial: plane 0 = out, plane k >= 1 = out1 + (k - 1) * pstride
+__device__ __forceinline__ cfloat* rank_plane_dst(const RankArgs& a, int strip, int cta)
+{
+    const int k = cta - int(rank_owner(long(strip) * a.C, a.units, a.G));
+    return k == 0 ? a.out : a.out1 + long(k - 1) * a.pstride;
 }
 
 // Per-CTA row plan (shared memory), rebuilt when the item's pattern changes.
@@ -269,7 +282,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
                 // ---- segment epilogue: 1/N1, + lambda x (plane 0), store, <p, Ap>
                 const int b = seg_s / nxb, xx = (seg_s - b * nxb) * W + w;
                 const long img_base = xx + a.X * Y * long(b);
-                cfloat* dst = seg_first ? a.out : a.out1;
+                cfloat* dst = rank_plane_dst(a, seg_s, blockIdx.x);
 #pragma unroll
                 for (int q = 0; q < N1; q++) {
                     const int y = j + N2 * q;
@@ -505,22 +518,25 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
 // out (+)= plane 1 for pixels of split strips (mode 0 result assembly)
 __global__ void __launch_bounds__(256) k_rank_merge(cfloat* out, const cfloat* plane1,
                                                     const unsigned char* __restrict__ split, int X, int rows, int Y,
-                                                    int nxb, int wshift)
+                                                    int nxb, int wshift, long pstride)
 {
     const int X2 = X >> 1;
     for (int row = blockIdx.x; row < rows; row += gridDim.x) {
         const int sb = (row / Y) * nxb;
         const long base = long(row) * X2;
         for (int xp = threadIdx.x; xp < X2; xp += blockDim.x) {
-            if (!split[sb + ((2 * xp) >> wshift)])
+            const int np = split[sb + ((2 * xp) >> wshift)];
+            if (np <= 1)
                 continue;
             const long i = base + xp;
             float4 o = reinterpret_cast<float4*>(out)[i];
-            const float4 t = reinterpret_cast<const float4*>(plane1)[i];
-            o.x += t.x;
-            o.y += t.y;
-            o.z += t.z;
-            o.w += t.w;
+            for (int k = 1; k < np; k++) { // fixed plane order: bitwise deterministic
+                const float4 t = reinterpret_cast<const float4*>(plane1)[i + long(k - 1) * (pstride / 2)];
+                o.x += t.x;
+                o.y += t.y;
+                o.z += t.z;
+                o.w += t.w;
+            }
             reinterpret_cast<float4*>(out)[i] = o;
         }
     }
@@ -534,7 +550,7 @@ __global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloa
                                                         const cfloat* __restrict__ ap,
                                                         const cfloat* __restrict__ ap1,
                                                         const unsigned char* __restrict__ split, int X, int rows,
-                                                        int Y, int nxb, int wshift, unsigned* errflags)
+                                                        int Y, int nxb, int wshift, long pstride, unsigned* errflags)
 {
     __shared__ float s_alpha;
     if (threadIdx.x == 0)
@@ -549,7 +565,8 @@ __global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloa
     float4* r4 = reinterpret_cast<float4*>(r);
     constexpr int U = 2; // element pairs in flight per thread
     float4 av[U], t1[U], pv[U], xv[U], rv[U];
-    bool sp[U], ok[U];
+    int sp[U];
+    bool ok[U];
     int i0 = blockIdx.x * blockDim.x + threadIdx.x;
     auto load = [&](int base) {
 #pragma unroll
@@ -578,11 +595,18 @@ __global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloa
             if (!ok[k])
                 continue;
             float4 a = av[k];
-            if (sp[k]) {
+            if (sp[k] > 1) {
                 a.x += t1[k].x;
                 a.y += t1[k].y;
                 a.z += t1[k].z;
                 a.w += t1[k].w;
+                for (int pk = 2; pk < sp[k]; pk++) { // rare: strips shared by 3+ CTAs
+                    const float4 t = ap14[i0 + k * stride + long(pk - 1) * (pstride / 2)];
+                    a.x += t.x;
+                    a.y += t.y;
+                    a.z += t.z;
+                    a.w += t.w;
+                }
             }
             float4 xx = xv[k], rr = rv[k];
             xx.x += al * pv[k].x;
@@ -612,7 +636,7 @@ __global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloa
 __global__ void k_rank_split_flags(unsigned char* flags, long strips, long C, long U, long G)
 {
     for (long s = blockIdx.x * long(blockDim.x) + threadIdx.x; s < strips; s += long(gridDim.x) * blockDim.x)
-        flags[s] = rank_split(s, C, U, G) ? 1 : 0;
+        flags[s] = (unsigned char)rank_planes(s, C, U, G);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 rank_encode_fn()
@@ -634,6 +658,7 @@ struct RankPlan {
     int N1 = 0, N2 = 0, W = 0;
     long nxb = 0, strips = 0, units = 0;
     int G = 0;
+    int planes = 1; // max CTAs sharing a strip (Ap planes)
     bool ok = false;
 };
 
@@ -667,8 +692,13 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
     case 512: minb = RankCfg<16, 32>::MINB; break;
     case 640: minb = RankCfg<16, 40>::MINB; break;
     }
-    r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : long(minb) * ctx().sm_count, r.strips));
-    r.ok = r.units < (1L << 30) && g.Y * g.C * g.B < (1L << 30) && g.X * g.Y < (1L << 30);
+    if (g_rank_tm && n1 == 16)
+        minb = 3; // k_normal_rank_tm: TMEM-resident accumulators, 3 CTAs per SM
+    r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : long(minb) * ctx().sm_count, r.units));
+    r.planes = 1;
+    for (long s = 0; s < r.strips; s++)
+        r.planes = std::max(r.planes, rank_planes(s, g.C, r.units, r.G));
+    r.ok = r.units < (1L << 30) && g.Y * g.C * g.B < (1L << 30) && g.X * g.Y < (1L << 30) && r.planes < 250;
     return r;
 }
 
@@ -750,10 +780,22 @@ void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsign
 #undef X_
 }
 
+#include "sense_rank_tm.cuh"
+
 void launch_rank(const RankPlan& rp, RankArgs a, const cfloat* coils, const SenseGeom& g,
                  const unsigned char* plans)
 {
     fill_rank_args(rp, a, g);
+    if (g_rank_tm && rp.N1 == 16) {
+        switch (g.Y) {
+        case 256: launch_rank_tm_t<16, 16>(a, coils, g, plans); return;
+        case 320: launch_rank_tm_t<16, 20>(a, coils, g, plans); return;
+        case 368: launch_rank_tm_t<16, 23>(a, coils, g, plans); return;
+        case 512: launch_rank_tm_t<16, 32>(a, coils, g, plans); return;
+        case 640: launch_rank_tm_t<16, 40>(a, coils, g, plans); return;
+        default: break;
+        }
+    }
 #define X_(YY, A1, A2) \
     case YY: launch_rank_t<A1, A2>(a, coils, g, plans); return;
     switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }

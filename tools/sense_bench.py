@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cg", type=int, default=1)
     ap.add_argument("--apply", type=int, default=1)
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (mdnn_set_option)")
     args = ap.parse_args()
     import torch
     from paper_2202_14005_b200 import load_library
@@ -27,6 +28,9 @@ def main():
 
     lib = load_library()
     lib.check(lib.so.mdnn_set_device(0))
+    for kv in args.opt:
+        k, v = kv.split("=")
+        lib.check(lib.so.mdnn_set_option(k.encode(), int(v)))
     stream = torch.cuda.ExternalStream(lib.so.mdnn_stream(), device=torch.device("cuda", 0))
     peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
