@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kT) k_apply(float* __restrict__ out, const flo
     const int tpp = C / 2, l = threadIdx.x % tpp;
     const ChanCoef k0 = coef(mu, istd, gamma, beta, 2 * l), k1 = coef(mu, istd, gamma, beta, 2 * l + 1);
     const long pstride = long(gridDim.x) * kT / tpp;
-    constexpr int U = 2;
+    constexpr int U = 4;
     for (long p = (long(blockIdx.x) * kT + threadIdx.x) / tpp; p < npix; p += U * pstride) {
         float2 re[U], im[U];
 #pragma unroll
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kT) k_bwd_reduce(double* __restrict__ part, co
     const ChanCoef kc[2] = {coef(mu, istd, gamma, beta, 2 * q.l), coef(mu, istd, gamma, beta, 2 * q.l + 1)};
     const long p0 = long(blockIdx.x) * pix_per_block, p1 = min(npix, p0 + pix_per_block);
     float f[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}; // fp32 per thread, double across threads (see k_stats)
-    constexpr int U = 2;
+    constexpr int U = 4; // 128 B of loads in flight per thread
     for (long p = p0 + q.pl; p < p1; p += U * q.ppb) {
         float2 xr[U], xi[U], gr[U], gi[U];
 #pragma unroll
@@ -304,9 +304,25 @@ __global__ void __launch_bounds__(kT) k_bwd_apply(float* __restrict__ dx, const 
     const float2 gmc[2] = {gm[2 * l], gm[2 * l + 1]};
     const float fc[2] = {fh[2 * l], fh[2 * l + 1]};
     const long pstride = long(gridDim.x) * kT / tpp;
-    for (long p = (long(blockIdx.x) * kT + threadIdx.x) / tpp; p < npix; p += pstride) {
-        const float2 xr = ld2(x + p * 2 * C + 2 * l), xi = ld2(x + p * 2 * C + C + 2 * l);
-        const float2 gr2 = ld2(gout + p * 2 * C + 2 * l), gi2 = ld2(gout + p * 2 * C + C + 2 * l);
+    constexpr int U = 2; // 64 B of loads in flight per thread
+    for (long p0 = (long(blockIdx.x) * kT + threadIdx.x) / tpp; p0 < npix; p0 += U * pstride) {
+    float2 xr_[U], xi_[U], gr_[U], gi_[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const long pp = p0 + u * pstride;
+        if (pp < npix) {
+            xr_[u] = ld2(x + pp * 2 * C + 2 * l);
+            xi_[u] = ld2(x + pp * 2 * C + C + 2 * l);
+            gr_[u] = ld2(gout + pp * 2 * C + 2 * l);
+            gi_[u] = ld2(gout + pp * 2 * C + C + 2 * l);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const long p = p0 + u * pstride;
+        if (p >= npix)
+            break;
+        const float2 xr = xr_[u], xi = xi_[u], gr2 = gr_[u], gi2 = gi_[u];
         float o_r[2], o_i[2];
 #pragma unroll
         for (int k = 0; k < 2; k++) {
@@ -322,6 +338,7 @@ __global__ void __launch_bounds__(kT) k_bwd_apply(float* __restrict__ dx, const 
         }
         st2(dx + p * 2 * C + 2 * l, float2{o_r[0], o_r[1]});
         st2(dx + p * 2 * C + C + 2 * l, float2{o_i[0], o_i[1]});
+    }
     }
 }
 
