@@ -69,7 +69,12 @@ int mdnn_set_device(int device);           /* GPU build: selects device + stream
 int mdnn_synchronize(void);
 /* "conv_tc" (1 = tcgen05 TF32 convolutions where supported, 0 = fp32 CUDA
    cores), "conv_chlast" (1 = auto-layout convolutions keep multi-channel
-   activations channels-last; test hook for the thin-conv kernels) */
+   activations channels-last; test hook for the thin-conv kernels),
+   "conv_tc_form" (1 = channel-major transposed tcgen05 kernel for 64-channel
+   outputs, 0 = pixel-major), "conv_tc_pair" (1 = CTA-pair cta_group::2
+   pixel-major kernel), "conv_tc_debug" (diagnostics: 1 = no epilogue stores,
+   2 = no epilogue; results invalid), "sense_rank" / "sense_rank_ctas" /
+   "sense_rank_tm" (A^H A kernel selection) */
 int mdnn_set_option(const char* key, long value);
 /* the library's CUDA stream on the current device (cudaStream_t), so callers
    can order collectives / events with its kernels; NULL in the CPU shim */

@@ -168,6 +168,12 @@ int mdnn_set_option(const char* key, long value)
             sense_rank_tm_enable(value != 0);
         else if (k == "conv_chlast")
             conv_force_chlast(value != 0);
+        else if (k == "conv_tc_debug")
+            conv_tc_debug(int(value));
+        else if (k == "conv_tc_pair")
+            conv_tc_pair_enable(value != 0);
+        else if (k == "conv_tc_form")
+            conv_tc_form(int(value));
         else
             throw ConfigError("unknown option '" + k + "'");
     });

@@ -7,13 +7,16 @@
 //   out[p, (Re f | Im f)] += in[p + tap, (Re c | Im c)] * [[Re u, Im u], [-Im u, Re u]]
 // with u = w[t,c,f] (forward) or conj(w[flip t, f, c]) (backward-data).
 //
-// CTA work unit ("super-tile"): 32 x 16 output pixels of one item = 4 UMMA
-// M-tiles of 8 x 16 pixels, each with its own TMEM accumulator (4 x N
-// columns).  Per 32-float K-chunk the CTA TMA-loads ONE zero-padded halo of
-// 34 x 18 pixels (pitch 40, SWIZZLE_128B, 92 KB) and feeds all 9 taps from
-// row-shifted shared-memory views of it (UMMA start address + base_offset), so
-// activations cross L2->SMEM 1.4x instead of 9x; the packed weights stream
-// per (tap, chunk) through a 2-stage TMA ring and are reused by the 4 M-tiles.
+// CTA work unit ("super-tile"): 16 x 16 output pixels of one item = 2 UMMA
+// M-tiles of 8 x 16 pixels, each with its own TMEM accumulator, and the
+// accumulator set double-buffered (2 x 2 x N columns) so that the epilogue of
+// one super-tile overlaps the MMAs of the next (serialised, the epilogue's
+// 256 KB of stores per 512 pixels cost ~30% of the MMA time).  Per 32-float
+// K-chunk the CTA TMA-loads ONE zero-padded halo of 18 x 18 pixels (pitch 24,
+// SWIZZLE_128B, 54 KB) and feeds all 9 taps from row-shifted shared-memory
+// views of it (UMMA start address + base_offset), so activations cross
+// L2->SMEM 1.7x instead of 9x; the packed weights stream per (tap, chunk)
+// through a 4-stage TMA ring and are reused by the M-tiles.
 // Warp roles: warp 0 TMA producer, warp 1 TMEM allocator + single-thread MMA
 // issuer, warps 2-5 epilogue (TMEM -> registers -> global).  Persistent grid.
 // Operands are rounded to TF32 with round-to-nearest by their producers
@@ -34,11 +37,12 @@ namespace {
 
 using namespace sm100;
 
-constexpr int TILE_X = 32, TILE_Y = 16;
-constexpr int HALO_P = 40;             // halo pitch (pixels per line, multiple of 8, >= TILE_X + 2)
+constexpr int NM = 2;                  // UMMA M-tiles (8 x 16 pixels each) per super-tile
+constexpr int TILE_X = 8 * NM, TILE_Y = 16;
+constexpr int HALO_P = 24;             // halo pitch (pixels per line, multiple of 8, >= TILE_X + 2)
 constexpr int HALO_L = TILE_Y + 2;     // halo lines
 constexpr int HALO_BYTES = HALO_L * HALO_P * 128;
-constexpr int NBSTAGE = 2;
+constexpr int NBSTAGE = 6;
 constexpr int NTHREADS = 192;
 
 // epilogue staging per warp: 32 pixels x 16 accumulator columns, pitch 20 floats
@@ -58,12 +62,13 @@ struct TcSmem {
 template<int CIN2, int N>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
-              float* __restrict__ out, int X, int Y, int B)
+              float* __restrict__ out, int X, int Y, int B, int dbg)
 {
     static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
-    static_assert(N % 16 == 0 && N >= 16 && 4 * N <= 512, "N must fit 4 accumulators in TMEM");
+    static_assert(N % 16 == 0 && N >= 16 && 2 * NM * N <= 512, "N must fit 2 x NM accumulators in TMEM");
     constexpr int NCH = CIN2 / 32;
-    constexpr int TMEM_COLS = 4 * N <= 32 ? 32 : (4 * N <= 64 ? 64 : (4 * N <= 128 ? 128 : (4 * N <= 256 ? 256 : 512)));
+    constexpr int ACC = 2 * NM * N; // double-buffered accumulators: epilogue of tile i overlaps MMAs of tile i+1
+    constexpr int TMEM_COLS = ACC <= 32 ? 32 : (ACC <= 64 ? 64 : (ACC <= 128 ? 128 : (ACC <= 256 ? 256 : 512)));
     using S = TcSmem<N>;
 
     extern __shared__ uint8_t smem_raw[];
@@ -75,9 +80,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint64_t* halo_empty = bars + 2;       // [2]
     uint64_t* b_full = bars + 4;           // [NBSTAGE]
     uint64_t* b_empty = bars + 4 + NBSTAGE;
-    uint64_t* tmem_full = bars + 4 + 2 * NBSTAGE;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* tmem_full = bars + 4 + 2 * NBSTAGE; // [2]
+    uint64_t* tmem_empty = tmem_full + 2;         // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int tiles_x = (X + TILE_X - 1) / TILE_X, tiles_y = (Y + TILE_Y - 1) / TILE_Y;
@@ -94,8 +99,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], 1);
         }
-        mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 128);
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 128);
+        }
         fence_barrier_init();
     }
     if (warp == 1)
@@ -133,7 +140,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             uint32_t hi = 0, bi = 0, ti = 0;
             const uint32_t halo_addr = smem_u32(halo), b_addr = smem_u32(bst);
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
-                mbar_wait(tmem_empty, (ti & 1) ^ 1);
+                const uint32_t ab = ti & 1, acc = tmem_base + ab * NM * N;
+                mbar_wait(&tmem_empty[ab], ((ti >> 1) & 1) ^ 1);
                 tc_fence_after();
                 for (int c = 0; c < NCH; c++, hi++) {
                     const uint32_t hb = hi & 1, hph = (hi >> 1) & 1;
@@ -147,20 +155,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const int ky = t / 3, kx = t % 3;
                         const uint32_t bbase = b_addr + st * S::B_BYTES;
 #pragma unroll
-                        for (int xt = 0; xt < 4; xt++) {
+                        for (int xt = 0; xt < NM; xt++) {
                             const uint32_t row0 = ky * HALO_P + xt * 8 + kx;
 #pragma unroll
                             for (int k = 0; k < 4; k++) {
                                 const uint64_t ad = umma_desc_sw128(hbase + row0 * 128 + k * 32, HALO_P * 128);
                                 const uint64_t bd = umma_desc_sw128(bbase + k * 32, 1024);
-                                mma_tf32(tmem_base + xt * N, ad, bd, idesc, (c | t | k) != 0);
+                                mma_tf32(acc + xt * N, ad, bd, idesc, (c | t | k) != 0);
                             }
                         }
                         mma_commit(&b_empty[st]);
                     }
                     mma_commit(&halo_empty[hb]);
                 }
-                mma_commit(tmem_full);
+                mma_commit(&tmem_full[ab]);
             }
         }
     } else {
@@ -171,19 +179,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
             const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
             const int x0 = tx * TILE_X, y0 = ty * TILE_Y;
-            mbar_wait(tmem_full, ti & 1);
+            const uint32_t ab = ti & 1, acc = tmem_base + ab * NM * N;
+            mbar_wait(&tmem_full[ab], (ti >> 1) & 1);
             tc_fence_after();
-                // Staged through shared memory so that each store instruction
+            if (dbg == 2) {
+                tc_fence_before();
+                mbar_arrive(&tmem_empty[ab]);
+                continue;
+            }
+            // Staged through shared memory so that each store instruction
             // writes 8 pixels x 64 contiguous bytes (lanes 4 per pixel)
             // instead of 32 scattered 16-byte pieces (LSU-throttled).
             // Warp lg owns pixel rows gy = 4 lg .. 4 lg + 3 of each M-tile.
             const int qd = lane & 3, pl = lane >> 2;
 #pragma unroll 1
-            for (int xt = 0; xt < 4; xt++) {
+            for (int xt = 0; xt < NM; xt++) {
 #pragma unroll 1
                 for (int nc = 0; nc < N / 16; nc++) {
                     float v[16];
-                    tmem_ld16(tmem_base + (uint32_t(lg * 32) << 16) + xt * N + nc * 16, v);
+                    tmem_ld16(acc + (uint32_t(lg * 32) << 16) + xt * N + nc * 16, v);
                     tmem_ld_wait();
                     float4* st4 = reinterpret_cast<float4*>(estage + lane * EPI_PITCH);
 #pragma unroll
@@ -195,14 +209,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         const int rr = it * 8 + pl; // staged pixel: row 4 lg + it, x offset pl
                         const int px = x0 + xt * 8 + pl, py = y0 + lg * 4 + it;
                         const float4 val = reinterpret_cast<const float4*>(estage + rr * EPI_PITCH)[qd];
-                        if (px < X && py < Y)
+                        if (px < X && py < Y && dbg != 1)
                             reinterpret_cast<float4*>(out + ((long(b) * Y + py) * X + px) * N + nc * 16)[qd] = val;
                     }
                     __syncwarp();
                 }
             }
             tc_fence_before();
-            mbar_arrive(tmem_empty);
+            mbar_arrive(&tmem_empty[ab]);
         }
     }
     tc_fence_before();
@@ -210,6 +224,365 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Transposed form for 2*Cout = 128 (the MoDL 64 -> 64 layers): one UMMA
+// computes D^T[n = output (re|im) channel, 128][p = pixel, 256] over an
+// 8 x 32 pixel super-tile, with the packed weights Bt[n][k] as the A operand
+// (M = 128) and the activation halo view as the B operand (N = 256, 8-pixel
+// core-matrix rows strided by the halo line pitch).  Against the pixel-major
+// form (M = 128 pixels, N = 128) every MMA instruction does twice the work --
+// the single-thread issue loop was the limit there -- and reads 12 KB of
+// operands per 2 x 128 x 128 x 8 MACs instead of 16 KB.  The accumulator is
+// double-buffered (2 x 256 TMEM columns) so the epilogue of one super-tile
+// overlaps the MMAs of the next; TMEM lane = output channel, so each warp
+// store writes one pixel's 32 consecutive channels (128 B, coalesced).
+constexpr int TT_X = 8, TT_Y = 32;             // super-tile (pixels)
+constexpr int TT_P = 16;                       // halo pitch (>= TT_X + 2, multiple of 8)
+constexpr int TT_L = TT_Y + 2;                 // halo lines
+constexpr int TT_HALO = TT_L * TT_P * 128;     // 68 KB per 32-float chunk
+constexpr int TT_WST = 4;                      // weight stages (16 KB each)
+
+struct TtSmem {
+    static constexpr int W_BYTES = 128 * 128;
+    static constexpr int HALO_OFF = 0;
+    static constexpr int W_OFF = 2 * TT_HALO;
+    static constexpr int BAR_OFF = W_OFF + TT_WST * W_BYTES;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template<int CIN2>
+__global__ void __launch_bounds__(NTHREADS, 1)
+    k_conv_tc_t(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
+                float* __restrict__ out, int X, int Y, int B, int dbg)
+{
+    static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
+    constexpr int N = 128, NP = TT_X * TT_Y, NCH = CIN2 / 32;
+    using S = TtSmem;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* halo = smem + S::HALO_OFF;
+    uint8_t* wst = smem + S::W_OFF;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* halo_full = bars;        // [2]
+    uint64_t* halo_empty = bars + 2;   // [2]
+    uint64_t* w_full = bars + 4;       // [TT_WST]
+    uint64_t* w_empty = bars + 4 + TT_WST;
+    uint64_t* tmem_full = bars + 4 + 2 * TT_WST; // [2]
+    uint64_t* tmem_empty = tmem_full + 2;        // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int tiles_x = (X + TT_X - 1) / TT_X, tiles_y = (Y + TT_Y - 1) / TT_Y;
+    const int ntiles = tiles_x * tiles_y * B;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_act);
+        prefetch_tmap(&tm_w);
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&halo_full[i], 1);
+            mbar_init(&halo_empty[i], 1);
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 128);
+        }
+        for (int i = 0; i < TT_WST; i++) {
+            mbar_init(&w_full[i], 1);
+            mbar_init(&w_empty[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1)
+        tmem_alloc<2 * NP>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer ----------------
+            uint32_t hi = 0, wi = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
+                const int x0 = tx * TT_X, y0 = ty * TT_Y;
+                for (int c = 0; c < NCH; c++, hi++) {
+                    const uint32_t hb = hi & 1, hph = (hi >> 1) & 1;
+                    mbar_wait(&halo_empty[hb], hph ^ 1);
+                    mbar_arrive_expect_tx(&halo_full[hb], TT_HALO);
+                    tma_load_4d(halo + hb * TT_HALO, &tm_act, &halo_full[hb], c * 32, x0 - 1, y0 - 1, b);
+                    for (int t = 0; t < 9; t++, wi++) {
+                        const uint32_t st = wi % TT_WST, ph = (wi / TT_WST) & 1;
+                        mbar_wait(&w_empty[st], ph ^ 1);
+                        mbar_arrive_expect_tx(&w_full[st], S::W_BYTES);
+                        tma_load_2d(wst + st * S::W_BYTES, &tm_w, &w_full[st], t * CIN2 + c * 32, 0);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer (single thread) ----------------
+            constexpr uint32_t idesc = idesc_tf32(128, NP);
+            uint32_t hi = 0, wi = 0, ti = 0;
+            const uint64_t hdesc0 = umma_desc_sw128(smem_u32(halo), TT_P * 128);
+            const uint64_t wdesc0 = umma_desc_sw128(smem_u32(wst), 1024);
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+                const uint32_t ab = ti & 1, acc = tmem_base + ab * NP;
+                mbar_wait(&tmem_empty[ab], ((ti >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (int c = 0; c < NCH; c++, hi++) {
+                    const uint32_t hb = hi & 1, hph = (hi >> 1) & 1;
+                    mbar_wait(&halo_full[hb], hph);
+                    tc_fence_after();
+                    const uint64_t hdesc = hdesc0 + (hb * TT_HALO >> 4);
+#pragma unroll
+                    for (int t = 0; t < 9; t++, wi++) {
+                        const uint32_t st = wi % TT_WST, ph = (wi / TT_WST) & 1;
+                        mbar_wait(&w_full[st], ph);
+                        tc_fence_after();
+                        const uint64_t wdesc = wdesc0 + (st * S::W_BYTES >> 4);
+                        const int ky = t / 3, kx = t % 3;
+#pragma unroll
+                        for (int k = 0; k < 4; k++)
+                            mma_tf32(acc, wdesc + (k * 32 >> 4), hdesc + (((ky * TT_P + kx) * 128 + k * 32) >> 4), idesc,
+                                     (c | t | k) != 0);
+                        mma_commit(&w_empty[st]);
+                    }
+                    mma_commit(&halo_empty[hb]);
+                }
+                mma_commit(&tmem_full[ab]);
+            }
+        }
+    } else {
+        // ---------------- epilogue: TMEM lane = channel, column = pixel ----------------
+        const int lg = warp & 3, n = lg * 32 + lane;
+        uint32_t ti = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+            const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
+            const int x0 = tx * TT_X, y0 = ty * TT_Y;
+            const uint32_t ab = ti & 1, acc = tmem_base + ab * NP + (uint32_t(lg * 32) << 16);
+            mbar_wait(&tmem_full[ab], (ti >> 1) & 1);
+            tc_fence_after();
+            const bool full_x = x0 + TT_X <= X;
+#pragma unroll 1
+            for (int jc = 0; jc < NP / 32 && dbg != 2; jc++) {
+                const int py0 = y0 + jc * 4; // 32 columns = 4 lines x 8 pixels
+                if (py0 >= Y)
+                    break;
+                float v[32];
+                tmem_ld32(acc + jc * 32, v);
+                tmem_ld_wait();
+                float* o = out + ((long(b) * Y + py0) * X + x0) * N + n;
+#pragma unroll
+                for (int j = 0; j < 32; j++) {
+                    const int l = j >> 3, xo = j & 7;
+                    if ((full_x || x0 + xo < X) && py0 + l < Y && dbg != 1)
+                        o[(long(l) * X + xo) * N] = v[j];
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tmem_empty[ab]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<2 * NP>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (cluster of 2, tcgen05 cta_group::2): the pair runs one
+// M = 256 UMMA per (M-tile, tap, k-step) whose rows 0-127 come from the leader
+// CTA's halo view and rows 128-255 from the peer's (two neighbouring
+// super-tiles), and whose B operand (packed weights) is split by N: each CTA
+// TMA-loads and holds only its N/2 rows of every weight stage.  Per CTA this
+// halves the weight traffic from L2 and the weight reads from shared memory
+// (the 1-CTA kernel's two limits: ~40 B/clk of L2->SMEM and ~120 B/clk of
+// SMEM operand reads per SM at the TF32 rate).  The leader's single thread
+// issues all MMAs; the TMA loads of both CTAs complete on the leader's
+// full-barriers (.cta_group::2), and the leader's commits arrive on the
+// empty / accumulator-full barriers of both CTAs (multicast).  Both epilogues
+// release the accumulator buffer on the leader's barrier (8 warp arrivals).
+template<int N>
+struct TcPairSmem {
+    static constexpr int B_BYTES = (N / 2) * 128; // this CTA's half of a weight stage
+    static constexpr int HALO_OFF = 0;
+    static constexpr int B_OFF = 2 * HALO_BYTES;
+    static constexpr int EPI_OFF = B_OFF + NBSTAGE * B_BYTES;
+    static constexpr int BAR_OFF = EPI_OFF + 4 * EPI_WARP_BYTES;
+    static constexpr int TOTAL = BAR_OFF + 256 + 1024;
+};
+
+template<int CIN2, int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    k_conv_tc_pair(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
+                   float* __restrict__ out, int X, int Y, int B, int dbg)
+{
+    static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
+    static_assert(N % 32 == 0 && N >= 32 && 2 * NM * N <= 512, "N must fit 2 x NM accumulators in TMEM");
+    constexpr int NCH = CIN2 / 32;
+    constexpr int ACC = 2 * NM * N;
+    constexpr int TMEM_COLS = ACC <= 32 ? 32 : (ACC <= 64 ? 64 : (ACC <= 128 ? 128 : (ACC <= 256 ? 256 : 512)));
+    using S = TcPairSmem<N>;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* halo = smem + S::HALO_OFF;
+    uint8_t* bst = smem + S::B_OFF;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
+    uint64_t* halo_full = bars;            // [2]   (leader's used)
+    uint64_t* halo_empty = bars + 2;       // [2]
+    uint64_t* b_full = bars + 4;           // [NBSTAGE] (leader's used)
+    uint64_t* b_empty = bars + 4 + NBSTAGE;
+    uint64_t* tmem_full = bars + 4 + 2 * NBSTAGE; // [2]
+    uint64_t* tmem_empty = tmem_full + 2;         // [2] (leader's used)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int tiles_x = (X + TILE_X - 1) / TILE_X, tiles_y = (Y + TILE_Y - 1) / TILE_Y;
+    const int ntiles = tiles_x * tiles_y * B;
+    const int npairs = (ntiles + 1) / 2, ncl = gridDim.x / 2, cid = blockIdx.x / 2;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_act);
+        prefetch_tmap(&tm_w);
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&halo_full[i], 1);
+            mbar_init(&halo_empty[i], 1);
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 8);
+        }
+        for (int i = 0; i < NBSTAGE; i++) {
+            mbar_init(&b_full[i], 1);
+            mbar_init(&b_empty[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1)
+        tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer (both CTAs) ----------------
+            uint32_t hi = 0, bi = 0;
+            for (int q = cid; q < npairs; q += ncl) {
+                const int tile = 2 * q + int(rank); // past the end: OOB coordinates, zero-filled
+                const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
+                const int x0 = tx * TILE_X, y0 = ty * TILE_Y;
+                for (int c = 0; c < NCH; c++, hi++) {
+                    const uint32_t hb = hi & 1, hph = (hi >> 1) & 1;
+                    mbar_wait(&halo_empty[hb], hph ^ 1);
+                    if (leader)
+                        mbar_arrive_expect_tx(&halo_full[hb], 2 * HALO_BYTES);
+                    tma_load_4d_pair(halo + hb * HALO_BYTES, &tm_act, mapa_shared(&halo_full[hb], 0), c * 32, x0 - 1,
+                                     y0 - 1, b);
+                    for (int t = 0; t < 9; t++, bi++) {
+                        const uint32_t st = bi % NBSTAGE, bph = (bi / NBSTAGE) & 1;
+                        mbar_wait(&b_empty[st], bph ^ 1);
+                        if (leader)
+                            mbar_arrive_expect_tx(&b_full[st], 2 * S::B_BYTES);
+                        tma_load_2d_pair(bst + st * S::B_BYTES, &tm_w, mapa_shared(&b_full[st], 0),
+                                         t * CIN2 + c * 32, int(rank) * (N / 2));
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ---------------- MMA issuer (leader CTA, single thread) ----------------
+            constexpr uint32_t idesc = idesc_tf32(256, N);
+            uint32_t hi = 0, bi = 0, ti = 0;
+            const uint32_t halo_addr = smem_u32(halo), b_addr = smem_u32(bst);
+            for (int q = cid; q < npairs; q += ncl, ti++) {
+                const uint32_t ab = ti & 1, acc = tmem_base + ab * NM * N;
+                mbar_wait(&tmem_empty[ab], ((ti >> 1) & 1) ^ 1);
+                tc_fence_after();
+                for (int c = 0; c < NCH; c++, hi++) {
+                    const uint32_t hb = hi & 1, hph = (hi >> 1) & 1;
+                    mbar_wait(&halo_full[hb], hph);
+                    tc_fence_after();
+                    const uint32_t hbase = halo_addr + hb * HALO_BYTES;
+                    for (int t = 0; t < 9; t++, bi++) {
+                        const uint32_t st = bi % NBSTAGE, bph = (bi / NBSTAGE) & 1;
+                        mbar_wait(&b_full[st], bph);
+                        tc_fence_after();
+                        const int ky = t / 3, kx = t % 3;
+                        const uint32_t bbase = b_addr + st * S::B_BYTES;
+#pragma unroll
+                        for (int xt = 0; xt < NM; xt++) {
+                            const uint32_t row0 = ky * HALO_P + xt * 8 + kx;
+#pragma unroll
+                            for (int k = 0; k < 4; k++) {
+                                const uint64_t ad = umma_desc_sw128(hbase + row0 * 128 + k * 32, HALO_P * 128);
+                                const uint64_t bd = umma_desc_sw128(bbase + k * 32, 1024);
+                                mma_tf32_pair(acc + xt * N, ad, bd, idesc, (c | t | k) != 0);
+                            }
+                        }
+                        mma_commit_pair(&b_empty[st], 0x3);
+                    }
+                    mma_commit_pair(&halo_empty[hb], 0x3);
+                }
+                mma_commit_pair(&tmem_full[ab], 0x3);
+            }
+        }
+    } else {
+        // ---------------- epilogue (both CTAs): own TMEM lanes = own super-tile ----------------
+        const int lg = warp & 3;
+        float* estage = reinterpret_cast<float*>(smem + S::EPI_OFF + lg * EPI_WARP_BYTES);
+        uint32_t ti = 0;
+        for (int q = cid; q < npairs; q += ncl, ti++) {
+            const int tile = 2 * q + int(rank);
+            const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
+            const int x0 = tx * TILE_X, y0 = ty * TILE_Y;
+            const uint32_t ab = ti & 1, acc = tmem_base + ab * NM * N;
+            mbar_wait(&tmem_full[ab], (ti >> 1) & 1);
+            tc_fence_after();
+            const bool store = tile < ntiles && dbg != 2;
+            const int qd = lane & 3, pl = lane >> 2;
+#pragma unroll 1
+            for (int xt = 0; xt < NM && store; xt++) {
+#pragma unroll 1
+                for (int nc = 0; nc < N / 16; nc++) {
+                    float v[16];
+                    tmem_ld16(acc + (uint32_t(lg * 32) << 16) + xt * N + nc * 16, v);
+                    tmem_ld_wait();
+                    float4* st4 = reinterpret_cast<float4*>(estage + lane * EPI_PITCH);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; q4++)
+                        st4[q4] = make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+                    __syncwarp();
+#pragma unroll
+                    for (int it = 0; it < 4; it++) {
+                        const int rr = it * 8 + pl;
+                        const int px = x0 + xt * 8 + pl, py = y0 + lg * 4 + it;
+                        const float4 val = reinterpret_cast<const float4*>(estage + rr * EPI_PITCH)[qd];
+                        if (px < X && py < Y && dbg != 1)
+                            reinterpret_cast<float4*>(out + ((long(b) * Y + py) * X + px) * N + nc * 16)[qd] = val;
+                    }
+                    __syncwarp();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive_cluster(mapa_shared(&tmem_empty[ab], 0));
+        }
+    }
+    tc_fence_before();
+    cluster_sync(); // the peer's smem and TMEM stay live until the leader's last MMAs are done
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<TMEM_COLS>(tmem_base);
     }
 }
 
@@ -442,12 +815,12 @@ CUtensorMap make_act_map(const float* base, int C2, int X, int Y, int B, int box
     return m;
 }
 
-CUtensorMap make_w_map(const float* base, int K, int N)
+CUtensorMap make_w_map(const float* base, int K, int N, int box_n = 0)
 {
     CUtensorMap m;
     cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(N)};
     cuuint64_t strides[1] = {cuuint64_t(K) * 4};
-    cuuint32_t box[2] = {32, cuuint32_t(N)};
+    cuuint32_t box[2] = {32, cuuint32_t(box_n ? box_n : N)};
     cuuint32_t es[2] = {1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -456,6 +829,10 @@ CUtensorMap make_w_map(const float* base, int K, int N)
         throw CudaError("cuTensorMapEncodeTiled(weights) failed: " + std::to_string(int(r)));
     return m;
 }
+
+int g_tc_dbg = 0; // diagnostics: 1 = epilogue without global stores, 2 = no epilogue
+bool g_tc_pair = true; // CTA-pair (cta_group::2) kernel for the fwd / bwd-data convolutions
+int g_tc_form = 1;     // 1: transposed (channel-major accumulator) kernel where 2 Cout = 128
 
 template<int CIN2, int N>
 void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int B)
@@ -474,9 +851,46 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
             done[c.device] = true;
         }
     }
+    if (N == 128 && g_tc_form == 1) {
+        // transposed form: D^T[channel][pixel], N = 256 pixels per MMA
+        CUtensorMap tat = make_act_map(act, CIN2, X, Y, B, TT_P, TT_L);
+        auto kt = k_conv_tc_t<CIN2>;
+        const int smem_t = TtSmem::TOTAL;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            static std::map<int, bool> done_t;
+            if (!done_t[c.device]) {
+                CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_t));
+                done_t[c.device] = true;
+            }
+        }
+        const int nt = ((X + TT_X - 1) / TT_X) * ((Y + TT_Y - 1) / TT_Y) * B;
+        kt<<<std::min(nt, c.sm_count), NTHREADS, smem_t, c.stream>>>(tat, tw, out, X, Y, B, g_tc_dbg);
+        KERNEL_CHECK();
+        return;
+    }
     const int ntiles = ((X + TILE_X - 1) / TILE_X) * ((Y + TILE_Y - 1) / TILE_Y) * B;
+    if (g_tc_pair) {
+        // CTA pairs: half of every weight stage per CTA, multicast commits
+        CUtensorMap twp = make_w_map(wpk, 9 * CIN2, N, N / 2);
+        auto kp = k_conv_tc_pair<CIN2, N>;
+        const int smem_p = TcPairSmem<N>::TOTAL;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            static std::map<int, bool> done_p;
+            if (!done_p[c.device]) {
+                CUDA_CHECK(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_p));
+                done_p[c.device] = true;
+            }
+        }
+        const int npairs = (ntiles + 1) / 2;
+        const int grid = 2 * std::min(npairs, c.sm_count / 2);
+        kp<<<grid, NTHREADS, smem_p, c.stream>>>(ta, twp, out, X, Y, B, g_tc_dbg);
+        KERNEL_CHECK();
+        return;
+    }
     const int grid = std::min(ntiles, c.sm_count);
-    kern<<<grid, NTHREADS, smem, c.stream>>>(ta, tw, out, X, Y, B);
+    kern<<<grid, NTHREADS, smem, c.stream>>>(ta, tw, out, X, Y, B, g_tc_dbg);
     KERNEL_CHECK();
 }
 
@@ -571,6 +985,9 @@ void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom
 }
 
 void conv_tc_enable(bool on) { g_tc_enabled = on; }
+void conv_tc_debug(int mode) { g_tc_dbg = mode; }
+void conv_tc_pair_enable(bool on) { g_tc_pair = on; }
+void conv_tc_form(int f) { g_tc_form = f; }
 
 namespace {
 bool g_force_chlast = false;

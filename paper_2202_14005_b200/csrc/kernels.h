@@ -122,6 +122,9 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
 // tcgen05 TF32 implicit-GEMM path (conv_tc.cu) for 3x3 layers with 32/64 channels
 void conv_tc_enable(bool on);
+void conv_tc_debug(int mode);
+void conv_tc_pair_enable(bool on);
+void conv_tc_form(int f);
 // persistent mask-pruned A^H A kernel (sense_rank.cuh); off = sense_fast.cuh path
 void sense_rank_enable(bool on);
 void sense_rank_ctas(long g);

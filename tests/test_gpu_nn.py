@@ -101,6 +101,28 @@ def test_conv_tensor_core_vs_cuda_core(gpu):
         assert rel_l2(a, b) <= 1e-3
 
 
+@pytest.mark.parametrize("opts", [{"conv_tc_form": 0, "conv_tc_pair": 0}, {"conv_tc_form": 0, "conv_tc_pair": 1},
+                                  {"conv_tc_form": 1, "conv_tc_pair": 0}])
+@pytest.mark.parametrize("cin,cout,X,Y,B", [(64, 64, 40, 70, 2), (32, 64, 17, 33, 1), (64, 32, 24, 16, 3)])
+def test_conv_tc_kernel_variants(gpu, ref, opts, cin, cout, X, Y, B):
+    """Every tcgen05 conv kernel form (pixel-major 1-CTA, CTA pair, channel-major
+    transposed) against the reference, fwd + bwd-data + bwd-weight, partial
+    super-tiles in x and y."""
+    rng = np.random.default_rng(cin + cout + X)
+    in_dims = list(d16(X, Y, cin))
+    in_dims[15] = B
+    try:
+        for k, v in opts.items():
+            gpu.check(gpu.so.mdnn_set_option(k.encode(), v))
+        mg = Model.conv_layer(gpu, "c", in_dims, (3, 3), cout)
+        mr = Model.conv_layer(ref, "c", in_dims, (3, 3), cout)
+        ins = [crand(rng, mr.nlop.in_dims(i)) for i in range(mr.nlop.n_in)]
+        _check_node(mg.nlop, mr.nlop, ins, rng, CONV_TOL, mr.arg_names)
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"conv_tc_form", 1))
+        gpu.check(gpu.so.mdnn_set_option(b"conv_tc_pair", 1))
+
+
 def test_conv_weights_init_bitwise(gpu, ref):
     in_dims = list(d16(8, 8, 4))
     mg = Model.conv_layer(gpu, "dw1", in_dims, (3, 3), 16)
