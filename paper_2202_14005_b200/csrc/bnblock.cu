@@ -137,6 +137,11 @@ __global__ void __launch_bounds__(kT) k_stats(double* __restrict__ part, const f
     fold_lanes<3>(part, a, q, C);
 }
 
+__device__ void stats_finish(const double (&r)[3], float2* __restrict__ mu, float* __restrict__ istd,
+                             float2* __restrict__ mean_out, float2* __restrict__ var_out, int c, long m,
+                             const float2* __restrict__ mean_in, const float2* __restrict__ var_in, float eps,
+                             float mom);
+
 // final: mean, var (biased), istd, moving statistics; one block per channel
 __global__ void __launch_bounds__(kT) k_stats_final(float2* __restrict__ mu, float* __restrict__ istd,
                                                     float2* __restrict__ mean_out, float2* __restrict__ var_out,
@@ -147,8 +152,32 @@ __global__ void __launch_bounds__(kT) k_stats_final(float2* __restrict__ mu, flo
     const int c = blockIdx.x;
     double r[3];
     sum_partials<3>(r, part, nblocks, C, c);
-    if (threadIdx.x != 0)
-        return;
+    if (threadIdx.x == 0)
+        stats_finish(r, mu, istd, mean_out, var_out, c, m, mean_in, var_in, eps, mom);
+}
+
+// final from producer partials (conv epilogue): part[blk][2C real channels][sum, sum of squares]
+__global__ void __launch_bounds__(kT) k_stats_final_pre(float2* __restrict__ mu, float* __restrict__ istd,
+                                                        float2* __restrict__ mean_out, float2* __restrict__ var_out,
+                                                        const double* __restrict__ part, int nblocks, int C, long m,
+                                                        const float2* __restrict__ mean_in,
+                                                        const float2* __restrict__ var_in, float eps, float mom)
+{
+    const int c = blockIdx.x;
+    double re[2], im[2];
+    sum_partials<2>(re, part, nblocks, 2 * C, c);
+    __syncthreads(); // sum_partials' shared scratch is reused
+    sum_partials<2>(im, part, nblocks, 2 * C, C + c);
+    const double r[3] = {re[0], im[0], re[1] + im[1]};
+    if (threadIdx.x == 0)
+        stats_finish(r, mu, istd, mean_out, var_out, c, m, mean_in, var_in, eps, mom);
+}
+
+__device__ void stats_finish(const double (&r)[3], float2* __restrict__ mu, float* __restrict__ istd,
+                             float2* __restrict__ mean_out, float2* __restrict__ var_out, int c, long m,
+                             const float2* __restrict__ mean_in, const float2* __restrict__ var_in, float eps,
+                             float mom)
+{
     const double mr = r[0] / double(m), mi = r[1] / double(m);
     const double var = r[2] / double(m) - (mr * mr + mi * mi);
     const float meanr = float(mr), meani = float(mi), v = float(var > 0 ? var : 0);
@@ -358,11 +387,21 @@ int grid_ew(long npix, int C)
 
 void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, float2* var_out, const float* x,
                      const float2* mean_in, const float2* var_in, const float2* gamma, const float2* beta, long npix,
-                     int C, float eps, float mom, bool round_tf32)
+                     int C, float eps, float mom, bool round_tf32, const double* pre_part, int pre_blocks)
 {
     auto& c = ctx();
     if (C < 2 || 256 % C != 0)
         throw ConfigError("bnblock: channel count must be >= 2 and divide 256");
+    if (pre_part && pre_blocks > 0) {
+        // statistics partials came with x from its producer: apply pass only
+        ProfScope prof("bnblock_fwd", 8.0 * 2 * npix * C);
+        k_stats_final_pre<<<C, kT, 0, c.stream>>>(mu, istd, mean_out, var_out, pre_part, pre_blocks, C, npix,
+                                                  mean_in, var_in, eps, mom);
+        KERNEL_CHECK();
+        k_apply<<<grid_ew(npix, C), kT, 0, c.stream>>>(out, x, mu, istd, gamma, beta, npix, C, round_tf32);
+        KERNEL_CHECK();
+        return;
+    }
     const int nb = reduce_blocks(npix);
     const long ppb = (npix + nb - 1) / nb;
     double* part;

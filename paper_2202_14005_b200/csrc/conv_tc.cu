@@ -256,7 +256,7 @@ struct TtSmem {
 template<int CIN2>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_conv_tc_t(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
-                float* __restrict__ out, int X, int Y, int B, int dbg)
+                float* __restrict__ out, int X, int Y, int B, int dbg, double* __restrict__ stats)
 {
     static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
     constexpr int N = 128, NP = TT_X * TT_Y, NCH = CIN2 / 32;
@@ -358,6 +358,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     } else {
         // ---------------- epilogue: TMEM lane = channel, column = pixel ----------------
         const int lg = warp & 3, n = lg * 32 + lane;
+        // per-channel sum and sum of squares of the stored values (fp32 over
+        // 32 pixels, then double), for a batch-norm consumer
+        double s_acc = 0, q_acc = 0;
         uint32_t ti = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
             const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
@@ -375,15 +378,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 tmem_ld32(acc + jc * 32, v);
                 tmem_ld_wait();
                 float* o = out + ((long(b) * Y + py0) * X + x0) * N + n;
+                float fs = 0.f, fq = 0.f;
 #pragma unroll
                 for (int j = 0; j < 32; j++) {
                     const int l = j >> 3, xo = j & 7;
-                    if ((full_x || x0 + xo < X) && py0 + l < Y && dbg != 1)
-                        o[(long(l) * X + xo) * N] = v[j];
+                    if ((full_x || x0 + xo < X) && py0 + l < Y) {
+                        if (dbg != 1)
+                            o[(long(l) * X + xo) * N] = v[j];
+                        fs += v[j];
+                        fq = fmaf(v[j], v[j], fq);
+                    }
                 }
+                s_acc += fs;
+                q_acc += fq;
             }
             tc_fence_before();
             mbar_arrive(&tmem_empty[ab]);
+        }
+        if (stats) {
+            stats[(size_t(blockIdx.x) * N + n) * 2] = s_acc;
+            stats[(size_t(blockIdx.x) * N + n) * 2 + 1] = q_acc;
         }
     }
     tc_fence_before();
@@ -835,8 +849,11 @@ bool g_tc_pair = true; // CTA-pair (cta_group::2) kernel for the fwd / bwd-data 
 int g_tc_form = 1;     // 1: transposed (channel-major accumulator) kernel where 2 Cout = 128
 
 template<int CIN2, int N>
-void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int B)
+void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int B, double* stats = nullptr,
+               int* stats_blocks = nullptr)
 {
+    if (stats_blocks)
+        *stats_blocks = 0;
     auto& c = ctx();
     CUtensorMap ta = make_act_map(act, CIN2, X, Y, B);
     CUtensorMap tw = make_w_map(wpk, 9 * CIN2, N);
@@ -865,8 +882,11 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
             }
         }
         const int nt = ((X + TT_X - 1) / TT_X) * ((Y + TT_Y - 1) / TT_Y) * B;
-        kt<<<std::min(nt, c.sm_count), NTHREADS, smem_t, c.stream>>>(tat, tw, out, X, Y, B, g_tc_dbg);
+        const int grid = std::min(nt, c.sm_count);
+        kt<<<grid, NTHREADS, smem_t, c.stream>>>(tat, tw, out, X, Y, B, g_tc_dbg, stats);
         KERNEL_CHECK();
+        if (stats && stats_blocks)
+            *stats_blocks = grid;
         return;
     }
     const int ntiles = ((X + TILE_X - 1) / TILE_X) * ((Y + TILE_Y - 1) / TILE_Y) * B;
@@ -1027,12 +1047,17 @@ void conv_tc_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvGeo
         const double flops = 8.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * 9;
         ProfScope prof(mode == 0 ? "conv_tc_fwd" : "conv_tc_bwd_data", flops);
         const int X = int(g.X), Y = int(g.Y), B = int(g.B);
+        // epilogue channel statistics for a batch-norm consumer (forward, CHLAST output)
+        double* st = (mode == 0 && out_chl) ? g.stats : nullptr;
+        int* stb = st ? g.stats_blocks : nullptr;
+        if (g.stats_blocks)
+            *g.stats_blocks = 0;
         if (nin == 64 && nout == 64)
-            launch_tc<128, 128>(act, wpk, res, X, Y, B);
+            launch_tc<128, 128>(act, wpk, res, X, Y, B, st, stb);
         else if (nin == 64 && nout == 32)
             launch_tc<128, 64>(act, wpk, res, X, Y, B);
         else if (nin == 32 && nout == 64)
-            launch_tc<64, 128>(act, wpk, res, X, Y, B);
+            launch_tc<64, 128>(act, wpk, res, X, Y, B, st, stb);
         else
             launch_tc<64, 64>(act, wpk, res, X, Y, B);
     }

@@ -114,6 +114,12 @@ struct DArray {
     // values are already rounded RN to TF32 (set by producers that feed a
     // tensor-core convolution; lets the consumer skip its operand conversion)
     bool tf32 = false;
+    // optional per-channel partial sums of these values written by the
+    // producer kernel (tcgen05 conv epilogue): chstats_blocks blocks x
+    // 2C real channels (re | im) x {sum, sum of squares}, doubles; lets a
+    // batch-norm consumer skip its statistics pass
+    std::shared_ptr<DArray> chstats;
+    int chstats_blocks = 0;
 
     DArray() = default;
     explicit DArray(Dims d, bool zero = true, Layout l = Layout::CANON);

@@ -113,6 +113,10 @@ struct ConvGeom {
     // (y / dy): false = CANON, true = CHLAST; *_tf32: operand already RN-rounded
     bool in_chlast = false, out_chlast = false;
     bool in_tf32 = false, out_tf32 = false;
+    // forward only: per-channel partial sums of y from the conv epilogue when
+    // the kernel form provides them (*stats_blocks = blocks written, else 0)
+    double* stats = nullptr;
+    int* stats_blocks = nullptr;
 };
 // y[p,f] = sum_{t,c} x[p+t-c0, c] w[t,c,f]
 void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g);
@@ -170,7 +174,8 @@ void launch_real_to_complex(cfloat* out, const float* in, long n);
 // device scratch kept by the node for the backward pass
 void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, float2* var_out, const float* x,
                      const float2* mean_in, const float2* var_in, const float2* gamma, const float2* beta, long npix,
-                     int C, float eps, float mom, bool round_tf32);
+                     int C, float eps, float mom, bool round_tf32, const double* pre_part = nullptr,
+                     int pre_blocks = 0);
 void bnblock_backward(float* dx, float2* dgamma, float2* dbeta, const float* gout, const float* x, const float2* mu,
                       const float* istd, const float2* gamma, const float2* beta, long npix, int C, bool round_tf32);
 

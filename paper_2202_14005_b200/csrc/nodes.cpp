@@ -1296,7 +1296,20 @@ private:
         DArray y(od, false, act_layout(false));
         ConvGeom g = g_;
         g.in_tf32 = x.tf32;
+        // channel statistics from the tensor-core epilogue (consumed by a BnBlockNode)
+        const long ny = 2 * g_.Cout;
+        DArray st;
+        int st_blocks = 0;
+        if (y.layout == Layout::CHLAST && ny == 128) {
+            st = DArray(Dims{long(ctx().sm_count) * ny * 2}, false);
+            g.stats = reinterpret_cast<double*>(st.data());
+            g.stats_blocks = &st_blocks;
+        }
         conv_fwd(y.data(), x.data(), w.data(), g);
+        if (st_blocks > 0) {
+            y.chstats = std::make_shared<DArray>(st);
+            y.chstats_blocks = st_blocks;
+        }
         return y;
     }
     DArray bwd_data(const DArray& dy0, const DArray& w) const
@@ -1364,8 +1377,11 @@ public:
         const Dims& sd = ins_[1];
         DArray y(ins_[0], false, Layout::CHLAST), mo(sd, false), vo(sd, false);
         DArray mu(sd, false), istd(Dims{C_}, false);
+        const bool pre = in[0].chstats && in[0].chstats_blocks > 0;
         bnblock_forward(y.fdata(), mu.data(), istd.fdata(), mo.data(), vo.data(), in[0].fdata(), in[1].data(),
-                        in[2].data(), in[3].data(), in[4].data(), npix_, int(C_), eps_, mom_, round_out_);
+                        in[2].data(), in[3].data(), in[4].data(), npix_, int(C_), eps_, mom_, round_out_,
+                        pre ? reinterpret_cast<const double*>(in[0].chstats->data()) : nullptr,
+                        pre ? in[0].chstats_blocks : 0);
         y.tf32 = round_out_;
         out[0] = mo;
         out[1] = vo;
