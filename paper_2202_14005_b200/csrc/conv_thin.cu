@@ -64,8 +64,11 @@ __device__ __forceinline__ void load_halo(float2* tile, const float2* __restrict
     }
 }
 
-// thin -> wide.  Block = TX x TY pixel tile of one item.
-template<int K>
+// thin -> wide.  Block = TX x TY pixel tile of one item.  P output channels
+// per thread (P = 2 when F is even: the window loads and the loop overhead are
+// shared by two channels and the stores are 8-byte channel pairs -- the P = 1
+// form was issue-bound with the FMA pipe half busy).
+template<int K, int P>
 __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, const float2* __restrict__ in,
                                                     const float2* __restrict__ U, int X, int Y, int F, int ox, int oy)
 {
@@ -75,11 +78,14 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
     const long XY = long(X) * Y;
     load_halo<HX, HY>(tile, in, X, Y, b, x0, y0, ox, oy);
-    const int f = threadIdx.x % F, lane = threadIdx.x / F, lanes = NT / F;
-    float2 u[K * K];
+    const int FP = F / P;
+    const int f = (threadIdx.x % FP) * P, lane = threadIdx.x / FP, lanes = NT / FP;
+    float2 u[P][K * K];
 #pragma unroll
-    for (int t = 0; t < K * K; t++)
-        u[t] = U[t * F + f];
+    for (int q = 0; q < P; q++)
+#pragma unroll
+        for (int t = 0; t < K * K; t++)
+            u[q][t] = U[t * F + f + q];
     __syncthreads();
     const int nseg = max(1, lanes / TY), seglen = TX / nseg;
     for (int it = lane; it < TY * nseg; it += lanes) {
@@ -101,24 +107,32 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
 #pragma unroll
             for (int ky = 0; ky < K; ky++)
                 win[ky][K - 1] = tile[(row + ky) * HX + px + K - 1];
-            // two accumulator pairs (even / odd taps): 4 FFMA per complex MAC, short chains
-            float2 acc{0.f, 0.f}, acc2{0.f, 0.f};
+            float2 acc[P];
 #pragma unroll
-            for (int ky = 0; ky < K; ky++)
+            for (int q = 0; q < P; q++) {
+                // two accumulator pairs (even / odd taps): 4 FFMA per complex MAC, short chains
+                float2 a0{0.f, 0.f}, a1{0.f, 0.f};
 #pragma unroll
-                for (int kx = 0; kx < K; kx++) {
-                    const float2 w_ = win[ky][kx], uu = u[kx + K * ky];
-                    float2& a_ = ((kx + K * ky) & 1) ? acc2 : acc;
-                    a_.x = fmaf(w_.x, uu.x, a_.x);
-                    a_.y = fmaf(w_.x, uu.y, a_.y);
-                    a_.x = fmaf(-w_.y, uu.y, a_.x);
-                    a_.y = fmaf(w_.y, uu.x, a_.y);
-                }
-            acc.x += acc2.x;
-            acc.y += acc2.y;
+                for (int ky = 0; ky < K; ky++)
+#pragma unroll
+                    for (int kx = 0; kx < K; kx++) {
+                        const float2 w_ = win[ky][kx], uu = u[q][kx + K * ky];
+                        float2& a_ = ((kx + K * ky) & 1) ? a1 : a0;
+                        a_.x = fmaf(w_.x, uu.x, a_.x);
+                        a_.y = fmaf(w_.x, uu.y, a_.y);
+                        a_.x = fmaf(-w_.y, uu.y, a_.x);
+                        a_.y = fmaf(w_.y, uu.x, a_.y);
+                    }
+                acc[q] = float2{a0.x + a1.x, a0.y + a1.y};
+            }
             if (x0 + px < X) {
-                op[0] = acc.x;
-                op[F] = acc.y;
+                if constexpr (P == 2) {
+                    *reinterpret_cast<float2*>(op) = float2{acc[0].x, acc[1].x};
+                    *reinterpret_cast<float2*>(op + F) = float2{acc[0].y, acc[1].y};
+                } else {
+                    op[0] = acc[0].x;
+                    op[F] = acc[0].y;
+                }
             }
 #pragma unroll
             for (int ky = 0; ky < K; ky++)
@@ -427,8 +441,12 @@ void run_thin(cfloat* outp, const cfloat* inp, const float2* U, const ConvGeom& 
     auto& c = ctx();
     if (expand) {
         dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + 7) / 8), unsigned(g.B));
-        k_thin_expand<K><<<grid, NT, 0, c.stream>>>(reinterpret_cast<float*>(outp), inp, U, int(g.X), int(g.Y), F,
-                                                    ox, oy);
+        if (F % 2 == 0 && NT % (F / 2) == 0)
+            k_thin_expand<K, 2><<<grid, NT, 0, c.stream>>>(reinterpret_cast<float*>(outp), inp, U, int(g.X),
+                                                           int(g.Y), F, ox, oy);
+        else
+            k_thin_expand<K, 1><<<grid, NT, 0, c.stream>>>(reinterpret_cast<float*>(outp), inp, U, int(g.X),
+                                                           int(g.Y), F, ox, oy);
     } else {
         using Cfg = ReduceCfg<K>;
         auto kern = k_thin_reduce<K>;
