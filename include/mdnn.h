@@ -233,6 +233,12 @@ void mdnn_train_cfg_default(mdnn_train_cfg* c);
 mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg* cfg, uint64_t seed);
 void mdnn_trainer_free(mdnn_trainer* t);
 int mdnn_trainer_set_data(mdnn_trainer* t, const char* name, const mdnn_array* a);
+/* input prefetch (the reconet loader's next-batch staging): queue a dense
+   host batch for data arg `name`; the copy runs asynchronously on a copy
+   stream and the next forward pass takes the oldest queued batch of each
+   name.  The host buffer (pinned for true overlap) must stay valid until that
+   forward pass has been issued.  The CPU shim copies synchronously. */
+int mdnn_trainer_stage_data(mdnn_trainer* t, const char* name, const mdnn_array* a);
 int mdnn_trainer_set_weight(mdnn_trainer* t, const char* name, const mdnn_array* a);
 int mdnn_trainer_get_weight(mdnn_trainer* t, const char* name, mdnn_array* out);
 int mdnn_trainer_get_grad(mdnn_trainer* t, const char* name, mdnn_array* out);

@@ -22,6 +22,7 @@
 #include <mdnn/cfl.hpp>
 
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <string>
 
@@ -387,6 +388,7 @@ struct mdnn_trainer {
     TrainConfig cfg;
     std::map<std::string, A> weights;
     std::map<std::string, A> batch;
+    std::map<std::string, std::deque<A>> staged; // mdnn_trainer_stage_data queue (copied synchronously)
     std::map<std::string, A> grads;
     std::vector<AdamState<R>> adam;
     std::vector<IpalmState<R>> ipalm;
@@ -395,6 +397,17 @@ struct mdnn_trainer {
     std::vector<A> last_outs;
     std::vector<float> flat;
 };
+
+// the oldest staged batch of every name becomes the current batch (shim of
+// the product's prefetch queue; the reference itself has no staging)
+static void take_staged(mdnn_trainer* t)
+{
+    for (auto& [name, q] : t->staged)
+        if (!q.empty()) {
+            t->batch[name] = q.front();
+            q.pop_front();
+        }
+}
 
 extern "C" {
 
@@ -861,6 +874,10 @@ int mdnn_trainer_set_data(mdnn_trainer* t, const char* name, const mdnn_array* a
 {
     return guard([&] { t->batch[name] = from_c(*a); });
 }
+int mdnn_trainer_stage_data(mdnn_trainer* t, const char* name, const mdnn_array* a)
+{
+    return guard([&] { t->staged[name].push_back(from_c(*a)); });
+}
 int mdnn_trainer_set_weight(mdnn_trainer* t, const char* name, const mdnn_array* a)
 {
     return guard([&] {
@@ -884,6 +901,7 @@ int mdnn_trainer_forward_backward(mdnn_trainer* t, double* loss)
     return guard([&] {
         auto& J = t->joint;
         const int loss_idx = J.output_index("loss");
+        take_staged(t);
         t->last_outs = J.op.apply(J.gather_inputs(t->weights, t->batch));
         double lv = t->last_outs[loss_idx].data()[0].real();
         if (!std::isfinite(lv))
@@ -945,6 +963,7 @@ int mdnn_trainer_step(mdnn_trainer* t, double* loss)
 {
     // the reference's own run_step (optim.hpp:314)
     return guard([&] {
+        take_staged(t);
         double lv = run_step(t->joint, t->weights, t->batch, t->cfg, t->adam, t->ipalm);
         if (loss)
             *loss = lv;

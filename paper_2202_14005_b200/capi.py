@@ -165,6 +165,7 @@ _SIGS = {
     "mdnn_trainer_create": (P, [P, C.POINTER(mdnn_train_cfg), C.c_uint64]),
     "mdnn_trainer_free": (None, [P]),
     "mdnn_trainer_set_data": (C.c_int, [P, C.c_char_p, C.POINTER(mdnn_array)]),
+    "mdnn_trainer_stage_data": (C.c_int, [P, C.c_char_p, C.POINTER(mdnn_array)]),
     "mdnn_trainer_set_weight": (C.c_int, [P, C.c_char_p, C.POINTER(mdnn_array)]),
     "mdnn_trainer_get_weight": (C.c_int, [P, C.c_char_p, C.POINTER(mdnn_array)]),
     "mdnn_trainer_get_grad": (C.c_int, [P, C.c_char_p, C.POINTER(mdnn_array)]),

@@ -684,6 +684,10 @@ int mdnn_trainer_set_data(mdnn_trainer* t, const char* name, const mdnn_array* a
 {
     return guard([&] { t->t->set_data(name, in_arr(*a)); });
 }
+int mdnn_trainer_stage_data(mdnn_trainer* t, const char* name, const mdnn_array* a)
+{
+    return guard([&] { t->t->stage_data(name, hv(*a)); });
+}
 int mdnn_trainer_set_weight(mdnn_trainer* t, const char* name, const mdnn_array* a)
 {
     return guard([&] { t->t->set_weight(name, in_arr(*a)); });

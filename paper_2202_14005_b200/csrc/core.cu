@@ -78,6 +78,7 @@ Context* make_ctx(int dev)
     c->device = dev;
     CUDA_CHECK(cudaSetDevice(dev));
     CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     cudaDeviceProp prop;
     CUDA_CHECK(cudaGetDeviceProperties(&prop, dev));
     c->sm_count = prop.multiProcessorCount;
@@ -283,6 +284,25 @@ DArray import_array(const HostView& v)
     }
     CUDA_CHECK(cudaMemcpyAsync(a.buf->ptr, tmp.data(), bytes, cudaMemcpyHostToDevice, c.stream));
     CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    return a;
+}
+
+DArray import_array_async(const HostView& v, cudaEvent_t done)
+{
+    if (v.device >= 0 || !is_default(v.dims, v.strides))
+        throw ConfigError("stage_data: a dense host array is required");
+    check_rank(v.dims);
+    auto& c = ctx();
+    DArray a;
+    a.dims = v.dims;
+    a.buf = std::make_shared<Buffer>();
+    a.buf->bytes = size_t(md_size(v.dims)) * sizeof(cfloat);
+    a.buf->device = c.device;
+    // allocated in the copy stream's order; freed later on the compute stream,
+    // which only touches it after waiting on `done`
+    CUDA_CHECK(cudaMallocAsync(&a.buf->ptr, a.buf->bytes, c.copy_stream));
+    CUDA_CHECK(cudaMemcpyAsync(a.buf->ptr, v.data, a.buf->bytes, cudaMemcpyHostToDevice, c.copy_stream));
+    CUDA_CHECK(cudaEventRecord(done, c.copy_stream));
     return a;
 }
 

@@ -70,6 +70,7 @@ using cfloat = float2; // interleaved complex64 on the device
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr; // host->device input staging (overlaps the compute stream)
     int sm_count = 148;
     size_t smem_optin = 227 * 1024;
     size_t pool_reserved = 0; // bytes mapped into the stream-ordered pool up front
@@ -146,6 +147,11 @@ struct HostView {
     Dims strides; // element strides
 };
 DArray import_array(const HostView& v);
+// asynchronous host->device copy on the context's copy stream into a fresh
+// array; `done` is recorded on the copy stream after the copy (the caller
+// makes the compute stream wait on it and keeps the host buffer alive until
+// then).  Dense (default-stride) host views only.
+DArray import_array_async(const HostView& v, cudaEvent_t done);
 void export_array(const DArray& a, const HostView& v);
 std::vector<std::complex<float>> to_host(const DArray& a);
 DArray from_host(const Dims& d, const std::complex<float>* v);

@@ -60,6 +60,39 @@ void Trainer::set_data(const std::string& name, DArray a)
     data_[name] = std::move(a);
 }
 
+void Trainer::stage_data(const std::string& name, const HostView& v)
+{
+    int i = joint_.arg_index(name);
+    if (joint_.args[i].kind != ArgKind::Data)
+        throw ConfigError("trainer: '" + name + "' is not a data argument");
+    if (v.dims != joint_.op.in_dims(i))
+        throw ShapeError("trainer: data '" + name + "' expected " + dims_to_string(joint_.op.in_dims(i)) + ", got "
+                         + dims_to_string(v.dims));
+    cudaEvent_t ev;
+    CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    staged_[name].push_back(Staged{import_array_async(v, ev), ev});
+}
+
+int Trainer::staged(const std::string& name) const
+{
+    auto it = staged_.find(name);
+    return it == staged_.end() ? 0 : int(it->second.size());
+}
+
+void Trainer::take_staged()
+{
+    auto& c = ctx();
+    for (auto& [name, q] : staged_) {
+        if (q.empty())
+            continue;
+        Staged s = std::move(q.front());
+        q.pop_front();
+        CUDA_CHECK(cudaStreamWaitEvent(c.stream, s.ev, 0));
+        CUDA_CHECK(cudaEventDestroy(s.ev));
+        data_[name] = std::move(s.a);
+    }
+}
+
 void Trainer::set_weight(const std::string& name, DArray a)
 {
     auto it = weights_.find(name);
@@ -107,6 +140,7 @@ double Trainer::forward_backward()
 {
     static const bool trace = std::getenv("MDNN_TRACE_HOST") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
+    take_staged();
     last_outs_ = joint_.op.apply(gather_inputs());
     std::vector<char> want(joint_.args.size(), 0);
     for (int i : wargs_)
@@ -210,6 +244,7 @@ double Trainer::ipalm_step()
         ipalm_prev_.resize(nb);
     const float lr = float(cfg_.lr), al = float(cfg_.ipalm_alpha), be = float(cfg_.ipalm_beta);
     // cur: the iterate the gradient oracle sees (blocks < j updated, j at z, > j old)
+    take_staged();
     std::vector<DArray> in = gather_inputs();
     double loss = 0;
     for (int j = 0; j < nb; j++) {

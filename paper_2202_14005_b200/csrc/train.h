@@ -6,6 +6,8 @@
 
 #include "model.h"
 
+#include <deque>
+
 namespace mdnn {
 
 // OptAlgo (optim.hpp:10) and the TrainConfig fields the step uses (optim.hpp:20-56)
@@ -21,6 +23,11 @@ public:
     Trainer(const Model& model, const TrainConfig& cfg, uint64_t seed);
 
     void set_data(const std::string& name, DArray a);
+    // prefetch: queue a host batch for `name`, copied asynchronously on the
+    // copy stream; each forward pass takes the oldest queued batch of every
+    // name (the host buffer must stay valid until that pass has been issued)
+    void stage_data(const std::string& name, const HostView& v);
+    int staged(const std::string& name) const;
     void set_weight(const std::string& name, DArray a);
     const DArray& weight(const std::string& name) const;
     DArray grad(const std::string& name) const;
@@ -47,6 +54,12 @@ public:
 
 private:
     std::vector<DArray> gather_inputs() const;
+    void take_staged(); // commit the oldest staged batch of every name (stream wait, no host sync)
+    struct Staged {
+        DArray a;
+        cudaEvent_t ev;
+    };
+    std::map<std::string, std::deque<Staged>> staged_;
 
     Model joint_;
     TrainConfig cfg_;

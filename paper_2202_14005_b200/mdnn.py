@@ -315,6 +315,15 @@ class Trainer:
         self._keep = a
         self.lib.check(self.lib.so.mdnn_trainer_set_data(self.h, name.encode(), C.byref(self.lib.arr(a))))
 
+    def stage_data(self, name, a):
+        """Queue a host batch for data argument `name` (asynchronous copy on the
+        library's copy stream; the next forward pass takes the oldest queued
+        batch).  `a` is kept alive until two further batches were queued."""
+        if isinstance(a, np.ndarray):
+            a = np.asfortranarray(a.astype(np.complex64))
+        self._staged = (getattr(self, "_staged", []) + [a])[-3 * 8:]
+        self.lib.check(self.lib.so.mdnn_trainer_stage_data(self.h, name.encode(), C.byref(self.lib.arr(a))))
+
     def set_weight(self, name, a):
         a = np.asfortranarray(np.asarray(a, dtype=np.complex64))
         self.lib.check(self.lib.so.mdnn_trainer_set_weight(self.h, name.encode(), C.byref(self.lib.arr(a))))

@@ -38,3 +38,33 @@ def test_reference_optimizers_step(ref, algo):
         with pytest.raises(MdnnError) as e:
             ref.check(ref.so.mdnn_trainer_update(t.h, 1.0))
         assert e.value.code == 4
+
+
+def test_stage_data_queue_order(ref):
+    """mdnn_trainer_stage_data on the shim: queued batches are consumed one per
+    step, oldest first, and match feeding the same batches with set_data."""
+    import ctypes as C
+    from util import kspace_dims
+    X, Y, NC = 8, 8, 2
+    ph, cm, pat = sim_data(ref, X, Y, NC, 1)
+    ks = np.zeros(kspace_dims(X, Y, NC), dtype=np.complex64, order="F")
+    ref.check(ref.so.mdnn_sense_forward(C.byref(ref.arr(cm)), C.byref(ref.arr(pat)), C.byref(ref.arr(ph)),
+                                        C.byref(ref.arr(ks))))
+    batches = [dict(kspace=ks, coils=cm, pattern=pat, reference=np.asfortranarray(ph * s)) for s in (1.0, 0.5)]
+    losses = []
+    for staged in (False, True):
+        m = Model.varnet(ref, iterations=1, filters=2, kernel=3, rbf=5, im_x=X, im_y=Y, coils=NC)
+        t = Trainer(ref, m, seed=1, lr=1e-2)
+        ls = []
+        if staged:
+            for b in batches:
+                for k, v in b.items():
+                    t.stage_data(k, v)
+            ls = [t.step(), t.step()]
+        else:
+            for b in batches:
+                for k, v in b.items():
+                    t.set_data(k, v)
+                ls.append(t.step())
+        losses.append(ls)
+    assert losses[0] == losses[1] and losses[0][0] != losses[0][1]

@@ -148,3 +148,35 @@ def test_optimizer_trajectories_match_reference(gpu, ref, net, algo):
     for name in trainers[1].weight_names():
         wg, wr = trainers[0].get_weight(name), trainers[1].get_weight(name)
         assert rel_l2(wg, wr) <= 1e-3, name
+
+
+@pytest.mark.parametrize("algo", ["adam", "ipalm"])
+def test_staged_batches_match_reference(gpu, ref, algo):
+    """Prefetch queue (mdnn_trainer_stage_data): three different batches queued
+    ahead of the steps, one taken per step, against the reference fed the same
+    batches in order (the shim's synchronous queue)."""
+    from paper_2202_14005_b200.capi import ALGO_ADAM, ALGO_IPALM
+    X, Y, NC, B = 16, 12, 3, 2
+    cfg = dict(iterations=2, layers=3, filters=4, cg_iter=5, im_x=X, im_y=Y, coils=NC, batch=B)
+    mref = Model.modl(ref, **cfg)
+    batches = []
+    for s in range(3):
+        data, _ = _inputs(ref, mref, X, Y, NC, B)
+        rng = np.random.default_rng(s)
+        data["reference"] = np.asfortranarray(data["reference"] * (1 + 0.1 * s)
+                                              + 0.01 * crand(rng, data["reference"].shape))
+        batches.append(data)
+    code = {"adam": ALGO_ADAM, "ipalm": ALGO_IPALM}[algo]
+    losses = []
+    for lib in (gpu, ref):
+        t = Trainer(lib, Model.modl(lib, **cfg), seed=42, lr=1e-3, algo=code)
+        for d in batches[:2]:
+            for k, v in d.items():
+                t.stage_data(k, v)
+        ls = [t.step()]
+        for k, v in batches[2].items():
+            t.stage_data(k, v)
+        ls += [t.step(), t.step()]
+        losses.append(ls)
+    np.testing.assert_allclose(losses[0], losses[1], rtol=1e-4)
+    assert len(set(np.round(losses[1], 12))) == 3  # three distinct batches were consumed
