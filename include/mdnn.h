@@ -73,7 +73,9 @@ int mdnn_synchronize(void);
    "conv_tc_form" (1 = channel-major transposed tcgen05 kernel for 64-channel
    outputs, 0 = pixel-major), "conv_tc_pair" (1 = CTA-pair cta_group::2
    pixel-major kernel), "conv_tc_debug" (diagnostics: 1 = no epilogue stores,
-   2 = no epilogue; results invalid), "sense_rank" / "sense_rank_ctas" /
+   2 = no epilogue; results invalid), "conv_bn_fuse" (1 = batch-norm
+   statistics / backward reductions folded into the tensor-core conv
+   epilogues), "sense_rank" / "sense_rank_ctas" /
    "sense_rank_tm" (A^H A kernel selection) */
 int mdnn_set_option(const char* key, long value);
 /* the library's CUDA stream on the current device (cudaStream_t), so callers

@@ -321,6 +321,33 @@ __global__ void __launch_bounds__(kT) k_bwd_final(float2* __restrict__ dbeta, fl
     fh[c] = float(-re2 * double(istd[c]) / double(m));
 }
 
+// final backward from producer partials (conv bwd-data epilogue):
+// part[blk][2C real channels][3] = (sum gz_comp, Re S2 contribution, Im S2 contribution)
+__global__ void __launch_bounds__(kT) k_bwd_final_pre(float2* __restrict__ dbeta, float2* __restrict__ dgamma,
+                                                      float2* __restrict__ gm, float* __restrict__ fh,
+                                                      const double* __restrict__ part, int nblocks, int C, long m,
+                                                      const float2* __restrict__ gamma,
+                                                      const float* __restrict__ istd)
+{
+    const int c = blockIdx.x;
+    double re[3], im[3];
+    sum_partials<3>(re, part, nblocks, 2 * C, c);
+    __syncthreads(); // sum_partials' shared scratch is reused
+    sum_partials<3>(im, part, nblocks, 2 * C, C + c);
+    if (threadIdx.x != 0)
+        return;
+    const double r[4] = {re[0], im[0], re[1] + im[1], re[2] + im[2]};
+    if (dbeta)
+        dbeta[c] = float2{float(r[0]), float(r[1])};
+    if (dgamma)
+        dgamma[c] = float2{float(r[2]), float(r[3])};
+    const double gr = gamma[c].x, gi = gamma[c].y;
+    const double c1r = gr * r[0] + gi * r[1], c1i = gr * r[1] - gi * r[0];
+    gm[c] = float2{float(c1r / double(m)), float(c1i / double(m))};
+    const double re2 = gr * r[2] + gi * r[3];
+    fh[c] = float(-re2 * double(istd[c]) / double(m));
+}
+
 // pass 2 backward: dx = (gz conj(g) - gm) istd + yhat * fh
 __global__ void __launch_bounds__(kT) k_bwd_apply(float* __restrict__ dx, const float* __restrict__ gout,
                                                   const float* __restrict__ x, const float2* __restrict__ mu,
@@ -418,28 +445,39 @@ void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, floa
 }
 
 void bnblock_backward(float* dx, float2* dgamma, float2* dbeta, const float* gout, const float* x, const float2* mu,
-                      const float* istd, const float2* gamma, const float2* beta, long npix, int C, bool round_tf32)
+                      const float* istd, const float2* gamma, const float2* beta, long npix, int C, bool round_tf32,
+                      const double* pre_part, int pre_blocks)
 {
     auto& c = ctx();
+    const bool pre = pre_part && pre_blocks > 0;
     const int nb = reduce_blocks(npix);
     const long ppb = (npix + nb - 1) / nb;
-    double* part;
+    double* part = nullptr;
     float2* gm;
     float* fh;
-    CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * 4 * C * nb, c.stream));
+    if (!pre)
+        CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * 4 * C * nb, c.stream));
     CUDA_CHECK(cudaMallocAsync(&gm, sizeof(float2) * C, c.stream));
     CUDA_CHECK(cudaMallocAsync(&fh, sizeof(float) * C, c.stream));
-    ProfScope prof("bnblock_bwd", 8.0 * 5 * npix * C);
-    k_bwd_reduce<<<nb, kT, sizeof(double) * 2 * 4 * kT, c.stream>>>(part, gout, x, mu, istd, gamma, beta, npix, C, ppb);
-    KERNEL_CHECK();
-    k_bwd_final<<<C, kT, 0, c.stream>>>(dbeta, dgamma, gm, fh, part, nb, C, npix, gamma, istd);
-    KERNEL_CHECK();
+    // algorithmic bytes: reduction pass (x, gout) unless folded into the producer, apply pass (x, gout, dx)
+    ProfScope prof("bnblock_bwd", 8.0 * (pre ? 3 : 5) * npix * C);
+    if (pre) {
+        k_bwd_final_pre<<<C, kT, 0, c.stream>>>(dbeta, dgamma, gm, fh, pre_part, pre_blocks, C, npix, gamma, istd);
+        KERNEL_CHECK();
+    } else {
+        k_bwd_reduce<<<nb, kT, sizeof(double) * 2 * 4 * kT, c.stream>>>(part, gout, x, mu, istd, gamma, beta, npix, C,
+                                                                      ppb);
+        KERNEL_CHECK();
+        k_bwd_final<<<C, kT, 0, c.stream>>>(dbeta, dgamma, gm, fh, part, nb, C, npix, gamma, istd);
+        KERNEL_CHECK();
+    }
     if (dx) {
         k_bwd_apply<<<grid_ew(npix, C), kT, 0, c.stream>>>(dx, gout, x, mu, istd, gamma, beta, gm, fh, npix, C,
                                                             round_tf32);
         KERNEL_CHECK();
     }
-    CUDA_CHECK(cudaFreeAsync(part, c.stream));
+    if (part)
+        CUDA_CHECK(cudaFreeAsync(part, c.stream));
     CUDA_CHECK(cudaFreeAsync(gm, c.stream));
     CUDA_CHECK(cudaFreeAsync(fh, c.stream));
 }

@@ -244,6 +244,8 @@ constexpr int TT_P = 16;                       // halo pitch (>= TT_X + 2, multi
 constexpr int TT_L = TT_Y + 2;                 // halo lines
 constexpr int TT_HALO = TT_L * TT_P * 128;     // 68 KB per 32-float chunk
 constexpr int TT_WST = 4;                      // weight stages (16 KB each)
+constexpr int TT_EPI_WARPS = 16;               // epilogue warps (4 per TMEM lane quarter)
+constexpr int TT_THREADS = 64 + 32 * TT_EPI_WARPS;
 
 struct TtSmem {
     static constexpr int W_BYTES = 128 * 128;
@@ -253,10 +255,23 @@ struct TtSmem {
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
+// batch-norm backward reduction folded into the bwd-data epilogue: the
+// produced cotangent is the BN block's output cotangent g; per real channel
+// lane (Re or Im part of complex channel c) accumulate the CReLU-masked g and
+// its contributions to S2 = sum gz conj(yhat) (bnblock.cu k_bwd_reduce).
+struct BnEpi {
+    const float* x = nullptr; // BN input (CHLAST, 2 C = 128 floats per pixel)
+    const float2* mu = nullptr;
+    const float* istd = nullptr;
+    const float2* gamma = nullptr;
+    const float2* beta = nullptr;
+    double* part = nullptr; // [blk][128][3]
+};
+
 template<int CIN2>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(TT_THREADS, 1)
     k_conv_tc_t(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
-                float* __restrict__ out, int X, int Y, int B, int dbg, double* __restrict__ stats)
+                float* __restrict__ out, int X, int Y, int B, int dbg, double* __restrict__ stats, const BnEpi be)
 {
     static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
     constexpr int N = 128, NP = TT_X * TT_Y, NCH = CIN2 / 32;
@@ -285,7 +300,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mbar_init(&halo_full[i], 1);
             mbar_init(&halo_empty[i], 1);
             mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 128);
+            mbar_init(&tmem_empty[i], 32 * TT_EPI_WARPS);
         }
         for (int i = 0; i < TT_WST; i++) {
             mbar_init(&w_full[i], 1);
@@ -357,10 +372,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else {
         // ---------------- epilogue: TMEM lane = channel, column = pixel ----------------
-        const int lg = warp & 3, n = lg * 32 + lane;
+        // TT_EPI_WARPS epilogue warps: TT_EPI_WARPS / 4 per TMEM lane quarter, interleaved 32-column chunks
+        const int lg = warp & 3, n = lg * 32 + lane, half = (warp - 2) >> 2;
         // per-channel sum and sum of squares of the stored values (fp32 over
         // 32 pixels, then double), for a batch-norm consumer
         double s_acc = 0, q_acc = 0;
+        // batch-norm backward partials (be.part): channel c = n mod 64, component n / 64
+        const int bc = n & 63, comp = n >> 6;
+        float2 bmu{0.f, 0.f}, bg{0.f, 0.f}, bb{0.f, 0.f};
+        float bs = 0.f;
+        if (be.part) {
+            bmu = be.mu[bc];
+            bs = be.istd[bc];
+            bg = be.gamma[bc];
+            bb = be.beta[bc];
+        }
+        double r0 = 0, r1 = 0, r2 = 0;
         uint32_t ti = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
             const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
@@ -370,17 +397,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc_fence_after();
             const bool full_x = x0 + TT_X <= X;
 #pragma unroll 1
-            for (int jc = 0; jc < NP / 32 && dbg != 2; jc++) {
-                const int py0 = y0 + jc * 4; // 32 columns = 4 lines x 8 pixels
+            for (int jc = half; jc < NP / 16 && dbg != 2; jc += TT_EPI_WARPS / 4) {
+                const int py0 = y0 + jc * 2; // 16 columns = 2 lines x 8 pixels
                 if (py0 >= Y)
                     break;
-                float v[32];
-                tmem_ld32(acc + jc * 32, v);
+                float v[16];
+                tmem_ld16(acc + jc * 16, v);
                 tmem_ld_wait();
                 float* o = out + ((long(b) * Y + py0) * X + x0) * N + n;
                 float fs = 0.f, fq = 0.f;
 #pragma unroll
-                for (int j = 0; j < 32; j++) {
+                for (int j = 0; j < 16; j++) {
                     const int l = j >> 3, xo = j & 7;
                     if ((full_x || x0 + xo < X) && py0 + l < Y) {
                         if (dbg != 1)
@@ -391,13 +418,50 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 }
                 s_acc += fs;
                 q_acc += fq;
+                if (be.part) {
+                    const float* xp = be.x + ((long(b) * Y + py0) * X + x0) * N + bc;
+                    float xr[16], xi[16];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) { // 32 loads in flight
+                        const int l = j >> 3, xo = j & 7;
+                        const bool ok = (full_x || x0 + xo < X) && py0 + l < Y;
+                        const long off = (long(l) * X + xo) * N;
+                        xr[j] = ok ? __ldg(xp + off) : 0.f;
+                        xi[j] = ok ? __ldg(xp + off + 64) : 0.f;
+                    }
+                    float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        const int l = j >> 3, xo = j & 7;
+                        const bool ok = (full_x || x0 + xo < X) && py0 + l < Y;
+                        // yhat and z exactly as bn_z (bnblock.cu)
+                        const float hr = (xr[j] - bmu.x) * bs, hi = (xi[j] - bmu.y) * bs;
+                        const float zr = bg.x * hr - bg.y * hi + bb.x;
+                        const float zi = bg.x * hi + bg.y * hr + bb.y;
+                        const float ge = (ok && (comp ? zi : zr) > 0.f) ? v[j] : 0.f;
+                        f0 += ge;
+                        // Re lane: (g_r hr, -g_r hi); Im lane: (g_i hi, g_i hr)
+                        f1 = fmaf(ge, comp ? hi : hr, f1);
+                        f2 = fmaf(ge, comp ? hr : -hi, f2);
+                    }
+                    r0 += f0;
+                    r1 += f1;
+                    r2 += f2;
+                }
             }
             tc_fence_before();
             mbar_arrive(&tmem_empty[ab]);
         }
+        // one partial block per (CTA, epilogue half)
+        const size_t slot = size_t(blockIdx.x) * (TT_EPI_WARPS / 4) + half;
         if (stats) {
-            stats[(size_t(blockIdx.x) * N + n) * 2] = s_acc;
-            stats[(size_t(blockIdx.x) * N + n) * 2 + 1] = q_acc;
+            stats[(slot * N + n) * 2] = s_acc;
+            stats[(slot * N + n) * 2 + 1] = q_acc;
+        }
+        if (be.part) {
+            be.part[(slot * N + n) * 3] = r0;
+            be.part[(slot * N + n) * 3 + 1] = r1;
+            be.part[(slot * N + n) * 3 + 2] = r2;
         }
     }
     tc_fence_before();
@@ -850,10 +914,12 @@ int g_tc_form = 1;     // 1: transposed (channel-major accumulator) kernel where
 
 template<int CIN2, int N>
 void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int B, double* stats = nullptr,
-               int* stats_blocks = nullptr)
+               int* stats_blocks = nullptr, const BnEpi& be = BnEpi{}, int* be_blocks = nullptr)
 {
     if (stats_blocks)
         *stats_blocks = 0;
+    if (be_blocks)
+        *be_blocks = 0;
     auto& c = ctx();
     CUtensorMap ta = make_act_map(act, CIN2, X, Y, B);
     CUtensorMap tw = make_w_map(wpk, 9 * CIN2, N);
@@ -883,10 +949,12 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
         }
         const int nt = ((X + TT_X - 1) / TT_X) * ((Y + TT_Y - 1) / TT_Y) * B;
         const int grid = std::min(nt, c.sm_count);
-        kt<<<grid, NTHREADS, smem_t, c.stream>>>(tat, tw, out, X, Y, B, g_tc_dbg, stats);
+        kt<<<grid, TT_THREADS, smem_t, c.stream>>>(tat, tw, out, X, Y, B, g_tc_dbg, stats, be);
         KERNEL_CHECK();
         if (stats && stats_blocks)
-            *stats_blocks = grid;
+            *stats_blocks = grid * (TT_EPI_WARPS / 4);
+        if (be.part && be_blocks)
+            *be_blocks = grid * (TT_EPI_WARPS / 4);
         return;
     }
     const int ntiles = ((X + TILE_X - 1) / TILE_X) * ((Y + TILE_Y - 1) / TILE_Y) * B;
@@ -1006,6 +1074,12 @@ void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom
 
 void conv_tc_enable(bool on) { g_tc_enabled = on; }
 void conv_tc_debug(int mode) { g_tc_dbg = mode; }
+int conv_tc_stat_slots() { return TT_EPI_WARPS / 4; }
+namespace {
+bool g_bn_fuse = true;
+}
+void conv_bn_fuse_enable(bool on) { g_bn_fuse = on; }
+bool conv_bn_fuse() { return g_bn_fuse; }
 void conv_tc_pair_enable(bool on) { g_tc_pair = on; }
 void conv_tc_form(int f) { g_tc_form = f; }
 
@@ -1052,12 +1126,21 @@ void conv_tc_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvGeo
         int* stb = st ? g.stats_blocks : nullptr;
         if (g.stats_blocks)
             *g.stats_blocks = 0;
+        // batch-norm backward partials for the BN block consuming dx (bwd-data, CHLAST)
+        BnEpi be{};
+        int* beb = nullptr;
+        if (g.bnb_blocks)
+            *g.bnb_blocks = 0;
+        if (mode == 1 && out_chl && g.bnb && g.bnb_part && g.bnb->C == 64 && g.bnb->npix == inner * g.B) {
+            be = BnEpi{g.bnb->x, g.bnb->mu, g.bnb->istd, g.bnb->gamma, g.bnb->beta, g.bnb_part};
+            beb = g.bnb_blocks;
+        }
         if (nin == 64 && nout == 64)
-            launch_tc<128, 128>(act, wpk, res, X, Y, B, st, stb);
+            launch_tc<128, 128>(act, wpk, res, X, Y, B, st, stb, be, beb);
         else if (nin == 64 && nout == 32)
             launch_tc<128, 64>(act, wpk, res, X, Y, B);
         else if (nin == 32 && nout == 64)
-            launch_tc<64, 128>(act, wpk, res, X, Y, B, st, stb);
+            launch_tc<64, 128>(act, wpk, res, X, Y, B, st, stb, be, beb);
         else
             launch_tc<64, 64>(act, wpk, res, X, Y, B);
     }

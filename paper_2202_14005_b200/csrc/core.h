@@ -121,6 +121,16 @@ struct DArray {
     // batch-norm consumer skip its statistics pass
     std::shared_ptr<DArray> chstats;
     int chstats_blocks = 0;
+    // 1: forward statistics [blk][2C][sum, sum sq]; 2: batch-norm backward
+    // partials [blk][2C][3] for the consumer identified by chstats_tag
+    int chstats_kind = 0;
+    const void* chstats_tag = nullptr;
+    void drop_chstats()
+    {
+        chstats.reset();
+        chstats_blocks = chstats_kind = 0;
+        chstats_tag = nullptr;
+    }
 
     DArray() = default;
     explicit DArray(Dims d, bool zero = true, Layout l = Layout::CANON);

@@ -117,6 +117,11 @@ struct ConvGeom {
     // the kernel form provides them (*stats_blocks = blocks written, else 0)
     double* stats = nullptr;
     int* stats_blocks = nullptr;
+    // bwd-data only: batch-norm backward partial sums of the produced
+    // cotangent for the BN block that consumes it (*bnb_blocks = blocks, else 0)
+    const struct BnBwdHint* bnb = nullptr;
+    double* bnb_part = nullptr;
+    int* bnb_blocks = nullptr;
 };
 // y[p,f] = sum_{t,c} x[p+t-c0, c] w[t,c,f]
 void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g);
@@ -127,6 +132,11 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
 // tcgen05 TF32 implicit-GEMM path (conv_tc.cu) for 3x3 layers with 32/64 channels
 void conv_tc_enable(bool on);
 void conv_tc_debug(int mode);
+int conv_tc_stat_slots(); // epilogue partial-sum blocks per CTA (ConvGeom::stats / bnb_part sizing)
+// batch-norm work folded into the tensor-core conv epilogues (forward
+// statistics, backward reduction); option "conv_bn_fuse", default on
+void conv_bn_fuse_enable(bool on);
+bool conv_bn_fuse();
 void conv_tc_pair_enable(bool on);
 void conv_tc_form(int f);
 // persistent mask-pruned A^H A kernel (sense_rank.cuh); off = sense_fast.cuh path
@@ -170,6 +180,17 @@ void launch_stat_mul_u_f(cfloat* out, const cfloat* u, const cfloat* f, const Is
 void launch_real_to_complex(cfloat* out, const float* in, long n);
 
 // ---- fused BN + gamma + beta + CReLU on CHLAST activations (bnblock.cu) --------------
+// forward state of a BN block that a producer of its output cotangent needs to
+// fold the backward reduction (S1 = sum gz, S2 = sum gz conj(yhat)) into its epilogue
+struct BnBwdHint {
+    const float* x = nullptr; // BN input, CHLAST
+    const float2* mu = nullptr;
+    const float* istd = nullptr;
+    const float2* gamma = nullptr;
+    const float2* beta = nullptr;
+    long npix = 0;
+    int C = 0;
+};
 // x, out, dx, gout: CHLAST floats of npix pixels x C channels; mu/istd: per-channel
 // device scratch kept by the node for the backward pass
 void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, float2* var_out, const float* x,
@@ -177,7 +198,8 @@ void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, floa
                      int C, float eps, float mom, bool round_tf32, const double* pre_part = nullptr,
                      int pre_blocks = 0);
 void bnblock_backward(float* dx, float2* dgamma, float2* dbeta, const float* gout, const float* x, const float2* mu,
-                      const float* istd, const float2* gamma, const float2* beta, long npix, int C, bool round_tf32);
+                      const float* istd, const float2* gamma, const float2* beta, long npix, int C, bool round_tf32,
+                      const double* pre_part = nullptr, int pre_blocks = 0);
 
 // ---- RBF (rbf.cu, ops.hpp:1308-1427) -------------------------------------------------
 struct RbfGeom {

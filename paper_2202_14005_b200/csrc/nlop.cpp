@@ -29,6 +29,7 @@ DArray accumulate(DArray acc, const DArray& add)
     DArray b = add.layout == acc.layout ? add : to_layout(add, acc.layout);
     if (acc.buf.use_count() == 1) {
         launch_axpy(acc.data(), cfloat{1.f, 0.f}, b.data(), acc.size());
+        acc.drop_chstats(); // producer statistics no longer describe the values
         return acc;
     }
     DArray out(acc.dims, false, acc.layout);
@@ -174,6 +175,7 @@ std::vector<DArray> Nlop::adjoint_all(int o, const DArray& dy, const std::vector
 
     std::vector<DArray> contrib;
     std::vector<char> wk;
+    std::vector<const void*> hints;
     for (auto it = topo_.rbegin(); it != topo_.rend(); ++it) {
         int ni = *it;
         if (!needs[ni])
@@ -188,7 +190,16 @@ std::vector<DArray> Nlop::adjoint_all(int o, const DArray& dy, const std::vector
             if (!cot[ni][p].valid())
                 continue;
             DArray g = as_layout(std::move(cot[ni][p]), node.out_layout(p));
+            // producers' hints for the cotangents this node is about to emit
+            hints.assign(node.n_in(), nullptr);
+            for (int k = 0; k < node.n_in(); k++) {
+                auto s = in_srcs_[ni][k];
+                if (s.node >= 0)
+                    hints[k] = nodes_[s.node]->cotangent_hint(s.port);
+            }
+            node.set_input_hints(hints);
             node.adjoint_all(p, g, contrib, wk);
+            node.set_input_hints({});
             for (int k = 0; k < node.n_in(); k++) {
                 if (k >= int(contrib.size()) || !contrib[k].valid())
                     continue;

@@ -66,15 +66,29 @@ public:
 
     uint64_t generation() const { return gen_; }
 
+    // Producer-side hint for the cotangent of output o: state of this node
+    // that the kernel computing that cotangent may fold work for (the
+    // batch-norm block's backward reduction into the convolution that
+    // produces its output cotangent); nullptr = none.
+    virtual const void* cotangent_hint(int o) const
+    {
+        (void)o;
+        return nullptr;
+    }
+    // set by the engine around adjoint calls: the producers' hints per input
+    void set_input_hints(std::vector<const void*> h) { in_hints_ = std::move(h); }
+
 protected:
     void bump_generation() { ++gen_; }
     void require_forward() const;
+    const void* input_hint(int i) const { return size_t(i) < in_hints_.size() ? in_hints_[size_t(i)] : nullptr; }
 
     std::string name_;
     std::vector<Dims> ins_, outs_;
 
 private:
     uint64_t gen_ = 0;
+    std::vector<const void*> in_hints_;
 };
 
 using NodePtr = std::shared_ptr<Node>;

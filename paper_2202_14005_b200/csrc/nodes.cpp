@@ -1276,7 +1276,7 @@ public:
     {
         require_forward();
         if (!t_)
-            return i == 0 ? bwd_data(g, st_[1]) : bwd_weight(st_[0], g);
+            return i == 0 ? bwd_data(g, st_[1], static_cast<const BnBwdHint*>(input_hint(0))) : bwd_weight(st_[0], g);
         // transposed: wrt y -> conv(g, w); wrt w -> bwd_weight(xin = g, dy = y)
         return i == 1 ? fwd(g, st_[0]) : bwd_weight(g, st_[1]);
     }
@@ -1300,8 +1300,8 @@ private:
         const long ny = 2 * g_.Cout;
         DArray st;
         int st_blocks = 0;
-        if (y.layout == Layout::CHLAST && ny == 128) {
-            st = DArray(Dims{long(ctx().sm_count) * ny * 2}, false);
+        if (y.layout == Layout::CHLAST && ny == 128 && conv_bn_fuse()) {
+            st = DArray(Dims{long(ctx().sm_count) * conv_tc_stat_slots() * ny * 2}, false);
             g.stats = reinterpret_cast<double*>(st.data());
             g.stats_blocks = &st_blocks;
         }
@@ -1309,17 +1309,34 @@ private:
         if (st_blocks > 0) {
             y.chstats = std::make_shared<DArray>(st);
             y.chstats_blocks = st_blocks;
+            y.chstats_kind = 1;
         }
         return y;
     }
-    DArray bwd_data(const DArray& dy0, const DArray& w) const
+    // hint: forward state of the batch-norm block that produced x (it consumes
+    // dx); the tensor-core epilogue then also emits that block's backward partials
+    DArray bwd_data(const DArray& dy0, const DArray& w, const BnBwdHint* hint = nullptr) const
     {
         DArray dy = as_out(dy0);
         Dims xd = t_ ? outs_[0] : ins_[0];
         DArray dx(xd, false, act_layout(true));
         ConvGeom g = g_;
         g.out_tf32 = dy.tf32;
+        DArray part;
+        int blocks = 0;
+        if (hint && dx.layout == Layout::CHLAST && 2 * g_.Cin == 128 && conv_bn_fuse()) {
+            part = DArray(Dims{long(ctx().sm_count) * conv_tc_stat_slots() * 128 * 3}, false);
+            g.bnb = hint;
+            g.bnb_part = reinterpret_cast<double*>(part.data());
+            g.bnb_blocks = &blocks;
+        }
         conv_bwd_data(dx.data(), dy.data(), w.data(), g);
+        if (blocks > 0) {
+            dx.chstats = std::make_shared<DArray>(part);
+            dx.chstats_blocks = blocks;
+            dx.chstats_kind = 2;
+            dx.chstats_tag = hint;
+        }
         return dx;
     }
     DArray bwd_weight(const DArray& x0, const DArray& dy0) const
@@ -1377,7 +1394,7 @@ public:
         const Dims& sd = ins_[1];
         DArray y(ins_[0], false, Layout::CHLAST), mo(sd, false), vo(sd, false);
         DArray mu(sd, false), istd(Dims{C_}, false);
-        const bool pre = in[0].chstats && in[0].chstats_blocks > 0;
+        const bool pre = in[0].chstats && in[0].chstats_kind == 1 && in[0].chstats_blocks > 0;
         bnblock_forward(y.fdata(), mu.data(), istd.fdata(), mo.data(), vo.data(), in[0].fdata(), in[1].data(),
                         in[2].data(), in[3].data(), in[4].data(), npix_, int(C_), eps_, mom_, round_out_,
                         pre ? reinterpret_cast<const double*>(in[0].chstats->data()) : nullptr,
@@ -1392,9 +1409,15 @@ public:
             b_ = in[4];
             mu_ = mu;
             istd_ = istd;
+            hint_ = BnBwdHint{x_.fdata(), mu_.data(), istd_.fdata(), g_.data(), b_.data(), npix_, int(C_)};
+        } else {
+            hint_ = BnBwdHint{};
         }
         bump_generation();
     }
+    // the producer of y's cotangent (a tensor-core bwd-data conv) may fold the
+    // backward reduction pass into its epilogue
+    const void* cotangent_hint(int o) const override { return (o == 2 && hint_.x) ? &hint_ : nullptr; }
     void adjoint_all(int o, const DArray& gin, std::vector<DArray>& dx, const std::vector<char>& want) override
     {
         require_forward();
@@ -1412,8 +1435,12 @@ public:
                 return;
             // the reduction pass always produces both sums; route them to scratch when unwanted
             DArray sg = want[3] ? dg : DArray(sd, false), sb = want[4] ? db : DArray(sd, false);
+            const bool pre = gin.chstats && gin.chstats_kind == 2 && gin.chstats_tag == &hint_ && hint_.x
+                             && gin.chstats_blocks > 0;
             bnblock_backward(want[0] ? dxx.fdata() : nullptr, sg.data(), sb.data(), gin.fdata(), x_.fdata(),
-                             mu_.data(), istd_.fdata(), g_.data(), b_.data(), npix_, int(C_), round_dx_);
+                             mu_.data(), istd_.fdata(), g_.data(), b_.data(), npix_, int(C_), round_dx_,
+                             pre ? reinterpret_cast<const double*>(gin.chstats->data()) : nullptr,
+                             pre ? gin.chstats_blocks : 0);
             if (want[0]) {
                 dxx.tf32 = round_dx_;
                 dx[0] = dxx;
@@ -1523,6 +1550,7 @@ private:
     double m_ = 1;
     IsoGeom geo_{};
     DArray x_, g_, b_, mu_, istd_;
+    BnBwdHint hint_{};
 };
 
 } // namespace

@@ -180,3 +180,37 @@ def test_staged_batches_match_reference(gpu, ref, algo):
         losses.append(ls)
     np.testing.assert_allclose(losses[0], losses[1], rtol=1e-4)
     assert len(set(np.round(losses[1], 12))) == 3  # three distinct batches were consumed
+
+
+def test_modl_64_filters_bn_fusion(gpu, ref):
+    """64-filter MoDL (the tensor-core conv path): batch-norm statistics taken
+    from the conv epilogue and the BN backward reduction folded into the
+    bwd-data conv epilogue agree with the unfused passes (summation order only)
+    and with the reference (TF32 budget)."""
+    X, Y, NC, B = 24, 40, 2, 2
+    cfg = dict(iterations=1, layers=3, filters=64, cg_iter=3, im_x=X, im_y=Y, coils=NC, batch=B)
+    mref = Model.modl(ref, **cfg)
+    data, _ = _inputs(ref, mref, X, Y, NC, B)
+    res = []
+    for fuse in (1, 0):
+        gpu.check(gpu.so.mdnn_set_option(b"conv_bn_fuse", fuse))
+        try:
+            t = Trainer(gpu, Model.modl(gpu, **cfg), seed=42, lr=1e-3)
+            for k, v in data.items():
+                t.set_data(k, v)
+            loss = t.forward_backward()
+            res.append((loss, {n: t.get_grad(n) for n in t.weight_names()}))
+        finally:
+            gpu.check(gpu.so.mdnn_set_option(b"conv_bn_fuse", 1))
+    tr = Trainer(ref, mref, seed=42, lr=1e-3)
+    for k, v in data.items():
+        tr.set_data(k, v)
+    lref = tr.forward_backward()
+    (lf, gf), (lu, gu) = res
+    assert abs(lf - lu) <= 1e-5 * abs(lu)
+    assert abs(lf - lref) <= 1e-3 * abs(lref)
+    # the fused path ran: BN statistics summed in a different order somewhere
+    assert any(not np.array_equal(gf[n], gu[n]) for n in gu)
+    for n in gu:
+        assert rel_l2(gf[n], gu[n]) <= 1e-4, n
+        assert rel_l2(gf[n], tr.get_grad(n)) <= 5e-3, n
