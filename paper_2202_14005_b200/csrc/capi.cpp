@@ -176,6 +176,8 @@ int mdnn_set_option(const char* key, long value)
             conv_tc_form(int(value));
         else if (k == "conv_bn_fuse")
             conv_bn_fuse_enable(value != 0);
+        else if (k == "conv_wgrad_mc")
+            conv_wgrad_mc_enable(value != 0);
         else
             throw ConfigError("unknown option '" + k + "'");
     });

@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer (single thread) ----------------
+        {
+            // ---------------- MMA issuer (whole warp, elected lane issues) ----------------
             constexpr uint32_t idesc = idesc_tf32(128, NP);
             uint32_t hi = 0, wi = 0, ti = 0;
             const uint64_t hdesc0 = umma_desc_sw128(smem_u32(halo), TT_P * 128);
@@ -361,13 +361,13 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
                         const int ky = t / 3, kx = t % 3;
 #pragma unroll
                         for (int k = 0; k < 4; k++)
-                            mma_tf32(acc, wdesc + (k * 32 >> 4), hdesc + (((ky * TT_P + kx) * 128 + k * 32) >> 4), idesc,
+                            mma_tf32_warp(acc, wdesc + (k * 32 >> 4), hdesc + (((ky * TT_P + kx) * 128 + k * 32) >> 4), idesc,
                                      (c | t | k) != 0);
-                        mma_commit(&w_empty[st]);
+                        mma_commit_warp(&w_empty[st]);
                     }
-                    mma_commit(&halo_empty[hb]);
+                    mma_commit_warp(&halo_empty[hb]);
                 }
-                mma_commit(&tmem_full[ab]);
+                mma_commit_warp(&tmem_full[ab]);
             }
         }
     } else {
@@ -687,7 +687,11 @@ struct WgSmem {
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
-template<int N>
+// MC: the three CTAs of a split (ky = 0, 1, 2) form a cluster; they walk the
+// same dy segments, so rank 0 TMA-multicasts each dy segment to all three
+// (L2->SMEM dy traffic / 3; the kernel is bound by that traffic, not by the
+// tensor pipe) and re-fills a stage only when all three released it.
+template<int N, bool MC>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_conv_tc_wgrad(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
                     float* __restrict__ part, int X, int Y, int B, int nsplit)
@@ -701,7 +705,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint64_t* full = bars;
     uint64_t* empty = bars + WG_STAGES;
     uint64_t* tmem_full = bars + 2 * WG_STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    uint64_t* dy_empty = tmem_full + 1; // [WG_STAGES], rank 0's used (MC)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dy_empty + WG_STAGES);
+    const uint32_t crank = MC ? cluster_ctarank() : 0;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int ky = blockIdx.x % 3, split = blockIdx.x / 3;
@@ -715,6 +721,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int i = 0; i < WG_STAGES; i++) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
+            mbar_init(&dy_empty[i], 3);
         }
         mbar_init(tmem_full, 1);
         fence_barrier_init();
@@ -722,7 +729,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == 1)
         tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (MC)
+        cluster_sync(); // peers' barriers initialised before any multicast / remote arrive
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -734,38 +744,54 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int x0 = sx * WG_SEG;
                 const uint32_t st = it % WG_STAGES, ph = (it / WG_STAGES) & 1;
                 mbar_wait(&empty[st], ph ^ 1);
+                if (MC && crank == 0)
+                    mbar_wait(&dy_empty[st], ph ^ 1); // all three CTAs released the stage
                 mbar_arrive_expect_tx(&full[st], 4 * (WG_SEG + 2) * 128 + NDB * WG_SEG * 128);
                 uint8_t* base = smem + st * S::STAGE;
                 for (int j = 0; j < 4; j++)
                     tma_load_4d(base + j * WG_XBLK, &tm_x, &full[st], j * 32, x0 - 1, y + ky - 1, b);
-                for (int j = 0; j < NDB; j++)
-                    tma_load_4d(base + 4 * WG_XBLK + j * WG_DBLK, &tm_dy, &full[st], j * 32, x0, y, b);
+                if (!MC) {
+                    for (int j = 0; j < NDB; j++)
+                        tma_load_4d(base + 4 * WG_XBLK + j * WG_DBLK, &tm_dy, &full[st], j * 32, x0, y, b);
+                } else if (crank == 0) {
+                    for (int j = 0; j < NDB; j++)
+                        tma_load_4d_mc(base + 4 * WG_XBLK + j * WG_DBLK, &tm_dy, &full[st], j * 32, x0, y, b, 0x7);
+                }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        { // whole warp, elected lane issues (mma_tf32_warp)
             // a_major = b_major = MN (bits 15, 16)
             // a_major = b_major = MN (bits 15, 16); operands SWIZZLE_128B_BASE32B
             constexpr uint32_t idesc = idesc_tf32(128, N) | (1u << 15) | (1u << 16);
             uint32_t it = 0;
             const uint32_t sbase = smem_u32(smem);
-            for (long s = s_begin; s < s_end; s++, it++) {
+            // descriptors of stage 0; every other view is a constant start-address offset
+            const uint64_t xd0 = umma_desc_mn_sw128_32b(sbase, 512, WG_XBLK);
+            const uint64_t dd0 = umma_desc_mn_sw128_32b(sbase + 4 * WG_XBLK, 512, WG_DBLK);
+            const int nseg_cta = int(s_end - s_begin);
+            for (int si = 0; si < nseg_cta; si++, it++) {
                 const uint32_t st = it % WG_STAGES, ph = (it / WG_STAGES) & 1;
                 mbar_wait(&full[st], ph);
                 tc_fence_after();
-                const uint32_t xb = sbase + st * S::STAGE, db = xb + 4 * WG_XBLK;
+                // start-address field (bits 0-13) + offset: no carry for smem < 256 KB
+                const uint32_t so = (st * S::STAGE) >> 4;
+                const uint32_t xlo = uint32_t(xd0) + so, dlo = uint32_t(dd0) + so;
+                const uint64_t xhi = xd0 & 0xFFFFFFFF00000000ull, dhi = dd0 & 0xFFFFFFFF00000000ull;
 #pragma unroll
                 for (int ks = 0; ks < WG_SEG / 8; ks++) {
-                    const uint64_t bd = umma_desc_mn_sw128_32b(db + ks * 8 * 128, 512, WG_DBLK);
+                    const uint64_t bd = dhi | (dlo + uint32_t((ks * 8 * 128) >> 4));
 #pragma unroll
-                    for (int kx = 0; kx < 3; kx++) {
-                        const uint64_t ad = umma_desc_mn_sw128_32b(xb + (kx + ks * 8) * 128, 512, WG_XBLK);
-                        mma_tf32(tmem_base + kx * N, ad, bd, idesc, (s != s_begin || ks != 0) ? 1u : 0u);
-                    }
+                    for (int kx = 0; kx < 3; kx++)
+                        mma_tf32_warp(tmem_base + kx * N, xhi | (xlo + uint32_t(((kx + ks * 8) * 128) >> 4)), bd, idesc,
+                                 (si != 0 || ks != 0) ? 1u : 0u);
                 }
-                mma_commit(&empty[st]);
+                mma_commit_warp(&empty[st]);
+                if constexpr (MC)
+                    if (lane == 0)
+                        mma_commit_mc(&dy_empty[st], 0x1);
             }
-            mma_commit(tmem_full);
+            mma_commit_warp(tmem_full);
         }
     } else {
         const int lg = warp & 3;
@@ -789,7 +815,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (MC)
+        cluster_sync(); // no CTA leaves while multicasts / remote arrivals may target it
+    else
+        __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
@@ -909,6 +938,7 @@ CUtensorMap make_w_map(const float* base, int K, int N, int box_n = 0)
 }
 
 int g_tc_dbg = 0; // diagnostics: 1 = epilogue without global stores, 2 = no epilogue
+bool g_wgrad_mc = false; // bwd-weight: 3-CTA clusters with multicast dy segments (measured slower: 427 vs 402 us at C2)
 bool g_tc_pair = true; // CTA-pair (cta_group::2) kernel for the fwd / bwd-data convolutions
 int g_tc_form = 1;     // 1: transposed (channel-major accumulator) kernel where 2 Cout = 128
 
@@ -988,7 +1018,8 @@ void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, 
     auto& c = ctx();
     CUtensorMap tx = make_act_map(x, 128, X, Y, B, WG_SEG + 2, 1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     CUtensorMap td = make_act_map(dy, N, X, Y, B, WG_SEG, 1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    auto kern = k_conv_tc_wgrad<N>;
+    auto kern = k_conv_tc_wgrad<N, false>;
+    auto kern_mc = k_conv_tc_wgrad<N, true>;
     const int smem = WgSmem<N>::TOTAL;
     static std::mutex mu;
     static std::map<int, bool> done;
@@ -996,14 +1027,53 @@ void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, 
         std::lock_guard<std::mutex> lk(mu);
         if (!done[c.device]) {
             CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            CUDA_CHECK(cudaFuncSetAttribute(kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             done[c.device] = true;
         }
     }
     const long nseg = long((X + WG_SEG - 1) / WG_SEG) * Y * B;
-    const int nsplit = int(std::max(1L, std::min<long>(c.sm_count / 3, nseg)));
+    int nsplit = int(std::max(1L, std::min<long>(c.sm_count / 3, nseg)));
+    if (g_wgrad_mc) {
+        // co-resident 3-CTA clusters (GPC packing can leave SMs over): one wave
+        static std::map<int, int> max_cl;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!max_cl.count(c.device)) {
+            cudaLaunchConfig_t q{};
+            q.gridDim = dim3(unsigned(3 * (c.sm_count / 3)));
+            q.blockDim = dim3(NTHREADS);
+            q.dynamicSmemBytes = size_t(smem);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 3;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            q.attrs = at;
+            q.numAttrs = 1;
+            int n = 0;
+            CUDA_CHECK(cudaOccupancyMaxActiveClusters(&n, kern_mc, &q));
+            max_cl[c.device] = std::max(1, n);
+        }
+        nsplit = std::max(1, std::min(nsplit, max_cl[c.device]));
+    }
     float* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float) * size_t(nsplit) * 9 * 128 * N, c.stream));
-    kern<<<3 * nsplit, NTHREADS, smem, c.stream>>>(tx, td, part, X, Y, B, nsplit);
+    if (g_wgrad_mc) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(3 * nsplit));
+        cfg.blockDim = dim3(NTHREADS);
+        cfg.dynamicSmemBytes = size_t(smem);
+        cfg.stream = c.stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 3;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern_mc, tx, td, part, X, Y, B, nsplit));
+    } else {
+        kern<<<3 * nsplit, NTHREADS, smem, c.stream>>>(tx, td, part, X, Y, B, nsplit);
+    }
     KERNEL_CHECK();
     k_wgrad_fold<<<int(std::min(1024, (9 * Cin * Cout + 255) / 256)), 256, 0, c.stream>>>(dw, part, Cin, Cout, N,
                                                                                          nsplit);
@@ -1081,6 +1151,7 @@ bool g_bn_fuse = true;
 void conv_bn_fuse_enable(bool on) { g_bn_fuse = on; }
 bool conv_bn_fuse() { return g_bn_fuse; }
 void conv_tc_pair_enable(bool on) { g_tc_pair = on; }
+void conv_wgrad_mc_enable(bool on) { g_wgrad_mc = on; }
 void conv_tc_form(int f) { g_tc_form = f; }
 
 namespace {

@@ -138,6 +138,7 @@ int conv_tc_stat_slots(); // epilogue partial-sum blocks per CTA (ConvGeom::stat
 void conv_bn_fuse_enable(bool on);
 bool conv_bn_fuse();
 void conv_tc_pair_enable(bool on);
+void conv_wgrad_mc_enable(bool on);
 void conv_tc_form(int f);
 // persistent mask-pruned A^H A kernel (sense_rank.cuh); off = sense_fast.cuh path
 void sense_rank_enable(bool on);
