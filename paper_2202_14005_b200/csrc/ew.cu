@@ -156,16 +156,26 @@ __device__ double2 block_sum2(double2 v)
 }
 
 __global__ void k_iso_partial(double2* part, const cfloat* a, const cfloat* b, long inner, long nstat, long outer,
-                              int mode, int nchunk)
+                              int mode, int nchunk, long chunk)
 {
     const long stat = blockIdx.y;
     const long total = inner * outer;
-    const long begin = long(blockIdx.x) * kRedChunk;
-    const long end = min(total, begin + kRedChunk);
+    const long begin = long(blockIdx.x) * chunk;
+    const long end = min(total, begin + chunk);
     double2 acc{0, 0};
-    for (long j = begin + threadIdx.x; j < end; j += blockDim.x) {
-        long i = j % inner, o = j / inner;
-        long idx = i + inner * (stat + nstat * o);
+    // element j of this statistic sits at i + inner (stat + nstat o), (i, o) = (j mod inner, j / inner):
+    // one division per thread, then walked incrementally (nstat == 1: idx = j)
+    long j = begin + threadIdx.x;
+    long i = j % inner, o = j / inner;
+    const long di = long(blockDim.x) % inner, dO = long(blockDim.x) / inner;
+    for (; j < end; j += blockDim.x) {
+        const long idx = nstat == 1 ? j : i + inner * (stat + nstat * o);
+        i += di;
+        o += dO;
+        if (i >= inner) {
+            i -= inner;
+            o++;
+        }
         cfloat x = a[idx];
         if (mode == 0) {
             acc.x += x.x;
@@ -203,11 +213,19 @@ void iso_reduce_impl(cfloat* out, double2* out_d, const cfloat* a, const cfloat*
 {
     auto& c = ctx();
     long total = inner * outer;
-    int nchunk = int(std::max(1L, (total + kRedChunk - 1) / kRedChunk));
+    // chunk: kRedChunk elements, smaller for large single statistics so that the
+    // grid fills the GPU (about 4 blocks per SM); fixed for given sizes -> deterministic
+    long chunk = kRedChunk;
+    if (total * nstat > long(kRedChunk) * 4 * c.sm_count)
+        chunk = kRedChunk;
+    else
+        chunk = std::max(2048L, (total * nstat + 4L * c.sm_count - 1) / (4L * c.sm_count) / std::max(1L, nstat));
+    chunk = std::min<long>(chunk, kRedChunk);
+    int nchunk = int(std::max(1L, (total + chunk - 1) / chunk));
     double2* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double2) * nchunk * nstat, c.stream));
     dim3 grid(nchunk, unsigned(nstat));
-    k_iso_partial<<<grid, kThreads, 0, c.stream>>>(part, a, b, inner, nstat, outer, mode, nchunk);
+    k_iso_partial<<<grid, kThreads, 0, c.stream>>>(part, a, b, inner, nstat, outer, mode, nchunk, chunk);
     KERNEL_CHECK();
     k_iso_final<<<int(std::min(1024L, (nstat + 127) / 128)), 128, 0, c.stream>>>(out, out_d, part, nstat, nchunk,
                                                                                  scale);
