@@ -353,6 +353,15 @@ unsigned* imag_flag(std::initializer_list<std::pair<const cfloat*, long>> ops)
 
 } // namespace
 
+long conv_epi_blocks(const ConvGeom& g, int mode)
+{
+    if (conv_tc_supported(g.Cin, g.Cout, g.KX, g.KY))
+        return long(ctx().sm_count) * conv_tc_stat_slots();
+    if (conv_thin_supported(g))
+        return conv_thin_epi_blocks(g, mode);
+    return 0;
+}
+
 void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
 {
     check_geom(g);

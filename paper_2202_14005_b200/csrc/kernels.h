@@ -153,6 +153,10 @@ void conv_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom&
 bool conv_tc_wgrad_supported(long cin, long cout, long kx, long ky);
 // thin layers (one side 1 channel, wide side CHLAST): conv_thin.cu
 bool conv_thin_supported(const ConvGeom& g);
+long conv_thin_epi_blocks(const ConvGeom& g, int mode);
+// upper bound on the epilogue partial blocks a conv launch writes into
+// ConvGeom::stats (mode 0) / bnb_part (mode 1); 0 = that path has none
+long conv_epi_blocks(const ConvGeom& g, int mode);
 void conv_thin_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode);
 void conv_thin_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
 void conv_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);

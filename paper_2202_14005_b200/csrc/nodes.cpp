@@ -1300,8 +1300,9 @@ private:
         const long ny = 2 * g_.Cout;
         DArray st;
         int st_blocks = 0;
-        if (y.layout == Layout::CHLAST && ny == 128 && conv_bn_fuse()) {
-            st = DArray(Dims{long(ctx().sm_count) * conv_tc_stat_slots() * ny * 2}, false);
+        const long eb = (y.layout == Layout::CHLAST && ny == 128 && conv_bn_fuse()) ? conv_epi_blocks(g_, 0) : 0;
+        if (eb > 0) {
+            st = DArray(Dims{eb * ny * 2}, false);
             g.stats = reinterpret_cast<double*>(st.data());
             g.stats_blocks = &st_blocks;
         }
@@ -1324,8 +1325,11 @@ private:
         g.out_tf32 = dy.tf32;
         DArray part;
         int blocks = 0;
-        if (hint && dx.layout == Layout::CHLAST && 2 * g_.Cin == 128 && conv_bn_fuse()) {
-            part = DArray(Dims{long(ctx().sm_count) * conv_tc_stat_slots() * 128 * 3}, false);
+        const long eb = (hint && dx.layout == Layout::CHLAST && 2 * g_.Cin == 128 && conv_bn_fuse())
+                            ? conv_epi_blocks(g_, 1)
+                            : 0;
+        if (eb > 0) {
+            part = DArray(Dims{eb * 128 * 3}, false);
             g.bnb = hint;
             g.bnb_part = reinterpret_cast<double*>(part.data());
             g.bnb_blocks = &blocks;
