@@ -825,20 +825,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
 }
 
-// dw[t, c, f] from the per-split real blocks (fixed split order, fp64 sums)
-__global__ void k_wgrad_fold(cfloat* __restrict__ dw, const float* __restrict__ part, int Cin, int Cout, int N,
-                             int nsplit)
+// dw[t, c, f] from the per-split real blocks (fp64 sums in a fixed order: split group g
+// sums splits g, g + 4, ...; the four groups are then added in order g = 0..3).
+// Block = 64 outputs (f fastest: coalesced partial rows) x 4 split groups.
+__global__ void __launch_bounds__(256) k_wgrad_fold(cfloat* __restrict__ dw, const float* __restrict__ part, int Cin,
+                                                    int Cout, int N, int nsplit)
 {
+    __shared__ double2 red[4][64];
     const int n_out = 9 * Cin * Cout;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_out; i += gridDim.x * blockDim.x) {
-        const int t = i % 9, c = (i / 9) % Cin, f = i / (9 * Cin);
-        double re = 0, im = 0;
-        for (int s = 0; s < nsplit; s++) {
-            const float* D = part + (size_t(s) * 9 + t) * 128 * N;
-            re += double(D[c * N + f]) + double(D[(Cin + c) * N + Cout + f]);
-            im += double(D[c * N + Cout + f]) - double(D[(Cin + c) * N + f]);
+    const int o = threadIdx.x & 63, g = threadIdx.x >> 6;
+    const int i = blockIdx.x * 64 + o;
+    double re = 0, im = 0;
+    int f = 0, c = 0, t = 0;
+    if (i < n_out) {
+        f = i % Cout;
+        c = (i / Cout) % Cin;
+        t = i / (Cout * Cin);
+        const size_t sstride = size_t(9) * 128 * N;
+        const float* D = part + size_t(t) * 128 * N + size_t(g) * sstride;
+#pragma unroll 4
+        for (int s = g; s < nsplit; s += 4, D += 4 * sstride) {
+            const float a0 = D[c * N + f], a1 = D[(Cin + c) * N + Cout + f];
+            const float b0 = D[c * N + Cout + f], b1 = D[(Cin + c) * N + f];
+            re += double(a0) + double(a1);
+            im += double(b0) - double(b1);
         }
-        dw[t + 9 * (c + Cin * f)] = float2{float(re), float(im)};
+    }
+    red[g][o] = double2{re, im};
+    __syncthreads();
+    if (g == 0 && i < n_out) {
+        double2 r = red[0][o];
+        for (int k = 1; k < 4; k++) {
+            r.x += red[k][o].x;
+            r.y += red[k][o].y;
+        }
+        dw[t + 9 * (c + Cin * f)] = float2{float(r.x), float(r.y)};
     }
 }
 
@@ -1075,7 +1096,7 @@ void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, 
         kern<<<3 * nsplit, NTHREADS, smem, c.stream>>>(tx, td, part, X, Y, B, nsplit);
     }
     KERNEL_CHECK();
-    k_wgrad_fold<<<int(std::min(1024, (9 * Cin * Cout + 255) / 256)), 256, 0, c.stream>>>(dw, part, Cin, Cout, N,
+    k_wgrad_fold<<<(9 * Cin * Cout + 63) / 64, 256, 0, c.stream>>>(dw, part, Cin, Cout, N,
                                                                                          nsplit);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
