@@ -747,13 +747,21 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
         // persistent rank kernel: Ap in plane 0 (+ plane 1 for split strips);
         // p ping-pongs between two buffers (no CTA reads a p another rewrites)
         // few update CTAs: one contended counter atomic per CTA in publish_partial
-        const int n_updr = int(std::min<long>(2L * c.sm_count, g.Y * g.B));
+        // Deferred x (up to 32 iterations): every direction p_it is kept (P[it + 1]),
+        // the update kernel touches Ap and r only, and x is summed once at the end.
+        const bool defer = max_iter <= 32 && g_cg_defer_x && n % 2 == 0;
+        constexpr int UR = 2; // element pairs per thread in k_cg_update_r
+        const long npair = n / 2;
+        const int n_updr = defer ? int(std::min<long>(3L * c.sm_count, (npair + 256L * UR - 1) / (256L * UR)))
+                                 : int(std::min<long>(2L * c.sm_count, g.Y * g.B));
         CgMem m = cg_alloc(max_iter, tol, rp.G, n_updr);
-        DArray r(Dims{n}, false), pb(Dims{2 * n}, false), ap(Dims{n * std::max(2, rp.planes)}, false);
+        DArray r(Dims{n}, false), pb(Dims{(defer ? max_iter + 1 : 2) * n}, false),
+            ap(Dims{n * std::max(2, rp.planes)}, false);
         DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
         unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
         cfloat* P[2] = {pb.data(), pb.data() + n};
-        cg_start(m, x, b, r.data(), P[1], n);
+        auto pdir = [&](int k) { return defer ? pb.data() + long(k) * n : P[k & 1]; }; // p_(k-1) lives at pdir(k)
+        cg_start(m, x, b, r.data(), pdir(1), n);
         {
             RankArgs a{};
             a.pattern = pattern;
@@ -766,8 +774,8 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             a.out1 = ap.data() + n;
             a.pstride = n;
             a.x = r.data();
-            a.p = P[it & 1];
-            a.p_out = P[(it + 1) & 1];
+            a.p = pdir(it);
+            a.p_out = pdir(it + 1);
             a.pattern = pattern;
             a.lam = lam;
             a.ps = pat_strides(g);
@@ -776,11 +784,23 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             a.cg = m.st;
             a.errflags = c.d_errflags;
             launch_rank(rp, a, coils, g, pl);
-            ProfScope prof("cg_update_rank", 8.0 * n * 7);
-            k_cg_update_rank<<<n_updr, 512, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(),
-                                                          ap.data() + n, rank_split_flags(g, pl), int(g.X),
-                                                          int(g.Y * g.B), int(g.Y), int(rp.nxb),
-                                                          rp.W == 8 ? 3 : 2, n, c.d_errflags);
+            if (defer) {
+                ProfScope prof("cg_update_rank", 8.0 * n * 4);
+                k_cg_update_r<UR><<<n_updr, 256, 0, c.stream>>>(m.st, it, r.data(), ap.data(), ap.data() + n,
+                                                               rank_split_flags(g, pl), int(g.X), int(g.Y * g.B),
+                                                               int(g.Y), int(rp.nxb), rp.W == 8 ? 3 : 2, n,
+                                                               c.d_errflags);
+            } else {
+                ProfScope prof("cg_update_rank", 8.0 * n * 7);
+                k_cg_update_rank<<<n_updr, 512, 0, c.stream>>>(m.st, it, x, r.data(), pdir(it + 1), ap.data(),
+                                                              ap.data() + n, rank_split_flags(g, pl), int(g.X),
+                                                              int(g.Y * g.B), int(g.Y), int(rp.nxb),
+                                                              rp.W == 8 ? 3 : 2, n, c.d_errflags);
+            }
+            KERNEL_CHECK();
+        }
+        if (defer) {
+            k_cg_x_sum<<<grid_for(n / 2), 256, 0, c.stream>>>(m.st, x, pb.data(), n);
             KERNEL_CHECK();
         }
         k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
@@ -866,6 +886,7 @@ bool g_rank_enabled = true;
 void sense_rank_enable(bool on) { g_rank_enabled = on; }
 void sense_rank_ctas(long g) { g_rank_ctas = g; }
 void sense_rank_tm_enable(bool on) { g_rank_tm = on; }
+void cg_defer_x_enable(bool on) { g_cg_defer_x = on; }
 bool rank_enabled() { return g_rank_enabled; }
 
 CgResult read_cg_status(const double* status_dev)

@@ -26,6 +26,7 @@
 
 #include <type_traits>
 
+bool g_cg_defer_x = true; // CG: keep every p, update r only per iteration, sum x once
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
 bool g_rank_tm = false; // TMEM-resident variant (sense_rank_tm.cuh) for N1 = 16
 
@@ -630,6 +631,109 @@ __global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloa
     }
     part = block_sum2(part);
     publish_partial(st->part_rr, &st->rr_sum, &st->cnt_rr, part);
+}
+
+// r-only CG update (x deferred): r -= alpha Ap ; <r, r> partial.  With every
+// search direction p_it kept, x = sum_it alpha_it p_it is formed once after the
+// loop by k_cg_x_sum in the same fma order as the per-iteration update (bitwise
+// identical), and each iteration streams 3 arrays instead of 5.
+template<int U>
+__global__ void __launch_bounds__(256) k_cg_update_r(CgDev* st, int it, cfloat* __restrict__ r,
+                                                     const cfloat* __restrict__ ap, const cfloat* __restrict__ ap1,
+                                                     const unsigned char* __restrict__ split, int X, int rows, int Y,
+                                                     int nxb, int wshift, long pstride, unsigned* errflags)
+{
+    __shared__ float s_alpha;
+    if (threadIdx.x == 0)
+        s_alpha = cg_alpha(st, it, errflags);
+    const int X2 = X >> 1;
+    const int npair = rows * X2;
+    const int stride = gridDim.x * blockDim.x;
+    const float4* ap4 = reinterpret_cast<const float4*>(ap);
+    const float4* ap14 = reinterpret_cast<const float4*>(ap1);
+    float4* r4 = reinterpret_cast<float4*>(r);
+    float4 av[U], t1[U], rv[U];
+    int sp[U];
+    bool ok[U];
+    int i0 = blockIdx.x * blockDim.x + threadIdx.x;
+    auto load = [&](int base) {
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            const int i = base + k * stride;
+            ok[k] = i < npair;
+            const int ii = ok[k] ? i : 0;
+            av[k] = ap4[ii];
+            t1[k] = ap14[ii]; // junk outside split strips: not used there
+            rv[k] = r4[ii];
+            const int row = ii / X2, xp = ii - row * X2;
+            sp[k] = split[(row / Y) * nxb + ((2 * xp) >> wshift)];
+        }
+    };
+    load(i0);
+    __syncthreads();
+    const float al = s_alpha;
+    if (!(al > 0.f))
+        return;
+    double2 part{0, 0};
+    while (true) {
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            if (!ok[k])
+                continue;
+            float4 a = av[k];
+            if (sp[k] > 1) {
+                a.x += t1[k].x;
+                a.y += t1[k].y;
+                a.z += t1[k].z;
+                a.w += t1[k].w;
+                for (int pk = 2; pk < sp[k]; pk++) {
+                    const float4 t = ap14[i0 + k * stride + long(pk - 1) * (pstride / 2)];
+                    a.x += t.x;
+                    a.y += t.y;
+                    a.z += t.z;
+                    a.w += t.w;
+                }
+            }
+            float4 rr = rv[k];
+            rr.x += -al * a.x;
+            rr.y += -al * a.y;
+            rr.z += -al * a.z;
+            rr.w += -al * a.w;
+            r4[i0 + k * stride] = rr;
+            part.x += double(rr.x) * rr.x + double(rr.y) * rr.y;
+            part.x += double(rr.z) * rr.z + double(rr.w) * rr.w;
+        }
+        i0 += U * stride;
+        if (i0 >= npair)
+            break;
+        load(i0);
+    }
+    part = block_sum2(part);
+    publish_partial(st->part_rr, &st->rr_sum, &st->cnt_rr, part);
+}
+
+// x += alpha_it p_it for every iteration that ran, in iteration order (the
+// per-iteration update's fma sequence); P holds p_it at P + (it + 1) * n
+__global__ void __launch_bounds__(256) k_cg_x_sum(const CgDev* __restrict__ st, cfloat* __restrict__ x,
+                                                  const cfloat* __restrict__ P, long n)
+{
+    const int nit = min(st->done_at, st->max_iter);
+    const long npair = n >> 1;
+    float4* x4 = reinterpret_cast<float4*>(x);
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < npair; i += long(gridDim.x) * blockDim.x) {
+        float4 xv = x4[i];
+        for (int it = 0; it < nit; it++) {
+            const float al = st->alpha[it];
+            if (!(al > 0.f))
+                continue;
+            const float4 pv = reinterpret_cast<const float4*>(P + (it + 1) * n)[i];
+            xv.x = fmaf(al, pv.x, xv.x);
+            xv.y = fmaf(al, pv.y, xv.y);
+            xv.z = fmaf(al, pv.z, xv.z);
+            xv.w = fmaf(al, pv.w, xv.w);
+        }
+        x4[i] = xv;
+    }
 }
 
 // split flags of every strip (written once per plan buffer)

@@ -137,3 +137,37 @@ def test_rank_deterministic(gpu, ref, rank_opts):
     a = _normal(gpu, cm, pat, ph)
     b = _normal(gpu, cm, pat, ph)
     assert np.array_equal(np.ascontiguousarray(a).view(np.uint32), np.ascontiguousarray(b).view(np.uint32))
+
+
+@pytest.mark.parametrize("tol", [0.0, 0.1])
+def test_cg_deferred_x_bitwise(gpu, ref, rank_opts, tol):
+    """CG with every search direction kept and x summed once after the loop
+    (`cg_defer_x`, default) is bitwise equal to the per-iteration x update, with
+    and without early convergence; both match the reference."""
+    X, Y, NC, B = 48, 368, 4, 2
+    ph, cm, pat = sim_data(ref, X, Y, NC, B)
+    rng = np.random.default_rng(8)
+    b = crand(rng, image_dims(X, Y, B))
+
+    def solve(lib):
+        x = np.zeros(b.shape, dtype=np.complex64, order="F")
+        it, rr = C.c_long(), C.c_double()
+        lib.check(lib.so.mdnn_cg_normal_solve(C.byref(lib.arr(cm)), C.byref(lib.arr(pat)), C.c_float(0.05),
+                                              C.byref(lib.arr(b)), 10, tol, C.byref(lib.arr(x)), C.byref(it),
+                                              C.byref(rr)))
+        return x, it.value
+
+    xr, itr = solve(ref)
+    res = []
+    try:
+        for d in (1, 0):
+            gpu.check(gpu.so.mdnn_set_option(b"cg_defer_x", d))
+            res.append(solve(gpu))
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"cg_defer_x", 1))
+    (x1, i1), (x0, i0) = res
+    assert i1 == i0 == itr
+    if tol > 0:
+        assert itr < 10
+    assert np.array_equal(np.ascontiguousarray(x1).view(np.uint32), np.ascontiguousarray(x0).view(np.uint32))
+    assert rel_l2(x1, xr) <= TOL
