@@ -168,6 +168,8 @@ int mdnn_set_option(const char* key, long value)
             sense_rank_tm_enable(value != 0);
         else if (k == "cg_defer_x")
             cg_defer_x_enable(value != 0);
+        else if (k == "sense_rank_split")
+            sense_rank_split_enable(value != 0);
         else if (k == "conv_chlast")
             conv_force_chlast(value != 0);
         else if (k == "conv_tc_debug")

@@ -145,6 +145,7 @@ void sense_rank_enable(bool on);
 void sense_rank_ctas(long g);
 void sense_rank_tm_enable(bool on);
 void cg_defer_x_enable(bool on);
+void sense_rank_split_enable(bool on);
 bool rank_enabled();
 // test hook: auto-layout convs store multi-channel activations channels-last
 void conv_force_chlast(bool on);

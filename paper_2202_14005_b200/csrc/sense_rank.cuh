@@ -26,6 +26,7 @@
 
 #include <type_traits>
 
+bool g_rank_split = false; // two threads per (column, j) in the q-DFTs (k_normal_rank<.., 2>): 116 vs 72 us at C2 (spills at the 2-CTA register cap)
 bool g_cg_defer_x = true; // CG: keep every p, update r only per iteration, sum x once
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
 bool g_rank_tm = false; // TMEM-resident variant (sense_rank_tm.cuh) for N1 = 16
@@ -177,6 +178,16 @@ __device__ void rank_build_plan(RankPlanSm<N1, N2>& pl, const RankArgs& a, int b
 }
 
 // Global plan record per pattern item: [RankPlanSm | ttw[TMAX * N2]], 16-B multiple.
+// v[q] *= exp(DIR 2 pi i q / N) for q = Q..NQ-1 (compile-time twiddles)
+template<int N, int DIR, int Q, int NQ>
+__device__ __forceinline__ void rank_rot_all(float2 (&v)[NQ])
+{
+    if constexpr (Q < NQ) {
+        v[Q] = fftd::rot<Q, N, DIR>(v[Q]);
+        rank_rot_all<N, DIR, Q + 1, NQ>(v);
+    }
+}
+
 template<int N1, int N2>
 struct RankPlanRec {
     static constexpr size_t PL = (sizeof(RankPlanSm<N1, N2>) + 15) & ~size_t(15);
@@ -192,13 +203,20 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT) k_rank_plan(RankArgs a, u
                             reinterpret_cast<float2*>(rec + RankPlanRec<N1, N2>::PL), a.tw);
 }
 
-template<int N1, int N2>
-__global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
+// H = 2: two threads per (column, j) share the N1-point q-DFTs (each holds N1/2
+// points; one 8-value shuffle exchange per DFT, radix-2 split over lane ^ 16),
+// halving the per-thread accumulator / coil / value arrays so twice the warps
+// are resident per SM (the kernel is latency-bound).
+template<int N1, int N2, int H>
+__global__ void __launch_bounds__(RankCfg<N1, N2>::NT * H, RankCfg<N1, N2>::MINB)
     k_normal_rank(RankArgs a, const __grid_constant__ CUtensorMap tmap, const unsigned char* __restrict__ plans)
 {
     using namespace fftd;
     using Cfg = RankCfg<N1, N2>;
-    constexpr int Y = Cfg::Y, W = Cfg::W, NT = Cfg::NT, JH = Cfg::JH, TMAX = Cfg::TMAX, N2P = Cfg::N2P;
+    constexpr int Y = Cfg::Y, W = Cfg::W, JH = Cfg::JH, TMAX = Cfg::TMAX, N2P = Cfg::N2P;
+    constexpr int NT = Cfg::NT * H; // threads of this CTA
+    constexpr int NQ = N1 / H;      // q points per thread
+    static_assert(H == 1 || (H == 2 && Cfg::NT % 16 == 0), "split threads pair across lane ^ 16");
     extern __shared__ __align__(128) float2 rank_smem[];
     float2* ring = rank_smem;
     float2* S = ring + 2 * Cfg::SLOT;
@@ -210,7 +228,17 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
     __shared__ __align__(16) RankPlanSm<N1, N2> pl;
 
     const int tid = threadIdx.x;
-    const int w = tid % W, j0 = tid / W;
+    int w, j0, h;
+    if constexpr (H == 1) {
+        w = tid % W;
+        j0 = tid / W;
+        h = 0;
+    } else {
+        const int t16 = (tid >> 5) * 16 + (tid & 15); // (w, j) slot; lane bit 4 = half
+        w = t16 % W;
+        j0 = t16 / W;
+        h = (tid >> 4) & 1;
+    }
     const bool active = j0 < N2;
     const int j = active ? j0 : N2 - 1;
     const int C = int(a.C), nxb = int(a.nxb);
@@ -258,7 +286,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
     int n_items = 0, my_h = 0, my_k1 = 0, my_ww = 0, my_md = 0, my_nt = 0, my_off = 0;
     bool my_item = false;
     double2 part{0, 0};
-    float2 acc[N1], cv[N1];
+    float2 acc[NQ], cv[NQ];
     int seg_s = u_begin / C;           // strip of the open segment
     int c_cur = u_begin - seg_s * C;   // coil of unit i
     bool seg_first = c_cur == 0;
@@ -268,13 +296,25 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
         const bool opens = i < n && (i == 0 || c_cur == 0);
         if (i >= 1) {
             // ---- C(i-1): inverse DFT over k1, conj-coil accumulate
-            float2 v[N1];
+            float2 v[NQ];
 #pragma unroll
-            for (int k1 = 0; k1 < N1; k1++)
-                v[k1] = S[(k1 * N2P + j) * W + w];
-            dft_reg<N1, +1>(v);
+            for (int m = 0; m < NQ; m++)
+                v[m] = S[((H * m + h) * N2P + j) * W + w]; // H = 2: rows of this thread's parity
+            if constexpr (H == 1) {
+                dft_reg<N1, +1>(v);
+            } else {
+                // x[q] = E[q] + w^q O[q], x[q + NQ] = E[q] - w^q O[q]  (w = e^{+2 pi i / N1})
+                dft_reg<NQ, +1>(v);
+                if (h)
+                    rank_rot_all<N1, +1, 0, NQ>(v);
 #pragma unroll
-            for (int q = 0; q < N1; q++) {
+                for (int q = 0; q < NQ; q++) {
+                    const float2 u{__shfl_xor_sync(0xffffffffu, v[q].x, 16), __shfl_xor_sync(0xffffffffu, v[q].y, 16)};
+                    v[q] = h ? csub(u, v[q]) : cadd(v[q], u);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
                 const float2 t = cmulc(v[q], cv[q]);
                 acc[q].x += t.x;
                 acc[q].y += t.y;
@@ -285,8 +325,8 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
                 const long img_base = xx + a.X * Y * long(b);
                 cfloat* dst = rank_plane_dst(a, seg_s, blockIdx.x);
 #pragma unroll
-                for (int q = 0; q < N1; q++) {
-                    const int y = j + N2 * q;
+                for (int q = 0; q < NQ; q++) {
+                    const int y = j + N2 * (h * NQ + q);
                     const float2 xv = xs[y * W + w];
                     float2 o{acc[q].x * invN1, acc[q].y * invN1};
                     if (seg_first) {
@@ -336,17 +376,17 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
                 const int xx = (seg_s - b * nxb) * W + w;
                 const bool colok = active && xx < a.X;
                 const long img_base = xx + a.X * Y * long(b);
-                float2 v[N1], pv[N1];
+                float2 v[NQ], pv[NQ];
                 const float2* src = a.mode == 0 ? a.x : (a.it == 0 ? a.p_out : a.x);
 #pragma unroll
-                for (int q = 0; q < N1; q++) {
-                    const long gi = img_base + a.X * (j + N2 * q);
+                for (int q = 0; q < NQ; q++) {
+                    const long gi = img_base + a.X * (j + N2 * (h * NQ + q));
                     v[q] = colok ? src[gi] : float2{0.f, 0.f};
                     pv[q] = (colok && upd) ? a.p[gi] : float2{0.f, 0.f};
                 }
 #pragma unroll
-                for (int q = 0; q < N1; q++) {
-                    const int y = j + N2 * q;
+                for (int q = 0; q < NQ; q++) {
+                    const int y = j + N2 * (h * NQ + q);
                     if (upd) {
                         v[q] = float2{v[q].x + beta * pv[q].x, v[q].y + beta * pv[q].y};
                         if (seg_first && colok)
@@ -361,21 +401,33 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
             const int slot = i & 1;
             const float2* cs = ring + slot * Cfg::SLOT;
             sm100::mbar_wait(&s_bar[slot], uint32_t((i >> 1) & 1));
-            float2 v[N1];
+            float2 v[NQ];
             // padding threads (j clamped) compute on valid rows; their results are never stored
-            const float2* csp = cs + j * W + w;
-            const float2* xsp = xs + j * W + w;
+            const float2* csp = cs + (j + N2 * h * NQ) * W + w;
+            const float2* xsp = xs + (j + N2 * h * NQ) * W + w;
 #pragma unroll
-            for (int q = 0; q < N1; q++)
+            for (int q = 0; q < NQ; q++)
                 cv[q] = csp[N2 * W * q];
 #pragma unroll
-            for (int q = 0; q < N1; q++)
+            for (int q = 0; q < NQ; q++)
                 v[q] = cmul(cv[q], xsp[N2 * W * q]);
-            dft_reg<N1, -1>(v);
+            if constexpr (H == 2) {
+                // X[2m] = DFT(a[q] + a[q + NQ]), X[2m + 1] = DFT((a[q] - a[q + NQ]) w^-q)
+#pragma unroll
+                for (int q = 0; q < NQ; q++) {
+                    const float2 u{__shfl_xor_sync(0xffffffffu, v[q].x, 16), __shfl_xor_sync(0xffffffffu, v[q].y, 16)};
+                    v[q] = h ? csub(u, v[q]) : cadd(v[q], u);
+                }
+                if (h)
+                    rank_rot_all<N1, -1, 0, NQ>(v);
+                dft_reg<NQ, -1>(v);
+            } else {
+                dft_reg<N1, -1>(v);
+            }
             if (active) {
 #pragma unroll
-                for (int k1 = 0; k1 < N1; k1++)
-                    S[(k1 * N2P + j) * W + w] = v[k1];
+                for (int m = 0; m < NQ; m++)
+                    S[((H * m + h) * N2P + j) * W + w] = v[m];
             }
         }
         __syncthreads();
@@ -820,17 +872,20 @@ void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const un
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS)
         throw CudaError("cuTensorMapEncodeTiled(coils) failed: " + std::to_string(int(res)));
-    auto kern = k_normal_rank<N1, N2>;
+    auto kern = g_rank_split && N1 == 16 ? k_normal_rank<N1, N2, 2> : k_normal_rank<N1, N2, 1>;
+    const int nthreads = (g_rank_split && N1 == 16 ? 2 : 1) * Cfg::NT;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_normal_rank<N1, N2, 1>),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_normal_rank<N1, N2, 2>),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
         attr = true;
     }
     const double xyb = double(g.X) * g.Y * g.B;
     const double work = 8.0 * xyb * (g.C + (a.mode == 1 ? 4 : 2));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    kern<<<a.G, Cfg::NT, Cfg::SMEM, ctx().stream>>>(a, m, plans);
+    kern<<<a.G, nthreads, Cfg::SMEM, ctx().stream>>>(a, m, plans);
     KERNEL_CHECK();
 }
 
