@@ -208,6 +208,25 @@ __global__ void k_iso_final(cfloat* out, double2* out_d, const double2* part, lo
     }
 }
 
+// one block per statistic: strided chunk sums, then a fixed-order block tree
+// (many chunks, few statistics: the serial loop above is latency-bound)
+__global__ void k_iso_final_block(cfloat* out, double2* out_d, const double2* part, int nchunk, float scale)
+{
+    const long s = blockIdx.x;
+    double2 acc{0, 0};
+    for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
+        acc.x += part[s * nchunk + c].x;
+        acc.y += part[s * nchunk + c].y;
+    }
+    acc = block_sum2(acc);
+    if (threadIdx.x == 0) {
+        if (out)
+            out[s] = cfloat{float(acc.x * scale), float(acc.y * scale)};
+        if (out_d)
+            out_d[s] = acc;
+    }
+}
+
 void iso_reduce_impl(cfloat* out, double2* out_d, const cfloat* a, const cfloat* b, long inner, long nstat,
                      long outer, int mode, float scale)
 {
@@ -227,8 +246,11 @@ void iso_reduce_impl(cfloat* out, double2* out_d, const cfloat* a, const cfloat*
     dim3 grid(nchunk, unsigned(nstat));
     k_iso_partial<<<grid, kThreads, 0, c.stream>>>(part, a, b, inner, nstat, outer, mode, nchunk, chunk);
     KERNEL_CHECK();
-    k_iso_final<<<int(std::min(1024L, (nstat + 127) / 128)), 128, 0, c.stream>>>(out, out_d, part, nstat, nchunk,
-                                                                                 scale);
+    if (nchunk >= 64 && nstat <= 4096)
+        k_iso_final_block<<<unsigned(nstat), 256, 0, c.stream>>>(out, out_d, part, nchunk, scale);
+    else
+        k_iso_final<<<int(std::min(1024L, (nstat + 127) / 128)), 128, 0, c.stream>>>(out, out_d, part, nstat, nchunk,
+                                                                                     scale);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
