@@ -75,7 +75,9 @@ int mdnn_synchronize(void);
    pixel-major kernel), "conv_tc_debug" (diagnostics: 1 = no epilogue stores,
    2 = no epilogue; results invalid), "conv_bn_fuse" (1 = batch-norm
    statistics / backward reductions folded into the tensor-core conv
-   epilogues), "sense_rank" / "sense_rank_ctas" /
+   epilogues), "conv_thin_tc" (1 = F -> 1 convolutions as tcgen05 tap
+   projections + gather), "conv_wgrad_mc", "conv_tc_pair", "cg_defer_x",
+   "sense_rank_split", "sense_rank" / "sense_rank_ctas" /
    "sense_rank_tm" (A^H A kernel selection) */
 int mdnn_set_option(const char* key, long value);
 /* the library's CUDA stream on the current device (cudaStream_t), so callers

@@ -170,6 +170,8 @@ int mdnn_set_option(const char* key, long value)
             cg_defer_x_enable(value != 0);
         else if (k == "sense_rank_split")
             sense_rank_split_enable(value != 0);
+        else if (k == "conv_thin_tc")
+            conv_thin_tc_enable(value != 0);
         else if (k == "conv_chlast")
             conv_force_chlast(value != 0);
         else if (k == "conv_tc_debug")

@@ -537,6 +537,8 @@ void run_thin(cfloat* outp, const cfloat* inp, const float2* U, const ConvGeom& 
             k_thin_expand<K, 1><<<grid, NT, 0, c.stream>>>(reinterpret_cast<float*>(outp), inp, U, int(g.X),
                                                            int(g.Y), F, ox, oy, ThinEpi{});
     } else {
+        if (thin_reduce_tc(outp, reinterpret_cast<const float*>(inp), U, g.X, g.Y, g.B, F, K * K, ox, oy))
+            return; // tensor-core projections + gather (conv_thin_tc.cu)
         using Cfg = ReduceCfg<K>;
         auto kern = k_thin_reduce<K>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));

@@ -156,6 +156,10 @@ bool conv_tc_wgrad_supported(long cin, long cout, long kx, long ky);
 // thin layers (one side 1 channel, wide side CHLAST): conv_thin.cu
 bool conv_thin_supported(const ConvGeom& g);
 long conv_thin_epi_blocks(const ConvGeom& g, int mode);
+// F -> 1 (3x3, F = 64) on the tensor cores; false when the shape is not covered
+bool thin_reduce_tc(cfloat* out, const float* wide, const float2* U, long X, long Y, long B, int F, int KK, int ox,
+                    int oy);
+void conv_thin_tc_enable(bool on);
 // upper bound on the epilogue partial blocks a conv launch writes into
 // ConvGeom::stats (mode 0) / bnb_part (mode 1); 0 = that path has none
 long conv_epi_blocks(const ConvGeom& g, int mode);

@@ -123,6 +123,32 @@ def test_conv_tc_kernel_variants(gpu, ref, opts, cin, cout, X, Y, B):
         gpu.check(gpu.so.mdnn_set_option(b"conv_tc_pair", 1))
 
 
+@pytest.mark.parametrize("transposed", [False, True])
+@pytest.mark.parametrize("X,Y,B", [(40, 36, 2), (33, 70, 1)])
+def test_thin_reduce_tensor_core(gpu, ref, transposed, X, Y, B):
+    """64 -> 1 (and the bwd-data of 1 -> 64) through the tcgen05 projection +
+    gather path (conv_thin_tc.cu) and through the CUDA-core kernel, against the
+    reference: fwd, bwd-data and bwd-weight at the TF32 budget."""
+    rng = np.random.default_rng(X + Y)
+    cin, cout = (1, 64) if transposed else (64, 1)
+    in_dims = list(d16(X, Y, cin))
+    in_dims[15] = B
+    mr = Model.conv_layer(ref, "c", in_dims, (3, 3), cout, transposed=transposed, bias=not transposed)
+    ins = [crand(rng, mr.nlop.in_dims(i)) for i in range(mr.nlop.n_in)]
+    outs = []
+    for tc in (1, 0):
+        gpu.check(gpu.so.mdnn_set_option(b"conv_chlast", 1))
+        gpu.check(gpu.so.mdnn_set_option(b"conv_thin_tc", tc))
+        try:
+            mg = Model.conv_layer(gpu, "c", in_dims, (3, 3), cout, transposed=transposed, bias=not transposed)
+            _check_node(mg.nlop, mr.nlop, ins, np.random.default_rng(1), CONV_TOL, mr.arg_names)
+            outs.append(mg.nlop.apply(ins)[0])
+        finally:
+            gpu.check(gpu.so.mdnn_set_option(b"conv_chlast", 0))
+            gpu.check(gpu.so.mdnn_set_option(b"conv_thin_tc", 1))
+    assert rel_l2(outs[0], outs[1]) <= CONV_TOL
+
+
 def test_conv_weights_init_bitwise(gpu, ref):
     in_dims = list(d16(8, 8, 4))
     mg = Model.conv_layer(gpu, "dw1", in_dims, (3, 3), 16)
