@@ -593,7 +593,8 @@ long conv_thin_epi_blocks(const ConvGeom& g, int mode)
     // replace (measured at C2: +2.4 ms vs -1.6 ms per two steps)
     if (!expand || F != 64 || mode != 0)
         return 0;
-    return ((g.X + TX - 1) / TX) * ((g.Y + 7) / 8) * g.B;
+    // allocation bound: the CUDA-core kernel's blocks or the tensor-core kernel's slots
+    return std::max(((g.X + TX - 1) / TX) * ((g.Y + 7) / 8) * g.B, thin_expand_tc_blocks());
 }
 
 // mode: 0 fwd, 1 bwd-data
@@ -618,7 +619,8 @@ void conv_thin_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvG
         *g.bnb_blocks = 0;
     if (eblocks > 0 && mode == 0 && g.stats && g.stats_blocks) {
         ep.stats = g.stats;
-        *g.stats_blocks = int(eblocks);
+        // blocks the CUDA-core expand writes (its grid); the tensor-core path resets this below
+        *g.stats_blocks = int(((g.X + TX - 1) / TX) * ((g.Y + 7) / 8) * g.B);
     }
     if (eblocks > 0 && mode == 1 && g.bnb && g.bnb_part && g.bnb_blocks && g.bnb->C == F
         && g.bnb->npix == g.X * g.Y * g.B) {
@@ -633,6 +635,16 @@ void conv_thin_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvG
     {
         // HBM-bound: algorithmic bytes = wide side once + thin side once
         ProfScope prof(mode == 0 ? "conv_thin_fwd" : "conv_thin_bwd_data", 8.0 * double(g.X) * g.Y * g.B * (F + 1));
+        int tc_blocks = 0;
+        if (expand && g.KX == 3
+            && thin_expand_tc(reinterpret_cast<float*>(outp), inp, U, g.X, g.Y, g.B, F, 9, ox, oy, ep.stats,
+                              &tc_blocks)) {
+            // tensor-core im2col GEMM (conv_thin_tc.cu); its statistics partials replace the CUDA-core ones
+            if (ep.stats && g.stats_blocks)
+                *g.stats_blocks = tc_blocks;
+            CUDA_CHECK(cudaFreeAsync(U, c.stream));
+            return;
+        }
         if (g.KX == 3)
             run_thin<3>(outp, inp, U, g, F, expand, ox, oy, ep);
         else

@@ -194,6 +194,221 @@ __global__ void __launch_bounds__(256) k_thin_gather(float2* __restrict__ out, c
     }
 }
 
+// ---------------------------------------------------------------------------
+// Thin -> wide (1 -> F = 64, 3x3; fwd of the first layer, bwd-data of the last)
+// in channel-major form: D^T[n = output (re|im) channel, 128][p = pixel, 256]
+// = Ue[n][k] x im2col[p][k], k = 2 t + (re|im) of thin[p + t - o] (18 used of
+// 32).  Four builder warps write the im2col rows (128 B, SWIZZLE_128B) for a
+// 256-pixel tile straight from the (L2-resident) thin image, the MMA warp
+// issues 4 UMMAs of 128 x 256 x 8 per tile, and 16 epilogue warps store
+// 128-B channel rows per pixel and accumulate the forward BN statistics
+// (same partial layout as the channel-major conv).  B tiles and TMEM
+// accumulators are double-buffered.
+constexpr int TE_P = 256;                 // pixels per tile (UMMA N)
+// split precision (3xTF32): K = 64 = [x_hi(18) | x_lo(18) | x_hi(18) | 0] against
+// [w_hi | w_hi | w_lo | 0], i.e. w_hi x_hi + w_hi x_lo + w_lo x_hi in one GEMM --
+// the first layer's output keeps fp32 accuracy (plain TF32 moved the MoDL
+// loss by 1e-3); two 128-B K chunks per row, each its own swizzled tile
+constexpr int TE_KCH = 2;
+constexpr int TE_BCH = TE_P * 128;          // one K chunk of the im2col tile: 32 KB
+constexpr int TE_BBYTES = TE_KCH * TE_BCH;  // 64 KB per buffer
+constexpr int TE_ACH = 128 * 128;           // one K chunk of the packed weights: 16 KB
+constexpr int TE_ABYTES = TE_KCH * TE_ACH;
+constexpr int TE_BUILD = 4, TE_EPI = 16;  // warps
+constexpr int TE_THREADS = 32 * (1 + TE_BUILD + TE_EPI);
+
+struct TeSmem {
+    static constexpr int B_OFF = 0;
+    static constexpr int A_OFF = 2 * TE_BBYTES;
+    static constexpr int BAR_OFF = A_OFF + TE_ABYTES;
+    // > half the SM's shared memory: one CTA per SM (it allocates all 512 TMEM columns)
+    static constexpr int TOTAL = (BAR_OFF + 256 + 1024) > 120 * 1024 ? (BAR_OFF + 256 + 1024) : 120 * 1024;
+};
+
+// Ue[c][n][32] (K chunk c of row n): n < 64: Re out_f = sum_t tr ur - ti ui ; n >= 64: Im = tr ui + ti ur;
+// K layout [w_hi(18) | w_hi(18) | w_lo(18) | 0]
+__global__ void k_pack_thin_expand(float* __restrict__ ue, const float2* __restrict__ U, int F, int KK)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 128 * 64; i += gridDim.x * blockDim.x) {
+        const int kk = i % 64, n = i / 64;
+        const int part = kk / 18, k = kk % 18;
+        const int t = k >> 1, comp = k & 1, f = n % F;
+        float v = 0.f;
+        if (part < 3 && t < KK) {
+            const float2 u = U[t * F + f];
+            const float w = n < F ? (comp ? -u.y : u.x) : (comp ? u.x : u.y);
+            const float hi = to_tf32(w);
+            v = part < 2 ? hi : to_tf32(w - hi);
+        }
+        ue[(size_t(kk >> 5) * 128 + n) * 32 + (kk & 31)] = v;
+    }
+}
+
+// byte offset of (row r, 16-B granule g) in a SWIZZLE_128B K-major tile (8-row atoms of 1024 B)
+__device__ __forceinline__ int sw128_off(int r, int g) { return (r >> 3) * 1024 + (r & 7) * 128 + ((g ^ (r & 7)) << 4); }
+
+__global__ void __launch_bounds__(TE_THREADS, 1)
+    k_thin_expand_tc(float* __restrict__ out, const float2* __restrict__ thin, const float* __restrict__ ue, int X,
+                     int Y, long npix, int ox, int oy, double* __restrict__ stats)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* bbuf = smem + TeSmem::B_OFF;
+    uint8_t* abuf = smem + TeSmem::A_OFF;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TeSmem::BAR_OFF);
+    uint64_t* b_full = bars;         // [2] builders -> MMA (128 arrivals)
+    uint64_t* b_empty = bars + 2;    // [2] MMA commit -> builders
+    uint64_t* tmem_full = bars + 4;  // [2]
+    uint64_t* tmem_empty = bars + 6; // [2] (32 * TE_EPI arrivals)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const long ntiles = (npix + TE_P - 1) / TE_P;
+
+    // packed weights (2 K chunks, 32 KB) into the swizzled A tiles; zero the im2col
+    // granules no builder writes (chunk 1, granules 6-7: k = 56..63) once
+    for (int e = threadIdx.x; e < TE_KCH * 128 * 8; e += TE_THREADS) {
+        const int c = e / (128 * 8), r = (e >> 3) % 128, g = e & 7;
+        *reinterpret_cast<float4*>(abuf + c * TE_ACH + sw128_off(r, g)) = reinterpret_cast<const float4*>(ue)[e];
+    }
+    for (int e = threadIdx.x; e < 2 * TE_P * 2; e += TE_THREADS) {
+        const int bb = e / (TE_P * 2), r = (e >> 1) % TE_P, g = 6 + (e & 1);
+        *reinterpret_cast<float4*>(bbuf + bb * TE_BBYTES + TE_BCH + sw128_off(r, g)) =
+            make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&b_full[i], 32 * TE_BUILD);
+            mbar_init(&b_empty[i], 1);
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 32 * TE_EPI);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0)
+        tmem_alloc<2 * TE_P>(tmem_slot);
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- MMA warp (elected lane issues) ----------------
+        constexpr uint32_t idesc = idesc_tf32(128, TE_P);
+        const uint64_t ad = umma_desc_sw128(smem_u32(abuf), 1024);
+        const uint64_t bd0 = umma_desc_sw128(smem_u32(bbuf), 1024);
+        uint32_t it = 0;
+        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const uint32_t st = it & 1, ph = (it >> 1) & 1;
+            mbar_wait(&tmem_empty[st], ph ^ 1);
+            mbar_wait(&b_full[st], ph);
+            tc_fence_after();
+            const uint64_t bd = bd0 + ((st * TE_BBYTES) >> 4);
+#pragma unroll
+            for (int c = 0; c < TE_KCH; c++)
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    mma_tf32_warp(tmem_base + st * TE_P, ad + ((c * TE_ACH + k * 32) >> 4),
+                                  bd + ((c * TE_BCH + k * 32) >> 4), idesc, (c | k) != 0);
+            mma_commit_warp(&b_empty[st]);
+            mma_commit_warp(&tmem_full[st]);
+        }
+    } else if (warp <= TE_BUILD) {
+        // ---------------- im2col builders: rows r = bt, bt + 128 of the tile ----------------
+        const int bt = threadIdx.x - 32;
+        uint32_t it = 0;
+        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const uint32_t st = it & 1, ph = (it >> 1) & 1;
+            mbar_wait(&b_empty[st], ph ^ 1);
+            uint8_t* tb = bbuf + st * TE_BBYTES;
+#pragma unroll
+            for (int rr = 0; rr < 2; rr++) {
+                const int r = bt + rr * 128;
+                const long p = tile * TE_P + r;
+                float v[20], lo[20];
+#pragma unroll
+                for (int q = 0; q < 20; q++)
+                    v[q] = lo[q] = 0.f;
+                if (p < npix) {
+                    const int x = int(p % X), y = int((p / X) % Y);
+                    const long b = p / (long(X) * Y);
+#pragma unroll
+                    for (int ty = 0; ty < 3; ty++)
+#pragma unroll
+                        for (int tx = 0; tx < 3; tx++) {
+                            const int hx = x + tx - ox, hy = y + ty - oy;
+                            if (hx >= 0 && hx < X && hy >= 0 && hy < Y) {
+                                const float2 tv = thin[(b * Y + hy) * X + hx];
+                                const int q = 2 * (tx + 3 * ty);
+                                v[q] = sm100::to_tf32(tv.x);
+                                v[q + 1] = sm100::to_tf32(tv.y);
+                                lo[q] = sm100::to_tf32(tv.x - v[q]);
+                                lo[q + 1] = sm100::to_tf32(tv.y - v[q + 1]);
+                            }
+                        }
+                }
+                // row k = [hi 0..17 | lo 18..35 | hi 36..53 | 0 54..63]
+                float row[56];
+#pragma unroll
+                for (int q = 0; q < 18; q++) {
+                    row[q] = v[q];
+                    row[18 + q] = lo[q];
+                    row[36 + q] = v[q];
+                }
+                row[54] = row[55] = 0.f;
+#pragma unroll
+                for (int g = 0; g < 14; g++)
+                    *reinterpret_cast<float4*>(tb + (g >> 3) * TE_BCH + sw128_off(r, g & 7)) =
+                        make_float4(row[4 * g], row[4 * g + 1], row[4 * g + 2], row[4 * g + 3]);
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&b_full[st]);
+        }
+    } else {
+        // ---------------- epilogue: TMEM lane = channel, column = pixel ----------------
+        const int ew = warp - 1 - TE_BUILD, lg = warp & 3, rep = ew >> 2, n = lg * 32 + lane;
+        double s_acc = 0, q_acc = 0;
+        uint32_t it = 0;
+        for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
+            const uint32_t st = it & 1, ph = (it >> 1) & 1;
+            mbar_wait(&tmem_full[st], ph);
+            tc_fence_after();
+            const uint32_t acc = tmem_base + st * TE_P + (uint32_t(lg * 32) << 16);
+#pragma unroll 1
+            for (int jc = rep; jc < TE_P / 16; jc += TE_EPI / 4) {
+                float v[16];
+                tmem_ld16(acc + jc * 16, v);
+                tmem_ld_wait();
+                const long p0 = tile * TE_P + jc * 16;
+                float fs = 0.f, fq = 0.f;
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    if (p0 + j < npix) {
+                        out[(p0 + j) * 128 + n] = v[j];
+                        fs += v[j];
+                        fq = fmaf(v[j], v[j], fq);
+                    }
+                }
+                s_acc += fs;
+                q_acc += fq;
+            }
+            tc_fence_before();
+            mbar_arrive(&tmem_empty[st]);
+        }
+        if (stats) {
+            const size_t slot = size_t(blockIdx.x) * (TE_EPI / 4) + rep;
+            stats[(slot * 128 + n) * 2] = s_acc;
+            stats[(slot * 128 + n) * 2 + 1] = q_acc;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<2 * TE_P>(tmem_base);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 tp_encode()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -228,6 +443,42 @@ bool g_thin_tc = true;
 } // namespace
 
 void conv_thin_tc_enable(bool on) { g_thin_tc = on; }
+
+long thin_expand_tc_blocks() { return long(ctx().sm_count) * (TE_EPI / 4); }
+
+bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, long Y, long B, int F, int KK, int ox,
+                    int oy, double* stats, int* stats_blocks)
+{
+    if (stats_blocks)
+        *stats_blocks = 0;
+    if (!g_thin_tc || F != 64 || KK != 9)
+        return false;
+    auto& c = ctx();
+    const long npix = X * Y * B;
+    float* ue;
+    CUDA_CHECK(cudaMallocAsync(&ue, sizeof(float) * 128 * 64, c.stream));
+    k_pack_thin_expand<<<32, 256, 0, c.stream>>>(ue, U, F, KK);
+    KERNEL_CHECK();
+    static std::mutex mu;
+    static std::map<int, bool> done;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done[c.device]) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_thin_expand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            TeSmem::TOTAL));
+            done[c.device] = true;
+        }
+    }
+    const long ntiles = (npix + TE_P - 1) / TE_P;
+    const int grid = int(std::min<long>(ntiles, c.sm_count));
+    k_thin_expand_tc<<<grid, TE_THREADS, TeSmem::TOTAL, c.stream>>>(out, thin, ue, int(X), int(Y), npix, ox, oy,
+                                                                    stats);
+    KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(ue, c.stream));
+    if (stats && stats_blocks)
+        *stats_blocks = grid * (TE_EPI / 4);
+    return true;
+}
 
 bool thin_reduce_tc(cfloat* out, const float* wide, const float2* U, long X, long Y, long B, int F, int KK, int ox,
                     int oy)

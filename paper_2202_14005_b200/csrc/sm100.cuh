@@ -323,5 +323,8 @@ __device__ __forceinline__ void mma_commit_warp(uint64_t* bar)
                  : "memory");
 }
 
+// generic-proxy shared-memory writes -> visible to the async proxy (UMMA operands)
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 } // namespace sm100
 } // namespace mdnn
