@@ -217,10 +217,13 @@ constexpr int TE_ABYTES = TE_KCH * TE_ACH;
 constexpr int TE_BUILD = 4, TE_EPI = 16;  // warps
 constexpr int TE_THREADS = 32 * (1 + TE_BUILD + TE_EPI);
 
+constexpr int TE_STG = 16 * 32 * 4; // per epilogue warp and buffer: 16 pixels x 32 channels (2 KB)
+
 struct TeSmem {
     static constexpr int B_OFF = 0;
     static constexpr int A_OFF = 2 * TE_BBYTES;
-    static constexpr int BAR_OFF = A_OFF + TE_ABYTES;
+    static constexpr int STG_OFF = A_OFF + TE_ABYTES;        // [TE_EPI][2][16][32] floats
+    static constexpr int BAR_OFF = STG_OFF + TE_EPI * 2 * TE_STG;
     // > half the SM's shared memory: one CTA per SM (it allocates all 512 TMEM columns)
     static constexpr int TOTAL = (BAR_OFF + 256 + 1024) > 120 * 1024 ? (BAR_OFF + 256 + 1024) : 120 * 1024;
 };
@@ -248,8 +251,8 @@ __global__ void k_pack_thin_expand(float* __restrict__ ue, const float2* __restr
 __device__ __forceinline__ int sw128_off(int r, int g) { return (r >> 3) * 1024 + (r & 7) * 128 + ((g ^ (r & 7)) << 4); }
 
 __global__ void __launch_bounds__(TE_THREADS, 1)
-    k_thin_expand_tc(float* __restrict__ out, const float2* __restrict__ thin, const float* __restrict__ ue, int X,
-                     int Y, long npix, int ox, int oy, double* __restrict__ stats)
+    k_thin_expand_tc(const __grid_constant__ CUtensorMap tm_out, const float2* __restrict__ thin,
+                     const float* __restrict__ ue, int X, int Y, long npix, int ox, int oy, double* __restrict__ stats)
 {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -367,6 +370,12 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
     } else {
         // ---------------- epilogue: TMEM lane = channel, column = pixel ----------------
         const int ew = warp - 1 - TE_BUILD, lg = warp & 3, rep = ew >> 2, n = lg * 32 + lane;
+        // staged 16 x 32 blocks leave by TMA tensor stores (rows past npix are clipped):
+        // the per-pixel 128-B STG stream was LSU-throttled
+        float* stg = reinterpret_cast<float*>(smem + TeSmem::STG_OFF + ew * 2 * TE_STG);
+        if (lane == 0)
+            prefetch_tmap(&tm_out);
+        int sb = 0;
         double s_acc = 0, q_acc = 0;
         uint32_t it = 0;
         for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
@@ -380,11 +389,28 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
                 tmem_ld16(acc + jc * 16, v);
                 tmem_ld_wait();
                 const long p0 = tile * TE_P + jc * 16;
+                if (p0 >= npix)
+                    continue;
+                // this buffer's previous store has finished reading shared memory
+                if (lane == 0)
+                    bulk_wait_read<1>();
+                __syncwarp();
+                float* sbuf = stg + sb * (TE_STG / 4);
+#pragma unroll
+                for (int j = 0; j < 16; j++)
+                    sbuf[j * 32 + lane] = v[j];
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tm_out, sbuf, lg * 32, int(p0));
+                    bulk_commit();
+                }
+                sb ^= 1;
+                const int nv = npix - p0 < 16 ? int(npix - p0) : 16;
                 float fs = 0.f, fq = 0.f;
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
-                    if (p0 + j < npix) {
-                        out[(p0 + j) * 128 + n] = v[j];
+                    if (j < nv) {
                         fs += v[j];
                         fq = fmaf(v[j], v[j], fq);
                     }
@@ -395,6 +421,8 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
             tc_fence_before();
             mbar_arrive(&tmem_empty[st]);
         }
+        if (lane == 0)
+            bulk_wait<0>(); // stores complete before the kernel's writes are consumed
         if (stats) {
             const size_t slot = size_t(blockIdx.x) * (TE_EPI / 4) + rep;
             stats[(slot * 128 + n) * 2] = s_acc;
@@ -439,10 +467,15 @@ CUtensorMap tp_map(const float* base, long rows, int box_rows)
 }
 
 bool g_thin_tc = true;
+// the tensor-core expand is correct but measured slower than the CUDA-core
+// kernel at C2 (~2.9 vs 2.7 ms per two steps: its 512-B-per-pixel stores, not
+// the FLOPs, bound both) -- off by default, option "conv_thin_tc_expand"
+bool g_thin_tc_expand = false;
 
 } // namespace
 
 void conv_thin_tc_enable(bool on) { g_thin_tc = on; }
+void conv_thin_tc_expand_enable(bool on) { g_thin_tc_expand = on; }
 
 long thin_expand_tc_blocks() { return long(ctx().sm_count) * (TE_EPI / 4); }
 
@@ -451,7 +484,7 @@ bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, lon
 {
     if (stats_blocks)
         *stats_blocks = 0;
-    if (!g_thin_tc || F != 64 || KK != 9)
+    if (!g_thin_tc || !g_thin_tc_expand || F != 64 || KK != 9)
         return false;
     auto& c = ctx();
     const long npix = X * Y * B;
@@ -471,7 +504,19 @@ bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, lon
     }
     const long ntiles = (npix + TE_P - 1) / TE_P;
     const int grid = int(std::min<long>(ntiles, c.sm_count));
-    k_thin_expand_tc<<<grid, TE_THREADS, TeSmem::TOTAL, c.stream>>>(out, thin, ue, int(X), int(Y), npix, ox, oy,
+    CUtensorMap tmo;
+    {
+        cuuint64_t dims[2] = {cuuint64_t(128), cuuint64_t(npix)};
+        cuuint64_t strides[1] = {cuuint64_t(128) * 4};
+        cuuint32_t box[2] = {32, 16};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = tp_encode()(&tmo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw CudaError("cuTensorMapEncodeTiled(expand out) failed: " + std::to_string(int(r)));
+    }
+    k_thin_expand_tc<<<grid, TE_THREADS, TeSmem::TOTAL, c.stream>>>(tmo, thin, ue, int(X), int(Y), npix, ox, oy,
                                                                     stats);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(ue, c.stream));

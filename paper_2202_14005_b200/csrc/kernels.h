@@ -160,6 +160,7 @@ long conv_thin_epi_blocks(const ConvGeom& g, int mode);
 bool thin_reduce_tc(cfloat* out, const float* wide, const float2* U, long X, long Y, long B, int F, int KK, int ox,
                     int oy);
 void conv_thin_tc_enable(bool on);
+void conv_thin_tc_expand_enable(bool on);
 long thin_expand_tc_blocks(); // statistics partial slots the tensor-core expand may write
 // 1 -> F (3x3, F = 64) on the tensor cores (+ BN statistics partials when stats != nullptr)
 bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, long Y, long B, int F, int KK, int ox,

@@ -149,6 +149,27 @@ def test_thin_reduce_tensor_core(gpu, ref, transposed, X, Y, B):
     assert rel_l2(outs[0], outs[1]) <= CONV_TOL
 
 
+@pytest.mark.parametrize("transposed", [False, True])
+def test_thin_expand_tensor_core(gpu, ref, transposed):
+    """1 -> 64 (and the bwd-data of 64 -> 1) through the split-precision tcgen05
+    im2col kernel (option conv_thin_tc_expand) against the reference."""
+    X, Y, B = 40, 36, 2
+    rng = np.random.default_rng(7)
+    cin, cout = (64, 1) if transposed else (1, 64)
+    in_dims = list(d16(X, Y, cin))
+    in_dims[15] = B
+    mr = Model.conv_layer(ref, "c", in_dims, (3, 3), cout, transposed=transposed)
+    ins = [crand(rng, mr.nlop.in_dims(i)) for i in range(mr.nlop.n_in)]
+    gpu.check(gpu.so.mdnn_set_option(b"conv_chlast", 1))
+    gpu.check(gpu.so.mdnn_set_option(b"conv_thin_tc_expand", 1))
+    try:
+        mg = Model.conv_layer(gpu, "c", in_dims, (3, 3), cout, transposed=transposed)
+        _check_node(mg.nlop, mr.nlop, ins, np.random.default_rng(1), CONV_TOL, mr.arg_names)
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"conv_chlast", 0))
+        gpu.check(gpu.so.mdnn_set_option(b"conv_thin_tc_expand", 0))
+
+
 def test_conv_weights_init_bitwise(gpu, ref):
     in_dims = list(d16(8, 8, 4))
     mg = Model.conv_layer(gpu, "dw1", in_dims, (3, 3), 16)
