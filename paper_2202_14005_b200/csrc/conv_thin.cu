@@ -383,7 +383,9 @@ __global__ void __launch_bounds__(NT, K == 3 ? 2 : 1) k_thin_reduce(float2* __re
 //   else (F -> 1 layer, g = dy thin, h = x wide), substituting p' = p + t - c0:
 //       acc[t] += g[p' - t + c0] conj(h[p', c]), window over g with offset K-1-c0
 //       and flipped tap index.
-template<int K, bool WIDE_IS_G>
+// P channels per thread (P = 2: 8-byte channel-pair loads, the window loads and
+// the loop overhead shared by two channels -- as in k_thin_expand)
+template<int K, bool WIDE_IS_G, int P>
 __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, const float* __restrict__ wide,
                                                    const float2* __restrict__ thin, int X, int Y, int B, int F,
                                                    int ox, int oy)
@@ -394,12 +396,15 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
     const long XY = long(X) * Y;
     const int ntx = (X + TX - 1) / TX, nty = (Y + TY - 1) / TY;
     const long ntiles = long(ntx) * nty * B;
-    const int f = threadIdx.x % F, lane = threadIdx.x / F, lanes = NT / F;
+    const int FP = F / P;
+    const int f = (threadIdx.x % FP) * P, lane = threadIdx.x / FP, lanes = NT / FP;
     const int nseg = max(1, lanes / TY), seglen = TX / nseg;
-    float2 acc[KK];
+    float2 acc[P][KK];
 #pragma unroll
-    for (int t = 0; t < KK; t++)
-        acc[t] = float2{0.f, 0.f};
+    for (int q = 0; q < P; q++)
+#pragma unroll
+        for (int t = 0; t < KK; t++)
+            acc[q][t] = float2{0.f, 0.f};
     for (long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
         const int x0 = int(tl % ntx) * TX, y0 = int((tl / ntx) % nty) * TY;
         const long b = tl / (long(ntx) * nty);
@@ -422,44 +427,75 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
             // of loads in flight ahead of the taps
             constexpr int PD = 4;
             const float* wp = wide + (b * XY + long(X) * gy + x0 + xs) * 2 * F + f;
-            float2 pre[PD];
+            // pre[d][q] = (Re, Im) of channel f + q at pixel i + d
+            float2 pre[PD][P];
+            auto ldpix = [&](const float* ptr, float2 (&o)[P]) {
+                if constexpr (P == 2) {
+                    const float2 re = __ldg(reinterpret_cast<const float2*>(ptr));
+                    const float2 im = __ldg(reinterpret_cast<const float2*>(ptr + F));
+                    o[0] = float2{re.x, im.x};
+                    o[1] = float2{re.y, im.y};
+                } else {
+                    o[0] = float2{__ldg(ptr), __ldg(ptr + F)};
+                }
+            };
 #pragma unroll
-            for (int d = 0; d < PD; d++)
-                pre[d] = d < xend ? float2{__ldg(wp + d * 2 * F), __ldg(wp + d * 2 * F + F)} : float2{0.f, 0.f};
+            for (int d = 0; d < PD; d++) {
+                if (d < xend)
+                    ldpix(wp + d * 2 * F, pre[d]);
+                else
+#pragma unroll
+                    for (int q = 0; q < P; q++)
+                        pre[d][q] = float2{0.f, 0.f};
+            }
             wp += PD * 2 * F;
 #pragma unroll 8
             for (int i = 0; i < xend; i++) {
                 const int px = xs + i;
-                const float2 v = pre[0];
+                float2 vv[P];
+#pragma unroll
+                for (int q = 0; q < P; q++)
+                    vv[q] = pre[0][q];
 #pragma unroll
                 for (int d = 0; d < PD - 1; d++)
-                    pre[d] = pre[d + 1];
-                pre[PD - 1] = i + PD < xend ? float2{__ldg(wp), __ldg(wp + F)} : float2{0.f, 0.f};
+#pragma unroll
+                    for (int q = 0; q < P; q++)
+                        pre[d][q] = pre[d + 1][q];
+                if (i + PD < xend)
+                    ldpix(wp, pre[PD - 1]);
+                else
+#pragma unroll
+                    for (int q = 0; q < P; q++)
+                        pre[PD - 1][q] = float2{0.f, 0.f};
                 wp += 2 * F;
 #pragma unroll
                 for (int ky = 0; ky < K; ky++)
                     win[ky][K - 1] = tile[(row + ky) * HX + px + K - 1];
 #pragma unroll
-                for (int ky = 0; ky < K; ky++)
+                for (int q = 0; q < P; q++) {
+                    const float2 v = vv[q];
 #pragma unroll
-                    for (int kx = 0; kx < K; kx++) {
-                        const float2 s = win[ky][kx];
-                        if (WIDE_IS_G) {
-                            // v * conj(s)
-                            float2& a_ = acc[kx + K * ky];
-                            a_.x = fmaf(v.x, s.x, a_.x);
-                            a_.y = fmaf(v.y, s.x, a_.y);
-                            a_.x = fmaf(v.y, s.y, a_.x);
-                            a_.y = fmaf(-v.x, s.y, a_.y);
-                        } else {
-                            // s * conj(v)
-                            float2& a_ = acc[(K - 1 - kx) + K * (K - 1 - ky)];
-                            a_.x = fmaf(s.x, v.x, a_.x);
-                            a_.y = fmaf(s.y, v.x, a_.y);
-                            a_.x = fmaf(s.y, v.y, a_.x);
-                            a_.y = fmaf(-s.x, v.y, a_.y);
+                    for (int ky = 0; ky < K; ky++)
+#pragma unroll
+                        for (int kx = 0; kx < K; kx++) {
+                            const float2 s = win[ky][kx];
+                            if (WIDE_IS_G) {
+                                // v * conj(s)
+                                float2& a_ = acc[q][kx + K * ky];
+                                a_.x = fmaf(v.x, s.x, a_.x);
+                                a_.y = fmaf(v.y, s.x, a_.y);
+                                a_.x = fmaf(v.y, s.y, a_.x);
+                                a_.y = fmaf(-v.x, s.y, a_.y);
+                            } else {
+                                // s * conj(v)
+                                float2& a_ = acc[q][(K - 1 - kx) + K * (K - 1 - ky)];
+                                a_.x = fmaf(s.x, v.x, a_.x);
+                                a_.y = fmaf(s.y, v.x, a_.y);
+                                a_.x = fmaf(s.y, v.y, a_.x);
+                                a_.y = fmaf(-s.x, v.y, a_.y);
+                            }
                         }
-                    }
+                }
 #pragma unroll
                 for (int ky = 0; ky < K; ky++)
 #pragma unroll
@@ -470,8 +506,10 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
     }
     // fold the lanes of each channel in a fixed order
 #pragma unroll
-    for (int t = 0; t < KK; t++)
-        sred[(lane * KK + t) * F + f] = acc[t];
+    for (int q = 0; q < P; q++)
+#pragma unroll
+        for (int t = 0; t < KK; t++)
+            sred[(lane * KK + t) * F + f + q] = acc[q][t];
     __syncthreads();
     for (int e = threadIdx.x; e < KK * F; e += NT) {
         float2 s{0.f, 0.f};
@@ -553,14 +591,16 @@ template<int K>
 void run_thin_wgrad(float2* part, int nblk, const cfloat* x, const cfloat* dy, const ConvGeom& g, int F, bool one_in)
 {
     auto& c = ctx();
-    const size_t smem = sizeof(float2) * NT * K * K;
+    // sred holds lanes x KK x F: lanes = NT / (F / P)
+    const bool pair = F % 2 == 0 && NT % (F / 2) == 0;
+    const size_t smem = sizeof(float2) * (pair ? 2 : 1) * NT * K * K;
     if (one_in) { // g = dy wide, h = x thin, window offset c0
-        auto kern = k_thin_wgrad<K, true>;
+        auto kern = pair ? k_thin_wgrad<K, true, 2> : k_thin_wgrad<K, true, 1>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
         kern<<<nblk, NT, smem, c.stream>>>(part, reinterpret_cast<const float*>(dy), x, int(g.X), int(g.Y), int(g.B),
                                            F, int(g.px), int(g.py));
     } else { // g = dy thin, h = x wide, window offset K-1-c0
-        auto kern = k_thin_wgrad<K, false>;
+        auto kern = pair ? k_thin_wgrad<K, false, 2> : k_thin_wgrad<K, false, 1>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
         kern<<<nblk, NT, smem, c.stream>>>(part, reinterpret_cast<const float*>(x), dy, int(g.X), int(g.Y), int(g.B),
                                            F, int(K - 1 - g.px), int(K - 1 - g.py));
