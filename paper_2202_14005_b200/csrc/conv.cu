@@ -76,9 +76,11 @@ __global__ void k_imag_any(const float2* __restrict__ a, long n, unsigned* flag)
 // channels Cout, weights conj(w[t,c,f]) flipped, output channel c)
 template<int MODE, int FG>
 __global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const cfloat* __restrict__ w, ConvGeom g,
-                                                        const unsigned* __restrict__ imag_flag)
+                                                        const unsigned* __restrict__ imag_flag, int skip_real)
 {
     const bool real = imag_flag && *imag_flag == 0;
+    if (real && skip_real)
+        return; // real operands: k_conv_direct_real computed this launch
     __shared__ float2 tile[TY + MAXK - 1][TX + MAXK - 1];
     __shared__ float2 wsh[MAXK * MAXK][FG];
     // real parts of the taps' weights, FG contiguous floats per tap (16-B aligned rows):
@@ -177,6 +179,115 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const c
         for (int f = 0; f < FG; f++)
             if (f0 + f < nout)
                 out.st(b, px + g.X * py, f0 + f, acc[f]);
+}
+
+// Real-operand path (VarNet: real images and real-valued weights stored complex)
+// register-blocked along x: a thread owns RPX consecutive output pixels and FG
+// output channels; per (channel, kernel row) it loads a window of RPX + KX - 1
+// real inputs once and slides over the KX taps with float4 weight rows, so a
+// tap costs (RPX + FG/4 + ...)/(RPX * FG) loads per FMA instead of ~1.
+// Launched alongside k_conv_direct; exactly one of the two does the work
+// (device-side imaginary-part flag, no host synchronisation).
+constexpr int RPX = 4, RTX = 16, RTY = 16; // 64 x 16 output pixels per block, 256 threads
+
+template<int MODE, int FG>
+__global__ void __launch_bounds__(RTX* RTY) k_conv_direct_real(Out out, Acc in, const cfloat* __restrict__ w,
+                                                              ConvGeom g, const unsigned* __restrict__ imag_flag)
+{
+    if (*imag_flag != 0)
+        return; // complex operands: k_conv_direct computes this launch
+    constexpr int OX = RTX * RPX, OY = RTY;
+    __shared__ float tile[OY + MAXK - 1][OX + MAXK - 1];
+    __shared__ __align__(16) float wre[MAXK * MAXK][FG];
+    const long nin = MODE == 0 ? g.Cin : g.Cout;
+    const long nout = MODE == 0 ? g.Cout : g.Cin;
+    const long ngrp = (nout + FG - 1) / FG;
+    const long b = blockIdx.z / ngrp;
+    const long f0 = (blockIdx.z % ngrp) * FG;
+    const long x0 = long(blockIdx.x) * OX, y0 = long(blockIdx.y) * OY;
+    const int KX = int(g.KX), KY = int(g.KY);
+    const long ox = MODE == 0 ? g.px : (g.KX - 1 - g.px);
+    const long oy = MODE == 0 ? g.py : (g.KY - 1 - g.py);
+    const int tx = threadIdx.x % RTX, ty = threadIdx.x / RTX;
+    float acc[RPX][FG];
+#pragma unroll
+    for (int p = 0; p < RPX; p++)
+#pragma unroll
+        for (int f = 0; f < FG; f++)
+            acc[p][f] = 0.f;
+    const int HX = OX + KX - 1, HY = OY + KY - 1;
+    for (long c = 0; c < nin; c++) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < HX * HY; e += blockDim.x) {
+            const int hx = e % HX, hy = e / HX;
+            const long gx = x0 + hx - ox, gy = y0 + hy - oy;
+            tile[hy][hx] = (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? in.ld(b, gx + g.X * gy, c).x : 0.f;
+        }
+        for (int e = threadIdx.x; e < KX * KY * FG; e += blockDim.x) {
+            const int t = e % (KX * KY), f = e / (KX * KY);
+            const long fo = f0 + f;
+            float v = 0.f;
+            if (fo < nout) {
+                if (MODE == 0) {
+                    v = w[t + g.KX * g.KY * (c + g.Cin * fo)].x;
+                } else {
+                    const int tpx = t % KX, tpy = t / KX;
+                    const long tt = (KX - 1 - tpx) + g.KX * (KY - 1 - tpy);
+                    v = w[tt + g.KX * g.KY * (fo + g.Cin * c)].x; // conj: real part unchanged
+                }
+            }
+            wre[t][f] = v;
+        }
+        __syncthreads();
+        for (int ky = 0; ky < KY; ky++) {
+            float win[RPX + MAXK - 1];
+            const float* trow = &tile[ty + ky][tx * RPX];
+#pragma unroll
+            for (int q = 0; q < RPX + MAXK - 1; q++)
+                win[q] = q < RPX + KX - 1 ? trow[q] : 0.f;
+#pragma unroll
+            for (int kx = 0; kx < MAXK; kx++) {
+                if (kx >= KX)
+                    break;
+                const int t = kx + KX * ky;
+                float wv[FG];
+                if constexpr (FG % 4 == 0) {
+#pragma unroll
+                    for (int f = 0; f < FG; f += 4) {
+                        const float4 q4 = *reinterpret_cast<const float4*>(&wre[t][f]);
+                        wv[f] = q4.x;
+                        wv[f + 1] = q4.y;
+                        wv[f + 2] = q4.z;
+                        wv[f + 3] = q4.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int f = 0; f < FG; f += 2) {
+                        const float2 q2 = *reinterpret_cast<const float2*>(&wre[t][f]);
+                        wv[f] = q2.x;
+                        wv[f + 1] = q2.y;
+                    }
+                }
+#pragma unroll
+                for (int p = 0; p < RPX; p++)
+#pragma unroll
+                    for (int f = 0; f < FG; f++)
+                        acc[p][f] = fmaf(win[p + kx], wv[f], acc[p][f]);
+            }
+        }
+    }
+    const long py = y0 + ty;
+    if (py >= g.Y)
+        return;
+#pragma unroll
+    for (int p = 0; p < RPX; p++) {
+        const long px = x0 + tx * RPX + p;
+        if (px < g.X)
+#pragma unroll
+            for (int f = 0; f < FG; f++)
+                if (f0 + f < nout)
+                    out.st(b, px + g.X * py, f0 + f, float2{acc[p][f], 0.f});
+    }
 }
 
 // bwd-weight: block = (c-group x f-group, split); loops over its share of
@@ -405,12 +516,23 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
     const long XY = g.X * g.Y;
     ProfScope prof("conv_fwd", conv_flops(g));
     unsigned* fl = imag_flag({{x, XY * g.Cin * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
+    {
+        dim3 rgrid(unsigned((g.X + RTX * RPX - 1) / (RTX * RPX)), unsigned((g.Y + RTY - 1) / RTY),
+                   unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
+        if (FGv == 2)
+            k_conv_direct_real<0, 2><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+                                                                          Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
+        else
+            k_conv_direct_real<0, 8><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+                                                                          Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
+        KERNEL_CHECK();
+    }
     if (FGv == 2)
         k_conv_direct<0, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
-                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
+                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl, 1);
     else
         k_conv_direct<0, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
-                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
+                                                                Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl, 1);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
 }
@@ -432,12 +554,23 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
     const long XY = g.X * g.Y;
     ProfScope prof("conv_bwd_data", conv_flops(g));
     unsigned* fl = imag_flag({{dy, XY * g.Cout * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
+    {
+        dim3 rgrid(unsigned((g.X + RTX * RPX - 1) / (RTX * RPX)), unsigned((g.Y + RTY - 1) / RTY),
+                   unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
+        if (FGv == 2)
+            k_conv_direct_real<1, 2><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+                                                                          Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
+        else
+            k_conv_direct_real<1, 8><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+                                                                          Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
+        KERNEL_CHECK();
+    }
     if (FGv == 2)
         k_conv_direct<1, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
-                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
+                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl, 1);
     else
         k_conv_direct<1, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
-                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
+                                                                Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl, 1);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
 }
