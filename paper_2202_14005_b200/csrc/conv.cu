@@ -366,7 +366,9 @@ __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, A
 // pixel row (1 dy + 1 x smem load per K complex MACs).  Block = all
 // (ky, c, f) combos (K * Cin * Cout <= 576 threads: the VarNet 2 <-> 24
 // 11x11 layers); grid = pixel-tile splits, partials folded by k_sum_splits.
-template<int K>
+// FP output channels per thread share the sliding x window (FP = 2: 3 loads per
+// 2K real FMAs instead of 2 per K)
+template<int K, int FP>
 __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part, Acc x, Acc dy, ConvGeom g,
                                                         int nsplit, const unsigned* __restrict__ imag_flag)
 {
@@ -376,16 +378,18 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
     const int Cin = int(g.Cin), Cout = int(g.Cout);
     float2* xt = wsm;                          // [Cin][HY][HX]
     float2* dyt = wsm + Cin * HY * HX;         // [Cout][WTY][WTX]
-    const int nthr = K * Cin * Cout;
+    const int nthr = K * Cin * (Cout / FP);
     const int tid = threadIdx.x;
-    const int ky = tid % K, c = (tid / K) % Cin, f = tid / (K * Cin);
+    const int ky = tid % K, c = (tid / K) % Cin, f = (tid / (K * Cin)) * FP;
     const bool act = tid < nthr;
     const long ntx = (g.X + WTX - 1) / WTX, nty = (g.Y + WTY - 1) / WTY;
     const long ntiles = ntx * nty * g.B;
-    float2 acc[K];
+    float2 acc[FP][K];
 #pragma unroll
-    for (int k = 0; k < K; k++)
-        acc[k] = float2{0.f, 0.f};
+    for (int q = 0; q < FP; q++)
+#pragma unroll
+        for (int k = 0; k < K; k++)
+            acc[q][k] = float2{0.f, 0.f};
     for (long tile = blockIdx.x; tile < ntiles; tile += nsplit) {
         const long b = tile / (ntx * nty);
         const long tr = tile % (ntx * nty);
@@ -415,10 +419,13 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
 #pragma unroll 4
                 for (int px = 0; px < WTX; px++) {
                     win[K - 1] = xr[px + K - 1];
-                    const float d = dr[px].x;
 #pragma unroll
-                    for (int kx = 0; kx < K; kx++)
-                        acc[kx].x = fmaf(d, win[kx].x, acc[kx].x);
+                    for (int q = 0; q < FP; q++) {
+                        const float d = dr[q * WTY * WTX + px].x;
+#pragma unroll
+                        for (int kx = 0; kx < K; kx++)
+                            acc[q][kx].x = fmaf(d, win[kx].x, acc[q][kx].x);
+                    }
 #pragma unroll
                     for (int k = 0; k < K - 1; k++)
                         win[k] = win[k + 1];
@@ -427,13 +434,16 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
 #pragma unroll 4
                 for (int px = 0; px < WTX; px++) {
                     win[K - 1] = xr[px + K - 1];
-                    const float2 d = dr[px];
 #pragma unroll
-                    for (int kx = 0; kx < K; kx++) { // acc[kx] += d * conj(x[px + kx])
-                        acc[kx].x = fmaf(d.x, win[kx].x, acc[kx].x);
-                        acc[kx].y = fmaf(d.y, win[kx].x, acc[kx].y);
-                        acc[kx].x = fmaf(d.y, win[kx].y, acc[kx].x);
-                        acc[kx].y = fmaf(-d.x, win[kx].y, acc[kx].y);
+                    for (int q = 0; q < FP; q++) {
+                        const float2 d = dr[q * WTY * WTX + px];
+#pragma unroll
+                        for (int kx = 0; kx < K; kx++) { // acc[kx] += d * conj(x[px + kx])
+                            acc[q][kx].x = fmaf(d.x, win[kx].x, acc[q][kx].x);
+                            acc[q][kx].y = fmaf(d.y, win[kx].x, acc[q][kx].y);
+                            acc[q][kx].x = fmaf(d.y, win[kx].y, acc[q][kx].x);
+                            acc[q][kx].y = fmaf(-d.x, win[kx].y, acc[q][kx].y);
+                        }
                     }
 #pragma unroll
                     for (int k = 0; k < K - 1; k++)
@@ -445,8 +455,11 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
     if (act) {
         const long KK = long(K) * K;
 #pragma unroll
-        for (int kx = 0; kx < K; kx++)
-            part[size_t(blockIdx.x) * KK * Cin * Cout + (kx + K * ky) + KK * (c + long(Cin) * f)] = acc[kx];
+        for (int q = 0; q < FP; q++)
+#pragma unroll
+            for (int kx = 0; kx < K; kx++)
+                part[size_t(blockIdx.x) * KK * Cin * Cout + (kx + K * ky) + KK * (c + long(Cin) * (f + q))] =
+                    acc[q][kx];
     }
 }
 
@@ -598,9 +611,10 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
         float2* part;
         CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
         ProfScope prof("conv_bwd_weight", conv_flops(g));
-        auto kern = k_conv_wgrad_rb<11>;
+        const bool fp2 = g.Cout % 2 == 0;
+        auto kern = fp2 ? k_conv_wgrad_rb<11, 2> : k_conv_wgrad_rb<11, 1>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
-        const int nthr = int(((11 * g.Cin * g.Cout + 31) / 32) * 32);
+        const int nthr = int(((11 * g.Cin * (fp2 ? g.Cout / 2 : g.Cout) + 31) / 32) * 32);
         unsigned* fl = imag_flag({{x, XY * g.Cin * g.B}, {dy, XY * g.Cout * g.B}});
         kern<<<nsplit, nthr, smem, c.stream>>>(part, Acc{x, g.Cin, XY, g.in_chlast}, Acc{dy, g.Cout, XY, g.out_chlast},
                                               g, nsplit, fl);
