@@ -19,38 +19,62 @@ int grid_for(long n)
     return int(std::max(1L, std::min(blocks, long(ctx().sm_count) * 8)));
 }
 
-__device__ __forceinline__ float gauss(float z, float mu, float sigma)
+// exp(-(z - mu)^2 / (2 sigma^2)) as exp2(-(z - mu)^2 * k2), k2 = log2(e) / (2 sigma^2):
+// no division, one MUFU.EX2 (the per-basis division + expf dominated the kernel)
+__device__ __forceinline__ float gauss2(float z, float mu, float k2)
 {
-    float d = (z - mu) / sigma;
-    return expf(-d * d / 2.f);
+    const float d = z - mu;
+    return exp2f(-(d * d) * k2);
 }
 
 // mode 0: y = phi(z); 1: dz = Re(g) * phi'(z) (adjoint, also tangent with g = dx);
-// 2: y = sum_j Re(dw) e_j (tangent wrt w)
+// 2: y = sum_j Re(dw) e_j (tangent wrt w).  The filter's weights and the centres
+// are staged in shared memory; the element loop walks (inner, filter, outer)
+// incrementally (no 64-bit division per element).
 __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z, const cfloat* __restrict__ w,
                           const cfloat* __restrict__ gin, const float* __restrict__ mu, RbfGeom g, int mode)
 {
     __shared__ float smu[kMaxW];
+    extern __shared__ float sw[]; // [nf][nw] real parts
     for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
         smu[j] = mu[j];
+    for (long e = threadIdx.x; e < g.nf * g.nw; e += blockDim.x) {
+        const long f = e / g.nw, j = e % g.nw;
+        sw[e] = w[f + j * g.nf].x;
+    }
     __syncthreads();
     const long n = g.inner * g.nf * g.outer;
     const float s2 = g.sigma * g.sigma;
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-        const long f = (i / g.inner) % g.nf;
+    const float inv_s2 = 1.f / s2;
+    const float k2 = 1.4426950408889634f / (2.f * s2);
+    const long stride = long(gridDim.x) * blockDim.x;
+    long i = blockIdx.x * long(blockDim.x) + threadIdx.x;
+    long f = (i / g.inner) % g.nf;
+    long rem = i % g.inner;
+    const long df = (stride / g.inner) % g.nf, drem = stride % g.inner;
+    for (; i < n; i += stride) {
         const float zk = z[i].x;
+        const float* wf = sw + f * g.nw;
         float acc = 0.f;
         for (int j = 0; j < g.nw; j++) {
-            const float e = gauss(zk, smu[j], g.sigma);
-            const float wj = w[f + j * g.nf].x;
+            const float e = gauss2(zk, smu[j], k2);
             if (mode == 1)
-                acc += wj * e * (-(zk - smu[j]) / s2);
+                acc = fmaf(wf[j] * e, -(zk - smu[j]) * inv_s2, acc);
             else
-                acc += wj * e;
+                acc = fmaf(wf[j], e, acc);
         }
         if (mode == 1)
             acc *= gin[i].x;
         out[i] = float2{acc, 0.f};
+        // advance (rem, f) by stride elements
+        rem += drem;
+        f += df;
+        if (rem >= g.inner) {
+            rem -= g.inner;
+            f++;
+        }
+        if (f >= g.nf)
+            f -= g.nf;
     }
 }
 
@@ -67,19 +91,21 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
     const long f = blockIdx.y;
     const long total = g.inner * g.outer;
     const long begin = long(blockIdx.x) * kChunk, end = min(total, begin + kChunk);
-    double acc[kMaxW];
+    // fp32 running sums per thread (kChunk / blockDim = 32 terms each), folded in double
+    float acc[kMaxW];
     for (int j = 0; j < g.nw; j++)
-        acc[j] = 0;
+        acc[j] = 0.f;
+    const float k2 = 1.4426950408889634f / (2.f * g.sigma * g.sigma);
     for (long t = begin + threadIdx.x; t < end; t += blockDim.x) {
         const long ii = t % g.inner, o = t / g.inner;
         const long idx = ii + g.inner * (f + g.nf * o);
         const float zk = z[idx].x, gv = dy[idx].x;
         for (int j = 0; j < g.nw; j++)
-            acc[j] += double(gauss(zk, smu[j], g.sigma) * gv);
+            acc[j] = fmaf(gauss2(zk, smu[j], k2), gv, acc[j]);
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = 0; j < g.nw; j++) {
-        double v = acc[j];
+        double v = double(acc[j]);
         for (int o2 = 16; o2 > 0; o2 >>= 1)
             v += __shfl_xor_sync(0xffffffffu, v, o2);
         if (lane == 0)
@@ -112,25 +138,25 @@ void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, c
 {
     if (g.nw > kMaxW)
         throw ConfigError("rbf: more than 64 basis functions not supported on device");
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(y, z, w, nullptr, mu, g, 0);
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(y, z, w, nullptr, mu, g, 0);
     KERNEL_CHECK();
 }
 
 void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
 {
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(dz, z, w, dy, mu, g, 1);
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(dz, z, w, dy, mu, g, 1);
     KERNEL_CHECK();
 }
 
 void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
 {
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(dy, z, w, dz, mu, g, 1);
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(dy, z, w, dz, mu, g, 1);
     KERNEL_CHECK();
 }
 
 void rbf_deriv_w(cfloat* dy, const cfloat* dw, const cfloat* z, const float* mu, const RbfGeom& g)
 {
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, 0, ctx().stream>>>(dy, z, dw, nullptr, mu, g, 2);
+    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(dy, z, dw, nullptr, mu, g, 2);
     KERNEL_CHECK();
 }
 
