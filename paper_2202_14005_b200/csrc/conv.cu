@@ -188,9 +188,12 @@ __global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const c
 // tap costs (RPX + FG/4 + ...)/(RPX * FG) loads per FMA instead of ~1.
 // Launched alongside k_conv_direct; exactly one of the two does the work
 // (device-side imaginary-part flag, no host synchronisation).
-constexpr int RPX = 4, RTX = 16, RTY = 16; // 64 x 16 output pixels per block, 256 threads
+constexpr int RTX = 16, RTY = 16; // 16 x 16 threads; RPX x 16 pixels... per block: (16 RPX) x 16 outputs
+// RPX pixels per thread (8 for FG = 2 measured no faster than 4)
+template<int FG>
+constexpr int rpx_for() { return 4; }
 
-template<int MODE, int FG>
+template<int MODE, int FG, int RPX = rpx_for<FG>()>
 __global__ void __launch_bounds__(RTX* RTY) k_conv_direct_real(Out out, Acc in, const cfloat* __restrict__ w,
                                                               ConvGeom g, const unsigned* __restrict__ imag_flag)
 {
@@ -463,15 +466,32 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
     }
 }
 
-__global__ void k_sum_splits(cfloat* out, const float2* part, long n, int nsplit)
+// out[i] = sum_s part[s][i]: block = 64 outputs x 4 split groups (group g sums
+// splits g, g + 4, ... in order; the groups are added in order): the serial
+// per-output loop over ~300 splits was latency-bound
+__global__ void __launch_bounds__(256) k_sum_splits(cfloat* out, const float2* part, long n, int nsplit)
 {
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-        double ar = 0, ai = 0;
-        for (int s = 0; s < nsplit; s++) {
-            ar += part[size_t(s) * n + i].x;
-            ai += part[size_t(s) * n + i].y;
+    __shared__ double2 red[4][64];
+    const int o = threadIdx.x & 63, gq = threadIdx.x >> 6;
+    const long i = long(blockIdx.x) * 64 + o;
+    double ar = 0, ai = 0;
+    if (i < n) {
+#pragma unroll 4
+        for (int s = gq; s < nsplit; s += 4) {
+            const float2 v = part[size_t(s) * n + i];
+            ar += v.x;
+            ai += v.y;
         }
-        out[i] = float2{float(ar), float(ai)};
+    }
+    red[gq][o] = double2{ar, ai};
+    __syncthreads();
+    if (gq == 0 && i < n) {
+        double2 r = red[0][o];
+        for (int k = 1; k < 4; k++) {
+            r.x += red[k][o].x;
+            r.y += red[k][o].y;
+        }
+        out[i] = float2{float(r.x), float(r.y)};
     }
 }
 
@@ -530,7 +550,8 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
     ProfScope prof("conv_fwd", conv_flops(g));
     unsigned* fl = imag_flag({{x, XY * g.Cin * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
     {
-        dim3 rgrid(unsigned((g.X + RTX * RPX - 1) / (RTX * RPX)), unsigned((g.Y + RTY - 1) / RTY),
+        const int RP = FGv == 2 ? rpx_for<2>() : rpx_for<8>();
+        dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
                    unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
         if (FGv == 2)
             k_conv_direct_real<0, 2><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
@@ -568,7 +589,8 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
     ProfScope prof("conv_bwd_data", conv_flops(g));
     unsigned* fl = imag_flag({{dy, XY * g.Cout * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
     {
-        dim3 rgrid(unsigned((g.X + RTX * RPX - 1) / (RTX * RPX)), unsigned((g.Y + RTY - 1) / RTY),
+        const int RP = FGv == 2 ? rpx_for<2>() : rpx_for<8>();
+        dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
                    unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
         if (FGv == 2)
             k_conv_direct_real<1, 2><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
@@ -620,7 +642,7 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
                                               g, nsplit, fl);
         KERNEL_CHECK();
         CUDA_CHECK(cudaFreeAsync(fl, c.stream));
-        k_sum_splits<<<int(std::min(1024L, (n + 255) / 256)), 256, 0, c.stream>>>(dw, part, n, nsplit);
+        k_sum_splits<<<int((n + 63) / 64), 256, 0, c.stream>>>(dw, part, n, nsplit);
         KERNEL_CHECK();
         CUDA_CHECK(cudaFreeAsync(part, c.stream));
         return;
@@ -646,7 +668,7 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     else
         k_conv_wgrad<1, 8><<<grid, 256, 0, c.stream>>>(part, ax, ad, g, nsplit);
     KERNEL_CHECK();
-    k_sum_splits<<<int(std::min(1024L, (n + 255) / 256)), 256, 0, c.stream>>>(dw, part, n, nsplit);
+    k_sum_splits<<<int((n + 63) / 64), 256, 0, c.stream>>>(dw, part, n, nsplit);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
