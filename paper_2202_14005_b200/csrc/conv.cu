@@ -548,7 +548,8 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
               unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
     ProfScope prof("conv_fwd", conv_flops(g));
-    unsigned* fl = imag_flag({{x, XY * g.Cin * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
+    const bool known = (g.real_known & 3) == 3;
+    unsigned* fl = known ? ctx().d_zero : imag_flag({{x, XY * g.Cin * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
     {
         const int RP = FGv == 2 ? rpx_for<2>() : rpx_for<8>();
         dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
@@ -568,7 +569,8 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
         k_conv_direct<0, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
                                                                 Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl, 1);
     KERNEL_CHECK();
-    CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
+    if (!known)
+        CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
 }
 
 void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom& g)
@@ -587,7 +589,8 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
               unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
     ProfScope prof("conv_bwd_data", conv_flops(g));
-    unsigned* fl = imag_flag({{dy, XY * g.Cout * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
+    const bool known = (g.real_known & 6) == 6;
+    unsigned* fl = known ? ctx().d_zero : imag_flag({{dy, XY * g.Cout * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
     {
         const int RP = FGv == 2 ? rpx_for<2>() : rpx_for<8>();
         dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
@@ -607,7 +610,8 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
         k_conv_direct<1, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
                                                                 Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl, 1);
     KERNEL_CHECK();
-    CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
+    if (!known)
+        CUDA_CHECK(cudaFreeAsync(fl, ctx().stream));
 }
 
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g)
@@ -637,11 +641,13 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
         auto kern = fp2 ? k_conv_wgrad_rb<11, 2> : k_conv_wgrad_rb<11, 1>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
         const int nthr = int(((11 * g.Cin * (fp2 ? g.Cout / 2 : g.Cout) + 31) / 32) * 32);
-        unsigned* fl = imag_flag({{x, XY * g.Cin * g.B}, {dy, XY * g.Cout * g.B}});
+        const bool known = (g.real_known & 5) == 5;
+        unsigned* fl = known ? c.d_zero : imag_flag({{x, XY * g.Cin * g.B}, {dy, XY * g.Cout * g.B}});
         kern<<<nsplit, nthr, smem, c.stream>>>(part, Acc{x, g.Cin, XY, g.in_chlast}, Acc{dy, g.Cout, XY, g.out_chlast},
                                               g, nsplit, fl);
         KERNEL_CHECK();
-        CUDA_CHECK(cudaFreeAsync(fl, c.stream));
+        if (!known)
+            CUDA_CHECK(cudaFreeAsync(fl, c.stream));
         k_sum_splits<<<int((n + 63) / 64), 256, 0, c.stream>>>(dw, part, n, nsplit);
         KERNEL_CHECK();
         CUDA_CHECK(cudaFreeAsync(part, c.stream));

@@ -102,6 +102,8 @@ Context* make_ctx(int dev)
     }
     CUDA_CHECK(cudaMalloc(&c->d_errflags, 64));
     CUDA_CHECK(cudaMemset(c->d_errflags, 0, 64));
+    CUDA_CHECK(cudaMalloc(&c->d_zero, 16));
+    CUDA_CHECK(cudaMemset(c->d_zero, 0, 16));
     return c.release();
 }
 } // namespace

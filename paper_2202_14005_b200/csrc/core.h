@@ -77,6 +77,7 @@ struct Context {
     // device-side error word: kernels OR in error bits (CG breakdown, ...)
     // which the host checks at synchronisation points (no per-iteration sync)
     unsigned* d_errflags = nullptr;
+    unsigned* d_zero = nullptr; // a device word that stays 0 ("no imaginary part" flag for known-real operands)
     std::string err_detail;
 };
 Context& ctx();             // context of the current device (creates on first use)
@@ -124,6 +125,10 @@ struct DArray {
     // 1: forward statistics [blk][2C][sum, sum sq]; 2: batch-norm backward
     // partials [blk][2C][3] for the consumer identified by chstats_tag
     int chstats_kind = 0;
+    // the producer guarantees zero imaginary parts (real-channel split, Re, RBF,
+    // real-weight arguments, convolutions of known-real operands); lets a consumer
+    // skip its device-side imaginary-part scan
+    bool known_real = false;
     const void* chstats_tag = nullptr;
     void drop_chstats()
     {

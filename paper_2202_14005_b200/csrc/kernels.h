@@ -117,6 +117,9 @@ struct ConvGeom {
     // the kernel form provides them (*stats_blocks = blocks written, else 0)
     double* stats = nullptr;
     int* stats_blocks = nullptr;
+    // operands whose imaginary parts are known zero on the host: 1 = x (Cin side),
+    // 2 = w, 4 = dy (Cout side); skips the device-side scan for the real-operand kernels
+    int real_known = 0;
     // bwd-data only: batch-norm backward partial sums of the produced
     // cotangent for the BN block that consumes it (*bnb_blocks = blocks, else 0)
     const struct BnBwdHint* bnb = nullptr;

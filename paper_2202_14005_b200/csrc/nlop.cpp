@@ -30,10 +30,12 @@ DArray accumulate(DArray acc, const DArray& add)
     if (acc.buf.use_count() == 1) {
         launch_axpy(acc.data(), cfloat{1.f, 0.f}, b.data(), acc.size());
         acc.drop_chstats(); // producer statistics no longer describe the values
+        acc.known_real = acc.known_real && b.known_real;
         return acc;
     }
     DArray out(acc.dims, false, acc.layout);
     launch_add(out.data(), acc.data(), b.data(), 1.f, acc.size());
+    out.known_real = acc.known_real && b.known_real;
     return out;
 }
 

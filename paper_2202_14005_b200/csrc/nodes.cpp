@@ -378,10 +378,13 @@ private:
     DArray run(const DArray& x) const
     {
         DArray o(x.dims, false);
-        if (k_ == Conj)
+        if (k_ == Conj) {
             launch_conj(o.data(), x.data(), o.size());
-        else
+            o.known_real = x.known_real;
+        } else {
             launch_real(o.data(), x.data(), o.size());
+            o.known_real = true;
+        }
         return o;
     }
     Kind k_;
@@ -428,6 +431,7 @@ private:
         Dims big = join_ ? ins_[0] : outs_[0];
         DArray o(big, false);
         launch_real_chan_split(o.data(), x.data(), inner_, outer_);
+        o.known_real = true;
         return o;
     }
     DArray do_join(const DArray& x) const
@@ -734,6 +738,7 @@ public:
         }
         DArray y(outs_[0], false);
         rbf_forward(y.data(), in[0].data(), in[1].data(), mu_.get(), g_);
+        y.known_real = true; // phi acts on Re z and writes zero imaginary parts
         out[0] = y;
         if (store) {
             z_ = in[0];
@@ -760,6 +765,7 @@ public:
         if (i == 0) {
             DArray dz(ins_[0], false);
             rbf_adjoint_z(dz.data(), dy.data(), z_.data(), w_.data(), mu_.get(), g_);
+            dz.known_real = true;
             return dz;
         }
         DArray dw(ins_[1], false);
@@ -1296,6 +1302,7 @@ private:
         DArray y(od, false, act_layout(false));
         ConvGeom g = g_;
         g.in_tf32 = x.tf32;
+        g.real_known = (x.known_real ? 1 : 0) | (w.known_real ? 2 : 0);
         // channel statistics from the tensor-core epilogue (consumed by a BnBlockNode)
         const long ny = 2 * g_.Cout;
         DArray st;
@@ -1307,6 +1314,7 @@ private:
             g.stats_blocks = &st_blocks;
         }
         conv_fwd(y.data(), x.data(), w.data(), g);
+        y.known_real = x.known_real && w.known_real;
         if (st_blocks > 0) {
             y.chstats = std::make_shared<DArray>(st);
             y.chstats_blocks = st_blocks;
@@ -1323,6 +1331,7 @@ private:
         DArray dx(xd, false, act_layout(true));
         ConvGeom g = g_;
         g.out_tf32 = dy.tf32;
+        g.real_known = (dy.known_real ? 4 : 0) | (w.known_real ? 2 : 0);
         DArray part;
         int blocks = 0;
         const long eb = (hint && dx.layout == Layout::CHLAST && 2 * g_.Cin == 128 && conv_bn_fuse())
@@ -1335,6 +1344,7 @@ private:
             g.bnb_blocks = &blocks;
         }
         conv_bwd_data(dx.data(), dy.data(), w.data(), g);
+        dx.known_real = dy.known_real && w.known_real;
         if (blocks > 0) {
             dx.chstats = std::make_shared<DArray>(part);
             dx.chstats_blocks = blocks;
@@ -1351,7 +1361,9 @@ private:
         ConvGeom g = g_;
         g.in_tf32 = x.tf32;
         g.out_tf32 = dy.tf32;
+        g.real_known = (x.known_real ? 1 : 0) | (dy.known_real ? 4 : 0);
         conv_bwd_weight(dw.data(), x.data(), dy.data(), g);
+        dw.known_real = x.known_real && dy.known_real;
         return dw;
     }
     bool t_;

@@ -100,6 +100,15 @@ void Trainer::set_weight(const std::string& name, DArray a)
         throw ConfigError("trainer: no weight named '" + name + "'");
     if (a.dims != it->second.dims)
         throw ShapeError("trainer: weight '" + name + "' shape mismatch");
+    // a caller-provided value of a real-weight argument is only tagged real
+    // (known_real in gather_inputs) when it is (weights are small: host check)
+    bool real = true;
+    for (const auto& v : to_host(a))
+        if (v.imag() != 0.f) {
+            real = false;
+            break;
+        }
+    not_real_[name] = !real;
     it->second = std::move(a);
 }
 
@@ -132,6 +141,11 @@ std::vector<DArray> Trainer::gather_inputs() const
         if (it == src.end())
             throw ConfigError("model: missing array for argument '" + a.name + "'");
         in.push_back(it->second);
+        // real-valued weights stay real under the realified updates (optim.hpp:382-399)
+        if (a.kind != ArgKind::Data && a.real_weights) {
+            auto nr = not_real_.find(a.name);
+            in.back().known_real = nr == not_real_.end() || !nr->second;
+        }
     }
     return in;
 }

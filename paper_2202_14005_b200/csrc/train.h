@@ -65,6 +65,7 @@ private:
     TrainConfig cfg_;
     int loss_idx_ = 0;
     std::map<std::string, DArray> weights_, data_;
+    std::map<std::string, bool> not_real_; // set_weight values of real-weight args with imaginary parts
     std::vector<int> wargs_;
     std::vector<std::string> wnames_;
     std::vector<long> woff_;

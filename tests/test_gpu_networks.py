@@ -214,3 +214,28 @@ def test_modl_64_filters_bn_fusion(gpu, ref):
     for n in gu:
         assert rel_l2(gf[n], gu[n]) <= 1e-4, n
         assert rel_l2(gf[n], tr.get_grad(n)) <= 5e-3, n
+
+
+def test_varnet_complex_values_in_real_weight_args(gpu, ref):
+    """Real-weight arguments are tagged known-real for the real-operand conv
+    kernels only when their values are real: a caller-provided complex value
+    (set_weight) must take the general kernels and match the reference."""
+    X, Y, NC, B = 16, 12, 3, 2
+    cfg = dict(iterations=2, filters=3, kernel=5, rbf=7, im_x=X, im_y=Y, coils=NC, batch=B)
+    mref = Model.varnet(ref, **cfg)
+    data, _ = _inputs(ref, mref, X, Y, NC, B)
+    rng = np.random.default_rng(17)
+    losses, pert = [], {}
+    for lib in (gpu, ref):
+        t = Trainer(lib, Model.varnet(lib, **cfg), seed=42, lr=1e-3)
+        for k, v in data.items():
+            t.set_data(k, v)
+        for name in t.weight_names():
+            if name.endswith("_k_w"):
+                w = t.get_weight(name)
+                if name not in pert:  # the same complex values on both sides
+                    pert[name] = (0.2j * rng.standard_normal(w.shape)).astype(np.complex64)
+                t.set_weight(name, np.asfortranarray(w + pert[name]))
+        losses.append(t.forward_backward())
+    assert pert
+    np.testing.assert_allclose(losses[0], losses[1], rtol=1e-4)
