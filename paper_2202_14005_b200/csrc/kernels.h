@@ -230,6 +230,9 @@ void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, c
 void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
 void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
 void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g);
+// both adjoints in one pass (dz and dw of the same cotangent)
+void rbf_adjoint_zw(cfloat* dz, cfloat* dw, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu,
+                    const RbfGeom& g);
 void rbf_deriv_w(cfloat* dy, const cfloat* dw, const cfloat* z, const float* mu, const RbfGeom& g);
 
 // ---- loss / optimiser (train.cu) ------------------------------------------------------

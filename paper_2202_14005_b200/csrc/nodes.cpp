@@ -772,6 +772,20 @@ public:
         rbf_adjoint_w(dw.data(), dy.data(), z_.data(), mu_.get(), g_);
         return dw;
     }
+    void adjoint_all(int o, const DArray& dy, std::vector<DArray>& dx, const std::vector<char>& want) override
+    {
+        if (!(want.size() > 1 && want[0] && want[1])) {
+            Atom::adjoint_all(o, dy, dx, want);
+            return;
+        }
+        require_forward();
+        dx.assign(n_in(), DArray{});
+        DArray dz(ins_[0], false), dw(ins_[1], false);
+        rbf_adjoint_zw(dz.data(), dw.data(), dy.data(), z_.data(), w_.data(), mu_.get(), g_);
+        dz.known_real = true;
+        dx[0] = dz;
+        dx[1] = dw;
+    }
 
 private:
     float sigma_;

@@ -80,15 +80,22 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
 
 // partial[(f * nw + j) * nchunk + chunk] = sum over the chunk of e_j(z) Re(g)
 constexpr int kChunk = 8192;
+// dz != nullptr: also the adjoint wrt z of the same elements (the basis values
+// e_j are shared: one pass instead of k_rbf_map mode 1 + this kernel)
 __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict__ dy, const cfloat* __restrict__ z,
-                            const float* __restrict__ mu, RbfGeom g, int nchunk)
+                            const float* __restrict__ mu, RbfGeom g, int nchunk, cfloat* __restrict__ dz,
+                            const cfloat* __restrict__ w)
 {
     __shared__ float smu[kMaxW];
+    __shared__ float swf[kMaxW];
     __shared__ double red[kMaxW][8];
-    for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
-        smu[j] = mu[j];
-    __syncthreads();
     const long f = blockIdx.y;
+    for (int j = threadIdx.x; j < g.nw; j += blockDim.x) {
+        smu[j] = mu[j];
+        swf[j] = dz ? w[f + j * g.nf].x : 0.f;
+    }
+    __syncthreads();
+    const float inv_s2 = 1.f / (g.sigma * g.sigma);
     const long total = g.inner * g.outer;
     const long begin = long(blockIdx.x) * kChunk, end = min(total, begin + kChunk);
     // fp32 running sums per thread (kChunk / blockDim = 32 terms each), folded in double
@@ -100,8 +107,18 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
         const long ii = t % g.inner, o = t / g.inner;
         const long idx = ii + g.inner * (f + g.nf * o);
         const float zk = z[idx].x, gv = dy[idx].x;
-        for (int j = 0; j < g.nw; j++)
-            acc[j] = fmaf(gauss2(zk, smu[j], k2), gv, acc[j]);
+        if (dz) {
+            float d = 0.f;
+            for (int j = 0; j < g.nw; j++) {
+                const float e = gauss2(zk, smu[j], k2);
+                acc[j] = fmaf(e, gv, acc[j]);
+                d = fmaf(swf[j] * e, -(zk - smu[j]) * inv_s2, d);
+            }
+            dz[idx] = float2{d * gv, 0.f};
+        } else {
+            for (int j = 0; j < g.nw; j++)
+                acc[j] = fmaf(gauss2(zk, smu[j], k2), gv, acc[j]);
+        }
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = 0; j < g.nw; j++) {
@@ -167,7 +184,22 @@ void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* m
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
-    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, 0, c.stream>>>(part, dy, z, mu, g, nchunk);
+    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, 0, c.stream>>>(part, dy, z, mu, g, nchunk, nullptr, nullptr);
+    KERNEL_CHECK();
+    k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
+    KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(part, c.stream));
+}
+
+void rbf_adjoint_zw(cfloat* dz, cfloat* dw, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu,
+                    const RbfGeom& g)
+{
+    auto& c = ctx();
+    const long total = g.inner * g.outer;
+    const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
+    double* part;
+    CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
+    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, 0, c.stream>>>(part, dy, z, mu, g, nchunk, dz, w);
     KERNEL_CHECK();
     k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
     KERNEL_CHECK();
