@@ -200,7 +200,12 @@ __global__ void __launch_bounds__(RTX* RTY) k_conv_direct_real(Out out, Acc in, 
     if (*imag_flag != 0)
         return; // complex operands: k_conv_direct computes this launch
     constexpr int OX = RTX * RPX, OY = RTY;
-    __shared__ float tile[OY + MAXK - 1][OX + MAXK - 1];
+    // row pitch rounded up to a float4 multiple (+4): the sliding window of
+    // RPX + KX - 1 values is read as 16-B vectors (scalar reads 4 words apart
+    // were bank-conflicted and issue-bound)
+    constexpr int HXP = ((OX + MAXK - 1 + 3) / 4) * 4 + 4;
+    constexpr int NV4 = (RPX + MAXK - 1 + 3) / 4;
+    __shared__ __align__(16) float tile[OY + MAXK - 1][HXP];
     __shared__ __align__(16) float wre[MAXK * MAXK][FG];
     const long nin = MODE == 0 ? g.Cin : g.Cout;
     const long nout = MODE == 0 ? g.Cout : g.Cin;
@@ -243,11 +248,16 @@ __global__ void __launch_bounds__(RTX* RTY) k_conv_direct_real(Out out, Acc in, 
         }
         __syncthreads();
         for (int ky = 0; ky < KY; ky++) {
-            float win[RPX + MAXK - 1];
-            const float* trow = &tile[ty + ky][tx * RPX];
+            float win[4 * NV4];
+            const float4* trow = reinterpret_cast<const float4*>(&tile[ty + ky][tx * RPX]);
 #pragma unroll
-            for (int q = 0; q < RPX + MAXK - 1; q++)
-                win[q] = q < RPX + KX - 1 ? trow[q] : 0.f;
+            for (int v4 = 0; v4 < NV4; v4++) {
+                const float4 q4 = trow[v4];
+                win[4 * v4] = q4.x;
+                win[4 * v4 + 1] = q4.y;
+                win[4 * v4 + 2] = q4.z;
+                win[4 * v4 + 3] = q4.w;
+            }
 #pragma unroll
             for (int kx = 0; kx < MAXK; kx++) {
                 if (kx >= KX)
