@@ -387,10 +387,13 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
 {
     const bool real = imag_flag && *imag_flag == 0;
     constexpr int HX = WTX + K - 1, HY = WTY + K - 1;
+    // odd float2 row pitch: the K kernel-row lanes of a warp read K different rows
+    // at the same column; an even pitch (42) mapped several of them to one bank
+    constexpr int HXP = HX | 1;
     extern __shared__ float2 wsm[];
     const int Cin = int(g.Cin), Cout = int(g.Cout);
     float2* xt = wsm;                          // [Cin][HY][HX]
-    float2* dyt = wsm + Cin * HY * HX;         // [Cout][WTY][WTX]
+    float2* dyt = wsm + Cin * HY * HXP;        // [Cout][WTY][WTX]
     const int nthr = K * Cin * (Cout / FP);
     const int tid = threadIdx.x;
     const int ky = tid % K, c = (tid / K) % Cin, f = (tid / (K * Cin)) * FP;
@@ -411,7 +414,8 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
         for (int e = tid; e < Cin * HX * HY; e += blockDim.x) {
             const int hx = e % HX, hy = (e / HX) % HY, cc = e / (HX * HY);
             const long gx = x0 + hx - g.px, gy = y0 + hy - g.py;
-            xt[e] = (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? x.ld(b, gx + g.X * gy, cc) : float2{0.f, 0.f};
+            xt[(cc * HY + hy) * HXP + hx] =
+                (gx >= 0 && gx < g.X && gy >= 0 && gy < g.Y) ? x.ld(b, gx + g.X * gy, cc) : float2{0.f, 0.f};
         }
         for (int e = tid; e < Cout * WTX * WTY; e += blockDim.x) {
             const int px = e % WTX, py = (e / WTX) % WTY, ff = e / (WTX * WTY);
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
         if (!act)
             continue;
         for (int py = 0; py < WTY; py++) {
-            const float2* xr = xt + (c * HY + py + ky) * HX;
+            const float2* xr = xt + (c * HY + py + ky) * HXP;
             const float2* dr = dyt + (f * WTY + py) * WTX;
             float2 win[K];
 #pragma unroll
@@ -643,7 +647,7 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
         const int nsplit = int(std::min<long>(ntiles, 2L * c.sm_count));
         const long n = KK * g.Cin * g.Cout;
         const long XY = g.X * g.Y;
-        const size_t smem = sizeof(float2) * (g.Cin * (WTY + 10) * (WTX + 10) + g.Cout * WTX * WTY);
+        const size_t smem = sizeof(float2) * (g.Cin * (WTY + 10) * ((WTX + 10) | 1) + g.Cout * WTX * WTY);
         float2* part;
         CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
         ProfScope prof("conv_bwd_weight", conv_flops(g));
