@@ -775,16 +775,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 mbar_wait(&full[st], ph);
                 tc_fence_after();
                 // start-address field (bits 0-13) + offset: no carry for smem < 256 KB
-                const uint32_t so = (st * S::STAGE) >> 4;
-                const uint32_t xlo = uint32_t(xd0) + so, dlo = uint32_t(dd0) + so;
-                const uint64_t xhi = xd0 & 0xFFFFFFFF00000000ull, dhi = dd0 & 0xFFFFFFFF00000000ull;
+                const uint64_t so = (st * S::STAGE) >> 4;
+                const uint64_t xd = xd0 + so, dd = dd0 + so;
 #pragma unroll
                 for (int ks = 0; ks < WG_SEG / 8; ks++) {
-                    const uint64_t bd = dhi | (dlo + uint32_t((ks * 8 * 128) >> 4));
+                    const uint64_t bd = dd + ((ks * 8 * 128) >> 4);
 #pragma unroll
                     for (int kx = 0; kx < 3; kx++)
-                        mma_tf32_warp(tmem_base + kx * N, xhi | (xlo + uint32_t(((kx + ks * 8) * 128) >> 4)), bd, idesc,
-                                 (si != 0 || ks != 0) ? 1u : 0u);
+                        mma_tf32_warp(tmem_base + kx * N, xd + (((kx + ks * 8) * 128) >> 4), bd, idesc,
+                                      (si != 0 || ks != 0) ? 1u : 0u);
                 }
                 mma_commit_warp(&empty[st]);
                 if constexpr (MC)
