@@ -770,8 +770,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint64_t xd0 = umma_desc_mn_sw128_32b(sbase, 512, WG_XBLK);
             const uint64_t dd0 = umma_desc_mn_sw128_32b(sbase + 4 * WG_XBLK, 512, WG_DBLK);
             const int nseg_cta = int(s_end - s_begin);
+            uint32_t st = 0, ph = 0; // ring position kept incrementally (no division by the stage count)
             for (int si = 0; si < nseg_cta; si++, it++) {
-                const uint32_t st = it % WG_STAGES, ph = (it / WG_STAGES) & 1;
+                if (si > 0 && ++st == WG_STAGES) {
+                    st = 0;
+                    ph ^= 1;
+                }
                 mbar_wait(&full[st], ph);
                 tc_fence_after();
                 // start-address field (bits 0-13) + offset: no carry for smem < 256 KB
