@@ -205,6 +205,7 @@ __global__ void __launch_bounds__(RTX* RTY) k_conv_direct_real(Out out, Acc in, 
     // were bank-conflicted and issue-bound)
     constexpr int HXP = ((OX + MAXK - 1 + 3) / 4) * 4 + 4;
     constexpr int NV4 = (RPX + MAXK - 1 + 3) / 4;
+    static_assert(RPX % 4 == 0, "the window is read as 16-B vectors from tx * RPX");
     __shared__ __align__(16) float tile[OY + MAXK - 1][HXP];
     __shared__ __align__(16) float wre[MAXK * MAXK][FG];
     const long nin = MODE == 0 ? g.Cin : g.Cout;
