@@ -174,6 +174,8 @@ int mdnn_set_option(const char* key, long value)
             conv_thin_tc_enable(value != 0);
         else if (k == "conv_thin_tc_expand")
             conv_thin_tc_expand_enable(value != 0);
+        else if (k == "conv_thin_tc_bnb")
+            conv_thin_tc_bnb_enable(value != 0);
         else if (k == "conv_chlast")
             conv_force_chlast(value != 0);
         else if (k == "conv_tc_debug")

@@ -628,11 +628,13 @@ long conv_thin_epi_blocks(const ConvGeom& g, int mode)
     const bool one_in = g.Cin == 1;
     const bool expand = (mode == 0) == one_in;
     const long F = one_in ? g.Cout : g.Cin;
-    // forward statistics only: the BN-backward partials (ThinEpi::bpart) cost
-    // the issue-bound expand loop more than the separate reduction pass they
-    // replace (measured at C2: +2.4 ms vs -1.6 ms per two steps)
-    if (!expand || F != 64 || mode != 0)
+    // forward statistics from either expand; BN-backward partials only from the
+    // tensor-core expand (in the issue-bound CUDA-core loop they cost more than
+    // the separate reduction pass they replace: +2.4 ms vs -1.6 ms per two steps)
+    if (!expand || F != 64)
         return 0;
+    if (mode == 1)
+        return conv_thin_tc_bnb() && g.KX == 3 ? thin_expand_tc_blocks() : 0;
     // allocation bound: the CUDA-core kernel's blocks or the tensor-core kernel's slots
     return std::max(((g.X + TX - 1) / TX) * ((g.Y + 7) / 8) * g.B, thin_expand_tc_blocks());
 }
@@ -662,23 +664,17 @@ void conv_thin_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvG
         // blocks the CUDA-core expand writes (its grid); the tensor-core path resets this below
         *g.stats_blocks = int(((g.X + TX - 1) / TX) * ((g.Y + 7) / 8) * g.B);
     }
-    if (eblocks > 0 && mode == 1 && g.bnb && g.bnb_part && g.bnb_blocks && g.bnb->C == F
-        && g.bnb->npix == g.X * g.Y * g.B) {
-        ep.bpart = g.bnb_part;
-        ep.bx = g.bnb->x;
-        ep.mu = g.bnb->mu;
-        ep.istd = g.bnb->istd;
-        ep.gamma = g.bnb->gamma;
-        ep.beta = g.bnb->beta;
-        *g.bnb_blocks = int(eblocks);
-    }
+    // mode 1 with a BN hint: only the tensor-core expand folds the BN-backward
+    // reduction (the CUDA-core loop measured slower with it)
+    const bool bn_tc = eblocks > 0 && mode == 1 && g.bnb && g.bnb_part && g.bnb_blocks;
     {
         // HBM-bound: algorithmic bytes = wide side once + thin side once
         ProfScope prof(mode == 0 ? "conv_thin_fwd" : "conv_thin_bwd_data", 8.0 * double(g.X) * g.Y * g.B * (F + 1));
         int tc_blocks = 0;
         if (expand && g.KX == 3
             && thin_expand_tc(reinterpret_cast<float*>(outp), inp, U, g.X, g.Y, g.B, F, 9, ox, oy, ep.stats,
-                              &tc_blocks)) {
+                              &tc_blocks, bn_tc ? g.bnb : nullptr, bn_tc ? g.bnb_part : nullptr,
+                              bn_tc ? g.bnb_blocks : nullptr)) {
             // tensor-core im2col GEMM (conv_thin_tc.cu); its statistics partials replace the CUDA-core ones
             if (ep.stats && g.stats_blocks)
                 *g.stats_blocks = tc_blocks;

@@ -250,9 +250,21 @@ __global__ void k_pack_thin_expand(float* __restrict__ ue, const float2* __restr
 // byte offset of (row r, 16-B granule g) in a SWIZZLE_128B K-major tile (8-row atoms of 1024 B)
 __device__ __forceinline__ int sw128_off(int r, int g) { return (r >> 3) * 1024 + (r & 7) * 128 + ((g ^ (r & 7)) << 4); }
 
+// BN-backward reduction in the epilogue (bwd-data of the last layer: the produced
+// cotangent is the last BN block's output cotangent) -- as in k_conv_tc_t
+struct TeBn {
+    const float* x = nullptr; // BN input, CHLAST 128 floats per pixel
+    const float2* mu = nullptr;
+    const float* istd = nullptr;
+    const float2* gamma = nullptr;
+    const float2* beta = nullptr;
+    double* part = nullptr;   // [blk][128][3]
+};
+
 __global__ void __launch_bounds__(TE_THREADS, 1)
     k_thin_expand_tc(const __grid_constant__ CUtensorMap tm_out, const float2* __restrict__ thin,
-                     const float* __restrict__ ue, int X, int Y, long npix, int ox, int oy, double* __restrict__ stats)
+                     const float* __restrict__ ue, int X, int Y, long npix, int ox, int oy, double* __restrict__ stats,
+                     const TeBn be)
 {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -377,6 +389,16 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
             prefetch_tmap(&tm_out);
         int sb = 0;
         double s_acc = 0, q_acc = 0;
+        const int bc = n & 63, comp = n >> 6;
+        float2 bmu{0.f, 0.f}, bg{0.f, 0.f}, bb{0.f, 0.f};
+        float bs = 0.f;
+        if (be.part) {
+            bmu = be.mu[bc];
+            bs = be.istd[bc];
+            bg = be.gamma[bc];
+            bb = be.beta[bc];
+        }
+        double r0 = 0, r1 = 0, r2 = 0;
         uint32_t it = 0;
         for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, it++) {
             const uint32_t st = it & 1, ph = (it >> 1) & 1;
@@ -417,12 +439,42 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
                 }
                 s_acc += fs;
                 q_acc += fq;
+                if (be.part) {
+                    const float* xp = be.x + p0 * 128 + bc;
+                    float xr[16], xi[16];
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        xr[j] = j < nv ? __ldg(xp + j * 128) : 0.f;
+                        xi[j] = j < nv ? __ldg(xp + j * 128 + 64) : 0.f;
+                    }
+                    float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        // yhat and z exactly as bn_z (bnblock.cu)
+                        const float hr = (xr[j] - bmu.x) * bs, hi = (xi[j] - bmu.y) * bs;
+                        const float zr = bg.x * hr - bg.y * hi + bb.x;
+                        const float zi = bg.x * hi + bg.y * hr + bb.y;
+                        const float ge = (j < nv && (comp ? zi : zr) > 0.f) ? v[j] : 0.f;
+                        f0 += ge;
+                        f1 = fmaf(ge, comp ? hi : hr, f1);
+                        f2 = fmaf(ge, comp ? hr : -hi, f2);
+                    }
+                    r0 += f0;
+                    r1 += f1;
+                    r2 += f2;
+                }
             }
             tc_fence_before();
             mbar_arrive(&tmem_empty[st]);
         }
         if (lane == 0)
             bulk_wait<0>(); // stores complete before the kernel's writes are consumed
+        if (be.part) {
+            const size_t slot = size_t(blockIdx.x) * (TE_EPI / 4) + rep;
+            be.part[(slot * 128 + n) * 3] = r0;
+            be.part[(slot * 128 + n) * 3 + 1] = r1;
+            be.part[(slot * 128 + n) * 3 + 2] = r2;
+        }
         if (stats) {
             const size_t slot = size_t(blockIdx.x) * (TE_EPI / 4) + rep;
             stats[(slot * 128 + n) * 2] = s_acc;
@@ -471,20 +523,29 @@ bool g_thin_tc = true;
 // kernel at C2 (~2.9 vs 2.7 ms per two steps: its 512-B-per-pixel stores, not
 // the FLOPs, bound both) -- off by default, option "conv_thin_tc_expand"
 bool g_thin_tc_expand = false;
+// the tensor-core expand for the last layer's bwd-data when its epilogue can
+// also take the last BN block's backward reduction
+bool g_thin_tc_bnb = true;
 
 } // namespace
 
 void conv_thin_tc_enable(bool on) { g_thin_tc = on; }
 void conv_thin_tc_expand_enable(bool on) { g_thin_tc_expand = on; }
+void conv_thin_tc_bnb_enable(bool on) { g_thin_tc_bnb = on; }
+bool conv_thin_tc_bnb() { return g_thin_tc && g_thin_tc_bnb; }
 
 long thin_expand_tc_blocks() { return long(ctx().sm_count) * (TE_EPI / 4); }
 
 bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, long Y, long B, int F, int KK, int ox,
-                    int oy, double* stats, int* stats_blocks)
+                    int oy, double* stats, int* stats_blocks, const BnBwdHint* bnb, double* bpart, int* bblocks)
 {
     if (stats_blocks)
         *stats_blocks = 0;
-    if (!g_thin_tc || !g_thin_tc_expand || F != 64 || KK != 9)
+    if (bblocks)
+        *bblocks = 0;
+    // the BN-backward-fused bwd-data (option conv_thin_tc_bnb) or everything (conv_thin_tc_expand)
+    const bool bn = bnb && bpart && bblocks && g_thin_tc_bnb && bnb->C == F && bnb->npix == X * Y * B;
+    if (!g_thin_tc || !(g_thin_tc_expand || bn) || F != 64 || KK != 9)
         return false;
     auto& c = ctx();
     const long npix = X * Y * B;
@@ -516,12 +577,17 @@ bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, lon
         if (r != CUDA_SUCCESS)
             throw CudaError("cuTensorMapEncodeTiled(expand out) failed: " + std::to_string(int(r)));
     }
+    TeBn be{};
+    if (bn)
+        be = TeBn{bnb->x, bnb->mu, bnb->istd, bnb->gamma, bnb->beta, bpart};
     k_thin_expand_tc<<<grid, TE_THREADS, TeSmem::TOTAL, c.stream>>>(tmo, thin, ue, int(X), int(Y), npix, ox, oy,
-                                                                    stats);
+                                                                    stats, be);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(ue, c.stream));
     if (stats && stats_blocks)
         *stats_blocks = grid * (TE_EPI / 4);
+    if (bn)
+        *bblocks = grid * (TE_EPI / 4);
     return true;
 }
 

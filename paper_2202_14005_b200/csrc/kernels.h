@@ -167,7 +167,10 @@ void conv_thin_tc_expand_enable(bool on);
 long thin_expand_tc_blocks(); // statistics partial slots the tensor-core expand may write
 // 1 -> F (3x3, F = 64) on the tensor cores (+ BN statistics partials when stats != nullptr)
 bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, long Y, long B, int F, int KK, int ox,
-                    int oy, double* stats, int* stats_blocks);
+                    int oy, double* stats, int* stats_blocks, const BnBwdHint* bnb = nullptr, double* bpart = nullptr,
+                    int* bblocks = nullptr);
+void conv_thin_tc_bnb_enable(bool on);
+bool conv_thin_tc_bnb();
 // upper bound on the epilogue partial blocks a conv launch writes into
 // ConvGeom::stats (mode 0) / bnb_part (mode 1); 0 = that path has none
 long conv_epi_blocks(const ConvGeom& g, int mode);
