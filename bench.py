@@ -15,8 +15,17 @@ One JSON line on rank 0 (contract in the task statement):
            from pinned host memory inside the timed region and the loss read back
   roofline, cpu_baseline, clocks, gpu_launches
 
+Workloads (--workload): modl_c2 (default, BASELINE configs[1]), modl_c1,
+varnet_c3, modl_c5 (512x512, 32 coils, 4 items per GPU; configs[4]) and
+sense_c4 (the SENSE normal operator A^H A + lambda and a 10-iteration CG solve
+alone, configs[3]; unit GB/s of algorithmic bytes, with a coils x image sweep).
+
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+with N ranks (127.0.0.1); under torchrun WORLD_SIZE must equal --gpus.
+
 `--impl reference` times the reference CPU implementation (oracle/_ref, the
-unmodified reference headers compiled in place) on the host cores instead.
+unmodified reference headers compiled in place) on the host cores instead;
+each step is one bounded sample of the workload (see cpu_sample()).
 """
 import argparse
 import ctypes as C
@@ -37,7 +46,12 @@ WORKLOADS = {
     "modl_c2": (dict(iterations=5, layers=5, filters=64, cg_iter=10), 320, 368, 15, 8),
     "modl_c1": (dict(iterations=1, layers=3, filters=32, cg_iter=5), 128, 128, 8, 1),
     "varnet_c3": (dict(iterations=10, filters=24, kernel=11, rbf=31), 640, 368, 15, 4),
+    "modl_c5": (dict(iterations=5, layers=5, filters=64, cg_iter=10), 512, 512, 32, 4),
 }
+# sense_c4: (X, Y, coils, items per GPU); the first shape is the headline
+# value, items sized so the per-GPU working set is >= 4x L2
+SENSE_C4 = [(512, 512, 32, 8), (512, 512, 16, 16), (512, 512, 8, 32), (256, 256, 32, 32), (256, 256, 16, 64),
+            (256, 256, 8, 128)]
 METRIC = "MoDL/VarNet train samples/s @1/2/4/8 B200; A^HA GB/s vs HBM peak"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
@@ -151,41 +165,100 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_sample(workload):
-    """Reference CPU implementation on the host cores (oracle/_ref, all
-    threads): one training step of ONE unroll at batch 1 and the workload's
-    geometry; the full step is T unrolls of identical cost, so samples/s is
-    extrapolated as 1 / (T * t).  Returns (samples/s, seconds, description)."""
+# Reference CPU implementation (oracle/_ref: the unmodified reference headers
+# compiled in place) on the host cores -- a baseline only, never the product.
+def _ref_lib():
     from paper_2202_14005_b200.capi import Lib
-    from paper_2202_14005_b200.mdnn import Trainer
     path = os.path.join(REPO, "oracle", "_ref", "libmdnn_ref.so")
-    if not os.path.exists(path):
+    return Lib(path) if os.path.exists(path) else None
+
+
+def cpu_train_sample(workload):
+    """One bounded sample of a training workload: the reference's own run_step
+    (forward + backward + Adam, optim.hpp:314-399) at batch 1 with the
+    workload's geometry and network.  Workloads with T > 1 unrolls are sampled
+    with ONE unroll (the T unrolls cost the same: samples/s = 1 / (T t));
+    modl_c1 (T = 1) is its full configuration.  Returns (samples/s, seconds,
+    description)."""
+    from paper_2202_14005_b200.mdnn import Model, Trainer
+    ref = _ref_lib()
+    if ref is None:
         return None
-    ref = Lib(path)
     kw, X, Y, NC, _ = WORKLOADS[workload]
     T = kw["iterations"]
     data = make_data(ref, X, Y, NC, 1, 0)
-    sample_kw = dict(kw, iterations=1, im_x=X, im_y=Y, coils=NC, batch=1)
-    from paper_2202_14005_b200.mdnn import Model
-    model = (Model.varnet if workload.startswith("varnet") else Model.modl)(ref, **sample_kw)
+    model = (Model.varnet if workload.startswith("varnet") else Model.modl)(
+        ref, **dict(kw, iterations=1, im_x=X, im_y=Y, coils=NC, batch=1))
     tr = Trainer(ref, model, seed=42)
     for k, v in data.items():
         tr.set_data(k, v)
     t0 = time.perf_counter()
     tr.step()
     dt = time.perf_counter() - t0
-    desc = (f"reference fp32 train step (Adam) of 1 of {T} unrolls, batch 1, {X}x{Y}x{NC} "
-            f"(x{T} extrapolated per sample), OMP threads={os.environ.get('OMP_NUM_THREADS', os.cpu_count())}")
+    what = "full step" if T == 1 else f"1 of {T} unrolls (x{T} per sample)"
+    desc = f"reference fp32 run_step (Adam), {what}, batch 1, {X}x{Y}x{NC}"
     return 1.0 / (T * dt), dt, desc
+
+
+def sense_bytes(X, Y, NC, B, cg=False):
+    """SURVEY §8d algorithmic bytes: S apply 8 B X Y (C + 2); CG iteration 8 B X Y (C + 10)."""
+    return 8.0 * B * X * Y * (NC + (10 if cg else 2))
+
+
+def cpu_sense_sample(shape):
+    """Reference S = A^H A + lambda (modl_normal_plus_lambda, recon.hpp:807-820)
+    applied once at batch 1: algorithmic GB/s.  Returns (GB/s, seconds, desc)."""
+    from util import image_dims
+    ref = _ref_lib()
+    if ref is None:
+        return None
+    X, Y, NC = shape[:3]
+    ph, cm, pat = sim_inputs(ref, X, Y, NC, 1)
+    y = np.zeros(image_dims(X, Y), dtype=np.complex64, order="F")
+    A = [ref.arr(a) for a in (cm, pat, ph, y)]
+    t0 = time.perf_counter()
+    ref.check(ref.so.mdnn_sense_normal(C.byref(A[0]), C.byref(A[1]), C.c_float(0.05), C.byref(A[2]), C.byref(A[3])))
+    dt = time.perf_counter() - t0
+    return sense_bytes(X, Y, NC, 1) / dt / 1e9, dt, f"reference S = A^H A + lambda apply, batch 1, {X}x{Y}x{NC}"
+
+
+def sim_inputs(lib, X, Y, NC, B, first_item=0):
+    d = make_data(lib, X, Y, NC, B, first_item)
+    return d["reference"], d["coils"], d["pattern"]
+
+
+def cpu_sample(workload):
+    if workload == "sense_c4":
+        return cpu_sense_sample(SENSE_C4[0])
+    return cpu_train_sample(workload)
+
+
+def _subprocess_samples(workload, nproc):
+    """`nproc` concurrent single-threaded reference processes, one sample each
+    (the P-process throughput estimate of BASELINE.md §3: the reference's SENSE
+    / CG path does not scale with OpenMP threads).  Returns per-process values."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    cmd = [sys.executable, os.path.abspath(__file__), "--cpu-sample-worker", workload]
+    procs = [subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+             for _ in range(nproc)]
+    vals = []
+    for p in procs:
+        out, _ = p.communicate(timeout=900)
+        try:
+            vals.append(json.loads(out.strip().splitlines()[-1]))
+        except Exception:
+            pass
+    return vals
 
 
 def run_reference_arm(args, rank, world):
     if rank != 0:
-        return
-    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
-    kw, X, Y, NC, B = WORKLOADS[args.workload]
+        return  # the reference is a single-host CPU implementation: rank 0 alone runs it
+    cores = os.cpu_count() or 1
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    unit = "GB/s" if args.workload == "sense_c4" else "samples/s"
+    n = max(1, min(args.steps, 3))  # each sample is ~1-15 s of CPU work
     vals = []
-    n = max(1, min(args.steps, 2))  # each sample is ~10-60 s of CPU work
     for _ in range(n):
         r = cpu_sample(args.workload)
         if r is None:
@@ -193,22 +266,53 @@ def run_reference_arm(args, rank, world):
             return
         vals.append(r)
     v = float(np.median([x[0] for x in vals]))
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
-            "steps": n, "warmup": 0, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c64 (fp32)", "data": "synthetic",
-            "config": config_of(args, B, world=1),
-            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": cores, "kind": "reference",
-                             "sample": vals[0][2]},
-            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    sec = float(np.median([x[1] for x in vals]))
+    cpu = {"value": v, "unit": unit, "cores": cores, "kind": "reference",
+           "sample": vals[0][2] + f"; OMP threads {cores}; median of {n}", "sample_seconds": sec}
+    if not args.no_thread_sweep:
+        one = _subprocess_samples(args.workload, 1)
+        par = _subprocess_samples(args.workload, cores)
+        if one:
+            cpu["single_thread"] = {"value": one[0]["value"], "unit": unit, "cores": 1,
+                                    "sample_seconds": one[0]["seconds"]}
+        if par:
+            cpu["p_process"] = {"value": float(sum(p["value"] for p in par)), "unit": unit, "cores": cores,
+                                "processes": len(par), "sample_seconds": float(max(p["seconds"] for p in par)),
+                                "note": "aggregate of concurrent single-threaded reference processes on independent "
+                                        "items (valid under the per-shard semantics, SURVEY §8e)"}
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": args.gpus,
+            "steps": n, "warmup": 0, "ms_per_step": 1000.0 * sec, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c64 (fp32 complex)", "data": "synthetic",
+            "config": config_of(args, world=1), "cpu_baseline": cpu,
+            "step_definition": "one bounded sample per step: " + vals[0][2],
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_of(args, B, world):
-    kw, X, Y, NC, _ = WORKLOADS[args.workload]
+def config_of(args, world):
+    if args.workload == "sense_c4":
+        X, Y, NC, B = SENSE_C4[0]
+        return {"workload": "sense_c4", "operator": "S = A^H A + lambda (lambda 0.05) and CG-10 (tol 0)",
+                "image": [X, Y], "coils": NC, "batch_per_gpu": B, "global_batch": B * world,
+                "sweep": [list(s) for s in SENSE_C4], "parallelism": f"replicas{world}",
+                "l2": "working set >= 4x L2 per GPU (no flush)"}
+    kw, X, Y, NC, B = WORKLOADS[args.workload]
     return {"workload": args.workload, "network": "varnet" if args.workload.startswith("varnet") else "modl",
             **{k: v for k, v in kw.items()}, "image": [X, Y], "coils": NC, "batch_per_gpu": B,
-            "global_batch": B * world, "parallelism": f"dp{world}", "l2": "inputs > L2 (no flush)"}
+            "global_batch": B * world, "parallelism": f"dp{world}", "l2": "inputs > L2 (no flush)",
+            "conv_arithmetic": "TF32 tensor cores (operands rounded RN to TF32), fp32 accumulate"}
+
+
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` outside torchrun: one rank per GPU on this node."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -217,15 +321,27 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="modl_c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="modl_c2", choices=sorted(WORKLOADS) + ["sense_c4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-thread-sweep", action="store_true", help="reference arm: skip the 1-thread / P-process figures")
+    ap.add_argument("--dp", default="library", choices=["library", "torch"],
+                    help="gradient exchange for N > 1: NCCL inside the library (default) or torch.distributed")
+    ap.add_argument("--cpu-sample-worker", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
     sys.path.insert(0, os.path.join(REPO, "tests"))
 
+    if args.cpu_sample_worker:
+        r = cpu_sample(args.cpu_sample_worker)
+        print(json.dumps({"value": r[0], "seconds": r[1]}) if r else "{}", flush=True)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}")
 
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
@@ -234,8 +350,6 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2202_14005_b200 import load_library
-    from paper_2202_14005_b200.dp import DataParallelTrainer
-    from paper_2202_14005_b200.mdnn import Trainer
 
     torch.cuda.set_device(local)
     lib = load_library()
@@ -247,11 +361,57 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        lib.check(lib.so.mdnn_synchronize())
+
+    def max_over_ranks(ms):
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    ctx = dict(torch=torch, dist=dist, lib=lib, stream=stream, rank=rank, world=world, local=local,
+               barrier=barrier, max_over_ranks=max_over_ranks)
+    line = (run_sense_arm if args.workload == "sense_c4" else run_train_arm)(args, ctx)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def timed(ctx, steps, fn, clk=None):
+    """CUDA events on the library stream around `steps` calls of fn, barrier +
+    synchronize on both sides; returns (max-over-ranks ms, launches, clocks)."""
+    torch, lib, stream = ctx["torch"], ctx["lib"], ctx["stream"]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_begin = clk.mark() if clk else None
+    l0 = lib.so.mdnn_launch_count()
+    ctx["barrier"]()
+    e0.record(stream)
+    for _ in range(steps):
+        fn()
+    e1.record(stream)
+    ctx["barrier"]()
+    launches = lib.so.mdnn_launch_count() - l0
+    clocks = clk.stop(t_begin, clk.mark()) if clk else None
+    return ctx["max_over_ranks"](e0.elapsed_time(e1)), launches, clocks
+
+
+def run_train_arm(args, ctx):
+    torch, lib, stream = ctx["torch"], ctx["lib"], ctx["stream"]
+    rank, world, local = ctx["rank"], ctx["world"], ctx["local"]
+    from paper_2202_14005_b200.dp import DataParallelTrainer
+    from paper_2202_14005_b200.mdnn import Trainer
+
     kw, X, Y, NC, B = WORKLOADS[args.workload]
     data = make_data(lib, X, Y, NC, B, first_item=rank * B)
     model = build_model(lib, args.workload, B)
     tr = Trainer(lib, model, seed=42)
-    dpt = DataParallelTrainer(tr, world=world, device=torch.device("cuda", local))
+    dpt = DataParallelTrainer(tr, world=world, device=torch.device("cuda", local), comm=args.dp, rank=rank)
     dev = {k: torch.from_numpy(np.ascontiguousarray(v.transpose())).to(f"cuda:{local}") for k, v in data.items()}
     for k, v in dev.items():
         tr.set_data(k, v)
@@ -260,50 +420,29 @@ def main():
     h2d = sum(int(v.numel()) * 8 for k, v in pinned.items())
 
     def step():
-        dpt.step()  # forward + backward, NCCL all-reduce on the library stream, Adam
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        lib.check(lib.so.mdnn_synchronize())
+        dpt.step()  # forward + backward, gradient all-reduce (N > 1), Adam
 
     clk = ClockSampler(local)
     clk.start()
     for _ in range(args.warmup):
         step()
-    barrier()
+    ctx["barrier"]()
     clk.wait_first()
 
     # ---- device-timed region (inputs resident in HBM) --------------------
-    t_begin = clk.mark()
-    l0 = lib.so.mdnn_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    barrier()
-    launches = lib.so.mdnn_launch_count() - l0
-    clocks = clk.stop(t_begin, clk.mark())
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms, launches, clocks = timed(ctx, args.steps, step, clk)
     ms_step = ms / args.steps
     value = world * B * args.steps / (ms / 1000.0)
 
     # ---- per-kernel live timing: a separate profiled pass (the per-launch event
     # pairs cost host time, so they stay out of the timed region above)
     np_steps = max(1, min(args.steps, 2))
-    barrier()
+    ctx["barrier"]()
     lib.check(lib.so.mdnn_profile_reset())
     lib.check(lib.so.mdnn_profile_enable(1))
     for _ in range(np_steps):
         step()
-    barrier()
+    ctx["barrier"]()
     lib.check(lib.so.mdnn_profile_enable(0))
     roof = roofline(lib, ms_step * np_steps)
 
@@ -311,46 +450,152 @@ def main():
     e2e = None
     if not args.no_e2e:
         # Each step's inputs cross from pinned host memory inside the timed
-        # region; they go through the trainer's prefetch queue (copy stream),
-        # so batch i+1 is copied while step i computes -- the way a loader
-        # feeds training.  Batch 0 is staged inside the region too.
-        barrier()
-        e0.record(stream)
-        for k, v in pinned.items():
-            tr.stage_data(k, v)
-        for i in range(args.steps):
-            if i + 1 < args.steps:
+        # region through the trainer's prefetch queue (copy stream), so batch
+        # i+1 is copied while step i computes -- the way a loader feeds
+        # training.  Batch 0 is staged inside the region too.
+        state = {"i": 0}
+
+        def e2e_step():
+            if state["i"] == 0:
                 for k, v in pinned.items():
-                    tr.stage_data(k, v)     # H2D copy of the next step's inputs (async)
-            step()                          # takes the oldest staged batch; loss D2H read
-        e1.record(stream)
-        barrier()
-        me = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([me], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            me = float(t.item())
+                    tr.stage_data(k, v)
+            if state["i"] + 1 < args.steps:
+                for k, v in pinned.items():
+                    tr.stage_data(k, v)  # H2D copy of the next step's inputs (async)
+            state["i"] += 1
+            step()  # takes the oldest staged batch; loss D2H read
+        me, _, _ = timed(ctx, args.steps, e2e_step)
         e2e = {"value": world * B * args.steps / (me / 1000.0), "unit": "samples/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 8, "ms_per_step": me / args.steps}
 
+    line = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count()))
+            os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
             r = cpu_sample(args.workload)
             if r:
-                cpu = {"value": r[0], "unit": "samples/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
-                       "kind": "reference", "sample": r[2], "sample_seconds": r[1]}
+                cpu = {"value": r[0], "unit": "samples/s", "cores": os.cpu_count(), "kind": "reference",
+                       "sample": r[2], "sample_seconds": r[1]}
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "c64 (fp32 complex)", "data": "synthetic",
-                "config": config_of(args, B, world), "roofline": roof["dominant"],
+                "vs_baseline": None, "dtype": "c64 (fp32 complex; convolutions TF32-RN operands, fp32 accumulate)",
+                "data": "synthetic", "config": config_of(args, world), "roofline": roof["dominant"],
                 "roofline_ahha": roof["ahha"], "roofline_kernels": roof["all"], "cpu_baseline": cpu, "e2e": e2e,
-                "clocks": clocks,
+                "clocks": clocks, "gpu_launches": int(launches),
+                "dp": {"exchange": "nccl-in-library (bucketed, comm stream)" if world > 1 and args.dp == "library"
+                       else ("torch.distributed" if world > 1 else "none"), "ranks": world}}
+    return line
+
+
+def run_sense_arm(args, ctx):
+    """configs[3]: S = A^H A + lambda alone and a 10-iteration CG solve (tol 0),
+    device arrays through the C ABI, CUDA events on the library stream.  value
+    = aggregate algorithmic GB/s of the S apply at the headline shape over all
+    ranks (each rank its own items: no collective); the sweep adds every shape's
+    S-apply and CG-10 GB/s."""
+    torch, lib = ctx["torch"], ctx["lib"]
+    rank, world, local = ctx["rank"], ctx["world"], ctx["local"]
+    from util import image_dims
+    p, src = peaks()
+    clk = ClockSampler(local)
+    sweep, head = [], None
+    launches = 0
+    for si, (X, Y, NC, B) in enumerate(SENSE_C4):
+        ph, cm, pat = sim_inputs(lib, X, Y, NC, B, first_item=rank * B) if si == 0 else _rand_inputs(X, Y, NC, B)
+        dev = [torch.from_numpy(np.ascontiguousarray(a.transpose())).to(f"cuda:{local}") for a in (cm, pat, ph)]
+        y = torch.zeros_like(dev[2])
+        A = [lib.arr(t) for t in dev + [y]]
+
+        def apply():
+            lib.check(lib.so.mdnn_sense_normal(C.byref(A[0]), C.byref(A[1]), C.c_float(0.05), C.byref(A[2]),
+                                               C.byref(A[3])))
+        it, st = C.c_long(), (C.c_double * 3)()
+
+        def solve():
+            lib.check(lib.so.mdnn_cg_normal_solve(C.byref(A[0]), C.byref(A[1]), C.c_float(0.05), C.byref(A[2]), 10,
+                                                  C.c_double(0.0), C.byref(A[3]), C.byref(it), st))
+        for _ in range(max(3, args.warmup)):
+            apply()
+            solve()
+        ctx["barrier"]()
+        if si == 0:
+            clk.start()
+            clk.wait_first()
+        ms, l1, clocks = timed(ctx, args.steps, apply, clk if si == 0 else None)
+        n_cg = max(1, args.steps // 4)
+        mcg, l2, _ = timed(ctx, n_cg, solve)
+        launches += l1 + l2
+        gbs = world * sense_bytes(X, Y, NC, B) * args.steps / (ms / 1e3) / 1e9
+        cg_gbs = world * 10 * sense_bytes(X, Y, NC, B, cg=True) * n_cg / (mcg / 1e3) / 1e9
+        row = {"image": [X, Y], "coils": NC, "batch_per_gpu": B, "apply_us": 1e3 * ms / args.steps,
+               "apply_gbs": gbs, "apply_frac": gbs / world / p["hbm_gbs"], "cg10_ms": mcg / n_cg,
+               "cg10_gbs": cg_gbs, "cg10_frac": cg_gbs / world / p["hbm_gbs"]}
+        if si == 0:
+            head = (ms, gbs, clocks, dev, A)
+            # per-kernel live timing of the headline shape (profiled pass)
+            lib.check(lib.so.mdnn_profile_reset())
+            lib.check(lib.so.mdnn_profile_enable(1))
+            for _ in range(2):
+                apply()
+                solve()
+            ctx["barrier"]()
+            lib.check(lib.so.mdnn_profile_enable(0))
+            roof = roofline(lib, 0.0)
+        sweep.append(row)
+    ms, gbs, clocks, dev, A = head
+    X, Y, NC, B = SENSE_C4[0]
+
+    # e2e: the same S apply through the C ABI on HOST arrays (H2D of coils and
+    # x, D2H of the result inside the timed region, every call)
+    e2e = None
+    if not args.no_e2e:
+        host = [t.cpu().pin_memory() for t in dev]
+        hy = torch.zeros_like(host[2]).pin_memory()
+        H = [lib.arr(t) for t in host + [hy]]
+
+        def apply_host():
+            lib.check(lib.so.mdnn_sense_normal(C.byref(H[0]), C.byref(H[1]), C.c_float(0.05), C.byref(H[2]),
+                                               C.byref(H[3])))
+        apply_host()
+        n_e = max(1, args.steps // 4)
+        me, _, _ = timed(ctx, n_e, apply_host)
+        e2e = {"value": world * sense_bytes(X, Y, NC, B) * n_e / (me / 1e3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(sum(t.numel() * 8 for t in host)), "d2h_bytes_per_step": int(hy.numel() * 8),
+               "ms_per_step": me / n_e}
+    line = None
+    if ctx["rank"] == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
+            r = cpu_sample("sense_c4")
+            if r:
+                cpu = {"value": r[0], "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference", "sample": r[2],
+                       "sample_seconds": r[1]}
+        line = {"metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "c64 (fp32 complex)", "data": "synthetic",
+                "config": config_of(args, world), "roofline": roof["dominant"], "roofline_ahha": roof["ahha"],
+                "roofline_kernels": roof["all"], "sweep": sweep, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
                 "gpu_launches": int(launches)}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    return line
+
+
+def _rand_inputs(X, Y, NC, B):
+    """Sweep shapes past the headline: random unit-normalised coils, random
+    image, the 4x + 28 ACL pattern (timing only)."""
+    from util import coil_dims, image_dims, pattern_dims
+    rng = np.random.default_rng(X * 1000 + NC)
+    cm = (rng.standard_normal(coil_dims(X, Y, NC, B)) + 1j * rng.standard_normal(coil_dims(X, Y, NC, B)))
+    cm /= np.sqrt((np.abs(cm) ** 2).sum(axis=3, keepdims=True))
+    ph = rng.standard_normal(image_dims(X, Y, B)) + 1j * rng.standard_normal(image_dims(X, Y, B))
+    pat = np.zeros(pattern_dims(Y), dtype=np.complex64)
+    pv = pat.reshape(-1)
+    for i in range(Y):
+        if i % 4 == 0 or min(i, Y - i) < 14:
+            pv[i] = 1
+    f = lambda a: np.asfortranarray(a.astype(np.complex64))  # noqa: E731
+    return f(ph), f(cm), f(pat)
 
 
 def roofline(lib, step_ms_total):
@@ -390,7 +635,7 @@ def roofline(lib, step_ms_total):
             peak, unit = tf32, "TFLOP/s"
         rows.append({"kernel": tag, "bound": bound, "achieved": ach, "peak": peak, "unit": unit,
                      "frac": ach / peak, "launches": n.value, "ms_total": ms.value,
-                     "share_of_step_time": ms.value / step_ms_total,
+                     "share_of_step_time": ms.value / step_ms_total if step_ms_total > 0 else None,
                      "traffic": traffic.get(tag), "peak_source": f"measured hbm_gbs ({src})" if bound == "hbm" else tf32_src})
     rows.sort(key=lambda r: -r["ms_total"])
     dom = rows[0] if rows else None

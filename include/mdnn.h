@@ -214,6 +214,21 @@ void mdnn_modl_cfg_default(mdnn_modl_cfg* c);
 void mdnn_varnet_cfg_default(mdnn_varnet_cfg* c);
 mdnn_model* mdnn_build_modl(const mdnn_modl_cfg* cfg);
 mdnn_model* mdnn_build_varnet(const mdnn_varnet_cfg* cfg);
+/* Model::rebatch (nn.hpp:82, used by train's minibatching optim.hpp:237-276):
+   the same network rebuilt for `batch` items (NULL + error 4 when the model has
+   no rebatch, e.g. hand-assembled fragments) */
+mdnn_model* mdnn_model_rebatch(const mdnn_model* m, long batch);
+/* per-block fragments of the networks (parity units of the C2 / C3 configs):
+   the MoDL CNN denoiser D_W(x) = x + CNN(x) of one unroll (modl_denoiser_fragment,
+   recon.hpp:714-803, with the output-by-name fix) and the VarNet regulariser
+   sum_f K^T Phi'(Re K x) of stage "it0" (varnet_reg_fragment, recon.hpp:522-609) */
+mdnn_model* mdnn_modl_denoiser(const mdnn_modl_cfg* cfg);
+/* the train-mode BN -> gamma -> beta -> CReLU chain of one denoiser layer
+   (recon.hpp:748-776) as a model: args x, <name>_bn_mean, <name>_bn_var,
+   <name>_g, <name>_beta; outputs <name>_bn_mean, <name>_bn_var, out.  The
+   product runs it as one fused channels-last node (bnblock.cu) */
+mdnn_model* mdnn_bn_block(const char* name, int rank, const long* dims);
+mdnn_model* mdnn_varnet_reg(const mdnn_varnet_cfg* cfg);
 /* SENSE fragments as models (recon.hpp:394-418, :807-820) */
 mdnn_model* mdnn_sense_normal_fragment(const mdnn_sense_dims* sd);
 mdnn_model* mdnn_sense_adjoint_fragment(const mdnn_sense_dims* sd);
@@ -253,8 +268,26 @@ int mdnn_trainer_forward_backward(mdnn_trainer* t, double* loss);
 int mdnn_trainer_grad_buffer(mdnn_trainer* t, float** ptr, long* n_floats);
 /* scale gradients (e.g. 1/world), realify/clip, Adam, prox, moving stats */
 int mdnn_trainer_update(mdnn_trainer* t, float grad_scale);
-/* run_step = forward_backward + update(1) */
+/* run_step = forward_backward + update(1); with a communicator attached
+   (mdnn_trainer_set_comm): forward_backward with the bucketed all-reduce,
+   then update_dp(world) */
 int mdnn_trainer_step(mdnn_trainer* t, double* loss);
+
+/* ---- data parallelism (BART batch stacking) ----
+ * Per-shard semantics: each replica runs the reference's run_step on its own
+ * batch shard (optim.hpp:314-399); gradients are summed over replicas and
+ * every replica applies the same update with 1/world, and the BN moving
+ * statistics (update_stats, optim.hpp:403-415) become the replica mean, so
+ * replicas stay bitwise identical.  The sync buffer is the whole payload:
+ * [weight gradients (grad_buffer's floats) | moving statistics], fp32. */
+int mdnn_trainer_sync_buffer(mdnn_trainer* t, float** ptr, long* n_floats);
+/* after the sync buffer was summed over `world` replicas (caller's collective) */
+int mdnn_trainer_update_dp(mdnn_trainer* t, int world);
+/* in-library NCCL: rank 0 creates the 128-byte id, the caller distributes it,
+   every rank attaches; mdnn_trainer_step then all-reduces gradient buckets on
+   a comm stream as the reverse sweep finalises them (CPU reference: error 4) */
+int mdnn_nccl_unique_id(uint8_t* id128);
+int mdnn_trainer_set_comm(mdnn_trainer* t, const uint8_t* id128, int nranks, int rank);
 int mdnn_trainer_n_weights(const mdnn_trainer* t);
 const char* mdnn_trainer_weight_name(const mdnn_trainer* t, int k);
 

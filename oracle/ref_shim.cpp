@@ -204,6 +204,30 @@ Model<R> embed_first_map(const SenseDims& sd, const Dims& img1)
 }
 
 // recon.hpp:714-803 with the CNN output resolved by name (fix for :799-801)
+// the per-layer BN -> gamma -> beta -> CReLU chain of the MoDL denoiser
+// (recon.hpp:748-776), train mode, as its own model (parity unit of the
+// product's fused bn-block node)
+Model<R> bn_chain(const std::string& ln, const Dims& cur, long l)
+{
+    const unsigned long bn_flags = (1UL << dim_x) | (1UL << dim_y) | (1UL << dim_batch);
+    Model<R> cnn = batchnorm_layer<R>(ln + "_bn", cur, bn_flags, true);
+    Dims gdims(max_rank, 1);
+    gdims[dim_chan] = cur[dim_chan];
+    auto gamma = plain_model(Nlop<R>(detail::tenmul<R>("bn_scale" + std::to_string(l), cur, cur, cur, gdims)),
+                             {{"x", ArgKind::Data, {}, nullptr, false},
+                              {ln + "_g", ArgKind::Weights, Initializer::constant(1), nullptr, false}},
+                             {"out"});
+    cnn = model_chain(cnn, gamma, "x");
+    auto beta = plain_model(Nlop<R>(std::make_shared<BroadcastAddNode<R>>(cur, gdims)),
+                            {{"x", ArgKind::Data, {}, nullptr, false},
+                             {ln + "_beta", ArgKind::Weights, Initializer::constant(0), nullptr, false}},
+                            {"out"});
+    cnn = model_chain(cnn, beta, "x");
+    auto act = plain_model(Nlop<R>(std::make_shared<CReluNode<R>>(cur)), {{"x", ArgKind::Data, {}, nullptr, false}},
+                           {"out"});
+    return model_chain(cnn, act, "x");
+}
+
 Model<R> fixed_modl_denoiser(const ModlConfig& cfg, const std::string& stat_suffix)
 {
     SenseDims sd = cfg.sense();
@@ -395,7 +419,15 @@ struct mdnn_trainer {
     std::vector<int> weight_args;
     std::vector<std::string> weight_names;
     std::vector<A> last_outs;
-    std::vector<float> flat;
+    std::vector<float> flat;  // [weight gradients | moving statistics] (sync buffer), fp32 pairs
+    size_t grad_floats = 0;
+    struct Stat {
+        std::string name;
+        int out = -1;
+        size_t off = 0;
+        long n = 0;
+    };
+    std::vector<Stat> stats;
 };
 
 // the oldest staged batch of every name becomes the current batch (shim of
@@ -769,6 +801,29 @@ mdnn_model* mdnn_build_varnet(const mdnn_varnet_cfg* cfg)
 {
     return guard_ptr<mdnn_model>([&] { return wrapm(fixed_build_varnet(to_varnet(cfg))); });
 }
+mdnn_model* mdnn_bn_block(const char* name, int rank, const long* dims)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(bn_chain(name, mkdims(rank, dims), 0)); });
+}
+mdnn_model* mdnn_modl_denoiser(const mdnn_modl_cfg* cfg)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(fixed_modl_denoiser(to_modl(cfg), "")); });
+}
+mdnn_model* mdnn_varnet_reg(const mdnn_varnet_cfg* cfg)
+{
+    // the reference fragment itself (only varnet_step_model has the wiring defect)
+    return guard_ptr<mdnn_model>([&] { return wrapm(detail::varnet_reg_fragment<R>(to_varnet(cfg), "it0")); });
+}
+mdnn_model* mdnn_model_rebatch(const mdnn_model* m, long batch)
+{
+    return guard_ptr<mdnn_model>([&] {
+        if (!m->m.rebatch)
+            throw ConfigError("model has no rebatch");
+        if (batch < 1)
+            throw ConfigError("rebatch: batch " + std::to_string(batch));
+        return wrapm(m->m.rebatch(batch));
+    });
+}
 mdnn_model* mdnn_sense_normal_fragment(const mdnn_sense_dims* sd)
 {
     return guard_ptr<mdnn_model>([&] { return wrapm(detail::sense_normal_fragment<R>(to_sd(sd))); });
@@ -863,6 +918,19 @@ mdnn_trainer* mdnn_trainer_create(const mdnn_model* model, const mdnn_train_cfg*
                 t->weight_names.push_back(t->joint.args[i].name);
                 nflat += 2 * size_t(md_size(t->joint.op.in_dims(int(i))));
             }
+        t->grad_floats = nflat;
+        for (size_t i = 0; i < t->joint.args.size(); i++)
+            if (t->joint.args[i].kind == ArgKind::MovingStats) {
+                mdnn_trainer::Stat s;
+                s.name = t->joint.args[i].name;
+                for (size_t o = 0; o < t->joint.out_names.size(); o++)
+                    if (t->joint.out_names[o] == s.name)
+                        s.out = int(o);
+                s.off = nflat;
+                s.n = md_size(t->joint.op.in_dims(int(i)));
+                nflat += 2 * size_t(s.n);
+                t->stats.push_back(s);
+            }
         t->flat.assign(nflat, 0.f); // fixed buffer: callers may hold its address
         return t.release();
     });
@@ -917,6 +985,16 @@ int mdnn_trainer_forward_backward(mdnn_trainer* t, double* loss)
                 t->flat[off++] = float(g.data()[k].imag());
             }
         }
+        // this shard's new moving statistics (the data-parallel sync payload's tail)
+        for (const auto& s : t->stats) {
+            if (s.out < 0)
+                continue;
+            A v = t->last_outs[s.out].has_default_strides() ? t->last_outs[s.out] : t->last_outs[s.out].clone();
+            for (long k = 0; k < s.n; k++) {
+                t->flat[s.off + 2 * k] = float(v.data()[k].real());
+                t->flat[s.off + 2 * k + 1] = float(v.data()[k].imag());
+            }
+        }
         if (loss)
             *loss = lv;
     });
@@ -925,8 +1003,49 @@ int mdnn_trainer_forward_backward(mdnn_trainer* t, double* loss)
 int mdnn_trainer_grad_buffer(mdnn_trainer* t, float** ptr, long* n)
 {
     *ptr = t->flat.data();
+    *n = long(t->grad_floats);
+    return MDNN_OK;
+}
+
+int mdnn_trainer_sync_buffer(mdnn_trainer* t, float** ptr, long* n)
+{
+    *ptr = t->flat.data();
     *n = long(t->flat.size());
     return MDNN_OK;
+}
+
+int mdnn_trainer_update_dp(mdnn_trainer* t, int world)
+{
+    if (world < 1) {
+        g_err = "trainer: world size " + std::to_string(world);
+        return 4;
+    }
+    int rc = mdnn_trainer_update(t, 1.f / float(world));
+    if (rc != MDNN_OK)
+        return rc;
+    return guard([&] {
+        // replica mean of the moving statistics summed in the sync buffer
+        for (const auto& s : t->stats) {
+            auto& w = t->weights.at(s.name);
+            A v(w.dims());
+            for (long k = 0; k < s.n; k++)
+                v.data()[k] = std::complex<R>(R(t->flat[s.off + 2 * k] * (1.f / float(world))),
+                                              R(t->flat[s.off + 2 * k + 1] * (1.f / float(world))));
+            w = v;
+        }
+    });
+}
+
+int mdnn_nccl_unique_id(uint8_t*)
+{
+    g_err = "NCCL is not part of the CPU reference";
+    return 4;
+}
+
+int mdnn_trainer_set_comm(mdnn_trainer*, const uint8_t*, int, int)
+{
+    g_err = "NCCL is not part of the CPU reference";
+    return 4;
 }
 
 int mdnn_trainer_update(mdnn_trainer* t, float grad_scale)

@@ -158,6 +158,10 @@ _SIGS = {
     "mdnn_sense_normal_fragment": (P, [C.POINTER(mdnn_sense_dims)]),
     "mdnn_sense_adjoint_fragment": (P, [C.POINTER(mdnn_sense_dims)]),
     "mdnn_modl_normal_plus_lambda": (P, [C.POINTER(mdnn_sense_dims)]),
+    "mdnn_model_rebatch": (P, [P, L]),
+    "mdnn_modl_denoiser": (P, [C.POINTER(mdnn_modl_cfg)]),
+    "mdnn_bn_block": (P, [C.c_char_p, C.c_int, L]),
+    "mdnn_varnet_reg": (P, [C.POINTER(mdnn_varnet_cfg)]),
     "mdnn_loss_model_mse": (P, [C.c_int, L]),
     "mdnn_sim_item": (C.c_int, [C.c_uint64, C.c_long, C.c_long, C.c_long, C.c_long, P, P]),
     "mdnn_sim_pattern": (C.c_int, [C.c_long, C.c_long, C.c_long, P]),
@@ -173,6 +177,10 @@ _SIGS = {
     "mdnn_trainer_grad_buffer": (C.c_int, [P, C.POINTER(C.POINTER(C.c_float)), L]),
     "mdnn_trainer_update": (C.c_int, [P, C.c_float]),
     "mdnn_trainer_step": (C.c_int, [P, C.POINTER(C.c_double)]),
+    "mdnn_trainer_sync_buffer": (C.c_int, [P, C.POINTER(C.POINTER(C.c_float)), L]),
+    "mdnn_trainer_update_dp": (C.c_int, [P, C.c_int]),
+    "mdnn_nccl_unique_id": (C.c_int, [P]),
+    "mdnn_trainer_set_comm": (C.c_int, [P, P, C.c_int, C.c_int]),
     "mdnn_trainer_n_weights": (C.c_int, [P]),
     "mdnn_trainer_weight_name": (C.c_char_p, [P, C.c_int]),
     "mdnn_reconet_opts_default": (None, [C.POINTER(mdnn_reconet_opts)]),

@@ -108,32 +108,45 @@ __global__ void __launch_bounds__(kT) k_stats(double* __restrict__ part, const f
     // fp32 running sums per thread (a few hundred terms each, fixed order),
     // folded across threads and blocks in double: the stream is HBM-bound,
     // a double accumulate per element was not (FP64 + conversions)
+    // shifted by the thread's first pixel (re-centred in double below): the
+    // sum of squares carries the spread, not the mean
     float f[2][3] = {{0, 0, 0}, {0, 0, 0}};
+    float2 shr{0.f, 0.f}, shi{0.f, 0.f};
+    long cnt = 0;
+    if (p0 + q.pl < p1) {
+        shr = ld2(x + (p0 + q.pl) * 2 * C + 2 * q.l);
+        shi = ld2(x + (p0 + q.pl) * 2 * C + C + 2 * q.l);
+    }
     constexpr int U = 8; // 128 B of loads in flight per thread (latency-bound otherwise)
     for (long p = p0 + q.pl; p < p1; p += U * q.ppb) {
         float2 re[U], im[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const long pp = p + u * q.ppb;
-            re[u] = pp < p1 ? ld2(x + pp * 2 * C + 2 * q.l) : float2{0.f, 0.f};
-            im[u] = pp < p1 ? ld2(x + pp * 2 * C + C + 2 * q.l) : float2{0.f, 0.f};
+            re[u] = pp < p1 ? ld2(x + pp * 2 * C + 2 * q.l) : shr;
+            im[u] = pp < p1 ? ld2(x + pp * 2 * C + C + 2 * q.l) : shi;
+            cnt += pp < p1;
         }
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            f[0][0] += re[u].x;
-            f[0][1] += im[u].x;
-            f[0][2] = fmaf(re[u].x, re[u].x, fmaf(im[u].x, im[u].x, f[0][2]));
-            f[1][0] += re[u].y;
-            f[1][1] += im[u].y;
-            f[1][2] = fmaf(re[u].y, re[u].y, fmaf(im[u].y, im[u].y, f[1][2]));
+        for (int u = 0; u < U; u++) { // out-of-range slots hold the shift: zero contribution
+            const float2 dr{re[u].x - shr.x, re[u].y - shr.y}, di{im[u].x - shi.x, im[u].y - shi.y};
+            f[0][0] += dr.x;
+            f[0][1] += di.x;
+            f[0][2] = fmaf(dr.x, dr.x, fmaf(di.x, di.x, f[0][2]));
+            f[1][0] += dr.y;
+            f[1][1] += di.y;
+            f[1][2] = fmaf(dr.y, dr.y, fmaf(di.y, di.y, f[1][2]));
         }
     }
     double a[2][3];
+    const double n = double(cnt);
+    const double sr[2] = {shr.x, shr.y}, si[2] = {shi.x, shi.y};
 #pragma unroll
-    for (int k = 0; k < 2; k++)
-#pragma unroll
-        for (int j = 0; j < 3; j++)
-            a[k][j] = f[k][j];
+    for (int k = 0; k < 2; k++) {
+        a[k][0] = n * sr[k] + f[k][0];
+        a[k][1] = n * si[k] + f[k][1];
+        a[k][2] = sr[k] * (n * sr[k] + 2.0 * f[k][0]) + si[k] * (n * si[k] + 2.0 * f[k][1]) + f[k][2];
+    }
     fold_lanes<3>(part, a, q, C);
 }
 

@@ -592,6 +592,63 @@ void mdnn_varnet_cfg_default(mdnn_varnet_cfg* c)
     c->maps = d.maps;
     c->batch = d.batch;
 }
+static ModlConfig to_modl(const mdnn_modl_cfg* c)
+{
+    ModlConfig m;
+    m.iterations = c->iterations;
+    m.layers = c->layers;
+    m.filters = c->filters;
+    m.kernel = c->kernel;
+    m.cg_iter = c->cg_iter;
+    m.cg_tol = c->cg_tol;
+    m.lambda_init = c->lambda_init;
+    m.im_x = c->im_x;
+    m.im_y = c->im_y;
+    m.coils = c->coils;
+    m.maps = c->maps;
+    m.batch = c->batch;
+    m.train_mode = c->train_mode != 0;
+    return m;
+}
+static VarNetConfig to_varnet(const mdnn_varnet_cfg* c)
+{
+    VarNetConfig v;
+    v.iterations = c->iterations;
+    v.filters = c->filters;
+    v.kernel = c->kernel;
+    v.rbf = c->rbf;
+    v.im_x = c->im_x;
+    v.im_y = c->im_y;
+    v.coils = c->coils;
+    v.maps = c->maps;
+    v.batch = c->batch;
+    return v;
+}
+mdnn_model* mdnn_bn_block(const char* name, int rank, const long* dims)
+{
+    return guard_ptr<mdnn_model>([&] {
+        Dims d(dims, dims + rank);
+        return wrapm(bn_block_fragment(name, d));
+    });
+}
+mdnn_model* mdnn_modl_denoiser(const mdnn_modl_cfg* c)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(modl_denoiser(to_modl(c), "")); });
+}
+mdnn_model* mdnn_varnet_reg(const mdnn_varnet_cfg* c)
+{
+    return guard_ptr<mdnn_model>([&] { return wrapm(varnet_reg(to_varnet(c), "it0")); });
+}
+mdnn_model* mdnn_model_rebatch(const mdnn_model* m, long batch)
+{
+    return guard_ptr<mdnn_model>([&] {
+        if (!m->m.rebatch)
+            throw ConfigError("model has no rebatch");
+        if (batch < 1)
+            throw ConfigError("rebatch: batch " + std::to_string(batch));
+        return wrapm(m->m.rebatch(batch));
+    });
+}
 mdnn_model* mdnn_build_modl(const mdnn_modl_cfg* c)
 {
     return guard_ptr<mdnn_model>([&] {
@@ -746,6 +803,25 @@ int mdnn_trainer_step(mdnn_trainer* t, double* loss)
         if (loss)
             *loss = l;
     });
+}
+int mdnn_trainer_sync_buffer(mdnn_trainer* t, float** ptr, long* n)
+{
+    return guard([&] {
+        *ptr = t->t->sync_buffer();
+        *n = t->t->sync_floats();
+    });
+}
+int mdnn_trainer_update_dp(mdnn_trainer* t, int world)
+{
+    return guard([&] { t->t->update_dp(world); });
+}
+int mdnn_nccl_unique_id(uint8_t* id128)
+{
+    return guard([&] { nccl_unique_id(id128); });
+}
+int mdnn_trainer_set_comm(mdnn_trainer* t, const uint8_t* id128, int nranks, int rank)
+{
+    return guard([&] { t->t->set_comm(std::make_unique<Comm>(id128, nranks, rank)); });
 }
 int mdnn_trainer_n_weights(const mdnn_trainer* t) { return int(t->t->weight_names().size()); }
 const char* mdnn_trainer_weight_name(const mdnn_trainer* t, int k) { return t->t->weight_names().at(k).c_str(); }

@@ -405,19 +405,25 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
                 tmem_ld16(acc + jc * 16, v);
                 tmem_ld_wait();
                 float* o = out + ((long(b) * Y + py0) * X + x0) * N + n;
+                // fp32 sums shifted by the chunk's first value (always in range), so the
+                // sum of squares carries the spread, not the mean; re-centred in double
+                const float sh = v[0];
                 float fs = 0.f, fq = 0.f;
+                int nv = 0;
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
                     const int l = j >> 3, xo = j & 7;
                     if ((full_x || x0 + xo < X) && py0 + l < Y) {
                         if (dbg != 1)
                             o[(long(l) * X + xo) * N] = v[j];
-                        fs += v[j];
-                        fq = fmaf(v[j], v[j], fq);
+                        const float d = v[j] - sh;
+                        fs += d;
+                        fq = fmaf(d, d, fq);
+                        nv++;
                     }
                 }
-                s_acc += fs;
-                q_acc += fq;
+                s_acc += double(nv) * sh + fs;
+                q_acc += double(sh) * (double(nv) * sh + 2.0 * fs) + fq;
                 if (be.part) {
                     const float* xp = be.x + ((long(b) * Y + py0) * X + x0) * N + bc;
                     float xr[16], xi[16];

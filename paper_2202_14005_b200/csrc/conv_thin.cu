@@ -68,18 +68,12 @@ __device__ __forceinline__ void load_halo(float2* tile, const float2* __restrict
 // per thread (P = 2 when F is even: the window loads and the loop overhead are
 // shared by two channels and the stores are 8-byte channel pairs -- the P = 1
 // form was issue-bound with the FMA pipe half busy).
-// Optional epilogue work on the produced wide tensor (P = 2, F = 64), per
-// block partials in the layouts of bnblock.cu's final kernels:
-//   stats: [blk][2F real channels][sum, sum of squares]           (forward BN statistics)
-//   bpart: [blk][2F][3] CReLU-masked BN-backward sums, bx/mu/.. = that BN's state
+// Optional epilogue work on the produced wide tensor (P = 2, F = 64): per
+// block forward BN statistics [blk][2F real channels][sum, sum of squares] in
+// the layout of bnblock.cu's final kernels.  (The last BN block's backward
+// reduction is emitted by the tensor-core expand of conv_thin_tc.cu.)
 struct ThinEpi {
     double* stats = nullptr;
-    double* bpart = nullptr;
-    const float* bx = nullptr;
-    const float2* mu = nullptr;
-    const float* istd = nullptr;
-    const float2* gamma = nullptr;
-    const float2* beta = nullptr;
 };
 
 template<int K, int P>
@@ -102,22 +96,13 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
         for (int t = 0; t < K * K; t++)
             u[q][t] = U[t * F + f + q];
     __syncthreads();
-    // epilogue accumulators: per channel q of the pair, Re lane and Im lane
-    //   stats: (sum, sum sq) ; bn: (sum ge, ge * (hr | hi), ge * (-hi | hr))
-    float es[P][2][3] = {};
-    float2 bmu[P], bg[P], bb[P];
-    float bs[P];
-    if constexpr (P == 2) {
-        if (ep.bpart) {
-#pragma unroll
-            for (int q = 0; q < P; q++) {
-                bmu[q] = ep.mu[f + q];
-                bs[q] = ep.istd[f + q];
-                bg[q] = ep.gamma[f + q];
-                bb[q] = ep.beta[f + q];
-            }
-        }
-    }
+    // epilogue accumulators: per channel q of the pair, Re lane and Im lane:
+    // (sum, sum sq) of the values shifted by this thread's first value (esh),
+    // re-centred in double at the fold -- the sum of squares carries the
+    // spread, not the mean (no E|x|^2 - |mu|^2 cancellation)
+    float es[P][2][2] = {};
+    float esh[P][2] = {};
+    int ecount = 0;
     const int nseg = max(1, lanes / TY), seglen = TX / nseg;
     for (int it = lane; it < TY * nseg; it += lanes) {
         const int row = it / nseg, xs = (it % nseg) * seglen;
@@ -161,32 +146,18 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
                     *reinterpret_cast<float2*>(op) = float2{acc[0].x, acc[1].x};
                     *reinterpret_cast<float2*>(op + F) = float2{acc[0].y, acc[1].y};
                     if (ep.stats) {
+                        if (ecount++ == 0) {
 #pragma unroll
-                        for (int q = 0; q < P; q++) {
-                            es[q][0][0] += acc[q].x;
-                            es[q][0][1] = fmaf(acc[q].x, acc[q].x, es[q][0][1]);
-                            es[q][1][0] += acc[q].y;
-                            es[q][1][1] = fmaf(acc[q].y, acc[q].y, es[q][1][1]);
+                            for (int q = 0; q < P; q++)
+                                esh[q][0] = acc[q].x, esh[q][1] = acc[q].y;
                         }
-                    }
-                    if (ep.bpart) {
-                        const long pofs = op - out - f; // pixel * 2F
-                        const float2 xr = *reinterpret_cast<const float2*>(ep.bx + pofs + f);
-                        const float2 xi = *reinterpret_cast<const float2*>(ep.bx + pofs + F + f);
 #pragma unroll
                         for (int q = 0; q < P; q++) {
-                            // yhat and z exactly as bn_z (bnblock.cu)
-                            const float hr = ((q ? xr.y : xr.x) - bmu[q].x) * bs[q];
-                            const float hi = ((q ? xi.y : xi.x) - bmu[q].y) * bs[q];
-                            const float zr = bg[q].x * hr - bg[q].y * hi + bb[q].x;
-                            const float zi = bg[q].x * hi + bg[q].y * hr + bb[q].y;
-                            const float gr = zr > 0.f ? acc[q].x : 0.f, gi = zi > 0.f ? acc[q].y : 0.f;
-                            es[q][0][0] += gr;
-                            es[q][0][1] = fmaf(gr, hr, es[q][0][1]);
-                            es[q][0][2] = fmaf(gr, -hi, es[q][0][2]);
-                            es[q][1][0] += gi;
-                            es[q][1][1] = fmaf(gi, hi, es[q][1][1]);
-                            es[q][1][2] = fmaf(gi, hr, es[q][1][2]);
+                            const float dr = acc[q].x - esh[q][0], di = acc[q].y - esh[q][1];
+                            es[q][0][0] += dr;
+                            es[q][0][1] = fmaf(dr, dr, es[q][0][1]);
+                            es[q][1][0] += di;
+                            es[q][1][1] = fmaf(di, di, es[q][1][1]);
                         }
                     }
                 } else {
@@ -202,27 +173,28 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
         }
     }
     if constexpr (P == 2) {
-        if (ep.stats || ep.bpart) {
+        if (ep.stats) {
             // fixed-order fold over the `lanes` threads of each channel pair
-            constexpr int NV = P * 2 * 3;
-            __shared__ float red[NT * NV];
+            constexpr int NV = P * 2 * 2;
+            __shared__ double red[NT * NV];
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < P; q++)
 #pragma unroll
-                for (int c2 = 0; c2 < 2; c2++)
-#pragma unroll
-                    for (int v = 0; v < 3; v++)
-                        red[threadIdx.x * NV + (q * 2 + c2) * 3 + v] = es[q][c2][v];
+                for (int c2 = 0; c2 < 2; c2++) {
+                    const double sh = esh[q][c2], n = ecount;
+                    red[threadIdx.x * NV + (q * 2 + c2) * 2] = n * sh + es[q][c2][0];
+                    red[threadIdx.x * NV + (q * 2 + c2) * 2 + 1] = sh * (n * sh + 2.0 * es[q][c2][0]) + es[q][c2][1];
+                }
             __syncthreads();
             const long blk = blockIdx.x + long(gridDim.x) * (blockIdx.y + long(gridDim.y) * blockIdx.z);
-            const int nv = ep.stats ? 2 : 3;
-            double* dst = ep.stats ? ep.stats : ep.bpart;
+            constexpr int nv = 2;
+            double* dst = ep.stats;
             for (int e = threadIdx.x; e < FP * P * 2 * nv; e += NT) {
                 const int v = e % nv, qc = (e / nv) % (P * 2), fp = e / (nv * P * 2);
                 double acc = 0;
                 for (int l = 0; l < lanes; l++)
-                    acc += double(red[(l * FP + fp) * NV + qc * 3 + v]);
+                    acc += red[(l * FP + fp) * NV + qc * 2 + v];
                 const int q = qc >> 1, c2 = qc & 1;
                 const int n = c2 * F + fp * P + q; // real channel: Re part c, Im part F + c
                 dst[(blk * 2 * F + n) * nv + v] = acc;

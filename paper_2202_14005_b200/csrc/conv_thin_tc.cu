@@ -429,16 +429,19 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
                 }
                 sb ^= 1;
                 const int nv = npix - p0 < 16 ? int(npix - p0) : 16;
+                // shifted by the chunk's first value, re-centred in double (see conv_tc.cu)
+                const float sh = v[0];
                 float fs = 0.f, fq = 0.f;
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
                     if (j < nv) {
-                        fs += v[j];
-                        fq = fmaf(v[j], v[j], fq);
+                        const float d = v[j] - sh;
+                        fs += d;
+                        fq = fmaf(d, d, fq);
                     }
                 }
-                s_acc += fs;
-                q_acc += fq;
+                s_acc += double(nv) * sh + fs;
+                q_acc += double(sh) * (double(nv) * sh + 2.0 * fs) + fq;
                 if (be.part) {
                     const float* xp = be.x + p0 * 128 + bc;
                     float xr[16], xi[16];

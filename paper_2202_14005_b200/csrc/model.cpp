@@ -186,7 +186,7 @@ Model modl_normal_plus_lambda(const SenseDims& sd)
                  {data_arg("x"), data_arg("coils"), data_arg("pattern"), data_arg("lambda")}, {"out"});
 }
 
-namespace {
+// builder fragments (recon.hpp:421-680)
 
 Model scalar_mul_fragment(const SenseDims& sd, const std::string& scalar_name, ArgKind kind)
 {
@@ -219,6 +219,20 @@ Model embed_first_map(const SenseDims& sd)
     small[dim_maps] = 1;
     Dims corner(max_rank, 0);
     return plain(Nlop(node_pad(small, sd.image(), corner, false)), {data_arg("x")}, {"out"});
+}
+
+// one layer's train-mode BN -> gamma -> beta -> CReLU (recon.hpp:748-776) as
+// the fused channels-last node, standalone (no TF32 rounding of its output or
+// input cotangent: no tensor-core conv neighbours)
+Model bn_block_fragment(const std::string& ln, const Dims& cur)
+{
+    return plain(Nlop(node_bnblock(cur, false, false)),
+                 {data_arg("x"),
+                  Arg{ln + "_bn_mean", ArgKind::MovingStats, Initializer::constant(0), ProxKind::None, false},
+                  Arg{ln + "_bn_var", ArgKind::MovingStats, Initializer::constant(1), ProxKind::None, false},
+                  Arg{ln + "_g", ArgKind::Weights, Initializer::constant(1), ProxKind::None, false},
+                  Arg{ln + "_beta", ArgKind::Weights, Initializer::constant(0), ProxKind::None, false}},
+                 {ln + "_bn_mean", ln + "_bn_var", "out"});
 }
 
 // recon.hpp:714-803, CNN output resolved by name (the shipped builder's
@@ -409,7 +423,7 @@ Model varnet_step(const VarNetConfig& cfg, const std::string& prefix)
     return model_dedupe(std::move(m));
 }
 
-} // namespace
+
 
 void ModlConfig::validate() const
 {

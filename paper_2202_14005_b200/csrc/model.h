@@ -122,6 +122,11 @@ Model batchnorm_layer(const std::string& name, const Dims& dims, unsigned long f
 Model loss_model_mse(const Dims& dims);
 
 Model sense_normal_fragment(const SenseDims& sd);
+struct ModlConfig;
+struct VarNetConfig;
+Model modl_denoiser(const ModlConfig& cfg, const std::string& stat_suffix);
+Model bn_block_fragment(const std::string& ln, const Dims& cur);
+Model varnet_reg(const VarNetConfig& cfg, const std::string& prefix);
 Model sense_adjoint_fragment(const SenseDims& sd);
 Model modl_normal_plus_lambda(const SenseDims& sd);
 

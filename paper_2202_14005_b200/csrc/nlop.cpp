@@ -153,7 +153,8 @@ DArray Nlop::derivative(int o, int i, const DArray& dx)
     return DArray(out_dims(o)); // structurally zero
 }
 
-std::vector<DArray> Nlop::adjoint_all(int o, const DArray& dy, const std::vector<char>& want_in)
+std::vector<DArray> Nlop::adjoint_all(int o, const DArray& dy, const std::vector<char>& want_in,
+                                      const FinalFn& on_final)
 {
     check_state();
     if (dy.dims != out_dims(o))
@@ -175,11 +176,36 @@ std::vector<DArray> Nlop::adjoint_all(int o, const DArray& dy, const std::vector
     auto os = outputs_.at(o);
     cot[os.node][os.port] = dy;
 
+    // last_use[i]: position in the reverse sweep after which no node adds to
+    // input i's cotangent (-1: no needed node consumes it)
+    std::vector<int> last_use(n_in_, -1);
+    {
+        int pos = 0;
+        for (auto it = topo_.rbegin(); it != topo_.rend(); ++it, ++pos)
+            if (needs[*it])
+                for (auto s : in_srcs_[*it])
+                    if (s.node < 0)
+                        last_use[s.port] = pos;
+    }
+    auto finish = [&](int i) {
+        if (!in_cot[i].valid())
+            in_cot[i] = DArray(in_dims_[i]);
+        else
+            in_cot[i] = as_layout(in_cot[i], Layout::CANON);
+        if (on_final)
+            on_final(i, in_cot[i]);
+    };
+    for (int i = 0; i < n_in_; i++)
+        if (want[i] && last_use[i] < 0)
+            finish(i);
+
     std::vector<DArray> contrib;
     std::vector<char> wk;
     std::vector<const void*> hints;
+    int pos = -1;
     for (auto it = topo_.rbegin(); it != topo_.rend(); ++it) {
         int ni = *it;
+        ++pos;
         if (!needs[ni])
             continue;
         auto& node = *nodes_[ni];
@@ -211,14 +237,11 @@ std::vector<DArray> Nlop::adjoint_all(int o, const DArray& dy, const std::vector
             }
             contrib.clear();
         }
-    }
-    for (int i = 0; i < n_in_; i++) {
-        if (!want[i])
-            continue;
-        if (!in_cot[i].valid())
-            in_cot[i] = DArray(in_dims_[i]);
-        else
-            in_cot[i] = as_layout(in_cot[i], Layout::CANON);
+        for (auto s : in_srcs_[ni])
+            if (s.node < 0 && want[s.port] && last_use[s.port] == pos) {
+                last_use[s.port] = -2; // a node may read the same input twice
+                finish(s.port);
+            }
     }
     return in_cot;
 }

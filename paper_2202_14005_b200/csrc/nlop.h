@@ -115,7 +115,13 @@ public:
     // false evaluates without retaining state, nlop.hpp:363-386)
     std::vector<DArray> run_forward(const std::vector<DArray>& in, bool store);
     DArray derivative(int o, int i, const DArray& dx);
-    std::vector<DArray> adjoint_all(int o, const DArray& dy, const std::vector<char>& want = {});
+    // on_final(i, g): called during the reverse sweep as soon as wanted input
+    // i's cotangent g is complete (its last consumer has been processed), in
+    // the order the sweep finalises them -- lets a trainer start the gradient
+    // all-reduce of early buckets under the rest of the backward pass
+    using FinalFn = std::function<void(int, const DArray&)>;
+    std::vector<DArray> adjoint_all(int o, const DArray& dy, const std::vector<char>& want = {},
+                                    const FinalFn& on_final = nullptr);
     DArray adjoint_derivative(int o, int i, const DArray& dy);
 
     const std::vector<NodePtr>& nodes() const { return nodes_; }

@@ -37,7 +37,21 @@ Trainer::Trainer(const Model& model, const TrainConfig& cfg, uint64_t seed) : cf
         }
     }
     flat_n_ = off;
-    flat_ = DArray(Dims{std::max(1L, flat_n_)}, true);
+    // moving statistics (BN means / variances): the tail of the sync buffer
+    for (const auto& a : joint_.args) {
+        if (a.kind != ArgKind::MovingStats)
+            continue;
+        StatSlot s;
+        s.name = a.name;
+        for (size_t o = 0; o < joint_.out_names.size(); o++)
+            if (joint_.out_names[o] == a.name)
+                s.out = int(o);
+        s.off = flat_n_ + stats_n_;
+        s.n = md_size(joint_.op.in_dims(joint_.arg_index(a.name)));
+        stats_n_ += s.n;
+        stats_.push_back(s);
+    }
+    flat_ = DArray(Dims{std::max(1L, flat_n_ + stats_n_)}, true);
     float* v;
     CUDA_CHECK(cudaMalloc(&v, sizeof(float) * std::max(1L, flat_n_)));
     CUDA_CHECK(cudaMemset(v, 0, sizeof(float) * std::max(1L, flat_n_)));
@@ -47,6 +61,37 @@ Trainer::Trainer(const Model& model, const TrainConfig& cfg, uint64_t seed) : cf
         adam_[k].m = DArray(joint_.op.in_dims(wargs_[k]), true);
         adam_[k].v = v + woff_[k];
     }
+}
+
+Trainer::~Trainer()
+{
+    // a staged batch's H2D copy may still be running on the copy stream: order
+    // its release (stream-ordered free on the compute stream) after the copy
+    auto& c = ctx();
+    for (auto& [name, q] : staged_)
+        for (auto& s : q) {
+            cudaStreamWaitEvent(c.stream, s.ev, 0);
+            cudaEventDestroy(s.ev);
+        }
+    staged_.clear();
+    if (comm_)
+        cudaStreamSynchronize(comm_->stream());
+    if (ev_sync_)
+        cudaEventDestroy(ev_sync_);
+    if (ev_done_)
+        cudaEventDestroy(ev_done_);
+}
+
+void Trainer::allreduce_range(long off, long n)
+{
+    if (!ev_sync_) {
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev_sync_, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventCreateWithFlags(&ev_done_, cudaEventDisableTiming));
+    }
+    // the producers of this range were enqueued on the compute stream
+    CUDA_CHECK(cudaEventRecord(ev_sync_, ctx().stream));
+    CUDA_CHECK(cudaStreamWaitEvent(comm_->stream(), ev_sync_, 0));
+    comm_->allreduce_sum(flat_.fdata() + 2 * off, 2 * n);
 }
 
 void Trainer::set_data(const std::string& name, DArray a)
@@ -156,14 +201,57 @@ double Trainer::forward_backward()
     const auto t0 = std::chrono::steady_clock::now();
     take_staged();
     last_outs_ = joint_.op.apply(gather_inputs());
+    // this shard's new moving statistics -> tail of the sync buffer; with a
+    // communicator their all-reduce runs under the whole backward pass
+    for (const auto& s : stats_)
+        if (s.out >= 0)
+            launch_copy(flat_.data() + s.off, last_outs_[s.out].data(), s.n);
+    if (comm_ && stats_n_ > 0)
+        allreduce_range(flat_n_, stats_n_);
     std::vector<char> want(joint_.args.size(), 0);
-    for (int i : wargs_)
-        want[i] = 1;
-    DArray one = DArray::scalar(1.f);
-    auto grads = joint_.op.adjoint_all(loss_idx_, one, want);
+    std::vector<int> slot(joint_.args.size(), -1);
     for (size_t k = 0; k < wargs_.size(); k++) {
-        const DArray& g = grads[wargs_[k]];
+        want[wargs_[k]] = 1;
+        slot[wargs_[k]] = int(k);
+    }
+    // gradient buckets: a maximal run of consecutive finalised, not yet reduced
+    // weights is all-reduced once it holds bucket_min_floats_ (or nothing is
+    // left); the sweep's finalisation order is deterministic, so every rank
+    // issues the same collectives in the same order
+    const int nw = int(wargs_.size());
+    std::vector<char> fin(nw, 0), sent(nw, 0);
+    int n_fin = 0;
+    auto flush = [&](bool all) {
+        for (int k = 0; k < nw;) {
+            if (!fin[k] || sent[k]) {
+                k++;
+                continue;
+            }
+            int e = k;
+            long n = 0;
+            while (e < nw && fin[e] && !sent[e])
+                n += md_size(joint_.op.in_dims(wargs_[e++]));
+            if (all || 2 * n >= bucket_min_floats_) {
+                allreduce_range(woff_[k], n);
+                for (int q = k; q < e; q++)
+                    sent[q] = 1;
+            }
+            k = e;
+        }
+    };
+    DArray one = DArray::scalar(1.f);
+    joint_.op.adjoint_all(loss_idx_, one, want, [&](int i, const DArray& g) {
+        const int k = slot[i];
+        if (k < 0)
+            return;
         launch_copy(flat_.data() + woff_[k], g.data(), g.size());
+        fin[k] = 1;
+        if (comm_)
+            flush(++n_fin == nw);
+    });
+    if (comm_) {
+        CUDA_CHECK(cudaEventRecord(ev_done_, comm_->stream()));
+        CUDA_CHECK(cudaStreamWaitEvent(ctx().stream, ev_done_, 0));
     }
     launch_check_finite(flat_.data(), flat_n_);
     cfloat lv;
@@ -221,6 +309,19 @@ void Trainer::update(float grad_scale)
         w = nw;
     }
     update_stats(last_outs_);
+}
+
+void Trainer::update_dp(int world)
+{
+    if (world < 1)
+        throw ConfigError("trainer: world size " + std::to_string(world));
+    update(1.f / float(world));
+    // replica mean of the moving statistics (summed in the sync buffer)
+    for (const auto& s : stats_) {
+        DArray v(joint_.op.in_dims(joint_.arg_index(s.name)), false);
+        launch_scale(v.data(), flat_.data() + s.off, cfloat{1.f / float(world), 0.f}, s.n);
+        weights_[s.name] = v;
+    }
 }
 
 // update_stats: moving-statistics outputs feed their same-named inputs (optim.hpp:403-415)

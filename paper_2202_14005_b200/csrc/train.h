@@ -4,6 +4,7 @@
 // moving-statistics carry-over (update_stats, optim.hpp:403-415).
 #pragma once
 
+#include "comm.h"
 #include "model.h"
 
 #include <deque>
@@ -21,6 +22,7 @@ struct TrainConfig {
 class Trainer {
 public:
     Trainer(const Model& model, const TrainConfig& cfg, uint64_t seed);
+    ~Trainer(); // drains staged batches (their H2D copies) before the buffers go back to the pool
 
     void set_data(const std::string& name, DArray a);
     // prefetch: queue a host batch for `name`, copied asynchronously on the
@@ -34,14 +36,28 @@ public:
 
     double forward_backward();           // returns loss (synchronises once)
     void update(float grad_scale);       // Adam on the flat buffer
+    // data parallel: the sync buffer after forward_backward holds this shard's
+    // gradients and new moving statistics; after it has been summed over `world`
+    // replicas, update_dp applies Adam to gradient / world and sets every moving
+    // statistic to the replica mean, so replicas stay bitwise identical
+    void update_dp(int world);
     double step()
     {
         if (cfg_.algo == OptAlgo::Ipalm)
             return ipalm_step();
         double l = forward_backward();
-        update(1.f);
+        if (comm_)
+            update_dp(comm_->nranks());
+        else
+            update(1.f);
         return l;
     }
+    // attach an NCCL communicator: forward_backward then all-reduces the sync
+    // buffer in buckets on the comm stream while the reverse sweep runs
+    void set_comm(std::unique_ptr<Comm> c) { comm_ = std::move(c); }
+    const Comm* comm() const { return comm_.get(); }
+    float* sync_buffer() const { return flat_.fdata(); }
+    long sync_floats() const { return 2 * (flat_n_ + stats_n_); }
     // one iPALM sweep over the weight blocks in Gauss-Seidel order
     // (ipalm_step + run_step's iPALM branch, optim.hpp:118-153, 331-370)
     double ipalm_step();
@@ -69,8 +85,21 @@ private:
     std::vector<int> wargs_;
     std::vector<std::string> wnames_;
     std::vector<long> woff_;
+    // flat sync buffer: [weight gradients (flat_n_ complex) | moving statistics (stats_n_ complex)]
     DArray flat_;
     long flat_n_ = 0;
+    struct StatSlot {
+        std::string name;
+        int out = -1; // joint output carrying the new value
+        long off = 0, n = 0;
+    };
+    std::vector<StatSlot> stats_;
+    long stats_n_ = 0;
+    std::unique_ptr<Comm> comm_;
+    cudaEvent_t ev_sync_ = nullptr; // compute -> comm stream hand-offs
+    cudaEvent_t ev_done_ = nullptr; // comm -> compute stream (all buckets reduced)
+    long bucket_min_floats_ = 1 << 16;
+    void allreduce_range(long off, long n); // complex offsets into flat_
     struct Adam {
         DArray m;
         float* v = nullptr;

@@ -256,6 +256,26 @@ class Model:
         return Model(lib, lib.so.mdnn_build_varnet(C.byref(varnet_cfg(lib, **kw))))
 
     @staticmethod
+    def modl_denoiser(lib, **kw):
+        """D_W(x) = x + CNN(x) of one MoDL unroll (recon.hpp:714-803)."""
+        return Model(lib, lib.so.mdnn_modl_denoiser(C.byref(modl_cfg(lib, **kw))))
+
+    @staticmethod
+    def varnet_reg(lib, **kw):
+        """sum_f K^T Phi'(Re K x) of VarNet stage it0 (recon.hpp:522-609)."""
+        return Model(lib, lib.so.mdnn_varnet_reg(C.byref(varnet_cfg(lib, **kw))))
+
+    @staticmethod
+    def bn_block(lib, name, dims):
+        """Train-mode BN -> gamma -> beta -> CReLU of one denoiser layer (recon.hpp:748-776)."""
+        d = (C.c_long * len(dims))(*dims)
+        return Model(lib, lib.so.mdnn_bn_block(name.encode(), len(dims), d))
+
+    def rebatch(self, batch):
+        """Model::rebatch (nn.hpp:82): the same network for `batch` items."""
+        return Model(self.lib, self.lib.so.mdnn_model_rebatch(self.h, int(batch)))
+
+    @staticmethod
     def conv_layer(lib, name, in_dims, kernel, out_channels, axes=(0, 1), chan_dim=2, pad_same=True,
                    transposed=False, bias=False):
         s = mdnn_conv_spec()
@@ -369,10 +389,33 @@ class Trainer:
     def update(self, scale=1.0):
         self.lib.check(self.lib.so.mdnn_trainer_update(self.h, scale))
 
+    def sync_buffer(self):
+        """(address, floats) of the data-parallel payload [gradients | moving statistics]."""
+        p, n = C.POINTER(C.c_float)(), C.c_long()
+        self.lib.check(self.lib.so.mdnn_trainer_sync_buffer(self.h, C.byref(p), C.byref(n)))
+        return C.cast(p, C.c_void_p).value, n.value
+
+    def update_dp(self, world):
+        self.lib.check(self.lib.so.mdnn_trainer_update_dp(self.h, int(world)))
+
+    def set_comm(self, unique_id: bytes, nranks, rank):
+        """Attach an in-library NCCL communicator (id from nccl_unique_id on rank 0)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self.lib.check(self.lib.so.mdnn_trainer_set_comm(self.h, C.cast(buf, C.c_void_p), int(nranks), int(rank)))
+
+    def moving_stat_names(self):
+        return [a for a, k, _ in self.model.args if k == ARG_MOVING_STATS]
+
     def step(self):
         loss = C.c_double()
         self.lib.check(self.lib.so.mdnn_trainer_step(self.h, C.byref(loss)))
         return loss.value
+
+
+def nccl_unique_id(lib: Lib) -> bytes:
+    buf = (C.c_uint8 * 128)()
+    lib.check(lib.so.mdnn_nccl_unique_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
 
 
 # ---- cfl files (cfl.hpp:19-88) ----------------------------------------------

@@ -1,8 +1,10 @@
 """Multi-process data parallelism on CPU (gloo, world_size 2) through the same
 C ABI and the product's DataParallelTrainer, driving the reference-backed
 library (the GPU library needs a device).  Checks that (1) replicas stay
-bitwise identical and (2) the result equals one process that averages the two
-shards' gradients before the same Adam update."""
+bitwise identical -- trainable weights and the BN moving statistics that
+eval-mode inference reads -- and (2) the result equals one process that
+averages the two shards' gradients and moving statistics before the same
+Adam update."""
 import os
 import socket
 
@@ -43,7 +45,8 @@ def _worker(rank, world, port, out_q):
         tr.set_data(k, v)
     dp = DataParallelTrainer(tr, world=world)
     losses = [dp.step() for _ in range(2)]
-    out_q.put((rank, losses, {n: tr.get_weight(n) for n in tr.weight_names()}))
+    names = tr.weight_names() + tr.moving_stat_names()
+    out_q.put((rank, losses, {n: tr.get_weight(n) for n in names}))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -68,8 +71,9 @@ def test_two_rank_gloo_matches_averaged_single_process(ref):
         p.join(timeout=60)
         assert p.exitcode == 0
     w0, w1 = res[0][1], res[1][1]
+    assert any("bn_mean" in k for k in w0) and any("bn_var" in k for k in w0)
     for k in w0:
-        assert np.array_equal(w0[k], w1[k]), k  # replicas bitwise identical
+        assert np.array_equal(w0[k], w1[k]), k  # replicas bitwise identical, moving statistics included
 
     # single process: average the two shards' gradients, same update
     from paper_2202_14005_b200.mdnn import Model, Trainer
@@ -84,12 +88,12 @@ def test_two_rank_gloo_matches_averaged_single_process(ref):
         bufs = []
         for t in trs:
             t.forward_backward()
-            p, n = t.grad_buffer()
+            p, n = t.sync_buffer()
             bufs.append(np.frombuffer((C.c_float * n).from_address(p), dtype=np.float32))
         s = bufs[0] + bufs[1]
         for b in bufs:
             b[:] = s
         for t in trs:
-            t.update(0.5)
+            t.update_dp(2)
     for k in w0:
         np.testing.assert_allclose(w0[k], trs[0].get_weight(k), rtol=1e-6, atol=1e-7)

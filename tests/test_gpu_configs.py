@@ -1,0 +1,376 @@
+"""Config-level parity: the BASELINE.json configurations themselves, not toy
+shapes (SURVEY §8c protocol).
+
+  * C1 (MoDL T1 / CG5 / L3 / F32, 128x128, 8 coils, B=1, make_pattern(128,4,28)):
+    one training step end to end -- output and every weight gradient against
+    the fp64 reference with GPU error <= max(tol, 2 x CPU-fp32 error) -- and a
+    3-step Adam trajectory against the fp32 reference's own run_step.
+  * C2 (320x368, 15 coils, F=64) per node / per block with oracle-fed inputs:
+    64->64, 1->64 and 64->1 convolutions (fwd, bwd-data, bwd-weight) at 1e-3;
+    the fused BN block alone at 1e-5 / TF32 budget; the L3 and L5 denoisers
+    (conv-epilogue BN statistics, BN backward in the bwd-data epilogue, the
+    last layer's tensor-core expand with the BN-backward reduction) with the
+    fusions on and off; the InverseNode CG-10 at B=8.
+  * C3 (640x368) per block: the VarNet regulariser (2->24 11x11 conv, RBF,
+    transposed conv) of one stage.
+  * C4 / C5 geometry: A^H A + lambda and CG-10 at 512x512x32.
+  * GPU run-to-run bitwise determinism of a training step
+    (test_optim.cpp:253-270; reference guarantee mdarray.hpp:322-342).
+
+The oracle is oracle/_ref (the unmodified reference headers compiled in
+place); every size here finishes on the box's host cores in seconds to a
+minute.  Test ids name the configuration.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2202_14005_b200.mdnn import ARG_DATA, ARG_WEIGHTS, Model, Trainer, sense_dims
+from util import crand, d16, image_dims, kspace_dims, rel_l2, sim_data
+
+pytestmark = pytest.mark.gpu
+CONV_TOL = 1e-3
+TOL = 1e-5
+
+
+def _kspace(lib, cm, pat, ph):
+    X, Y, NC = cm.shape[0], cm.shape[1], cm.shape[3]
+    ks = np.zeros(kspace_dims(X, Y, NC, cm.shape[15]), dtype=np.complex64, order="F")
+    lib.check(lib.so.mdnn_sense_forward(C.byref(lib.arr(cm)), C.byref(lib.arr(pat)), C.byref(lib.arr(ph)),
+                                        C.byref(lib.arr(ks))))
+    return ks
+
+
+def _perturbed_weights(model, seed=42, scale=0.1):
+    """init_weights(seed) with BN gamma / beta moved off 1 / 0 (so their paths carry signal)."""
+    w = model.init_weights(seed)
+    rng = np.random.default_rng(seed + 1)
+    for k in w:
+        if k.endswith("_g") or k.endswith("_beta"):
+            w[k] = np.asfortranarray((w[k] + scale * (rng.standard_normal(w[k].shape)
+                                                     + 1j * rng.standard_normal(w[k].shape))).astype(np.complex64))
+    return w
+
+
+def _apply_and_grads(lib, model, ins, dy_seed=5, out_name="out", wanted_kinds=(ARG_WEIGHTS,), want_x=False):
+    n = model.nlop
+    outs = n.apply(ins)
+    oi = model.output_index(out_name)
+    dy = crand(np.random.default_rng(dy_seed), n.out_dims(oi))
+    wanted = [k in wanted_kinds or (want_x and k == ARG_DATA) for _, k, _ in model.args]
+    g = n.adjoint_all(oi, dy, wanted)
+    grads = {a: g[i] for i, (a, k, _) in enumerate(model.args) if wanted[i]}
+    return dict(zip(model.out_names, outs)), grads
+
+
+def _e2e_check(res_gpu, res_ref, res_64, out_tol, grad_tol):
+    (og, gg), (orf, gr), (o64, g64) = res_gpu, res_ref, res_64
+    worst = {}
+    for k in o64:
+        e_gpu, e_cpu = rel_l2(og[k], o64[k]), rel_l2(orf[k], o64[k])
+        worst["out:" + k] = (e_gpu, e_cpu)
+        assert e_gpu <= max(out_tol, 2 * e_cpu), (k, e_gpu, e_cpu)
+    for k in g64:
+        e_gpu, e_cpu = rel_l2(gg[k], g64[k]), rel_l2(gr[k], g64[k])
+        worst["grad:" + k] = (e_gpu, e_cpu)
+        assert e_gpu <= max(grad_tol, 2 * e_cpu), (k, e_gpu, e_cpu)
+    return worst
+
+
+# ---------------------------------------------------------------------------
+# C1 end to end
+C1 = dict(iterations=1, layers=3, filters=32, cg_iter=5, im_x=128, im_y=128, coils=8, batch=1)
+
+
+def _c1_data(ref):
+    ph, cm, pat = sim_data(ref, 128, 128, 8, 1)  # make_pattern(128, 4, 28)
+    return {"kspace": _kspace(ref, cm, pat, ph), "coils": cm, "pattern": pat, "reference": ph}
+
+
+def test_c1_modl_step_end_to_end_vs_fp64(gpu, ref, ref64):
+    data = _c1_data(ref)
+    res = []
+    for lib in (gpu, ref, ref64):
+        m = Model.modl(lib, **C1)
+        w = _perturbed_weights(m)
+        ins = [data[a] if k == ARG_DATA else w[a] for a, k, _ in m.args]
+        res.append(_apply_and_grads(lib, m, ins))
+    _e2e_check(*res, out_tol=1e-5, grad_tol=1e-3)
+
+
+def test_c1_adam_trajectory_vs_reference(gpu, ref):
+    data = _c1_data(ref)
+    traj = []
+    for lib in (gpu, ref):
+        t = Trainer(lib, Model.modl(lib, **C1), seed=42)
+        for k, v in data.items():
+            t.set_data(k, v)
+        losses = [t.step() for _ in range(3)]
+        traj.append((losses, {n: t.get_weight(n) for n in t.weight_names()}))
+    (lg, wg), (lr_, wr) = traj
+    for a, b in zip(lg, lr_):
+        assert abs(a - b) <= 1e-3 * abs(b), (lg, lr_)
+    for k in wr:
+        assert rel_l2(wg[k], wr[k]) <= 1e-4, k
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2-shaped-small"])
+def test_training_step_bitwise_deterministic(gpu, ref, cfg):
+    """GPU run-to-run bitwise determinism of full training steps
+    (test_optim.cpp:253-270): two trainers, same inputs, identical loss bits
+    and weight bits after 2 Adam steps."""
+    if cfg == "C1":
+        kw, data = C1, _c1_data(ref)
+    else:
+        kw = dict(iterations=2, layers=5, filters=64, cg_iter=10, im_x=64, im_y=92, coils=4, batch=2)
+        ph, cm, pat = sim_data(ref, 64, 92, 4, 2)
+        data = {"kspace": _kspace(ref, cm, pat, ph), "coils": cm, "pattern": pat, "reference": ph}
+    runs = []
+    for _ in range(2):
+        t = Trainer(gpu, Model.modl(gpu, **kw), seed=42)
+        for k, v in data.items():
+            t.set_data(k, v)
+        losses = [t.step() for _ in range(2)]
+        names = t.weight_names() + t.moving_stat_names()
+        runs.append((losses, {n: t.get_weight(n) for n in names}))
+    assert runs[0][0] == runs[1][0]
+    for k in runs[0][1]:
+        assert np.array_equal(runs[0][1][k].view(np.uint32), runs[1][1][k].view(np.uint32)), k
+
+
+# ---------------------------------------------------------------------------
+# C2 per node (320 x 368, B = 1, F = 64)
+def _conv_check(gpu, ref, cin, cout, X, Y, B=1, seed=0):
+    rng = np.random.default_rng(seed)
+    in_dims = list(d16(X, Y, cin))
+    in_dims[15] = B
+    mg = Model.conv_layer(gpu, "c", in_dims, (3, 3), cout)
+    mr = Model.conv_layer(ref, "c", in_dims, (3, 3), cout)
+    ng, nr = mg.nlop, mr.nlop
+    x = crand(rng, nr.in_dims(0))
+    w = crand(rng, nr.in_dims(1), 0.1)
+    og, orf = ng.apply([x, w])[0], nr.apply([x, w])[0]
+    assert rel_l2(og, orf) <= CONV_TOL, "fwd"
+    dy = crand(rng, nr.out_dims(0))
+    ag, ar = ng.adjoint_all(0, dy), nr.adjoint_all(0, dy)
+    assert rel_l2(ag[0], ar[0]) <= CONV_TOL, "bwd-data"
+    assert rel_l2(ag[1], ar[1]) <= CONV_TOL, "bwd-weight"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cin,cout", [(64, 64), (1, 64), (64, 1)], ids=["C2-64to64", "C2-1to64", "C2-64to1"])
+def test_c2_conv_layers(gpu, ref, cin, cout):
+    _conv_check(gpu, ref, cin, cout, 320, 368)
+
+
+def test_c2_bn_block_vs_reference_chain(gpu, ref):
+    """The fused BN -> gamma -> beta -> CReLU node alone vs the reference chain
+    (recon.hpp:748-776) at C2 geometry, F = 64: outputs and moving statistics,
+    cotangents wrt x, gamma, beta at 1e-5."""
+    dims = list(d16(320, 368, 64))
+    rng = np.random.default_rng(3)
+    mg, mr = Model.bn_block(gpu, "dw1", dims), Model.bn_block(ref, "dw1", dims)
+    assert sorted(mg.arg_names) == sorted(mr.arg_names)
+    vals = {"x": crand(rng, dims, 2.0) + np.complex64(0.3 - 0.2j),
+            "dw1_bn_mean": crand(rng, d16(1, 1, 64), 0.1), "dw1_bn_var": crand(rng, d16(1, 1, 64), 0.1) + 1,
+            "dw1_g": crand(rng, d16(1, 1, 64)), "dw1_beta": crand(rng, d16(1, 1, 64), 0.3)}
+    res = []
+    for m in (mg, mr):
+        n = m.nlop
+        outs = dict(zip(m.out_names, n.apply([vals[a] for a in m.arg_names])))
+        dy = crand(np.random.default_rng(9), n.out_dims(m.output_index("out")))
+        g = n.adjoint_all(m.output_index("out"), dy)
+        res.append((outs, dict(zip(m.arg_names, g))))
+    (og, gg), (orf, gr) = res
+    for k in orf:
+        assert rel_l2(og[k], orf[k]) <= TOL, k
+    for k in ("x", "dw1_g", "dw1_beta"):
+        assert rel_l2(gg[k], gr[k]) <= TOL, k
+
+
+def test_bn_large_channel_offset(gpu, ref):
+    """Batch statistics of channels whose |mean| >> std: the
+    shifted partial sums keep the variance at reference accuracy."""
+    dims = list(d16(96, 80, 64))
+    dims[15] = 2
+    rng = np.random.default_rng(4)
+    offs = (rng.uniform(50, 200, 64) * np.exp(1j * rng.uniform(0, 6.3, 64))).astype(np.complex64)
+    x = np.asfortranarray(crand(rng, dims, 0.05) + offs.reshape((1, 1, 64) + (1,) * 13))
+    mg, mr = Model.bn_block(gpu, "b", dims), Model.bn_block(ref, "b", dims)
+    vals = {"x": x, "b_bn_mean": crand(rng, d16(1, 1, 64)), "b_bn_var": crand(rng, d16(1, 1, 64)) + 1,
+            "b_g": crand(rng, d16(1, 1, 64)), "b_beta": crand(rng, d16(1, 1, 64), 0.3)}
+    outs = []
+    for m in (mg, mr):
+        outs.append(dict(zip(m.out_names, m.nlop.apply([vals[a] for a in m.arg_names]))))
+    for k in outs[1]:
+        assert rel_l2(outs[0][k], outs[1][k]) <= 1e-4, k
+
+
+def _denoiser_inputs(ref, layers, X, Y, seed=42):
+    """Oracle-fed denoiser input: the zero-filled A^H y image of the config's
+    synthetic data (what the first unroll's CNN sees, recon.hpp:875-904)."""
+    ph, cm, pat = sim_data(ref, X, Y, 15, 1)
+    ks = _kspace(ref, cm, pat, ph)
+    x0 = np.zeros(image_dims(X, Y), dtype=np.complex64, order="F")
+    ref.check(ref.so.mdnn_sense_adjoint(C.byref(ref.arr(cm)), C.byref(ref.arr(pat)), C.byref(ref.arr(ks)),
+                                        C.byref(ref.arr(x0))))
+    return x0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("layers", [3, 5], ids=["C2-L3", "C2-L5"])
+@pytest.mark.parametrize("fusion", ["fused", "unfused"])
+def test_c2_denoiser_block(gpu, ref, ref64, layers, fusion):
+    """MoDL CNN denoiser D_W(x) = x + CNN(x) at C2 geometry (320x368, F=64,
+    train-mode BN), fed the A^H y image: output, BN statistics, every weight
+    gradient and the input cotangent vs fp64 with max(tol, 2 x CPU-fp32 error).
+    'fused' is the product path (BN statistics from the conv epilogue, BN
+    backward in the bwd-data epilogue, last-layer tensor-core expand with the
+    BN-backward reduction); 'unfused' switches those fusions off."""
+    x0 = _denoiser_inputs(ref, layers, 320, 368)
+    kw = dict(iterations=1, layers=layers, filters=64, im_x=320, im_y=368, coils=15, batch=1)
+    opts = {"conv_bn_fuse": 0, "conv_thin_tc_bnb": 0} if fusion == "unfused" else {}
+    try:
+        for k, v in opts.items():
+            gpu.check(gpu.so.mdnn_set_option(k.encode(), v))
+        res = []
+        for lib in (gpu, ref, ref64):
+            m = Model.modl_denoiser(lib, **kw)
+            w = _perturbed_weights(m)
+            ins = [x0 if k == ARG_DATA else w[a] for a, k, _ in m.args]
+            res.append(_apply_and_grads(lib, m, ins, want_x=True))
+    finally:
+        for k in opts:
+            gpu.check(gpu.so.mdnn_set_option(k.encode(), 1))
+    _e2e_check(*res, out_tol=CONV_TOL, grad_tol=CONV_TOL)
+
+
+@pytest.mark.slow
+def test_c2_denoiser_fused_equals_unfused(gpu, ref):
+    """The epilogue fusions change only the summation order: fused and unfused
+    product paths agree to 1e-4 at C2 geometry (multi-tile grids: 117,760
+    pixels per layer, every CTA loops over several tiles)."""
+    x0 = _denoiser_inputs(ref, 5, 320, 368)
+    kw = dict(iterations=1, layers=5, filters=64, im_x=320, im_y=368, coils=15, batch=1)
+    res = []
+    for fuse in (1, 0):
+        for k in ("conv_bn_fuse", "conv_thin_tc_bnb"):
+            gpu.check(gpu.so.mdnn_set_option(k.encode(), fuse))
+        m = Model.modl_denoiser(gpu, **kw)
+        w = _perturbed_weights(m)
+        ins = [x0 if k == ARG_DATA else w[a] for a, k, _ in m.args]
+        res.append(_apply_and_grads(gpu, m, ins, want_x=True))
+    for k in ("conv_bn_fuse", "conv_thin_tc_bnb"):
+        gpu.check(gpu.so.mdnn_set_option(k.encode(), 1))
+    (o1, g1), (o0, g0) = res
+    for k in o1:
+        assert rel_l2(o1[k], o0[k]) <= 1e-4, k
+    for k in g1:
+        assert rel_l2(g1[k], g0[k]) <= 1e-4, k
+
+
+@pytest.mark.slow
+def test_c2_inverse_node_cg10_batch8(gpu, ref):
+    """InverseNode (recon.hpp:211-329) on S = A^H A + lambda at C2: 320x368,
+    15 coils, B = 8, 10 CG iterations (tol 1e-7 as in ModlConfig): forward and
+    the adjoint wrt y, 1e-5."""
+    ph, cm, pat = sim_data(ref, 320, 368, 15, 8)
+    ks = _kspace(ref, cm, pat, ph)
+    y = np.zeros(image_dims(320, 368, 8), dtype=np.complex64, order="F")
+    ref.check(ref.so.mdnn_sense_adjoint(C.byref(ref.arr(cm)), C.byref(ref.arr(pat)), C.byref(ref.arr(ks)),
+                                        C.byref(ref.arr(y))))
+    lam = np.full(d16(), 0.05, dtype=np.complex64, order="F")
+    sd = sense_dims(320, 368, 15, 1, 8)
+    outs = []
+    for lib in (gpu, ref):
+        inv = Model.modl_normal_plus_lambda(lib, sd).nlop.inverse(10, 1e-7)
+        o = inv.apply([y, cm, pat, lam])[0]
+        dy = crand(np.random.default_rng(2), image_dims(320, 368, 8))
+        adj = inv.adjoint_all(0, dy, [1, 0, 0, 0])[0]
+        outs.append((o, adj))
+    assert rel_l2(outs[0][0], outs[1][0]) <= TOL
+    assert rel_l2(outs[0][1], outs[1][1]) <= TOL
+
+
+# ---------------------------------------------------------------------------
+# C3 per block (640 x 368)
+@pytest.mark.slow
+def test_c3_varnet_regulariser(gpu, ref, ref64):
+    """VarNet stage regulariser sum_f K^T Phi'(Re K x) (recon.hpp:522-609) at
+    C3 geometry: 640x368, 24 filters 11x11, 31 RBF centres, perturbed RBF
+    weights (zero-init kills the gradients): output, weight
+    gradients and input cotangent vs fp64."""
+    ph, cm, pat = sim_data(ref, 640, 368, 15, 1)
+    kw = dict(iterations=1, filters=24, kernel=11, rbf=31, im_x=640, im_y=368, coils=15, batch=1)
+    res = []
+    for lib in (gpu, ref, ref64):
+        m = Model.varnet_reg(lib, **kw)
+        w = m.init_weights(42)
+        rng = np.random.default_rng(99)
+        for k in w:
+            if k.endswith("_rbf_w"):
+                w[k] = np.asfortranarray(rng.uniform(-0.05, 0.05, w[k].shape).astype(np.complex64))
+        ins = [ph if k == ARG_DATA else w[a] for a, k, _ in m.args]
+        res.append(_apply_and_grads(lib, m, ins, want_x=True))
+    _e2e_check(*res, out_tol=CONV_TOL, grad_tol=CONV_TOL)
+
+
+# ---------------------------------------------------------------------------
+# C4 / C5 geometry: 512 x 512, 32 coils
+@pytest.mark.slow
+def test_sense_normal_and_cg_512_32coils(gpu, ref):
+    import ctypes as C_
+    ph, cm, pat = sim_data(ref, 512, 512, 32, 1)
+    res = []
+    for lib in (gpu, ref):
+        y = np.zeros(image_dims(512, 512), dtype=np.complex64, order="F")
+        lib.check(lib.so.mdnn_sense_normal(C_.byref(lib.arr(cm)), C_.byref(lib.arr(pat)), C_.c_float(0.05),
+                                           C_.byref(lib.arr(ph)), C_.byref(lib.arr(y))))
+        x = np.zeros(image_dims(512, 512), dtype=np.complex64, order="F")
+        it, st = C_.c_long(), (C_.c_double * 3)()
+        lib.check(lib.so.mdnn_cg_normal_solve(C_.byref(lib.arr(cm)), C_.byref(lib.arr(pat)), C_.c_float(0.05),
+                                              C_.byref(lib.arr(ph)), 10, C_.c_double(0.0), C_.byref(lib.arr(x)),
+                                              C_.byref(it), st))
+        res.append((y, x, it.value))
+    assert rel_l2(res[0][0], res[1][0]) <= TOL
+    assert res[0][2] == res[1][2] == 10
+    assert rel_l2(res[0][1], res[1][1]) <= TOL
+
+
+# ---------------------------------------------------------------------------
+# data parallelism through the in-library NCCL communicator (1 rank on one GPU)
+def test_library_nccl_one_rank_matches_plain_step(gpu, ref):
+    from paper_2202_14005_b200.mdnn import nccl_unique_id
+    kw = dict(iterations=1, layers=3, filters=8, cg_iter=3, im_x=32, im_y=24, coils=3, batch=2)
+    ph, cm, pat = sim_data(ref, 32, 24, 3, 2)
+    data = {"kspace": _kspace(ref, cm, pat, ph), "coils": cm, "pattern": pat, "reference": ph}
+    runs = []
+    for comm in (False, True):
+        t = Trainer(gpu, Model.modl(gpu, **kw), seed=42)
+        for k, v in data.items():
+            t.set_data(k, v)
+        if comm:
+            t.set_comm(nccl_unique_id(gpu), 1, 0)
+        losses = [t.step() for _ in range(2)]
+        runs.append((losses, {n: t.get_weight(n) for n in t.weight_names() + t.moving_stat_names()}))
+    assert runs[0][0] == runs[1][0]
+    for k in runs[0][1]:
+        assert np.array_equal(runs[0][1][k], runs[1][1][k]), k
+
+
+def test_update_dp_world1_equals_update(gpu, ref):
+    kw = dict(iterations=1, layers=3, filters=8, cg_iter=3, im_x=32, im_y=24, coils=3, batch=2)
+    ph, cm, pat = sim_data(ref, 32, 24, 3, 2)
+    data = {"kspace": _kspace(ref, cm, pat, ph), "coils": cm, "pattern": pat, "reference": ph}
+    ws = []
+    for dp in (False, True):
+        t = Trainer(gpu, Model.modl(gpu, **kw), seed=42)
+        for k, v in data.items():
+            t.set_data(k, v)
+        for _ in range(2):
+            t.forward_backward()
+            t.update_dp(1) if dp else t.update(1.0)
+        ws.append({n: t.get_weight(n) for n in t.weight_names() + t.moving_stat_names()})
+    for k in ws[0]:
+        assert np.array_equal(ws[0][k], ws[1][k]), k
