@@ -64,17 +64,17 @@ def _apply_and_grads(lib, model, ins, dy_seed=5, out_name="out", wanted_kinds=(A
     return dict(zip(model.out_names, outs)), grads
 
 
-def _e2e_check(res_gpu, res_ref, res_64, out_tol, grad_tol):
+def _e2e_check(res_gpu, res_ref, res_64, out_tol, grad_tol, cpu_factor=2):
     (og, gg), (orf, gr), (o64, g64) = res_gpu, res_ref, res_64
     worst = {}
     for k in o64:
         e_gpu, e_cpu = rel_l2(og[k], o64[k]), rel_l2(orf[k], o64[k])
         worst["out:" + k] = (e_gpu, e_cpu)
-        assert e_gpu <= max(out_tol, 2 * e_cpu), (k, e_gpu, e_cpu)
+        assert e_gpu <= max(out_tol, cpu_factor * e_cpu), (k, e_gpu, e_cpu)
     for k in g64:
         e_gpu, e_cpu = rel_l2(gg[k], g64[k]), rel_l2(gr[k], g64[k])
         worst["grad:" + k] = (e_gpu, e_cpu)
-        assert e_gpu <= max(grad_tol, 2 * e_cpu), (k, e_gpu, e_cpu)
+        assert e_gpu <= max(grad_tol, cpu_factor * e_cpu), (k, e_gpu, e_cpu)
     return worst
 
 
@@ -88,31 +88,82 @@ def _c1_data(ref):
     return {"kspace": _kspace(ref, cm, pat, ph), "coils": cm, "pattern": pat, "reference": ph}
 
 
-def test_c1_modl_step_end_to_end_vs_fp64(gpu, ref, ref64):
+# Two arithmetic modes of the product library.  "fp32-convs" switches the
+# convolutions to the fp32 CUDA-core kernels (options conv_tc = conv_thin_tc = 0):
+# every kernel then computes in fp32 with double-accumulated reductions and the
+# bound is the SENSE/CG one, max(1e-5, 2 x CPU-fp32 error).  "tf32" is the
+# default training path (tensor-core convolutions, operands rounded RN to
+# TF32): per layer it is held to 1e-3 (test_c2_conv_layers); end to end the
+# TF32 rounding of three stacked layers compounds -- measured at C1 with a
+# random output cotangent: out 8.5e-4, lam_log 1.3e-3, last-layer weight
+# gradient 3.5e-3 (tools/probes/parity_probe.py) -- so the e2e bound is 5e-3.
+# Gradients through the train-mode BN / CReLU chain are ill-conditioned (the
+# fp32 reference itself is off by 2e-2 .. 1.5e-1 on dw*_g / dw*_beta / dw0_w:
+# rounding flips CReLU masks); there TF32 flips more of them (measured 2.2x
+# the fp32 reference's error on dw0_g), so the TF32 multiple of the CPU-fp32
+# error is 4 instead of 2.
+MODES = {"fp32-convs": ({"conv_tc": 0, "conv_thin_tc": 0}, TOL, TOL, 2), "tf32": ({}, CONV_TOL, 5e-3, 4)}
+
+
+class _Options:
+    def __init__(self, lib, opts):
+        self.lib, self.opts = lib, opts
+
+    def __enter__(self):
+        for k, v in self.opts.items():
+            self.lib.check(self.lib.so.mdnn_set_option(k.encode(), v))
+
+    def __exit__(self, *exc):
+        for k in self.opts:
+            self.lib.check(self.lib.so.mdnn_set_option(k.encode(), 1))
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_c1_modl_step_end_to_end_vs_fp64(gpu, ref, ref64, mode):
+    opts, out_tol, grad_tol, factor = MODES[mode]
     data = _c1_data(ref)
     res = []
-    for lib in (gpu, ref, ref64):
-        m = Model.modl(lib, **C1)
-        w = _perturbed_weights(m)
-        ins = [data[a] if k == ARG_DATA else w[a] for a, k, _ in m.args]
-        res.append(_apply_and_grads(lib, m, ins))
-    _e2e_check(*res, out_tol=1e-5, grad_tol=1e-3)
+    with _Options(gpu, opts):
+        for lib in (gpu, ref, ref64):
+            m = Model.modl(lib, **C1)
+            w = _perturbed_weights(m)
+            ins = [data[a] if k == ARG_DATA else w[a] for a, k, _ in m.args]
+            res.append(_apply_and_grads(lib, m, ins))
+    _e2e_check(*res, out_tol=out_tol, grad_tol=grad_tol, cpu_factor=factor)
 
 
-def test_c1_adam_trajectory_vs_reference(gpu, ref):
+def _c1_trajectory(lib, data, steps=3):
+    t = Trainer(lib, Model.modl(lib, **C1), seed=42)
+    for k, v in data.items():
+        t.set_data(k, v)
+    losses = [t.step() for _ in range(steps)]
+    return losses, {n: t.get_weight(n) for n in t.weight_names()}
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_c1_adam_trajectory_vs_fp64(gpu, ref, ref64, mode):
+    """3 Adam steps of the reference's run_step (optim.hpp:314-399) at C1: the
+    GPU trajectory against the fp64 reference's.  fp32-convs: losses and
+    weights within max(1e-5, 2 x the fp32 reference's own deviation).  tf32:
+    Adam's m / sqrt(v) normalisation turns the TF32 gradient error into
+    per-element update noise on the small-gradient BN betas; measured after 3
+    steps: loss 8.6e-3 relative, dw1_beta 7.9e-2 rel-L2, every other weight
+    <= 2e-3 -- bounded here at 1.5e-2 / 0.15 / 5e-3."""
+    opts = MODES[mode][0]
     data = _c1_data(ref)
-    traj = []
-    for lib in (gpu, ref):
-        t = Trainer(lib, Model.modl(lib, **C1), seed=42)
-        for k, v in data.items():
-            t.set_data(k, v)
-        losses = [t.step() for _ in range(3)]
-        traj.append((losses, {n: t.get_weight(n) for n in t.weight_names()}))
-    (lg, wg), (lr_, wr) = traj
-    for a, b in zip(lg, lr_):
-        assert abs(a - b) <= 1e-3 * abs(b), (lg, lr_)
-    for k in wr:
-        assert rel_l2(wg[k], wr[k]) <= 1e-4, k
+    with _Options(gpu, opts):
+        lg, wg = _c1_trajectory(gpu, data)
+    lr_, wr = _c1_trajectory(ref, data)
+    l64, w64 = _c1_trajectory(ref64, data)
+    for a, b, c in zip(lg, lr_, l64):
+        dev_gpu, dev_cpu = abs(a - c) / abs(c), abs(b - c) / abs(c)
+        assert dev_gpu <= (max(TOL, 2 * dev_cpu) if mode == "fp32-convs" else 1.5e-2), (lg, lr_, l64)
+    for k in w64:
+        e_gpu, e_cpu = rel_l2(wg[k], w64[k]), rel_l2(wr[k], w64[k])
+        if mode == "fp32-convs":
+            assert e_gpu <= max(TOL, 2 * e_cpu), (k, e_gpu, e_cpu)
+        else:
+            assert e_gpu <= (0.15 if k.endswith("_beta") else 5e-3), (k, e_gpu, e_cpu)
 
 
 @pytest.mark.parametrize("cfg", ["C1", "C2-shaped-small"])
@@ -136,7 +187,7 @@ def test_training_step_bitwise_deterministic(gpu, ref, cfg):
         runs.append((losses, {n: t.get_weight(n) for n in names}))
     assert runs[0][0] == runs[1][0]
     for k in runs[0][1]:
-        assert np.array_equal(runs[0][1][k].view(np.uint32), runs[1][1][k].view(np.uint32)), k
+        assert runs[0][1][k].tobytes(order="A") == runs[1][1][k].tobytes(order="A"), k
 
 
 # ---------------------------------------------------------------------------
@@ -164,47 +215,50 @@ def test_c2_conv_layers(gpu, ref, cin, cout):
     _conv_check(gpu, ref, cin, cout, 320, 368)
 
 
-def test_c2_bn_block_vs_reference_chain(gpu, ref):
+def _bn_block_run(lib, dims, vals, prefix):
+    m = Model.bn_block(lib, prefix, dims)
+    n = m.nlop
+    outs = dict(zip(m.out_names, n.apply([vals[a] for a in m.arg_names])))
+    dy = crand(np.random.default_rng(9), n.out_dims(m.output_index("out")))
+    g = n.adjoint_all(m.output_index("out"), dy)
+    grads = {k: v for k, v in zip(m.arg_names, g) if k == "x" or k.endswith("_g") or k.endswith("_beta")}
+    return outs, grads
+
+
+def test_c2_bn_block_vs_reference_chain(gpu, ref, ref64):
     """The fused BN -> gamma -> beta -> CReLU node alone vs the reference chain
-    (recon.hpp:748-776) at C2 geometry, F = 64: outputs and moving statistics,
-    cotangents wrt x, gamma, beta at 1e-5."""
+    (recon.hpp:748-776) at C2 geometry, F = 64: outputs, batch statistics and
+    the cotangents wrt x, gamma, beta against the fp64 reference with
+    max(1e-5, 2 x CPU-fp32 error).  (The fp32 reference's own cotangent error
+    here is 4e-4 .. 9e-4 -- sequential fp32 sums over 117,760 pixels -- the
+    GPU's is 7e-8 .. 1.3e-7, double-folded partials.)"""
     dims = list(d16(320, 368, 64))
     rng = np.random.default_rng(3)
-    mg, mr = Model.bn_block(gpu, "dw1", dims), Model.bn_block(ref, "dw1", dims)
-    assert sorted(mg.arg_names) == sorted(mr.arg_names)
+    assert sorted(Model.bn_block(gpu, "dw1", dims).arg_names) == sorted(Model.bn_block(ref, "dw1", dims).arg_names)
     vals = {"x": crand(rng, dims, 2.0) + np.complex64(0.3 - 0.2j),
             "dw1_bn_mean": crand(rng, d16(1, 1, 64), 0.1), "dw1_bn_var": crand(rng, d16(1, 1, 64), 0.1) + 1,
             "dw1_g": crand(rng, d16(1, 1, 64)), "dw1_beta": crand(rng, d16(1, 1, 64), 0.3)}
-    res = []
-    for m in (mg, mr):
-        n = m.nlop
-        outs = dict(zip(m.out_names, n.apply([vals[a] for a in m.arg_names])))
-        dy = crand(np.random.default_rng(9), n.out_dims(m.output_index("out")))
-        g = n.adjoint_all(m.output_index("out"), dy)
-        res.append((outs, dict(zip(m.arg_names, g))))
-    (og, gg), (orf, gr) = res
-    for k in orf:
-        assert rel_l2(og[k], orf[k]) <= TOL, k
-    for k in ("x", "dw1_g", "dw1_beta"):
-        assert rel_l2(gg[k], gr[k]) <= TOL, k
+    res = [_bn_block_run(lib, dims, vals, "dw1") for lib in (gpu, ref, ref64)]
+    _e2e_check(*res, out_tol=TOL, grad_tol=TOL)
 
 
-def test_bn_large_channel_offset(gpu, ref):
-    """Batch statistics of channels whose |mean| >> std: the
-    shifted partial sums keep the variance at reference accuracy."""
+def test_bn_large_channel_offset(gpu, ref, ref64):
+    """Batch statistics of channels whose |mean| >> std (|mean| /
+    std = 1000 .. 4000): the shifted partial sums keep the GPU at 9e-5 on the
+    outputs and <= 9e-3 on the cotangents vs fp64, where the fp32 reference
+    itself is off by 0.12 / 0.3 (measured)."""
     dims = list(d16(96, 80, 64))
     dims[15] = 2
     rng = np.random.default_rng(4)
     offs = (rng.uniform(50, 200, 64) * np.exp(1j * rng.uniform(0, 6.3, 64))).astype(np.complex64)
     x = np.asfortranarray(crand(rng, dims, 0.05) + offs.reshape((1, 1, 64) + (1,) * 13))
-    mg, mr = Model.bn_block(gpu, "b", dims), Model.bn_block(ref, "b", dims)
     vals = {"x": x, "b_bn_mean": crand(rng, d16(1, 1, 64)), "b_bn_var": crand(rng, d16(1, 1, 64)) + 1,
             "b_g": crand(rng, d16(1, 1, 64)), "b_beta": crand(rng, d16(1, 1, 64), 0.3)}
-    outs = []
-    for m in (mg, mr):
-        outs.append(dict(zip(m.out_names, m.nlop.apply([vals[a] for a in m.arg_names]))))
-    for k in outs[1]:
-        assert rel_l2(outs[0][k], outs[1][k]) <= 1e-4, k
+    (og, gg), (orf, gr), (o64, g64) = [_bn_block_run(lib, dims, vals, "b") for lib in (gpu, ref, ref64)]
+    for k in o64:
+        assert rel_l2(og[k], o64[k]) <= 2e-4, k
+    for k in g64:
+        assert rel_l2(gg[k], g64[k]) <= min(2e-2, 0.1 * rel_l2(gr[k], g64[k])), k
 
 
 def _denoiser_inputs(ref, layers, X, Y, seed=42):
@@ -247,27 +301,35 @@ def test_c2_denoiser_block(gpu, ref, ref64, layers, fusion):
 
 
 @pytest.mark.slow
-def test_c2_denoiser_fused_equals_unfused(gpu, ref):
+def test_c2_denoiser_fused_equals_unfused(gpu, ref, ref64):
     """The epilogue fusions change only the summation order: fused and unfused
-    product paths agree to 1e-4 at C2 geometry (multi-tile grids: 117,760
-    pixels per layer, every CTA loops over several tiles)."""
+    product paths at C2 geometry (multi-tile grids: 117,760 pixels per layer,
+    every CTA loops over several tiles) agree to 1e-4 on outputs and BN
+    statistics, and their gradients differ by at most half the fp32
+    reference's own error vs fp64 (a train-mode BN / CReLU chain: summation-
+    order rounding flips CReLU masks, measured fused-vs-unfused 2.3e-3 on the
+    input cotangent against 3.0e-2 for the fp32 reference vs fp64)."""
     x0 = _denoiser_inputs(ref, 5, 320, 368)
     kw = dict(iterations=1, layers=5, filters=64, im_x=320, im_y=368, coils=15, batch=1)
     res = []
     for fuse in (1, 0):
-        for k in ("conv_bn_fuse", "conv_thin_tc_bnb"):
-            gpu.check(gpu.so.mdnn_set_option(k.encode(), fuse))
-        m = Model.modl_denoiser(gpu, **kw)
+        with _Options(gpu, {"conv_bn_fuse": fuse, "conv_thin_tc_bnb": fuse}):
+            m = Model.modl_denoiser(gpu, **kw)
+            w = _perturbed_weights(m)
+            ins = [x0 if k == ARG_DATA else w[a] for a, k, _ in m.args]
+            res.append(_apply_and_grads(gpu, m, ins, want_x=True))
+    cpu = []
+    for lib in (ref, ref64):
+        m = Model.modl_denoiser(lib, **kw)
         w = _perturbed_weights(m)
         ins = [x0 if k == ARG_DATA else w[a] for a, k, _ in m.args]
-        res.append(_apply_and_grads(gpu, m, ins, want_x=True))
-    for k in ("conv_bn_fuse", "conv_thin_tc_bnb"):
-        gpu.check(gpu.so.mdnn_set_option(k.encode(), 1))
+        cpu.append(_apply_and_grads(lib, m, ins, want_x=True))
     (o1, g1), (o0, g0) = res
+    (_, gr), (_, g64) = cpu
     for k in o1:
         assert rel_l2(o1[k], o0[k]) <= 1e-4, k
     for k in g1:
-        assert rel_l2(g1[k], g0[k]) <= 1e-4, k
+        assert rel_l2(g1[k], g0[k]) <= max(1e-4, 0.5 * rel_l2(gr[k], g64[k])), k
 
 
 @pytest.mark.slow
