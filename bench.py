@@ -610,7 +610,18 @@ def roofline(lib, step_ms_total):
     # kernels beat the cuBLAS TF32 figure measured on this pool
     # (profiles/tf32_peak.json, 741 TFLOP/s burst), so the denominator is the
     # nominal dense TF32 rate of B200_PROFILING.md (1.1 PFLOP/s)
-    tf32, tf32_src = 1100.0, "nominal tf32 dense 1.1 PFLOP/s (B200_PROFILING.md; cuBLAS TF32 measured 741)"
+    tf32, tf32_src = 1100.0, "nominal tf32 dense 1.1 PFLOP/s (B200_PROFILING.md)"
+    # second denominator for the tensor-bound rows: the TF32 rate measured on
+    # this pool (cuBLAS fp32 GEMM with TF32 tensor cores, profiles/tf32_peak.json),
+    # else half the measured bf16 rate of MEASURED_PEAKS.json
+    tf32_meas, tf32_meas_src = None, None
+    try:
+        with open(os.path.join(REPO, "profiles", "tf32_peak.json")) as f:
+            tf32_meas = float(json.load(f)["tf32_tflops"])
+            tf32_meas_src = "cuBLAS TF32 GEMM 8192^3 measured on this pool (profiles/tf32_peak.json)"
+    except Exception:
+        if "bf16_tflops" in p:
+            tf32_meas, tf32_meas_src = p["bf16_tflops"] / 2, "bf16_tflops / 2 (MEASURED_PEAKS.json)"
     traffic = {}
     try:
         with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
@@ -637,6 +648,9 @@ def roofline(lib, step_ms_total):
                      "frac": ach / peak, "launches": n.value, "ms_total": ms.value,
                      "share_of_step_time": ms.value / step_ms_total if step_ms_total > 0 else None,
                      "traffic": traffic.get(tag), "peak_source": f"measured hbm_gbs ({src})" if bound == "hbm" else tf32_src})
+        if bound == "tensor" and tf32_meas:
+            rows[-1].update({"peak_measured": tf32_meas, "frac_vs_measured": ach / tf32_meas,
+                             "peak_measured_source": tf32_meas_src})
     rows.sort(key=lambda r: -r["ms_total"])
     dom = rows[0] if rows else None
     ahha = next((r for r in rows if r["kernel"].startswith("sense_normal_y")), None)

@@ -164,12 +164,8 @@ int mdnn_set_option(const char* key, long value)
             sense_rank_enable(value != 0);
         else if (k == "sense_rank_ctas")
             sense_rank_ctas(value);
-        else if (k == "sense_rank_tm")
-            sense_rank_tm_enable(value != 0);
         else if (k == "cg_defer_x")
             cg_defer_x_enable(value != 0);
-        else if (k == "sense_rank_split")
-            sense_rank_split_enable(value != 0);
         else if (k == "conv_thin_tc")
             conv_thin_tc_enable(value != 0);
         else if (k == "conv_thin_tc_expand")
@@ -180,14 +176,8 @@ int mdnn_set_option(const char* key, long value)
             conv_force_chlast(value != 0);
         else if (k == "conv_tc_debug")
             conv_tc_debug(int(value));
-        else if (k == "conv_tc_pair")
-            conv_tc_pair_enable(value != 0);
-        else if (k == "conv_tc_form")
-            conv_tc_form(int(value));
         else if (k == "conv_bn_fuse")
             conv_bn_fuse_enable(value != 0);
-        else if (k == "conv_wgrad_mc")
-            conv_wgrad_mc_enable(value != 0);
         else
             throw ConfigError("unknown option '" + k + "'");
     });

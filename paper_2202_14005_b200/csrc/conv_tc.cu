@@ -49,184 +49,6 @@ constexpr int NTHREADS = 192;
 constexpr int EPI_PITCH = 20;
 constexpr int EPI_WARP_BYTES = 32 * EPI_PITCH * 4;
 
-template<int N>
-struct TcSmem {
-    static constexpr int B_BYTES = N * 128;
-    static constexpr int HALO_OFF = 0;
-    static constexpr int B_OFF = 2 * HALO_BYTES;
-    static constexpr int EPI_OFF = B_OFF + NBSTAGE * B_BYTES;
-    static constexpr int BAR_OFF = EPI_OFF + 4 * EPI_WARP_BYTES;
-    static constexpr int TOTAL = BAR_OFF + 256 + 1024; // + barriers + alignment slack
-};
-
-template<int CIN2, int N>
-__global__ void __launch_bounds__(NTHREADS, 1)
-    k_conv_tc(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
-              float* __restrict__ out, int X, int Y, int B, int dbg)
-{
-    static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
-    static_assert(N % 16 == 0 && N >= 16 && 2 * NM * N <= 512, "N must fit 2 x NM accumulators in TMEM");
-    constexpr int NCH = CIN2 / 32;
-    constexpr int ACC = 2 * NM * N; // double-buffered accumulators: epilogue of tile i overlaps MMAs of tile i+1
-    constexpr int TMEM_COLS = ACC <= 32 ? 32 : (ACC <= 64 ? 64 : (ACC <= 128 ? 128 : (ACC <= 256 ? 256 : 512)));
-    using S = TcSmem<N>;
-
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* halo = smem + S::HALO_OFF;
-    uint8_t* bst = smem + S::B_OFF;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
-    uint64_t* halo_full = bars;            // [2]
-    uint64_t* halo_empty = bars + 2;       // [2]
-    uint64_t* b_full = bars + 4;           // [NBSTAGE]
-    uint64_t* b_empty = bars + 4 + NBSTAGE;
-    uint64_t* tmem_full = bars + 4 + 2 * NBSTAGE; // [2]
-    uint64_t* tmem_empty = tmem_full + 2;         // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
-
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int tiles_x = (X + TILE_X - 1) / TILE_X, tiles_y = (Y + TILE_Y - 1) / TILE_Y;
-    const int ntiles = tiles_x * tiles_y * B;
-
-    if (warp == 0 && lane == 0) {
-        prefetch_tmap(&tm_act);
-        prefetch_tmap(&tm_w);
-        for (int i = 0; i < 2; i++) {
-            mbar_init(&halo_full[i], 1);
-            mbar_init(&halo_empty[i], 1);
-        }
-        for (int i = 0; i < NBSTAGE; i++) {
-            mbar_init(&b_full[i], 1);
-            mbar_init(&b_empty[i], 1);
-        }
-        for (int i = 0; i < 2; i++) {
-            mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 128);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 1)
-        tmem_alloc<TMEM_COLS>(tmem_slot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer ----------------
-            uint32_t hi = 0, bi = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
-                const int x0 = tx * TILE_X, y0 = ty * TILE_Y;
-                for (int c = 0; c < NCH; c++, hi++) {
-                    const uint32_t hb = hi & 1, hph = (hi >> 1) & 1;
-                    mbar_wait(&halo_empty[hb], hph ^ 1);
-                    mbar_arrive_expect_tx(&halo_full[hb], HALO_BYTES);
-                    tma_load_4d(halo + hb * HALO_BYTES, &tm_act, &halo_full[hb], c * 32, x0 - 1, y0 - 1, b);
-                    for (int t = 0; t < 9; t++, bi++) {
-                        const uint32_t st = bi % NBSTAGE, bph = (bi / NBSTAGE) & 1;
-                        mbar_wait(&b_empty[st], bph ^ 1);
-                        mbar_arrive_expect_tx(&b_full[st], S::B_BYTES);
-                        tma_load_2d(bst + st * S::B_BYTES, &tm_w, &b_full[st], t * CIN2 + c * 32, 0);
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer (single thread) ----------------
-            constexpr uint32_t idesc = idesc_tf32(128, N);
-            uint32_t hi = 0, bi = 0, ti = 0;
-            const uint32_t halo_addr = smem_u32(halo), b_addr = smem_u32(bst);
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
-                const uint32_t ab = ti & 1, acc = tmem_base + ab * NM * N;
-                mbar_wait(&tmem_empty[ab], ((ti >> 1) & 1) ^ 1);
-                tc_fence_after();
-                for (int c = 0; c < NCH; c++, hi++) {
-                    const uint32_t hb = hi & 1, hph = (hi >> 1) & 1;
-                    mbar_wait(&halo_full[hb], hph);
-                    tc_fence_after();
-                    const uint32_t hbase = halo_addr + hb * HALO_BYTES;
-                    for (int t = 0; t < 9; t++, bi++) {
-                        const uint32_t st = bi % NBSTAGE, bph = (bi / NBSTAGE) & 1;
-                        mbar_wait(&b_full[st], bph);
-                        tc_fence_after();
-                        const int ky = t / 3, kx = t % 3;
-                        const uint32_t bbase = b_addr + st * S::B_BYTES;
-#pragma unroll
-                        for (int xt = 0; xt < NM; xt++) {
-                            const uint32_t row0 = ky * HALO_P + xt * 8 + kx;
-#pragma unroll
-                            for (int k = 0; k < 4; k++) {
-                                const uint64_t ad = umma_desc_sw128(hbase + row0 * 128 + k * 32, HALO_P * 128);
-                                const uint64_t bd = umma_desc_sw128(bbase + k * 32, 1024);
-                                mma_tf32(acc + xt * N, ad, bd, idesc, (c | t | k) != 0);
-                            }
-                        }
-                        mma_commit(&b_empty[st]);
-                    }
-                    mma_commit(&halo_empty[hb]);
-                }
-                mma_commit(&tmem_full[ab]);
-            }
-        }
-    } else {
-        // ---------------- epilogue: TMEM -> registers -> global ----------------
-        const int lg = warp & 3; // TMEM lane group this warp may access
-        float* estage = reinterpret_cast<float*>(smem + S::EPI_OFF + lg * EPI_WARP_BYTES);
-        uint32_t ti = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
-            const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
-            const int x0 = tx * TILE_X, y0 = ty * TILE_Y;
-            const uint32_t ab = ti & 1, acc = tmem_base + ab * NM * N;
-            mbar_wait(&tmem_full[ab], (ti >> 1) & 1);
-            tc_fence_after();
-            if (dbg == 2) {
-                tc_fence_before();
-                mbar_arrive(&tmem_empty[ab]);
-                continue;
-            }
-            // Staged through shared memory so that each store instruction
-            // writes 8 pixels x 64 contiguous bytes (lanes 4 per pixel)
-            // instead of 32 scattered 16-byte pieces (LSU-throttled).
-            // Warp lg owns pixel rows gy = 4 lg .. 4 lg + 3 of each M-tile.
-            const int qd = lane & 3, pl = lane >> 2;
-#pragma unroll 1
-            for (int xt = 0; xt < NM; xt++) {
-#pragma unroll 1
-                for (int nc = 0; nc < N / 16; nc++) {
-                    float v[16];
-                    tmem_ld16(acc + (uint32_t(lg * 32) << 16) + xt * N + nc * 16, v);
-                    tmem_ld_wait();
-                    float4* st4 = reinterpret_cast<float4*>(estage + lane * EPI_PITCH);
-#pragma unroll
-                    for (int q = 0; q < 4; q++)
-                        st4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                    __syncwarp();
-#pragma unroll
-                    for (int it = 0; it < 4; it++) {
-                        const int rr = it * 8 + pl; // staged pixel: row 4 lg + it, x offset pl
-                        const int px = x0 + xt * 8 + pl, py = y0 + lg * 4 + it;
-                        const float4 val = reinterpret_cast<const float4*>(estage + rr * EPI_PITCH)[qd];
-                        if (px < X && py < Y && dbg != 1)
-                            reinterpret_cast<float4*>(out + ((long(b) * Y + py) * X + px) * N + nc * 16)[qd] = val;
-                    }
-                    __syncwarp();
-                }
-            }
-            tc_fence_before();
-            mbar_arrive(&tmem_empty[ab]);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem_base);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Transposed form for 2*Cout = 128 (the MoDL 64 -> 64 layers): one UMMA
 // computes D^T[n = output (re|im) channel, 128][p = pixel, 256] over an
@@ -693,11 +515,7 @@ struct WgSmem {
     static constexpr int TOTAL = BAR_OFF + 256 + 1024;
 };
 
-// MC: the three CTAs of a split (ky = 0, 1, 2) form a cluster; they walk the
-// same dy segments, so rank 0 TMA-multicasts each dy segment to all three
-// (L2->SMEM dy traffic / 3; the kernel is bound by that traffic, not by the
-// tensor pipe) and re-fills a stage only when all three released it.
-template<int N, bool MC>
+template<int N>
 __global__ void __launch_bounds__(NTHREADS, 1)
     k_conv_tc_wgrad(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
                     float* __restrict__ part, int X, int Y, int B, int nsplit)
@@ -711,9 +529,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint64_t* full = bars;
     uint64_t* empty = bars + WG_STAGES;
     uint64_t* tmem_full = bars + 2 * WG_STAGES;
-    uint64_t* dy_empty = tmem_full + 1; // [WG_STAGES], rank 0's used (MC)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dy_empty + WG_STAGES);
-    const uint32_t crank = MC ? cluster_ctarank() : 0;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int ky = blockIdx.x % 3, split = blockIdx.x / 3;
@@ -727,7 +543,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int i = 0; i < WG_STAGES; i++) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
-            mbar_init(&dy_empty[i], 3);
         }
         mbar_init(tmem_full, 1);
         fence_barrier_init();
@@ -735,10 +550,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (warp == 1)
         tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
-    if constexpr (MC)
-        cluster_sync(); // peers' barriers initialised before any multicast / remote arrive
-    else
-        __syncthreads();
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -750,19 +562,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 const int x0 = sx * WG_SEG;
                 const uint32_t st = it % WG_STAGES, ph = (it / WG_STAGES) & 1;
                 mbar_wait(&empty[st], ph ^ 1);
-                if (MC && crank == 0)
-                    mbar_wait(&dy_empty[st], ph ^ 1); // all three CTAs released the stage
                 mbar_arrive_expect_tx(&full[st], 4 * (WG_SEG + 2) * 128 + NDB * WG_SEG * 128);
                 uint8_t* base = smem + st * S::STAGE;
                 for (int j = 0; j < 4; j++)
                     tma_load_4d(base + j * WG_XBLK, &tm_x, &full[st], j * 32, x0 - 1, y + ky - 1, b);
-                if (!MC) {
-                    for (int j = 0; j < NDB; j++)
-                        tma_load_4d(base + 4 * WG_XBLK + j * WG_DBLK, &tm_dy, &full[st], j * 32, x0, y, b);
-                } else if (crank == 0) {
-                    for (int j = 0; j < NDB; j++)
-                        tma_load_4d_mc(base + 4 * WG_XBLK + j * WG_DBLK, &tm_dy, &full[st], j * 32, x0, y, b, 0x7);
-                }
+                for (int j = 0; j < NDB; j++)
+                    tma_load_4d(base + 4 * WG_XBLK + j * WG_DBLK, &tm_dy, &full[st], j * 32, x0, y, b);
             }
         }
     } else if (warp == 1) {
@@ -796,9 +601,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                                       (si != 0 || ks != 0) ? 1u : 0u);
                 }
                 mma_commit_warp(&empty[st]);
-                if constexpr (MC)
-                    if (lane == 0)
-                        mma_commit_mc(&dy_empty[st], 0x1);
             }
             mma_commit_warp(tmem_full);
         }
@@ -824,10 +626,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     }
     tc_fence_before();
-    if constexpr (MC)
-        cluster_sync(); // no CTA leaves while multicasts / remote arrivals may target it
-    else
-        __syncthreads();
+    __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<TMEM_COLS>(tmem_base);
@@ -968,10 +767,9 @@ CUtensorMap make_w_map(const float* base, int K, int N, int box_n = 0)
 }
 
 int g_tc_dbg = 0; // diagnostics: 1 = epilogue without global stores, 2 = no epilogue
-bool g_wgrad_mc = false; // bwd-weight: 3-CTA clusters with multicast dy segments (measured slower: 427 vs 402 us at C2)
-bool g_tc_pair = true; // CTA-pair (cta_group::2) kernel for the fwd / bwd-data convolutions
-int g_tc_form = 1;     // 1: transposed (channel-major accumulator) kernel where 2 Cout = 128
 
+// 2 Cout = 128: channel-major kernel (k_conv_tc_t); 2 Cout = 64: CTA-pair
+// pixel-major kernel (k_conv_tc_pair)
 template<int CIN2, int N>
 void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int B, double* stats = nullptr,
                int* stats_blocks = nullptr, const BnEpi& be = BnEpi{}, int* be_blocks = nullptr)
@@ -981,20 +779,9 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
     if (be_blocks)
         *be_blocks = 0;
     auto& c = ctx();
-    CUtensorMap ta = make_act_map(act, CIN2, X, Y, B);
-    CUtensorMap tw = make_w_map(wpk, 9 * CIN2, N);
-    auto kern = k_conv_tc<CIN2, N>;
-    const int smem = TcSmem<N>::TOTAL;
     static std::mutex mu;
-    static std::map<int, bool> done;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (!done[c.device]) {
-            CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            done[c.device] = true;
-        }
-    }
-    if (N == 128 && g_tc_form == 1) {
+    CUtensorMap tw = make_w_map(wpk, 9 * CIN2, N);
+    if constexpr (N == 128) {
         // transposed form: D^T[channel][pixel], N = 256 pixels per MMA
         CUtensorMap tat = make_act_map(act, CIN2, X, Y, B, TT_P, TT_L);
         auto kt = k_conv_tc_t<CIN2>;
@@ -1015,11 +802,10 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
             *stats_blocks = grid * (TT_EPI_WARPS / 4);
         if (be.part && be_blocks)
             *be_blocks = grid * (TT_EPI_WARPS / 4);
-        return;
-    }
-    const int ntiles = ((X + TILE_X - 1) / TILE_X) * ((Y + TILE_Y - 1) / TILE_Y) * B;
-    if (g_tc_pair) {
+    } else {
         // CTA pairs: half of every weight stage per CTA, multicast commits
+        CUtensorMap ta = make_act_map(act, CIN2, X, Y, B);
+        const int ntiles = ((X + TILE_X - 1) / TILE_X) * ((Y + TILE_Y - 1) / TILE_Y) * B;
         CUtensorMap twp = make_w_map(wpk, 9 * CIN2, N, N / 2);
         auto kp = k_conv_tc_pair<CIN2, N>;
         const int smem_p = TcPairSmem<N>::TOTAL;
@@ -1035,11 +821,7 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
         const int grid = 2 * std::min(npairs, c.sm_count / 2);
         kp<<<grid, NTHREADS, smem_p, c.stream>>>(ta, twp, out, X, Y, B, g_tc_dbg);
         KERNEL_CHECK();
-        return;
     }
-    const int grid = std::min(ntiles, c.sm_count);
-    kern<<<grid, NTHREADS, smem, c.stream>>>(ta, tw, out, X, Y, B, g_tc_dbg);
-    KERNEL_CHECK();
 }
 
 template<int N>
@@ -1048,8 +830,7 @@ void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, 
     auto& c = ctx();
     CUtensorMap tx = make_act_map(x, 128, X, Y, B, WG_SEG + 2, 1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     CUtensorMap td = make_act_map(dy, N, X, Y, B, WG_SEG, 1, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    auto kern = k_conv_tc_wgrad<N, false>;
-    auto kern_mc = k_conv_tc_wgrad<N, true>;
+    auto kern = k_conv_tc_wgrad<N>;
     const int smem = WgSmem<N>::TOTAL;
     static std::mutex mu;
     static std::map<int, bool> done;
@@ -1057,56 +838,16 @@ void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, 
         std::lock_guard<std::mutex> lk(mu);
         if (!done[c.device]) {
             CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            CUDA_CHECK(cudaFuncSetAttribute(kern_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             done[c.device] = true;
         }
     }
     const long nseg = long((X + WG_SEG - 1) / WG_SEG) * Y * B;
-    int nsplit = int(std::max(1L, std::min<long>(c.sm_count / 3, nseg)));
-    if (g_wgrad_mc) {
-        // co-resident 3-CTA clusters (GPC packing can leave SMs over): one wave
-        static std::map<int, int> max_cl;
-        std::lock_guard<std::mutex> lk(mu);
-        if (!max_cl.count(c.device)) {
-            cudaLaunchConfig_t q{};
-            q.gridDim = dim3(unsigned(3 * (c.sm_count / 3)));
-            q.blockDim = dim3(NTHREADS);
-            q.dynamicSmemBytes = size_t(smem);
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = 3;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            q.attrs = at;
-            q.numAttrs = 1;
-            int n = 0;
-            CUDA_CHECK(cudaOccupancyMaxActiveClusters(&n, kern_mc, &q));
-            max_cl[c.device] = std::max(1, n);
-        }
-        nsplit = std::max(1, std::min(nsplit, max_cl[c.device]));
-    }
+    const int nsplit = int(std::max(1L, std::min<long>(c.sm_count / 3, nseg)));
     float* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float) * size_t(nsplit) * 9 * 128 * N, c.stream));
-    if (g_wgrad_mc) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(unsigned(3 * nsplit));
-        cfg.blockDim = dim3(NTHREADS);
-        cfg.dynamicSmemBytes = size_t(smem);
-        cfg.stream = c.stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 3;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern_mc, tx, td, part, X, Y, B, nsplit));
-    } else {
-        kern<<<3 * nsplit, NTHREADS, smem, c.stream>>>(tx, td, part, X, Y, B, nsplit);
-    }
+    kern<<<3 * nsplit, NTHREADS, smem, c.stream>>>(tx, td, part, X, Y, B, nsplit);
     KERNEL_CHECK();
-    k_wgrad_fold<<<(9 * Cin * Cout + 63) / 64, 256, 0, c.stream>>>(dw, part, Cin, Cout, N,
-                                                                                         nsplit);
+    k_wgrad_fold<<<(9 * Cin * Cout + 63) / 64, 256, 0, c.stream>>>(dw, part, Cin, Cout, N, nsplit);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
@@ -1180,9 +921,6 @@ bool g_bn_fuse = true;
 }
 void conv_bn_fuse_enable(bool on) { g_bn_fuse = on; }
 bool conv_bn_fuse() { return g_bn_fuse; }
-void conv_tc_pair_enable(bool on) { g_tc_pair = on; }
-void conv_wgrad_mc_enable(bool on) { g_wgrad_mc = on; }
-void conv_tc_form(int f) { g_tc_form = f; }
 
 namespace {
 bool g_force_chlast = false;

@@ -294,25 +294,6 @@ __global__ void k_fmac_gather(FmacPlan p, long nout_total, long nred_total, cflo
     }
 }
 
-__global__ void k_fmac_atomic(Md3 m, long n, cfloat* out, const cfloat* a, const cfloat* b, bool conj2)
-{
-    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
-        long r = i, oo = 0, o1 = 0, o2 = 0;
-        for (int d = 0; d < m.rank; d++) {
-            long q = r % m.dims[d];
-            r /= m.dims[d];
-            oo += q * m.s0[d];
-            o1 += q * m.s1[d];
-            o2 += q * m.s2[d];
-        }
-        cfloat u = a[o1], v = b[o2];
-        if (conj2)
-            v.y = -v.y;
-        atomicAdd(&out[oo].x, u.x * v.x - u.y * v.y);
-        atomicAdd(&out[oo].y, u.x * v.y + u.y * v.x);
-    }
-}
-
 // layout conversion: CANON [inner][C][outer] <-> CHLAST per pixel [re C][im C]
 __global__ void k_canon_to_chlast(float* __restrict__ out, const cfloat* __restrict__ in, long inner, long C,
                                   long outer)
@@ -552,50 +533,70 @@ double host_znorm(const cfloat* a, long n)
     return std::sqrt(h[0]);
 }
 
+// Generic md_fmac2 (ops.hpp:79-111 via mdarray.hpp md_zfmac2 / md_zfmacc2).
+// Output dims whose strides overlap (an adjoint through a strided window view,
+// e.g. a convolution written as TenMul) cannot run as one gather: the greedy
+// injective chain of output dims (ascending stride) stays in the kernel and
+// every index of the remaining "serial" dims is its own launch, in a fixed
+// order -- no atomics, bitwise run-to-run deterministic (SURVEY §7 hard part 5,
+// reference guarantee mdarray.hpp:322-342).
 void launch_fmac_generic(const Dims& iter, cfloat* out, const Dims& so, const cfloat* in1, const Dims& s1,
                          const cfloat* in2, const Dims& s2, bool conj2)
 {
-    // split iteration dims into output (so != 0) and reduction (so == 0) dims
-    FmacPlan p{};
-    std::vector<std::pair<long, long>> outs; // (stride, extent) for injectivity check
+    struct Dim {
+        long n, so, s1, s2;
+    };
+    std::vector<Dim> odim, rdim;
     for (size_t d = 0; d < iter.size(); d++) {
         if (iter[d] == 1)
             continue;
-        if (so[d] != 0) {
-            p.odims[p.nout] = iter[d];
-            p.oso[p.nout] = so[d];
-            p.os1[p.nout] = s1[d];
-            p.os2[p.nout] = s2[d];
-            p.nout++;
-            outs.push_back({std::labs(so[d]), iter[d]});
+        (so[d] != 0 ? odim : rdim).push_back({iter[d], so[d], s1[d], s2[d]});
+    }
+    std::stable_sort(odim.begin(), odim.end(), [](const Dim& a, const Dim& b) { return std::labs(a.so) < std::labs(b.so); });
+    std::vector<Dim> inj, serial;
+    long span = 1;
+    for (const Dim& d : odim) {
+        if (std::labs(d.so) >= span) {
+            inj.push_back(d);
+            span = std::labs(d.so) * d.n;
         } else {
-            p.rdims[p.nred] = iter[d];
-            p.rs1[p.nred] = s1[d];
-            p.rs2[p.nred] = s2[d];
-            p.nred++;
+            serial.push_back(d);
         }
     }
-    std::sort(outs.begin(), outs.end());
-    bool injective = true;
-    long span = 1;
-    for (auto& [s, e] : outs) {
-        if (s < span)
-            injective = false;
-        span = s * e;
+    FmacPlan p{};
+    for (const Dim& d : inj) {
+        p.odims[p.nout] = d.n;
+        p.oso[p.nout] = d.so;
+        p.os1[p.nout] = d.s1;
+        p.os2[p.nout] = d.s2;
+        p.nout++;
     }
-    long nout = 1, nred = 1;
+    for (const Dim& d : rdim) {
+        p.rdims[p.nred] = d.n;
+        p.rs1[p.nred] = d.s1;
+        p.rs2[p.nred] = d.s2;
+        p.nred++;
+    }
+    long nout = 1, nred = 1, nser = 1;
     for (int i = 0; i < p.nout; i++)
         nout *= p.odims[i];
     for (int i = 0; i < p.nred; i++)
         nred *= p.rdims[i];
-    if (injective) {
-        k_fmac_gather<<<grid_for(nout), kThreads, 0, ctx().stream>>>(p, nout, nred, out, in1, in2, conj2);
-    } else {
-        auto m = make_md3(iter, so, s1, s2);
-        long n = md_size(iter);
-        k_fmac_atomic<<<grid_for(n), kThreads, 0, ctx().stream>>>(m, n, out, in1, in2, conj2);
+    for (const Dim& d : serial)
+        nser *= d.n;
+    for (long k = 0; k < nser; k++) {
+        long r = k, oo = 0, o1 = 0, o2 = 0;
+        for (const Dim& d : serial) {
+            const long q = r % d.n;
+            r /= d.n;
+            oo += q * d.so;
+            o1 += q * d.s1;
+            o2 += q * d.s2;
+        }
+        k_fmac_gather<<<grid_for(nout), kThreads, 0, ctx().stream>>>(p, nout, nred, out + oo, in1 + o1, in2 + o2,
+                                                                     conj2);
+        KERNEL_CHECK();
     }
-    KERNEL_CHECK();
 }
 
 void launch_copy(cfloat* dst, const cfloat* src, long n)

@@ -140,15 +140,10 @@ int conv_tc_stat_slots(); // epilogue partial-sum blocks per CTA (ConvGeom::stat
 // statistics, backward reduction); option "conv_bn_fuse", default on
 void conv_bn_fuse_enable(bool on);
 bool conv_bn_fuse();
-void conv_tc_pair_enable(bool on);
-void conv_wgrad_mc_enable(bool on);
-void conv_tc_form(int f);
 // persistent mask-pruned A^H A kernel (sense_rank.cuh); off = sense_fast.cuh path
 void sense_rank_enable(bool on);
 void sense_rank_ctas(long g);
-void sense_rank_tm_enable(bool on);
 void cg_defer_x_enable(bool on);
-void sense_rank_split_enable(bool on);
 bool rank_enabled();
 // test hook: auto-layout convs store multi-channel activations channels-last
 void conv_force_chlast(bool on);

@@ -885,9 +885,7 @@ bool g_rank_enabled = true;
 // rank-kernel CTA count override lives in sense_rank.cuh (g_rank_ctas)
 void sense_rank_enable(bool on) { g_rank_enabled = on; }
 void sense_rank_ctas(long g) { g_rank_ctas = g; }
-void sense_rank_tm_enable(bool on) { g_rank_tm = on; }
 void cg_defer_x_enable(bool on) { g_cg_defer_x = on; }
-void sense_rank_split_enable(bool on) { g_rank_split = on; }
 bool rank_enabled() { return g_rank_enabled; }
 
 CgResult read_cg_status(const double* status_dev)

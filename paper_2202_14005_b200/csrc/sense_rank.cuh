@@ -26,10 +26,8 @@
 
 #include <type_traits>
 
-bool g_rank_split = false; // two threads per (column, j) in the q-DFTs (k_normal_rank<.., 2>): 116 vs 72 us at C2 (spills at the 2-CTA register cap)
 bool g_cg_defer_x = true; // CG: keep every p, update r only per iteration, sum x once
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
-bool g_rank_tm = false; // TMEM-resident variant (sense_rank_tm.cuh) for N1 = 16
 
 constexpr int rank_nbox(int Y)
 {
@@ -178,16 +176,6 @@ __device__ void rank_build_plan(RankPlanSm<N1, N2>& pl, const RankArgs& a, int b
 }
 
 // Global plan record per pattern item: [RankPlanSm | ttw[TMAX * N2]], 16-B multiple.
-// v[q] *= exp(DIR 2 pi i q / N) for q = Q..NQ-1 (compile-time twiddles)
-template<int N, int DIR, int Q, int NQ>
-__device__ __forceinline__ void rank_rot_all(float2 (&v)[NQ])
-{
-    if constexpr (Q < NQ) {
-        v[Q] = fftd::rot<Q, N, DIR>(v[Q]);
-        rank_rot_all<N, DIR, Q + 1, NQ>(v);
-    }
-}
-
 template<int N1, int N2>
 struct RankPlanRec {
     static constexpr size_t PL = (sizeof(RankPlanSm<N1, N2>) + 15) & ~size_t(15);
@@ -203,20 +191,15 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT) k_rank_plan(RankArgs a, u
                             reinterpret_cast<float2*>(rec + RankPlanRec<N1, N2>::PL), a.tw);
 }
 
-// H = 2: two threads per (column, j) share the N1-point q-DFTs (each holds N1/2
-// points; one 8-value shuffle exchange per DFT, radix-2 split over lane ^ 16),
-// halving the per-thread accumulator / coil / value arrays so twice the warps
-// are resident per SM (the kernel is latency-bound).
-template<int N1, int N2, int H>
-__global__ void __launch_bounds__(RankCfg<N1, N2>::NT * H, RankCfg<N1, N2>::MINB)
+template<int N1, int N2>
+__global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
     k_normal_rank(RankArgs a, const __grid_constant__ CUtensorMap tmap, const unsigned char* __restrict__ plans)
 {
     using namespace fftd;
     using Cfg = RankCfg<N1, N2>;
     constexpr int Y = Cfg::Y, W = Cfg::W, JH = Cfg::JH, TMAX = Cfg::TMAX, N2P = Cfg::N2P;
-    constexpr int NT = Cfg::NT * H; // threads of this CTA
-    constexpr int NQ = N1 / H;      // q points per thread
-    static_assert(H == 1 || (H == 2 && Cfg::NT % 16 == 0), "split threads pair across lane ^ 16");
+    constexpr int NT = Cfg::NT; // threads of this CTA
+    constexpr int NQ = N1;      // q points per thread
     extern __shared__ __align__(128) float2 rank_smem[];
     float2* ring = rank_smem;
     float2* S = ring + 2 * Cfg::SLOT;
@@ -228,17 +211,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT * H, RankCfg<N1, N2>::MINB
     __shared__ __align__(16) RankPlanSm<N1, N2> pl;
 
     const int tid = threadIdx.x;
-    int w, j0, h;
-    if constexpr (H == 1) {
-        w = tid % W;
-        j0 = tid / W;
-        h = 0;
-    } else {
-        const int t16 = (tid >> 5) * 16 + (tid & 15); // (w, j) slot; lane bit 4 = half
-        w = t16 % W;
-        j0 = t16 / W;
-        h = (tid >> 4) & 1;
-    }
+    const int w = tid % W, j0 = tid / W;
     const bool active = j0 < N2;
     const int j = active ? j0 : N2 - 1;
     const int C = int(a.C), nxb = int(a.nxb);
@@ -299,20 +272,8 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT * H, RankCfg<N1, N2>::MINB
             float2 v[NQ];
 #pragma unroll
             for (int m = 0; m < NQ; m++)
-                v[m] = S[((H * m + h) * N2P + j) * W + w]; // H = 2: rows of this thread's parity
-            if constexpr (H == 1) {
-                dft_reg<N1, +1>(v);
-            } else {
-                // x[q] = E[q] + w^q O[q], x[q + NQ] = E[q] - w^q O[q]  (w = e^{+2 pi i / N1})
-                dft_reg<NQ, +1>(v);
-                if (h)
-                    rank_rot_all<N1, +1, 0, NQ>(v);
-#pragma unroll
-                for (int q = 0; q < NQ; q++) {
-                    const float2 u{__shfl_xor_sync(0xffffffffu, v[q].x, 16), __shfl_xor_sync(0xffffffffu, v[q].y, 16)};
-                    v[q] = h ? csub(u, v[q]) : cadd(v[q], u);
-                }
-            }
+                v[m] = S[(m * N2P + j) * W + w];
+            dft_reg<N1, +1>(v);
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
                 const float2 t = cmulc(v[q], cv[q]);
@@ -326,7 +287,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT * H, RankCfg<N1, N2>::MINB
                 cfloat* dst = rank_plane_dst(a, seg_s, blockIdx.x);
 #pragma unroll
                 for (int q = 0; q < NQ; q++) {
-                    const int y = j + N2 * (h * NQ + q);
+                    const int y = j + N2 * q;
                     const float2 xv = xs[y * W + w];
                     float2 o{acc[q].x * invN1, acc[q].y * invN1};
                     if (seg_first) {
@@ -380,13 +341,13 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT * H, RankCfg<N1, N2>::MINB
                 const float2* src = a.mode == 0 ? a.x : (a.it == 0 ? a.p_out : a.x);
 #pragma unroll
                 for (int q = 0; q < NQ; q++) {
-                    const long gi = img_base + a.X * (j + N2 * (h * NQ + q));
+                    const long gi = img_base + a.X * (j + N2 * q);
                     v[q] = colok ? src[gi] : float2{0.f, 0.f};
                     pv[q] = (colok && upd) ? a.p[gi] : float2{0.f, 0.f};
                 }
 #pragma unroll
                 for (int q = 0; q < NQ; q++) {
-                    const int y = j + N2 * (h * NQ + q);
+                    const int y = j + N2 * q;
                     if (upd) {
                         v[q] = float2{v[q].x + beta * pv[q].x, v[q].y + beta * pv[q].y};
                         if (seg_first && colok)
@@ -403,31 +364,19 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT * H, RankCfg<N1, N2>::MINB
             sm100::mbar_wait(&s_bar[slot], uint32_t((i >> 1) & 1));
             float2 v[NQ];
             // padding threads (j clamped) compute on valid rows; their results are never stored
-            const float2* csp = cs + (j + N2 * h * NQ) * W + w;
-            const float2* xsp = xs + (j + N2 * h * NQ) * W + w;
+            const float2* csp = cs + j * W + w;
+            const float2* xsp = xs + j * W + w;
 #pragma unroll
             for (int q = 0; q < NQ; q++)
                 cv[q] = csp[N2 * W * q];
 #pragma unroll
             for (int q = 0; q < NQ; q++)
                 v[q] = cmul(cv[q], xsp[N2 * W * q]);
-            if constexpr (H == 2) {
-                // X[2m] = DFT(a[q] + a[q + NQ]), X[2m + 1] = DFT((a[q] - a[q + NQ]) w^-q)
-#pragma unroll
-                for (int q = 0; q < NQ; q++) {
-                    const float2 u{__shfl_xor_sync(0xffffffffu, v[q].x, 16), __shfl_xor_sync(0xffffffffu, v[q].y, 16)};
-                    v[q] = h ? csub(u, v[q]) : cadd(v[q], u);
-                }
-                if (h)
-                    rank_rot_all<N1, -1, 0, NQ>(v);
-                dft_reg<NQ, -1>(v);
-            } else {
-                dft_reg<N1, -1>(v);
-            }
+            dft_reg<N1, -1>(v);
             if (active) {
 #pragma unroll
                 for (int m = 0; m < NQ; m++)
-                    S[((H * m + h) * N2P + j) * W + w] = v[m];
+                    S[(m * N2P + j) * W + w] = v[m];
             }
         }
         __syncthreads();
@@ -848,8 +797,6 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
     case 512: minb = RankCfg<16, 32>::MINB; break;
     case 640: minb = RankCfg<16, 40>::MINB; break;
     }
-    if (g_rank_tm && n1 == 16)
-        minb = 3; // k_normal_rank_tm: TMEM-resident accumulators, 3 CTAs per SM
     r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : long(minb) * ctx().sm_count, r.units));
     r.planes = 1;
     for (long s = 0; s < r.strips; s++)
@@ -872,13 +819,11 @@ void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const un
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS)
         throw CudaError("cuTensorMapEncodeTiled(coils) failed: " + std::to_string(int(res)));
-    auto kern = g_rank_split && N1 == 16 ? k_normal_rank<N1, N2, 2> : k_normal_rank<N1, N2, 1>;
-    const int nthreads = (g_rank_split && N1 == 16 ? 2 : 1) * Cfg::NT;
+    auto kern = k_normal_rank<N1, N2>;
+    const int nthreads = Cfg::NT;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_normal_rank<N1, N2, 1>),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
-        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_normal_rank<N1, N2, 2>),
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_normal_rank<N1, N2>),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(Cfg::SMEM)));
         attr = true;
     }
@@ -939,22 +884,10 @@ void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsign
 #undef X_
 }
 
-#include "sense_rank_tm.cuh"
-
 void launch_rank(const RankPlan& rp, RankArgs a, const cfloat* coils, const SenseGeom& g,
                  const unsigned char* plans)
 {
     fill_rank_args(rp, a, g);
-    if (g_rank_tm && rp.N1 == 16) {
-        switch (g.Y) {
-        case 256: launch_rank_tm_t<16, 16>(a, coils, g, plans); return;
-        case 320: launch_rank_tm_t<16, 20>(a, coils, g, plans); return;
-        case 368: launch_rank_tm_t<16, 23>(a, coils, g, plans); return;
-        case 512: launch_rank_tm_t<16, 32>(a, coils, g, plans); return;
-        case 640: launch_rank_tm_t<16, 40>(a, coils, g, plans); return;
-        default: break;
-        }
-    }
 #define X_(YY, A1, A2) \
     case YY: launch_rank_t<A1, A2>(a, coils, g, plans); return;
     switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }

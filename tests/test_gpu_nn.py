@@ -101,26 +101,19 @@ def test_conv_tensor_core_vs_cuda_core(gpu):
         assert rel_l2(a, b) <= 1e-3
 
 
-@pytest.mark.parametrize("opts", [{"conv_tc_form": 0, "conv_tc_pair": 0}, {"conv_tc_form": 0, "conv_tc_pair": 1},
-                                  {"conv_tc_form": 1, "conv_tc_pair": 0}])
-@pytest.mark.parametrize("cin,cout,X,Y,B", [(64, 64, 40, 70, 2), (32, 64, 17, 33, 1), (64, 32, 24, 16, 3)])
-def test_conv_tc_kernel_variants(gpu, ref, opts, cin, cout, X, Y, B):
-    """Every tcgen05 conv kernel form (pixel-major 1-CTA, CTA pair, channel-major
-    transposed) against the reference, fwd + bwd-data + bwd-weight, partial
-    super-tiles in x and y."""
+@pytest.mark.parametrize("cin,cout,X,Y,B", [(64, 64, 40, 70, 2), (32, 64, 17, 33, 1), (64, 32, 24, 16, 3),
+                                           (32, 32, 40, 50, 2)])
+def test_conv_tc_kernel_variants(gpu, ref, cin, cout, X, Y, B):
+    """Both tcgen05 conv kernel forms -- channel-major k_conv_tc_t (2 Cout = 128)
+    and the CTA-pair pixel-major k_conv_tc_pair (2 Cout = 64) -- against the
+    reference, fwd + bwd-data + bwd-weight, partial super-tiles in x and y."""
     rng = np.random.default_rng(cin + cout + X)
     in_dims = list(d16(X, Y, cin))
     in_dims[15] = B
-    try:
-        for k, v in opts.items():
-            gpu.check(gpu.so.mdnn_set_option(k.encode(), v))
-        mg = Model.conv_layer(gpu, "c", in_dims, (3, 3), cout)
-        mr = Model.conv_layer(ref, "c", in_dims, (3, 3), cout)
-        ins = [crand(rng, mr.nlop.in_dims(i)) for i in range(mr.nlop.n_in)]
-        _check_node(mg.nlop, mr.nlop, ins, rng, CONV_TOL, mr.arg_names)
-    finally:
-        gpu.check(gpu.so.mdnn_set_option(b"conv_tc_form", 1))
-        gpu.check(gpu.so.mdnn_set_option(b"conv_tc_pair", 1))
+    mg = Model.conv_layer(gpu, "c", in_dims, (3, 3), cout)
+    mr = Model.conv_layer(ref, "c", in_dims, (3, 3), cout)
+    ins = [crand(rng, mr.nlop.in_dims(i)) for i in range(mr.nlop.n_in)]
+    _check_node(mg.nlop, mr.nlop, ins, rng, CONV_TOL, mr.arg_names)
 
 
 @pytest.mark.parametrize("transposed", [False, True])
@@ -241,6 +234,33 @@ def test_bcast_add_and_tenmul(gpu, ref):
     so, sw, sx = (1, 0, 5) + (0,) * 13, (1, 5, 0) + (0,) * 13, (0, 1, 7) + (0,) * 13
     args = (it, yd, so, wd, sw, xd, sx)
     _check_node(Nlop.tenmul(gpu, *args), Nlop.tenmul(ref, *args), [crand(rng, wd), crand(rng, xd)], rng, TOL)
+
+
+def test_tenmul_overlapping_window_adjoint_deterministic(gpu, ref):
+    """A 2-D valid correlation written as one TenMul (conv_layer's wiring,
+    nn.hpp:305-337 / ops.hpp:79-111): the adjoint wrt the windowed input has
+    overlapping output strides.  Values match the reference and two runs are
+    bitwise identical (serial launches over the overlapping dims, no float
+    atomics)."""
+    rng = np.random.default_rng(18)
+    OX, OY, KX, KY, CI, CO = 9, 7, 3, 3, 2, 3
+    IX, IY = OX + KX - 1, OY + KY - 1
+    # iteration (ox, oy, kx, ky, ci, co); x[ox + kx, oy + ky, ci]; w[kx, ky, ci, co]; y[ox, oy, co]
+    it = (OX, OY, KX, KY, CI, CO) + (1,) * 10
+    xd, wd, yd = (IX, IY, CI) + (1,) * 13, (KX, KY, CI, CO) + (1,) * 12, (OX, OY, CO) + (1,) * 13
+    sx = (1, IX, 1, IX, IX * IY, 0) + (0,) * 10
+    sw = (0, 0, 1, KX, KX * KY, KX * KY * CI) + (0,) * 10
+    sy = (1, OX, 0, 0, 0, OX * OY) + (0,) * 10
+    args = (it, yd, sy, xd, sx, wd, sw)
+    ins = [crand(rng, xd), crand(rng, wd)]
+    _check_node(Nlop.tenmul(gpu, *args), Nlop.tenmul(ref, *args), ins, rng, TOL)
+    dy = crand(rng, yd)
+    runs = []
+    for _ in range(2):
+        n = Nlop.tenmul(gpu, *args)
+        n.apply(ins)
+        runs.append(n.adjoint_all(0, dy)[0])
+    assert runs[0].tobytes(order="A") == runs[1].tobytes(order="A")
 
 
 def test_pad_and_dft_nodes(gpu, ref):
