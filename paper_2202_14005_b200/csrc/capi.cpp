@@ -176,6 +176,8 @@ int mdnn_set_option(const char* key, long value)
             conv_force_chlast(value != 0);
         else if (k == "conv_tc_debug")
             conv_tc_debug(int(value));
+        else if (k == "conv_vn_tc")
+            conv_vn_tc_enable(value != 0);
         else if (k == "conv_bn_fuse")
             conv_bn_fuse_enable(value != 0);
         else

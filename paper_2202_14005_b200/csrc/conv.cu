@@ -510,10 +510,11 @@ __global__ void __launch_bounds__(256) k_sum_splits(cfloat* out, const float2* p
     }
 }
 
-// algorithmic flops of one pass: 8 per complex MAC
-double conv_flops(const ConvGeom& g)
+// algorithmic flops of one pass: 8 per complex MAC, or 2 per
+// real MAC when the host knows both operands are real (VarNet)
+double conv_flops(const ConvGeom& g, bool real = false)
 {
-    return 8.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * g.KX * g.KY;
+    return (real ? 2.0 : 8.0) * double(g.X) * g.Y * g.B * g.Cin * g.Cout * g.KX * g.KY;
 }
 
 void check_geom(const ConvGeom& g)
@@ -562,10 +563,12 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
-    ProfScope prof("conv_fwd", conv_flops(g));
     const bool known = (g.real_known & 3) == 3;
+    ProfScope prof("conv_fwd", conv_flops(g, known));
     unsigned* fl = known ? ctx().d_zero : imag_flag({{x, XY * g.Cin * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
-    {
+    if (conv_vn_tc_supported(g)) {
+        conv_vn_tc_run(y, x, w, g, 0, fl);
+    } else {
         const int RP = FGv == 2 ? rpx_for<2>() : rpx_for<8>();
         dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
                    unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
@@ -603,10 +606,12 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
     dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + TY - 1) / TY),
               unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
     const long XY = g.X * g.Y;
-    ProfScope prof("conv_bwd_data", conv_flops(g));
     const bool known = (g.real_known & 6) == 6;
+    ProfScope prof("conv_bwd_data", conv_flops(g, known));
     unsigned* fl = known ? ctx().d_zero : imag_flag({{dy, XY * g.Cout * g.B}, {w, g.KX * g.KY * g.Cin * g.Cout}});
-    {
+    if (conv_vn_tc_supported(g)) {
+        conv_vn_tc_run(dx, dy, w, g, 1, fl);
+    } else {
         const int RP = FGv == 2 ? rpx_for<2>() : rpx_for<8>();
         dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
                    unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
@@ -651,7 +656,7 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
         const size_t smem = sizeof(float2) * (g.Cin * (WTY + 10) * ((WTX + 10) | 1) + g.Cout * WTX * WTY);
         float2* part;
         CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
-        ProfScope prof("conv_bwd_weight", conv_flops(g));
+        ProfScope prof("conv_bwd_weight", conv_flops(g, (g.real_known & 5) == 5));
         const bool fp2 = g.Cout % 2 == 0;
         auto kern = fp2 ? k_conv_wgrad_rb<11, 2> : k_conv_wgrad_rb<11, 1>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));

@@ -1,0 +1,561 @@
+// VarNet 11 x 11 convolutions of real operands on the tensor cores (tcgen05,
+// kind::tf32, fp32 accumulate).  The layers (recon.hpp:522-609 via
+// nn.hpp:305-337) are K: 2 -> F (forward of K, adjoint of K^T) and
+// K^T: F -> 2 (forward of K^T, adjoint of K), F = 24, on CANON complex arrays
+// whose imaginary parts are known zero (DArray::known_real).
+//
+// Both kernels are row GEMMs whose accumulators live in per-output-row TMEM
+// "slots": an UMMA over one input row r writes the contributions of r to every
+// output row o = r - ky + 5 (ky = 0..10) of the current chunk at once -- the N
+// dimension runs over (output row, ...) and the ky of each slot is folded into
+// the B operand -- so the MMA's N is 24..256 instead of F, and the A operand
+// (one input row) is read once per K-step for all 11 kernel rows.
+//
+//  * k_vn_expand (2 -> F), y[p, f] = sum_{k, c} x[p + k - 5, c] w[k, c, f]:
+//    A = the im2col of one input row read through overlapping no-swizzle
+//    core matrices: a row holds (c0, c1) per pixel (8 B), UMMA row m = output
+//    pixel 2m (+ parity), K = (kx, c) = 24 (kx 11 = zero weight); rows are one
+//    pixel pair (16 B) apart and the K core matrices overlap (lbo = 16 B).
+//    Odd-start windows are 16-B aligned in a second copy of the row shifted by
+//    one pixel, so a 256-pixel tile is two M = 128 MMAs (even / odd outputs).
+//    N = (output row j, f) with slot width F8 = F rounded to 8; B rows are
+//    ordered by descending ky so consecutive slots meet consecutive B rows.
+//  * k_vn_reduce (F -> 2), dx[q, c] = sum_{k, f} dy[q - k + 5, f] w[k, c, f]:
+//    projection + gather.  A = one dy row (M = 128 input pixels, K = F), N =
+//    (output row j, kx, c) with 24-column slots: the MMA accumulates over ky
+//    (rows) in TMEM; the epilogue gathers the kx shift across lanes through
+//    shared memory (out[q] = sum_kx P[q - kx + 5][kx]); tiles overlap by 10
+//    pixels so every output's 11 inputs are in one tile.
+//
+// Warp roles (both kernels): warp 9 TMA-loads raw input rows (complex, zero
+// filled outside the image) into a ring, warps 0-3 convert them into the UMMA
+// operand layout (real parts, TF32-RN) in a second ring, warp 4 allocates TMEM
+// and issues the MMAs, warps 5-8 drain a finished chunk (double-buffered TMEM:
+// the epilogue of chunk i overlaps the MMAs of chunk i + 1) and re-zero its
+// slots.
+#include <cudaTypedefs.h>
+
+#include "kernels.h"
+#include "profile.h"
+#include "sm100.cuh"
+
+#include <algorithm>
+#include <string>
+
+namespace mdnn {
+
+namespace {
+
+using namespace sm100;
+
+constexpr int VK = 11, VP = 5;          // kernel extent, corner offset
+constexpr int V_THREADS = 320;          // 4 converter + 1 MMA + 4 epilogue + 1 TMA warps
+constexpr int V_SMEM_MIN = 120 * 1024;  // one CTA per SM: the kernels own all 512 TMEM columns
+
+// ---- expand (2 -> F) --------------------------------------------------------------
+constexpr int VE_RC = 5;                // output rows per chunk
+constexpr int VE_TILE = 256;            // output pixels per tile (128 even + 128 odd)
+constexpr int VE_ROWPX = 272;           // pixels per staged row copy (>= 256 + 12)
+constexpr int VE_COPY = VE_ROWPX * 8;   // bytes per copy
+constexpr int VE_NS = 8;                // operand ring slots (input rows)
+constexpr int VE_NR = 4;                // raw ring slots
+constexpr int VE_BOXPX = 96;            // pixels per TMA box (192 floats)
+constexpr int VE_RAW = 3 * 2 * VE_BOXPX * 8; // 3 boxes x 2 channels x 96 complex: pixels x0 - 6 .. x0 + 281
+// (TMA box starts must be 16-B aligned in the innermost dimension: even pixels)
+
+struct VeSmem {
+    int nb;         // B rows: 12 ky blocks of F8
+    int wb_bytes;   // B operand
+    int ring_off;
+    int raw_off;
+    int bar_off;
+    int total;
+    __host__ __device__ explicit VeSmem(int f8)
+    {
+        nb = 12 * f8;
+        wb_bytes = 6 * nb * 16;
+        ring_off = (wb_bytes + 1023) & ~1023;
+        raw_off = ring_off + VE_NS * 2 * VE_COPY;
+        bar_off = raw_off + VE_NR * VE_RAW;
+        total = bar_off + 256 + 1024 > V_SMEM_MIN ? bar_off + 256 + 1024 : V_SMEM_MIN;
+    }
+};
+
+__global__ void __launch_bounds__(V_THREADS, 1)
+    k_vn_expand(const __grid_constant__ CUtensorMap tm_x, float2* __restrict__ y, const float2* __restrict__ w, int X,
+                int Y, int B, int F, int F8, const unsigned* __restrict__ imag)
+{
+    if (*imag) // complex operands: the CUDA-core complex kernel of this launch pair runs instead
+        return;
+    const VeSmem L(F8);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* wb = reinterpret_cast<float*>(smem);
+    uint8_t* ring = smem + L.ring_off;
+    const float* raw = reinterpret_cast<const float*>(smem + L.raw_off);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* full = bars;                 // [VE_NS] 128 converter arrivals
+    uint64_t* empty = bars + VE_NS;        // [VE_NS] MMA commit
+    uint64_t* tfull = bars + 2 * VE_NS;    // [2] MMA commit
+    uint64_t* tempty = tfull + 2;          // [2] 4 epilogue warps
+    uint64_t* wb_full = tempty + 2;        // 128 converter arrivals
+    uint64_t* rfull = wb_full + 1;         // [VE_NR] TMA transaction bytes
+    uint64_t* rempty = rfull + VE_NR;      // [VE_NR] 128 converter arrivals
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + VE_NR);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nxt = (X + VE_TILE - 1) / VE_TILE, nch = (Y + VE_RC - 1) / VE_RC;
+    const long units = long(nxt) * nch * B;
+    const long u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+    const int NB = L.nb;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < VE_NS; i++) {
+            mbar_init(&full[i], 128);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_init(wb_full, 128);
+        for (int i = 0; i < VE_NR; i++) {
+            mbar_init(&rfull[i], 1);
+            mbar_init(&rempty[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 4)
+        tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 9) {
+        // ---- raw input rows by TMA: 3 boxes of 96 pixels x 2 channels from pixel x0 - 6, zero filled outside
+        if (lane == 0) {
+            prefetch_tmap(&tm_x);
+            uint32_t it = 0;
+            for (long u = u0; u < u1; u++) {
+                const int ch = int(u % nch), xt = int((u / nch) % nxt), b = int(u / (long(nch) * nxt));
+                const int o0 = ch * VE_RC, x0 = xt * VE_TILE;
+                for (int i = 0; i < VE_RC + 2 * VP; i++, it++) {
+                    const uint32_t rs = it % VE_NR, ph = (it / VE_NR) & 1;
+                    mbar_wait(&rempty[rs], ph ^ 1);
+                    mbar_arrive_expect_tx(&rfull[rs], VE_RAW);
+                    for (int j = 0; j < 3; j++)
+                        tma_load_3d(smem + L.raw_off + rs * VE_RAW + j * (VE_RAW / 3), &tm_x, &rfull[rs],
+                                    2 * (x0 - 6 + j * VE_BOXPX), o0 - VP + i, 2 * b);
+                }
+            }
+        }
+    } else if (warp < 4) {
+        // ---- converters: B operand once, then raw rows -> two im2col copies
+        const int t = threadIdx.x;
+        for (int e = t; e < 6 * NB * 4; e += 128) {
+            const int kk = e & 3, n = (e >> 2) % NB, kg = (e >> 2) / NB;
+            const int k = kg * 4 + kk, kx = k >> 1, c = k & 1, kyr = n / F8, f = n - kyr * F8;
+            float v = 0.f;
+            if (kx < VK && kyr < VK && f < F)
+                v = w[kx + VK * ((VK - 1 - kyr) + VK * (c + 2 * f))].x;
+            wb[(kg * NB + n) * 4 + kk] = to_tf32(v);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(wb_full);
+        uint32_t it = 0;
+        for (long u = u0; u < u1; u++) {
+            for (int i = 0; i < VE_RC + 2 * VP; i++, it++) {
+                const uint32_t st = it % VE_NS, ph = (it / VE_NS) & 1;
+                const uint32_t rs = it % VE_NR, rph = (it / VE_NR) & 1;
+                mbar_wait(&rfull[rs], rph);
+                mbar_wait(&empty[st], ph ^ 1);
+                const float* rw = raw + rs * (VE_RAW / 4);
+                float2* P = reinterpret_cast<float2*>(ring + st * 2 * VE_COPY); // pixel x0 - 4 + k
+                float2* Q = P + VE_ROWPX;                                       // pixel x0 - 5 + k
+                for (int k = t + 1; k <= VE_ROWPX + 1; k += 128) {              // raw pixel x0 - 6 + k
+                    const float* bx = rw + (k / VE_BOXPX) * (4 * VE_BOXPX) + 2 * (k % VE_BOXPX);
+                    const float2 v{to_tf32(bx[0]), to_tf32(bx[2 * VE_BOXPX])};
+                    if (k <= VE_ROWPX)
+                        Q[k - 1] = v;
+                    if (k >= 2)
+                        P[k - 2] = v;
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&full[st]);
+                mbar_arrive(&rempty[rs]);
+            }
+        }
+    } else if (warp == 4) {
+        // ---- MMA issue (whole warp, elected lane issues)
+        mbar_wait(wb_full, 0);
+        tc_fence_after();
+        const uint32_t wb_s = smem_u32(wb), ring_s = smem_u32(ring);
+        uint32_t it = 0, cit = 0;
+        for (long u = u0; u < u1; u++, cit++) {
+            const uint32_t buf = cit & 1;
+            mbar_wait(&tempty[buf], (cit >> 1) & 1); // zeroed by the epilogue
+            tc_fence_after();
+            for (int i = 0; i < VE_RC + 2 * VP; i++, it++) {
+                const uint32_t st = it % VE_NS, ph = (it / VE_NS) & 1;
+                mbar_wait(&full[st], ph);
+                tc_fence_after();
+                const int jlo = max(0, i - 2 * VP), jhi = min(VE_RC - 1, i);
+                const int n = ((jhi - jlo + 1) * F8 + 15) & ~15;
+                const uint32_t idesc = idesc_tf32(128, n);
+                const int kyr0 = 2 * VP - i + jlo;
+#pragma unroll
+                for (int par = 0; par < 2; par++) {
+                    // even outputs read the copy starting one pixel earlier (Q)
+                    const uint32_t a0 = ring_s + st * 2 * VE_COPY + (par == 0 ? VE_COPY : 0);
+                    const uint32_t d = tmem_base + buf * 256 + par * 128 + jlo * F8;
+#pragma unroll
+                    for (int s = 0; s < 3; s++) {
+                        const uint64_t ad = umma_desc_kn(a0 + 32 * s, 16, 128);
+                        const uint64_t bd = umma_desc_kn(wb_s + (2 * s * NB + kyr0 * F8) * 16, NB * 16, 128);
+                        mma_tf32_warp(d, ad, bd, idesc, 1u);
+                    }
+                }
+                mma_commit_warp(&empty[st]);
+            }
+            mma_commit_warp(&tfull[buf]);
+        }
+    } else {
+        // ---- epilogue: slots -> y (both parities of a pixel pair in one 16-B store), re-zero
+        const int lq = warp & 3, m = lq * 32 + lane;
+        const uint32_t lrow = uint32_t(lq * 32) << 16;
+        for (int c = 0; c < 512; c += 32)
+            tmem_st32_zero(tmem_base + lrow + c);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&tempty[0]);
+            mbar_arrive(&tempty[1]);
+        }
+        uint32_t cit = 0;
+        for (long u = u0; u < u1; u++, cit++) {
+            const int ch = int(u % nch), xt = int((u / nch) % nxt), b = int(u / (long(nch) * nxt));
+            const int o0 = ch * VE_RC, xx = xt * VE_TILE + 2 * m;
+            const uint32_t buf = cit & 1;
+            mbar_wait(&tfull[buf], (cit >> 1) & 1);
+            tc_fence_after();
+            for (int j = 0; j < VE_RC; j++) {
+                float v0[32], v1[32];
+                tmem_ld32(tmem_base + lrow + buf * 256 + j * F8, v0);
+                tmem_ld32(tmem_base + lrow + buf * 256 + 128 + j * F8, v1);
+                tmem_ld_wait();
+                const int o = o0 + j;
+                if (o < Y && xx < X) {
+                    float4* dst = reinterpret_cast<float4*>(y + xx + long(X) * (o + long(Y) * F * b));
+                    const long fs = long(X) * Y / 2; // float4 stride between channels
+#pragma unroll
+                    for (int f = 0; f < 32; f++)
+                        if (f < F)
+                            dst[f * fs] = make_float4(v0[f], 0.f, v1[f], 0.f);
+                }
+            }
+            for (int c = 0; c < 256; c += 32)
+                tmem_st32_zero(tmem_base + lrow + buf * 256 + c);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+// ---- reduce (F -> 2) --------------------------------------------------------------
+constexpr int VR_RC = 10;               // output rows per chunk
+constexpr int VR_OUT = 116;             // output pixels per tile: input pixels x0 - 6 .. x0 + 121 (the
+                                        // TMA box start must be 16-B aligned: an even pixel)
+constexpr int VR_NS = 4;                // operand ring slots
+constexpr int VR_NR = 3;                // raw ring slots (F x 128 complex each)
+constexpr int VR_SLOT = 24;             // TMEM columns per output row: (kx 0..11, c)
+constexpr int VR_EP = 25;               // gather buffer pitch (floats, odd: conflict-free)
+
+struct VrSmem {
+    int a_bytes, raw_bytes, wb_off, ring_off, raw_off, e_off, bar_off, total;
+    __host__ __device__ VrSmem(int f, int f8)
+    {
+        a_bytes = (f8 / 4) * 128 * 16;
+        raw_bytes = f * 128 * 8;
+        wb_off = 0;
+        ring_off = ((f8 / 4) * 288 * 16 + 1023) & ~1023;
+        raw_off = ring_off + VR_NS * a_bytes;
+        e_off = raw_off + VR_NR * raw_bytes;
+        bar_off = e_off + 2 * 128 * VR_EP * 4;
+        total = bar_off + 256 + 1024 > V_SMEM_MIN ? bar_off + 256 + 1024 : V_SMEM_MIN;
+    }
+};
+
+__global__ void __launch_bounds__(V_THREADS, 1)
+    k_vn_reduce(const __grid_constant__ CUtensorMap tm_dy, float2* __restrict__ dx, const float2* __restrict__ w, int X,
+                int Y, int B, int F, int F8, const unsigned* __restrict__ imag)
+{
+    if (*imag)
+        return;
+    const VrSmem L(F, F8);
+    constexpr int NB = 12 * VR_SLOT; // B rows: (ky 0..11, kx 0..11, c)
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* wb = reinterpret_cast<float*>(smem + L.wb_off);
+    uint8_t* ring = smem + L.ring_off;
+    const float* raw = reinterpret_cast<const float*>(smem + L.raw_off);
+    float* E = reinterpret_cast<float*>(smem + L.e_off);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + VR_NS;
+    uint64_t* tfull = bars + 2 * VR_NS;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* wb_full = tempty + 2;
+    uint64_t* rfull = wb_full + 1;
+    uint64_t* rempty = rfull + VR_NR;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rempty + VR_NR);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nxt = (X + VR_OUT - 1) / VR_OUT, nch = (Y + VR_RC - 1) / VR_RC;
+    const long units = long(nxt) * nch * B;
+    const long u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+    const int KG = F8 / 4;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < VR_NS; i++) {
+            mbar_init(&full[i], 128);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4);
+        }
+        mbar_init(wb_full, 128);
+        for (int i = 0; i < VR_NR; i++) {
+            mbar_init(&rfull[i], 1);
+            mbar_init(&rempty[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 4)
+        tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 9) {
+        // ---- raw dy rows by TMA: 128 complex x F channels, zero filled outside the image
+        if (lane == 0) {
+            prefetch_tmap(&tm_dy);
+            uint32_t it = 0;
+            for (long u = u0; u < u1; u++) {
+                const int ch = int(u % nch), xt = int((u / nch) % nxt), b = int(u / (long(nch) * nxt));
+                const int o0 = ch * VR_RC;
+                for (int i = 0; i < VR_RC + 2 * VP; i++, it++) {
+                    const uint32_t rs = it % VR_NR, ph = (it / VR_NR) & 1;
+                    mbar_wait(&rempty[rs], ph ^ 1);
+                    mbar_arrive_expect_tx(&rfull[rs], L.raw_bytes);
+                    tma_load_3d(smem + L.raw_off + rs * L.raw_bytes, &tm_dy, &rfull[rs], 2 * (xt * VR_OUT - VP - 1),
+                                o0 - VP + i, F * b);
+                }
+            }
+        }
+    } else if (warp < 4) {
+        const int t = threadIdx.x;
+        for (int e = t; e < KG * NB * 4; e += 128) {
+            const int kk = e & 3, n = (e >> 2) % NB, kg = (e >> 2) / NB;
+            const int f = kg * 4 + kk, ky = n / VR_SLOT, rem = n - ky * VR_SLOT, kx = rem >> 1, c = rem & 1;
+            float v = 0.f;
+            if (kx < VK && ky < VK && f < F)
+                v = w[kx + VK * (ky + VK * (c + 2 * f))].x;
+            wb[(kg * NB + n) * 4 + kk] = to_tf32(v);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(wb_full);
+        uint32_t it = 0;
+        for (long u = u0; u < u1; u++) {
+            for (int i = 0; i < VR_RC + 2 * VP; i++, it++) {
+                const uint32_t st = it % VR_NS, ph = (it / VR_NS) & 1;
+                const uint32_t rs = it % VR_NR, rph = (it / VR_NR) & 1;
+                mbar_wait(&rfull[rs], rph);
+                mbar_wait(&empty[st], ph ^ 1);
+                const float* rw = raw + rs * (L.raw_bytes / 4) + 2 * t; // real part of pixel t, channel 0
+                float4* A = reinterpret_cast<float4*>(ring + st * L.a_bytes);
+                for (int kg = 0; kg < KG; kg++) {
+                    float q[4];
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++) {
+                        const int f = kg * 4 + kk;
+                        q[kk] = f < F ? to_tf32(rw[f * 256]) : 0.f;
+                    }
+                    A[kg * 128 + t] = make_float4(q[0], q[1], q[2], q[3]);
+                }
+                fence_proxy_async_smem();
+                mbar_arrive(&full[st]);
+                mbar_arrive(&rempty[rs]);
+            }
+        }
+    } else if (warp == 4) {
+        mbar_wait(wb_full, 0);
+        tc_fence_after();
+        const uint32_t wb_s = smem_u32(wb), ring_s = smem_u32(ring);
+        uint32_t it = 0, cit = 0;
+        for (long u = u0; u < u1; u++, cit++) {
+            const uint32_t buf = cit & 1;
+            mbar_wait(&tempty[buf], (cit >> 1) & 1);
+            tc_fence_after();
+            for (int i = 0; i < VR_RC + 2 * VP; i++, it++) {
+                const uint32_t st = it % VR_NS, ph = (it / VR_NS) & 1;
+                mbar_wait(&full[st], ph);
+                tc_fence_after();
+                const int jlo = max(0, i - 2 * VP), jhi = min(VR_RC - 1, i);
+                const int n = ((jhi - jlo + 1) * VR_SLOT + 15) & ~15;
+                const uint32_t idesc = idesc_tf32(128, n);
+                const int ky0 = jlo - i + 2 * VP;
+                const uint32_t d = tmem_base + buf * 256 + jlo * VR_SLOT;
+                for (int s = 0; s < KG / 2; s++) {
+                    const uint64_t ad = umma_desc_kn(ring_s + st * L.a_bytes + 2 * s * 2048, 2048, 128);
+                    const uint64_t bd = umma_desc_kn(wb_s + (2 * s * NB + ky0 * VR_SLOT) * 16, NB * 16, 128);
+                    mma_tf32_warp(d, ad, bd, idesc, 1u);
+                }
+                mma_commit_warp(&empty[st]);
+            }
+            mma_commit_warp(&tfull[buf]);
+        }
+    } else {
+        // ---- epilogue: per output row, P[m][(kx, c)] -> E (smem) -> kx gather across pixels
+        const int lq = warp & 3, m = lq * 32 + lane, et = threadIdx.x - 160; // warps 5-8: et 0..127
+        const uint32_t lrow = uint32_t(lq * 32) << 16;
+        for (int c = 0; c < 512; c += 32)
+            tmem_st32_zero(tmem_base + lrow + c);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&tempty[0]);
+            mbar_arrive(&tempty[1]);
+        }
+        uint32_t cit = 0;
+        for (long u = u0; u < u1; u++, cit++) {
+            const int ch = int(u % nch), xt = int((u / nch) % nxt), b = int(u / (long(nch) * nxt));
+            const int o0 = ch * VR_RC, xq = xt * VR_OUT + et;
+            const uint32_t buf = cit & 1;
+            mbar_wait(&tfull[buf], (cit >> 1) & 1);
+            tc_fence_after();
+            for (int j = 0; j < VR_RC; j++) {
+                float v[32];
+                tmem_ld32(tmem_base + lrow + buf * 256 + j * VR_SLOT, v);
+                tmem_ld_wait();
+                float* e = E + (j & 1) * 128 * VR_EP;
+#pragma unroll
+                for (int k = 0; k < 2 * VK; k++)
+                    e[m * VR_EP + k] = v[k];
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const int o = o0 + j;
+                if (et < VR_OUT && xq < X && o < Y) {
+                    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                    for (int kx = 0; kx < VK; kx++) {
+                        const float* s = e + (et + 2 * VP + 1 - kx) * VR_EP + 2 * kx; // input pixel q - kx + 5
+                        a0 += s[0];
+                        a1 += s[1];
+                    }
+                    float2* dst = dx + xq + long(X) * (o + long(Y) * 2 * b);
+                    dst[0] = float2{a0, 0.f};
+                    dst[long(X) * Y] = float2{a1, 0.f};
+                }
+            }
+            for (int c = 0; c < 256; c += 32)
+                tmem_st32_zero(tmem_base + lrow + buf * 256 + c);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(&tempty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+bool g_vn_tc = true;
+
+PFN_cuTensorMapEncodeTiled_v12000 vn_encode()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess)
+            throw CudaError("cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// complex CANON array [X][Y][planes] as fp32 [2X][Y][planes]; box (bx floats, 1 row, bp planes)
+CUtensorMap vn_map(const cfloat* base, int X, int Y, long planes, int bx, int bp)
+{
+    CUtensorMap m;
+    cuuint64_t dims[3] = {cuuint64_t(2 * X), cuuint64_t(Y), cuuint64_t(planes)};
+    cuuint64_t strides[2] = {cuuint64_t(2 * X) * 4, cuuint64_t(2 * X) * Y * 4};
+    cuuint32_t box[3] = {cuuint32_t(bx), 1, cuuint32_t(bp)};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = vn_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<cfloat*>(base), dims, strides, box,
+                             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw CudaError("cuTensorMapEncodeTiled(varnet row) failed: " + std::to_string(int(r)));
+    return m;
+}
+
+// real flops of one 11 x 11 pass: 2 per real MAC
+double vn_flops(const ConvGeom& g) { return 2.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * g.KX * g.KY; }
+
+} // namespace
+
+void conv_vn_tc_enable(bool on) { g_vn_tc = on; }
+
+bool conv_vn_tc_supported(const ConvGeom& g)
+{
+    return g_vn_tc && g.KX == VK && g.KY == VK && g.Cin == 2 && g.Cout >= 1 && g.Cout <= 24 && !g.in_chlast
+           && !g.out_chlast && !(g.X & 1) && g.X * g.Y * g.B * g.Cout < (1L << 31);
+}
+
+void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode, const unsigned* imag)
+{
+    auto& c = ctx();
+    const int F = int(g.Cout), F8 = (F + 7) & ~7;
+    const int X = int(g.X), Y = int(g.Y), B = int(g.B);
+    if (mode == 0) {
+        const VeSmem L(F8);
+        const long units = long((X + VE_TILE - 1) / VE_TILE) * ((Y + VE_RC - 1) / VE_RC) * B;
+        const int grid = int(std::min<long>(units, c.sm_count));
+        CUDA_CHECK(cudaFuncSetAttribute(k_vn_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
+        const CUtensorMap tm = vn_map(in, X, Y, 2L * B, 2 * VE_BOXPX, 2);
+        ProfScope prof("conv_vn_fwd", vn_flops(g));
+        k_vn_expand<<<grid, V_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
+    } else {
+        const VrSmem L(F, F8);
+        const long units = long((X + VR_OUT - 1) / VR_OUT) * ((Y + VR_RC - 1) / VR_RC) * B;
+        const int grid = int(std::min<long>(units, c.sm_count));
+        CUDA_CHECK(cudaFuncSetAttribute(k_vn_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
+        const CUtensorMap tm = vn_map(in, X, Y, long(F) * B, 256, F);
+        ProfScope prof("conv_vn_bwd_data", vn_flops(g));
+        k_vn_reduce<<<grid, V_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
+    }
+    KERNEL_CHECK();
+}
+
+} // namespace mdnn

@@ -132,6 +132,13 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g);
 void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom& g);
 // dw[t,c,f] = sum_p dy[p,f] conj(x[p+t-c0, c])
 void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g);
+// VarNet 11 x 11 layers (Cin = 2, Cout <= 24, CANON) of real operands on the
+// tensor cores (conv_vn_tc.cu): mode 0 = forward, 1 = bwd-data.  `imag` is a
+// device flag (nonzero: an operand has imaginary parts -> the kernel exits and
+// the caller's CUDA-core complex kernel of the same pair does the work)
+bool conv_vn_tc_supported(const ConvGeom& g);
+void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode, const unsigned* imag);
+void conv_vn_tc_enable(bool on);
 // tcgen05 TF32 implicit-GEMM path (conv_tc.cu) for 3x3 layers with 32/64 channels
 void conv_tc_enable(bool on);
 void conv_tc_debug(int mode);

@@ -362,7 +362,9 @@ def test_c3_varnet_regulariser(gpu, ref, ref64):
     """VarNet stage regulariser sum_f K^T Phi'(Re K x) (recon.hpp:522-609) at
     C3 geometry: 640x368, 24 filters 11x11, 31 RBF centres, perturbed RBF
     weights (zero-init kills the gradients): output, weight
-    gradients and input cotangent vs fp64."""
+    gradients and input cotangent vs fp64.  The 11 x 11 convolutions run on
+    the tensor cores (TF32): outputs at 1e-3, gradients at the end-to-end TF32
+    bound 5e-3 (measured: weight gradient 1.04e-3)."""
     ph, cm, pat = sim_data(ref, 640, 368, 15, 1)
     kw = dict(iterations=1, filters=24, kernel=11, rbf=31, im_x=640, im_y=368, coils=15, batch=1)
     res = []
@@ -375,7 +377,7 @@ def test_c3_varnet_regulariser(gpu, ref, ref64):
                 w[k] = np.asfortranarray(rng.uniform(-0.05, 0.05, w[k].shape).astype(np.complex64))
         ins = [ph if k == ARG_DATA else w[a] for a, k, _ in m.args]
         res.append(_apply_and_grads(lib, m, ins, want_x=True))
-    _e2e_check(*res, out_tol=CONV_TOL, grad_tol=CONV_TOL)
+    _e2e_check(*res, out_tol=CONV_TOL, grad_tol=MODES["tf32"][2])  # TF32 11x11 convs: e2e bound as C1
 
 
 # ---------------------------------------------------------------------------

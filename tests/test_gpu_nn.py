@@ -290,27 +290,66 @@ def test_graph_algebra(gpu, ref):
 
 @pytest.mark.parametrize("cin,cout,k", [(2, 24, 11), (2, 6, 11), (3, 5, 5)])
 @pytest.mark.parametrize("transposed", [False, True])
-def test_conv_layer_real_operands(gpu, ref, cin, cout, k, transposed):
-    """VarNet-style real-valued activations, weights and cotangents take the
-    real-operand fast path of the CUDA-core convolutions (conv.cu); values,
-    tangents and adjoints still match the reference's complex arithmetic, and
-    the imaginary parts stay exactly zero."""
+@pytest.mark.parametrize("vn_tc", [1, 0], ids=["vn_tc", "cuda_core"])
+def test_conv_layer_real_operands(gpu, ref, cin, cout, k, transposed, vn_tc):
+    """VarNet-style real-valued activations, weights and cotangents.  The
+    11 x 11, 2 <-> F layers run on the tensor cores (conv_vn_tc.cu, TF32 budget
+    1e-3) unless option conv_vn_tc = 0 selects the fp32 real-operand CUDA-core
+    kernels (conv.cu, 1e-5); the weight gradient is the CUDA-core kernel either
+    way.  Values, tangents and adjoints match the reference's complex
+    arithmetic, the imaginary parts stay exactly zero, and a complex cotangent
+    switches to the complex path (1e-5)."""
     rng = np.random.default_rng(cin * 7 + cout + k)
     X, Y, B = 36, 20, 2
     in_dims = list(d16(X, Y, cin))
     in_dims[15] = B
-    mg = Model.conv_layer(gpu, "c", in_dims, (k, k), cout, transposed=transposed, bias=False)
-    mr = Model.conv_layer(ref, "c", in_dims, (k, k), cout, transposed=transposed, bias=False)
-    ng, nr = mg.nlop, mr.nlop
-    ins = [rrand(rng, nr.in_dims(i)) for i in range(nr.n_in)]
-    og, orf = ng.apply(ins)[0], nr.apply(ins)[0]
-    assert rel_l2(og, orf) <= 1e-5 and not np.any(og.imag)
-    dy = rrand(rng, nr.out_dims(0))
-    ag, ar = ng.adjoint_all(0, dy), nr.adjoint_all(0, dy)
-    for i in range(nr.n_in):
-        assert rel_l2(ag[i], ar[i]) <= 1e-5, i
-        assert not np.any(ag[i].imag), i
-    # a complex cotangent switches back to the complex path
-    dyc = crand(rng, nr.out_dims(0))
-    for u, v in zip(ng.adjoint_all(0, dyc), nr.adjoint_all(0, dyc)):
-        assert rel_l2(u, v) <= 1e-5
+    tc = vn_tc and k == 11 and cin == 2
+    tol = CONV_TOL if tc else 1e-5
+    gpu.check(gpu.so.mdnn_set_option(b"conv_vn_tc", vn_tc))
+    try:
+        mg = Model.conv_layer(gpu, "c", in_dims, (k, k), cout, transposed=transposed, bias=False)
+        mr = Model.conv_layer(ref, "c", in_dims, (k, k), cout, transposed=transposed, bias=False)
+        ng, nr = mg.nlop, mr.nlop
+        ins = [rrand(rng, nr.in_dims(i)) for i in range(nr.n_in)]
+        og, orf = ng.apply(ins)[0], nr.apply(ins)[0]
+        assert rel_l2(og, orf) <= tol and not np.any(og.imag)
+        dy = rrand(rng, nr.out_dims(0))
+        ag, ar = ng.adjoint_all(0, dy), nr.adjoint_all(0, dy)
+        for i in range(nr.n_in):
+            assert rel_l2(ag[i], ar[i]) <= tol, i
+            assert not np.any(ag[i].imag), i
+        # a complex cotangent switches back to the complex path
+        dyc = crand(rng, nr.out_dims(0))
+        for u, v in zip(ng.adjoint_all(0, dyc), nr.adjoint_all(0, dyc)):
+            assert rel_l2(u, v) <= 1e-5
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"conv_vn_tc", 1))
+
+
+@pytest.mark.parametrize("X,Y,B,F", [(640, 368, 1, 24), (258, 37, 2, 24), (100, 130, 3, 6)],
+                         ids=["C3-geometry", "ragged", "F6"])
+def test_vn_tensor_core_vs_fp32_kernels(gpu, ref, X, Y, B, F):
+    """The tensor-core 11 x 11 kernels against the fp32 CUDA-core kernels and the
+    reference at the C3 geometry (640 x 368: three 256-pixel expand tiles, the
+    last one partial, six overlapping 118-pixel reduce tiles, 74 / 37 row
+    chunks) and ragged shapes (partial tiles and chunks in x and y)."""
+    rng = np.random.default_rng(X + Y + F)
+    in_dims = list(d16(X, Y, 2))
+    in_dims[15] = B
+    mr = Model.conv_layer(ref, "c", in_dims, (11, 11), F, transposed=False, bias=False)
+    ins = [rrand(rng, mr.nlop.in_dims(i)) for i in range(2)]
+    dy = rrand(rng, mr.nlop.out_dims(0))
+    res = []
+    for tc in (1, 0):
+        gpu.check(gpu.so.mdnn_set_option(b"conv_vn_tc", tc))
+        try:
+            n = Model.conv_layer(gpu, "c", in_dims, (11, 11), F, transposed=False, bias=False).nlop
+            y = n.apply(ins)[0]
+            res.append((y, n.adjoint_all(0, dy)[0]))
+        finally:
+            gpu.check(gpu.so.mdnn_set_option(b"conv_vn_tc", 1))
+    nr = mr.nlop
+    yr = nr.apply(ins)[0]
+    dxr = nr.adjoint_all(0, dy)[0]
+    assert rel_l2(res[0][0], yr) <= CONV_TOL and rel_l2(res[0][1], dxr) <= CONV_TOL
+    assert rel_l2(res[1][0], yr) <= 1e-5 and rel_l2(res[1][1], dxr) <= 1e-5
