@@ -629,7 +629,7 @@ def roofline(lib, step_ms_total):
     except Exception:
         pass
     tags = {"sense_normal_y_cg": "hbm", "sense_normal_y": "hbm", "cg_update_rank": "hbm", "fft": "hbm", "conv_fwd": "tensor",
-            "conv_bwd_data": "tensor", "conv_bwd_weight": "tensor", "conv_tc_fwd": "tensor", "conv_vn_fwd": "tensor", "conv_vn_bwd_data": "tensor",
+            "conv_bwd_data": "tensor", "conv_bwd_weight": "tensor", "conv_tc_fwd": "tensor", "conv_vn_fwd": "tensor", "conv_vn_bwd_data": "tensor", "conv_vn_bwd_weight": "tensor",
             "conv_tc_bwd_data": "tensor", "conv_tc_bwd_weight": "tensor", "conv_thin_fwd": "hbm",
             "conv_thin_bwd_data": "hbm", "conv_thin_bwd_weight": "hbm", "bnblock_fwd": "hbm", "bnblock_bwd": "hbm"}
     rows = []

@@ -384,9 +384,12 @@ __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, A
 // 2K real FMAs instead of 2 per K)
 template<int K, int FP>
 __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part, Acc x, Acc dy, ConvGeom g,
-                                                        int nsplit, const unsigned* __restrict__ imag_flag)
+                                                        int nsplit, const unsigned* __restrict__ imag_flag,
+                                                        bool complex_only = false)
 {
     const bool real = imag_flag && *imag_flag == 0;
+    if (complex_only && real) // the tensor-core kernel of this launch pair handles real operands
+        return;
     constexpr int HX = WTX + K - 1, HY = WTY + K - 1;
     // odd float2 row pitch: the K kernel-row lanes of a warp read K different rows
     // at the same column; an even pitch (42) mapped several of them to one bank
@@ -484,8 +487,11 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
 // out[i] = sum_s part[s][i]: block = 64 outputs x 4 split groups (group g sums
 // splits g, g + 4, ... in order; the groups are added in order): the serial
 // per-output loop over ~300 splits was latency-bound
-__global__ void __launch_bounds__(256) k_sum_splits(cfloat* out, const float2* part, long n, int nsplit)
+__global__ void __launch_bounds__(256) k_sum_splits(cfloat* out, const float2* part, long n, int nsplit,
+                                                    const unsigned* __restrict__ complex_only = nullptr)
 {
+    if (complex_only && *complex_only == 0)
+        return;
     __shared__ double2 red[4][64];
     const int o = threadIdx.x & 63, gq = threadIdx.x >> 6;
     const long i = long(blockIdx.x) * 64 + o;
@@ -647,30 +653,37 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     }
     const long KK = g.KX * g.KY;
     if (g.KX == 11 && g.KY == 11 && 11 * g.Cin * g.Cout <= 576) {
-        // register-blocked kernel (VarNet K = 11 layers)
+        // VarNet K = 11 layers: tensor cores for real operands (conv_vn_tc.cu),
+        // the register-blocked CUDA-core kernel for complex ones; with operands not
+        // known real on the host both are launched and the device imag flag picks
         auto& c = ctx();
-        const long ntiles = ((g.X + WTX - 1) / WTX) * ((g.Y + WTY - 1) / WTY) * g.B;
-        const int nsplit = int(std::min<long>(ntiles, 2L * c.sm_count));
-        const long n = KK * g.Cin * g.Cout;
         const long XY = g.X * g.Y;
-        const size_t smem = sizeof(float2) * (g.Cin * (WTY + 10) * ((WTX + 10) | 1) + g.Cout * WTX * WTY);
-        float2* part;
-        CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
-        ProfScope prof("conv_bwd_weight", conv_flops(g, (g.real_known & 5) == 5));
-        const bool fp2 = g.Cout % 2 == 0;
-        auto kern = fp2 ? k_conv_wgrad_rb<11, 2> : k_conv_wgrad_rb<11, 1>;
-        allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
-        const int nthr = int(((11 * g.Cin * (fp2 ? g.Cout / 2 : g.Cout) + 31) / 32) * 32);
         const bool known = (g.real_known & 5) == 5;
+        const bool tc = conv_vn_tc_supported(g);
         unsigned* fl = known ? c.d_zero : imag_flag({{x, XY * g.Cin * g.B}, {dy, XY * g.Cout * g.B}});
-        kern<<<nsplit, nthr, smem, c.stream>>>(part, Acc{x, g.Cin, XY, g.in_chlast}, Acc{dy, g.Cout, XY, g.out_chlast},
-                                              g, nsplit, fl);
-        KERNEL_CHECK();
+        if (tc)
+            conv_vn_tc_wgrad(dw, x, dy, g, fl);
+        if (!tc || !known) {
+            const long ntiles = ((g.X + WTX - 1) / WTX) * ((g.Y + WTY - 1) / WTY) * g.B;
+            const int nsplit = int(std::min<long>(ntiles, 2L * c.sm_count));
+            const long n = KK * g.Cin * g.Cout;
+            const size_t smem = sizeof(float2) * (g.Cin * (WTY + 10) * ((WTX + 10) | 1) + g.Cout * WTX * WTY);
+            float2* part;
+            CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * nsplit, c.stream));
+            ProfScope prof("conv_bwd_weight", conv_flops(g, known));
+            const bool fp2 = g.Cout % 2 == 0;
+            auto kern = fp2 ? k_conv_wgrad_rb<11, 2> : k_conv_wgrad_rb<11, 1>;
+            allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
+            const int nthr = int(((11 * g.Cin * (fp2 ? g.Cout / 2 : g.Cout) + 31) / 32) * 32);
+            kern<<<nsplit, nthr, smem, c.stream>>>(part, Acc{x, g.Cin, XY, g.in_chlast},
+                                                  Acc{dy, g.Cout, XY, g.out_chlast}, g, nsplit, fl, tc);
+            KERNEL_CHECK();
+            k_sum_splits<<<int((n + 63) / 64), 256, 0, c.stream>>>(dw, part, n, nsplit, tc ? fl : nullptr);
+            KERNEL_CHECK();
+            CUDA_CHECK(cudaFreeAsync(part, c.stream));
+        }
         if (!known)
             CUDA_CHECK(cudaFreeAsync(fl, c.stream));
-        k_sum_splits<<<int((n + 63) / 64), 256, 0, c.stream>>>(dw, part, n, nsplit);
-        KERNEL_CHECK();
-        CUDA_CHECK(cudaFreeAsync(part, c.stream));
         return;
     }
     const bool small_k = KK * 4 * 8 <= 256 * WMAXC;

@@ -488,6 +488,241 @@ __global__ void __launch_bounds__(V_THREADS, 1)
     }
 }
 
+// ---- weight gradient ---------------------------------------------------------------
+// dw[kx, ky, c, f] = sum_p x[p + (kx - 5, ky - 5), c] dy[p, f] as a K = pixels
+// GEMM per dy row o: D_g[m = (ky, s, c), f] for kx = 4 g + s (g = 0..2, three
+// M = 128 accumulators, 32 TMEM columns each).  A is a window of the 11 x rows
+// o - 5 .. o + 5 staged as [pixel quad][row slot][s][c][4 px] with the four
+// one-pixel phases s pre-shifted: the kx = 4 g shift is a whole quad (+LBO)
+// and consecutive row slots are consecutive 8-row groups (SBO = 128 B), so
+// every MMA's M rows are the 11 kernel rows (+5 unused slots) of one g.  The
+// window is a ring of 16 rows stored twice (slots j and j + 16) so the 16
+// slots an MMA reads are always contiguous.  B = the dy row as [quad][f][4].
+constexpr int VW_PC = 64;               // dy pixels per column chunk
+constexpr int VW_PQ = 19;               // staged x pixel quads: p0 - 5 + 4 pq + s + i
+constexpr int VW_SL = 16;               // window rows (ring)
+constexpr int VW_XRAW = 2 * 160 * 4;    // raw x row: 2 planes x 80 complex from pixel p0 - 6
+constexpr int VW_NXR = 16;              // raw x ring
+constexpr int VW_NB = 3;                // B ring
+constexpr int VW_BB = (VW_PC / 4) * 32 * 16; // B slot: 16 quads x 32 f rows x 16 B
+constexpr int VW_MD = 8;                // dy-row completion ring
+
+struct VwSmem {
+    int xb_off, b_off, xr_off, dr_off, bar_off, total, dr_bytes;
+    __host__ __device__ explicit VwSmem(int f)
+    {
+        dr_bytes = f * VW_PC * 8;
+        xb_off = 0;
+        b_off = VW_PQ * 2 * VW_SL * 128;
+        xr_off = b_off + VW_NB * VW_BB;
+        dr_off = xr_off + VW_NXR * VW_XRAW;
+        bar_off = dr_off + 2 * dr_bytes;
+        total = bar_off + 512 + 1024 > V_SMEM_MIN ? bar_off + 512 + 1024 : V_SMEM_MIN;
+    }
+};
+
+__global__ void __launch_bounds__(V_THREADS, 1)
+    k_vn_wgrad(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
+               float2* __restrict__ part, int X, int Y, int B, int F, const unsigned* __restrict__ imag)
+{
+    if (*imag)
+        return;
+    const VwSmem L(F);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* xb = reinterpret_cast<float*>(smem + L.xb_off);
+    uint8_t* bring = smem + L.b_off;
+    const float* xr = reinterpret_cast<const float*>(smem + L.xr_off);
+    const float* dr = reinterpret_cast<const float*>(smem + L.dr_off);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* bfull = bars;                  // [VW_NB] 128 converter arrivals
+    uint64_t* bempty = bfull + VW_NB;        // [VW_NB] MMA commit
+    uint64_t* mdone = bempty + VW_NB;        // [VW_MD] MMA commit per dy row
+    uint64_t* xfull = mdone + VW_MD;         // [VW_NXR] TMA
+    uint64_t* xempty = xfull + VW_NXR;       // [VW_NXR] 128 converter arrivals
+    uint64_t* dfull = xempty + VW_NXR;       // [2] TMA
+    uint64_t* dempty = dfull + 2;            // [2] 128 converter arrivals
+    uint64_t* tfull = dempty + 2;            // MMA commit after the last row
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int nxc = (X + VW_PC - 1) / VW_PC;
+    const long items = long(nxc) * Y * B;
+    const long i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < VW_NB; i++) {
+            mbar_init(&bfull[i], 128);
+            mbar_init(&bempty[i], 1);
+        }
+        for (int i = 0; i < VW_MD; i++)
+            mbar_init(&mdone[i], 1);
+        for (int i = 0; i < VW_NXR; i++) {
+            mbar_init(&xfull[i], 1);
+            mbar_init(&xempty[i], 128);
+        }
+        for (int i = 0; i < 2; i++) {
+            mbar_init(&dfull[i], 1);
+            mbar_init(&dempty[i], 128);
+        }
+        mbar_init(tfull, 1);
+        fence_barrier_init();
+    }
+    if (warp == 4)
+        tmem_alloc<128>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 9) {
+        if (lane == 0) {
+            prefetch_tmap(&tm_x);
+            prefetch_tmap(&tm_dy);
+            uint32_t xit = 0;
+            auto load_x = [&](int r, int p0, int b) {
+                const uint32_t s = xit % VW_NXR, ph = (xit / VW_NXR) & 1;
+                mbar_wait(&xempty[s], ph ^ 1);
+                mbar_arrive_expect_tx(&xfull[s], VW_XRAW);
+                tma_load_3d(smem + L.xr_off + s * VW_XRAW, &tm_x, &xfull[s], 2 * (p0 - 6), r, 2 * b);
+                xit++;
+            };
+            uint32_t it = 0;
+            for (long w = i0; w < i1; w++, it++) {
+                const int o = int(w % Y), xc = int((w / Y) % nxc), b = int(w / (long(Y) * nxc));
+                const int p0 = xc * VW_PC;
+                if (w == i0 || o == 0)
+                    for (int r = o - VP; r < o + VP; r++)
+                        load_x(r, p0, b);
+                load_x(o + VP, p0, b);
+                const uint32_t s = it & 1, ph = (it >> 1) & 1;
+                mbar_wait(&dempty[s], ph ^ 1);
+                mbar_arrive_expect_tx(&dfull[s], L.dr_bytes);
+                tma_load_3d(smem + L.dr_off + s * L.dr_bytes, &tm_dy, &dfull[s], 2 * p0, o, F * b);
+            }
+        }
+    } else if (warp < 4) {
+        // ---- converters
+        const int t = threadIdx.x;
+        for (int e = t; e < VW_NB * (VW_PC / 4) * (32 - F) * 4; e += 128) { // unused f rows stay zero
+            const int per = (32 - F) * 4, sl = e / ((VW_PC / 4) * per), rem = e % ((VW_PC / 4) * per);
+            const int pq = rem / per, fi = rem % per;
+            reinterpret_cast<float*>(bring + sl * VW_BB)[(pq * 32 + F + fi / 4) * 4 + (fi & 3)] = 0.f;
+        }
+        uint32_t xit = 0;
+        auto stage_x = [&](int r) { // raw x row -> window slot r mod 16 (both copies)
+            const uint32_t s = xit % VW_NXR, ph = (xit / VW_NXR) & 1;
+            mbar_wait(&xfull[s], ph);
+            const float* raw = xr + s * (VW_XRAW / 4);
+            const int j = r & (VW_SL - 1);
+            for (int e = t; e < VW_PQ * 32; e += 128) {
+                const int pq = e >> 5, q = e & 31, ss = q >> 3, c = (q >> 2) & 1, i = q & 3;
+                const float v = to_tf32(raw[c * 160 + 2 * (1 + 4 * pq + ss + i)]);
+                xb[(pq * 2 * VW_SL + j) * 32 + q] = v;
+                xb[(pq * 2 * VW_SL + j + VW_SL) * 32 + q] = v;
+            }
+            mbar_arrive(&xempty[s]);
+            xit++;
+        };
+        uint32_t it = 0, seg_it = 0;
+        for (long w = i0; w < i1; w++, it++) {
+            const int o = int(w % Y);
+            if (w == i0 || o == 0) {
+                if (it > 0) // window slots of the previous column: every MMA issued so far done
+                    mbar_wait(&mdone[(it - 1) % VW_MD], ((it - 1) / VW_MD) & 1);
+                seg_it = it;
+                for (int r = o - VP; r < o + VP; r++)
+                    stage_x(r);
+            } else if (it >= seg_it + 6) {
+                // slot of row o + 5 last held row o - 11, read by dy rows up to o - 6
+                mbar_wait(&mdone[(it - 6) % VW_MD], ((it - 6) / VW_MD) & 1);
+            }
+            stage_x(o + VP);
+            const uint32_t ds = it & 1, dph = (it >> 1) & 1;
+            const uint32_t bs = it % VW_NB, bph = (it / VW_NB) & 1;
+            mbar_wait(&dfull[ds], dph);
+            mbar_wait(&bempty[bs], bph ^ 1);
+            const float* raw = dr + ds * (L.dr_bytes / 4);
+            float4* bo = reinterpret_cast<float4*>(bring + bs * VW_BB);
+            for (int e = t; e < (VW_PC / 4) * F; e += 128) {
+                const int pq = e / F, f = e - pq * F;
+                const float* src = raw + f * 2 * VW_PC + 8 * pq;
+                bo[pq * 32 + f] = make_float4(to_tf32(src[0]), to_tf32(src[2]), to_tf32(src[4]), to_tf32(src[6]));
+            }
+            mbar_arrive(&dempty[ds]);
+            fence_proxy_async_smem();
+            mbar_arrive(&bfull[bs]);
+        }
+    } else if (warp == 4) {
+        constexpr uint32_t idesc = idesc_tf32(128, 32);
+        const uint32_t xb_s = smem_u32(xb), b_s = smem_u32(bring);
+        uint32_t it = 0;
+        bool started = false;
+        for (long w = i0; w < i1; w++, it++) {
+            const int o = int(w % Y);
+            const uint32_t bs = it % VW_NB, bph = (it / VW_NB) & 1;
+            mbar_wait(&bfull[bs], bph);
+            tc_fence_after();
+            const int ws = (o - VP) & (VW_SL - 1);
+#pragma unroll
+            for (int g = 0; g < 3; g++)
+#pragma unroll
+                for (int ks = 0; ks < VW_PC / 8; ks++) {
+                    const uint64_t ad = umma_desc_kn(xb_s + ((2 * ks + g) * 2 * VW_SL + ws) * 128, 2 * VW_SL * 128, 128);
+                    const uint64_t bd = umma_desc_kn(b_s + bs * VW_BB + 2 * ks * 512, 512, 128);
+                    mma_tf32_warp(tmem_base + g * 32, ad, bd, idesc, (started || ks > 0) ? 1u : 0u);
+                }
+            started = true;
+            mma_commit_warp(&bempty[bs]);
+            mma_commit_warp(&mdone[it % VW_MD]);
+        }
+        mma_commit_warp(tfull);
+    } else if (warp >= 5) {
+        const int lq = warp & 3, m = lq * 32 + lane;
+        const int ky = m >> 3, s = (m >> 1) & 3, c = m & 1;
+        const bool any = i1 > i0;
+        if (any) {
+            mbar_wait(tfull, 0);
+            tc_fence_after();
+        }
+        const long n = 121L * 2 * F;
+        float2* dst = part + size_t(blockIdx.x) * n;
+        for (int g = 0; g < 3; g++) {
+            float v[32];
+            if (any) {
+                tmem_ld32(tmem_base + (uint32_t(lq * 32) << 16) + g * 32, v);
+                tmem_ld_wait();
+            }
+            const int kx = 4 * g + s;
+            if (kx < VK && ky < VK)
+#pragma unroll
+                for (int f = 0; f < 32; f++)
+                    if (f < F)
+                        dst[kx + VK * (ky + VK * (c + 2 * f))] = float2{any ? v[f] : 0.f, 0.f};
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc<128>(tmem_base);
+    }
+}
+
+// dw[i] = sum_s part[s][i] (fixed order, double accumulation: deterministic)
+__global__ void __launch_bounds__(256) k_vn_fold(float2* __restrict__ dw, const float2* __restrict__ part, long n,
+                                                 int nsplit, const unsigned* __restrict__ imag)
+{
+    if (*imag)
+        return;
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+        double a = 0;
+        for (int s = 0; s < nsplit; s++)
+            a += part[size_t(s) * n + i].x;
+        dw[i] = float2{float(a), 0.f};
+    }
+}
+
 bool g_vn_tc = true;
 
 PFN_cuTensorMapEncodeTiled_v12000 vn_encode()
@@ -531,6 +766,29 @@ bool conv_vn_tc_supported(const ConvGeom& g)
 {
     return g_vn_tc && g.KX == VK && g.KY == VK && g.Cin == 2 && g.Cout >= 1 && g.Cout <= 24 && !g.in_chlast
            && !g.out_chlast && !(g.X & 1) && g.X * g.Y * g.B * g.Cout < (1L << 31);
+}
+
+void conv_vn_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g, const unsigned* imag)
+{
+    auto& c = ctx();
+    const int F = int(g.Cout), X = int(g.X), Y = int(g.Y), B = int(g.B);
+    const VwSmem L(F);
+    const long items = long((X + VW_PC - 1) / VW_PC) * Y * B;
+    const int grid = int(std::min<long>(items, c.sm_count));
+    const long n = 121L * 2 * F;
+    CUDA_CHECK(cudaFuncSetAttribute(k_vn_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
+    const CUtensorMap tx = vn_map(x, X, Y, 2L * B, 160, 2);
+    const CUtensorMap td = vn_map(dy, X, Y, long(F) * B, 2 * VW_PC, F);
+    float2* part;
+    CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * grid, c.stream));
+    {
+        ProfScope prof("conv_vn_bwd_weight", vn_flops(g));
+        k_vn_wgrad<<<grid, V_THREADS, L.total, c.stream>>>(tx, td, part, X, Y, B, F, imag);
+        KERNEL_CHECK();
+    }
+    k_vn_fold<<<int((n + 255) / 256), 256, 0, c.stream>>>(dw, part, n, grid, imag);
+    KERNEL_CHECK();
+    CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
 
 void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode, const unsigned* imag)

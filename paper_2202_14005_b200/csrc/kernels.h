@@ -138,6 +138,8 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
 // the caller's CUDA-core complex kernel of the same pair does the work)
 bool conv_vn_tc_supported(const ConvGeom& g);
 void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGeom& g, int mode, const unsigned* imag);
+// weight gradient dw[t, c, f] = sum_p dy[p, f] x[p + t - 5, c] (the imag flag covers x and dy)
+void conv_vn_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGeom& g, const unsigned* imag);
 void conv_vn_tc_enable(bool on);
 // tcgen05 TF32 implicit-GEMM path (conv_tc.cu) for 3x3 layers with 32/64 channels
 void conv_tc_enable(bool on);

@@ -332,7 +332,8 @@ def test_vn_tensor_core_vs_fp32_kernels(gpu, ref, X, Y, B, F):
     """The tensor-core 11 x 11 kernels against the fp32 CUDA-core kernels and the
     reference at the C3 geometry (640 x 368: three 256-pixel expand tiles, the
     last one partial, six overlapping 118-pixel reduce tiles, 74 / 37 row
-    chunks) and ragged shapes (partial tiles and chunks in x and y)."""
+    chunks, 64-pixel weight-gradient columns) and ragged shapes (partial tiles
+    and chunks in x and y): forward, bwd-data and bwd-weight."""
     rng = np.random.default_rng(X + Y + F)
     in_dims = list(d16(X, Y, 2))
     in_dims[15] = B
@@ -345,11 +346,13 @@ def test_vn_tensor_core_vs_fp32_kernels(gpu, ref, X, Y, B, F):
         try:
             n = Model.conv_layer(gpu, "c", in_dims, (11, 11), F, transposed=False, bias=False).nlop
             y = n.apply(ins)[0]
-            res.append((y, n.adjoint_all(0, dy)[0]))
+            res.append((y, *n.adjoint_all(0, dy)))
         finally:
             gpu.check(gpu.so.mdnn_set_option(b"conv_vn_tc", 1))
     nr = mr.nlop
     yr = nr.apply(ins)[0]
-    dxr = nr.adjoint_all(0, dy)[0]
-    assert rel_l2(res[0][0], yr) <= CONV_TOL and rel_l2(res[0][1], dxr) <= CONV_TOL
-    assert rel_l2(res[1][0], yr) <= 1e-5 and rel_l2(res[1][1], dxr) <= 1e-5
+    dxr, dwr = nr.adjoint_all(0, dy)
+    for got, want in zip(res[0], (yr, dxr, dwr)):  # forward, bwd-data, bwd-weight on the tensor cores
+        assert rel_l2(got, want) <= CONV_TOL
+    for got, want in zip(res[1], (yr, dxr, dwr)):  # fp32 CUDA-core kernels
+        assert rel_l2(got, want) <= 1e-5
