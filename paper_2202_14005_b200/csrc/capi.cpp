@@ -74,6 +74,22 @@ HostView hv(const mdnn_array& a)
 }
 
 DArray in_arr(const mdnn_array& a) { return import_array(hv(a)); }
+// inputs of calls that do not keep them: dense device arrays are used in place
+DArray in_view(const mdnn_array& a) { return borrow_array(hv(a)); }
+// output buffer: the caller's dense device array in place, else a fresh array
+// copied out by out_arr
+DArray out_target(mdnn_array& a, const Dims& d)
+{
+    const HostView v = hv(a);
+    if (v.device == ctx().device && v.dims == d && (v.strides.empty() || v.strides == default_strides(d)))
+        return borrow_array(v);
+    return DArray(d, false);
+}
+void out_arr_if_needed(const DArray& d, mdnn_array& a)
+{
+    if (d.buf->owned)
+        export_array(d, hv(a));
+}
 void out_arr(const DArray& d, mdnn_array& a) { export_array(d, hv(a)); }
 
 mdnn_nlop* wrap(Nlop op) { return new mdnn_nlop{std::move(op)}; }
@@ -429,15 +445,17 @@ int mdnn_sense_normal(const mdnn_array* coils, const mdnn_array* pattern, float 
                       mdnn_array* y)
 {
     return guard([&] {
-        DArray C = in_arr(*coils), P = in_arr(*pattern), X = in_arr(*x);
+        DArray C = in_view(*coils), P = in_view(*pattern), X = in_view(*x);
         check_binary(P);
         SenseGeom g = geom_from(C, P);
         if (X.dims != img_dims(g))
             throw ShapeError("linop normal: expected " + dims_to_string(img_dims(g)));
         DArray lam = DArray::scalar(lambda);
-        DArray out(img_dims(g), false);
+        DArray out = out_target(*y, img_dims(g));
+        if (out.data() == X.data())
+            out = DArray(img_dims(g), false); // in-place call: keep x intact until the kernel is done
         sense_normal(out.data(), X.data(), C.data(), P.data(), lam.data(), g);
-        out_arr(out, *y);
+        out_arr_if_needed(out, *y);
         sync_and_check();
     });
 }
@@ -448,7 +466,7 @@ int mdnn_cg_normal_solve(const mdnn_array* coils, const mdnn_array* pattern, flo
     return guard([&] {
         if (lambda < 0)
             throw ConfigError("cg_normal_solve: lambda must be nonnegative");
-        DArray C = in_arr(*coils), P = in_arr(*pattern), B = in_arr(*b);
+        DArray C = in_view(*coils), P = in_view(*pattern), B = in_view(*b);
         check_binary(P);
         SenseGeom g = geom_from(C, P);
         if (B.dims != img_dims(g))

@@ -289,6 +289,21 @@ DArray import_array(const HostView& v)
     return a;
 }
 
+DArray borrow_array(const HostView& v)
+{
+    if (v.device != ctx().device || !is_default(v.dims, v.strides))
+        return import_array(v);
+    check_rank(v.dims);
+    DArray a;
+    a.dims = v.dims;
+    a.buf = std::make_shared<Buffer>();
+    a.buf->ptr = const_cast<float*>(v.data);
+    a.buf->bytes = size_t(md_size(v.dims)) * sizeof(cfloat);
+    a.buf->device = v.device;
+    a.buf->owned = false;
+    return a;
+}
+
 DArray import_array_async(const HostView& v, cudaEvent_t done)
 {
     if (v.device >= 0 || !is_default(v.dims, v.strides))

@@ -162,6 +162,9 @@ struct HostView {
     Dims strides; // element strides
 };
 DArray import_array(const HostView& v);
+// a dense device array on the current device is borrowed (no copy, not freed):
+// for calls that do not retain their inputs past the call (standalone SENSE / CG)
+DArray borrow_array(const HostView& v);
 // asynchronous host->device copy on the context's copy stream into a fresh
 // array; `done` is recorded on the copy stream after the copy (the caller
 // makes the compute stream wait on it and keeps the host buffer alive until
