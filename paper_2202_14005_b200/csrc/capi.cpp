@@ -126,11 +126,10 @@ SenseGeom geom_from(const DArray& coils, const DArray& pattern)
 
 void check_binary(const DArray& pattern)
 {
-    // recon.hpp:67-77
-    auto h = to_host(pattern);
-    for (auto& v : h)
-        if (v.imag() != 0 || (v.real() != 0 && v.real() != 1))
-            throw ConfigError("sense: sampling pattern must be binary");
+    // recon.hpp:67-77, evaluated on the device (no host round trip per call): a
+    // non-binary pattern sets ERRF_PATTERN, which the call's closing
+    // sync_and_check() raises as the reference's ConfigError
+    launch_check_binary(pattern.data(), pattern.size());
 }
 
 Dims img_dims(const SenseGeom& g)
@@ -178,6 +177,8 @@ int mdnn_set_option(const char* key, long value)
             conv_tc_enable(value != 0);
         else if (k == "sense_rank")
             sense_rank_enable(value != 0);
+        else if (k == "sense_ws")
+            sense_ws_enable(value != 0);
         else if (k == "sense_rank_ctas")
             sense_rank_ctas(value);
         else if (k == "cg_defer_x")

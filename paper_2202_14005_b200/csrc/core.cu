@@ -156,6 +156,8 @@ void sync_and_check()
     CUDA_CHECK(cudaMemcpy(&flags, c.d_errflags, sizeof(unsigned), cudaMemcpyDeviceToHost));
     if (flags) {
         CUDA_CHECK(cudaMemset(c.d_errflags, 0, sizeof(unsigned)));
+        if (flags & ERRF_PATTERN) // raised before any result is used, as the reference's check (recon.hpp:67-77)
+            throw ConfigError("sense: sampling pattern must be binary");
         if (flags & ERRF_CG_BREAKDOWN)
             throw SolverError("cg: numerical breakdown (p^H A p <= 0 or non-finite)");
         if (flags & ERRF_CG_NONFINITE)

@@ -349,6 +349,17 @@ __global__ void k_check_finite(const float* a, long n, unsigned* flags)
         atomicOr(flags, unsigned(ERRF_NONFINITE_GRAD));
 }
 
+__global__ void k_check_binary(const cfloat* a, long n, unsigned* flags)
+{
+    bool bad = false;
+    for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
+        const cfloat v = a[i];
+        bad |= v.y != 0.f || (v.x != 0.f && v.x != 1.f);
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0)
+        atomicOr(flags, unsigned(ERRF_PATTERN));
+}
+
 __global__ void k_split(cfloat* out, const cfloat* in, long inner, long outer)
 {
     long n = inner * outer;
@@ -608,6 +619,12 @@ void launch_check_finite(const cfloat* a, long n)
 {
     k_check_finite<<<grid_for(2 * n), kThreads, 0, ctx().stream>>>(reinterpret_cast<const float*>(a), 2 * n,
                                                                    ctx().d_errflags);
+    KERNEL_CHECK();
+}
+
+void launch_check_binary(const cfloat* a, long n)
+{
+    k_check_binary<<<int(std::min<long>(grid_for(n), 64)), kThreads, 0, ctx().stream>>>(a, n, ctx().d_errflags);
     KERNEL_CHECK();
 }
 

@@ -152,6 +152,7 @@ bool conv_bn_fuse();
 // persistent mask-pruned A^H A kernel (sense_rank.cuh); off = sense_fast.cuh path
 void sense_rank_enable(bool on);
 void sense_rank_ctas(long g);
+void sense_ws_enable(bool on);
 void cg_defer_x_enable(bool on);
 bool rank_enabled();
 // test hook: auto-layout convs store multi-channel activations channels-last
@@ -251,6 +252,7 @@ void adam_update(cfloat* theta, cfloat* m, float* v, const cfloat* g, long n, fl
 // flat gradient gather/scatter
 void launch_copy(cfloat* dst, const cfloat* src, long n);
 void launch_check_finite(const cfloat* a, long n); // sets ERRF_NONFINITE_GRAD
+void launch_check_binary(const cfloat* a, long n); // sets ERRF_PATTERN unless every value is 0 or 1
 // sgd_step with the clip scale, realify and NonNegProx folded in
 void sgd_update(cfloat* theta, const cfloat* g, long n, float lr, float gscale, bool real_weights, bool nonneg_prox);
 // NonNegProx (nn.hpp:57-64): v = (max(Re v, 0), 0)

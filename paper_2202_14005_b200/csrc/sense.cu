@@ -391,6 +391,7 @@ namespace mdnn {
 namespace {
 #include "sense_fast.cuh"
 #include "sense_rank.cuh"
+#include "sense_ws.cuh"
 
 bool fast_ok(const SenseGeom& g, const cfloat* coils, const cfloat* coils2)
 {
@@ -885,6 +886,7 @@ bool g_rank_enabled = true;
 // rank-kernel CTA count override lives in sense_rank.cuh (g_rank_ctas)
 void sense_rank_enable(bool on) { g_rank_enabled = on; }
 void sense_rank_ctas(long g) { g_rank_ctas = g; }
+void sense_ws_enable(bool on) { g_sense_ws = on; }
 void cg_defer_x_enable(bool on) { g_cg_defer_x = on; }
 bool rank_enabled() { return g_rank_enabled; }
 

@@ -28,6 +28,7 @@
 
 bool g_cg_defer_x = true; // CG: keep every p, update r only per iteration, sum x once
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
+bool g_sense_ws = true; // warp-specialised kernel (sense_ws.cuh), one CTA per SM
 
 constexpr int rank_nbox(int Y)
 {
@@ -765,6 +766,7 @@ struct RankPlan {
     long nxb = 0, strips = 0, units = 0;
     int G = 0;
     int planes = 1; // max CTAs sharing a strip (Ap planes)
+    bool ws = false; // warp-specialised kernel (sense_ws.cuh)
     bool ok = false;
 };
 
@@ -798,6 +800,9 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
     case 512: minb = RankCfg<16, 32>::MINB; break;
     case 640: minb = RankCfg<16, 40>::MINB; break;
     }
+    r.ws = g_sense_ws && r.W == 8; // W = 4 strips (N2 > 24) measured faster on k_normal_rank
+    if (r.ws)
+        minb = 1;
     r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : long(minb) * ctx().sm_count, r.units));
     r.planes = 1;
     for (long s = 0; s < r.strips; s++)
@@ -885,12 +890,20 @@ void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsign
 #undef X_
 }
 
+template<int N1, int N2>
+void launch_ws_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const unsigned char* plans);
+
 void launch_rank(const RankPlan& rp, RankArgs a, const cfloat* coils, const SenseGeom& g,
                  const unsigned char* plans)
 {
     fill_rank_args(rp, a, g);
 #define X_(YY, A1, A2) \
-    case YY: launch_rank_t<A1, A2>(a, coils, g, plans); return;
+    case YY:                                     \
+        if (rp.ws)                               \
+            launch_ws_t<A1, A2>(a, coils, g, plans); \
+        else                                     \
+            launch_rank_t<A1, A2>(a, coils, g, plans); \
+        return;
     switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }
 #undef X_
 }

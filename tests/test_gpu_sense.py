@@ -9,15 +9,12 @@ import ctypes as C
 import numpy as np
 import pytest
 
+from paper_2202_14005_b200.capi import MdnnError
 from paper_2202_14005_b200.mdnn import Model, Nlop, sense_dims
 from util import (coil_dims, crand, d16, image_dims, kspace_dims, pattern_dims, rel_l2, sim_data)
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-5
-
-
-def _call(lib, fn, *arrays_out, **kw):
-    pass
 
 
 @pytest.mark.parametrize("dims,flags", [
@@ -164,3 +161,38 @@ def test_sense_normal_y_only_at_target_shape(gpu, ref):
     g = _sense_call(gpu, "mdnn_sense_normal", cm, pat, ph, image_dims(X, Y), 0.05)
     r = _sense_call(ref, "mdnn_sense_normal", cm, pat, ph, image_dims(X, Y), 0.05)
     assert rel_l2(g, r) <= TOL
+
+
+@pytest.mark.parametrize("entry", ["normal", "cg", "forward"])
+def test_nonbinary_pattern_is_a_config_error(gpu, ref, entry):
+    """recon.hpp:67-77: a sampling pattern with a value other than 0 or 1 is a
+    ConfigError (code 4) with the reference's message, on every standalone SENSE
+    entry point (the product checks it on the device and raises at the call's
+    closing synchronisation); the library stays usable afterwards."""
+    X, Y, NC = 16, 12, 3
+    ph, cm, pat = sim_data(ref, X, Y, NC, 1)
+    bad = pat.copy(order="F")
+    bad.reshape(-1, order="F")[3] = 0.5
+    for lib in (gpu, ref):
+        for p, ok in ((bad, False), (pat, True)):
+            if entry == "normal":
+                out = np.zeros(image_dims(X, Y), dtype=np.complex64, order="F")
+                call = lambda: lib.so.mdnn_sense_normal(C.byref(lib.arr(cm)), C.byref(lib.arr(p)), C.c_float(0.1),  # noqa: E731
+                                                        C.byref(lib.arr(ph)), C.byref(lib.arr(out)))
+            elif entry == "cg":
+                out = np.zeros(image_dims(X, Y), dtype=np.complex64, order="F")
+                it, rr = C.c_long(), C.c_double()
+                call = lambda: lib.so.mdnn_cg_normal_solve(C.byref(lib.arr(cm)), C.byref(lib.arr(p)),  # noqa: E731
+                                                           C.c_float(0.1), C.byref(lib.arr(ph)), 3, C.c_double(0.0),
+                                                           C.byref(lib.arr(out)), C.byref(it), C.byref(rr))
+            else:
+                out = np.zeros(kspace_dims(X, Y, NC), dtype=np.complex64, order="F")
+                call = lambda: lib.so.mdnn_sense_forward(C.byref(lib.arr(cm)), C.byref(lib.arr(p)),  # noqa: E731
+                                                         C.byref(lib.arr(ph)), C.byref(lib.arr(out)))
+            if ok:
+                lib.check(call())
+            else:
+                with pytest.raises(MdnnError) as e:
+                    lib.check(call())
+                assert e.value.code == 4
+                assert "binary" in str(e.value)

@@ -45,7 +45,9 @@ def main(path, kre=None, n=40):
     tot = sum(r[0] for r in recs) or 1
     toti = sum(r[1] for r in recs) or 1
     print(f"total samples {tot}, warp-instructions {toti}")
-    for s, ins, f, ln, src, top in sorted(recs, key=lambda r: -r[0])[:int(n)]:
+    import os
+    key = (lambda r: -r[1]) if os.environ.get("SORT") == "ins" else (lambda r: -r[0])
+    for s, ins, f, ln, src, top in sorted(recs, key=key)[:int(n)]:
         print(f"{100*s/tot:5.1f}% {100*ins/toti:5.1f}%i {f}:{ln:5s} {src:70s} {top}")
 
 
