@@ -24,6 +24,7 @@
 //    stash in shared memory.
 #pragma once
 
+#include <algorithm>
 #include <utility>
 
 namespace cx2 {
@@ -199,12 +200,17 @@ struct WsCfg {
     static constexpr int TMAX = RC::TMAX;
     static constexpr int NBOX = RC::NBOX, BOXR = RC::BOXR;
     static constexpr int NT_AC = ((W * N2 + 31) / 32) * 32;  // A/C threads (w, j)
-    static constexpr int NT_B = ((N1 * W + 31) / 32) * 32;   // stage-B threads (row, column)
+    static constexpr int JH = N2P / 2;                        // j per stage-B half row
+    // stage-B threads (row, column, half row); 6 warps cover the 12 ACL rows of
+    // the reference pattern family in one pass, more rows loop
+    static constexpr int NT_B = std::min(((2 * N1 * W + 31) / 32) * 32, 192);
     static constexpr int NT = NT_AC + NT_B + 32;             // + TMA producer warp
     static constexpr int SLOT = Y * W;                        // float2 per coil slice / stash
-    // S row pitch (float2): = 8 (mod 16), so the 4 rows x 8 columns of a stage-B
-    // warp load split over both halves of the banks
-    static constexpr int RP = (N2P * W) % 16 == 8 ? N2P * W : ((N2P * W + 15) / 16) * 16 + 8;
+    // S layout: element (row m, j, column w) at m * RP + SOFF(j) + w, with the
+    // second half row (j >= JH) shifted by 8 float2, so the two halves of a
+    // stage-B thread pair fall in opposite halves of the banks (conflict-free)
+    static constexpr int RP = N2P * W + 8;
+    __host__ __device__ static constexpr int SOFF(int j) { return j * W + (j >= JH ? 8 : 0); }
     static constexpr int SBUF = N1 * RP;
     static constexpr size_t STATIC_EST = 4096;                // plan, barriers, reductions
     // 2 S buffers, stash, 2 staging strips (x or r, and p_prev), twiddle rows
@@ -384,56 +390,67 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
             }
             WS_WAIT(1, &bar_sfull[i & 1], uint32_t((i >> 1) & 1));
             float2* S = Sb + (i & 1) * SBUF;
-            const int nitems = pl.nwork * W;
+            const int nitems = 2 * pl.nwork * W;
             for (int item = bt; item < nitems; item += NT_B) {
-                const int r = item / W, ww = item - r * W;
+                // thread pair (h = 0, 1) per (row, column): each half row in registers,
+                // dot products combined with one shuffle
+                const int h = item & 1, pr = item >> 1;
+                const int r = pr / W, ww = pr - r * W;
                 const int k1 = pl.work_k1[r];
                 const int md = pl.mode[k1], nt = pl.nt[k1], off = pl.off[k1];
-                float2* row = S + k1 * RP + ww;
-                float2 u[N2];
+                const int jb = h * Cfg::JH;
+                float2* row = S + k1 * RP + (h ? Cfg::JH * W + 8 : 0) + ww; // element jb + jj at row[jj * W]
+                const unsigned pmask = 3u << ((tid & 31) & ~1);
+                constexpr int NJ = Cfg::JH;
+                float2 u[NJ];
 #pragma unroll
-                for (int jj = 0; jj < N2; jj++)
-                    u[jj] = row[jj * W];
+                for (int jj = 0; jj < NJ; jj++)
+                    u[jj] = (jb + jj < N2) ? row[jj * W] : float2{0.f, 0.f};
                 if (nt <= 2 && off + nt <= TMAX) {
                     auto fast = [&](auto TWO) {
                         constexpr bool two = decltype(TWO)::value;
-                        const float4* t0v = reinterpret_cast<const float4*>(ttw + off * N2P); // 16-B aligned (N2P even)
-                        const float4* t1v = reinterpret_cast<const float4*>(ttw + (two ? off + 1 : off) * N2P);
+                        // 16-B aligned: N2P and JH even; pad twiddles (j >= N2) are zero
+                        const float4* t0v = reinterpret_cast<const float4*>(ttw + off * N2P + jb);
+                        const float4* t1v = reinterpret_cast<const float4*>(ttw + (two ? off + 1 : off) * N2P + jb);
                         float2 d0a{0.f, 0.f}, d0b{0.f, 0.f}, d1a{0.f, 0.f}, d1b{0.f, 0.f};
 #pragma unroll
-                        for (int jj = 0; jj < N2; jj += 2) {
+                        for (int jj = 0; jj < NJ; jj += 2) {
                             const float4 q0 = t0v[jj >> 1];
                             d0a = cx2::mac(d0a, u[jj], float2{q0.x, q0.y});
-                            if (jj + 1 < N2)
-                                d0b = cx2::mac(d0b, u[jj + 1], float2{q0.z, q0.w});
+                            d0b = cx2::mac(d0b, u[jj + 1], float2{q0.z, q0.w});
                             if constexpr (two) {
                                 const float4 q1 = t1v[jj >> 1];
                                 d1a = cx2::mac(d1a, u[jj], float2{q1.x, q1.y});
-                                if (jj + 1 < N2)
-                                    d1b = cx2::mac(d1b, u[jj + 1], float2{q1.z, q1.w});
+                                d1b = cx2::mac(d1b, u[jj + 1], float2{q1.z, q1.w});
                             }
                         }
-                        float2 d0 = nt > 0 ? cx2::mul(cx2::add(d0a, d0b), pl.coef[off]) : float2{0.f, 0.f};
+                        float2 d0 = cx2::add(d0a, d0b);
+                        d0.x += __shfl_xor_sync(pmask, d0.x, 1);
+                        d0.y += __shfl_xor_sync(pmask, d0.y, 1);
+                        d0 = nt > 0 ? cx2::mul(d0, pl.coef[off]) : float2{0.f, 0.f};
                         const float2 e0{d0.y, -d0.x};
                         float2 d1{0.f, 0.f}, e1{0.f, 0.f};
                         if constexpr (two) {
-                            d1 = cx2::mul(cx2::add(d1a, d1b), pl.coef[off + 1]);
+                            d1 = cx2::add(d1a, d1b);
+                            d1.x += __shfl_xor_sync(pmask, d1.x, 1);
+                            d1.y += __shfl_xor_sync(pmask, d1.y, 1);
+                            d1 = cx2::mul(d1, pl.coef[off + 1]);
                             e1 = float2{d1.y, -d1.x};
                         }
 #pragma unroll
-                        for (int jj = 0; jj < N2; jj += 2) {
+                        for (int jj = 0; jj < NJ; jj += 2) {
                             const float4 q0 = t0v[jj >> 1];
                             float4 q1;
                             if constexpr (two)
                                 q1 = t1v[jj >> 1];
 #pragma unroll
-                            for (int h = 0; h < 2; h++) {
-                                if (jj + h < N2) {
-                                    float2 r0 = md == 1 ? u[jj + h] : float2{0.f, 0.f};
-                                    r0 = cx2::mac_dconj(r0, d0, e0, h ? float2{q0.z, q0.w} : float2{q0.x, q0.y});
+                            for (int hh = 0; hh < 2; hh++) {
+                                if (jb + jj + hh < N2) {
+                                    float2 r0 = md == 1 ? u[jj + hh] : float2{0.f, 0.f};
+                                    r0 = cx2::mac_dconj(r0, d0, e0, hh ? float2{q0.z, q0.w} : float2{q0.x, q0.y});
                                     if constexpr (two)
-                                        r0 = cx2::mac_dconj(r0, d1, e1, h ? float2{q1.z, q1.w} : float2{q1.x, q1.y});
-                                    row[(jj + h) * W] = r0;
+                                        r0 = cx2::mac_dconj(r0, d1, e1, hh ? float2{q1.z, q1.w} : float2{q1.x, q1.y});
+                                    row[(jj + hh) * W] = r0;
                                 }
                             }
                         }
@@ -444,20 +461,21 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                         fast(std::false_type{});
                 } else {
                     // general rows: any number of terms, twiddles indexed on the fly;
-                    // the row in shared memory is the running result (u stays in
-                    // registers for the dot products)
+                    // the half row in shared memory is the running result
                     if (md != 1) {
 #pragma unroll
-                        for (int jj = 0; jj < N2; jj++)
-                            row[jj * W] = float2{0.f, 0.f};
+                        for (int jj = 0; jj < NJ; jj++)
+                            if (jb + jj < N2)
+                                row[jj * W] = float2{0.f, 0.f};
                     }
                     for (int t = off; t < off + nt; t++) {
                         const int k = pl.tk[t];
-                        int m0 = 0;
+                        const int m00 = (jb * k) % Y;
+                        int m0 = m00;
                         float2 da{0.f, 0.f}, db{0.f, 0.f};
 #pragma unroll
-                        for (int jj = 0; jj < N2; jj++) {
-                            const float2 tv = __ldg(&a.tw[m0]);
+                        for (int jj = 0; jj < NJ; jj++) {
+                            const float2 tv = (jb + jj < N2) ? __ldg(&a.tw[m0]) : float2{0.f, 0.f};
                             if (jj & 1)
                                 db = cx2::mac(db, u[jj], tv);
                             else
@@ -465,12 +483,16 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                             m0 += k;
                             m0 -= m0 >= Y ? Y : 0;
                         }
-                        const float2 d = cx2::mul(cx2::add(da, db), pl.coef[t]);
+                        float2 d = cx2::add(da, db);
+                        d.x += __shfl_xor_sync(pmask, d.x, 1);
+                        d.y += __shfl_xor_sync(pmask, d.y, 1);
+                        d = cx2::mul(d, pl.coef[t]);
                         const float2 e{d.y, -d.x};
-                        m0 = 0;
+                        m0 = m00;
 #pragma unroll
-                        for (int jj = 0; jj < N2; jj++) {
-                            row[jj * W] = cx2::mac_dconj(row[jj * W], d, e, __ldg(&a.tw[m0]));
+                        for (int jj = 0; jj < NJ; jj++) {
+                            if (jb + jj < N2)
+                                row[jj * W] = cx2::mac_dconj(row[jj * W], d, e, __ldg(&a.tw[m0]));
                             m0 += k;
                             m0 -= m0 >= Y ? Y : 0;
                         }
@@ -576,7 +598,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                 v[q] = cx2::mul(csp[N2 * W * q], xr[q]);
             cx2::dft<N1, -1>(v);
             if (active) {
-                float2* S = Sb + (i & 1) * SBUF + j * W + w;
+                float2* S = Sb + (i & 1) * SBUF + Cfg::SOFF(j) + w;
 #pragma unroll
                 for (int m = 0; m < N1; m++)
                     S[m * RP] = v[m];
@@ -592,7 +614,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
 #ifdef WS_PROF
             long long t0 = clock64();
 #endif
-            const float2* S = Sb + (i & 1) * SBUF + j * W + w;
+            const float2* S = Sb + (i & 1) * SBUF + Cfg::SOFF(j) + w;
             const int slot = i % NSLOT;
             const float2* csp = ring + size_t(slot) * SLOT + j * W + w;
             float2 v[N1], cv[N1];
