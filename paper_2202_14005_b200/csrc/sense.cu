@@ -600,7 +600,7 @@ void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloa
             unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
             launch_rank_plan(rp, a, g, pl);
             launch_rank(rp, a, coils, g, pl);
-            k_rank_merge<<<grid_for(n), 256, 0, ctx().stream>>>(out, plane1.data(), rank_split_flags(g, pl),
+            k_rank_merge<<<grid_for(n), 256, 0, ctx().stream>>>(out, plane1.data(), rank_split_flags(g, rp, pl),
                                                                 int(g.X), int(g.Y * g.B), int(g.Y), int(rp.nxb),
                                                                 rp.W == 8 ? 3 : 2, n);
             KERNEL_CHECK();
@@ -788,13 +788,13 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             if (defer) {
                 ProfScope prof("cg_update_rank", 8.0 * n * 4);
                 k_cg_update_r<UR><<<n_updr, 256, 0, c.stream>>>(m.st, it, r.data(), ap.data(), ap.data() + n,
-                                                               rank_split_flags(g, pl), int(g.X), int(g.Y * g.B),
+                                                               rank_split_flags(g, rp, pl), int(g.X), int(g.Y * g.B),
                                                                int(g.Y), int(rp.nxb), rp.W == 8 ? 3 : 2, n,
                                                                c.d_errflags);
             } else {
                 ProfScope prof("cg_update_rank", 8.0 * n * 7);
                 k_cg_update_rank<<<n_updr, 512, 0, c.stream>>>(m.st, it, x, r.data(), pdir(it + 1), ap.data(),
-                                                              ap.data() + n, rank_split_flags(g, pl), int(g.X),
+                                                              ap.data() + n, rank_split_flags(g, rp, pl), int(g.X),
                                                               int(g.Y * g.B), int(g.Y), int(rp.nxb),
                                                               rp.W == 8 ? 3 : 2, n, c.d_errflags);
             }

@@ -59,7 +59,6 @@ struct RankCfg {
     static constexpr int MINB = 4 * (SMEM + 4096) <= 228 * 1024 ? 4 : 3 * (SMEM + 4096) <= 228 * 1024 ? 3
                               : 2 * (SMEM + 4096) <= 228 * 1024 ? 2 : 1;
     static_assert(Y % NBOX == 0, "TMA box rows must tile Y");
-    static_assert(JH % 2 == 0, "stage-B half rows are read as float4 pairs");
 };
 
 struct RankArgs {
@@ -200,6 +199,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
     using namespace fftd;
     using Cfg = RankCfg<N1, N2>;
     constexpr int Y = Cfg::Y, W = Cfg::W, JH = Cfg::JH, TMAX = Cfg::TMAX, N2P = Cfg::N2P;
+    static_assert(JH % 2 == 0, "stage-B half rows are read as float4 pairs");
     constexpr int NT = Cfg::NT; // threads of this CTA
     constexpr int NQ = N1;      // q points per thread
     extern __shared__ __align__(128) float2 rank_smem[];
@@ -800,7 +800,11 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
     case 512: minb = RankCfg<16, 32>::MINB; break;
     case 640: minb = RankCfg<16, 40>::MINB; break;
     }
-    r.ws = g_sense_ws && r.W == 8; // W = 4 strips (N2 > 24) measured faster on k_normal_rank
+    // warp-specialised kernel for the W = 8 shapes (N2 <= 24); Y = 512 / 640 keep
+    // k_normal_rank (their ws buffers do not fit shared memory).  N1 = 8 with
+    // twice the A/C warps was measured slower at Y = 368 (71.9 vs 63 us per CG
+    // launch): stage B then carries ~3.3 terms per row over 46-point rows.
+    r.ws = g_sense_ws && r.W == 8;
     if (r.ws)
         minb = 1;
     r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : long(minb) * ctx().sm_count, r.units));
@@ -849,21 +853,26 @@ void launch_rank_plan_t(const RankArgs& a, unsigned char* plans, int nitems)
 }
 
 #define RANK_SHAPES(X_) X_(128, 8, 16) X_(256, 16, 16) X_(320, 16, 20) X_(368, 16, 23) X_(512, 16, 32) X_(640, 16, 40)
+// (N1, N2) of every plan record layout: the k_normal_rank shapes and the ws shapes
+#define PLAN_SHAPES(X_) RANK_SHAPES(X_)
+#define WS_SHAPES(X_) X_(368, 16, 23) X_(320, 16, 20) X_(256, 16, 16) X_(128, 8, 16)
 
 // device memory for the per-item plans of a pattern
-size_t rank_plan_record_bytes(const SenseGeom& g)
+size_t rank_plan_record_bytes(const SenseGeom& g, const RankPlan& rp)
 {
     const long items = g.pat_b > 1 ? g.pat_b : 1;
 #define X_(YY, A1, A2) \
-    case YY: return RankPlanRec<A1, A2>::BYTES * items;
-    switch (g.Y) { RANK_SHAPES(X_) default: return 0; }
+    if (rp.N1 == A1 && rp.N2 == A2) \
+        return RankPlanRec<A1, A2>::BYTES * items;
+    PLAN_SHAPES(X_)
 #undef X_
+    return 0;
 }
 // [per-item plan records | split flag per strip]
-size_t rank_plan_bytes(const SenseGeom& g, const RankPlan& rp) { return rank_plan_record_bytes(g) + size_t(rp.strips); }
-const unsigned char* rank_split_flags(const SenseGeom& g, const unsigned char* plans)
+size_t rank_plan_bytes(const SenseGeom& g, const RankPlan& rp) { return rank_plan_record_bytes(g, rp) + size_t(rp.strips); }
+const unsigned char* rank_split_flags(const SenseGeom& g, const RankPlan& rp, const unsigned char* plans)
 {
-    return plans + rank_plan_record_bytes(g);
+    return plans + rank_plan_record_bytes(g, rp);
 }
 
 void fill_rank_args(const RankPlan& rp, RankArgs& a, const SenseGeom& g)
@@ -882,12 +891,16 @@ void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsign
     fill_rank_args(rp, a, g);
     const int items = int(g.pat_b > 1 ? g.pat_b : 1);
     k_rank_split_flags<<<int(std::min<long>((rp.strips + 255) / 256, 64)), 256, 0, ctx().stream>>>(
-        plans + rank_plan_record_bytes(g), rp.strips, g.C, rp.units, rp.G);
+        plans + rank_plan_record_bytes(g, rp), rp.strips, g.C, rp.units, rp.G);
     KERNEL_CHECK();
-#define X_(YY, A1, A2) \
-    case YY: launch_rank_plan_t<A1, A2>(a, plans, items); return;
-    switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }
+#define X_(YY, A1, A2)                                \
+    if (rp.N1 == A1 && rp.N2 == A2) {                 \
+        launch_rank_plan_t<A1, A2>(a, plans, items); \
+        return;                                       \
+    }
+    PLAN_SHAPES(X_)
 #undef X_
+    throw Error("rank A^H A: unsupported factorisation");
 }
 
 template<int N1, int N2>
@@ -897,13 +910,18 @@ void launch_rank(const RankPlan& rp, RankArgs a, const cfloat* coils, const Sens
                  const unsigned char* plans)
 {
     fill_rank_args(rp, a, g);
+    if (rp.ws) {
+#define X_(YY, A1, A2)                               \
+    if (rp.N1 == A1 && rp.N2 == A2) {                \
+        launch_ws_t<A1, A2>(a, coils, g, plans);     \
+        return;                                      \
+    }
+        WS_SHAPES(X_)
+#undef X_
+        throw Error("ws A^H A: unsupported factorisation");
+    }
 #define X_(YY, A1, A2) \
-    case YY:                                     \
-        if (rp.ws)                               \
-            launch_ws_t<A1, A2>(a, coils, g, plans); \
-        else                                     \
-            launch_rank_t<A1, A2>(a, coils, g, plans); \
-        return;
+    case YY: launch_rank_t<A1, A2>(a, coils, g, plans); return;
     switch (g.Y) { RANK_SHAPES(X_) default: throw Error("rank A^H A: unsupported Y"); }
 #undef X_
 }

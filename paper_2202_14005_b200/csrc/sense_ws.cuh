@@ -193,34 +193,36 @@ __device__ __forceinline__ void dft(float2 (&v)[R])
 
 template<int N1, int N2>
 struct WsCfg {
-    using RC = RankCfg<N1, N2>;
+    using RC = RankCfg<N1, N2>; // plan record layout (TMAX, N2P) and TMA boxes
     static constexpr int Y = N1 * N2;
-    static constexpr int W = RC::W;
+    static constexpr int W = 8;
     static constexpr int N2P = RC::N2P;
     static constexpr int TMAX = RC::TMAX;
     static constexpr int NBOX = RC::NBOX, BOXR = RC::BOXR;
     static constexpr int NT_AC = ((W * N2 + 31) / 32) * 32;  // A/C threads (w, j)
-    static constexpr int JH = N2P / 2;                        // j per stage-B half row
-    // stage-B threads (row, column, half row); 6 warps cover the 12 ACL rows of
-    // the reference pattern family in one pass, more rows loop
-    static constexpr int NT_B = std::min(((2 * N1 * W + 31) / 32) * 32, 192);
+    // stage B: BQ threads per (row, column), each JQ consecutive j (even: float4 twiddle pairs)
+    static constexpr int BQ = N2 > 24 ? 4 : 2;
+    static constexpr int JQ = (((N2P + BQ - 1) / BQ) + 1) & ~1;
+    static constexpr int NT_B = std::min(((BQ * N1 * W + 31) / 32) * 32, 192);
     static constexpr int NT = NT_AC + NT_B + 32;             // + TMA producer warp
     static constexpr int SLOT = Y * W;                        // float2 per coil slice / stash
-    // S layout: element (row m, j, column w) at m * RP + SOFF(j) + w, with the
-    // second half row (j >= JH) shifted by 8 float2, so the two halves of a
-    // stage-B thread pair fall in opposite halves of the banks (conflict-free)
-    static constexpr int RP = N2P * W + 8;
-    __host__ __device__ static constexpr int SOFF(int j) { return j * W + (j >= JH ? 8 : 0); }
+    // S layout: element (row m, j, column w) at m * RP + SOFF(j) + w; j-part p
+    // is shifted by 8 p float2 so the BQ parts of a stage-B item fall in
+    // alternate halves of the banks (conflict-free)
+    static constexpr int RP = N2P * W + 8 * BQ;
+    __host__ __device__ static constexpr int SOFF(int j) { return j * W + 8 * (j / JQ); }
     static constexpr int SBUF = N1 * RP;
+    static constexpr int TTW = TMAX * N2P + 8;                // twiddle rows + zero pad (last part's reads)
     static constexpr size_t STATIC_EST = 4096;                // plan, barriers, reductions
     // 2 S buffers, stash, 2 staging strips (x or r, and p_prev), twiddle rows
-    static constexpr size_t FIXED = sizeof(float2) * (size_t(2) * SBUF + 3 * size_t(SLOT) + size_t(TMAX) * N2P);
+    static constexpr size_t FIXED = sizeof(float2) * (size_t(2) * SBUF + 3 * size_t(SLOT) + size_t(TTW));
     static constexpr size_t SMEM_MAX = 227 * 1024;
     static constexpr int NSLOT_FIT = int((SMEM_MAX - STATIC_EST - FIXED) / (sizeof(float2) * SLOT));
     static constexpr int NSLOT = NSLOT_FIT > 6 ? 6 : NSLOT_FIT;
     static constexpr size_t SMEM = FIXED + sizeof(float2) * size_t(NSLOT) * SLOT;
-    static_assert(NSLOT >= 2, "coil ring needs two slots");
+    static_assert(NSLOT >= 3, "coil ring needs three slots");
     static_assert(N1 == 8 || N1 == 16, "paired DFT sizes");
+    static_assert(W * 8 * 2 % 16 == 0 && (JQ * W) % 16 == 0, "bank layout");
 };
 
 #ifdef WS_PROF
@@ -385,83 +387,95 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                 int4* dtw = reinterpret_cast<int4*>(ttw);
                 for (int e = bt; e < int(TMAX * N2P * sizeof(float2) / 16); e += NT_B)
                     dtw[e] = src2[e];
+                for (int e = bt; e < Cfg::TTW - TMAX * N2P; e += NT_B)
+                    ttw[TMAX * N2P + e] = float2{0.f, 0.f};
                 named_bar_sync(1, NT_B);
                 plan_b = b;
             }
             WS_WAIT(1, &bar_sfull[i & 1], uint32_t((i >> 1) & 1));
             float2* S = Sb + (i & 1) * SBUF;
-            const int nitems = 2 * pl.nwork * W;
+            constexpr int BQ = Cfg::BQ, NJ = Cfg::JQ;
+            const int nitems = BQ * pl.nwork * W;
             for (int item = bt; item < nitems; item += NT_B) {
-                // thread pair (h = 0, 1) per (row, column): each half row in registers,
-                // dot products combined with one shuffle
-                const int h = item & 1, pr = item >> 1;
+                // BQ threads per (row, column): each NJ consecutive j in registers,
+                // dot products combined with log2(BQ) shuffles
+                const int h = item % BQ, pr = item / BQ;
                 const int r = pr / W, ww = pr - r * W;
                 const int k1 = pl.work_k1[r];
                 const int md = pl.mode[k1], nt = pl.nt[k1], off = pl.off[k1];
-                const int jb = h * Cfg::JH;
-                float2* row = S + k1 * RP + (h ? Cfg::JH * W + 8 : 0) + ww; // element jb + jj at row[jj * W]
-                const unsigned pmask = 3u << ((tid & 31) & ~1);
-                constexpr int NJ = Cfg::JH;
+                const int jb = h * NJ;
+                float2* row = S + k1 * RP + Cfg::SOFF(jb) + ww; // element jb + jj at row[jj * W]
+                const unsigned pmask = ((1u << BQ) - 1) << ((tid & 31) & ~(BQ - 1));
+                auto qsum = [&](float2 d) {
+#pragma unroll
+                    for (int o = 1; o < BQ; o <<= 1) {
+                        d.x += __shfl_xor_sync(pmask, d.x, o);
+                        d.y += __shfl_xor_sync(pmask, d.y, o);
+                    }
+                    return d;
+                };
                 float2 u[NJ];
 #pragma unroll
                 for (int jj = 0; jj < NJ; jj++)
                     u[jj] = (jb + jj < N2) ? row[jj * W] : float2{0.f, 0.f};
-                if (nt <= 2 && off + nt <= TMAX) {
-                    auto fast = [&](auto TWO) {
-                        constexpr bool two = decltype(TWO)::value;
-                        // 16-B aligned: N2P and JH even; pad twiddles (j >= N2) are zero
-                        const float4* t0v = reinterpret_cast<const float4*>(ttw + off * N2P + jb);
-                        const float4* t1v = reinterpret_cast<const float4*>(ttw + (two ? off + 1 : off) * N2P + jb);
-                        float2 d0a{0.f, 0.f}, d0b{0.f, 0.f}, d1a{0.f, 0.f}, d1b{0.f, 0.f};
+                if (nt <= 4 && off + nt <= TMAX) {
+                    // up to 4 terms with precomputed twiddle rows: all dot products in
+                    // one pass over the part (2 chains per term), then one scatter pass
+                    auto fast = [&](auto NTT_) {
+                        constexpr int NTT = decltype(NTT_)::value;
+                        // 16-B aligned: N2P and NJ even; reads past N2 meet zero u (or the zero pad)
+                        const float4* tv[NTT > 0 ? NTT : 1];
+#pragma unroll
+                        for (int t = 0; t < NTT; t++)
+                            tv[t] = reinterpret_cast<const float4*>(ttw + (off + t) * N2P + jb);
+                        float2 da[NTT > 0 ? NTT : 1], db[NTT > 0 ? NTT : 1];
+#pragma unroll
+                        for (int t = 0; t < NTT; t++)
+                            da[t] = db[t] = float2{0.f, 0.f};
 #pragma unroll
                         for (int jj = 0; jj < NJ; jj += 2) {
-                            const float4 q0 = t0v[jj >> 1];
-                            d0a = cx2::mac(d0a, u[jj], float2{q0.x, q0.y});
-                            d0b = cx2::mac(d0b, u[jj + 1], float2{q0.z, q0.w});
-                            if constexpr (two) {
-                                const float4 q1 = t1v[jj >> 1];
-                                d1a = cx2::mac(d1a, u[jj], float2{q1.x, q1.y});
-                                d1b = cx2::mac(d1b, u[jj + 1], float2{q1.z, q1.w});
+#pragma unroll
+                            for (int t = 0; t < NTT; t++) {
+                                const float4 q = tv[t][jj >> 1];
+                                da[t] = cx2::mac(da[t], u[jj], float2{q.x, q.y});
+                                db[t] = cx2::mac(db[t], u[jj + 1], float2{q.z, q.w});
                             }
                         }
-                        float2 d0 = cx2::add(d0a, d0b);
-                        d0.x += __shfl_xor_sync(pmask, d0.x, 1);
-                        d0.y += __shfl_xor_sync(pmask, d0.y, 1);
-                        d0 = nt > 0 ? cx2::mul(d0, pl.coef[off]) : float2{0.f, 0.f};
-                        const float2 e0{d0.y, -d0.x};
-                        float2 d1{0.f, 0.f}, e1{0.f, 0.f};
-                        if constexpr (two) {
-                            d1 = cx2::add(d1a, d1b);
-                            d1.x += __shfl_xor_sync(pmask, d1.x, 1);
-                            d1.y += __shfl_xor_sync(pmask, d1.y, 1);
-                            d1 = cx2::mul(d1, pl.coef[off + 1]);
-                            e1 = float2{d1.y, -d1.x};
+                        float2 d[NTT > 0 ? NTT : 1], e[NTT > 0 ? NTT : 1];
+#pragma unroll
+                        for (int t = 0; t < NTT; t++) {
+                            d[t] = cx2::mul(qsum(cx2::add(da[t], db[t])), pl.coef[off + t]);
+                            e[t] = float2{d[t].y, -d[t].x};
                         }
 #pragma unroll
                         for (int jj = 0; jj < NJ; jj += 2) {
-                            const float4 q0 = t0v[jj >> 1];
-                            float4 q1;
-                            if constexpr (two)
-                                q1 = t1v[jj >> 1];
+                            float4 q[NTT > 0 ? NTT : 1];
+#pragma unroll
+                            for (int t = 0; t < NTT; t++)
+                                q[t] = tv[t][jj >> 1];
 #pragma unroll
                             for (int hh = 0; hh < 2; hh++) {
                                 if (jb + jj + hh < N2) {
                                     float2 r0 = md == 1 ? u[jj + hh] : float2{0.f, 0.f};
-                                    r0 = cx2::mac_dconj(r0, d0, e0, hh ? float2{q0.z, q0.w} : float2{q0.x, q0.y});
-                                    if constexpr (two)
-                                        r0 = cx2::mac_dconj(r0, d1, e1, hh ? float2{q1.z, q1.w} : float2{q1.x, q1.y});
+#pragma unroll
+                                    for (int t = 0; t < NTT; t++)
+                                        r0 = cx2::mac_dconj(r0, d[t], e[t],
+                                                            hh ? float2{q[t].z, q[t].w} : float2{q[t].x, q[t].y});
                                     row[(jj + hh) * W] = r0;
                                 }
                             }
                         }
                     };
-                    if (nt == 2)
-                        fast(std::true_type{});
-                    else
-                        fast(std::false_type{});
+                    switch (nt) {
+                    case 0: fast(std::integral_constant<int, 0>{}); break;
+                    case 1: fast(std::integral_constant<int, 1>{}); break;
+                    case 2: fast(std::integral_constant<int, 2>{}); break;
+                    case 3: fast(std::integral_constant<int, 3>{}); break;
+                    default: fast(std::integral_constant<int, 4>{}); break;
+                    }
                 } else {
                     // general rows: any number of terms, twiddles indexed on the fly;
-                    // the half row in shared memory is the running result
+                    // the part row in shared memory is the running result
                     if (md != 1) {
 #pragma unroll
                         for (int jj = 0; jj < NJ; jj++)
@@ -483,10 +497,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                             m0 += k;
                             m0 -= m0 >= Y ? Y : 0;
                         }
-                        float2 d = cx2::add(da, db);
-                        d.x += __shfl_xor_sync(pmask, d.x, 1);
-                        d.y += __shfl_xor_sync(pmask, d.y, 1);
-                        d = cx2::mul(d, pl.coef[t]);
+                        const float2 d = cx2::mul(qsum(cx2::add(da, db)), pl.coef[t]);
                         const float2 e{d.y, -d.x};
                         m0 = m00;
 #pragma unroll
@@ -671,14 +682,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
         stage_c(n - 1, false);
     }
 #ifdef WS_PROF
-    if (tid == 0) {
-        unsigned long long gt;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        printf("ws ctaend %d sm %u start_ns %llu dur_cyc %lld\n", int(blockIdx.x), smid, gt, clock64() - tstart);
-    }
-    if (tid == 0 || tid == NT_AC || tid == NT_AC + NT_B)
+    if (blockIdx.x < 2 && (tid == 0 || tid == NT_AC || tid == NT_AC + NT_B))
         printf("ws cta %d role %s n %d total %lld wait empty %lld sfull %lld full %lld sdone %lld | open %lld A %lld C "
                "%lld epi %lld\n",
                int(blockIdx.x), tid == 0 ? "AC" : tid == NT_AC ? "B" : "P", n, clock64() - tstart, wprof[0], wprof[1],
