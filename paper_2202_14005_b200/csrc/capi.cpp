@@ -177,6 +177,8 @@ int mdnn_set_option(const char* key, long value)
             conv_tc_enable(value != 0);
         else if (k == "sense_rank")
             sense_rank_enable(value != 0);
+        else if (k == "rbf_window")
+            rbf_window_enable(value != 0);
         else if (k == "sense_ws")
             sense_ws_enable(value != 0);
         else if (k == "sense_rank_ctas")

@@ -5,6 +5,7 @@
 #include "core.h"
 
 #include <functional>
+#include <vector>
 
 namespace mdnn {
 
@@ -233,8 +234,16 @@ struct RbfGeom {
     long inner, nf, outer; // z viewed [inner][filter][outer]
     int nw;
     float sigma;
+    // evenly spaced centres: only the `win` centres around the nearest one are
+    // evaluated (every skipped basis value is below 2^-52 of the nearest one,
+    // i.e. under fp32 rounding of the sum); win = 0 evaluates all nw
+    int win = 0;
+    float mu0 = 0.f, inv_dmu = 0.f;
 };
 void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
+// decides g.win for the centres (host); honours the rbf_window option
+void rbf_set_window(RbfGeom& g, const std::vector<float>& mu);
+void rbf_window_enable(bool on);
 void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
 void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
 void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g);

@@ -727,6 +727,7 @@ public:
         g_.nw = int(mu.size());
         g_.sigma = sigma;
         mu_host_ = mu;
+        rbf_set_window(g_, mu);
     }
     void forward(const std::vector<DArray>& in, std::vector<DArray>& out, bool store) override
     {

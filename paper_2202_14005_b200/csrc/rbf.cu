@@ -5,10 +5,22 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cmath>
 
 namespace mdnn {
 
 namespace {
+
+bool g_rbf_window = true;
+
+// first centre of the evaluation window of z (evenly spaced centres): the
+// nearest centre +- (win - 1) / 2, clamped into [0, nw - win]
+__device__ __forceinline__ int rbf_wstart(float zk, const RbfGeom& g)
+{
+    const float t = rintf((zk - g.mu0) * g.inv_dmu) - float(g.win / 2);
+    const float hi = float(g.nw - g.win);
+    return int(fminf(fmaxf(t, 0.f), hi)); // NaN z: fmax(NaN, 0) = 0
+}
 
 constexpr int kT = 256;
 constexpr int kMaxW = 64;
@@ -56,7 +68,8 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
         const float zk = z[i].x;
         const float* wf = sw + f * g.nw;
         float acc = 0.f;
-        for (int j = 0; j < g.nw; j++) {
+        const int j0 = g.win ? rbf_wstart(zk, g) : 0, j1 = g.win ? j0 + g.win : g.nw;
+        for (int j = j0; j < j1; j++) {
             const float e = gauss2(zk, smu[j], k2);
             if (mode == 1)
                 acc = fmaf(wf[j] * e, -(zk - smu[j]) * inv_s2, acc);
@@ -98,16 +111,34 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
     const float inv_s2 = 1.f / (g.sigma * g.sigma);
     const long total = g.inner * g.outer;
     const long begin = long(blockIdx.x) * kChunk, end = min(total, begin + kChunk);
-    // fp32 running sums per thread (kChunk / blockDim = 32 terms each), folded in double
+    // fp32 running sums per thread (kChunk / blockDim = 32 terms each), folded in
+    // double.  Windowed centres: the sums live in shared memory [j][thread]
+    // (the window start varies per element; bank = thread, conflict-free)
+    extern __shared__ float sacc[];
     float acc[kMaxW];
-    for (int j = 0; j < g.nw; j++)
+    for (int j = 0; j < g.nw; j++) {
         acc[j] = 0.f;
+        if (g.win)
+            sacc[j * blockDim.x + threadIdx.x] = 0.f;
+    }
     const float k2 = 1.4426950408889634f / (2.f * g.sigma * g.sigma);
     for (long t = begin + threadIdx.x; t < end; t += blockDim.x) {
         const long ii = t % g.inner, o = t / g.inner;
         const long idx = ii + g.inner * (f + g.nf * o);
         const float zk = z[idx].x, gv = dy[idx].x;
-        if (dz) {
+        if (g.win) {
+            const int j0 = rbf_wstart(zk, g);
+            float d = 0.f;
+            for (int j = j0; j < j0 + g.win; j++) {
+                const float e = gauss2(zk, smu[j], k2);
+                float* a = sacc + j * blockDim.x + threadIdx.x;
+                *a = fmaf(e, gv, *a);
+                if (dz)
+                    d = fmaf(swf[j] * e, -(zk - smu[j]) * inv_s2, d);
+            }
+            if (dz)
+                dz[idx] = float2{d * gv, 0.f};
+        } else if (dz) {
             float d = 0.f;
             for (int j = 0; j < g.nw; j++) {
                 const float e = gauss2(zk, smu[j], k2);
@@ -119,6 +150,10 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
             for (int j = 0; j < g.nw; j++)
                 acc[j] = fmaf(gauss2(zk, smu[j], k2), gv, acc[j]);
         }
+    }
+    if (g.win) {
+        for (int j = 0; j < g.nw; j++)
+            acc[j] = sacc[j * blockDim.x + threadIdx.x];
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int j = 0; j < g.nw; j++) {
@@ -150,6 +185,29 @@ __global__ void k_rbf_wfinal(cfloat* dw, const double* part, RbfGeom g, int nchu
 }
 
 } // namespace
+
+void rbf_window_enable(bool on) { g_rbf_window = on; }
+
+void rbf_set_window(RbfGeom& g, const std::vector<float>& mu)
+{
+    g.win = 0;
+    const int n = int(mu.size());
+    if (!g_rbf_window || n < 3)
+        return;
+    const double dmu = (double(mu[n - 1]) - mu[0]) / (n - 1);
+    for (int j = 0; j < n; j++)
+        if (std::fabs(double(mu[j]) - (mu[0] + j * dmu)) > 1e-5 * dmu)
+            return; // not evenly spaced
+    // skipped centres lie >= (K + 1/2) dmu - (rounding slack) from z; 8.5 sigma
+    // puts their basis values below exp(-36) = 2^-52 of the nearest one's
+    const int K = int(std::ceil(8.5 * g.sigma / dmu + 0.5));
+    const int win = 2 * K + 1;
+    if (win >= n)
+        return;
+    g.win = win;
+    g.mu0 = mu[0];
+    g.inv_dmu = float(1.0 / dmu);
+}
 
 void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
 {
@@ -184,7 +242,8 @@ void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* m
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
-    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, 0, c.stream>>>(part, dy, z, mu, g, nchunk, nullptr, nullptr);
+    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, g.win ? sizeof(float) * kT * g.nw : 0, c.stream>>>(
+        part, dy, z, mu, g, nchunk, nullptr, nullptr);
     KERNEL_CHECK();
     k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
     KERNEL_CHECK();
@@ -199,7 +258,8 @@ void rbf_adjoint_zw(cfloat* dz, cfloat* dw, const cfloat* dy, const cfloat* z, c
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
-    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, 0, c.stream>>>(part, dy, z, mu, g, nchunk, dz, w);
+    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, g.win ? sizeof(float) * kT * g.nw : 0, c.stream>>>(
+        part, dy, z, mu, g, nchunk, dz, w);
     KERNEL_CHECK();
     k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
     KERNEL_CHECK();

@@ -206,16 +206,27 @@ def test_real_chan(gpu, ref, join):
     _check_node(ng, nr, [crand(rng, dims)], rng, TOL)
 
 
-def test_rbf(gpu, ref):
-    rng = np.random.default_rng(14)
-    nw, nf = 31, 6
+@pytest.mark.parametrize("window", [1, 0], ids=["window", "all-centres"])
+@pytest.mark.parametrize("nw,width,zscale", [(31, 1.0, 1.2), (64, 0.5, 3.0), (9, 1.0, 1.0)])
+def test_rbf(gpu, ref, window, nw, width, zscale):
+    """RbfNode (ops.hpp:1308-1427) against the reference: VarNet's 31 centres at
+    sigma = spacing, narrow Gaussians over 64 centres with z far outside the
+    centre range, and few centres (no window).  With evenly spaced centres the
+    product evaluates only the centres within 8.5 sigma of z (option
+    rbf_window); both paths are checked."""
+    rng = np.random.default_rng(14 + nw)
+    nf = 6
     z = list(d16(16, 12, nf))
     z[15] = 2
     centers = [-1 + 2 * j / (nw - 1) for j in range(nw)]
-    sigma = 2 / (nw - 1)
-    ng, nr = Nlop.rbf(gpu, z, 2, centers, sigma), Nlop.rbf(ref, z, 2, centers, sigma)
-    ins = [rrand(rng, z, 1.2), rrand(rng, nr.in_dims(1), 0.05)]
-    _check_node(ng, nr, ins, rng, TOL)
+    sigma = width * 2 / (nw - 1)
+    gpu.check(gpu.so.mdnn_set_option(b"rbf_window", window))
+    try:
+        ng, nr = Nlop.rbf(gpu, z, 2, centers, sigma), Nlop.rbf(ref, z, 2, centers, sigma)
+        ins = [rrand(rng, z, zscale), rrand(rng, nr.in_dims(1), 0.05)]
+        _check_node(ng, nr, ins, rng, TOL)
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"rbf_window", 1))
 
 
 def test_bcast_add_and_tenmul(gpu, ref):
