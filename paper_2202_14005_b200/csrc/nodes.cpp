@@ -377,6 +377,8 @@ public:
 private:
     DArray run(const DArray& x) const
     {
+        if (x.known_real) // Re(x) = conj(x) = x (values are immutable: share the array)
+            return x;
         DArray o(x.dims, false);
         if (k_ == Conj) {
             launch_conj(o.data(), x.data(), o.size());

@@ -122,9 +122,17 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
             sacc[j * blockDim.x + threadIdx.x] = 0.f;
     }
     const float k2 = 1.4426950408889634f / (2.f * g.sigma * g.sigma);
+    // element t = ii + inner * o walked incrementally (no 64-bit division per element)
+    long ii = (begin + threadIdx.x) % g.inner, o = (begin + threadIdx.x) / g.inner;
+    const long dii = long(blockDim.x) % g.inner, dob = long(blockDim.x) / g.inner;
     for (long t = begin + threadIdx.x; t < end; t += blockDim.x) {
-        const long ii = t % g.inner, o = t / g.inner;
         const long idx = ii + g.inner * (f + g.nf * o);
+        ii += dii;
+        o += dob;
+        if (ii >= g.inner) {
+            ii -= g.inner;
+            o++;
+        }
         const float zk = z[idx].x, gv = dy[idx].x;
         if (g.win) {
             const int j0 = rbf_wstart(zk, g);
@@ -235,6 +243,21 @@ void rbf_deriv_w(cfloat* dy, const cfloat* dw, const cfloat* z, const float* mu,
     KERNEL_CHECK();
 }
 
+// dynamic shared memory of k_rbf_wgrad (windowed: per-thread sums [nw][kT])
+size_t rbf_wgrad_smem(const RbfGeom& g)
+{
+    if (!g.win)
+        return 0;
+    const size_t bytes = sizeof(float) * kT * g.nw;
+    static size_t granted = 48 * 1024;
+    if (bytes > granted) {
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+        granted = bytes;
+    }
+    return bytes;
+}
+
 void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g)
 {
     auto& c = ctx();
@@ -242,7 +265,7 @@ void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* m
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
-    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, g.win ? sizeof(float) * kT * g.nw : 0, c.stream>>>(
+    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
         part, dy, z, mu, g, nchunk, nullptr, nullptr);
     KERNEL_CHECK();
     k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
@@ -258,7 +281,7 @@ void rbf_adjoint_zw(cfloat* dz, cfloat* dw, const cfloat* dy, const cfloat* z, c
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
-    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, g.win ? sizeof(float) * kT * g.nw : 0, c.stream>>>(
+    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
         part, dy, z, mu, g, nchunk, dz, w);
     KERNEL_CHECK();
     k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
