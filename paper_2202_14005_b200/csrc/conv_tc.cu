@@ -223,45 +223,59 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
                 const int py0 = y0 + jc * 2; // 16 columns = 2 lines x 8 pixels
                 if (py0 >= Y)
                     break;
-                float v[16];
-                tmem_ld16(acc + jc * 16, v);
-                tmem_ld_wait();
-                float* o = out + ((long(b) * Y + py0) * X + x0) * N + n;
-                // fp32 sums shifted by the chunk's first value (always in range), so the
-                // sum of squares carries the spread, not the mean; re-centred in double
-                const float sh = v[0];
-                float fs = 0.f, fq = 0.f;
-                int nv = 0;
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const int l = j >> 3, xo = j & 7;
-                    if ((full_x || x0 + xo < X) && py0 + l < Y) {
-                        if (dbg != 1)
-                            o[(long(l) * X + xo) * N] = v[j];
-                        const float d = v[j] - sh;
-                        fs += d;
-                        fq = fmaf(d, d, fq);
-                        nv++;
-                    }
-                }
-                s_acc += double(nv) * sh + fs;
-                q_acc += double(sh) * (double(nv) * sh + 2.0 * fs) + fq;
+                // every pixel of the chunk in range (all but the image's last tile row / column)
+                const bool full = (full_x || x0 + 8 <= X) && py0 + 2 <= Y;
+                // BN-backward consumer: the BN input x of the chunk's pixels, issued
+                // before the TMEM load so their latency overlaps it and the stores
+                float xr[16], xi[16];
                 if (be.part) {
                     const float* xp = be.x + ((long(b) * Y + py0) * X + x0) * N + bc;
-                    float xr[16], xi[16];
 #pragma unroll
                     for (int j = 0; j < 16; j++) { // 32 loads in flight
                         const int l = j >> 3, xo = j & 7;
-                        const bool ok = (full_x || x0 + xo < X) && py0 + l < Y;
+                        const bool ok = full || ((full_x || x0 + xo < X) && py0 + l < Y);
                         const long off = (long(l) * X + xo) * N;
                         xr[j] = ok ? __ldg(xp + off) : 0.f;
                         xi[j] = ok ? __ldg(xp + off + 64) : 0.f;
                     }
+                }
+                float v[16];
+                tmem_ld16(acc + jc * 16, v);
+                tmem_ld_wait();
+                float* o = out + ((long(b) * Y + py0) * X + x0) * N + n;
+                if (dbg != 1) {
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        const int l = j >> 3, xo = j & 7;
+                        if (full || ((full_x || x0 + xo < X) && py0 + l < Y))
+                            o[(long(l) * X + xo) * N] = v[j];
+                    }
+                }
+                if (stats) {
+                    // fp32 sums shifted by the chunk's first value (always in range), so the
+                    // sum of squares carries the spread, not the mean; re-centred in double
+                    const float sh = v[0];
+                    float fs = 0.f, fq = 0.f;
+                    int nv = 0;
+#pragma unroll
+                    for (int j = 0; j < 16; j++) {
+                        const int l = j >> 3, xo = j & 7;
+                        if (full || ((full_x || x0 + xo < X) && py0 + l < Y)) {
+                            const float d = v[j] - sh;
+                            fs += d;
+                            fq = fmaf(d, d, fq);
+                            nv++;
+                        }
+                    }
+                    s_acc += double(nv) * sh + fs;
+                    q_acc += double(sh) * (double(nv) * sh + 2.0 * fs) + fq;
+                }
+                if (be.part) {
                     float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
                         const int l = j >> 3, xo = j & 7;
-                        const bool ok = (full_x || x0 + xo < X) && py0 + l < Y;
+                        const bool ok = full || ((full_x || x0 + xo < X) && py0 + l < Y);
                         // yhat and z exactly as bn_z (bnblock.cu)
                         const float hr = (xr[j] - bmu.x) * bs, hi = (xi[j] - bmu.y) * bs;
                         const float zr = bg.x * hr - bg.y * hi + bb.x;
