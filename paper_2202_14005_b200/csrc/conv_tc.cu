@@ -90,7 +90,10 @@ struct BnEpi {
     double* part = nullptr; // [blk][128][3]
 };
 
-template<int CIN2>
+// EPI: epilogue kind, a compile-time choice so each form carries only its own
+// registers (the 576-thread CTA caps them at 96): 0 = store only, 1 = store +
+// forward BN statistics, 2 = store + BN-backward partials (bwd-data)
+template<int CIN2, int EPI>
 __global__ void __launch_bounds__(TT_THREADS, 1)
     k_conv_tc_t(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
                 float* __restrict__ out, int X, int Y, int B, int dbg, double* __restrict__ stats, const BnEpi be)
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
         const int bc = n & 63, comp = n >> 6;
         float2 bmu{0.f, 0.f}, bg{0.f, 0.f}, bb{0.f, 0.f};
         float bs = 0.f;
-        if (be.part) {
+        if (EPI == 2) {
             bmu = be.mu[bc];
             bs = be.istd[bc];
             bg = be.gamma[bc];
@@ -212,6 +215,9 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
         double r0 = 0, r1 = 0, r2 = 0;
         uint32_t ti = 0;
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ti++) {
+            // BN-backward sums of this tile's chunks (fp32 over NP / 16 / 4 chunks of
+            // 16 pixels, then double: one FP64 add per tile, not per chunk)
+            float t0 = 0.f, t1 = 0.f, t2 = 0.f;
             const int tx = tile % tiles_x, ty = (tile / tiles_x) % tiles_y, b = tile / (tiles_x * tiles_y);
             const int x0 = tx * TT_X, y0 = ty * TT_Y;
             const uint32_t ab = ti & 1, acc = tmem_base + ab * NP + (uint32_t(lg * 32) << 16);
@@ -228,7 +234,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
                 // BN-backward consumer: the BN input x of the chunk's pixels, issued
                 // before the TMEM load so their latency overlaps it and the stores
                 float xr[16], xi[16];
-                if (be.part) {
+                if (EPI == 2) {
                     const float* xp = be.x + ((long(b) * Y + py0) * X + x0) * N + bc;
 #pragma unroll
                     for (int j = 0; j < 16; j++) { // 32 loads in flight
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
                             o[(long(l) * X + xo) * N] = v[j];
                     }
                 }
-                if (stats) {
+                if (EPI == 1) {
                     // fp32 sums shifted by the chunk's first value (always in range), so the
                     // sum of squares carries the spread, not the mean; re-centred in double
                     const float sh = v[0];
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
                     s_acc += double(nv) * sh + fs;
                     q_acc += double(sh) * (double(nv) * sh + 2.0 * fs) + fq;
                 }
-                if (be.part) {
+                if (EPI == 2) {
                     float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
@@ -286,21 +292,26 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
                         f1 = fmaf(ge, comp ? hi : hr, f1);
                         f2 = fmaf(ge, comp ? hr : -hi, f2);
                     }
-                    r0 += f0;
-                    r1 += f1;
-                    r2 += f2;
+                    t0 += f0;
+                    t1 += f1;
+                    t2 += f2;
                 }
             }
             tc_fence_before();
             mbar_arrive(&tmem_empty[ab]);
+            if (EPI == 2) {
+                r0 += t0;
+                r1 += t1;
+                r2 += t2;
+            }
         }
         // one partial block per (CTA, epilogue half)
         const size_t slot = size_t(blockIdx.x) * (TT_EPI_WARPS / 4) + half;
-        if (stats) {
+        if (EPI == 1) {
             stats[(slot * N + n) * 2] = s_acc;
             stats[(slot * N + n) * 2 + 1] = q_acc;
         }
-        if (be.part) {
+        if (EPI == 2) {
             be.part[(slot * N + n) * 3] = r0;
             be.part[(slot * N + n) * 3 + 1] = r1;
             be.part[(slot * N + n) * 3 + 2] = r2;
@@ -798,14 +809,15 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
     if constexpr (N == 128) {
         // transposed form: D^T[channel][pixel], N = 256 pixels per MMA
         CUtensorMap tat = make_act_map(act, CIN2, X, Y, B, TT_P, TT_L);
-        auto kt = k_conv_tc_t<CIN2>;
+        const int epi = be.part ? 2 : stats ? 1 : 0;
+        auto kt = epi == 2 ? k_conv_tc_t<CIN2, 2> : epi == 1 ? k_conv_tc_t<CIN2, 1> : k_conv_tc_t<CIN2, 0>;
         const int smem_t = TtSmem::TOTAL;
         {
             std::lock_guard<std::mutex> lk(mu);
             static std::map<int, bool> done_t;
-            if (!done_t[c.device]) {
+            if (!done_t[c.device * 4 + epi]) {
                 CUDA_CHECK(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_t));
-                done_t[c.device] = true;
+                done_t[c.device * 4 + epi] = true;
             }
         }
         const int nt = ((X + TT_X - 1) / TT_X) * ((Y + TT_Y - 1) / TT_Y) * B;
