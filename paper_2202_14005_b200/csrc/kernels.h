@@ -154,6 +154,7 @@ bool conv_bn_fuse();
 void sense_rank_enable(bool on);
 void sense_rank_ctas(long g);
 void sense_ws_enable(bool on);
+void rank_rr_enable(bool on);
 void cg_defer_x_enable(bool on);
 bool rank_enabled();
 // test hook: auto-layout convs store multi-channel activations channels-last

@@ -887,6 +887,7 @@ bool g_rank_enabled = true;
 void sense_rank_enable(bool on) { g_rank_enabled = on; }
 void sense_rank_ctas(long g) { g_rank_ctas = g; }
 void sense_ws_enable(bool on) { g_sense_ws = on; }
+void rank_rr_enable(bool on) { g_rank_rr = on; }
 void cg_defer_x_enable(bool on) { g_cg_defer_x = on; }
 bool rank_enabled() { return g_rank_enabled; }
 

@@ -29,6 +29,7 @@
 bool g_cg_defer_x = true; // CG: keep every p, update r only per iteration, sum x once
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
 bool g_sense_ws = true; // warp-specialised kernel (sense_ws.cuh), one CTA per SM
+bool g_rank_rr = true;  // whole strips round robin for 32-B strips (RankPlan::rr)
 
 constexpr int rank_nbox(int Y)
 {
@@ -75,6 +76,7 @@ struct RankArgs {
     long nxb;             // strips per item
     long units;           // strips * C
     int G;                // CTAs
+    int rr;               // 1: CTA g owns whole strips g, g + G, g + 2G, ... (no split strips)
     PatStr ps;
     int mode, it;
     CgDev* cg;
@@ -95,6 +97,8 @@ __host__ __device__ __forceinline__ int rank_planes(long s, long C, long U, long
 // destination of a segment's partial: plane 0 = out, plane k >= 1 = out1 + (k - 1) * pstride
 __device__ __forceinline__ cfloat* rank_plane_dst(const RankArgs& a, int strip, int cta)
 {
+    if (a.rr)
+        return a.out;
     const int k = cta - int(rank_owner(long(strip) * a.C, a.units, a.G));
     return k == 0 ? a.out : a.out1 + long(k - 1) * a.pstride;
 }
@@ -218,8 +222,15 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
     const int j = active ? j0 : N2 - 1;
     const int C = int(a.C), nxb = int(a.nxb);
     const int U = int(a.units);
-    const int u_begin = int(long(U) * blockIdx.x / a.G), u_end = int(long(U) * (blockIdx.x + 1) / a.G);
-    const int n = u_end - u_begin;
+    // contiguous unit ranges, or (a.rr) whole strips g, g + G, ...: the CTAs then
+    // read neighbouring strips of the same coil at the same time, so the 128-B
+    // DRAM lines of narrow (32-B) strips are fetched once
+    const int u_begin = a.rr ? int(blockIdx.x) * C : int(long(U) * blockIdx.x / a.G);
+    const int u_end = int(long(U) * (blockIdx.x + 1) / a.G);
+    const int nstrips_rr = a.rr ? int((U / C - 1 - int(blockIdx.x)) / a.G + 1) : 0;
+    const int n = a.rr ? nstrips_rr * C : u_end - u_begin;
+    // global unit of local unit i
+    auto unit_of = [&](int i) { return a.rr ? (int(blockIdx.x) + (i / C) * a.G) * C + i % C : u_begin + i; };
 
     auto issue = [&](int u, int slot) { // TMA of unit u's coil slice into ring slot
         const int s = u / C, c = u - s * C;
@@ -237,7 +248,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
         sm100::mbar_init(&s_bar[1], 1);
         sm100::fence_barrier_init();
         for (int i = 0; i < n && i < 2; i++)
-            issue(u_begin + i, i);
+            issue(unit_of(i), i);
         s_beta = a.mode == 1 ? cg_prologue(a.cg, a.it, a.errflags) : 0.f;
         s_lam = a.lam ? a.lam[0] : float2{0.f, 0.f};
     }
@@ -308,7 +319,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
         if (i < n) {
             if (opens) {
                 if (i > 0)
-                    seg_s++;
+                    seg_s += a.rr ? a.G : 1;
                 seg_first = c_cur == 0;
                 const int b = seg_s / nxb;
                 if (b != plan_b && (plan_b < 0 || a.ps.sb != 0)) {
@@ -387,7 +398,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
         c_cur = c_cur + 1 == C ? 0 : c_cur + 1;
         // slot i & 1 is consumed (coils now live in registers): refill it
         if (tid == 0 && i + 2 < n)
-            issue(u_begin + i + 2, i & 1);
+            issue(unit_of(i + 2), i & 1);
         // ---- B(i): per non-identity row, a thread pair (h = j half) per column:
         //   r = b A + sum_t coef_t (sum_j A_j w_t[j]) conj(w_t[j])
         for (int item = tid; item < n_items; item += NT) {
@@ -740,10 +751,10 @@ __global__ void __launch_bounds__(256) k_cg_x_sum(const CgDev* __restrict__ st, 
 }
 
 // split flags of every strip (written once per plan buffer)
-__global__ void k_rank_split_flags(unsigned char* flags, long strips, long C, long U, long G)
+__global__ void k_rank_split_flags(unsigned char* flags, long strips, long C, long U, long G, int rr)
 {
     for (long s = blockIdx.x * long(blockDim.x) + threadIdx.x; s < strips; s += long(gridDim.x) * blockDim.x)
-        flags[s] = (unsigned char)rank_planes(s, C, U, G);
+        flags[s] = rr ? 1 : (unsigned char)rank_planes(s, C, U, G);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 rank_encode_fn()
@@ -767,6 +778,7 @@ struct RankPlan {
     int G = 0;
     int planes = 1; // max CTAs sharing a strip (Ap planes)
     bool ws = false; // warp-specialised kernel (sense_ws.cuh)
+    bool rr = false; // k_normal_rank with whole strips per CTA, round robin (32-B strips)
     bool ok = false;
 };
 
@@ -800,17 +812,25 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
     case 512: minb = RankCfg<16, 32>::MINB; break;
     case 640: minb = RankCfg<16, 40>::MINB; break;
     }
-    // warp-specialised kernel for the W = 8 shapes (N2 <= 24); Y = 512 / 640 keep
-    // k_normal_rank (their ws buffers do not fit shared memory).  N1 = 8 with
-    // twice the A/C warps was measured slower at Y = 368 (71.9 vs 63 us per CG
-    // launch): stage B then carries ~3.3 terms per row over 46-point rows.
-    r.ws = g_sense_ws && r.W == 8;
+    // warp-specialised kernel (k_normal_rank stays behind option sense_ws = 0).
+    // N1 = 8 with twice the A/C warps was measured slower at Y = 368 (71.9 vs 63
+    // us per CG launch): stage B then carries ~3.3 terms per row over 46-point rows.
+    r.ws = g_sense_ws;
     if (r.ws)
         minb = 1;
     r.G = int(std::min<long>(g_rank_ctas > 0 ? g_rank_ctas : long(minb) * ctx().sm_count, r.units));
+    // 32-B strips (W = 4): contiguous unit ranges put neighbouring strips of a
+    // 128-B DRAM line on CTAs at different coils, and each line was fetched up to
+    // 4x (1.09 GB for 302 MB algorithmic at 512^2 x 32 coils).  Whole strips
+    // round robin keep neighbours in step; the load imbalance (ceil(strips / G))
+    // is the smaller cost.
+    r.rr = r.W == 4 && g_rank_rr && r.strips >= r.G;
+    if (r.rr)
+        r.G = int(std::min<long>(r.G, r.strips));
     r.planes = 1;
-    for (long s = 0; s < r.strips; s++)
-        r.planes = std::max(r.planes, rank_planes(s, g.C, r.units, r.G));
+    if (!r.rr)
+        for (long s = 0; s < r.strips; s++)
+            r.planes = std::max(r.planes, rank_planes(s, g.C, r.units, r.G));
     r.ok = r.units < (1L << 30) && g.Y * g.C * g.B < (1L << 30) && g.X * g.Y < (1L << 30) && r.planes < 250;
     return r;
 }
@@ -824,9 +844,15 @@ void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const un
     cuuint64_t strides[1] = {cuuint64_t(2 * g.X) * 4};
     cuuint32_t box[2] = {cuuint32_t(2 * Cfg::W), cuuint32_t(Cfg::BOXR)};
     cuuint32_t es[2] = {1, 1};
+    // promote only to the box row: 32-B rows (W = 4) promoted to 128 B read the
+    // neighbouring strips too, which other CTAs fetch again later (3.5x the
+    // algorithmic DRAM bytes measured at 512^2 x 32 coils)
     CUresult res = rank_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<cfloat*>(coils), dims, strides,
                                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                    Cfg::W * 8 >= 128  ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                    : Cfg::W * 8 >= 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                                       : CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (res != CUDA_SUCCESS)
         throw CudaError("cuTensorMapEncodeTiled(coils) failed: " + std::to_string(int(res)));
     auto kern = k_normal_rank<N1, N2>;
@@ -855,7 +881,7 @@ void launch_rank_plan_t(const RankArgs& a, unsigned char* plans, int nitems)
 #define RANK_SHAPES(X_) X_(128, 8, 16) X_(256, 16, 16) X_(320, 16, 20) X_(368, 16, 23) X_(512, 16, 32) X_(640, 16, 40)
 // (N1, N2) of every plan record layout: the k_normal_rank shapes and the ws shapes
 #define PLAN_SHAPES(X_) RANK_SHAPES(X_)
-#define WS_SHAPES(X_) X_(368, 16, 23) X_(320, 16, 20) X_(256, 16, 16) X_(128, 8, 16)
+#define WS_SHAPES(X_) RANK_SHAPES(X_)
 
 // device memory for the per-item plans of a pattern
 size_t rank_plan_record_bytes(const SenseGeom& g, const RankPlan& rp)
@@ -884,6 +910,7 @@ void fill_rank_args(const RankPlan& rp, RankArgs& a, const SenseGeom& g)
     a.nxb = rp.nxb;
     a.units = rp.units;
     a.G = rp.G;
+    a.rr = rp.rr ? 1 : 0;
 }
 
 void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsigned char* plans)
@@ -891,7 +918,7 @@ void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsign
     fill_rank_args(rp, a, g);
     const int items = int(g.pat_b > 1 ? g.pat_b : 1);
     k_rank_split_flags<<<int(std::min<long>((rp.strips + 255) / 256, 64)), 256, 0, ctx().stream>>>(
-        plans + rank_plan_record_bytes(g, rp), rp.strips, g.C, rp.units, rp.G);
+        plans + rank_plan_record_bytes(g, rp), rp.strips, g.C, rp.units, rp.G, rp.rr ? 1 : 0);
     KERNEL_CHECK();
 #define X_(YY, A1, A2)                                \
     if (rp.N1 == A1 && rp.N2 == A2) {                 \

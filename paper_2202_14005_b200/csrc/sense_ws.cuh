@@ -195,21 +195,23 @@ template<int N1, int N2>
 struct WsCfg {
     using RC = RankCfg<N1, N2>; // plan record layout (TMAX, N2P) and TMA boxes
     static constexpr int Y = N1 * N2;
-    static constexpr int W = 8;
+    static constexpr int W = N2 <= 24 ? 8 : 4;                // as k_normal_rank (32-B strips past N2 = 24)
     static constexpr int N2P = RC::N2P;
     static constexpr int TMAX = RC::TMAX;
     static constexpr int NBOX = RC::NBOX, BOXR = RC::BOXR;
     static constexpr int NT_AC = ((W * N2 + 31) / 32) * 32;  // A/C threads (w, j)
     // stage B: BQ threads per (row, column), each JQ consecutive j (even: float4 twiddle pairs)
     static constexpr int BQ = N2 > 24 ? 4 : 2;
-    static constexpr int JQ = (((N2P + BQ - 1) / BQ) + 1) & ~1;
+    static constexpr int jq(int v) { return (v * W) % 16 == 0 ? v : jq(v + 2); }
+    static constexpr int JQ = jq((((N2P + BQ - 1) / BQ) + 1) & ~1); // parts start 16-float2 aligned
     static constexpr int NT_B = std::min(((BQ * N1 * W + 31) / 32) * 32, 192);
     static constexpr int NT = NT_AC + NT_B + 32;             // + TMA producer warp
     static constexpr int SLOT = Y * W;                        // float2 per coil slice / stash
     // S layout: element (row m, j, column w) at m * RP + SOFF(j) + w; j-part p
     // is shifted by 8 p float2 so the BQ parts of a stage-B item fall in
     // alternate halves of the banks (conflict-free)
-    static constexpr int RP = N2P * W + 8 * BQ;
+    // (W = 4: + 4 more, so the two rows of a stage-B warp use opposite bank quarters)
+    static constexpr int RP = N2P * W + 8 * BQ + (W == 4 ? 4 : 0);
     __host__ __device__ static constexpr int SOFF(int j) { return j * W + 8 * (j / JQ); }
     static constexpr int SBUF = N1 * RP;
     static constexpr int TTW = TMAX * N2P + 8;                // twiddle rows + zero pad (last part's reads)
@@ -222,7 +224,7 @@ struct WsCfg {
     static constexpr size_t SMEM = FIXED + sizeof(float2) * size_t(NSLOT) * SLOT;
     static_assert(NSLOT >= 3, "coil ring needs three slots");
     static_assert(N1 == 8 || N1 == 16, "paired DFT sizes");
-    static_assert(W * 8 * 2 % 16 == 0 && (JQ * W) % 16 == 0, "bank layout");
+    static_assert((JQ * W) % 16 == 0, "bank layout");
 };
 
 #ifdef WS_PROF
@@ -265,8 +267,20 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
     const int tid = threadIdx.x;
     const int C = int(a.C), nxb = int(a.nxb);
     const int U = int(a.units);
-    const int u_begin = int(long(U) * blockIdx.x / a.G), u_end = int(long(U) * (blockIdx.x + 1) / a.G);
-    const int n = u_end - u_begin;
+    // contiguous unit ranges, or (a.rr, 32-B strips) whole strips g, g + G, ...
+    // so that neighbouring strips of one 128-B DRAM line are read together
+    const int u_begin = a.rr ? int(blockIdx.x) * C : int(long(U) * blockIdx.x / a.G);
+    const int n = a.rr ? C * ((U / C - 1 - int(blockIdx.x)) / a.G + 1)
+                       : int(long(U) * (blockIdx.x + 1) / a.G) - u_begin;
+    const int sstep = a.rr ? a.G : 1; // strip step between segments
+    // next segment's strip: (b, xb) advanced by sstep strips
+    auto next_strip = [&](int& xb, int& b) {
+        xb += sstep;
+        while (xb >= nxb) {
+            xb -= nxb;
+            ++b;
+        }
+    };
 
     if (tid == 0) {
         for (int s = 0; s < NSLOT; s++) {
@@ -327,10 +341,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                                            Y * st_b + k * Cfg::BOXR);
                 }
                 nst++;
-                if (++st_xb == nxb) {
-                    st_xb = 0;
-                    ++st_b;
-                }
+                next_strip(st_xb, st_b);
             };
             for (int i = 0; i < n; i++) {
                 if (seg_start(nst) == i)
@@ -342,10 +353,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                 const int xb_i = xblk;
                 if (++c == C) {
                     c = 0;
-                    if (++xblk == nxb) {
-                        xblk = 0;
-                        ++b;
-                    }
+                    next_strip(xblk, b);
                 }
                 sm100::mbar_arrive_expect_tx(&bar_full[slot], uint32_t(SLOT * sizeof(float2)));
 #pragma unroll
@@ -371,10 +379,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
             const int b = w_b;
             if (++w_c == C) {
                 w_c = 0;
-                if (++w_xb == nxb) {
-                    w_xb = 0;
-                    ++w_b;
-                }
+                next_strip(w_xb, w_b);
             }
             if (b != plan_b && (plan_b < 0 || a.ps.sb != 0)) {
                 using Rec = RankPlanRec<N1, N2>;
@@ -554,7 +559,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                 prev_first = cur_first;
                 prev_b = cur_b;
                 prev_xb = cur_xb;
-                cur_s = i == 0 ? cur_s : cur_s + 1;
+                cur_s = i == 0 ? cur_s : cur_s + sstep;
                 cur_first = a_c == 0;
                 cur_b = a_b;
                 cur_xb = a_xb;
@@ -589,10 +594,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
             // advance the stage-A walker
             if (++a_c == C) {
                 a_c = 0;
-                if (++a_xb == nxb) {
-                    a_xb = 0;
-                    ++a_b;
-                }
+                next_strip(a_xb, a_b);
             }
             const int slot = i % NSLOT;
 #ifdef WS_PROF

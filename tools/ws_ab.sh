@@ -11,7 +11,7 @@ for lib in $ALT_LIBS; do
   MDNN_B200_LIB=$lib timeout 300 python tools/sense_bench.py $SH --iters 20 >> gpurun_out/ab.log 2>&1
 done
 echo "== sense_ws=0" >> gpurun_out/ab.log
-timeout 300 python tools/sense_bench.py $SH --iters 20 --opt sense_ws=0 >> gpurun_out/ab.log 2>&1
+timeout 300 python tools/sense_bench.py $SH --iters 20 --opt sense_ws=0 ${ALT_OPT} >> gpurun_out/ab.log 2>&1
 if [ -n "$TESTS" ]; then timeout 600 python -m pytest -q -x tests/test_gpu_sense_rank.py tests/test_gpu_sense.py tests/test_gpu_golden.py > gpurun_out/ab_tests.log 2>&1; tail -2 gpurun_out/ab_tests.log; fi
 python - <<'PY'
 import json
