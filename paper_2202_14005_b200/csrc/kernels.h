@@ -239,7 +239,8 @@ struct RbfGeom {
     // evaluated (every skipped basis value is below 2^-52 of the nearest one,
     // i.e. under fp32 rounding of the sum); win = 0 evaluates all nw
     int win = 0;
-    float mu0 = 0.f, inv_dmu = 0.f;
+    float mu0 = 0.f, inv_dmu = 0.f, dmu = 0.f;
+    float q = 0.f; // exp(-dmu^2 / sigma^2): ratio of consecutive recurrence factors
 };
 void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
 // decides g.win for the centres (host); honours the rbf_window option

@@ -13,17 +13,51 @@ namespace {
 
 bool g_rbf_window = true;
 
-// first centre of the evaluation window of z (evenly spaced centres): the
-// nearest centre +- (win - 1) / 2, clamped into [0, nw - win]
-__device__ __forceinline__ int rbf_wstart(float zk, const RbfGeom& g)
-{
-    const float t = rintf((zk - g.mu0) * g.inv_dmu) - float(g.win / 2);
-    const float hi = float(g.nw - g.win);
-    return int(fminf(fmaxf(t, 0.f), hi)); // NaN z: fmax(NaN, 0) = 0
-}
-
 constexpr int kT = 256;
 constexpr int kMaxW = 64;
+
+// Evenly spaced centres (g.win = 2K + 1 > 0): visits (j, e_j, d_j = z - mu_j) for the
+// centres within K of the one nearest z, by the Gaussian recurrence
+//   e_{j+1} = e_j U_j, U_{j+1} = U_j q ;  e_{j-1} = e_j D_j, D_{j-1} = D_j q,
+//   U_j = exp(dmu (2 d_j - dmu) / 2s^2), D_j = exp(-dmu (2 d_j + dmu) / 2s^2),
+// 3 MUFU per element instead of one per centre.  Rounding grows ~k^2 / 2 ulp over k
+// steps, where the basis value is already below exp(-k^2 / 2) of the peak.
+template<int KT, class F>
+__device__ __forceinline__ void rbf_visit_k(float zk, const float* smu, const RbfGeom& g, float k2, F&& f)
+{
+    const int K = KT > 0 ? KT : (g.win >> 1);
+    const float t = rintf((zk - g.mu0) * g.inv_dmu);
+    const int jc = int(fminf(fmaxf(t, 0.f), float(g.nw - 1))); // NaN z: fmax(NaN, 0) = 0
+    const float dc = zk - smu[jc];
+    const float ec = exp2f(-(dc * dc) * k2);
+    f(jc, ec, dc);
+    const float dm = g.dmu;
+    float U = exp2f(k2 * dm * (2.f * dc - dm)), D = exp2f(-k2 * dm * (2.f * dc + dm));
+    float eu = ec, ed = ec;
+    const bool inner = jc >= K && jc + K < g.nw; // no edge: every visited centre exists
+#pragma unroll
+    for (int k = 1; k <= (KT > 0 ? KT : 64); k++) {
+        if (KT == 0 && k > K)
+            break;
+        eu *= U;
+        U *= g.q;
+        ed *= D;
+        D *= g.q;
+        if (inner || jc + k < g.nw)
+            f(jc + k, eu, fmaf(-float(k), dm, dc));
+        if (inner || jc - k >= 0)
+            f(jc - k, ed, fmaf(float(k), dm, dc));
+    }
+}
+
+template<class F>
+__device__ __forceinline__ void rbf_visit(float zk, const float* smu, const RbfGeom& g, float k2, F&& f)
+{
+    if (g.win == 19) // VarNet: 31 centres at sigma = spacing
+        rbf_visit_k<9>(zk, smu, g, k2, f);
+    else
+        rbf_visit_k<0>(zk, smu, g, k2, f);
+}
 
 int grid_for(long n)
 {
@@ -68,13 +102,19 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
         const float zk = z[i].x;
         const float* wf = sw + f * g.nw;
         float acc = 0.f;
-        const int j0 = g.win ? rbf_wstart(zk, g) : 0, j1 = g.win ? j0 + g.win : g.nw;
-        for (int j = j0; j < j1; j++) {
-            const float e = gauss2(zk, smu[j], k2);
+        if (g.win) {
             if (mode == 1)
-                acc = fmaf(wf[j] * e, -(zk - smu[j]) * inv_s2, acc);
+                rbf_visit(zk, smu, g, k2, [&](int j, float e, float d) { acc = fmaf(wf[j] * e, -d * inv_s2, acc); });
             else
-                acc = fmaf(wf[j], e, acc);
+                rbf_visit(zk, smu, g, k2, [&](int j, float e, float) { acc = fmaf(wf[j], e, acc); });
+        } else {
+            for (int j = 0; j < g.nw; j++) {
+                const float e = gauss2(zk, smu[j], k2);
+                if (mode == 1)
+                    acc = fmaf(wf[j] * e, -(zk - smu[j]) * inv_s2, acc);
+                else
+                    acc = fmaf(wf[j], e, acc);
+            }
         }
         if (mode == 1)
             acc *= gin[i].x;
@@ -135,17 +175,17 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
         }
         const float zk = z[idx].x, gv = dy[idx].x;
         if (g.win) {
-            const int j0 = rbf_wstart(zk, g);
             float d = 0.f;
-            for (int j = j0; j < j0 + g.win; j++) {
-                const float e = gauss2(zk, smu[j], k2);
-                float* a = sacc + j * blockDim.x + threadIdx.x;
-                *a = fmaf(e, gv, *a);
-                if (dz)
-                    d = fmaf(swf[j] * e, -(zk - smu[j]) * inv_s2, d);
-            }
-            if (dz)
+            float* ab = sacc + threadIdx.x;
+            if (dz) {
+                rbf_visit(zk, smu, g, k2, [&](int j, float e, float dj) {
+                    ab[j * blockDim.x] = fmaf(e, gv, ab[j * blockDim.x]);
+                    d = fmaf(swf[j] * e, -dj * inv_s2, d);
+                });
                 dz[idx] = float2{d * gv, 0.f};
+            } else {
+                rbf_visit(zk, smu, g, k2, [&](int j, float e, float) { ab[j * blockDim.x] = fmaf(e, gv, ab[j * blockDim.x]); });
+            }
         } else if (dz) {
             float d = 0.f;
             for (int j = 0; j < g.nw; j++) {
@@ -180,6 +220,98 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
     }
 }
 
+// Windowed form with a compile-time half width K (VarNet: K = 9 of 31 centres):
+// the per-thread sums live in shared memory rows padded by K on both sides
+// ([nw + 2K][thread]), so the 2K + 1 read-modify-writes of an element need no
+// bounds checks, and they are issued as independent loads, FMAs and stores
+// (distinct rows) instead of one serialised load-add-store per centre.
+template<int K>
+__global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, const cfloat* __restrict__ dy,
+                                                   const cfloat* __restrict__ z, const float* __restrict__ mu,
+                                                   RbfGeom g, int nchunk, cfloat* __restrict__ dz,
+                                                   const cfloat* __restrict__ w)
+{
+    constexpr int NW2 = 2 * K + 1;
+    __shared__ float smu[kMaxW];
+    __shared__ float swf[kMaxW + 2 * K]; // weights, zero outside [0, nw)
+    __shared__ double red[kMaxW][kT / 32];
+    extern __shared__ float sacc[];    // [nw + 2K][kT]
+    const long f = blockIdx.y;
+    for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
+        smu[j] = mu[j];
+    for (int j = threadIdx.x; j < g.nw + 2 * K; j += blockDim.x)
+        swf[j] = (dz && j >= K && j < g.nw + K) ? w[f + (j - K) * g.nf].x : 0.f;
+    for (int j = 0; j < g.nw + 2 * K; j++)
+        sacc[j * kT + threadIdx.x] = 0.f;
+    __syncthreads();
+    const float inv_s2 = 1.f / (g.sigma * g.sigma);
+    const float k2 = 1.4426950408889634f / (2.f * g.sigma * g.sigma);
+    const float dm = g.dmu;
+    const long total = g.inner * g.outer;
+    const long begin = long(blockIdx.x) * kChunk, end = min(total, begin + kChunk);
+    long ii = (begin + threadIdx.x) % g.inner, o = (begin + threadIdx.x) / g.inner;
+    const long dii = long(kT) % g.inner, dob = long(kT) / g.inner;
+    for (long t = begin + threadIdx.x; t < end; t += kT) {
+        const long idx = ii + g.inner * (f + g.nf * o);
+        ii += dii;
+        o += dob;
+        if (ii >= g.inner) {
+            ii -= g.inner;
+            o++;
+        }
+        const float zk = z[idx].x, gv = dy[idx].x;
+        // basis values around the nearest centre jc (rbf_visit_k), position k <-> j = jc - K + k;
+        // positions outside [0, nw) are zeroed (their recurrence values may overflow)
+        const float tt = rintf((zk - g.mu0) * g.inv_dmu);
+        const int jc = int(fminf(fmaxf(tt, 0.f), float(g.nw - 1)));
+        const float dc = zk - smu[jc];
+        float ew[NW2];
+        ew[K] = exp2f(-(dc * dc) * k2);
+        float U = exp2f(k2 * dm * (2.f * dc - dm)), D = exp2f(-k2 * dm * (2.f * dc + dm));
+        float eu = ew[K], ed = ew[K];
+#pragma unroll
+        for (int k = 1; k <= K; k++) {
+            eu *= U;
+            U *= g.q;
+            ed *= D;
+            D *= g.q;
+            ew[K + k] = jc + k < g.nw ? eu : 0.f;
+            ew[K - k] = jc - k >= 0 ? ed : 0.f;
+        }
+        float* ab = sacc + jc * kT + threadIdx.x; // padded row jc - K + k + K = jc + k
+        float cur[NW2];
+#pragma unroll
+        for (int k = 0; k < NW2; k++)
+            cur[k] = ab[k * kT];
+#pragma unroll
+        for (int k = 0; k < NW2; k++)
+            ab[k * kT] = fmaf(ew[k], gv, cur[k]);
+        if (dz) {
+            float d = 0.f;
+#pragma unroll
+            for (int k = 0; k < NW2; k++)
+                d = fmaf(swf[jc + k] * ew[k], -fmaf(-float(k - K), dm, dc) * inv_s2, d);
+            dz[idx] = float2{d * gv, 0.f};
+        }
+    }
+    __syncthreads(); // (own column only, but keep the reduction below ordered)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = 0; j < g.nw; j++) {
+        double v = double(sacc[(j + K) * kT + threadIdx.x]);
+        for (int o2 = 16; o2 > 0; o2 >>= 1)
+            v += __shfl_xor_sync(0xffffffffu, v, o2);
+        if (lane == 0)
+            red[j][warp] = v;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < g.nw; j += blockDim.x) {
+        double s = 0;
+        for (int ww = 0; ww < kT / 32; ww++)
+            s += red[j][ww];
+        part[(f * g.nw + j) * nchunk + blockIdx.x] = s;
+    }
+}
+
 __global__ void k_rbf_wfinal(cfloat* dw, const double* part, RbfGeom g, int nchunk)
 {
     const long n = g.nf * g.nw;
@@ -208,13 +340,15 @@ void rbf_set_window(RbfGeom& g, const std::vector<float>& mu)
             return; // not evenly spaced
     // skipped centres lie >= (K + 1/2) dmu - (rounding slack) from z; 8.5 sigma
     // puts their basis values below exp(-36) = 2^-52 of the nearest one's
-    const int K = int(std::ceil(8.5 * g.sigma / dmu + 0.5));
+    const int K = int(std::ceil(8.5 * g.sigma / dmu + 0.5 - 1e-6)); // sigma = spacing: K = 9 (not 10 on rounding)
     const int win = 2 * K + 1;
     if (win >= n)
         return;
     g.win = win;
     g.mu0 = mu[0];
     g.inv_dmu = float(1.0 / dmu);
+    g.dmu = float(dmu);
+    g.q = float(std::exp(-dmu * dmu / (double(g.sigma) * g.sigma)));
 }
 
 void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
@@ -258,6 +392,24 @@ size_t rbf_wgrad_smem(const RbfGeom& g)
     return bytes;
 }
 
+// the K = 9 windowed weight-gradient kernel, or false when the geometry needs the generic one
+bool launch_wgrad_w9(double* part, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g, int nchunk,
+                     cfloat* dz, const cfloat* w)
+{
+    if (g.win != 19)
+        return false;
+    const size_t bytes = sizeof(float) * kT * (g.nw + 18);
+    static size_t granted = 48 * 1024;
+    if (bytes > granted) {
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<9>),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+        granted = bytes;
+    }
+    k_rbf_wgrad_w<9><<<dim3(nchunk, unsigned(g.nf)), kT, bytes, ctx().stream>>>(part, dy, z, mu, g, nchunk, dz, w);
+    KERNEL_CHECK();
+    return true;
+}
+
 void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g)
 {
     auto& c = ctx();
@@ -265,9 +417,11 @@ void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* m
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
-    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
-        part, dy, z, mu, g, nchunk, nullptr, nullptr);
-    KERNEL_CHECK();
+    if (!launch_wgrad_w9(part, dy, z, mu, g, nchunk, nullptr, nullptr)) {
+        k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
+            part, dy, z, mu, g, nchunk, nullptr, nullptr);
+        KERNEL_CHECK();
+    }
     k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
@@ -281,9 +435,11 @@ void rbf_adjoint_zw(cfloat* dz, cfloat* dw, const cfloat* dy, const cfloat* z, c
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
-    k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
-        part, dy, z, mu, g, nchunk, dz, w);
-    KERNEL_CHECK();
+    if (!launch_wgrad_w9(part, dy, z, mu, g, nchunk, dz, w)) {
+        k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
+            part, dy, z, mu, g, nchunk, dz, w);
+        KERNEL_CHECK();
+    }
     k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
