@@ -757,6 +757,10 @@ CUtensorMap vn_map(const cfloat* base, int X, int Y, long planes, int bx, int bp
 
 // real flops of one 11 x 11 pass: 2 per real MAC
 double vn_flops(const ConvGeom& g) { return 2.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * g.KX * g.KY; }
+// algorithmic HBM bytes (complex CANON arrays, 8 B per element): the thin side
+// (2 channels) makes these layers memory-bound (~55 flop/B against a TF32 ridge
+// of ~110), so the roofline row is bytes; the flops row is kept (tag suffix _tf)
+double vn_bytes(const ConvGeom& g) { return 8.0 * double(g.X) * g.Y * g.B * (g.Cin + g.Cout); }
 
 } // namespace
 
@@ -782,7 +786,8 @@ void conv_vn_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvG
     float2* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float2) * n * grid, c.stream));
     {
-        ProfScope prof("conv_vn_bwd_weight", vn_flops(g));
+        ProfScope prof("conv_vn_bwd_weight", vn_bytes(g));
+        ProfScope prof_tf("conv_vn_bwd_weight_tf", vn_flops(g));
         k_vn_wgrad<<<grid, V_THREADS, L.total, c.stream>>>(tx, td, part, X, Y, B, F, imag);
         KERNEL_CHECK();
     }
@@ -802,7 +807,8 @@ void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGe
         const int grid = int(std::min<long>(units, c.sm_count));
         CUDA_CHECK(cudaFuncSetAttribute(k_vn_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
         const CUtensorMap tm = vn_map(in, X, Y, 2L * B, 2 * VE_BOXPX, 2);
-        ProfScope prof("conv_vn_fwd", vn_flops(g));
+        ProfScope prof("conv_vn_fwd", vn_bytes(g));
+        ProfScope prof_tf("conv_vn_fwd_tf", vn_flops(g));
         k_vn_expand<<<grid, V_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
     } else {
         const VrSmem L(F, F8);
@@ -810,7 +816,8 @@ void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGe
         const int grid = int(std::min<long>(units, c.sm_count));
         CUDA_CHECK(cudaFuncSetAttribute(k_vn_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize, L.total));
         const CUtensorMap tm = vn_map(in, X, Y, long(F) * B, 256, F);
-        ProfScope prof("conv_vn_bwd_data", vn_flops(g));
+        ProfScope prof("conv_vn_bwd_data", vn_bytes(g));
+        ProfScope prof_tf("conv_vn_bwd_data_tf", vn_flops(g));
         k_vn_reduce<<<grid, V_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
     }
     KERNEL_CHECK();

@@ -3,6 +3,7 @@
 // acting on Re z, with z viewed as [inner][filter][outer] and w as [nf, nw].
 // Weight gradients reduce per (filter, basis) with fixed-order partials.
 #include "kernels.h"
+#include "profile.h"
 
 #include <algorithm>
 #include <cmath>
@@ -355,6 +356,8 @@ void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, c
 {
     if (g.nw > kMaxW)
         throw ConfigError("rbf: more than 64 basis functions not supported on device");
+    // algorithmic bytes: z in, y out (complex, 8 B each)
+    ProfScope prof("rbf", 16.0 * double(g.inner) * g.nf * g.outer);
     k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(y, z, w, nullptr, mu, g, 0);
     KERNEL_CHECK();
 }
@@ -431,6 +434,8 @@ void rbf_adjoint_zw(cfloat* dz, cfloat* dw, const cfloat* dy, const cfloat* z, c
                     const RbfGeom& g)
 {
     auto& c = ctx();
+    // algorithmic bytes: z and dy in, dz out (complex, 8 B each)
+    ProfScope prof("rbf_adjoint", 24.0 * double(g.inner) * g.nf * g.outer);
     const long total = g.inner * g.outer;
     const int nchunk = int(std::max(1L, (total + kChunk - 1) / kChunk));
     double* part;
