@@ -102,7 +102,9 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
     constexpr int N = 128, NP = TT_X * TT_Y, NCH = CIN2 / 32;
     using S = TtSmem;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* halo = smem + S::HALO_OFF;
     uint8_t* wst = smem + S::W_OFF;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
@@ -361,7 +363,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     using S = TcPairSmem<N>;
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* halo = smem + S::HALO_OFF;
     uint8_t* bst = smem + S::B_OFF;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
@@ -549,7 +553,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     constexpr int TMEM_COLS = 3 * N <= 128 ? 128 : (3 * N <= 256 ? 256 : 512);
     constexpr int NDB = N / 32;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::BAR_OFF);
     uint64_t* full = bars;
     uint64_t* empty = bars + WG_STAGES;

@@ -65,7 +65,9 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
                 float* __restrict__ z, long npix)
 {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* abuf = smem + TpSmem::A_OFF;
     uint8_t* bbuf = smem + TpSmem::B_OFF;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TpSmem::BAR_OFF);
@@ -267,7 +269,9 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
                      const TeBn be)
 {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* bbuf = smem + TeSmem::B_OFF;
     uint8_t* abuf = smem + TeSmem::A_OFF;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + TeSmem::BAR_OFF);

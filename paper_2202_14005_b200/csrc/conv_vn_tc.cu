@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(V_THREADS, 1)
         return;
     const VeSmem L(F8);
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     float* wb = reinterpret_cast<float*>(smem);
     uint8_t* ring = smem + L.ring_off;
     const float* raw = reinterpret_cast<const float*>(smem + L.raw_off);
@@ -305,7 +307,9 @@ __global__ void __launch_bounds__(V_THREADS, 1)
     const VrSmem L(F, F8);
     constexpr int NB = 12 * VR_SLOT; // B rows: (ky 0..11, kx 0..11, c)
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     float* wb = reinterpret_cast<float*>(smem + L.wb_off);
     uint8_t* ring = smem + L.ring_off;
     const float* raw = reinterpret_cast<const float*>(smem + L.raw_off);
@@ -529,7 +533,9 @@ __global__ void __launch_bounds__(V_THREADS, 1)
         return;
     const VwSmem L(F);
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from the shared array (not an integer round trip), so
+    // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (sm100::smem_u32(smem_raw) & 1023u)) & 1023u);
     float* xb = reinterpret_cast<float*>(smem + L.xb_off);
     uint8_t* bring = smem + L.b_off;
     const float* xr = reinterpret_cast<const float*>(smem + L.xr_off);
