@@ -1,4 +1,7 @@
-"""GPU parity of the persistent mask-pruned A^H A kernel (csrc/sense_rank.cuh)
+"""GPU parity of the persistent mask-pruned A^H A kernels -- the warp-specialised
+k_normal_ws (csrc/sense_ws.cuh, default) and the round-1 k_normal_rank
+(csrc/sense_rank.cuh, option `sense_ws` = 0), each with contiguous unit ranges
+and with whole strips round robin (option `rank_rr`, used for 32-B strips) --
 against the reference CPU implementation (oracle/_ref).
 
 Covers every row mode of the pruned stage B (identity, rank-1 terms added to
@@ -22,11 +25,16 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-@pytest.fixture
-def rank_opts(gpu):
+@pytest.fixture(params=[(1, 1), (1, 0), (0, 1)], ids=["ws", "ws-contiguous", "rank"])
+def rank_opts(gpu, request):
+    ws, rr = request.param
+    gpu.check(gpu.so.mdnn_set_option(b"sense_ws", ws))
+    gpu.check(gpu.so.mdnn_set_option(b"rank_rr", rr))
     yield gpu
     gpu.check(gpu.so.mdnn_set_option(b"sense_rank", 1))
     gpu.check(gpu.so.mdnn_set_option(b"sense_rank_ctas", 0))
+    gpu.check(gpu.so.mdnn_set_option(b"sense_ws", 1))
+    gpu.check(gpu.so.mdnn_set_option(b"rank_rr", 1))
 
 
 def _normal(lib, cm, pat, x, lam=0.05):
