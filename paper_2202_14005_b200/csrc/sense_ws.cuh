@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                 const int xx = a_xb * W + w;
                 const bool colok = active && xx < a.X;
                 const long img_base = xx + a.X * Y * long(a_b);
-                WS_WAIT(2, &bar_xfull, uint32_t(nseg & 1));
+                WS_WAIT(0, &bar_xfull, uint32_t(nseg & 1));
                 nseg++;
                 // padding threads and columns past X read zeros from the TMA fill (j clamped rows are valid)
 #pragma unroll
@@ -665,8 +665,9 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                         o = cx2::add(o, cx2::mul(xv, lam));
                     if (active && xx < a.X) {
                         dst[img_base + a.X * y] = o;
-                        part.x += double(xv.x) * o.x + double(xv.y) * o.y;
-                        part.y += double(xv.y) * o.x - double(xv.x) * o.y;
+                        // Re <p, Ap> only (CG reads the real part; mode 0 needs none)
+                        if (a.mode == 1)
+                            part.x += double(xv.x) * o.x + double(xv.y) * o.y;
                     }
                     acc[q] = float2{0.f, 0.f};
                 }
