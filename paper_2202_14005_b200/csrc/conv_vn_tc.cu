@@ -650,10 +650,18 @@ __global__ void __launch_bounds__(V_THREADS, 1)
             mbar_wait(&bempty[bs], bph ^ 1);
             const float* raw = dr + ds * (L.dr_bytes / 4);
             float4* bo = reinterpret_cast<float4*>(bring + bs * VW_BB);
-            for (int e = t; e < (VW_PC / 4) * F; e += 128) {
-                const int pq = e / F, f = e - pq * F;
-                const float* src = raw + f * 2 * VW_PC + 8 * pq;
-                bo[pq * 32 + f] = make_float4(to_tf32(src[0]), to_tf32(src[2]), to_tf32(src[4]), to_tf32(src[6]));
+            // lanes = 8 channels x 4 pixel quads: the raw rows (pitch 2 VW_PC floats, a
+            // multiple of the bank count) put every channel of one quad in the same bank,
+            // so 8 channels per quad bound the read conflicts at 8-way (24-way with all
+            // channels of a quad in one warp), and the B-slot writes stay conflict-free
+            const int fgroups = (F + 7) >> 3;
+            for (int e = t; e < (VW_PC / 4) * 8 * fgroups; e += 128) {
+                const int ln = e & 31, k = e >> 5;
+                const int f = 8 * (k % fgroups) + (ln & 7), pq = 4 * (k / fgroups) + (ln >> 3);
+                if (f < F) {
+                    const float* src = raw + f * 2 * VW_PC + 8 * pq;
+                    bo[pq * 32 + f] = make_float4(to_tf32(src[0]), to_tf32(src[2]), to_tf32(src[4]), to_tf32(src[6]));
+                }
             }
             mbar_arrive(&dempty[ds]);
             fence_proxy_async_smem();
