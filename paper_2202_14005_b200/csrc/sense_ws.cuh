@@ -634,9 +634,10 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
 #pragma unroll
             for (int q = 0; q < N1; q++)
                 cv[q] = csp[N2 * W * q];
+            // padding threads (j clamped) read nothing another thread writes
 #pragma unroll
             for (int m = 0; m < N1; m++)
-                v[m] = S[m * RP];
+                v[m] = active ? S[m * RP] : float2{0.f, 0.f};
             cx2::dft<N1, +1>(v);
 #pragma unroll
             for (int q = 0; q < N1; q++)
@@ -659,7 +660,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
 #pragma unroll
                 for (int q = 0; q < N1; q++) {
                     const int y = j + N2 * q;
-                    const float2 xv = from_stash ? stash[y * W + w] : xr[q];
+                    const float2 xv = from_stash ? (active ? stash[y * W + w] : float2{0.f, 0.f}) : xr[q];
                     float2 o = cx2::scale(acc[q], invN1);
                     if (first)
                         o = cx2::add(o, cx2::mul(xv, lam));
