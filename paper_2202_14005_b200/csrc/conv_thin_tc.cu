@@ -263,6 +263,9 @@ struct TeBn {
     double* part = nullptr;   // [blk][128][3]
 };
 
+// EPI: 0 = store only, 1 = + forward BN statistics, 2 = + BN-backward partials
+// (compile-time, as in conv_tc.cu: each form carries only its own registers)
+template<int EPI>
 __global__ void __launch_bounds__(TE_THREADS, 1)
     k_thin_expand_tc(const __grid_constant__ CUtensorMap tm_out, const float2* __restrict__ thin,
                      const float* __restrict__ ue, int X, int Y, long npix, int ox, int oy, double* __restrict__ stats,
@@ -396,7 +399,7 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
         const int bc = n & 63, comp = n >> 6;
         float2 bmu{0.f, 0.f}, bg{0.f, 0.f}, bb{0.f, 0.f};
         float bs = 0.f;
-        if (be.part) {
+        if (EPI == 2) {
             bmu = be.mu[bc];
             bs = be.istd[bc];
             bg = be.gamma[bc];
@@ -409,12 +412,14 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
             mbar_wait(&tmem_full[st], ph);
             tc_fence_after();
             const uint32_t acc = tmem_base + st * TE_P + (uint32_t(lg * 32) << 16);
+            float t0 = 0.f, t1 = 0.f, t2 = 0.f; // BN-backward sums of the tile (fp32, then double)
 #pragma unroll 1
             for (int jc = rep; jc < TE_P / 16; jc += TE_EPI / 4) {
+                const long p0 = tile * TE_P + jc * 16;
+                const int nv = npix - p0 < 16 ? int(npix - p0) : 16;
                 float v[16];
                 tmem_ld16(acc + jc * 16, v);
                 tmem_ld_wait();
-                const long p0 = tile * TE_P + jc * 16;
                 if (p0 >= npix)
                     continue;
                 // this buffer's previous store has finished reading shared memory
@@ -432,23 +437,26 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
                     bulk_commit();
                 }
                 sb ^= 1;
-                const int nv = npix - p0 < 16 ? int(npix - p0) : 16;
-                // shifted by the chunk's first value, re-centred in double (see conv_tc.cu)
-                const float sh = v[0];
-                float fs = 0.f, fq = 0.f;
+                if (EPI == 1) {
+                    // shifted by the chunk's first value, re-centred in double (see conv_tc.cu)
+                    const float sh = v[0];
+                    float fs = 0.f, fq = 0.f;
 #pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    if (j < nv) {
-                        const float d = v[j] - sh;
-                        fs += d;
-                        fq = fmaf(d, d, fq);
+                    for (int j = 0; j < 16; j++) {
+                        if (j < nv) {
+                            const float d = v[j] - sh;
+                            fs += d;
+                            fq = fmaf(d, d, fq);
+                        }
                     }
+                    s_acc += double(nv) * sh + fs;
+                    q_acc += double(sh) * (double(nv) * sh + 2.0 * fs) + fq;
                 }
-                s_acc += double(nv) * sh + fs;
-                q_acc += double(sh) * (double(nv) * sh + 2.0 * fs) + fq;
-                if (be.part) {
-                    const float* xp = be.x + p0 * 128 + bc;
+                if (EPI == 2) {
+                    // BN input of the chunk (after the store is staged: the 672-thread CTA
+                    // caps registers at 80, and holding x across the staging spilled)
                     float xr[16], xi[16];
+                    const float* xp = be.x + p0 * 128 + bc;
 #pragma unroll
                     for (int j = 0; j < 16; j++) {
                         xr[j] = j < nv ? __ldg(xp + j * 128) : 0.f;
@@ -466,23 +474,28 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
                         f1 = fmaf(ge, comp ? hi : hr, f1);
                         f2 = fmaf(ge, comp ? hr : -hi, f2);
                     }
-                    r0 += f0;
-                    r1 += f1;
-                    r2 += f2;
+                    t0 += f0;
+                    t1 += f1;
+                    t2 += f2;
                 }
             }
             tc_fence_before();
             mbar_arrive(&tmem_empty[st]);
+            if (EPI == 2) {
+                r0 += t0;
+                r1 += t1;
+                r2 += t2;
+            }
         }
         if (lane == 0)
             bulk_wait<0>(); // stores complete before the kernel's writes are consumed
-        if (be.part) {
+        if (EPI == 2) {
             const size_t slot = size_t(blockIdx.x) * (TE_EPI / 4) + rep;
             be.part[(slot * 128 + n) * 3] = r0;
             be.part[(slot * 128 + n) * 3 + 1] = r1;
             be.part[(slot * 128 + n) * 3 + 2] = r2;
         }
-        if (stats) {
+        if (EPI == 1) {
             const size_t slot = size_t(blockIdx.x) * (TE_EPI / 4) + rep;
             stats[(slot * 128 + n) * 2] = s_acc;
             stats[(slot * 128 + n) * 2 + 1] = q_acc;
@@ -560,16 +573,6 @@ bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, lon
     CUDA_CHECK(cudaMallocAsync(&ue, sizeof(float) * 128 * 64, c.stream));
     k_pack_thin_expand<<<32, 256, 0, c.stream>>>(ue, U, F, KK);
     KERNEL_CHECK();
-    static std::mutex mu;
-    static std::map<int, bool> done;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (!done[c.device]) {
-            CUDA_CHECK(cudaFuncSetAttribute(k_thin_expand_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            TeSmem::TOTAL));
-            done[c.device] = true;
-        }
-    }
     const long ntiles = (npix + TE_P - 1) / TE_P;
     const int grid = int(std::min<long>(ntiles, c.sm_count));
     CUtensorMap tmo;
@@ -587,8 +590,18 @@ bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, lon
     TeBn be{};
     if (bn)
         be = TeBn{bnb->x, bnb->mu, bnb->istd, bnb->gamma, bnb->beta, bpart};
-    k_thin_expand_tc<<<grid, TE_THREADS, TeSmem::TOTAL, c.stream>>>(tmo, thin, ue, int(X), int(Y), npix, ox, oy,
-                                                                    stats, be);
+    auto kern = bn ? k_thin_expand_tc<2> : stats ? k_thin_expand_tc<1> : k_thin_expand_tc<0>;
+    {
+        static std::mutex mu;
+        static std::map<int, bool> done;
+        const int e = bn ? 2 : stats ? 1 : 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done[c.device * 4 + e]) {
+            CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TeSmem::TOTAL));
+            done[c.device * 4 + e] = true;
+        }
+    }
+    kern<<<grid, TE_THREADS, TeSmem::TOTAL, c.stream>>>(tmo, thin, ue, int(X), int(Y), npix, ox, oy, stats, be);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(ue, c.stream));
     if (stats && stats_blocks)

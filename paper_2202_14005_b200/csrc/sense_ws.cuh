@@ -191,6 +191,9 @@ __device__ __forceinline__ void dft(float2 (&v)[R])
 }
 } // namespace cx2
 
+#ifndef WS_NTW
+#define WS_NTW 12 // warps per CTA (at least)
+#endif
 template<int N1, int N2>
 struct WsCfg {
     using RC = RankCfg<N1, N2>; // plan record layout (TMAX, N2P) and TMA boxes
@@ -204,7 +207,11 @@ struct WsCfg {
     static constexpr int BQ = N2 > 24 ? 4 : 2;
     static constexpr int jq(int v) { return (v * W) % 16 == 0 ? v : jq(v + 2); }
     static constexpr int JQ = jq((((N2P + BQ - 1) / BQ) + 1) & ~1); // parts start 16-float2 aligned
-    static constexpr int NT_B = std::min(((BQ * N1 * W + 31) / 32) * 32, 192);
+    // 12 warps in all: ptxas sizes the register budget for a multiple of 4 warps
+    // (13 warps got the 16-warp cap of 128 registers and spilled)
+    // one pass over the (row, column, part) items of the reference pattern family
+    // (12 rows x W x BQ <= 192); with 13 warps ptxas budgets registers for 16 (128)
+    static constexpr int NT_B = 32 * (WS_NTW - NT_AC / 32 - 1) >= 192 ? 32 * (WS_NTW - NT_AC / 32 - 1) : 192;
     static constexpr int NT = NT_AC + NT_B + 32;             // + TMA producer warp
     static constexpr int SLOT = Y * W;                        // float2 per coil slice / stash
     // S layout: element (row m, j, column w) at m * RP + SOFF(j) + w; j-part p
@@ -217,7 +224,10 @@ struct WsCfg {
     static constexpr int TTW = TMAX * N2P + 8;                // twiddle rows + zero pad (last part's reads)
     static constexpr size_t STATIC_EST = 4096;                // plan, barriers, reductions
     // 2 S buffers, stash, 2 staging strips (x or r, and p_prev), twiddle rows
-    static constexpr size_t FIXED = sizeof(float2) * (size_t(2) * SBUF + 3 * size_t(SLOT) + size_t(TTW));
+    // (+ 16 float2 = 128 B: the stash's extra row Y, read only by padding threads;
+    // keeps the TMA-written staging buffers 128-B aligned)
+    static constexpr int STASH_PAD = 16;
+    static constexpr size_t FIXED = sizeof(float2) * (size_t(2) * SBUF + 3 * size_t(SLOT) + STASH_PAD + size_t(TTW));
     static constexpr size_t SMEM_MAX = 227 * 1024;
     static constexpr int NSLOT_FIT = int((SMEM_MAX - STATIC_EST - FIXED) / (sizeof(float2) * SLOT));
     static constexpr int NSLOT = NSLOT_FIT > 6 ? 6 : NSLOT_FIT;
@@ -256,7 +266,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
     float2* ring = ws_smem;
     float2* Sb = ring + size_t(NSLOT) * SLOT;
     float2* stash = Sb + 2 * SBUF;
-    float2* stg = stash + SLOT; // [2][SLOT]: strip of x (or r) and of p_prev, TMA-staged one segment ahead
+    float2* stg = stash + SLOT + Cfg::STASH_PAD; // [2][SLOT]: strip of x (or r) and of p_prev, TMA-staged one segment ahead
     float2* ttw = stg + 2 * SLOT;
     __shared__ __align__(8) uint64_t bar_full[NSLOT], bar_empty[NSLOT], bar_sfull[2], bar_sdone[2], bar_xfull,
         bar_xempty;
@@ -627,17 +637,18 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
 #ifdef WS_PROF
             long long t0 = clock64();
 #endif
-            const float2* S = Sb + (i & 1) * SBUF + Cfg::SOFF(j) + w;
+            // padding threads (j0 >= N2; only N2 = 23, where j0 = N2 < N2P) read the
+            // never-written pad column instead of their active twin's row (racecheck)
+            const float2* S = Sb + (i & 1) * SBUF + Cfg::SOFF(j0) + w;
             const int slot = i % NSLOT;
             const float2* csp = ring + size_t(slot) * SLOT + j * W + w;
             float2 v[N1], cv[N1];
 #pragma unroll
             for (int q = 0; q < N1; q++)
                 cv[q] = csp[N2 * W * q];
-            // padding threads (j clamped) read nothing another thread writes
 #pragma unroll
             for (int m = 0; m < N1; m++)
-                v[m] = active ? S[m * RP] : float2{0.f, 0.f};
+                v[m] = S[m * RP];
             cx2::dft<N1, +1>(v);
 #pragma unroll
             for (int q = 0; q < N1; q++)
@@ -657,18 +668,20 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
                 const int b = from_stash ? prev_b : cur_b, xx = (from_stash ? prev_xb : cur_xb) * W + w;
                 const long img_base = xx + a.X * Y * long(b);
                 cfloat* dst = rank_plane_dst(a, s, blockIdx.x);
+                // stash rows: y = j + N2 q; padding threads read the extra row Y (never
+                // written) instead of rows their active twins rewrite at the next open
+                const int sy0 = active ? j : Y, sdy = active ? N2 : 0;
 #pragma unroll
                 for (int q = 0; q < N1; q++) {
                     const int y = j + N2 * q;
-                    const float2 xv = from_stash ? (active ? stash[y * W + w] : float2{0.f, 0.f}) : xr[q];
+                    const float2 xv = from_stash ? stash[(sy0 + sdy * q) * W + w] : xr[q];
                     float2 o = cx2::scale(acc[q], invN1);
                     if (first)
                         o = cx2::add(o, cx2::mul(xv, lam));
                     if (active && xx < a.X) {
                         dst[img_base + a.X * y] = o;
-                        // Re <p, Ap> only (CG reads the real part; mode 0 needs none)
-                        if (a.mode == 1)
-                            part.x += double(xv.x) * o.x + double(xv.y) * o.y;
+                        // Re <p, Ap> only (CG reads the real part; mode 0 ignores it)
+                        part.x += double(xv.x) * o.x + double(xv.y) * o.y;
                     }
                     acc[q] = float2{0.f, 0.f};
                 }
