@@ -12,10 +12,12 @@ import sys
 
 # kernel-name regex -> (tag, kernels per tag launch)
 TAGS = [
-    (r"k_normal_rank", "sense_normal_y_cg"),
+    (r"k_normal_(rank|ws)", "sense_normal_y_cg"),
     (r"k_cg_update_r", "cg_update_rank"),
     (r"k_conv_tc_wgrad|k_wgrad_fold", "conv_tc_bwd_weight"),
-    (r"k_conv_tc(_t|_pair)?<", "conv_tc_fwd_or_bwd_data"),
+    (r"k_conv_tc_t<\d+, 2>", "conv_tc_bwd_data"),
+    (r"k_conv_tc_t<\d+, [01]>", "conv_tc_fwd"),
+    (r"k_conv_tc(_pair)?<", "conv_tc_fwd_or_bwd_data"),
     (r"k_stats|k_stats_final|k_apply\b", "bnblock_fwd"),
     (r"k_bwd_reduce|k_bwd_final|k_bwd_apply", "bnblock_bwd"),
     (r"k_thin_wgrad|k_thin_wsum", "conv_thin_bwd_weight"),
@@ -23,8 +25,9 @@ TAGS = [
     (r"k_fft_lines", "fft"),
 ]
 # launches of each tag per ncu capture are counted from its anchor kernel
-ANCHOR = {"sense_normal_y_cg": "k_normal_rank", "cg_update_rank": "k_cg_update_r",
-          "conv_tc_bwd_weight": "k_conv_tc_wgrad", "conv_tc_fwd_or_bwd_data": "k_conv_tc(_t|_pair)?<",
+ANCHOR = {"sense_normal_y_cg": "k_normal_(rank|ws)", "cg_update_rank": "k_cg_update_r",
+          "conv_tc_bwd_weight": "k_conv_tc_wgrad", "conv_tc_bwd_data": "k_conv_tc_t<\\d+, 2>",
+          "conv_tc_fwd": "k_conv_tc_t<\\d+, [01]>", "conv_tc_fwd_or_bwd_data": "k_conv_tc(_pair)?<",
           "bnblock_fwd": "k_apply", "bnblock_bwd": "k_bwd_apply", "conv_thin_bwd_weight": "k_thin_wgrad",
           "conv_thin_fwd_or_bwd_data": "k_thin_(expand|reduce)", "fft": "k_fft_lines"}
 
@@ -62,7 +65,7 @@ def main(path, out):
                  ("conv_thin_fwd_or_bwd_data", ("conv_thin_fwd", "conv_thin_bwd_data"))):
         if a in res:
             for t in b:
-                res[t] = res[a]
+                res.setdefault(t, res[a])
     json.dump({k: round(v) for k, v in sorted(res.items())}, open(out, "w"), indent=1)
     print(json.dumps({k: f"{v / 1e6:.1f} MB" for k, v in sorted(res.items())}, indent=1))
 
