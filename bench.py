@@ -444,7 +444,7 @@ def run_train_arm(args, ctx):
         step()
     ctx["barrier"]()
     lib.check(lib.so.mdnn_profile_enable(0))
-    roof = roofline(lib, ms_step * np_steps)
+    roof = roofline(lib, ms_step * np_steps, args.workload)
 
     # ---- end-to-end leg through the public C ABI (host inputs each step) ----
     e2e = None
@@ -541,7 +541,7 @@ def run_sense_arm(args, ctx):
                 solve()
             ctx["barrier"]()
             lib.check(lib.so.mdnn_profile_enable(0))
-            roof = roofline(lib, 0.0)
+            roof = roofline(lib, 0.0, "sense_c4")
         sweep.append(row)
     ms, gbs, clocks, dev, A = head
     X, Y, NC, B = SENSE_C4[0]
@@ -598,7 +598,7 @@ def _rand_inputs(X, Y, NC, B):
     return f(ph), f(cm), f(pat)
 
 
-def roofline(lib, step_ms_total):
+def roofline(lib, step_ms_total, workload="modl_c2"):
     """Per-kernel live timing (CUDA events around each tagged launch on the
     library stream, from the profiled pass): achieved = algorithmic work per
     launch / mean launch duration; share = kernel ms / (unprofiled step time x
@@ -624,7 +624,9 @@ def roofline(lib, step_ms_total):
             tf32_meas, tf32_meas_src = p["bf16_tflops"] / 2, "bf16_tflops / 2 (MEASURED_PEAKS.json)"
     traffic = {}
     try:
-        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+        # per-launch DRAM bytes of each tag from one ncu capture of THIS workload
+        # (tools/ncu_traffic.py); other workloads report traffic = null
+        with open(os.path.join(REPO, "profiles", f"ncu_traffic_{workload}.json")) as f:
             traffic = json.load(f)
     except Exception:
         pass
