@@ -50,6 +50,9 @@ using namespace sm100;
 
 constexpr int VK = 11, VP = 5;          // kernel extent, corner offset
 constexpr int V_THREADS = 320;          // 4 converter + 1 MMA + 4 epilogue + 1 TMA warps
+// k_vn_reduce: 4 more converter warps (10-13): its per-row conversion (F channels of 128
+// pixels -> the K-major A operand) was the critical path
+constexpr int VR_THREADS = V_THREADS + 128, VR_CONV = 256;
 constexpr int V_SMEM_MIN = 120 * 1024;  // one CTA per SM: the kernels own all 512 TMEM columns
 
 // ---- expand (2 -> F) --------------------------------------------------------------
@@ -298,7 +301,7 @@ struct VrSmem {
     }
 };
 
-__global__ void __launch_bounds__(V_THREADS, 1)
+__global__ void __launch_bounds__(VR_THREADS, 1)
     k_vn_reduce(const __grid_constant__ CUtensorMap tm_dy, float2* __restrict__ dx, const float2* __restrict__ w, int X,
                 int Y, int B, int F, int F8, const unsigned* __restrict__ imag)
 {
@@ -332,17 +335,17 @@ __global__ void __launch_bounds__(V_THREADS, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < VR_NS; i++) {
-            mbar_init(&full[i], 128);
+            mbar_init(&full[i], VR_CONV);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], 4);
         }
-        mbar_init(wb_full, 128);
+        mbar_init(wb_full, VR_CONV);
         for (int i = 0; i < VR_NR; i++) {
             mbar_init(&rfull[i], 1);
-            mbar_init(&rempty[i], 128);
+            mbar_init(&rempty[i], VR_CONV);
         }
         fence_barrier_init();
     }
@@ -370,9 +373,12 @@ __global__ void __launch_bounds__(V_THREADS, 1)
                 }
             }
         }
-    } else if (warp < 4) {
-        const int t = threadIdx.x;
-        for (int e = t; e < KG * NB * 4; e += 128) {
+    } else if (warp < 4 || warp >= 10) {
+        // converter ct: pixel t = ct % 128, channel groups [kg0, kg1) of half ct / 128
+        const int ct = warp < 4 ? int(threadIdx.x) : int(threadIdx.x) - V_THREADS + 128;
+        const int t = ct & 127, half = ct >> 7;
+        const int kgh = (KG + 1) / 2, kg0 = half * kgh, kg1 = min(KG, kg0 + kgh);
+        for (int e = ct; e < KG * NB * 4; e += VR_CONV) {
             const int kk = e & 3, n = (e >> 2) % NB, kg = (e >> 2) / NB;
             const int f = kg * 4 + kk, ky = n / VR_SLOT, rem = n - ky * VR_SLOT, kx = rem >> 1, c = rem & 1;
             float v = 0.f;
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(V_THREADS, 1)
                 mbar_wait(&empty[st], ph ^ 1);
                 const float* rw = raw + rs * (L.raw_bytes / 4) + 2 * t; // real part of pixel t, channel 0
                 float4* A = reinterpret_cast<float4*>(ring + st * L.a_bytes);
-                for (int kg = 0; kg < KG; kg++) {
+                for (int kg = kg0; kg < kg1; kg++) {
                     float q[4];
 #pragma unroll
                     for (int kk = 0; kk < 4; kk++) {
@@ -832,7 +838,7 @@ void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGe
         const CUtensorMap tm = vn_map(in, X, Y, long(F) * B, 256, F);
         ProfScope prof("conv_vn_bwd_data", vn_bytes(g));
         ProfScope prof_tf("conv_vn_bwd_data_tf", vn_flops(g));
-        k_vn_reduce<<<grid, V_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
+        k_vn_reduce<<<grid, VR_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
     }
     KERNEL_CHECK();
 }
