@@ -531,7 +531,7 @@ struct VwSmem {
     }
 };
 
-__global__ void __launch_bounds__(V_THREADS, 1)
+__global__ void __launch_bounds__(VR_THREADS, 1)
     k_vn_wgrad(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
                float2* __restrict__ part, int X, int Y, int B, int F, const unsigned* __restrict__ imag)
 {
@@ -564,18 +564,18 @@ __global__ void __launch_bounds__(V_THREADS, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < VW_NB; i++) {
-            mbar_init(&bfull[i], 128);
+            mbar_init(&bfull[i], VR_CONV);
             mbar_init(&bempty[i], 1);
         }
         for (int i = 0; i < VW_MD; i++)
             mbar_init(&mdone[i], 1);
         for (int i = 0; i < VW_NXR; i++) {
             mbar_init(&xfull[i], 1);
-            mbar_init(&xempty[i], 128);
+            mbar_init(&xempty[i], VR_CONV);
         }
         for (int i = 0; i < 2; i++) {
             mbar_init(&dfull[i], 1);
-            mbar_init(&dempty[i], 128);
+            mbar_init(&dempty[i], VR_CONV);
         }
         mbar_init(tfull, 1);
         fence_barrier_init();
@@ -613,10 +613,10 @@ __global__ void __launch_bounds__(V_THREADS, 1)
                 tma_load_3d(smem + L.dr_off + s * L.dr_bytes, &tm_dy, &dfull[s], 2 * p0, o, F * b);
             }
         }
-    } else if (warp < 4) {
-        // ---- converters
-        const int t = threadIdx.x;
-        for (int e = t; e < VW_NB * (VW_PC / 4) * (32 - F) * 4; e += 128) { // unused f rows stay zero
+    } else if (warp < 4 || warp >= 10) {
+        // ---- converters (8 warps: 0-3 and 10-13)
+        const int t = warp < 4 ? int(threadIdx.x) : int(threadIdx.x) - V_THREADS + 128;
+        for (int e = t; e < VW_NB * (VW_PC / 4) * (32 - F) * 4; e += VR_CONV) { // unused f rows stay zero
             const int per = (32 - F) * 4, sl = e / ((VW_PC / 4) * per), rem = e % ((VW_PC / 4) * per);
             const int pq = rem / per, fi = rem % per;
             reinterpret_cast<float*>(bring + sl * VW_BB)[(pq * 32 + F + fi / 4) * 4 + (fi & 3)] = 0.f;
@@ -627,7 +627,7 @@ __global__ void __launch_bounds__(V_THREADS, 1)
             mbar_wait(&xfull[s], ph);
             const float* raw = xr + s * (VW_XRAW / 4);
             const int j = r & (VW_SL - 1);
-            for (int e = t; e < VW_PQ * 32; e += 128) {
+            for (int e = t; e < VW_PQ * 32; e += VR_CONV) {
                 const int pq = e >> 5, q = e & 31, ss = q >> 3, c = (q >> 2) & 1, i = q & 3;
                 const float v = to_tf32(raw[c * 160 + 2 * (1 + 4 * pq + ss + i)]);
                 xb[(pq * 2 * VW_SL + j) * 32 + q] = v;
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(V_THREADS, 1)
             // so 8 channels per quad bound the read conflicts at 8-way (24-way with all
             // channels of a quad in one warp), and the B-slot writes stay conflict-free
             const int fgroups = (F + 7) >> 3;
-            for (int e = t; e < (VW_PC / 4) * 8 * fgroups; e += 128) {
+            for (int e = t; e < (VW_PC / 4) * 8 * fgroups; e += VR_CONV) {
                 const int ln = e & 31, k = e >> 5;
                 const int f = 8 * (k % fgroups) + (ln & 7), pq = 4 * (k / fgroups) + (ln >> 3);
                 if (f < F) {
@@ -808,7 +808,7 @@ void conv_vn_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvG
     {
         ProfScope prof("conv_vn_bwd_weight", vn_bytes(g));
         ProfScope prof_tf("conv_vn_bwd_weight_tf", vn_flops(g));
-        k_vn_wgrad<<<grid, V_THREADS, L.total, c.stream>>>(tx, td, part, X, Y, B, F, imag);
+        k_vn_wgrad<<<grid, VR_THREADS, L.total, c.stream>>>(tx, td, part, X, Y, B, F, imag);
         KERNEL_CHECK();
     }
     k_vn_fold<<<int((n + 255) / 256), 256, 0, c.stream>>>(dw, part, n, grid, imag);
