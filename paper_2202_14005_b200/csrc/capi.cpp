@@ -451,15 +451,14 @@ int mdnn_sense_normal(const mdnn_array* coils, const mdnn_array* pattern, float 
 {
     return guard([&] {
         DArray C = in_view(*coils), P = in_view(*pattern), X = in_view(*x);
-        check_binary(P);
         SenseGeom g = geom_from(C, P);
         if (X.dims != img_dims(g))
             throw ShapeError("linop normal: expected " + dims_to_string(img_dims(g)));
-        DArray lam = DArray::scalar(lambda);
         DArray out = out_target(*y, img_dims(g));
         if (out.data() == X.data())
             out = DArray(img_dims(g), false); // in-place call: keep x intact until the kernel is done
-        sense_normal(out.data(), X.data(), C.data(), P.data(), lam.data(), g);
+        // the binary-pattern check (check_binary) rides in the A^H A plan pass
+        sense_normal_value(out.data(), X.data(), C.data(), P.data(), lambda, g, true);
         out_arr_if_needed(out, *y);
         sync_and_check();
     });

@@ -88,6 +88,10 @@ void sense_adjoint(cfloat* x, const cfloat* y, const cfloat* coils, const cfloat
 // coils2 (nullable) = the maps of the adjoint coil combine when they differ
 void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloat* pattern, const cfloat* lam,
                   const SenseGeom& g, const cfloat* coils2 = nullptr);
+// A^H A + lambda with lambda by value (the C ABI's call); check_pattern: also raise
+// ERRF_PATTERN for a non-binary pattern (recon.hpp:67-77), folded into the plan pass
+void sense_normal_value(cfloat* out, const cfloat* x, const cfloat* coils, const cfloat* pattern, float lambda,
+                        const SenseGeom& g, bool check_pattern);
 // CG on S = A^H A + lam (recon.hpp:143-181), device-resident state and scalars.
 struct CgResult {
     long iterations;

@@ -1121,14 +1121,9 @@ public:
         require_forward();
         if (i == 0)
             return solve(dx, false);
-        DArray w;
-        if (fused_) {
-            // D_p S at x*: reuse the node's tangent formulas via a private forward
-            settle();
-        } else {
-            settle();
-        }
-        w = s_.derivative(0, i, dx);
+        // D_p S at x*: the inner node's tangent formulas after a private forward at x*
+        settle();
+        DArray w = s_.derivative(0, i, dx);
         DArray z = solve(w, false);
         DArray o(z.dims, false);
         launch_neg(o.data(), z.data(), o.size());

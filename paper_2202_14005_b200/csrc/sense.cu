@@ -576,37 +576,66 @@ void sense_adjoint(cfloat* x, const cfloat* y, const cfloat* coils, const cfloat
     launch_coil_adj(x, t.data(), coils, g);
 }
 
+// Rank-factorised A^H A + lambda (sense_rank.cuh / sense_ws.cuh), lambda from the
+// device (lam) or by value (lam == nullptr: lamv).  Launches: the plan pass (split
+// flags and, with check_pattern, the binary-pattern check folded in), the A^H A
+// kernel, and the plane merge only when strips are shared.  false: shape unsupported.
+static bool sense_normal_rank(cfloat* out, const cfloat* x, const cfloat* coils, const cfloat* pattern,
+                              const cfloat* lam, float2 lamv, const SenseGeom& g, bool check_pattern)
+{
+    if (!rank_enabled())
+        return false;
+    const RankPlan rp = rank_plan(g, coils);
+    if (!rp.ok)
+        return false;
+    const long n = g.X * g.Y * g.B;
+    DArray plane1;
+    if (rp.planes > 1)
+        plane1 = DArray(Dims{n * (rp.planes - 1)}, false);
+    DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
+    RankArgs a{};
+    a.out = out;
+    a.out1 = rp.planes > 1 ? plane1.data() : nullptr;
+    a.pstride = n;
+    a.x = x;
+    a.pattern = pattern;
+    a.lam = lam;
+    a.lamv = lamv;
+    a.ps = pat_strides(g);
+    a.mode = 0;
+    a.errflags = ctx().d_errflags;
+    a.check_pattern = check_pattern ? 1 : 0;
+    unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
+    launch_rank_plan(rp, a, g, pl);
+    a.check_pattern = 0;
+    launch_rank(rp, a, coils, g, pl);
+    if (rp.planes > 1) {
+        k_rank_merge<<<grid_for(n), 256, 0, ctx().stream>>>(out, plane1.data(), rank_split_flags(g, rp, pl),
+                                                            int(g.X), int(g.Y * g.B), int(g.Y), int(rp.nxb),
+                                                            rp.W == 8 ? 3 : 2, n);
+        KERNEL_CHECK();
+    }
+    return true;
+}
+
+void sense_normal_value(cfloat* out, const cfloat* x, const cfloat* coils, const cfloat* pattern, float lambda,
+                        const SenseGeom& g, bool check_pattern)
+{
+    if (sense_normal_rank(out, x, coils, pattern, nullptr, float2{lambda, 0.f}, g, check_pattern))
+        return;
+    if (check_pattern)
+        launch_check_binary(pattern, g.pat_x * g.pat_y * g.pat_c * g.pat_b);
+    DArray lam = DArray::scalar(lambda);
+    sense_normal(out, x, coils, pattern, lam.data(), g);
+}
+
 void sense_normal(cfloat* out, const cfloat* x, const cfloat* coils, const cfloat* pattern, const cfloat* lam,
                   const SenseGeom& g, const cfloat* coils2)
 {
     if (!coils2)
         coils2 = coils;
-    if (coils2 == coils && rank_enabled()) {
-        const RankPlan rp = rank_plan(g, coils);
-        if (rp.ok) {
-            const long n = g.X * g.Y * g.B;
-            DArray plane1(Dims{n * std::max(1, rp.planes - 1)}, false);
-            DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
-            RankArgs a{};
-            a.out = out;
-            a.out1 = plane1.data();
-            a.pstride = n;
-            a.x = x;
-            a.pattern = pattern;
-            a.lam = lam;
-            a.ps = pat_strides(g);
-            a.mode = 0;
-            a.errflags = ctx().d_errflags;
-            unsigned char* pl = reinterpret_cast<unsigned char*>(plans.data());
-            launch_rank_plan(rp, a, g, pl);
-            launch_rank(rp, a, coils, g, pl);
-            k_rank_merge<<<grid_for(n), 256, 0, ctx().stream>>>(out, plane1.data(), rank_split_flags(g, rp, pl),
-                                                                int(g.X), int(g.Y * g.B), int(g.Y), int(rp.nxb),
-                                                                rp.W == 8 ? 3 : 2, n);
-            KERNEL_CHECK();
-            return;
-        }
-    }
+    if (coils2 == coils && sense_normal_rank(out, x, coils, pattern, lam, float2{0.f, 0.f}, g, false))
+        return;
     if (fast_ok(g, coils, coils2)) {
         NormalArgs a{};
         a.out = out;

@@ -70,7 +70,8 @@ struct RankArgs {
     cfloat* p;            // mode 1: previous search direction
     cfloat* p_out;        // mode 1: new search direction (== x source at it 0)
     const cfloat* pattern;
-    const cfloat* lam;
+    const cfloat* lam;    // device lambda, or nullptr: lamv
+    float2 lamv;
     const float2* tw;     // exp(-2 pi i m / Y), m < Y
     long X, C, B;
     long nxb;             // strips per item
@@ -81,6 +82,9 @@ struct RankArgs {
     int mode, it;
     CgDev* cg;
     unsigned* errflags;
+    unsigned char* split; // k_rank_plan: split flag per strip (planes sharing it)
+    long strips;
+    int check_pattern;    // k_rank_plan: also run the binary-pattern check
 };
 
 // CTA owning unit u, for ranges [floor(U g / G), floor(U (g+1) / G))
@@ -194,6 +198,22 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT) k_rank_plan(RankArgs a, u
     unsigned char* rec = plans + RankPlanRec<N1, N2>::BYTES * blockIdx.x;
     rank_build_plan<N1, N2>(*reinterpret_cast<RankPlanSm<N1, N2>*>(rec), a, int(blockIdx.x),
                             reinterpret_cast<float2*>(rec + RankPlanRec<N1, N2>::PL), a.tw);
+    constexpr int NT = RankCfg<N1, N2>::NT;
+    if (a.check_pattern) {
+        // recon.hpp:67-77 on this item's pattern column (the plan reads exactly these
+        // values), folded into the plan pass: ERRF_PATTERN is raised at the call's sync
+        const long pb = long(blockIdx.x) * a.ps.sb;
+        bool bad = false;
+        for (int y = threadIdx.x; y < N1 * N2; y += NT) {
+            const float2 pv = a.pattern[y * a.ps.sy + pb];
+            bad |= pv.y != 0.f || (pv.x != 0.f && pv.x != 1.f);
+        }
+        if (__syncthreads_or(bad) && threadIdx.x == 0)
+            atomicOr(a.errflags, unsigned(ERRF_PATTERN));
+    }
+    // split flag of every strip (planes sharing it; 1 for round-robin strips)
+    for (long s = blockIdx.x * long(NT) + threadIdx.x; s < a.strips; s += long(gridDim.x) * NT)
+        a.split[s] = a.rr ? 1 : (unsigned char)rank_planes(s, a.C, a.units, a.G);
 }
 
 template<int N1, int N2>
@@ -250,7 +270,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
         for (int i = 0; i < n && i < 2; i++)
             issue(unit_of(i), i);
         s_beta = a.mode == 1 ? cg_prologue(a.cg, a.it, a.errflags) : 0.f;
-        s_lam = a.lam ? a.lam[0] : float2{0.f, 0.f};
+        s_lam = a.lam ? a.lam[0] : a.lamv;
     }
     if constexpr (N2P != N2) { // pad column of S stays zero (read by stage B, never by A/C)
         for (int e = tid; e < N1 * W; e += NT)
@@ -750,13 +770,6 @@ __global__ void __launch_bounds__(256) k_cg_x_sum(const CgDev* __restrict__ st, 
     }
 }
 
-// split flags of every strip (written once per plan buffer)
-__global__ void k_rank_split_flags(unsigned char* flags, long strips, long C, long U, long G, int rr)
-{
-    for (long s = blockIdx.x * long(blockDim.x) + threadIdx.x; s < strips; s += long(gridDim.x) * blockDim.x)
-        flags[s] = rr ? 1 : (unsigned char)rank_planes(s, C, U, G);
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 rank_encode_fn()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -917,9 +930,8 @@ void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsign
 {
     fill_rank_args(rp, a, g);
     const int items = int(g.pat_b > 1 ? g.pat_b : 1);
-    k_rank_split_flags<<<int(std::min<long>((rp.strips + 255) / 256, 64)), 256, 0, ctx().stream>>>(
-        plans + rank_plan_record_bytes(g, rp), rp.strips, g.C, rp.units, rp.G, rp.rr ? 1 : 0);
-    KERNEL_CHECK();
+    a.split = plans + rank_plan_record_bytes(g, rp);
+    a.strips = rp.strips;
 #define X_(YY, A1, A2)                                \
     if (rp.N1 == A1 && rp.N2 == A2) {                 \
         launch_rank_plan_t<A1, A2>(a, plans, items); \

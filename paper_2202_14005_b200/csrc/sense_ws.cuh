@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
         sm100::mbar_init(&bar_xempty, NT_AC);
         sm100::fence_barrier_init();
         s_beta = a.mode == 1 ? cg_prologue(a.cg, a.it, a.errflags) : 0.f;
-        s_lam = a.lam ? a.lam[0] : float2{0.f, 0.f};
+        s_lam = a.lam ? a.lam[0] : a.lamv;
     }
     __syncthreads();
     const float beta = s_beta;
