@@ -183,6 +183,10 @@ int mdnn_set_option(const char* key, long value)
             rank_rr_enable(value != 0);
         else if (k == "sense_ws")
             sense_ws_enable(value != 0);
+        else if (k == "cg_pdl")
+            cg_pdl_enable(value != 0);
+        else if (k == "cg_fuse")
+            cg_fuse_enable(int(value));
         else if (k == "sense_rank_ctas")
             sense_rank_ctas(value);
         else if (k == "cg_defer_x")

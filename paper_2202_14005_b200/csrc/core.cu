@@ -164,6 +164,8 @@ void sync_and_check()
             throw SolverError("cg: non-finite residual");
         if (flags & ERRF_NONFINITE_GRAD)
             throw SolverError("non-finite gradient");
+        if (flags & ERRF_GRID_BARRIER)
+            throw CudaError("A^H A: fused CG update grid barrier timed out (CTAs not co-resident)");
         throw SolverError("device error flags set");
     }
 }

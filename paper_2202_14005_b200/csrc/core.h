@@ -91,7 +91,8 @@ void allow_max_dyn_smem(const void* func);
 void reserve_pool(size_t bytes);
 void set_device(int dev);
 void sync_and_check();      // cudaStreamSynchronize + device error flags
-enum ErrFlag : unsigned { ERRF_CG_BREAKDOWN = 1u, ERRF_CG_NONFINITE = 2u, ERRF_NONFINITE_GRAD = 4u, ERRF_PATTERN = 8u };
+enum ErrFlag : unsigned { ERRF_CG_BREAKDOWN = 1u, ERRF_CG_NONFINITE = 2u, ERRF_NONFINITE_GRAD = 4u, ERRF_PATTERN = 8u,
+                        ERRF_GRID_BARRIER = 16u };
 
 struct Buffer {
     void* ptr = nullptr;

@@ -158,6 +158,8 @@ bool conv_bn_fuse();
 void sense_rank_enable(bool on);
 void sense_rank_ctas(long g);
 void sense_ws_enable(bool on);
+void cg_pdl_enable(bool on); // programmatic dependent launch in the CG loop
+void cg_fuse_enable(int mode); // CG r-update fused into the ws A^H A launch (grid barrier)
 void rank_rr_enable(bool on);
 void cg_defer_x_enable(bool on);
 bool rank_enabled();

@@ -120,6 +120,7 @@ struct CgDev {
     double rr_sum;    // <r, r> after the latest update
     unsigned cnt_pap; // CTA arrival counters (reset by the folding CTA)
     unsigned cnt_rr;
+    unsigned ws_bar;  // grid barrier of the fused CG update (k_normal_ws): G arrivals per iteration
     float* rs;        // [max_iter + 1]
     float* alpha;     // [max_iter]
     float* beta;      // [max_iter]
@@ -160,11 +161,10 @@ __device__ float cg_prologue(CgDev* st, int it, unsigned* errflags)
     return beta;
 }
 
-__device__ float cg_alpha(CgDev* st, int it, unsigned* errflags)
+__device__ float cg_alpha_sum(CgDev* st, int it, double s, unsigned* errflags)
 {
     if (st->done_at <= it)
         return 0.f;
-    double s = st->pap_sum;
     float pap = float(s);
     if (!isfinite(pap) || pap <= 0.f) {
         if (blockIdx.x == 0) {
@@ -178,6 +178,8 @@ __device__ float cg_alpha(CgDev* st, int it, unsigned* errflags)
         st->alpha[it] = a;
     return a;
 }
+
+__device__ float cg_alpha(CgDev* st, int it, unsigned* errflags) { return cg_alpha_sum(st, it, st->pap_sum, errflags); }
 
 __device__ __forceinline__ double2 warp_sum2(double2 v)
 {
@@ -782,9 +784,16 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
         const bool defer = max_iter <= 32 && g_cg_defer_x && n % 2 == 0;
         constexpr int UR = 2; // element pairs per thread in k_cg_update_r
         const long npair = n / 2;
-        const int n_updr = defer ? int(std::min<long>(3L * c.sm_count, (npair + 256L * UR - 1) / (256L * UR)))
+        // deferred update: as few latency rounds per thread as 4 co-resident
+        // 256-thread CTAs per SM allow, every round full (no partial last round)
+        const long upd_round = 256L * UR * 4 * c.sm_count;
+        const long upd_rounds = std::max(1L, (npair + upd_round - 1) / upd_round);
+        const int n_updr = defer ? int((npair + 256L * UR * upd_rounds - 1) / (256L * UR * upd_rounds))
                                  : int(std::min<long>(2L * c.sm_count, g.Y * g.B));
-        CgMem m = cg_alloc(max_iter, tol, rp.G, n_updr);
+        // fused update (ws kernel, deferred x): r -= alpha Ap after a grid barrier in
+        // the A^H A launch itself, one launch per iteration
+        const bool fuse = defer && rp.ws && g_cg_fuse != 0;
+        CgMem m = cg_alloc(max_iter, tol, rp.G, std::max(n_updr, rp.G));
         DArray r(Dims{n}, false), pb(Dims{(defer ? max_iter + 1 : 2) * n}, false),
             ap(Dims{n * std::max(2, rp.planes)}, false);
         DArray plans(Dims{long((rank_plan_bytes(g, rp) + 7) / 8)}, false);
@@ -813,13 +822,22 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             a.it = it;
             a.cg = m.st;
             a.errflags = c.d_errflags;
+            if (fuse) {
+                a.r_upd = r.data();
+                a.split = const_cast<unsigned char*>(rank_split_flags(g, rp, pl));
+                a.upd_rows = int(g.Y * g.B);
+                a.upd_Y = int(g.Y);
+                a.upd_wshift = rp.W == 8 ? 3 : 2;
+            }
             launch_rank(rp, a, coils, g, pl);
-            if (defer) {
+            if (fuse) {
+                // (the update ran in the A^H A launch)
+            } else if (defer) {
                 ProfScope prof("cg_update_rank", 8.0 * n * 4);
-                k_cg_update_r<UR><<<n_updr, 256, 0, c.stream>>>(m.st, it, r.data(), ap.data(), ap.data() + n,
-                                                               rank_split_flags(g, rp, pl), int(g.X), int(g.Y * g.B),
-                                                               int(g.Y), int(rp.nxb), rp.W == 8 ? 3 : 2, n,
-                                                               c.d_errflags);
+                launch_maybe_pdl(g_cg_pdl && rp.ws, k_cg_update_r<UR>, dim3(n_updr), dim3(256), 0, m.st, it, r.data(),
+                                 static_cast<const cfloat*>(ap.data()), static_cast<const cfloat*>(ap.data() + n),
+                                 rank_split_flags(g, rp, pl), int(g.X), int(g.Y * g.B), int(g.Y), int(rp.nxb),
+                                 rp.W == 8 ? 3 : 2, n, c.d_errflags);
             } else {
                 ProfScope prof("cg_update_rank", 8.0 * n * 7);
                 k_cg_update_rank<<<n_updr, 512, 0, c.stream>>>(m.st, it, x, r.data(), pdir(it + 1), ap.data(),
@@ -916,6 +934,8 @@ bool g_rank_enabled = true;
 void sense_rank_enable(bool on) { g_rank_enabled = on; }
 void sense_rank_ctas(long g) { g_rank_ctas = g; }
 void sense_ws_enable(bool on) { g_sense_ws = on; }
+void cg_pdl_enable(bool on) { g_cg_pdl = on; }
+void cg_fuse_enable(int mode) { g_cg_fuse = mode; }
 void rank_rr_enable(bool on) { g_rank_rr = on; }
 void cg_defer_x_enable(bool on) { g_cg_defer_x = on; }
 bool rank_enabled() { return g_rank_enabled; }

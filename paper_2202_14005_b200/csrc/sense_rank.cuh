@@ -29,6 +29,43 @@
 bool g_cg_defer_x = true; // CG: keep every p, update r only per iteration, sum x once
 long g_rank_ctas = 0; // 0: 2 per SM (tests force fewer to exercise split strips)
 bool g_sense_ws = true; // warp-specialised kernel (sense_ws.cuh), one CTA per SM
+// programmatic dependent launch of the CG loop's A^H A and update kernels: each
+// kernel's launch and CTA start overlap the previous kernel's tail
+bool g_cg_pdl = true;
+
+// fused CG update inside the ws kernel (one launch per CG iteration; grid barrier):
+// 0 off, 1 on, 2 on with a cooperative launch
+int g_cg_fuse = 1;
+
+// kernel launch on the library stream with optional programmatic serialisation
+// (pdl) and cooperative residency (coop: every CTA co-resident, or the launch fails)
+template<class... KArgs, class... Args>
+void launch_ex(bool pdl, bool coop, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx().stream;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (coop) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na++].val.cooperative = 1;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+template<class... KArgs, class... Args>
+void launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args)
+{
+    launch_ex(pdl, false, kern, grid, block, smem, std::forward<Args>(args)...);
+}
 bool g_rank_rr = true;  // whole strips round robin for 32-B strips (RankPlan::rr)
 
 constexpr int rank_nbox(int Y)
@@ -82,8 +119,10 @@ struct RankArgs {
     int mode, it;
     CgDev* cg;
     unsigned* errflags;
-    unsigned char* split; // k_rank_plan: split flag per strip (planes sharing it)
+    unsigned char* split; // k_rank_plan: split flag per strip (planes sharing it); ws fused update: read
     long strips;
+    cfloat* r_upd;        // mode 1, k_normal_ws: fused CG update r -= alpha Ap (cg_defer_x path), or nullptr
+    int upd_rows, upd_Y, upd_wshift;
     int check_pattern;    // k_rank_plan: also run the binary-pattern check
 };
 
@@ -671,44 +710,40 @@ __global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloa
 // search direction p_it kept, x = sum_it alpha_it p_it is formed once after the
 // loop by k_cg_x_sum in the same fma order as the per-iteration update (bitwise
 // identical), and each iteration streams 3 arrays instead of 5.
+// r -= alpha Ap (Ap = plane 0 + the planes of split strips) over the pixel pairs
+// i0, i0 + stride, ... ; returns this thread's <r, r> partial.  L2 loads: in the
+// fused form (k_normal_ws) Ap was stored by other CTAs of the same grid.
 template<int U>
-__global__ void __launch_bounds__(256) k_cg_update_r(CgDev* st, int it, cfloat* __restrict__ r,
-                                                     const cfloat* __restrict__ ap, const cfloat* __restrict__ ap1,
+__device__ __forceinline__ double2 cg_r_update_pairs(float al, cfloat* __restrict__ r, const cfloat* __restrict__ ap,
+                                                     const cfloat* __restrict__ ap1,
                                                      const unsigned char* __restrict__ split, int X, int rows, int Y,
-                                                     int nxb, int wshift, long pstride, unsigned* errflags)
+                                                     int nxb, int wshift, long pstride, int i0, int stride)
 {
-    __shared__ float s_alpha;
-    if (threadIdx.x == 0)
-        s_alpha = cg_alpha(st, it, errflags);
     const int X2 = X >> 1;
     const int npair = rows * X2;
-    const int stride = gridDim.x * blockDim.x;
     const float4* ap4 = reinterpret_cast<const float4*>(ap);
     const float4* ap14 = reinterpret_cast<const float4*>(ap1);
     float4* r4 = reinterpret_cast<float4*>(r);
     float4 av[U], t1[U], rv[U];
     int sp[U];
     bool ok[U];
-    int i0 = blockIdx.x * blockDim.x + threadIdx.x;
     auto load = [&](int base) {
 #pragma unroll
         for (int k = 0; k < U; k++) {
             const int i = base + k * stride;
             ok[k] = i < npair;
             const int ii = ok[k] ? i : 0;
-            av[k] = ap4[ii];
-            t1[k] = ap14[ii]; // junk outside split strips: not used there
-            rv[k] = r4[ii];
+            av[k] = __ldcg(ap4 + ii);
+            t1[k] = __ldcg(ap14 + ii); // junk outside split strips: not used there
+            rv[k] = __ldcg(r4 + ii);
             const int row = ii / X2, xp = ii - row * X2;
             sp[k] = split[(row / Y) * nxb + ((2 * xp) >> wshift)];
         }
     };
-    load(i0);
-    __syncthreads();
-    const float al = s_alpha;
-    if (!(al > 0.f))
-        return;
     double2 part{0, 0};
+    if (i0 >= npair)
+        return part;
+    load(i0);
     while (true) {
 #pragma unroll
         for (int k = 0; k < U; k++) {
@@ -721,7 +756,7 @@ __global__ void __launch_bounds__(256) k_cg_update_r(CgDev* st, int it, cfloat* 
                 a.z += t1[k].z;
                 a.w += t1[k].w;
                 for (int pk = 2; pk < sp[k]; pk++) {
-                    const float4 t = ap14[i0 + k * stride + long(pk - 1) * (pstride / 2)];
+                    const float4 t = __ldcg(ap14 + i0 + k * stride + long(pk - 1) * (pstride / 2));
                     a.x += t.x;
                     a.y += t.y;
                     a.z += t.z;
@@ -742,6 +777,31 @@ __global__ void __launch_bounds__(256) k_cg_update_r(CgDev* st, int it, cfloat* 
             break;
         load(i0);
     }
+    return part;
+}
+
+// r-only CG update (x deferred): r -= alpha Ap ; <r, r> partial.  With every
+// search direction p_it kept, x = sum_it alpha_it p_it is formed once after the
+// loop by k_cg_x_sum in the same fma order as the per-iteration update (bitwise
+// identical), and each iteration streams 3 arrays instead of 5.
+template<int U>
+__global__ void __launch_bounds__(256) k_cg_update_r(CgDev* st, int it, cfloat* __restrict__ r,
+                                                     const cfloat* __restrict__ ap, const cfloat* __restrict__ ap1,
+                                                     const unsigned char* __restrict__ split, int X, int rows, int Y,
+                                                     int nxb, int wshift, long pstride, unsigned* errflags)
+{
+    __shared__ float s_alpha;
+    sm100::griddep_wait(); // Ap and <p, Ap> of the A^H A launch before (PDL)
+    if (threadIdx.x == 0) {
+        sm100::griddep_launch();
+        s_alpha = cg_alpha(st, it, errflags);
+    }
+    __syncthreads();
+    const float al = s_alpha;
+    if (!(al > 0.f))
+        return;
+    double2 part = cg_r_update_pairs<U>(al, r, ap, ap1, split, X, rows, Y, nxb, wshift, pstride,
+                                        int(blockIdx.x * blockDim.x + threadIdx.x), int(gridDim.x * blockDim.x));
     part = block_sum2(part);
     publish_partial(st->part_rr, &st->rr_sum, &st->cnt_rr, part);
 }

@@ -253,6 +253,56 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads)
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Fused CG update of iteration a.it (cg_defer_x path; replaces the k_cg_update_r
+// launch): every CTA stores its <p, Ap> partial and meets the others at a grid
+// barrier (cooperative launch: all CTAs co-resident), folds the partials exactly
+// as publish_partial's last CTA would (same order, same block size: bitwise the
+// same alpha on every CTA), then updates r over a grid-stride range of pixel pairs
+// and publishes its <r, r> partial.
+__device__ void ws_cg_update(const RankArgs& a, double2 part)
+{
+    CgDev* st = a.cg;
+    __shared__ float s_al;
+    if (threadIdx.x == 0) {
+        st->part_pap[blockIdx.x] = part;
+        __threadfence();
+        atomicAdd(&st->ws_bar, 1u);
+        const unsigned target = unsigned(a.it + 1) * gridDim.x;
+        // bounded spin (~seconds): a grid that is not co-resident raises an error
+        // instead of hanging the device
+        for (long spin = 0;; spin++) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&st->ws_bar) : "memory");
+            if (v >= target)
+                break;
+            if (spin > (1L << 26)) {
+                atomicOr(a.errflags, unsigned(ERRF_GRID_BARRIER));
+                break;
+            }
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+    double2 v{0, 0};
+    for (unsigned k = threadIdx.x; k < gridDim.x; k += blockDim.x)
+        v.x += __ldcg(&st->part_pap[k].x);
+    v = block_sum2(v);
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0)
+            st->pap_sum = v.x;
+        s_al = cg_alpha_sum(st, a.it, v.x, a.errflags);
+    }
+    __syncthreads();
+    const float al = s_al;
+    if (!(al > 0.f))
+        return;
+    double2 pr = cg_r_update_pairs<2>(al, a.r_upd, a.out, a.out1, a.split, int(a.X), a.upd_rows, a.upd_Y,
+                                      int(a.nxb), a.upd_wshift, a.pstride, int(blockIdx.x * blockDim.x + threadIdx.x),
+                                      int(gridDim.x * blockDim.x));
+    pr = block_sum2(pr);
+    publish_partial(st->part_rr, &st->rr_sum, &st->cnt_rr, pr);
+}
+
 template<int N1, int N2>
 __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
     k_normal_ws(RankArgs a, const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmx,
@@ -292,7 +342,12 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
         }
     };
 
+    // launched with programmatic serialisation in the CG loop: the previous kernel's
+    // r / p / CG scalars are read only after this wait; from here on the next
+    // kernel (the CG update) may be scheduled
+    sm100::griddep_wait();
     if (tid == 0) {
+        sm100::griddep_launch();
         for (int s = 0; s < NSLOT; s++) {
             sm100::mbar_init(&bar_full[s], 1);
             sm100::mbar_init(&bar_empty[s], NT_AC);
@@ -707,7 +762,10 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
 #endif
     if (a.mode == 1) {
         part = block_sum2(part);
-        publish_partial(a.cg->part_pap, &a.cg->pap_sum, &a.cg->cnt_pap, part);
+        if (a.r_upd)
+            ws_cg_update(a, part);
+        else
+            publish_partial(a.cg->part_pap, &a.cg->pap_sum, &a.cg->cnt_pap, part);
     } else {
         // keep every role resident until the A/C warps are done: letting the
         // producer and stage-B warps exit early made the mode-0 launch 1.7x
@@ -754,6 +812,7 @@ void launch_ws_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const unsi
     const double xyb = double(g.X) * g.Y * g.B;
     const double work = 8.0 * xyb * (g.C + (a.mode == 1 ? 4 : 2));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    k_normal_ws<N1, N2><<<a.G, Cfg::NT, Cfg::SMEM, ctx().stream>>>(a, m, mx, mp, plans);
+    launch_ex(g_cg_pdl, a.r_upd != nullptr && g_cg_fuse == 2, k_normal_ws<N1, N2>, dim3(a.G), dim3(Cfg::NT), size_t(Cfg::SMEM), a, m, mx, mp,
+              plans);
     KERNEL_CHECK();
 }

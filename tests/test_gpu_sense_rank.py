@@ -179,3 +179,41 @@ def test_cg_deferred_x_bitwise(gpu, ref, rank_opts, tol):
         assert itr < 10
     assert np.array_equal(np.ascontiguousarray(x1).view(np.uint32), np.ascontiguousarray(x0).view(np.uint32))
     assert rel_l2(x1, xr) <= TOL
+
+
+@pytest.mark.parametrize("tol", [0.0, 0.1])
+def test_cg_fused_update(gpu, ref, tol):
+    """The CG r-update fused into the warp-specialised A^H A launch (grid barrier;
+    option `cg_fuse` 1 default, 2 with a cooperative launch) against the separate
+    update kernel (`cg_fuse` = 0) and the reference, with programmatic dependent
+    launch on and off; strips split between CTAs and early convergence included."""
+    X, Y, NC, B = 320, 368, 6, 2
+    ph, cm, pat = sim_data(ref, X, Y, NC, B)
+    rng = np.random.default_rng(11)
+    b = crand(rng, image_dims(X, Y, B))
+
+    def solve(lib):
+        x = np.zeros(b.shape, dtype=np.complex64, order="F")
+        it, rr = C.c_long(), C.c_double()
+        lib.check(lib.so.mdnn_cg_normal_solve(C.byref(lib.arr(cm)), C.byref(lib.arr(pat)), C.c_float(0.05),
+                                              C.byref(lib.arr(b)), 10, tol, C.byref(lib.arr(x)), C.byref(it),
+                                              C.byref(rr)))
+        return x, it.value
+
+    xr, itr = solve(ref)
+    res = {}
+    try:
+        for fuse, pdl in ((0, 1), (1, 1), (2, 1), (1, 0)):
+            gpu.check(gpu.so.mdnn_set_option(b"cg_fuse", fuse))
+            gpu.check(gpu.so.mdnn_set_option(b"cg_pdl", pdl))
+            res[(fuse, pdl)] = solve(gpu)
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"cg_fuse", 1))
+        gpu.check(gpu.so.mdnn_set_option(b"cg_pdl", 1))
+    x0, i0 = res[(0, 1)]
+    for k, (x, i) in res.items():
+        assert i == itr, k
+        assert rel_l2(x, xr) <= TOL, k
+        assert rel_l2(x, x0) <= 1e-6, k
+    if tol > 0:
+        assert itr < 10
