@@ -21,6 +21,7 @@ int grid_for(long n)
 __global__ void k_sub_stat(cfloat* __restrict__ u, const cfloat* __restrict__ x, const cfloat* __restrict__ mu,
                            long inner, long nstat, long n)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long s = (i / inner) % nstat;
         float2 v = x[i], m = mu[s];
@@ -32,6 +33,7 @@ __global__ void k_stats_finish(cfloat* istd, cfloat* mean_out, cfloat* var_out, 
                                const cfloat* var, const cfloat* mean_in, const cfloat* var_in, long nstat, float eps,
                                float mom, int train)
 {
+    MDNN_PDL_ENTRY();
     for (long s = blockIdx.x * long(blockDim.x) + threadIdx.x; s < nstat; s += long(gridDim.x) * blockDim.x) {
         float v = var[s].x;
         istd[s] = float2{1.f / sqrtf(v + eps), 0.f};
@@ -54,6 +56,7 @@ __global__ void k_stats_finish(cfloat* istd, cfloat* mean_out, cfloat* var_out, 
 __global__ void k_stat_mul(cfloat* __restrict__ out, const cfloat* __restrict__ in, const cfloat* __restrict__ s,
                            long inner, long nstat, long n, bool cj)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         float2 v = in[i], w = s[(i / inner) % nstat];
         if (cj)
@@ -65,6 +68,7 @@ __global__ void k_stat_mul(cfloat* __restrict__ out, const cfloat* __restrict__ 
 __global__ void k_stat_add(cfloat* __restrict__ out, const cfloat* __restrict__ in, const cfloat* __restrict__ b,
                            long inner, long nstat, long n)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         float2 v = in[i], w = b[(i / inner) % nstat];
         out[i] = float2{v.x + w.x, v.y + w.y};
@@ -76,6 +80,7 @@ __global__ void k_bn_combine(cfloat* __restrict__ dx, const cfloat* __restrict__
                              const cfloat* __restrict__ gm, const cfloat* __restrict__ istd,
                              const cfloat* __restrict__ f, long inner, long nstat, long n)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long s = (i / inner) % nstat;
         float2 gv = g[i], m = gm[s], uv = u[i], fs = f[s];
@@ -90,6 +95,7 @@ __global__ void k_bn_combine(cfloat* __restrict__ dx, const cfloat* __restrict__
 // f[s] = coef * Re(p[s]) * istd^3   (complex (f, 0))
 __global__ void k_bn_f(cfloat* f, const cfloat* p, const cfloat* istd, long nstat, float coef)
 {
+    MDNN_PDL_ENTRY();
     for (long s = blockIdx.x * long(blockDim.x) + threadIdx.x; s < nstat; s += long(gridDim.x) * blockDim.x) {
         float is = istd[s].x;
         f[s] = float2{coef * p[s].x * is * is * is, 0.f};
@@ -101,14 +107,14 @@ __global__ void k_bn_f(cfloat* f, const cfloat* p, const cfloat* istd, long nsta
 void launch_stat_mul(cfloat* out, const cfloat* in, const cfloat* s, const IsoGeom& g, bool conj_s)
 {
     long n = g.inner * g.nstat * g.outer;
-    k_stat_mul<<<grid_for(n), kT, 0, ctx().stream>>>(out, in, s, g.inner, g.nstat, n, conj_s);
+    pdl_launch(k_stat_mul, grid_for(n), kT, 0, ctx().stream, out, in, s, g.inner, g.nstat, n, conj_s);
     KERNEL_CHECK();
 }
 
 void launch_stat_add(cfloat* out, const cfloat* in, const cfloat* b, const IsoGeom& g)
 {
     long n = g.inner * g.nstat * g.outer;
-    k_stat_add<<<grid_for(n), kT, 0, ctx().stream>>>(out, in, b, g.inner, g.nstat, n);
+    pdl_launch(k_stat_add, grid_for(n), kT, 0, ctx().stream, out, in, b, g.inner, g.nstat, n);
     KERNEL_CHECK();
 }
 
@@ -120,6 +126,7 @@ void launch_stat_mul_u_f(cfloat* out, const cfloat* u, const cfloat* f, const Is
 namespace {
 __global__ void k_real_to_complex(cfloat* out, const float* in, long n)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
         out[i] = cfloat{in[i], 0.f};
 }
@@ -127,7 +134,7 @@ __global__ void k_real_to_complex(cfloat* out, const float* in, long n)
 
 void launch_real_to_complex(cfloat* out, const float* in, long n)
 {
-    k_real_to_complex<<<grid_for(n), kT, 0, ctx().stream>>>(out, in, n);
+    pdl_launch(k_real_to_complex, grid_for(n), kT, 0, ctx().stream, out, in, n);
     KERNEL_CHECK();
 }
 
@@ -139,10 +146,10 @@ void bn_train_forward(cfloat* y, cfloat* u, cfloat* istd, cfloat* mean_out, cflo
     const float inv_m = float(1.0 / double(g.inner * g.outer));
     DArray mean(Dims{g.nstat}, false), var(Dims{g.nstat}, false);
     launch_iso_reduce(mean.data(), x, nullptr, g.inner, g.nstat, g.outer, 0, inv_m);
-    k_sub_stat<<<grid_for(n), kT, 0, c.stream>>>(u, x, mean.data(), g.inner, g.nstat, n);
+    pdl_launch(k_sub_stat, grid_for(n), kT, 0, c.stream, u, x, mean.data(), g.inner, g.nstat, n);
     KERNEL_CHECK();
     launch_iso_reduce(var.data(), u, u, g.inner, g.nstat, g.outer, 2, inv_m);
-    k_stats_finish<<<1, 128, 0, c.stream>>>(istd, mean_out, var_out, mean.data(), var.data(), mean_in, var_in,
+    pdl_launch(k_stats_finish, 1, 128, 0, c.stream, istd, mean_out, var_out, mean.data(), var.data(), mean_in, var_in,
                                             g.nstat, eps, mom, 1);
     KERNEL_CHECK();
     launch_stat_mul(y, u, istd, g, false);
@@ -153,10 +160,10 @@ void bn_infer_forward(cfloat* y, cfloat* u, cfloat* istd, const cfloat* x, const
 {
     auto& c = ctx();
     const long n = g.inner * g.nstat * g.outer;
-    k_stats_finish<<<1, 128, 0, c.stream>>>(istd, nullptr, nullptr, nullptr, var_in, nullptr, nullptr, g.nstat, eps,
+    pdl_launch(k_stats_finish, 1, 128, 0, c.stream, istd, nullptr, nullptr, nullptr, var_in, nullptr, nullptr, g.nstat, eps,
                                             0.f, 0);
     KERNEL_CHECK();
-    k_sub_stat<<<grid_for(n), kT, 0, c.stream>>>(u, x, mean_in, g.inner, g.nstat, n);
+    pdl_launch(k_sub_stat, grid_for(n), kT, 0, c.stream, u, x, mean_in, g.inner, g.nstat, n);
     KERNEL_CHECK();
     launch_stat_mul(y, u, istd, g, false);
 }
@@ -170,9 +177,9 @@ void bn_train_adjoint_x(cfloat* dx, const cfloat* gin, const cfloat* u, const cf
     DArray gm(Dims{g.nstat}, false), p(Dims{g.nstat}, false), f(Dims{g.nstat}, false);
     launch_iso_reduce(gm.data(), gin, nullptr, g.inner, g.nstat, g.outer, 0, float(1.0 / m));
     launch_iso_reduce(p.data(), gin, u, g.inner, g.nstat, g.outer, 1, 1.f);
-    k_bn_f<<<1, 128, 0, c.stream>>>(f.data(), p.data(), istd, g.nstat, float(-1.0 / m));
+    pdl_launch(k_bn_f, 1, 128, 0, c.stream, f.data(), p.data(), istd, g.nstat, float(-1.0 / m));
     KERNEL_CHECK();
-    k_bn_combine<<<grid_for(n), kT, 0, c.stream>>>(dx, gin, u, gm.data(), istd, f.data(), g.inner, g.nstat, n);
+    pdl_launch(k_bn_combine, grid_for(n), kT, 0, c.stream, dx, gin, u, gm.data(), istd, f.data(), g.inner, g.nstat, n);
     KERNEL_CHECK();
 }
 
@@ -185,9 +192,9 @@ void bn_train_deriv_x(cfloat* dy, const cfloat* dx, const cfloat* u, const cfloa
     DArray gm(Dims{g.nstat}, false), p(Dims{g.nstat}, false), f(Dims{g.nstat}, false);
     launch_iso_reduce(gm.data(), dx, nullptr, g.inner, g.nstat, g.outer, 0, float(1.0 / m));
     launch_iso_reduce(p.data(), dx, u, g.inner, g.nstat, g.outer, 1, 1.f);
-    k_bn_f<<<1, 128, 0, c.stream>>>(f.data(), p.data(), istd, g.nstat, float(-1.0 / m));
+    pdl_launch(k_bn_f, 1, 128, 0, c.stream, f.data(), p.data(), istd, g.nstat, float(-1.0 / m));
     KERNEL_CHECK();
-    k_bn_combine<<<grid_for(n), kT, 0, c.stream>>>(dy, dx, u, gm.data(), istd, f.data(), g.inner, g.nstat, n);
+    pdl_launch(k_bn_combine, grid_for(n), kT, 0, c.stream, dy, dx, u, gm.data(), istd, f.data(), g.inner, g.nstat, n);
     KERNEL_CHECK();
 }
 

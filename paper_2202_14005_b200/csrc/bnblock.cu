@@ -103,6 +103,7 @@ __device__ void sum_partials(double (&r)[NV], const double* __restrict__ part, i
 __global__ void __launch_bounds__(kT) k_stats(double* __restrict__ part, const float* __restrict__ x, long npix,
                                               int C, long pix_per_block)
 {
+    MDNN_PDL_ENTRY();
     const Pair q(C);
     const long p0 = long(blockIdx.x) * pix_per_block, p1 = min(npix, p0 + pix_per_block);
     // fp32 running sums per thread (a few hundred terms each, fixed order),
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(kT) k_stats_final(float2* __restrict__ mu, flo
                                                     const float2* __restrict__ mean_in,
                                                     const float2* __restrict__ var_in, float eps, float mom)
 {
+    MDNN_PDL_ENTRY();
     const int c = blockIdx.x;
     double r[3];
     sum_partials<3>(r, part, nblocks, C, c);
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(kT) k_stats_final_pre(float2* __restrict__ mu,
                                                         const float2* __restrict__ mean_in,
                                                         const float2* __restrict__ var_in, float eps, float mom)
 {
+    MDNN_PDL_ENTRY();
     const int c = blockIdx.x;
     double re[2], im[2];
     sum_partials<2>(re, part, nblocks, 2 * C, c);
@@ -231,6 +234,7 @@ __global__ void __launch_bounds__(kT) k_apply(float* __restrict__ out, const flo
                                               const float2* __restrict__ gamma, const float2* __restrict__ beta,
                                               long npix, int C, bool rnd)
 {
+    MDNN_PDL_ENTRY();
     const int tpp = C / 2, l = threadIdx.x % tpp;
     const ChanCoef k0 = coef(mu, istd, gamma, beta, 2 * l), k1 = coef(mu, istd, gamma, beta, 2 * l + 1);
     const long pstride = long(gridDim.x) * kT / tpp;
@@ -268,6 +272,7 @@ __global__ void __launch_bounds__(kT) k_bwd_reduce(double* __restrict__ part, co
                                                    const float2* __restrict__ beta, long npix, int C,
                                                    long pix_per_block)
 {
+    MDNN_PDL_ENTRY();
     const Pair q(C);
     const ChanCoef kc[2] = {coef(mu, istd, gamma, beta, 2 * q.l), coef(mu, istd, gamma, beta, 2 * q.l + 1)};
     const long p0 = long(blockIdx.x) * pix_per_block, p1 = min(npix, p0 + pix_per_block);
@@ -316,6 +321,7 @@ __global__ void __launch_bounds__(kT) k_bwd_final(float2* __restrict__ dbeta, fl
                                                   const double* __restrict__ part, int nblocks, int C, long m,
                                                   const float2* __restrict__ gamma, const float* __restrict__ istd)
 {
+    MDNN_PDL_ENTRY();
     const int c = blockIdx.x;
     double r[4];
     sum_partials<4>(r, part, nblocks, C, c);
@@ -342,6 +348,7 @@ __global__ void __launch_bounds__(kT) k_bwd_final_pre(float2* __restrict__ dbeta
                                                       const float2* __restrict__ gamma,
                                                       const float* __restrict__ istd)
 {
+    MDNN_PDL_ENTRY();
     const int c = blockIdx.x;
     double re[3], im[3];
     sum_partials<3>(re, part, nblocks, 2 * C, c);
@@ -368,6 +375,7 @@ __global__ void __launch_bounds__(kT) k_bwd_apply(float* __restrict__ dx, const 
                                                   const float2* __restrict__ beta, const float2* __restrict__ gm,
                                                   const float* __restrict__ fh, long npix, int C, bool rnd)
 {
+    MDNN_PDL_ENTRY();
     const int tpp = C / 2, l = threadIdx.x % tpp;
     const ChanCoef kc[2] = {coef(mu, istd, gamma, beta, 2 * l), coef(mu, istd, gamma, beta, 2 * l + 1)};
     const float2 gmc[2] = {gm[2 * l], gm[2 * l + 1]};
@@ -435,10 +443,10 @@ void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, floa
     if (pre_part && pre_blocks > 0) {
         // statistics partials came with x from its producer: apply pass only
         ProfScope prof("bnblock_fwd", 8.0 * 2 * npix * C);
-        k_stats_final_pre<<<C, kT, 0, c.stream>>>(mu, istd, mean_out, var_out, pre_part, pre_blocks, C, npix,
+        pdl_launch(k_stats_final_pre, C, kT, 0, c.stream, mu, istd, mean_out, var_out, pre_part, pre_blocks, C, npix,
                                                   mean_in, var_in, eps, mom);
         KERNEL_CHECK();
-        k_apply<<<grid_ew(npix, C), kT, 0, c.stream>>>(out, x, mu, istd, gamma, beta, npix, C, round_tf32);
+        pdl_launch(k_apply, grid_ew(npix, C), kT, 0, c.stream, out, x, mu, istd, gamma, beta, npix, C, round_tf32);
         KERNEL_CHECK();
         return;
     }
@@ -447,12 +455,12 @@ void bnblock_forward(float* out, float2* mu, float* istd, float2* mean_out, floa
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * 3 * C * nb, c.stream));
     ProfScope prof("bnblock_fwd", 8.0 * 2 * npix * C + 8.0 * npix * C);
-    k_stats<<<nb, kT, sizeof(double) * 2 * 3 * kT, c.stream>>>(part, x, npix, C, ppb);
+    pdl_launch(k_stats, nb, kT, sizeof(double) * 2 * 3 * kT, c.stream, part, x, npix, C, ppb);
     KERNEL_CHECK();
-    k_stats_final<<<C, kT, 0, c.stream>>>(mu, istd, mean_out, var_out, part, nb, C, npix, mean_in,
+    pdl_launch(k_stats_final, C, kT, 0, c.stream, mu, istd, mean_out, var_out, part, nb, C, npix, mean_in,
                                                        var_in, eps, mom);
     KERNEL_CHECK();
-    k_apply<<<grid_ew(npix, C), kT, 0, c.stream>>>(out, x, mu, istd, gamma, beta, npix, C, round_tf32);
+    pdl_launch(k_apply, grid_ew(npix, C), kT, 0, c.stream, out, x, mu, istd, gamma, beta, npix, C, round_tf32);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
@@ -475,17 +483,17 @@ void bnblock_backward(float* dx, float2* dgamma, float2* dbeta, const float* gou
     // algorithmic bytes: reduction pass (x, gout) unless folded into the producer, apply pass (x, gout, dx)
     ProfScope prof("bnblock_bwd", 8.0 * (pre ? 3 : 5) * npix * C);
     if (pre) {
-        k_bwd_final_pre<<<C, kT, 0, c.stream>>>(dbeta, dgamma, gm, fh, pre_part, pre_blocks, C, npix, gamma, istd);
+        pdl_launch(k_bwd_final_pre, C, kT, 0, c.stream, dbeta, dgamma, gm, fh, pre_part, pre_blocks, C, npix, gamma, istd);
         KERNEL_CHECK();
     } else {
-        k_bwd_reduce<<<nb, kT, sizeof(double) * 2 * 4 * kT, c.stream>>>(part, gout, x, mu, istd, gamma, beta, npix, C,
+        pdl_launch(k_bwd_reduce, nb, kT, sizeof(double) * 2 * 4 * kT, c.stream, part, gout, x, mu, istd, gamma, beta, npix, C,
                                                                       ppb);
         KERNEL_CHECK();
-        k_bwd_final<<<C, kT, 0, c.stream>>>(dbeta, dgamma, gm, fh, part, nb, C, npix, gamma, istd);
+        pdl_launch(k_bwd_final, C, kT, 0, c.stream, dbeta, dgamma, gm, fh, part, nb, C, npix, gamma, istd);
         KERNEL_CHECK();
     }
     if (dx) {
-        k_bwd_apply<<<grid_ew(npix, C), kT, 0, c.stream>>>(dx, gout, x, mu, istd, gamma, beta, gm, fh, npix, C,
+        pdl_launch(k_bwd_apply, grid_ew(npix, C), kT, 0, c.stream, dx, gout, x, mu, istd, gamma, beta, gm, fh, npix, C,
                                                             round_tf32);
         KERNEL_CHECK();
     }

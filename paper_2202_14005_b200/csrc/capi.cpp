@@ -187,6 +187,8 @@ int mdnn_set_option(const char* key, long value)
             cg_pdl_enable(value != 0);
         else if (k == "cg_fuse")
             cg_fuse_enable(int(value));
+        else if (k == "pdl")
+            g_pdl = value != 0;
         else if (k == "sense_rank_ctas")
             sense_rank_ctas(value);
         else if (k == "cg_defer_x")

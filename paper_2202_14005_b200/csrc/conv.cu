@@ -64,6 +64,7 @@ struct Out {
 // inner loop — no host synchronisation, any complex input takes the full path.
 __global__ void k_imag_any(const float2* __restrict__ a, long n, unsigned* flag)
 {
+    MDNN_PDL_ENTRY();
     int any = 0;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
         any |= a[i].y != 0.f;
@@ -78,6 +79,7 @@ template<int MODE, int FG>
 __global__ void __launch_bounds__(TX* TY) k_conv_direct(Out out, Acc in, const cfloat* __restrict__ w, ConvGeom g,
                                                         const unsigned* __restrict__ imag_flag, int skip_real)
 {
+    MDNN_PDL_ENTRY();
     const bool real = imag_flag && *imag_flag == 0;
     if (real && skip_real)
         return; // real operands: k_conv_direct_real computed this launch
@@ -197,6 +199,7 @@ template<int MODE, int FG, int RPX = rpx_for<FG>()>
 __global__ void __launch_bounds__(RTX* RTY) k_conv_direct_real(Out out, Acc in, const cfloat* __restrict__ w,
                                                               ConvGeom g, const unsigned* __restrict__ imag_flag)
 {
+    MDNN_PDL_ENTRY();
     if (*imag_flag != 0)
         return; // complex operands: k_conv_direct computes this launch
     constexpr int OX = RTX * RPX, OY = RTY;
@@ -313,6 +316,7 @@ constexpr int WMAXC = 4;                  // combos per thread
 template<int WG_C, int WG_F>
 __global__ void __launch_bounds__(256) k_conv_wgrad(float2* __restrict__ part, Acc x, Acc dy, ConvGeom g, int nsplit)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float2 xt[WG_C][WTY + MAXK - 1][WTX + MAXK - 1];
     __shared__ float2 dyt[WG_F][WTY][WTX];
     const int KX = int(g.KX), KY = int(g.KY), KK = KX * KY;
@@ -387,6 +391,7 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
                                                         int nsplit, const unsigned* __restrict__ imag_flag,
                                                         bool complex_only = false)
 {
+    MDNN_PDL_ENTRY();
     const bool real = imag_flag && *imag_flag == 0;
     if (complex_only && real) // the tensor-core kernel of this launch pair handles real operands
         return;
@@ -490,6 +495,7 @@ __global__ void __launch_bounds__(576) k_conv_wgrad_rb(float2* __restrict__ part
 __global__ void __launch_bounds__(256) k_sum_splits(cfloat* out, const float2* part, long n, int nsplit,
                                                     const unsigned* __restrict__ complex_only = nullptr)
 {
+    MDNN_PDL_ENTRY();
     if (complex_only && *complex_only == 0)
         return;
     __shared__ double2 red[4][64];
@@ -537,7 +543,7 @@ unsigned* imag_flag(std::initializer_list<std::pair<const cfloat*, long>> ops)
     CUDA_CHECK(cudaMallocAsync(&f, sizeof(unsigned), c.stream));
     CUDA_CHECK(cudaMemsetAsync(f, 0, sizeof(unsigned), c.stream));
     for (auto [p, n] : ops) {
-        k_imag_any<<<int(std::min<long>((n + 255) / 256, 2L * c.sm_count)), 256, 0, c.stream>>>(p, n, f);
+        pdl_launch(k_imag_any, int(std::min<long>((n + 255) / 256, 2L * c.sm_count)), 256, 0, c.stream, p, n, f);
         KERNEL_CHECK();
     }
     return f;
@@ -579,18 +585,18 @@ void conv_fwd(cfloat* y, const cfloat* x, const cfloat* w, const ConvGeom& g)
         dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
                    unsigned(g.B * ((g.Cout + FGv - 1) / FGv)));
         if (FGv == 2)
-            k_conv_direct_real<0, 2><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+            pdl_launch(k_conv_direct_real<0, 2>, rgrid, RTX * RTY, 0, ctx().stream, Out{y, g.Cout, XY, g.out_chlast},
                                                                           Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
         else
-            k_conv_direct_real<0, 8><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+            pdl_launch(k_conv_direct_real<0, 8>, rgrid, RTX * RTY, 0, ctx().stream, Out{y, g.Cout, XY, g.out_chlast},
                                                                           Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl);
         KERNEL_CHECK();
     }
     if (FGv == 2)
-        k_conv_direct<0, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+        pdl_launch(k_conv_direct<0, 2>, grid, TX * TY, 0, ctx().stream, Out{y, g.Cout, XY, g.out_chlast},
                                                                 Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl, 1);
     else
-        k_conv_direct<0, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{y, g.Cout, XY, g.out_chlast},
+        pdl_launch(k_conv_direct<0, 8>, grid, TX * TY, 0, ctx().stream, Out{y, g.Cout, XY, g.out_chlast},
                                                                 Acc{x, g.Cin, XY, g.in_chlast}, w, g, fl, 1);
     KERNEL_CHECK();
     if (!known)
@@ -622,18 +628,18 @@ void conv_bwd_data(cfloat* dx, const cfloat* dy, const cfloat* w, const ConvGeom
         dim3 rgrid(unsigned((g.X + RTX * RP - 1) / (RTX * RP)), unsigned((g.Y + RTY - 1) / RTY),
                    unsigned(g.B * ((g.Cin + FGv - 1) / FGv)));
         if (FGv == 2)
-            k_conv_direct_real<1, 2><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+            pdl_launch(k_conv_direct_real<1, 2>, rgrid, RTX * RTY, 0, ctx().stream, Out{dx, g.Cin, XY, g.in_chlast},
                                                                           Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
         else
-            k_conv_direct_real<1, 8><<<rgrid, RTX * RTY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+            pdl_launch(k_conv_direct_real<1, 8>, rgrid, RTX * RTY, 0, ctx().stream, Out{dx, g.Cin, XY, g.in_chlast},
                                                                           Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl);
         KERNEL_CHECK();
     }
     if (FGv == 2)
-        k_conv_direct<1, 2><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+        pdl_launch(k_conv_direct<1, 2>, grid, TX * TY, 0, ctx().stream, Out{dx, g.Cin, XY, g.in_chlast},
                                                                 Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl, 1);
     else
-        k_conv_direct<1, 8><<<grid, TX * TY, 0, ctx().stream>>>(Out{dx, g.Cin, XY, g.in_chlast},
+        pdl_launch(k_conv_direct<1, 8>, grid, TX * TY, 0, ctx().stream, Out{dx, g.Cin, XY, g.in_chlast},
                                                                 Acc{dy, g.Cout, XY, g.out_chlast}, w, g, fl, 1);
     KERNEL_CHECK();
     if (!known)
@@ -675,10 +681,10 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
             auto kern = fp2 ? k_conv_wgrad_rb<11, 2> : k_conv_wgrad_rb<11, 1>;
             allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
             const int nthr = int(((11 * g.Cin * (fp2 ? g.Cout / 2 : g.Cout) + 31) / 32) * 32);
-            kern<<<nsplit, nthr, smem, c.stream>>>(part, Acc{x, g.Cin, XY, g.in_chlast},
+            pdl_launch(kern, nsplit, nthr, smem, c.stream, part, Acc{x, g.Cin, XY, g.in_chlast},
                                                   Acc{dy, g.Cout, XY, g.out_chlast}, g, nsplit, fl, tc);
             KERNEL_CHECK();
-            k_sum_splits<<<int((n + 63) / 64), 256, 0, c.stream>>>(dw, part, n, nsplit, tc ? fl : nullptr);
+            pdl_launch(k_sum_splits, int((n + 63) / 64), 256, 0, c.stream, dw, part, n, nsplit, tc ? fl : nullptr);
             KERNEL_CHECK();
             CUDA_CHECK(cudaFreeAsync(part, c.stream));
         }
@@ -703,11 +709,11 @@ void conv_bwd_weight(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
     ProfScope prof("conv_bwd_weight", conv_flops(g));
     Acc ax{x, g.Cin, XY, g.in_chlast}, ad{dy, g.Cout, XY, g.out_chlast};
     if (small_k)
-        k_conv_wgrad<4, 8><<<grid, 256, 0, c.stream>>>(part, ax, ad, g, nsplit);
+        pdl_launch(k_conv_wgrad<4, 8>, grid, 256, 0, c.stream, part, ax, ad, g, nsplit);
     else
-        k_conv_wgrad<1, 8><<<grid, 256, 0, c.stream>>>(part, ax, ad, g, nsplit);
+        pdl_launch(k_conv_wgrad<1, 8>, grid, 256, 0, c.stream, part, ax, ad, g, nsplit);
     KERNEL_CHECK();
-    k_sum_splits<<<int((n + 63) / 64), 256, 0, c.stream>>>(dw, part, n, nsplit);
+    pdl_launch(k_sum_splits, int((n + 63) / 64), 256, 0, c.stream, dw, part, n, nsplit, nullptr);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }

@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(TT_THREADS, 1)
     k_conv_tc_t(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
                 float* __restrict__ out, int X, int Y, int B, int dbg, double* __restrict__ stats, const BnEpi be)
 {
+    MDNN_PDL_ENTRY();
     static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
     constexpr int N = 128, NP = TT_X * TT_Y, NCH = CIN2 / 32;
     using S = TtSmem;
@@ -355,6 +356,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     k_conv_tc_pair(const __grid_constant__ CUtensorMap tm_act, const __grid_constant__ CUtensorMap tm_w,
                    float* __restrict__ out, int X, int Y, int B, int dbg)
 {
+    MDNN_PDL_ENTRY();
     static_assert(CIN2 % 32 == 0, "K per tap must be a multiple of 32 floats");
     static_assert(N % 32 == 0 && N >= 32 && 2 * NM * N <= 512, "N must fit 2 x NM accumulators in TMEM");
     constexpr int NCH = CIN2 / 32;
@@ -549,6 +551,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     k_conv_tc_wgrad(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
                     float* __restrict__ part, int X, int Y, int B, int nsplit)
 {
+    MDNN_PDL_ENTRY();
     using S = WgSmem<N>;
     constexpr int TMEM_COLS = 3 * N <= 128 ? 128 : (3 * N <= 256 ? 256 : 512);
     constexpr int NDB = N / 32;
@@ -670,6 +673,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 __global__ void __launch_bounds__(256) k_wgrad_fold(cfloat* __restrict__ dw, const float* __restrict__ part, int Cin,
                                                     int Cout, int N, int nsplit)
 {
+    MDNN_PDL_ENTRY();
     __shared__ double2 red[4][64];
     const int n_out = 9 * Cin * Cout;
     const int o = threadIdx.x & 63, g = threadIdx.x >> 6;
@@ -707,6 +711,7 @@ __global__ void __launch_bounds__(256) k_wgrad_fold(cfloat* __restrict__ dw, con
 __global__ void k_pack_weights(float* __restrict__ bt, const cfloat* __restrict__ w, int KX, int KY, int Cin,
                                int Cout, int mode)
 {
+    MDNN_PDL_ENTRY();
     const int taps = KX * KY;
     const int nin = mode == 0 ? Cin : Cout, nout = mode == 0 ? Cout : Cin;
     const int K = taps * 2 * nin, N = 2 * nout;
@@ -734,6 +739,7 @@ __global__ void k_pack_weights(float* __restrict__ bt, const cfloat* __restrict_
 __global__ void k_to_chlast_tf32(float* __restrict__ out, const cfloat* __restrict__ in, long inner, long C,
                                  long outer)
 {
+    MDNN_PDL_ENTRY();
     __shared__ cfloat tile[32][33];
     const long pix0 = long(blockIdx.x) * 32, c0 = long(blockIdx.y) * 32, o = blockIdx.z;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -828,7 +834,7 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
         }
         const int nt = ((X + TT_X - 1) / TT_X) * ((Y + TT_Y - 1) / TT_Y) * B;
         const int grid = std::min(nt, c.sm_count);
-        kt<<<grid, TT_THREADS, smem_t, c.stream>>>(tat, tw, out, X, Y, B, g_tc_dbg, stats, be);
+        pdl_launch(kt, grid, TT_THREADS, smem_t, c.stream, tat, tw, out, X, Y, B, g_tc_dbg, stats, be);
         KERNEL_CHECK();
         if (stats && stats_blocks)
             *stats_blocks = grid * (TT_EPI_WARPS / 4);
@@ -851,7 +857,7 @@ void launch_tc(const float* act, const float* wpk, float* out, int X, int Y, int
         }
         const int npairs = (ntiles + 1) / 2;
         const int grid = 2 * std::min(npairs, c.sm_count / 2);
-        kp<<<grid, NTHREADS, smem_p, c.stream>>>(ta, twp, out, X, Y, B, g_tc_dbg);
+        pdl_launch(kp, grid, NTHREADS, smem_p, c.stream, ta, twp, out, X, Y, B, g_tc_dbg);
         KERNEL_CHECK();
     }
 }
@@ -877,9 +883,9 @@ void launch_tc_wgrad(const float* x, const float* dy, cfloat* dw, int X, int Y, 
     const int nsplit = int(std::max(1L, std::min<long>(c.sm_count / 3, nseg)));
     float* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(float) * size_t(nsplit) * 9 * 128 * N, c.stream));
-    kern<<<3 * nsplit, NTHREADS, smem, c.stream>>>(tx, td, part, X, Y, B, nsplit);
+    pdl_launch(kern, 3 * nsplit, NTHREADS, smem, c.stream, tx, td, part, X, Y, B, nsplit);
     KERNEL_CHECK();
-    k_wgrad_fold<<<(9 * Cin * Cout + 63) / 64, 256, 0, c.stream>>>(dw, part, Cin, Cout, N, nsplit);
+    pdl_launch(k_wgrad_fold, (9 * Cin * Cout + 63) / 64, 256, 0, c.stream, dw, part, Cin, Cout, N, nsplit);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
@@ -898,6 +904,7 @@ namespace {
 
 __global__ void k_round_tf32(float* __restrict__ out, const float* __restrict__ in, long n)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
         out[i] = to_tf32(in[i]);
 }
@@ -913,11 +920,10 @@ const float* stage_operand(const cfloat* p, long C, const ConvGeom& g, bool chla
     const long inner = g.X * g.Y, n = 2 * C * inner * g.B;
     CUDA_CHECK(cudaMallocAsync(tmp, sizeof(float) * n, c.stream));
     if (chlast) {
-        k_round_tf32<<<int(std::min<long>(c.sm_count * 8, (n + 255) / 256)), 256, 0, c.stream>>>(
-            *tmp, reinterpret_cast<const float*>(p), n);
+        pdl_launch(k_round_tf32, int(std::min<long>(c.sm_count * 8, (n + 255) / 256)), 256, 0, c.stream, *tmp, reinterpret_cast<const float*>(p), n);
     } else {
-        k_to_chlast_tf32<<<dim3(unsigned((inner + 31) / 32), unsigned((C + 31) / 32), unsigned(g.B)), dim3(32, 8), 0,
-                           c.stream>>>(*tmp, p, inner, C, g.B);
+        pdl_launch(k_to_chlast_tf32, dim3(unsigned((inner + 31) / 32), unsigned((C + 31) / 32), unsigned(g.B)), dim3(32, 8), 0,
+                           c.stream, *tmp, p, inner, C, g.B);
     }
     KERNEL_CHECK();
     return *tmp;
@@ -985,8 +991,7 @@ void conv_tc_run(cfloat* outp, const cfloat* inp, const cfloat* w, const ConvGeo
     if (!out_chl)
         CUDA_CHECK(cudaMallocAsync(&res, sizeof(float) * 2 * nout * inner * g.B, c.stream));
     CUDA_CHECK(cudaMallocAsync(&wpk, sizeof(float) * K * N, c.stream));
-    k_pack_weights<<<int(std::min<long>(1024, (K * N + 255) / 256)), 256, 0, c.stream>>>(
-        wpk, w, int(g.KX), int(g.KY), int(g.Cin), int(g.Cout), mode);
+    pdl_launch(k_pack_weights, int(std::min<long>(1024, (K * N + 255) / 256)), 256, 0, c.stream, wpk, w, int(g.KX), int(g.KY), int(g.Cin), int(g.Cout), mode);
     KERNEL_CHECK();
     {
         const double flops = 8.0 * double(g.X) * g.Y * g.B * g.Cin * g.Cout * 9;

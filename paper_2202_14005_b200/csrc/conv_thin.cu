@@ -35,6 +35,7 @@ constexpr int TX = 32, NT = 256, MAXF = 256;
 //   mode 3: bwd-data of 1 -> F   U[t][f] = conj(w[flip t, 0, f])
 __global__ void k_pack_thin(float2* U, const float2* w, int KX, int KY, int F, int mode)
 {
+    MDNN_PDL_ENTRY();
     const int KK = KX * KY;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < KK * F; i += gridDim.x * blockDim.x) {
         const int t = i % KK, f = i / KK;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(NT) k_thin_expand(float* __restrict__ out, con
                                                     const float2* __restrict__ U, int X, int Y, int F, int ox, int oy,
                                                     const ThinEpi ep)
 {
+    MDNN_PDL_ENTRY();
     constexpr int TY = 8, HX = TX + K - 1, HY = TY + K - 1;
     __shared__ float2 tile[HX * HY];
     const long b = blockIdx.z;
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(NT, K == 3 ? 2 : 1) k_thin_reduce(float2* __re
                                                        const float2* __restrict__ U, int X, int Y, int F, int ox,
                                                        int oy)
 {
+    MDNN_PDL_ENTRY();
     using Cfg = ReduceCfg<K>;
     constexpr int HX = Cfg::HX, NH = Cfg::NH, KK = Cfg::KK, PP = Cfg::PP, TY = Cfg::TY;
     extern __shared__ float4 smr4[];
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
                                                    const float2* __restrict__ thin, int X, int Y, int B, int F,
                                                    int ox, int oy)
 {
+    MDNN_PDL_ENTRY();
     constexpr int TY = 8, HX = TX + K - 1, HY = TY + K - 1, KK = K * K;
     __shared__ float2 tile[HX * HY];
     extern __shared__ float2 sred[]; // [lanes][KK][F] = NT * KK float2
@@ -498,6 +502,7 @@ __global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, co
 __global__ void __launch_bounds__(NT) k_thin_wsum(float2* __restrict__ dw, const float2* __restrict__ part, int nblk,
                                                   int KK, int F)
 {
+    MDNN_PDL_ENTRY();
     __shared__ double sr[NT], si[NT];
     const int e = blockIdx.x;
     double a = 0, c = 0;
@@ -528,7 +533,7 @@ float2* pack_u(const cfloat* w, const ConvGeom& g, int F, int pmode)
     const int KK = int(g.KX * g.KY);
     float2* U;
     CUDA_CHECK(cudaMallocAsync(&U, sizeof(float2) * KK * F, c.stream));
-    k_pack_thin<<<std::max(1, (KK * F + 255) / 256), 256, 0, c.stream>>>(U, w, int(g.KX), int(g.KY), F, pmode);
+    pdl_launch(k_pack_thin, std::max(1, (KK * F + 255) / 256), 256, 0, c.stream, U, w, int(g.KX), int(g.KY), F, pmode);
     KERNEL_CHECK();
     return U;
 }
@@ -541,10 +546,10 @@ void run_thin(cfloat* outp, const cfloat* inp, const float2* U, const ConvGeom& 
     if (expand) {
         dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + 7) / 8), unsigned(g.B));
         if (F % 2 == 0 && NT % (F / 2) == 0)
-            k_thin_expand<K, 2><<<grid, NT, 0, c.stream>>>(reinterpret_cast<float*>(outp), inp, U, int(g.X),
+            pdl_launch(k_thin_expand<K, 2>, grid, NT, 0, c.stream, reinterpret_cast<float*>(outp), inp, U, int(g.X),
                                                            int(g.Y), F, ox, oy, ep);
         else
-            k_thin_expand<K, 1><<<grid, NT, 0, c.stream>>>(reinterpret_cast<float*>(outp), inp, U, int(g.X),
+            pdl_launch(k_thin_expand<K, 1>, grid, NT, 0, c.stream, reinterpret_cast<float*>(outp), inp, U, int(g.X),
                                                            int(g.Y), F, ox, oy, ThinEpi{});
     } else {
         if (thin_reduce_tc(outp, reinterpret_cast<const float*>(inp), U, g.X, g.Y, g.B, F, K * K, ox, oy))
@@ -553,7 +558,7 @@ void run_thin(cfloat* outp, const cfloat* inp, const float2* U, const ConvGeom& 
         auto kern = k_thin_reduce<K>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
         dim3 grid(unsigned((g.X + TX - 1) / TX), unsigned((g.Y + Cfg::TY - 1) / Cfg::TY), unsigned(g.B));
-        kern<<<grid, NT, Cfg::smem(F), c.stream>>>(outp, reinterpret_cast<const float*>(inp), U, int(g.X), int(g.Y),
+        pdl_launch(kern, grid, NT, Cfg::smem(F), c.stream, outp, reinterpret_cast<const float*>(inp), U, int(g.X), int(g.Y),
                                                   F, ox, oy);
     }
     KERNEL_CHECK();
@@ -569,12 +574,12 @@ void run_thin_wgrad(float2* part, int nblk, const cfloat* x, const cfloat* dy, c
     if (one_in) { // g = dy wide, h = x thin, window offset c0
         auto kern = pair ? k_thin_wgrad<K, true, 2> : k_thin_wgrad<K, true, 1>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
-        kern<<<nblk, NT, smem, c.stream>>>(part, reinterpret_cast<const float*>(dy), x, int(g.X), int(g.Y), int(g.B),
+        pdl_launch(kern, nblk, NT, smem, c.stream, part, reinterpret_cast<const float*>(dy), x, int(g.X), int(g.Y), int(g.B),
                                            F, int(g.px), int(g.py));
     } else { // g = dy thin, h = x wide, window offset K-1-c0
         auto kern = pair ? k_thin_wgrad<K, false, 2> : k_thin_wgrad<K, false, 1>;
         allow_max_dyn_smem(reinterpret_cast<const void*>(kern));
-        kern<<<nblk, NT, smem, c.stream>>>(part, reinterpret_cast<const float*>(x), dy, int(g.X), int(g.Y), int(g.B),
+        pdl_launch(kern, nblk, NT, smem, c.stream, part, reinterpret_cast<const float*>(x), dy, int(g.X), int(g.Y), int(g.B),
                                            F, int(K - 1 - g.px), int(K - 1 - g.py));
     }
     KERNEL_CHECK();
@@ -678,7 +683,7 @@ void conv_thin_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvGe
             run_thin_wgrad<3>(part, nblk, x, dy, g, F, one_in);
         else
             run_thin_wgrad<5>(part, nblk, x, dy, g, F, one_in);
-        k_thin_wsum<<<KK * F, NT, 0, c.stream>>>(dw, part, nblk, KK, F);
+        pdl_launch(k_thin_wsum, KK * F, NT, 0, c.stream, dw, part, nblk, KK, F);
         KERNEL_CHECK();
     }
     CUDA_CHECK(cudaFreeAsync(part, c.stream));

@@ -46,6 +46,7 @@ struct TpSmem {
 // Ut[n][k]: row n = 2 t + comp (comp 0: Re z_t, 1: Im z_t); k < F: Re wide_c, k >= F: Im wide_c
 __global__ void k_pack_thin_tc(float* __restrict__ ut, const float2* __restrict__ U, int F, int KK)
 {
+    MDNN_PDL_ENTRY();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < TP_N * 2 * F; i += gridDim.x * blockDim.x) {
         const int k = i % (2 * F), n = i / (2 * F);
         const int t = n >> 1, comp = n & 1;
@@ -64,6 +65,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
     k_thin_proj(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                 float* __restrict__ z, long npix)
 {
+    MDNN_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     // aligned by an offset from the shared array (not an integer round trip), so
     // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
 __global__ void __launch_bounds__(256) k_thin_gather(float2* __restrict__ out, const float* __restrict__ z, int X, int Y,
                                                      long npix, int ox, int oy)
 {
+    MDNN_PDL_ENTRY();
     for (long q = blockIdx.x * long(blockDim.x) + threadIdx.x; q < npix; q += long(gridDim.x) * blockDim.x) {
         const int x = int(q % X), y = int((q / X) % Y);
         const long b = q / (long(X) * Y);
@@ -234,6 +237,7 @@ struct TeSmem {
 // K layout [w_hi(18) | w_hi(18) | w_lo(18) | 0]
 __global__ void k_pack_thin_expand(float* __restrict__ ue, const float2* __restrict__ U, int F, int KK)
 {
+    MDNN_PDL_ENTRY();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 128 * 64; i += gridDim.x * blockDim.x) {
         const int kk = i % 64, n = i / 64;
         const int part = kk / 18, k = kk % 18;
@@ -271,6 +275,7 @@ __global__ void __launch_bounds__(TE_THREADS, 1)
                      const float* __restrict__ ue, int X, int Y, long npix, int ox, int oy, double* __restrict__ stats,
                      const TeBn be)
 {
+    MDNN_PDL_ENTRY();
     extern __shared__ uint8_t smem_raw[];
     // aligned by an offset from the shared array (not an integer round trip), so
     // the compiler keeps the shared address space: LDS/STS, not generic LD/ST
@@ -571,7 +576,7 @@ bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, lon
     const long npix = X * Y * B;
     float* ue;
     CUDA_CHECK(cudaMallocAsync(&ue, sizeof(float) * 128 * 64, c.stream));
-    k_pack_thin_expand<<<32, 256, 0, c.stream>>>(ue, U, F, KK);
+    pdl_launch(k_pack_thin_expand, 32, 256, 0, c.stream, ue, U, F, KK);
     KERNEL_CHECK();
     const long ntiles = (npix + TE_P - 1) / TE_P;
     const int grid = int(std::min<long>(ntiles, c.sm_count));
@@ -601,7 +606,7 @@ bool thin_expand_tc(float* out, const cfloat* thin, const float2* U, long X, lon
             done[c.device * 4 + e] = true;
         }
     }
-    kern<<<grid, TE_THREADS, TeSmem::TOTAL, c.stream>>>(tmo, thin, ue, int(X), int(Y), npix, ox, oy, stats, be);
+    pdl_launch(kern, grid, TE_THREADS, TeSmem::TOTAL, c.stream, tmo, thin, ue, int(X), int(Y), npix, ox, oy, stats, be);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(ue, c.stream));
     if (stats && stats_blocks)
@@ -621,7 +626,7 @@ bool thin_reduce_tc(cfloat* out, const float* wide, const float2* U, long X, lon
     float *ut, *z;
     CUDA_CHECK(cudaMallocAsync(&ut, sizeof(float) * TP_N * TP_K, c.stream));
     CUDA_CHECK(cudaMallocAsync(&z, sizeof(float) * size_t(npix) * TP_ZP, c.stream));
-    k_pack_thin_tc<<<(TP_N * TP_K + 255) / 256, 256, 0, c.stream>>>(ut, U, F, KK);
+    pdl_launch(k_pack_thin_tc, (TP_N * TP_K + 255) / 256, 256, 0, c.stream, ut, U, F, KK);
     KERNEL_CHECK();
     const CUtensorMap ta = tp_map(wide, npix, TP_ROWS), tb = tp_map(ut, TP_N, TP_N);
     static std::mutex mu;
@@ -634,10 +639,9 @@ bool thin_reduce_tc(cfloat* out, const float* wide, const float2* U, long X, lon
         }
     }
     const long ntiles = (npix + TP_ROWS - 1) / TP_ROWS;
-    k_thin_proj<<<int(std::min<long>(ntiles, c.sm_count)), TP_THREADS, TpSmem::TOTAL, c.stream>>>(ta, tb, z, npix);
+    pdl_launch(k_thin_proj, int(std::min<long>(ntiles, c.sm_count)), TP_THREADS, TpSmem::TOTAL, c.stream, ta, tb, z, npix);
     KERNEL_CHECK();
-    k_thin_gather<<<int(std::min<long>((npix + 255) / 256, 8L * c.sm_count)), 256, 0, c.stream>>>(
-        out, z, int(X), int(Y), npix, ox, oy);
+    pdl_launch(k_thin_gather, int(std::min<long>((npix + 255) / 256, 8L * c.sm_count)), 256, 0, c.stream, out, z, int(X), int(Y), npix, ox, oy);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(ut, c.stream));
     CUDA_CHECK(cudaFreeAsync(z, c.stream));

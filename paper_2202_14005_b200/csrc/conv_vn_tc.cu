@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(V_THREADS, 1)
     k_vn_expand(const __grid_constant__ CUtensorMap tm_x, float2* __restrict__ y, const float2* __restrict__ w, int X,
                 int Y, int B, int F, int F8, const unsigned* __restrict__ imag)
 {
+    MDNN_PDL_ENTRY();
     if (*imag) // complex operands: the CUDA-core complex kernel of this launch pair runs instead
         return;
     const VeSmem L(F8);
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(VR_THREADS, 1)
     k_vn_reduce(const __grid_constant__ CUtensorMap tm_dy, float2* __restrict__ dx, const float2* __restrict__ w, int X,
                 int Y, int B, int F, int F8, const unsigned* __restrict__ imag)
 {
+    MDNN_PDL_ENTRY();
     if (*imag)
         return;
     const VrSmem L(F, F8);
@@ -535,6 +537,7 @@ __global__ void __launch_bounds__(VR_THREADS, 1)
     k_vn_wgrad(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_dy,
                float2* __restrict__ part, int X, int Y, int B, int F, const unsigned* __restrict__ imag)
 {
+    MDNN_PDL_ENTRY();
     if (*imag)
         return;
     const VwSmem L(F);
@@ -733,6 +736,7 @@ __global__ void __launch_bounds__(VR_THREADS, 1)
 __global__ void __launch_bounds__(256) k_vn_fold(float2* __restrict__ dw, const float2* __restrict__ part, long n,
                                                  int nsplit, const unsigned* __restrict__ imag)
 {
+    MDNN_PDL_ENTRY();
     if (*imag)
         return;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
@@ -808,10 +812,10 @@ void conv_vn_tc_wgrad(cfloat* dw, const cfloat* x, const cfloat* dy, const ConvG
     {
         ProfScope prof("conv_vn_bwd_weight", vn_bytes(g));
         ProfScope prof_tf("conv_vn_bwd_weight_tf", vn_flops(g));
-        k_vn_wgrad<<<grid, VR_THREADS, L.total, c.stream>>>(tx, td, part, X, Y, B, F, imag);
+        pdl_launch(k_vn_wgrad, grid, VR_THREADS, L.total, c.stream, tx, td, part, X, Y, B, F, imag);
         KERNEL_CHECK();
     }
-    k_vn_fold<<<int((n + 255) / 256), 256, 0, c.stream>>>(dw, part, n, grid, imag);
+    pdl_launch(k_vn_fold, int((n + 255) / 256), 256, 0, c.stream, dw, part, n, grid, imag);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
@@ -829,7 +833,7 @@ void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGe
         const CUtensorMap tm = vn_map(in, X, Y, 2L * B, 2 * VE_BOXPX, 2);
         ProfScope prof("conv_vn_fwd", vn_bytes(g));
         ProfScope prof_tf("conv_vn_fwd_tf", vn_flops(g));
-        k_vn_expand<<<grid, V_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
+        pdl_launch(k_vn_expand, grid, V_THREADS, L.total, c.stream, tm, out, w, X, Y, B, F, F8, imag);
     } else {
         const VrSmem L(F, F8);
         const long units = long((X + VR_OUT - 1) / VR_OUT) * ((Y + VR_RC - 1) / VR_RC) * B;
@@ -838,7 +842,7 @@ void conv_vn_tc_run(cfloat* out, const cfloat* in, const cfloat* w, const ConvGe
         const CUtensorMap tm = vn_map(in, X, Y, long(F) * B, 256, F);
         ProfScope prof("conv_vn_bwd_data", vn_bytes(g));
         ProfScope prof_tf("conv_vn_bwd_data_tf", vn_flops(g));
-        k_vn_reduce<<<grid, VR_THREADS, L.total, c.stream>>>(tm, out, w, X, Y, B, F, F8, imag);
+        pdl_launch(k_vn_reduce, grid, VR_THREADS, L.total, c.stream, tm, out, w, X, Y, B, F, F8, imag);
     }
     KERNEL_CHECK();
 }

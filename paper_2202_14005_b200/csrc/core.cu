@@ -10,6 +10,9 @@
 
 namespace mdnn {
 
+bool g_pdl = true;
+
+
 void cuda_check(cudaError_t e, const char* what, const char* file, int line)
 {
     if (e != cudaSuccess)
@@ -203,14 +206,15 @@ DArray DArray::clone() const
 }
 
 namespace {
-__global__ void k_set_scalar(float2* p, float re, float im) { *p = float2{re, im}; }
+__global__ void k_set_scalar(float2* p, float re, float im) {
+    MDNN_PDL_ENTRY(); *p = float2{re, im}; }
 } // namespace
 
 DArray DArray::scalar(float re, float im)
 {
     // value travels as a kernel argument: no host staging, no stream synchronisation
     DArray a(Dims{1}, false);
-    k_set_scalar<<<1, 1, 0, ctx().stream>>>(a.data(), re, im);
+    pdl_launch(k_set_scalar, 1, 1, 0, ctx().stream, a.data(), re, im);
     KERNEL_CHECK();
     return a;
 }

@@ -14,6 +14,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace mdnn {
@@ -52,6 +53,30 @@ long launch_count();
         ::mdnn::count_launch();                                                       \
         ::mdnn::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);  \
     } while (0)
+
+// Programmatic dependent launch (option "pdl", default on): every library kernel
+// starts with MDNN_PDL_ENTRY() -- wait until the previous kernel in the stream has
+// completed and its memory is visible, then let the next kernel be scheduled --
+// and is launched with the programmatic-stream-serialisation attribute, so its
+// launch and CTA start overlap the previous kernel's tail.
+extern bool g_pdl;
+template<class... KArgs, class... Args>
+inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+#define MDNN_PDL_ENTRY() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
 
 using Dims = std::vector<long>;
 long md_size(const Dims& d);

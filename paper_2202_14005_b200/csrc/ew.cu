@@ -45,6 +45,7 @@ __device__ __forceinline__ cfloat cmulc(cfloat a, cfloat b) { return {a.x * b.x 
 
 __global__ void k_strided_copy(Md3 m, long n, cfloat* dst, const cfloat* src)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long r = i, od = 0, os = 0;
         for (int d = 0; d < m.rank; d++) {
@@ -59,6 +60,7 @@ __global__ void k_strided_copy(Md3 m, long n, cfloat* dst, const cfloat* src)
 
 __global__ void k_bcast_binary(Md3 m, long n, cfloat* out, const cfloat* a, const cfloat* b, int op)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long r = i, oa = 0, ob = 0;
         for (int d = 0; d < m.rank; d++) {
@@ -76,6 +78,7 @@ __global__ void k_bcast_binary(Md3 m, long n, cfloat* out, const cfloat* a, cons
 template<class F>
 __global__ void k_map1(cfloat* __restrict__ out, const cfloat* __restrict__ in, long n, F f)
 {
+    MDNN_PDL_ENTRY();
     long n2 = n / 2;
     const float4* in4 = reinterpret_cast<const float4*>(in);
     float4* out4 = reinterpret_cast<float4*>(out);
@@ -92,6 +95,7 @@ template<class F>
 __global__ void k_map2(cfloat* __restrict__ out, const cfloat* __restrict__ a, const cfloat* __restrict__ b, long n,
                        F f)
 {
+    MDNN_PDL_ENTRY();
     long n2 = n / 2;
     const float4* a4 = reinterpret_cast<const float4*>(a);
     const float4* b4 = reinterpret_cast<const float4*>(b);
@@ -114,7 +118,7 @@ void map1(cfloat* out, const cfloat* in, long n, F f)
         return;
     if (!aligned16(out) || !aligned16(in))
         throw Error("map1: misaligned buffers");
-    k_map1<<<grid_for(n / 2 + 1), kThreads, 0, ctx().stream>>>(out, in, n, f);
+    pdl_launch(k_map1<F>, grid_for(n / 2 + 1), kThreads, 0, ctx().stream, out, in, n, f);
     KERNEL_CHECK();
 }
 
@@ -123,7 +127,7 @@ void map2(cfloat* out, const cfloat* a, const cfloat* b, long n, F f)
 {
     if (n <= 0)
         return;
-    k_map2<<<grid_for(n / 2 + 1), kThreads, 0, ctx().stream>>>(out, a, b, n, f);
+    pdl_launch(k_map2<F>, grid_for(n / 2 + 1), kThreads, 0, ctx().stream, out, a, b, n, f);
     KERNEL_CHECK();
 }
 
@@ -158,6 +162,7 @@ __device__ double2 block_sum2(double2 v)
 __global__ void k_iso_partial(double2* part, const cfloat* a, const cfloat* b, long inner, long nstat, long outer,
                               int mode, int nchunk, long chunk)
 {
+    MDNN_PDL_ENTRY();
     const long stat = blockIdx.y;
     const long total = inner * outer;
     const long begin = long(blockIdx.x) * chunk;
@@ -195,6 +200,7 @@ __global__ void k_iso_partial(double2* part, const cfloat* a, const cfloat* b, l
 
 __global__ void k_iso_final(cfloat* out, double2* out_d, const double2* part, long nstat, int nchunk, float scale)
 {
+    MDNN_PDL_ENTRY();
     for (long s = blockIdx.x * long(blockDim.x) + threadIdx.x; s < nstat; s += long(gridDim.x) * blockDim.x) {
         double2 acc{0, 0};
         for (int c = 0; c < nchunk; c++) {
@@ -212,6 +218,7 @@ __global__ void k_iso_final(cfloat* out, double2* out_d, const double2* part, lo
 // (many chunks, few statistics: the serial loop above is latency-bound)
 __global__ void k_iso_final_block(cfloat* out, double2* out_d, const double2* part, int nchunk, float scale)
 {
+    MDNN_PDL_ENTRY();
     const long s = blockIdx.x;
     double2 acc{0, 0};
     for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
@@ -244,12 +251,12 @@ void iso_reduce_impl(cfloat* out, double2* out_d, const cfloat* a, const cfloat*
     double2* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double2) * nchunk * nstat, c.stream));
     dim3 grid(nchunk, unsigned(nstat));
-    k_iso_partial<<<grid, kThreads, 0, c.stream>>>(part, a, b, inner, nstat, outer, mode, nchunk, chunk);
+    pdl_launch(k_iso_partial, grid, kThreads, 0, c.stream, part, a, b, inner, nstat, outer, mode, nchunk, chunk);
     KERNEL_CHECK();
     if (nchunk >= 64 && nstat <= 4096)
-        k_iso_final_block<<<unsigned(nstat), 256, 0, c.stream>>>(out, out_d, part, nchunk, scale);
+        pdl_launch(k_iso_final_block, unsigned(nstat), 256, 0, c.stream, out, out_d, part, nchunk, scale);
     else
-        k_iso_final<<<int(std::min(1024L, (nstat + 127) / 128)), 128, 0, c.stream>>>(out, out_d, part, nstat, nchunk,
+        pdl_launch(k_iso_final, int(std::min(1024L, (nstat + 127) / 128)), 128, 0, c.stream, out, out_d, part, nstat, nchunk,
                                                                                      scale);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
@@ -265,6 +272,7 @@ struct FmacPlan {
 __global__ void k_fmac_gather(FmacPlan p, long nout_total, long nred_total, cfloat* out, const cfloat* a,
                               const cfloat* b, bool conj2)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < nout_total; i += long(gridDim.x) * blockDim.x) {
         long r = i, oo = 0, o1 = 0, o2 = 0;
         for (int d = 0; d < p.nout; d++) {
@@ -298,6 +306,7 @@ __global__ void k_fmac_gather(FmacPlan p, long nout_total, long nred_total, cflo
 __global__ void k_canon_to_chlast(float* __restrict__ out, const cfloat* __restrict__ in, long inner, long C,
                                   long outer)
 {
+    MDNN_PDL_ENTRY();
     __shared__ cfloat tile[32][33];
     long pix0 = long(blockIdx.x) * 32; // pixel within item
     long c0 = long(blockIdx.y) * 32;
@@ -321,6 +330,7 @@ __global__ void k_canon_to_chlast(float* __restrict__ out, const cfloat* __restr
 __global__ void k_chlast_to_canon(cfloat* __restrict__ out, const float* __restrict__ in, long inner, long C,
                                   long outer)
 {
+    MDNN_PDL_ENTRY();
     __shared__ cfloat tile[32][33];
     long pix0 = long(blockIdx.x) * 32;
     long c0 = long(blockIdx.y) * 32;
@@ -342,6 +352,7 @@ __global__ void k_chlast_to_canon(cfloat* __restrict__ out, const float* __restr
 
 __global__ void k_check_finite(const float* a, long n, unsigned* flags)
 {
+    MDNN_PDL_ENTRY();
     bool bad = false;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
         bad |= !isfinite(a[i]);
@@ -351,6 +362,7 @@ __global__ void k_check_finite(const float* a, long n, unsigned* flags)
 
 __global__ void k_check_binary(const cfloat* a, long n, unsigned* flags)
 {
+    MDNN_PDL_ENTRY();
     bool bad = false;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         const cfloat v = a[i];
@@ -362,6 +374,7 @@ __global__ void k_check_binary(const cfloat* a, long n, unsigned* flags)
 
 __global__ void k_split(cfloat* out, const cfloat* in, long inner, long outer)
 {
+    MDNN_PDL_ENTRY();
     long n = inner * outer;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long p = i % inner, o = i / inner;
@@ -373,6 +386,7 @@ __global__ void k_split(cfloat* out, const cfloat* in, long inner, long outer)
 
 __global__ void k_join(cfloat* out, const cfloat* in, long inner, long outer)
 {
+    MDNN_PDL_ENTRY();
     long n = inner * outer;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long p = i % inner, o = i / inner;
@@ -388,7 +402,7 @@ void launch_strided_copy(const Dims& dims, cfloat* dst, const Dims& sd, const cf
     if (n == 0)
         return;
     auto m = make_md3(dims, sd, ss, {});
-    k_strided_copy<<<grid_for(n), kThreads, 0, ctx().stream>>>(m, n, dst, src);
+    pdl_launch(k_strided_copy, grid_for(n), kThreads, 0, ctx().stream, m, n, dst, src);
     KERNEL_CHECK();
 }
 
@@ -401,9 +415,9 @@ void launch_layout_convert(const DArray& in, const DArray& out)
     dim3 grid(unsigned((inner + 31) / 32), unsigned((C + 31) / 32), unsigned(outer));
     dim3 block(32, 8);
     if (in.layout == Layout::CANON && out.layout == Layout::CHLAST)
-        k_canon_to_chlast<<<grid, block, 0, ctx().stream>>>(out.fdata(), in.data(), inner, C, outer);
+        pdl_launch(k_canon_to_chlast, grid, block, 0, ctx().stream, out.fdata(), in.data(), inner, C, outer);
     else if (in.layout == Layout::CHLAST && out.layout == Layout::CANON)
-        k_chlast_to_canon<<<grid, block, 0, ctx().stream>>>(out.data(), in.fdata(), inner, C, outer);
+        pdl_launch(k_chlast_to_canon, grid, block, 0, ctx().stream, out.data(), in.fdata(), inner, C, outer);
     else
         throw Error("layout_convert: unsupported pair");
     KERNEL_CHECK();
@@ -429,6 +443,7 @@ void launch_scale(cfloat* out, const cfloat* in, cfloat s, long n)
 namespace {
 __global__ void k_scale_dev(cfloat* out, const cfloat* in, const cfloat* sp, bool cj, long n)
 {
+    MDNN_PDL_ENTRY();
     cfloat s = *sp;
     if (cj)
         s.y = -s.y;
@@ -442,30 +457,32 @@ __global__ void k_scale_dev(cfloat* out, const cfloat* in, const cfloat* sp, boo
 namespace {
 __global__ void k_scale_dev_real(cfloat* out, const cfloat* in, const cfloat* sp, float factor, long n)
 {
+    MDNN_PDL_ENTRY();
     const float s = factor * sp[0].x;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         cfloat v = in[i];
         out[i] = cfloat{s * v.x, s * v.y};
     }
 }
-__global__ void k_real_scalar(cfloat* out, const cfloat* in, float factor) { out[0] = cfloat{factor * in[0].x, 0.f}; }
+__global__ void k_real_scalar(cfloat* out, const cfloat* in, float factor) {
+    MDNN_PDL_ENTRY(); out[0] = cfloat{factor * in[0].x, 0.f}; }
 } // namespace
 
 void launch_scale_dev_real(cfloat* out, const cfloat* in, const cfloat* s, float factor, long n)
 {
-    k_scale_dev_real<<<grid_for(n), kThreads, 0, ctx().stream>>>(out, in, s, factor, n);
+    pdl_launch(k_scale_dev_real, grid_for(n), kThreads, 0, ctx().stream, out, in, s, factor, n);
     KERNEL_CHECK();
 }
 
 void launch_real_scalar(cfloat* out, const cfloat* in, float factor)
 {
-    k_real_scalar<<<1, 1, 0, ctx().stream>>>(out, in, factor);
+    pdl_launch(k_real_scalar, 1, 1, 0, ctx().stream, out, in, factor);
     KERNEL_CHECK();
 }
 
 void launch_scale_dev(cfloat* out, const cfloat* in, const cfloat* s, bool conj_s, long n)
 {
-    k_scale_dev<<<grid_for(n), kThreads, 0, ctx().stream>>>(out, in, s, conj_s, n);
+    pdl_launch(k_scale_dev, grid_for(n), kThreads, 0, ctx().stream, out, in, s, conj_s, n);
     KERNEL_CHECK();
 }
 
@@ -502,12 +519,12 @@ void launch_mul_real_real(cfloat* out, const cfloat* y, const cfloat* d, long n)
 
 void launch_real_chan_split(cfloat* out, const cfloat* in, long inner, long outer)
 {
-    k_split<<<grid_for(inner * outer), kThreads, 0, ctx().stream>>>(out, in, inner, outer);
+    pdl_launch(k_split, grid_for(inner * outer), kThreads, 0, ctx().stream, out, in, inner, outer);
     KERNEL_CHECK();
 }
 void launch_real_chan_join(cfloat* out, const cfloat* in, long inner, long outer)
 {
-    k_join<<<grid_for(inner * outer), kThreads, 0, ctx().stream>>>(out, in, inner, outer);
+    pdl_launch(k_join, grid_for(inner * outer), kThreads, 0, ctx().stream, out, in, inner, outer);
     KERNEL_CHECK();
 }
 
@@ -516,7 +533,7 @@ void launch_bcast_binary(const Dims& dims, cfloat* out, const cfloat* a, const D
 {
     long n = md_size(dims);
     auto m = make_md3(dims, {}, sa, sb);
-    k_bcast_binary<<<grid_for(n), kThreads, 0, ctx().stream>>>(m, n, out, a, b, op);
+    pdl_launch(k_bcast_binary, grid_for(n), kThreads, 0, ctx().stream, m, n, out, a, b, op);
     KERNEL_CHECK();
 }
 
@@ -604,7 +621,7 @@ void launch_fmac_generic(const Dims& iter, cfloat* out, const Dims& so, const cf
             o1 += q * d.s1;
             o2 += q * d.s2;
         }
-        k_fmac_gather<<<grid_for(nout), kThreads, 0, ctx().stream>>>(p, nout, nred, out + oo, in1 + o1, in2 + o2,
+        pdl_launch(k_fmac_gather, grid_for(nout), kThreads, 0, ctx().stream, p, nout, nred, out + oo, in1 + o1, in2 + o2,
                                                                      conj2);
         KERNEL_CHECK();
     }
@@ -617,14 +634,14 @@ void launch_copy(cfloat* dst, const cfloat* src, long n)
 
 void launch_check_finite(const cfloat* a, long n)
 {
-    k_check_finite<<<grid_for(2 * n), kThreads, 0, ctx().stream>>>(reinterpret_cast<const float*>(a), 2 * n,
+    pdl_launch(k_check_finite, grid_for(2 * n), kThreads, 0, ctx().stream, reinterpret_cast<const float*>(a), 2 * n,
                                                                    ctx().d_errflags);
     KERNEL_CHECK();
 }
 
 void launch_check_binary(const cfloat* a, long n)
 {
-    k_check_binary<<<int(std::min<long>(grid_for(n), 64)), kThreads, 0, ctx().stream>>>(a, n, ctx().d_errflags);
+    pdl_launch(k_check_binary, int(std::min<long>(grid_for(n), 64)), kThreads, 0, ctx().stream, a, n, ctx().d_errflags);
     KERNEL_CHECK();
 }
 

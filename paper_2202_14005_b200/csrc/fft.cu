@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(256) k_fft_lines(cfloat* __restrict__ out, con
                                                    fftd::Plan plan, long sd, long outer, int W, int LD, int mode,
                                                    bool inverse, float scale)
 {
+    MDNN_PDL_ENTRY();
     extern __shared__ float2 smem[];
     const int n = plan.n;
     float2* a = smem;
@@ -213,7 +214,7 @@ void launch_fft_dim(cfloat* out, const cfloat* in, const Dims& dims, int dim, bo
     long blocks = mode == 0 ? ((sd + W - 1) / W) * outer : (outer + W - 1) / W;
     float scale = float(1.0 / std::sqrt(double(n)));
     ProfScope prof("fft", 16.0 * double(n) * double(sd) * double(outer));
-    k_fft_lines<<<unsigned(blocks), 256, smem, c.stream>>>(out, in, plan, sd, outer, W, LD, mode, inverse, scale);
+    pdl_launch(k_fft_lines, unsigned(blocks), 256, smem, c.stream, out, in, plan, sd, outer, W, LD, mode, inverse, scale);
     KERNEL_CHECK();
 }
 

@@ -81,6 +81,7 @@ __device__ __forceinline__ float gauss2(float z, float mu, float k2)
 __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z, const cfloat* __restrict__ w,
                           const cfloat* __restrict__ gin, const float* __restrict__ mu, RbfGeom g, int mode)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float smu[kMaxW];
     extern __shared__ float sw[]; // [nf][nw] real parts
     for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
@@ -140,6 +141,7 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
                             const float* __restrict__ mu, RbfGeom g, int nchunk, cfloat* __restrict__ dz,
                             const cfloat* __restrict__ w)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float smu[kMaxW];
     __shared__ float swf[kMaxW];
     __shared__ double red[kMaxW][8];
@@ -232,6 +234,7 @@ __global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, c
                                                    RbfGeom g, int nchunk, cfloat* __restrict__ dz,
                                                    const cfloat* __restrict__ w)
 {
+    MDNN_PDL_ENTRY();
     constexpr int NW2 = 2 * K + 1;
     __shared__ float smu[kMaxW];
     __shared__ float swf[kMaxW + 2 * K]; // weights, zero outside [0, nw)
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, c
 
 __global__ void k_rbf_wfinal(cfloat* dw, const double* part, RbfGeom g, int nchunk)
 {
+    MDNN_PDL_ENTRY();
     const long n = g.nf * g.nw;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         const long f = i / g.nw, j = i % g.nw;
@@ -358,25 +362,25 @@ void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, c
         throw ConfigError("rbf: more than 64 basis functions not supported on device");
     // algorithmic bytes: z in, y out (complex, 8 B each)
     ProfScope prof("rbf", 16.0 * double(g.inner) * g.nf * g.outer);
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(y, z, w, nullptr, mu, g, 0);
+    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, y, z, w, nullptr, mu, g, 0);
     KERNEL_CHECK();
 }
 
 void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
 {
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(dz, z, w, dy, mu, g, 1);
+    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, dz, z, w, dy, mu, g, 1);
     KERNEL_CHECK();
 }
 
 void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
 {
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(dy, z, w, dz, mu, g, 1);
+    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, dy, z, w, dz, mu, g, 1);
     KERNEL_CHECK();
 }
 
 void rbf_deriv_w(cfloat* dy, const cfloat* dw, const cfloat* z, const float* mu, const RbfGeom& g)
 {
-    k_rbf_map<<<grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream>>>(dy, z, dw, nullptr, mu, g, 2);
+    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, dy, z, dw, nullptr, mu, g, 2);
     KERNEL_CHECK();
 }
 
@@ -408,7 +412,7 @@ bool launch_wgrad_w9(double* part, const cfloat* dy, const cfloat* z, const floa
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
         granted = bytes;
     }
-    k_rbf_wgrad_w<9><<<dim3(nchunk, unsigned(g.nf)), kT, bytes, ctx().stream>>>(part, dy, z, mu, g, nchunk, dz, w);
+    pdl_launch(k_rbf_wgrad_w<9>, dim3(nchunk, unsigned(g.nf)), kT, bytes, ctx().stream, part, dy, z, mu, g, nchunk, dz, w);
     KERNEL_CHECK();
     return true;
 }
@@ -421,11 +425,10 @@ void rbf_adjoint_w(cfloat* dw, const cfloat* dy, const cfloat* z, const float* m
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
     if (!launch_wgrad_w9(part, dy, z, mu, g, nchunk, nullptr, nullptr)) {
-        k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
-            part, dy, z, mu, g, nchunk, nullptr, nullptr);
+        pdl_launch(k_rbf_wgrad, dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream, part, dy, z, mu, g, nchunk, nullptr, nullptr);
         KERNEL_CHECK();
     }
-    k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
+    pdl_launch(k_rbf_wfinal, 4, 256, 0, c.stream, dw, part, g, nchunk);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }
@@ -441,11 +444,10 @@ void rbf_adjoint_zw(cfloat* dz, cfloat* dw, const cfloat* dy, const cfloat* z, c
     double* part;
     CUDA_CHECK(cudaMallocAsync(&part, sizeof(double) * g.nf * g.nw * nchunk, c.stream));
     if (!launch_wgrad_w9(part, dy, z, mu, g, nchunk, dz, w)) {
-        k_rbf_wgrad<<<dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream>>>(
-            part, dy, z, mu, g, nchunk, dz, w);
+        pdl_launch(k_rbf_wgrad, dim3(nchunk, unsigned(g.nf)), kT, rbf_wgrad_smem(g), c.stream, part, dy, z, mu, g, nchunk, dz, w);
         KERNEL_CHECK();
     }
-    k_rbf_wfinal<<<4, 256, 0, c.stream>>>(dw, part, g, nchunk);
+    pdl_launch(k_rbf_wfinal, 4, 256, 0, c.stream, dw, part, g, nchunk);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(part, c.stream));
 }

@@ -10,6 +10,7 @@ namespace {
 // one CTA per line y: any nonzero over (x, everything outside x/y)
 __global__ void k_estimate_pattern(float2* p, const float2* __restrict__ k, long X, long Y, long rest)
 {
+    MDNN_PDL_ENTRY();
     const long y = blockIdx.x;
     int any = 0;
     for (long r = 0; r < rest && !any; r++)
@@ -26,6 +27,7 @@ __global__ void k_estimate_pattern(float2* p, const float2* __restrict__ k, long
 // computed in double (order-independent: max is exact)
 __global__ void k_item_maxabs(double* out, const float2* __restrict__ x, long per)
 {
+    MDNN_PDL_ENTRY();
     const long b = blockIdx.x;
     double m = 0;
     for (long i = threadIdx.x; i < per; i += blockDim.x) {
@@ -48,6 +50,7 @@ __global__ void k_item_maxabs(double* out, const float2* __restrict__ x, long pe
 __global__ void k_scale_items(float2* out, const float2* __restrict__ in, const float2* __restrict__ s, long per,
                               long n, bool invert)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < per * n; i += long(gridDim.x) * blockDim.x) {
         float2 sv = s[i / per];
         if (invert) { // complex reciprocal of a real scale
@@ -63,20 +66,20 @@ __global__ void k_scale_items(float2* out, const float2* __restrict__ in, const 
 
 void launch_estimate_pattern(cfloat* pattern, const cfloat* kspace, long X, long Y, long rest)
 {
-    k_estimate_pattern<<<unsigned(Y), 256, 0, ctx().stream>>>(pattern, kspace, X, Y, rest);
+    pdl_launch(k_estimate_pattern, unsigned(Y), 256, 0, ctx().stream, pattern, kspace, X, Y, rest);
     KERNEL_CHECK();
 }
 
 void launch_item_maxabs(double* out, const cfloat* x, long per_item, long items)
 {
-    k_item_maxabs<<<unsigned(items), 256, 0, ctx().stream>>>(out, x, per_item);
+    pdl_launch(k_item_maxabs, unsigned(items), 256, 0, ctx().stream, out, x, per_item);
     KERNEL_CHECK();
 }
 
 void launch_scale_items(cfloat* out, const cfloat* in, const cfloat* scale, long per_item, long items, bool invert)
 {
     const long n = per_item * items;
-    k_scale_items<<<int(std::min<long>((n + 255) / 256, 4096)), 256, 0, ctx().stream>>>(out, in, scale, per_item, items,
+    pdl_launch(k_scale_items, int(std::min<long>((n + 255) / 256, 4096)), 256, 0, ctx().stream, out, in, scale, per_item, items,
                                                                                        invert);
     KERNEL_CHECK();
 }

@@ -48,6 +48,7 @@ struct PatStr {
 __global__ void k_coil_mul(cfloat* __restrict__ u, const cfloat* __restrict__ x, const cfloat* __restrict__ coils,
                            long XY, long C, long M, long B)
 {
+    MDNN_PDL_ENTRY();
     const long n = XY * C * B;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long p = i % XY, c = (i / XY) % C, b = i / (XY * C);
@@ -65,6 +66,7 @@ __global__ void k_coil_mul(cfloat* __restrict__ u, const cfloat* __restrict__ x,
 __global__ void k_coil_adj(cfloat* __restrict__ x, const cfloat* __restrict__ u, const cfloat* __restrict__ coils,
                            long XY, long C, long M, long B)
 {
+    MDNN_PDL_ENTRY();
     const long n = XY * M * B;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long p = i % XY, m = (i / XY) % M, b = i / (XY * M);
@@ -82,6 +84,7 @@ __global__ void k_coil_adj(cfloat* __restrict__ x, const cfloat* __restrict__ u,
 __global__ void k_pattern_mul(cfloat* __restrict__ out, const cfloat* __restrict__ u, const cfloat* __restrict__ pat,
                               long X, long Y, long C, long B, PatStr ps)
 {
+    MDNN_PDL_ENTRY();
     const long n = X * Y * C * B;
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x) {
         long x = i % X, y = (i / X) % Y, c = (i / (X * Y)) % C, b = i / (X * Y * C);
@@ -258,6 +261,7 @@ struct NormalArgs {
 
 __global__ void __launch_bounds__(kT) k_normal_y(NormalArgs a, fftd::Plan plan)
 {
+    MDNN_PDL_ENTRY();
     extern __shared__ float2 sm[];
     const int Y = int(a.Y), W = a.W, M = int(a.M);
     const int nYW = Y * W;
@@ -427,7 +431,7 @@ void launch_normal_y(NormalArgs a, const SenseGeom& g)
     const double xyb = double(g.X) * g.Y * g.B;
     const double work = 8.0 * xyb * (g.C * g.M + (a.mode == 1 ? 4 : 2) * g.M);
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    k_normal_y<<<unsigned(nxb * g.B), kT, smem, c.stream>>>(a, plan);
+    pdl_launch(k_normal_y, unsigned(nxb * g.B), kT, smem, c.stream, a, plan);
     KERNEL_CHECK();
 }
 
@@ -440,6 +444,7 @@ long normal_y_ctas(const SenseGeom& g)
 // ---- CG helper kernels -------------------------------------------------------
 __global__ void k_cg_init(CgDev* st, const double2* bsum)
 {
+    MDNN_PDL_ENTRY();
     double s = bsum[0].x;
     st->bnorm = sqrt(s);
     st->rs[0] = float(s);
@@ -449,6 +454,7 @@ __global__ void k_cg_init(CgDev* st, const double2* bsum)
 // generic path: p-update (prologue) as its own kernel
 __global__ void k_cg_pupdate(CgDev* st, int it, cfloat* p, const cfloat* r, long n, unsigned* errflags, int* skip)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float s_beta;
     if (threadIdx.x == 0)
         s_beta = cg_prologue(st, it, errflags);
@@ -466,6 +472,7 @@ __global__ void k_cg_pupdate(CgDev* st, int it, cfloat* p, const cfloat* r, long
 
 __global__ void k_cg_pap(CgDev* st, int it, const cfloat* p, const cfloat* ap, long n)
 {
+    MDNN_PDL_ENTRY();
     if (st->done_at <= it)
         return;
     double2 part{0, 0};
@@ -481,6 +488,7 @@ __global__ void k_cg_pap(CgDev* st, int it, const cfloat* p, const cfloat* ap, l
 __global__ void k_cg_update(CgDev* st, int it, cfloat* x, cfloat* r, const cfloat* p, const cfloat* ap, long n,
                             unsigned* errflags)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float s_alpha;
     if (threadIdx.x == 0)
         s_alpha = cg_alpha(st, it, errflags);
@@ -506,6 +514,7 @@ __global__ void k_cg_update(CgDev* st, int it, cfloat* x, cfloat* r, const cfloa
 
 __global__ void k_cg_final(CgDev* st, double* status_out, unsigned* errflags)
 {
+    MDNN_PDL_ENTRY();
     // CgStatus after the loop (recon.hpp:176-178)
     int it = st->done_at;
     bool conv = false;
@@ -535,20 +544,20 @@ __global__ void k_cg_final(CgDev* st, double* status_out, unsigned* errflags)
 void launch_coil_mul(cfloat* u, const cfloat* x, const cfloat* coils, const SenseGeom& g)
 {
     long XY = g.X * g.Y;
-    k_coil_mul<<<grid_for(XY * g.C * g.B), kT, 0, ctx().stream>>>(u, x, coils, XY, g.C, g.M, g.B);
+    pdl_launch(k_coil_mul, grid_for(XY * g.C * g.B), kT, 0, ctx().stream, u, x, coils, XY, g.C, g.M, g.B);
     KERNEL_CHECK();
 }
 
 void launch_coil_adj(cfloat* x, const cfloat* u, const cfloat* coils, const SenseGeom& g)
 {
     long XY = g.X * g.Y;
-    k_coil_adj<<<grid_for(XY * g.M * g.B), kT, 0, ctx().stream>>>(x, u, coils, XY, g.C, g.M, g.B);
+    pdl_launch(k_coil_adj, grid_for(XY * g.M * g.B), kT, 0, ctx().stream, x, u, coils, XY, g.C, g.M, g.B);
     KERNEL_CHECK();
 }
 
 void launch_pattern_mul(cfloat* out, const cfloat* u, const cfloat* pattern, const SenseGeom& g)
 {
-    k_pattern_mul<<<grid_for(g.X * g.Y * g.C * g.B), kT, 0, ctx().stream>>>(out, u, pattern, g.X, g.Y, g.C, g.B,
+    pdl_launch(k_pattern_mul, grid_for(g.X * g.Y * g.C * g.B), kT, 0, ctx().stream, out, u, pattern, g.X, g.Y, g.C, g.B,
                                                                              pat_strides(g));
     KERNEL_CHECK();
 }
@@ -612,7 +621,7 @@ static bool sense_normal_rank(cfloat* out, const cfloat* x, const cfloat* coils,
     a.check_pattern = 0;
     launch_rank(rp, a, coils, g, pl);
     if (rp.planes > 1) {
-        k_rank_merge<<<grid_for(n), 256, 0, ctx().stream>>>(out, plane1.data(), rank_split_flags(g, rp, pl),
+        pdl_launch(k_rank_merge, grid_for(n), 256, 0, ctx().stream, out, plane1.data(), rank_split_flags(g, rp, pl),
                                                             int(g.X), int(g.Y * g.B), int(g.Y), int(rp.nxb),
                                                             rp.W == 8 ? 3 : 2, n);
         KERNEL_CHECK();
@@ -731,7 +740,7 @@ void cg_start(const CgMem& m, cfloat* x, const cfloat* b, cfloat* r, cfloat* p, 
     launch_copy(r, b, n);
     launch_copy(p, b, n);
     launch_zdot(reinterpret_cast<double*>(cg_bsum(m)), b, b, n);
-    k_cg_init<<<1, 1, 0, c.stream>>>(m.st, cg_bsum(m));
+    pdl_launch(k_cg_init, 1, 1, 0, c.stream, m.st, cg_bsum(m));
     KERNEL_CHECK();
 }
 
@@ -747,17 +756,17 @@ void cg_generic_device(cfloat* x, const cfloat* b, long n, const CgApply& apply,
     cg_start(m, x, b, r.data(), p.data(), n);
     int* d_skip = reinterpret_cast<int*>(cg_bsum(m) + 1);
     for (int it = 0; it < max_iter; it++) {
-        k_cg_pupdate<<<n_upd, kT, 0, c.stream>>>(m.st, it, p.data(), r.data(), n, c.d_errflags, d_skip);
+        pdl_launch(k_cg_pupdate, n_upd, kT, 0, c.stream, m.st, it, p.data(), r.data(), n, c.d_errflags, d_skip);
         KERNEL_CHECK();
         // S p is always evaluated; iterations after convergence are discarded
         // by the device-side state (no host synchronisation in the loop)
         apply(p.data(), ap.data());
-        k_cg_pap<<<n_upd, kT, 0, c.stream>>>(m.st, it, p.data(), ap.data(), n);
+        pdl_launch(k_cg_pap, n_upd, kT, 0, c.stream, m.st, it, p.data(), ap.data(), n);
         KERNEL_CHECK();
-        k_cg_update<<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), p.data(), ap.data(), n, c.d_errflags);
+        pdl_launch(k_cg_update, n_upd, kT, 0, c.stream, m.st, it, x, r.data(), p.data(), ap.data(), n, c.d_errflags);
         KERNEL_CHECK();
     }
-    k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
+    pdl_launch(k_cg_final, 1, 1, 0, c.stream, m.st, status_out, c.d_errflags);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(m.mem, c.stream));
 }
@@ -840,7 +849,7 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
                                  rp.W == 8 ? 3 : 2, n, c.d_errflags);
             } else {
                 ProfScope prof("cg_update_rank", 8.0 * n * 7);
-                k_cg_update_rank<<<n_updr, 512, 0, c.stream>>>(m.st, it, x, r.data(), pdir(it + 1), ap.data(),
+                pdl_launch(k_cg_update_rank, n_updr, 512, 0, c.stream, m.st, it, x, r.data(), pdir(it + 1), ap.data(),
                                                               ap.data() + n, rank_split_flags(g, rp, pl), int(g.X),
                                                               int(g.Y * g.B), int(g.Y), int(rp.nxb),
                                                               rp.W == 8 ? 3 : 2, n, c.d_errflags);
@@ -848,10 +857,10 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             KERNEL_CHECK();
         }
         if (defer) {
-            k_cg_x_sum<<<grid_for(n / 2), 256, 0, c.stream>>>(m.st, x, pb.data(), n);
+            pdl_launch(k_cg_x_sum, grid_for(n / 2), 256, 0, c.stream, m.st, x, pb.data(), n);
             KERNEL_CHECK();
         }
-        k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
+        pdl_launch(k_cg_final, 1, 1, 0, c.stream, m.st, status_out, c.d_errflags);
         KERNEL_CHECK();
         CUDA_CHECK(cudaFreeAsync(m.mem, c.stream));
         return;
@@ -886,11 +895,11 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
             a.errflags = c.d_errflags;
             a.nsplit = NS;
             dispatch_fast(a, P[(it + 1) & 1], n);
-            k_cg_update_planes<<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(), n,
+            pdl_launch(k_cg_update_planes, n_upd, kT, 0, c.stream, m.st, it, x, r.data(), P[(it + 1) & 1], ap.data(), n,
                                                           NS, n, c.d_errflags);
             KERNEL_CHECK();
         }
-        k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
+        pdl_launch(k_cg_final, 1, 1, 0, c.stream, m.st, status_out, c.d_errflags);
         KERNEL_CHECK();
         CUDA_CHECK(cudaFreeAsync(m.mem, c.stream));
         return;
@@ -919,10 +928,10 @@ void cg_normal_device(cfloat* x, const cfloat* b, const cfloat* coils, const cfl
         a.cg = m.st;
         a.errflags = c.d_errflags;
         launch_normal_y(a, g);
-        k_cg_update<<<n_upd, kT, 0, c.stream>>>(m.st, it, x, r.data(), p.data(), ap.data(), n, c.d_errflags);
+        pdl_launch(k_cg_update, n_upd, kT, 0, c.stream, m.st, it, x, r.data(), p.data(), ap.data(), n, c.d_errflags);
         KERNEL_CHECK();
     }
-    k_cg_final<<<1, 1, 0, c.stream>>>(m.st, status_out, c.d_errflags);
+    pdl_launch(k_cg_final, 1, 1, 0, c.stream, m.st, status_out, c.d_errflags);
     KERNEL_CHECK();
     CUDA_CHECK(cudaFreeAsync(m.mem, c.stream));
 }

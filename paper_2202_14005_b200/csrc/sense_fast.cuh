@@ -77,6 +77,7 @@ template<int N1, int N2, int W>
 __global__ void __launch_bounds__(fast_threads<N1, N2, W>(), (fast_min_blocks<N1, N2, W>()))
     k_normal_fast(NormalArgs a, const float2* __restrict__ tw, cfloat* __restrict__ p_out, long plane)
 {
+    MDNN_PDL_ENTRY();
     using namespace fftd;
     constexpr int Y = N1 * N2;
     constexpr int NT = fast_threads<N1, N2, W>();
@@ -406,7 +407,7 @@ void launch_fast(NormalArgs a, cfloat* p_out, long plane)
     const double xyb = double(a.X) * a.Y * a.B;
     const double work = 8.0 * xyb * (a.C + (a.mode == 1 ? 4 : 2));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    kern<<<unsigned(nxb * a.B * a.nsplit), fast_threads<N1, N2, W>(), smem, ctx().stream>>>(a, fast_twiddles(N1, N2), p_out, plane);
+    pdl_launch(kern, unsigned(nxb * a.B * a.nsplit), fast_threads<N1, N2, W>(), smem, ctx().stream, a, fast_twiddles(N1, N2), p_out, plane);
     KERNEL_CHECK();
 }
 
@@ -459,6 +460,7 @@ int fast_nsplit(const SenseGeom& g)
 __global__ void k_cg_update_planes(CgDev* st, int it, cfloat* x, cfloat* r, const cfloat* p, const cfloat* ap,
                                    long n, int nplanes, long plane, unsigned* errflags)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float s_alpha;
     if (threadIdx.x == 0)
         s_alpha = cg_alpha(st, it, errflags);

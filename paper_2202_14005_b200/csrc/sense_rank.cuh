@@ -49,7 +49,7 @@ void launch_ex(bool pdl, bool coop, void (*kern)(KArgs...), dim3 grid, dim3 bloc
     cfg.stream = ctx().stream;
     cudaLaunchAttribute at[2];
     int na = 0;
-    if (pdl) {
+    if (pdl && g_pdl) {
         at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         at[na++].val.programmaticStreamSerializationAllowed = 1;
     }
@@ -234,6 +234,7 @@ struct RankPlanRec {
 template<int N1, int N2>
 __global__ void __launch_bounds__(RankCfg<N1, N2>::NT) k_rank_plan(RankArgs a, unsigned char* plans)
 {
+    MDNN_PDL_ENTRY();
     unsigned char* rec = plans + RankPlanRec<N1, N2>::BYTES * blockIdx.x;
     rank_build_plan<N1, N2>(*reinterpret_cast<RankPlanSm<N1, N2>*>(rec), a, int(blockIdx.x),
                             reinterpret_cast<float2*>(rec + RankPlanRec<N1, N2>::PL), a.tw);
@@ -259,6 +260,7 @@ template<int N1, int N2>
 __global__ void __launch_bounds__(RankCfg<N1, N2>::NT, RankCfg<N1, N2>::MINB)
     k_normal_rank(RankArgs a, const __grid_constant__ CUtensorMap tmap, const unsigned char* __restrict__ plans)
 {
+    MDNN_PDL_ENTRY();
     using namespace fftd;
     using Cfg = RankCfg<N1, N2>;
     constexpr int Y = Cfg::Y, W = Cfg::W, JH = Cfg::JH, TMAX = Cfg::TMAX, N2P = Cfg::N2P;
@@ -594,6 +596,7 @@ __global__ void __launch_bounds__(256) k_rank_merge(cfloat* out, const cfloat* p
                                                     const unsigned char* __restrict__ split, int X, int rows, int Y,
                                                     int nxb, int wshift, long pstride)
 {
+    MDNN_PDL_ENTRY();
     const int X2 = X >> 1;
     for (int row = blockIdx.x; row < rows; row += gridDim.x) {
         const int sb = (row / Y) * nxb;
@@ -626,6 +629,7 @@ __global__ void __launch_bounds__(512) k_cg_update_rank(CgDev* st, int it, cfloa
                                                         const unsigned char* __restrict__ split, int X, int rows,
                                                         int Y, int nxb, int wshift, long pstride, unsigned* errflags)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float s_alpha;
     if (threadIdx.x == 0)
         s_alpha = cg_alpha(st, it, errflags);
@@ -790,12 +794,10 @@ __global__ void __launch_bounds__(256) k_cg_update_r(CgDev* st, int it, cfloat* 
                                                      const unsigned char* __restrict__ split, int X, int rows, int Y,
                                                      int nxb, int wshift, long pstride, unsigned* errflags)
 {
+    MDNN_PDL_ENTRY();
     __shared__ float s_alpha;
-    sm100::griddep_wait(); // Ap and <p, Ap> of the A^H A launch before (PDL)
-    if (threadIdx.x == 0) {
-        sm100::griddep_launch();
+    if (threadIdx.x == 0)
         s_alpha = cg_alpha(st, it, errflags);
-    }
     __syncthreads();
     const float al = s_alpha;
     if (!(al > 0.f))
@@ -811,6 +813,7 @@ __global__ void __launch_bounds__(256) k_cg_update_r(CgDev* st, int it, cfloat* 
 __global__ void __launch_bounds__(256) k_cg_x_sum(const CgDev* __restrict__ st, cfloat* __restrict__ x,
                                                   const cfloat* __restrict__ P, long n)
 {
+    MDNN_PDL_ENTRY();
     const int nit = min(st->done_at, st->max_iter);
     const long npair = n >> 1;
     float4* x4 = reinterpret_cast<float4*>(x);
@@ -939,7 +942,7 @@ void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const un
     const double xyb = double(g.X) * g.Y * g.B;
     const double work = 8.0 * xyb * (g.C + (a.mode == 1 ? 4 : 2));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
-    kern<<<a.G, nthreads, Cfg::SMEM, ctx().stream>>>(a, m, plans);
+    pdl_launch(kern, a.G, nthreads, Cfg::SMEM, ctx().stream, a, m, plans);
     KERNEL_CHECK();
 }
 
@@ -947,7 +950,7 @@ void launch_rank_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const un
 template<int N1, int N2>
 void launch_rank_plan_t(const RankArgs& a, unsigned char* plans, int nitems)
 {
-    k_rank_plan<N1, N2><<<nitems, RankCfg<N1, N2>::NT, 0, ctx().stream>>>(a, plans);
+    pdl_launch(k_rank_plan<N1, N2>, nitems, RankCfg<N1, N2>::NT, 0, ctx().stream, a, plans);
     KERNEL_CHECK();
 }
 

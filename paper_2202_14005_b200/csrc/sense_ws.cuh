@@ -308,6 +308,7 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
     k_normal_ws(RankArgs a, const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmx,
                 const __grid_constant__ CUtensorMap tmp, const unsigned char* __restrict__ plans)
 {
+    MDNN_PDL_ENTRY();
     using Cfg = WsCfg<N1, N2>;
     constexpr int Y = Cfg::Y, W = Cfg::W, N2P = Cfg::N2P, TMAX = Cfg::TMAX, RP = Cfg::RP;
     constexpr int NT_AC = Cfg::NT_AC, NT_B = Cfg::NT_B, NSLOT = Cfg::NSLOT;
@@ -342,12 +343,9 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
         }
     };
 
-    // launched with programmatic serialisation in the CG loop: the previous kernel's
-    // r / p / CG scalars are read only after this wait; from here on the next
-    // kernel (the CG update) may be scheduled
-    sm100::griddep_wait();
+    // (MDNN_PDL_ENTRY above: the previous kernel's r / p / CG scalars are read only
+    // after its wait; from there on the next kernel may be scheduled)
     if (tid == 0) {
-        sm100::griddep_launch();
         for (int s = 0; s < NSLOT; s++) {
             sm100::mbar_init(&bar_full[s], 1);
             sm100::mbar_init(&bar_empty[s], NT_AC);
@@ -810,7 +808,9 @@ void launch_ws_t(RankArgs a, const cfloat* coils, const SenseGeom& g, const unsi
         attr = true;
     }
     const double xyb = double(g.X) * g.Y * g.B;
-    const double work = 8.0 * xyb * (g.C + (a.mode == 1 ? 4 : 2));
+    // algorithmic bytes: coils once, x (r, p_prev, p_out) and Ap; the fused CG
+    // update adds r and Ap read, r written
+    const double work = 8.0 * xyb * (g.C + (a.mode == 1 ? 4 : 2) + (a.r_upd ? 3 : 0));
     ProfScope prof(a.mode == 1 ? "sense_normal_y_cg" : "sense_normal_y", work);
     launch_ex(g_cg_pdl, a.r_upd != nullptr && g_cg_fuse == 2, k_normal_ws<N1, N2>, dim3(a.G), dim3(Cfg::NT), size_t(Cfg::SMEM), a, m, mx, mp,
               plans);

@@ -18,6 +18,7 @@ int grid_for(long n)
 
 __global__ void k_diff(cfloat* __restrict__ d, const cfloat* __restrict__ p, const cfloat* __restrict__ r, long n)
 {
+    MDNN_PDL_ENTRY();
     for (long i = blockIdx.x * long(blockDim.x) + threadIdx.x; i < n; i += long(gridDim.x) * blockDim.x)
         d[i] = float2{p[i].x - r[i].x, p[i].y - r[i].y};
 }
@@ -26,6 +27,7 @@ __global__ void k_adam(cfloat* __restrict__ th, cfloat* __restrict__ m, float* _
                        const cfloat* __restrict__ g, long n, float lr, float b1, float b2, float eps, float c1,
                        float c2, float gscale, bool real_w, bool nonneg)
 {
+    MDNN_PDL_ENTRY();
     for (long k = blockIdx.x * long(blockDim.x) + threadIdx.x; k < n; k += long(gridDim.x) * blockDim.x) {
         float2 gv = g[k];
         gv.x *= gscale;
@@ -54,6 +56,7 @@ __global__ void k_adam(cfloat* __restrict__ th, cfloat* __restrict__ m, float* _
 __global__ void k_sgd(float2* __restrict__ th, const float2* __restrict__ g, long n, float lr, float gscale,
                       bool real_w, bool nonneg)
 {
+    MDNN_PDL_ENTRY();
     for (long k = blockIdx.x * long(blockDim.x) + threadIdx.x; k < n; k += long(gridDim.x) * blockDim.x) {
         float2 gv = g[k];
         gv.x *= gscale;
@@ -71,6 +74,7 @@ __global__ void k_sgd(float2* __restrict__ th, const float2* __restrict__ g, lon
 
 __global__ void k_prox_nonneg(float2* w, long n)
 {
+    MDNN_PDL_ENTRY();
     for (long k = blockIdx.x * long(blockDim.x) + threadIdx.x; k < n; k += long(gridDim.x) * blockDim.x) {
         const float2 t = w[k];
         w[k] = float2{t.x > 0.f ? t.x : 0.f, 0.f};
@@ -81,19 +85,19 @@ __global__ void k_prox_nonneg(float2* w, long n)
 
 void sgd_update(cfloat* theta, const cfloat* g, long n, float lr, float gscale, bool real_weights, bool nonneg_prox)
 {
-    k_sgd<<<grid_for(n), kT, 0, ctx().stream>>>(theta, g, n, lr, gscale, real_weights, nonneg_prox);
+    pdl_launch(k_sgd, grid_for(n), kT, 0, ctx().stream, theta, g, n, lr, gscale, real_weights, nonneg_prox);
     KERNEL_CHECK();
 }
 
 void launch_prox_nonneg(cfloat* w, long n)
 {
-    k_prox_nonneg<<<grid_for(n), kT, 0, ctx().stream>>>(w, n);
+    pdl_launch(k_prox_nonneg, grid_for(n), kT, 0, ctx().stream, w, n);
     KERNEL_CHECK();
 }
 
 void mse_forward(cfloat* loss, cfloat* diff, const cfloat* p, const cfloat* r, long n)
 {
-    k_diff<<<grid_for(n), kT, 0, ctx().stream>>>(diff, p, r, n);
+    pdl_launch(k_diff, grid_for(n), kT, 0, ctx().stream, diff, p, r, n);
     KERNEL_CHECK();
     launch_iso_reduce(loss, diff, diff, n, 1, 1, 2, float(1.0 / double(n)));
 }
@@ -101,7 +105,7 @@ void mse_forward(cfloat* loss, cfloat* diff, const cfloat* p, const cfloat* r, l
 void adam_update(cfloat* theta, cfloat* m, float* v, const cfloat* g, long n, float lr, float b1, float b2,
                  float eps, float c1, float c2, float gscale, bool real_weights, bool nonneg_prox)
 {
-    k_adam<<<grid_for(n), kT, 0, ctx().stream>>>(theta, m, v, g, n, lr, b1, b2, eps, c1, c2, gscale, real_weights,
+    pdl_launch(k_adam, grid_for(n), kT, 0, ctx().stream, theta, m, v, g, n, lr, b1, b2, eps, c1, c2, gscale, real_weights,
                                                  nonneg_prox);
     KERNEL_CHECK();
 }
