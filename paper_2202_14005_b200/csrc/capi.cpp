@@ -181,6 +181,8 @@ int mdnn_set_option(const char* key, long value)
             rbf_window_enable(value != 0);
         else if (k == "rank_rr")
             rank_rr_enable(value != 0);
+        else if (k == "rank_vh")
+            rank_vh_set(int(value));
         else if (k == "sense_ws")
             sense_ws_enable(value != 0);
         else if (k == "cg_pdl")

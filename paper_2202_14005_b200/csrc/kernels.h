@@ -161,6 +161,7 @@ void sense_ws_enable(bool on);
 void cg_pdl_enable(bool on); // programmatic dependent launch in the CG loop
 void cg_fuse_enable(int mode); // CG r-update fused into the ws A^H A launch (grid barrier)
 void rank_rr_enable(bool on);
+void rank_vh_set(int vh); // ws A^H A: per-strip overhead weight of the cost-balanced unit ranges (0: equal counts)
 void cg_defer_x_enable(bool on);
 bool rank_enabled();
 // test hook: auto-layout convs store multi-channel activations channels-last

@@ -946,6 +946,7 @@ void sense_ws_enable(bool on) { g_sense_ws = on; }
 void cg_pdl_enable(bool on) { g_cg_pdl = on; }
 void cg_fuse_enable(int mode) { g_cg_fuse = mode; }
 void rank_rr_enable(bool on) { g_rank_rr = on; }
+void rank_vh_set(int vh) { g_rank_vh = vh < 0 ? 0 : vh; }
 void cg_defer_x_enable(bool on) { g_cg_defer_x = on; }
 bool rank_enabled() { return g_rank_enabled; }
 

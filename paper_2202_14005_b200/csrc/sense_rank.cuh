@@ -66,7 +66,8 @@ void launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, s
 {
     launch_ex(pdl, false, kern, grid, block, smem, std::forward<Args>(args)...);
 }
-bool g_rank_rr = true;  // whole strips round robin for 32-B strips (RankPlan::rr)
+bool g_rank_rr = true;
+int g_rank_vh = 9;     // ws kernel: segment overhead ~2.25 units (RANK_VQ = 4; 0: equal unit counts)  // whole strips round robin for 32-B strips (RankPlan::rr)
 
 constexpr int rank_nbox(int Y)
 {
@@ -115,6 +116,7 @@ struct RankArgs {
     long units;           // strips * C
     int G;                // CTAs
     int rr;               // 1: CTA g owns whole strips g, g + G, g + 2G, ... (no split strips)
+    int vh;               // contiguous ranges: per-strip overhead weight (rank_ubegin; 0: equal unit counts)
     PatStr ps;
     int mode, it;
     CgDev* cg;
@@ -126,23 +128,53 @@ struct RankArgs {
     int check_pattern;    // k_rank_plan: also run the binary-pattern check
 };
 
-// CTA owning unit u, for ranges [floor(U g / G), floor(U (g+1) / G))
-__host__ __device__ __forceinline__ long rank_owner(long u, long U, long G) { return ((u + 1) * G + U - 1) / U - 1; }
-__host__ __device__ __forceinline__ bool rank_split(long s, long C, long U, long G)
+// Contiguous unit ranges.  vh = 0: [floor(U g / G), floor(U (g+1) / G)).
+// vh > 0 (k_normal_ws): ranges of equal *cost*, where a unit weighs RANK_VQ and
+// every strip an extra vh for its segment open + epilogue (x strip load, store,
+// <p, Ap>): unit u = (s, c) sits at virtual position s (C RANK_VQ + vh) + vh +
+// c RANK_VQ of V = strips (C RANK_VQ + vh), and CTA g owns the units whose
+// position lies in [floor(V g / G), floor(V (g+1) / G)).  Equal unit counts
+// left the CTAs that open one segment more ~6% behind the others, which the
+// fused CG update's grid barrier turns into idle time on every CTA.
+constexpr long RANK_VQ = 4;
+__host__ __device__ __forceinline__ long rank_vpos(long u, long C, long vh)
 {
-    return rank_owner(s * C, U, G) != rank_owner(s * C + C - 1, U, G);
+    const long s = u / C;
+    return s * (C * RANK_VQ + vh) + vh + (u - s * C) * RANK_VQ;
 }
-// number of CTAs (= Ap planes) sharing strip s
-__host__ __device__ __forceinline__ int rank_planes(long s, long C, long U, long G)
+// CTA owning unit u
+__host__ __device__ __forceinline__ long rank_owner(long u, long C, long U, long G, long vh)
 {
-    return int(rank_owner(s * C + C - 1, U, G) - rank_owner(s * C, U, G) + 1);
+    if (vh == 0)
+        return ((u + 1) * G + U - 1) / U - 1;
+    const long V = (U / C) * (C * RANK_VQ + vh), p = rank_vpos(u, C, vh);
+    return ((p + 1) * G + V - 1) / V - 1;
+}
+// first unit of CTA g (g = G: U)
+__host__ __device__ __forceinline__ long rank_ubegin(long g, long C, long U, long G, long vh)
+{
+    if (vh == 0)
+        return U * g / G;
+    const long SW = C * RANK_VQ + vh, v = (U / C) * SW * g / G;
+    const long s = v / SW, o = v - s * SW;
+    return s * C + (o <= vh ? 0 : (o - vh + RANK_VQ - 1) / RANK_VQ);
+}
+__host__ __device__ __forceinline__ bool rank_split(long s, long C, long U, long G, long vh)
+{
+    return rank_owner(s * C, C, U, G, vh) != rank_owner(s * C + C - 1, C, U, G, vh);
+}
+// number of CTAs (= Ap planes) sharing strip s (a CTA with an empty range never
+// falls inside a strip's span: its range lies in the gap before a strip's first unit)
+__host__ __device__ __forceinline__ int rank_planes(long s, long C, long U, long G, long vh)
+{
+    return int(rank_owner(s * C + C - 1, C, U, G, vh) - rank_owner(s * C, C, U, G, vh) + 1);
 }
 // destination of a segment's partial: plane 0 = out, plane k >= 1 = out1 + (k - 1) * pstride
 __device__ __forceinline__ cfloat* rank_plane_dst(const RankArgs& a, int strip, int cta)
 {
     if (a.rr)
         return a.out;
-    const int k = cta - int(rank_owner(long(strip) * a.C, a.units, a.G));
+    const int k = cta - int(rank_owner(long(strip) * a.C, a.C, a.units, a.G, a.vh));
     return k == 0 ? a.out : a.out1 + long(k - 1) * a.pstride;
 }
 
@@ -253,7 +285,7 @@ __global__ void __launch_bounds__(RankCfg<N1, N2>::NT) k_rank_plan(RankArgs a, u
     }
     // split flag of every strip (planes sharing it; 1 for round-robin strips)
     for (long s = blockIdx.x * long(NT) + threadIdx.x; s < a.strips; s += long(gridDim.x) * NT)
-        a.split[s] = a.rr ? 1 : (unsigned char)rank_planes(s, a.C, a.units, a.G);
+        a.split[s] = a.rr ? 1 : (unsigned char)rank_planes(s, a.C, a.units, a.G, a.vh);
 }
 
 template<int N1, int N2>
@@ -855,6 +887,7 @@ struct RankPlan {
     int planes = 1; // max CTAs sharing a strip (Ap planes)
     bool ws = false; // warp-specialised kernel (sense_ws.cuh)
     bool rr = false; // k_normal_rank with whole strips per CTA, round robin (32-B strips)
+    int vh = 0;      // per-strip overhead weight of the cost-balanced ranges (ws kernel)
     bool ok = false;
 };
 
@@ -903,10 +936,11 @@ RankPlan rank_plan(const SenseGeom& g, const cfloat* coils)
     r.rr = r.W == 4 && g_rank_rr && r.strips >= r.G;
     if (r.rr)
         r.G = int(std::min<long>(r.G, r.strips));
+    r.vh = r.ws && !r.rr ? g_rank_vh : 0;
     r.planes = 1;
     if (!r.rr)
         for (long s = 0; s < r.strips; s++)
-            r.planes = std::max(r.planes, rank_planes(s, g.C, r.units, r.G));
+            r.planes = std::max(r.planes, rank_planes(s, g.C, r.units, r.G, r.vh));
     r.ok = r.units < (1L << 30) && g.Y * g.C * g.B < (1L << 30) && g.X * g.Y < (1L << 30) && r.planes < 250;
     return r;
 }
@@ -987,6 +1021,7 @@ void fill_rank_args(const RankPlan& rp, RankArgs& a, const SenseGeom& g)
     a.units = rp.units;
     a.G = rp.G;
     a.rr = rp.rr ? 1 : 0;
+    a.vh = rp.vh;
 }
 
 void launch_rank_plan(const RankPlan& rp, RankArgs a, const SenseGeom& g, unsigned char* plans)

@@ -330,9 +330,9 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
     const int U = int(a.units);
     // contiguous unit ranges, or (a.rr, 32-B strips) whole strips g, g + G, ...
     // so that neighbouring strips of one 128-B DRAM line are read together
-    const int u_begin = a.rr ? int(blockIdx.x) * C : int(long(U) * blockIdx.x / a.G);
+    const int u_begin = a.rr ? int(blockIdx.x) * C : int(rank_ubegin(blockIdx.x, C, U, a.G, a.vh));
     const int n = a.rr ? C * ((U / C - 1 - int(blockIdx.x)) / a.G + 1)
-                       : int(long(U) * (blockIdx.x + 1) / a.G) - u_begin;
+                       : int(rank_ubegin(blockIdx.x + 1, C, U, a.G, a.vh)) - u_begin;
     const int sstep = a.rr ? a.G : 1; // strip step between segments
     // next segment's strip: (b, xb) advanced by sstep strips
     auto next_strip = [&](int& xb, int& b) {
@@ -749,7 +749,8 @@ __global__ void __launch_bounds__(WsCfg<N1, N2>::NT, 1)
             if (i > 0)
                 stage_c(i - 1, opened); // unit i opened a new segment: unit i-1's x is stashed
         }
-        stage_c(n - 1, false);
+        if (n > 0) // (cost-balanced ranges can leave a CTA without units)
+            stage_c(n - 1, false);
     }
 #ifdef WS_PROF
     if (blockIdx.x < 2 && (tid == 0 || tid == NT_AC || tid == NT_AC + NT_B))

@@ -11,7 +11,9 @@ partial column strips, strips split between two CTAs (forced with the
 modl_normal_plus_lambda fragment, whose pattern is a data input:
 recon.hpp:371-379, 807-820), the CG variant, and agreement with the previous
 register-resident kernel (`sense_rank` = 0).  Tolerance: rel-L2 <= 1e-5
-(BASELINE.json north_star, fp32 SENSE/CG path).
+(BASELINE.json north_star, fp32 SENSE/CG path).  The ws kernel's contiguous
+ranges are cost-balanced (option `rank_vh`, per-strip overhead weight; "ws-equal"
+runs the equal-unit-count ranges), including CTAs left without units.
 """
 import ctypes as C
 
@@ -25,12 +27,14 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-@pytest.fixture(params=[(1, 1), (1, 0), (0, 1)], ids=["ws", "ws-contiguous", "rank"])
+@pytest.fixture(params=[(1, 1, 9), (1, 0, 9), (1, 0, 0), (0, 1, 9)], ids=["ws", "ws-contiguous", "ws-equal", "rank"])
 def rank_opts(gpu, request):
-    ws, rr = request.param
+    ws, rr, vh = request.param
     gpu.check(gpu.so.mdnn_set_option(b"sense_ws", ws))
     gpu.check(gpu.so.mdnn_set_option(b"rank_rr", rr))
+    gpu.check(gpu.so.mdnn_set_option(b"rank_vh", vh))
     yield gpu
+    gpu.check(gpu.so.mdnn_set_option(b"rank_vh", 9))
     gpu.check(gpu.so.mdnn_set_option(b"sense_rank", 1))
     gpu.check(gpu.so.mdnn_set_option(b"sense_rank_ctas", 0))
     gpu.check(gpu.so.mdnn_set_option(b"sense_ws", 1))
@@ -217,3 +221,30 @@ def test_cg_fused_update(gpu, ref, tol):
         assert rel_l2(x, x0) <= 1e-6, k
     if tol > 0:
         assert itr < 10
+
+
+@pytest.mark.parametrize("vh", [9, 40])
+def test_ws_cost_ranges_with_empty_ctas(gpu, ref, vh):
+    """Cost-balanced ranges with many CTAs: some CTAs own no unit (their range
+    lies in a strip-overhead gap) and strips are split across several CTAs; the
+    normal operator and CG still match the reference."""
+    X, Y, NC, B = 36, 368, 3, 2    # 10 strips x 3 coils = 30 units
+    ph, cm, pat = sim_data(ref, X, Y, NC, B)
+    rng = np.random.default_rng(21)
+    x = crand(rng, image_dims(X, Y, B))
+    r = _normal(ref, cm, pat, x)
+    xr, itr = _cg(ref, cm, pat, x)
+    try:
+        gpu.check(gpu.so.mdnn_set_option(b"sense_ws", 1))
+        gpu.check(gpu.so.mdnn_set_option(b"rank_rr", 0))
+        gpu.check(gpu.so.mdnn_set_option(b"rank_vh", vh))
+        for ctas in (7, 24, 30):
+            gpu.check(gpu.so.mdnn_set_option(b"sense_rank_ctas", ctas))
+            assert rel_l2(_normal(gpu, cm, pat, x), r) <= TOL, ctas
+            xg, itg = _cg(gpu, cm, pat, x)
+            assert itg == itr
+            assert rel_l2(xg, xr) <= TOL, ctas
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"sense_rank_ctas", 0))
+        gpu.check(gpu.so.mdnn_set_option(b"rank_rr", 1))
+        gpu.check(gpu.so.mdnn_set_option(b"rank_vh", 9))
