@@ -79,10 +79,26 @@ __device__ void sum_partials(double (&r)[NV], const double* __restrict__ part, i
 #pragma unroll
     for (int j = 0; j < NV; j++)
         a[j] = 0;
-    for (int k = threadIdx.x; k < nblocks; k += kT)
+    // KU rows' loads in flight per thread (the rows are 2C NV doubles apart: one
+    // sector each, latency-bound when issued one at a time), summed in the same
+    // order as the one-at-a-time loop
+    constexpr int KU = 8;
+    for (int k0 = threadIdx.x; k0 < nblocks; k0 += KU * kT) {
+        double v[KU][NV];
 #pragma unroll
-        for (int j = 0; j < NV; j++)
-            a[j] += part[(size_t(k) * C + c) * NV + j];
+        for (int u = 0; u < KU; u++) {
+            const int k = k0 + u * kT;
+#pragma unroll
+            for (int j = 0; j < NV; j++)
+                v[u][j] = k < nblocks ? __ldcg(part + (size_t(k) * C + c) * NV + j) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < KU; u++)
+            if (k0 + u * kT < nblocks)
+#pragma unroll
+                for (int j = 0; j < NV; j++)
+                    a[j] += v[u][j];
+    }
 #pragma unroll
     for (int j = 0; j < NV; j++)
         s[j][threadIdx.x] = a[j];

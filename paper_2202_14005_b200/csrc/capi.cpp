@@ -179,6 +179,8 @@ int mdnn_set_option(const char* key, long value)
             sense_rank_enable(value != 0);
         else if (k == "rbf_window")
             rbf_window_enable(value != 0);
+        else if (k == "rbf_pair")
+            rbf_pair_enable(value != 0);
         else if (k == "rank_rr")
             rank_rr_enable(value != 0);
         else if (k == "rank_vh")

@@ -13,6 +13,7 @@ namespace mdnn {
 namespace {
 
 bool g_rbf_window = true;
+int g_rbf_pair = 8; // k_rbf_map mode flag: paired-fp32 K = 9 window (0: rbf_visit_k)
 
 constexpr int kT = 256;
 constexpr int kMaxW = 64;
@@ -74,6 +75,59 @@ __device__ __forceinline__ float gauss2(float z, float mu, float k2)
     return exp2f(-(d * d) * k2);
 }
 
+// K-windowed phi(z) (mode 0) or sum_j w_j phi_j'(z) (mode 1) for evenly spaced
+// centres, in paired fp32: the up / down recurrences of rbf_visit_k advance as one
+// FMUL2 each step (bitwise the same basis values), their weighted sums as FFMA2 /
+// FADD2 pairs.  Mode 1 uses sum_j w_j e_j (-d_j) = dm B - dc A with
+// A = sum_j w_j e_j, B = sum_j w_j e_j (j - jc)  (d_j = dc - (j - jc) dm).
+template<int K, bool INNER>
+__device__ __forceinline__ float rbf_map_win(const float* wf, int jc, float dc, float ec, float U, float D,
+                                             const RbfGeom& g, float inv_s2, int mode)
+{
+    float2 st = make_float2(U, D), e2 = make_float2(ec, ec);
+    const float2 q2 = make_float2(g.q, g.q);
+    float2 a2 = make_float2(0.f, 0.f), b2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 1; k <= K; k++) {
+        e2 = __fmul2_rn(e2, st);
+        st = __fmul2_rn(st, q2);
+        float2 es = e2, w2;
+        if (INNER) {
+            w2 = make_float2(wf[jc + k], wf[jc - k]);
+        } else { // edge: centres outside [0, nw) contribute nothing (their recurrence may overflow)
+            const bool up = jc + k < g.nw, dn = jc - k >= 0;
+            es = make_float2(up ? e2.x : 0.f, dn ? e2.y : 0.f);
+            w2 = make_float2(up ? wf[jc + k] : 0.f, dn ? wf[jc - k] : 0.f);
+        }
+        if (mode == 0) {
+            a2 = __ffma2_rn(w2, es, a2);
+        } else {
+            const float2 p2 = __fmul2_rn(w2, es);
+            a2 = __fadd2_rn(a2, p2);
+            b2 = __ffma2_rn(p2, make_float2(float(k), -float(k)), b2);
+        }
+    }
+    const float a = fmaf(wf[jc], ec, a2.x + a2.y);
+    if (mode == 0)
+        return a;
+    return (g.dmu * (b2.x + b2.y) - dc * a) * inv_s2;
+}
+
+template<int K>
+__device__ __forceinline__ float rbf_map_w(float zk, const float* wf, const float* smu, const RbfGeom& g, float k2,
+                                           float inv_s2, int mode)
+{
+    const float t = rintf((zk - g.mu0) * g.inv_dmu);
+    const int jc = int(fminf(fmaxf(t, 0.f), float(g.nw - 1))); // NaN z: fmax(NaN, 0) = 0
+    const float dc = zk - smu[jc];
+    const float ec = exp2f(-(dc * dc) * k2);
+    const float dm = g.dmu;
+    const float U = exp2f(k2 * dm * (2.f * dc - dm)), D = exp2f(-k2 * dm * (2.f * dc + dm));
+    if (jc >= K && jc + K < g.nw)
+        return rbf_map_win<K, true>(wf, jc, dc, ec, U, D, g, inv_s2, mode);
+    return rbf_map_win<K, false>(wf, jc, dc, ec, U, D, g, inv_s2, mode);
+}
+
 // mode 0: y = phi(z); 1: dz = Re(g) * phi'(z) (adjoint, also tangent with g = dx);
 // 2: y = sum_j Re(dw) e_j (tangent wrt w).  The filter's weights and the centres
 // are staged in shared memory; the element loop walks (inner, filter, outer)
@@ -82,6 +136,8 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
                           const cfloat* __restrict__ gin, const float* __restrict__ mu, RbfGeom g, int mode)
 {
     MDNN_PDL_ENTRY();
+    const bool paired = mode & 8; // rbf_map_w (option rbf_pair) for the K = 9 window
+    mode &= 7;
     __shared__ float smu[kMaxW];
     extern __shared__ float sw[]; // [nf][nw] real parts
     for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
@@ -100,6 +156,45 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
     long f = (i / g.inner) % g.nf;
     long rem = i % g.inner;
     const long df = (stride / g.inner) % g.nf, drem = stride % g.inner;
+    // advance (rem, f) by stride elements
+    auto step = [&](long& r_, long& f_) {
+        r_ += drem;
+        f_ += df;
+        if (r_ >= g.inner) {
+            r_ -= g.inner;
+            f_++;
+        }
+        if (f_ >= g.nf)
+            f_ -= g.nf;
+    };
+    if (paired && g.win == 19 && mode != 2) {
+        // UE elements per thread per round, their loads issued together (one
+        // element in flight per thread left the kernel latency-bound)
+        constexpr int UE = 4;
+        for (; i < n; i += UE * stride) {
+            float zk[UE], gk[UE];
+            long fe[UE];
+#pragma unroll
+            for (int u = 0; u < UE; u++) {
+                const long ie = i + u * stride;
+                zk[u] = ie < n ? z[ie].x : 0.f;
+                gk[u] = (mode == 1 && ie < n) ? gin[ie].x : 0.f;
+                fe[u] = f;
+                step(rem, f);
+            }
+#pragma unroll
+            for (int u = 0; u < UE; u++) {
+                const long ie = i + u * stride;
+                if (ie < n) {
+                    float acc = rbf_map_w<9>(zk[u], sw + fe[u] * g.nw, smu, g, k2, inv_s2, mode);
+                    if (mode == 1)
+                        acc *= gk[u];
+                    out[ie] = float2{acc, 0.f};
+                }
+            }
+        }
+        return;
+    }
     for (; i < n; i += stride) {
         const float zk = z[i].x;
         const float* wf = sw + f * g.nw;
@@ -121,15 +216,7 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
         if (mode == 1)
             acc *= gin[i].x;
         out[i] = float2{acc, 0.f};
-        // advance (rem, f) by stride elements
-        rem += drem;
-        f += df;
-        if (rem >= g.inner) {
-            rem -= g.inner;
-            f++;
-        }
-        if (f >= g.nf)
-            f -= g.nf;
+        step(rem, f);
     }
 }
 
@@ -255,15 +342,32 @@ __global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, c
     const long begin = long(blockIdx.x) * kChunk, end = min(total, begin + kChunk);
     long ii = (begin + threadIdx.x) % g.inner, o = (begin + threadIdx.x) / g.inner;
     const long dii = long(kT) % g.inner, dob = long(kT) / g.inner;
-    for (long t = begin + threadIdx.x; t < end; t += kT) {
-        const long idx = ii + g.inner * (f + g.nf * o);
+    // the next element's z and dy are loaded while this one is processed
+    auto next_idx = [&]() {
+        const long v = ii + g.inner * (f + g.nf * o);
         ii += dii;
         o += dob;
         if (ii >= g.inner) {
             ii -= g.inner;
             o++;
         }
-        const float zk = z[idx].x, gv = dy[idx].x;
+        return v;
+    };
+    long idx_n = 0;
+    float z_n = 0.f, g_n = 0.f;
+    if (begin + threadIdx.x < end) {
+        idx_n = next_idx();
+        z_n = z[idx_n].x;
+        g_n = dy[idx_n].x;
+    }
+    for (long t = begin + threadIdx.x; t < end; t += kT) {
+        const long idx = idx_n;
+        const float zk = z_n, gv = g_n;
+        if (t + kT < end) {
+            idx_n = next_idx();
+            z_n = z[idx_n].x;
+            g_n = dy[idx_n].x;
+        }
         // basis values around the nearest centre jc (rbf_visit_k), position k <-> j = jc - K + k;
         // positions outside [0, nw) are zeroed (their recurrence values may overflow)
         const float tt = rintf((zk - g.mu0) * g.inv_dmu);
@@ -271,30 +375,47 @@ __global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, c
         const float dc = zk - smu[jc];
         float ew[NW2];
         ew[K] = exp2f(-(dc * dc) * k2);
-        float U = exp2f(k2 * dm * (2.f * dc - dm)), D = exp2f(-k2 * dm * (2.f * dc + dm));
-        float eu = ew[K], ed = ew[K];
+        // up / down recurrences as one FMUL2 per step (bitwise rbf_visit_k's values)
+        float2 st = make_float2(exp2f(k2 * dm * (2.f * dc - dm)), exp2f(-k2 * dm * (2.f * dc + dm)));
+        float2 e2 = make_float2(ew[K], ew[K]);
+        const float2 q2 = make_float2(g.q, g.q);
 #pragma unroll
         for (int k = 1; k <= K; k++) {
-            eu *= U;
-            U *= g.q;
-            ed *= D;
-            D *= g.q;
-            ew[K + k] = jc + k < g.nw ? eu : 0.f;
-            ew[K - k] = jc - k >= 0 ? ed : 0.f;
+            e2 = __fmul2_rn(e2, st);
+            st = __fmul2_rn(st, q2);
+            ew[K + k] = e2.x;
+            ew[K - k] = e2.y;
+        }
+        if (jc < K || jc + K >= g.nw) {
+#pragma unroll
+            for (int k = 1; k <= K; k++) {
+                ew[K + k] = jc + k < g.nw ? ew[K + k] : 0.f;
+                ew[K - k] = jc - k >= 0 ? ew[K - k] : 0.f;
+            }
         }
         float* ab = sacc + jc * kT + threadIdx.x; // padded row jc - K + k + K = jc + k
         float cur[NW2];
 #pragma unroll
         for (int k = 0; k < NW2; k++)
             cur[k] = ab[k * kT];
+        const float2 g2 = make_float2(gv, gv);
 #pragma unroll
-        for (int k = 0; k < NW2; k++)
-            ab[k * kT] = fmaf(ew[k], gv, cur[k]);
+        for (int k = 0; k + 1 < NW2; k += 2) {
+            const float2 r2 = __ffma2_rn(make_float2(ew[k], ew[k + 1]), g2, make_float2(cur[k], cur[k + 1]));
+            ab[k * kT] = r2.x;
+            ab[(k + 1) * kT] = r2.y;
+        }
+        ab[(NW2 - 1) * kT] = fmaf(ew[NW2 - 1], gv, cur[NW2 - 1]);
         if (dz) {
-            float d = 0.f;
+            // sum_k w e_k (-(dc - (k - K) dm)) / s^2 = (dm B - dc A) / s^2,
+            // (A, B) = sum_k w e_k (1, k - K) as one FFMA2 per centre
+            float2 ab2 = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = 0; k < NW2; k++)
-                d = fmaf(swf[jc + k] * ew[k], -fmaf(-float(k - K), dm, dc) * inv_s2, d);
+            for (int k = 0; k < NW2; k++) {
+                const float pk = swf[jc + k] * ew[k];
+                ab2 = __ffma2_rn(make_float2(pk, pk), make_float2(1.f, float(k - K)), ab2);
+            }
+            const float d = (dm * ab2.y - dc * ab2.x) * inv_s2;
             dz[idx] = float2{d * gv, 0.f};
         }
     }
@@ -332,6 +453,7 @@ __global__ void k_rbf_wfinal(cfloat* dw, const double* part, RbfGeom g, int nchu
 } // namespace
 
 void rbf_window_enable(bool on) { g_rbf_window = on; }
+void rbf_pair_enable(bool on) { g_rbf_pair = on ? 8 : 0; }
 
 void rbf_set_window(RbfGeom& g, const std::vector<float>& mu)
 {
@@ -362,19 +484,19 @@ void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, c
         throw ConfigError("rbf: more than 64 basis functions not supported on device");
     // algorithmic bytes: z in, y out (complex, 8 B each)
     ProfScope prof("rbf", 16.0 * double(g.inner) * g.nf * g.outer);
-    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, y, z, w, nullptr, mu, g, 0);
+    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, y, z, w, nullptr, mu, g, 0 | g_rbf_pair);
     KERNEL_CHECK();
 }
 
 void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
 {
-    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, dz, z, w, dy, mu, g, 1);
+    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, dz, z, w, dy, mu, g, 1 | g_rbf_pair);
     KERNEL_CHECK();
 }
 
 void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g)
 {
-    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, dy, z, w, dz, mu, g, 1);
+    pdl_launch(k_rbf_map, grid_for(g.inner * g.nf * g.outer), kT, sizeof(float) * g.nf * g.nw, ctx().stream, dy, z, w, dz, mu, g, 1 | g_rbf_pair);
     KERNEL_CHECK();
 }
 

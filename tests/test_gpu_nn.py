@@ -229,6 +229,24 @@ def test_rbf(gpu, ref, window, nw, width, zscale):
         gpu.check(gpu.so.mdnn_set_option(b"rbf_window", 1))
 
 
+@pytest.mark.parametrize("pair", [1, 0], ids=["paired", "visit"])
+def test_rbf_window_map_forms(gpu, ref, pair):
+    """VarNet's K = 9 window (31 centres, sigma = spacing, z also outside the
+    centre range): the paired-fp32 map (option rbf_pair, forward and z-adjoint)
+    and the rbf_visit_k form both match the reference."""
+    rng = np.random.default_rng(77)
+    z = list(d16(40, 24, 24))
+    z[15] = 2
+    centers = [-1 + 2 * j / 30 for j in range(31)]
+    gpu.check(gpu.so.mdnn_set_option(b"rbf_pair", pair))
+    try:
+        ng, nr = Nlop.rbf(gpu, z, 2, centers, 2 / 30), Nlop.rbf(ref, z, 2, centers, 2 / 30)
+        ins = [rrand(rng, z, 1.5), rrand(rng, nr.in_dims(1), 0.05)]
+        _check_node(ng, nr, ins, rng, TOL)
+    finally:
+        gpu.check(gpu.so.mdnn_set_option(b"rbf_pair", 1))
+
+
 def test_bcast_add_and_tenmul(gpu, ref):
     rng = np.random.default_rng(15)
     x = d16(10, 8, 4)
