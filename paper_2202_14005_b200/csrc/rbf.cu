@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 namespace mdnn {
 
@@ -80,9 +81,9 @@ __device__ __forceinline__ float gauss2(float z, float mu, float k2)
 // FMUL2 each step (bitwise the same basis values), their weighted sums as FFMA2 /
 // FADD2 pairs.  Mode 1 uses sum_j w_j e_j (-d_j) = dm B - dc A with
 // A = sum_j w_j e_j, B = sum_j w_j e_j (j - jc)  (d_j = dc - (j - jc) dm).
-template<int K, bool INNER>
+template<int K, bool INNER, int MODE>
 __device__ __forceinline__ float rbf_map_win(const float* wf, int jc, float dc, float ec, float U, float D,
-                                             const RbfGeom& g, float inv_s2, int mode)
+                                             const RbfGeom& g, float inv_s2)
 {
     float2 st = make_float2(U, D), e2 = make_float2(ec, ec);
     const float2 q2 = make_float2(g.q, g.q);
@@ -99,7 +100,7 @@ __device__ __forceinline__ float rbf_map_win(const float* wf, int jc, float dc, 
             es = make_float2(up ? e2.x : 0.f, dn ? e2.y : 0.f);
             w2 = make_float2(up ? wf[jc + k] : 0.f, dn ? wf[jc - k] : 0.f);
         }
-        if (mode == 0) {
+        if constexpr (MODE == 0) {
             a2 = __ffma2_rn(w2, es, a2);
         } else {
             const float2 p2 = __fmul2_rn(w2, es);
@@ -108,14 +109,14 @@ __device__ __forceinline__ float rbf_map_win(const float* wf, int jc, float dc, 
         }
     }
     const float a = fmaf(wf[jc], ec, a2.x + a2.y);
-    if (mode == 0)
+    if constexpr (MODE == 0)
         return a;
     return (g.dmu * (b2.x + b2.y) - dc * a) * inv_s2;
 }
 
-template<int K>
+template<int K, int MODE>
 __device__ __forceinline__ float rbf_map_w(float zk, const float* wf, const float* smu, const RbfGeom& g, float k2,
-                                           float inv_s2, int mode)
+                                           float inv_s2)
 {
     const float t = rintf((zk - g.mu0) * g.inv_dmu);
     const int jc = int(fminf(fmaxf(t, 0.f), float(g.nw - 1))); // NaN z: fmax(NaN, 0) = 0
@@ -124,8 +125,8 @@ __device__ __forceinline__ float rbf_map_w(float zk, const float* wf, const floa
     const float dm = g.dmu;
     const float U = exp2f(k2 * dm * (2.f * dc - dm)), D = exp2f(-k2 * dm * (2.f * dc + dm));
     if (jc >= K && jc + K < g.nw)
-        return rbf_map_win<K, true>(wf, jc, dc, ec, U, D, g, inv_s2, mode);
-    return rbf_map_win<K, false>(wf, jc, dc, ec, U, D, g, inv_s2, mode);
+        return rbf_map_win<K, true, MODE>(wf, jc, dc, ec, U, D, g, inv_s2);
+    return rbf_map_win<K, false, MODE>(wf, jc, dc, ec, U, D, g, inv_s2);
 }
 
 // mode 0: y = phi(z); 1: dz = Re(g) * phi'(z) (adjoint, also tangent with g = dx);
@@ -169,30 +170,38 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
     };
     if (paired && g.win == 19 && mode != 2) {
         // UE elements per thread per round, their loads issued together (one
-        // element in flight per thread left the kernel latency-bound)
-        constexpr int UE = 4;
-        for (; i < n; i += UE * stride) {
-            float zk[UE], gk[UE];
-            long fe[UE];
+        // element in flight per thread left the kernel latency-bound); the mode is
+        // a template argument (a runtime mode predicated both forms' instructions)
+        auto run = [&](auto MODE_) {
+            constexpr int M = decltype(MODE_)::value;
+            constexpr int UE = 4;
+            for (; i < n; i += UE * stride) {
+                float zk[UE], gk[UE];
+                long fe[UE];
 #pragma unroll
-            for (int u = 0; u < UE; u++) {
-                const long ie = i + u * stride;
-                zk[u] = ie < n ? z[ie].x : 0.f;
-                gk[u] = (mode == 1 && ie < n) ? gin[ie].x : 0.f;
-                fe[u] = f;
-                step(rem, f);
-            }
+                for (int u = 0; u < UE; u++) {
+                    const long ie = i + u * stride;
+                    zk[u] = ie < n ? z[ie].x : 0.f;
+                    gk[u] = (M == 1 && ie < n) ? gin[ie].x : 0.f;
+                    fe[u] = f;
+                    step(rem, f);
+                }
 #pragma unroll
-            for (int u = 0; u < UE; u++) {
-                const long ie = i + u * stride;
-                if (ie < n) {
-                    float acc = rbf_map_w<9>(zk[u], sw + fe[u] * g.nw, smu, g, k2, inv_s2, mode);
-                    if (mode == 1)
-                        acc *= gk[u];
-                    out[ie] = float2{acc, 0.f};
+                for (int u = 0; u < UE; u++) {
+                    const long ie = i + u * stride;
+                    if (ie < n) {
+                        float acc = rbf_map_w<9, M>(zk[u], sw + fe[u] * g.nw, smu, g, k2, inv_s2);
+                        if (M == 1)
+                            acc *= gk[u];
+                        out[ie] = float2{acc, 0.f};
+                    }
                 }
             }
-        }
+        };
+        if (mode == 0)
+            run(std::integral_constant<int, 0>{});
+        else
+            run(std::integral_constant<int, 1>{});
         return;
     }
     for (; i < n; i += stride) {
@@ -315,7 +324,7 @@ __global__ void k_rbf_wgrad(double* __restrict__ part, const cfloat* __restrict_
 // ([nw + 2K][thread]), so the 2K + 1 read-modify-writes of an element need no
 // bounds checks, and they are issued as independent loads, FMAs and stores
 // (distinct rows) instead of one serialised load-add-store per centre.
-template<int K>
+template<int K, bool DZ>
 __global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, const cfloat* __restrict__ dy,
                                                    const cfloat* __restrict__ z, const float* __restrict__ mu,
                                                    RbfGeom g, int nchunk, cfloat* __restrict__ dz,
@@ -331,7 +340,7 @@ __global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, c
     for (int j = threadIdx.x; j < g.nw; j += blockDim.x)
         smu[j] = mu[j];
     for (int j = threadIdx.x; j < g.nw + 2 * K; j += blockDim.x)
-        swf[j] = (dz && j >= K && j < g.nw + K) ? w[f + (j - K) * g.nf].x : 0.f;
+        swf[j] = (DZ && j >= K && j < g.nw + K) ? w[f + (j - K) * g.nf].x : 0.f;
     for (int j = 0; j < g.nw + 2 * K; j++)
         sacc[j * kT + threadIdx.x] = 0.f;
     __syncthreads();
@@ -406,7 +415,7 @@ __global__ void __launch_bounds__(kT) k_rbf_wgrad_w(double* __restrict__ part, c
             ab[(k + 1) * kT] = r2.y;
         }
         ab[(NW2 - 1) * kT] = fmaf(ew[NW2 - 1], gv, cur[NW2 - 1]);
-        if (dz) {
+        if constexpr (DZ) {
             // sum_k w e_k (-(dc - (k - K) dm)) / s^2 = (dm B - dc A) / s^2,
             // (A, B) = sum_k w e_k (1, k - K) as one FFMA2 per centre
             float2 ab2 = make_float2(0.f, 0.f);
@@ -530,11 +539,14 @@ bool launch_wgrad_w9(double* part, const cfloat* dy, const cfloat* z, const floa
     const size_t bytes = sizeof(float) * kT * (g.nw + 18);
     static size_t granted = 48 * 1024;
     if (bytes > granted) {
-        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<9>),
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<9, true>),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<9, false>),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
         granted = bytes;
     }
-    pdl_launch(k_rbf_wgrad_w<9>, dim3(nchunk, unsigned(g.nf)), kT, bytes, ctx().stream, part, dy, z, mu, g, nchunk, dz, w);
+    pdl_launch(dz ? k_rbf_wgrad_w<9, true> : k_rbf_wgrad_w<9, false>, dim3(nchunk, unsigned(g.nf)), kT, bytes,
+               ctx().stream, part, dy, z, mu, g, nchunk, dz, w);
     KERNEL_CHECK();
     return true;
 }
