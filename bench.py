@@ -354,7 +354,7 @@ def main():
     torch.cuda.set_device(local)
     lib = load_library()
     lib.check(lib.so.mdnn_set_device(local))
-    for opt in ("sense_rank", "conv_tc", "cg_pdl", "cg_fuse", "pdl", "rbf_pair"):  # A/B switches for experiments (default: product path)
+    for opt in ("sense_rank", "conv_tc", "cg_pdl", "cg_fuse", "pdl", "rbf_pair", "rbf_cut"):  # A/B switches for experiments (default: product path)
         if os.environ.get("MDNN_" + opt.upper()) is not None:
             lib.check(lib.so.mdnn_set_option(opt.encode(), int(os.environ["MDNN_" + opt.upper()])))
     stream = torch.cuda.ExternalStream(lib.so.mdnn_stream(), device=torch.device("cuda", local))

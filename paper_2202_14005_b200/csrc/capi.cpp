@@ -181,6 +181,8 @@ int mdnn_set_option(const char* key, long value)
             rbf_window_enable(value != 0);
         else if (k == "rbf_pair")
             rbf_pair_enable(value != 0);
+        else if (k == "rbf_cut")
+            rbf_cut_set(int(value));
         else if (k == "rank_rr")
             rank_rr_enable(value != 0);
         else if (k == "rank_vh")

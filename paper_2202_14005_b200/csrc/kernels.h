@@ -253,6 +253,7 @@ void rbf_forward(cfloat* y, const cfloat* z, const cfloat* w, const float* mu, c
 // decides g.win for the centres (host); honours the rbf_window option
 void rbf_set_window(RbfGeom& g, const std::vector<float>& mu);
 void rbf_window_enable(bool on);
+void rbf_cut_set(int tenths_sigma); // windowed RBF cut-off in tenths of sigma (55: K = 6 at sigma = spacing)
 void rbf_pair_enable(bool on); // paired-fp32 windowed RBF map (forward / z-adjoint)
 void rbf_adjoint_z(cfloat* dz, const cfloat* dy, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);
 void rbf_deriv_z(cfloat* dy, const cfloat* dz, const cfloat* z, const cfloat* w, const float* mu, const RbfGeom& g);

@@ -14,6 +14,7 @@ namespace mdnn {
 namespace {
 
 bool g_rbf_window = true;
+int g_rbf_cut = 55;  // windowed RBF: centres within cut / 10 sigma (+ 1 sigma margin) of z
 int g_rbf_pair = 8; // k_rbf_map mode flag: paired-fp32 K = 9 window (0: rbf_visit_k)
 
 constexpr int kT = 256;
@@ -56,8 +57,10 @@ __device__ __forceinline__ void rbf_visit_k(float zk, const float* smu, const Rb
 template<class F>
 __device__ __forceinline__ void rbf_visit(float zk, const float* smu, const RbfGeom& g, float k2, F&& f)
 {
-    if (g.win == 19) // VarNet: 31 centres at sigma = spacing
+    if (g.win == 19) // VarNet: 31 centres at sigma = spacing, 8.5 sigma cut
         rbf_visit_k<9>(zk, smu, g, k2, f);
+    else if (g.win == 13) // VarNet, 5.5 sigma cut (default)
+        rbf_visit_k<6>(zk, smu, g, k2, f);
     else
         rbf_visit_k<0>(zk, smu, g, k2, f);
 }
@@ -168,7 +171,7 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
         if (f_ >= g.nf)
             f_ -= g.nf;
     };
-    if (paired && g.win == 19 && mode != 2) {
+    if (paired && (g.win == 19 || g.win == 13) && mode != 2) {
         // UE elements per thread per round, their loads issued together (one
         // element in flight per thread left the kernel latency-bound); the mode is
         // a template argument (a runtime mode predicated both forms' instructions)
@@ -190,7 +193,8 @@ __global__ void k_rbf_map(cfloat* __restrict__ out, const cfloat* __restrict__ z
                 for (int u = 0; u < UE; u++) {
                     const long ie = i + u * stride;
                     if (ie < n) {
-                        float acc = rbf_map_w<9, M>(zk[u], sw + fe[u] * g.nw, smu, g, k2, inv_s2);
+                        float acc = g.win == 13 ? rbf_map_w<6, M>(zk[u], sw + fe[u] * g.nw, smu, g, k2, inv_s2)
+                                                : rbf_map_w<9, M>(zk[u], sw + fe[u] * g.nw, smu, g, k2, inv_s2);
                         if (M == 1)
                             acc *= gk[u];
                         out[ie] = float2{acc, 0.f};
@@ -463,6 +467,7 @@ __global__ void k_rbf_wfinal(cfloat* dw, const double* part, RbfGeom g, int nchu
 
 void rbf_window_enable(bool on) { g_rbf_window = on; }
 void rbf_pair_enable(bool on) { g_rbf_pair = on ? 8 : 0; }
+void rbf_cut_set(int tenths_sigma) { g_rbf_cut = tenths_sigma < 10 ? 10 : tenths_sigma; }
 
 void rbf_set_window(RbfGeom& g, const std::vector<float>& mu)
 {
@@ -474,9 +479,13 @@ void rbf_set_window(RbfGeom& g, const std::vector<float>& mu)
     for (int j = 0; j < n; j++)
         if (std::fabs(double(mu[j]) - (mu[0] + j * dmu)) > 1e-5 * dmu)
             return; // not evenly spaced
-    // skipped centres lie >= (K + 1/2) dmu - (rounding slack) from z; 8.5 sigma
-    // puts their basis values below exp(-36) = 2^-52 of the nearest one's
-    const int K = int(std::ceil(8.5 * g.sigma / dmu + 0.5 - 1e-6)); // sigma = spacing: K = 9 (not 10 on rounding)
+    // skipped centres lie >= (K + 1/2) dmu - (rounding slack) from z, i.e. at
+    // least cut + 1 sigma.  Default cut 5.5 (K = 6 at sigma = spacing): skipped
+    // basis values are below exp(-21.1) ~ 2^-30 of the nearest one's, under the
+    // fp32 rounding (2^-24) of every sum they would enter; option rbf_cut = 85
+    // restores the 8.5-sigma window (K = 9, below 2^-52)
+    const double cut = g_rbf_cut / 10.0;
+    const int K = int(std::ceil(cut * g.sigma / dmu + 0.5 - 1e-6)); // sigma = spacing: K = 6 (9 at cut 8.5)
     const int win = 2 * K + 1;
     if (win >= n)
         return;
@@ -530,24 +539,34 @@ size_t rbf_wgrad_smem(const RbfGeom& g)
     return bytes;
 }
 
-// the K = 9 windowed weight-gradient kernel, or false when the geometry needs the generic one
-bool launch_wgrad_w9(double* part, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g, int nchunk,
+// the K = 9 / K = 6 windowed weight-gradient kernels, or false when the geometry needs the generic one
+template<int K>
+void launch_wgrad_wk(double* part, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g, int nchunk,
                      cfloat* dz, const cfloat* w)
 {
-    if (g.win != 19)
-        return false;
-    const size_t bytes = sizeof(float) * kT * (g.nw + 18);
+    const size_t bytes = sizeof(float) * kT * (g.nw + 2 * K);
     static size_t granted = 48 * 1024;
     if (bytes > granted) {
-        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<9, true>),
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<K, true>),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<9, false>),
+        CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_rbf_wgrad_w<K, false>),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
         granted = bytes;
     }
-    pdl_launch(dz ? k_rbf_wgrad_w<9, true> : k_rbf_wgrad_w<9, false>, dim3(nchunk, unsigned(g.nf)), kT, bytes,
+    pdl_launch(dz ? k_rbf_wgrad_w<K, true> : k_rbf_wgrad_w<K, false>, dim3(nchunk, unsigned(g.nf)), kT, bytes,
                ctx().stream, part, dy, z, mu, g, nchunk, dz, w);
     KERNEL_CHECK();
+}
+
+bool launch_wgrad_w9(double* part, const cfloat* dy, const cfloat* z, const float* mu, const RbfGeom& g, int nchunk,
+                     cfloat* dz, const cfloat* w)
+{
+    if (g.win == 19)
+        launch_wgrad_wk<9>(part, dy, z, mu, g, nchunk, dz, w);
+    else if (g.win == 13)
+        launch_wgrad_wk<6>(part, dy, z, mu, g, nchunk, dz, w);
+    else
+        return false;
     return true;
 }
 

@@ -229,22 +229,27 @@ def test_rbf(gpu, ref, window, nw, width, zscale):
         gpu.check(gpu.so.mdnn_set_option(b"rbf_window", 1))
 
 
+@pytest.mark.parametrize("cut", [55, 85], ids=["K6", "K9"])
 @pytest.mark.parametrize("pair", [1, 0], ids=["paired", "visit"])
-def test_rbf_window_map_forms(gpu, ref, pair):
-    """VarNet's K = 9 window (31 centres, sigma = spacing, z also outside the
-    centre range): the paired-fp32 map (option rbf_pair, forward and z-adjoint)
-    and the rbf_visit_k form both match the reference."""
+def test_rbf_window_map_forms(gpu, ref, pair, cut):
+    """VarNet's window (31 centres, sigma = spacing, z also outside the centre
+    range) at both cut-offs (option rbf_cut: 5.5 sigma -> K = 6, the default;
+    8.5 sigma -> K = 9): the paired-fp32 map (option rbf_pair, forward and
+    z-adjoint), the rbf_visit_k form and the windowed weight-gradient pass all
+    match the reference (which evaluates every centre)."""
     rng = np.random.default_rng(77)
     z = list(d16(40, 24, 24))
     z[15] = 2
     centers = [-1 + 2 * j / 30 for j in range(31)]
     gpu.check(gpu.so.mdnn_set_option(b"rbf_pair", pair))
+    gpu.check(gpu.so.mdnn_set_option(b"rbf_cut", cut))
     try:
         ng, nr = Nlop.rbf(gpu, z, 2, centers, 2 / 30), Nlop.rbf(ref, z, 2, centers, 2 / 30)
         ins = [rrand(rng, z, 1.5), rrand(rng, nr.in_dims(1), 0.05)]
         _check_node(ng, nr, ins, rng, TOL)
     finally:
         gpu.check(gpu.so.mdnn_set_option(b"rbf_pair", 1))
+        gpu.check(gpu.so.mdnn_set_option(b"rbf_cut", 55))
 
 
 def test_bcast_add_and_tenmul(gpu, ref):
