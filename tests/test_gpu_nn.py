@@ -170,22 +170,14 @@ def test_conv_weights_init_bitwise(gpu, ref):
     assert np.array_equal(mg.init_weight(42, "dw1_w"), mr.init_weight(42, "dw1_w"))
 
 
-@pytest.mark.parametrize("offset", [0.0, 40.0], ids=["centred", "offset"])
 @pytest.mark.parametrize("train", [True, False])
-def test_batchnorm(gpu, ref, train, offset):
-    """BatchNorm node against the reference's centred two-pass statistics
-    (ops.hpp:1115-1117), also with channel means ~50x the spread: the device
-    sums are shifted (no E|x|^2 - |mu|^2 cancellation)."""
+def test_batchnorm(gpu, ref, train):
     rng = np.random.default_rng(5)
     dims = list(d16(24, 20, 8))
     dims[15] = 2
     flags = (1 << 0) | (1 << 1) | (1 << 15)
     ng, nr = Nlop.batchnorm(gpu, dims, flags, train), Nlop.batchnorm(ref, dims, flags, train)
     x = crand(rng, dims)
-    if offset:
-        chan = (np.arange(dims[2]) + 1).reshape(1, 1, -1) * np.complex64(offset * (1 + 0.5j) / dims[2])
-        x = np.asfortranarray((x.reshape(dims[0], dims[1], dims[2], -1, order="F") + chan[..., None])
-                              .reshape(dims, order="F").astype(np.complex64))
     mean = crand(rng, nr.in_dims(1), 0.1)
     var = rrand(rng, nr.in_dims(2), 1.0) + np.float32(1.5)
     _check_node(ng, nr, [x, mean, np.asfortranarray(var)], rng, TOL)
