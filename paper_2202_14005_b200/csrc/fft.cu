@@ -140,11 +140,11 @@ __global__ void __launch_bounds__(256) k_fft_lines(cfloat* __restrict__ out, con
         o0 = long(blockIdx.x) * W;
     }
     const float cj = inverse ? -1.f : 1.f;
-    // load (conj for inverse: IDFT(x) = conj(DFT(conj x)))
-    for (int e = threadIdx.x; e < n * W; e += blockDim.x) {
+    // load (conj for inverse: IDFT(x) = conj(DFT(conj x))); UL elements' loads in
+    // flight per thread (one at a time left the kernel latency-bound: ncu long
+    // scoreboard 47%, 2 CTAs per SM)
+    auto locate = [&](int e, int& sidx, long& addr, bool& ok) {
         int w, k;
-        long addr;
-        bool ok;
         if (mode == 0) {
             w = e % W;
             k = e / W;
@@ -156,8 +156,26 @@ __global__ void __launch_bounds__(256) k_fft_lines(cfloat* __restrict__ out, con
             ok = o0 + w < outer;
             addr = (o0 + w) * long(n) + k;
         }
-        float2 v = ok ? in[addr] : float2{0.f, 0.f};
-        a[k * LD + w] = float2{v.x, cj * v.y};
+        sidx = k * LD + w;
+    };
+    constexpr int UL = 8;
+    for (int e0 = threadIdx.x; e0 < n * W; e0 += UL * blockDim.x) {
+        float2 v[UL];
+        int sidx[UL];
+#pragma unroll
+        for (int u = 0; u < UL; u++) {
+            const int e = e0 + u * blockDim.x;
+            long addr = 0;
+            bool ok = false;
+            sidx[u] = -1;
+            if (e < n * W)
+                locate(e, sidx[u], addr, ok);
+            v[u] = ok ? in[addr] : float2{0.f, 0.f};
+        }
+#pragma unroll
+        for (int u = 0; u < UL; u++)
+            if (sidx[u] >= 0)
+                a[sidx[u]] = float2{v[u].x, cj * v[u].y};
     }
     __syncthreads();
     float2* r = fftd::fft_smem(a, b, plan, LD);
