@@ -27,6 +27,10 @@ namespace mdnn {
 namespace {
 
 constexpr int TX = 32, NT = 256, MAXF = 256;
+// CTAs per SM the 3x3 weight-gradient kernels are built for: 3 (80 registers, ~100 B
+// spilled) beat 2 (128 registers): 3.61 -> 3.37 ms per two C2 steps; the expand
+// kernel at 3 lost more (2.66 -> 2.85 ms) and keeps 2
+#define THIN_WG_MINB(K) ((K) == 3 ? 3 : 1)
 
 // U[t][f] for the 4 uses; w has dims [KX, KY, Cin, Cout]
 //   mode 0: fwd 1 -> F           U[t][f] = w[t, 0, f]
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(NT, K == 3 ? 2 : 1) k_thin_reduce(float2* __re
 // P channels per thread (P = 2: 8-byte channel-pair loads, the window loads and
 // the loop overhead shared by two channels -- as in k_thin_expand)
 template<int K, bool WIDE_IS_G, int P>
-__global__ void __launch_bounds__(NT) k_thin_wgrad(float2* __restrict__ part, const float* __restrict__ wide,
+__global__ void __launch_bounds__(NT, THIN_WG_MINB(K)) k_thin_wgrad(float2* __restrict__ part, const float* __restrict__ wide,
                                                    const float2* __restrict__ thin, int X, int Y, int B, int F,
                                                    int ox, int oy)
 {
